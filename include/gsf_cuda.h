@@ -1,0 +1,280 @@
+/* gsf_cuda.h — C-ABI of the B200-native CG-SLAM rasterizer / track-step / map-step.
+ *
+ * This is the drop-in boundary for the reference's hot path (arxiv 2403.16095 "gsfield",
+ * /root/reference/proj).  Every entry point below replaces one reference C++ function;
+ * the citation next to it names the interface it stands in for.  Plain C types only:
+ * pointers, sizes, PODs.  No torch types, no C++ types.
+ *
+ * Conventions
+ *   - Images are row-major (x fastest), index y*W + x, like gsf::Image (core/image.hpp:10-48).
+ *     RGB images interleave channels: rgb[3*(y*W+x) + c].
+ *   - Per-primitive host arrays are AoS per primitive, like GaussianPrimitive
+ *     (geometry/primitive.hpp:16-59): mean[3*i+a], log_scale[3*i+a], quat[4*i+k] (w,x,y,z),
+ *     opacity_logit[i], sh[3*K*i + 3*b + c] (K coefficients per channel, 1/4/9/16).
+ *   - The device keeps the map as SoA fp32 ([field][P]); poses, loss scalars and the
+ *     camera rotation are fp64.  Pixel maps are returned as fp32.
+ *   - Every function returns a gsf_status.  GSF_OK = 0.  On failure gsf_last_error(ctx)
+ *     holds the message the reference would have put in its exception, and
+ *     gsf_last_error_index(ctx) the offending primitive index (or -1).
+ *   - A context owns one CUDA device + stream.  It is not thread-safe; use one per thread.
+ *   - There is no CPU fallback: if the device or the kernels are unavailable every call
+ *     fails with GSF_ECUDA.
+ */
+#ifndef GSF_CUDA_H
+#define GSF_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSF_ABI_VERSION 1
+
+typedef enum {
+  GSF_OK = 0,
+  GSF_EINVAL = 1,        /* std::invalid_argument in the reference */
+  GSF_ENONFINITE = 2,    /* invalid_argument("render: primitive i has non-finite parameters") */
+  GSF_EDIVERGED = 3,     /* std::runtime_error("... diverged ...") */
+  GSF_ECUDA = 4,         /* device / launch failure (no fallback exists) */
+  GSF_EUNSUPPORTED = 5,  /* a runtime value the device path does not implement (e.g. tile_size != 16) */
+  GSF_ENOMEM = 6
+} gsf_status;
+
+typedef struct gsf_ctx_s* gsf_ctx;
+
+/* CameraIntrinsics (geometry/camera.hpp:9-36). */
+typedef struct {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double depth_scale, near_plane, far_plane;
+} gsf_intrinsics;
+
+/* RasterConfig (raster/config.hpp:5-16).  tile_size must be 16 on the device path;
+ * threads is accepted and ignored (the device has its own parallelism). */
+typedef struct {
+  double alpha_clamp, alpha_skip, termination_threshold, footprint_sigma, dilation;
+  int32_t tile_size;
+  int32_t uncertainty_full_gradient;
+  int32_t threads;
+} gsf_raster_cfg;
+
+/* CameraPose (geometry/pose.hpp:13-49): p_cam = exp(rotation_tangent) p_world + translation. */
+typedef struct {
+  double rotation_tangent[3];
+  double translation[3];
+} gsf_pose;
+
+/* LossWeights (loss/losses.hpp:13-31). */
+typedef struct {
+  double w_color, w_ssim, w_geo, w_align, w_iso, w_var;
+  double t_color, t_geo;
+  double iso_epsilon, opacity_floor;
+  int32_t normalize_by_valid;
+} gsf_loss_weights;
+
+/* TrackerConfig (track/tracker.hpp:11-22). */
+typedef struct {
+  double lr_rotation, lr_translation;
+  int32_t iterations, ba_window, ba_iterations, keyframe_interval, recent_keyframes;
+  int32_t freeze_oldest_pose;
+  double degraded_loss_ratio;
+} gsf_tracker_cfg;
+
+/* The MapperConfig fields used by map_step / sliding_ba (map/mapper.hpp:21-41). */
+typedef struct {
+  int32_t sh_coeffs;
+  double scene_extent, lr_mean, lr_sh, lr_opacity, lr_scale, lr_rotation;
+  int32_t densify_interval;   /* DensifyConfig::interval; densify runs on the host layer */
+  double densify_grad_threshold, densify_split_factor, densify_size_fraction, densify_cull_opacity;
+  double uncertainty_tau, uncertainty_reduced_opacity;   /* UncertaintyConfig */
+  uint64_t seed;
+  gsf_raster_cfg raster;
+  gsf_loss_weights weights;
+} gsf_mapper_cfg;
+
+/* Host view of a primitive list (std::vector<GaussianPrimitive>). */
+typedef struct {
+  int64_t count;
+  int32_t sh_coeffs;
+  double* mean;           /* 3*count */
+  double* log_scale;      /* 3*count */
+  double* quat;           /* 4*count */
+  double* opacity_logit;  /* count */
+  double* sh;             /* 3*sh_coeffs*count */
+  double* uncertainty;    /* count, may be NULL */
+  uint8_t* observed;      /* count, may be NULL */
+} gsf_map_host;
+
+/* RenderOutput (raster/output.hpp:15-28) + the per-pixel parts of BlendRecord
+ * (dominant, median_prim, visible; output.hpp:32-45).  Any pointer may be NULL. */
+typedef struct {
+  float* color;               /* 3*W*H */
+  float* alpha_depth;         /* W*H */
+  float* median_depth;
+  uint8_t* median_valid;
+  float* opacity;
+  float* uncertainty;
+  float* final_transmittance;
+  int32_t* per_pixel_count;
+  int32_t* dominant;          /* -1 where no contributor */
+  int32_t* median_prim;       /* -1 where T never crossed 0.5 */
+  float* dominant_weight;     /* alpha*T of the dominant contributor (0 if none) */
+  uint8_t* visible;           /* count (per primitive) */
+  int32_t has_uncertainty;    /* out */
+  int64_t num_visible;        /* out: primitives surviving culling */
+  int64_t num_pairs;          /* out: (tile, primitive) list entries */
+} gsf_render_out;
+
+/* UpstreamGradients (raster/output.hpp:54-60).  NULL = that map carries no gradient. */
+typedef struct {
+  const float* d_color;        /* 3*W*H */
+  const float* d_alpha_depth;
+  const float* d_median_depth;
+  const float* d_opacity;
+  const float* d_uncertainty;
+} gsf_upstream;
+
+/* GradientBundle (raster/output.hpp:64-77).  Any array pointer may be NULL. */
+typedef struct {
+  float* d_mean;            /* 3*count */
+  float* d_log_scale;       /* 3*count */
+  float* d_quat;            /* 4*count */
+  float* d_opacity_logit;   /* count */
+  float* d_sh;              /* 3*K*count */
+  float* d_mean2d;          /* 2*count */
+  double d_pose[6];         /* out: (rot, trans) in the CameraPose::perturbed tangent */
+} gsf_grads_out;
+
+/* TrackResult (track/tracker.hpp:28-33). */
+typedef struct {
+  gsf_pose pose;
+  double final_loss;
+  int32_t degraded;
+  int32_t iterations_run;
+  double initial_loss;
+} gsf_track_result;
+
+/* Loss scalars of evaluate_tracking_loss / evaluate_mapping_loss (losses.hpp:65-87). */
+typedef struct {
+  double color, ssim, geo, align, iso, var, total;
+  int32_t valid_color, valid_geo, any_empty_mask;
+} gsf_loss_terms;
+
+/* ---- context ------------------------------------------------------------------------ */
+int gsf_abi_version(void);
+int gsf_ctx_create(int device, gsf_ctx* out);
+int gsf_ctx_destroy(gsf_ctx ctx);
+const char* gsf_last_error(gsf_ctx ctx);
+int64_t gsf_last_error_index(gsf_ctx ctx);
+/* Device-side kernel launches issued by this context since creation (evidence counter). */
+int64_t gsf_kernel_launches(gsf_ctx ctx);
+int gsf_synchronize(gsf_ctx ctx);
+
+/* ---- timing hooks (benchmark evidence; no effect on results) -------------------------------
+ * CUDA events on the context's stream.  Kernel classes for gsf_profile_read: 0 preprocess,
+ * 1 scan+sort+binning, 2 blend (forward), 3 backward (per-pixel reverse sweep), 4 chain
+ * (per-primitive fp64 chain + pose reduction). */
+int gsf_profile_enable(gsf_ctx ctx, int32_t on);
+int gsf_profile_read(gsf_ctx ctx, int32_t kernel_class, double* total_ms, int64_t* launches);
+int gsf_event_record(gsf_ctx ctx, int32_t slot);                       /* slot 0..7 */
+int gsf_event_elapsed(gsf_ctx ctx, int32_t a, int32_t b, double* ms);  /* waits for b */
+
+/* ---- map residency ------------------------------------------------------------------
+ * Replaces the implicit per-call read of const std::vector<GaussianPrimitive>& in every
+ * reference entry point: the map is uploaded once and stays resident.  Validation of
+ * non-finite parameters (rasterizer.cpp:34-44) happens at upload and again on device. */
+int gsf_map_upload(gsf_ctx ctx, const gsf_map_host* map);
+int gsf_map_download(gsf_ctx ctx, gsf_map_host* map);   /* map->count must match */
+int64_t gsf_map_count(gsf_ctx ctx);
+/* Reset the Adam moments/step counts of the primitive optimizer (PrimitiveOptimizer,
+ * map/mapper.hpp:92-105) — a fresh MapState. */
+int gsf_optimizer_reset(gsf_ctx ctx);
+
+/* ---- forward / backward (raster/rasterizer.hpp:19-35) --------------------------------- */
+/* render(): observed_depth may be NULL (then has_uncertainty = 0). */
+int gsf_render(gsf_ctx ctx, const gsf_pose* pose, const gsf_intrinsics* K,
+               const float* observed_depth, const gsf_raster_cfg* cfg, gsf_render_out* out);
+/* render_backward() over the record of the most recent gsf_render on this context.
+ * observed_depth must be the same buffer contents as for that render (or NULL). */
+int gsf_render_backward(gsf_ctx ctx, const gsf_upstream* up, const float* observed_depth,
+                        gsf_grads_out* out);
+/* The CSR BlendRecord of the most recent render (output.hpp:32-45, rasterizer.cpp:240-259).
+ * Call with prim == NULL to get *total; then again with buffers of that size. */
+int gsf_render_record(gsf_ctx ctx, uint32_t* row_start, int32_t* prim, float* alpha,
+                      float* transmittance, int64_t* total);
+
+/* Tile binning of the most recent render, for bit-exact checks of the hand-written sort:
+ * rank_to_id[V] (global (depth, id) order, rasterizer.cpp:69-79), tile_range[2*tiles]
+ * ([start, end) into the pair list) and pair_rank[M] (tile lists, rasterizer.cpp:199-212).
+ * Any pointer may be NULL; capacities are checked against the counts of gsf_render_out. */
+int gsf_render_tiles(gsf_ctx ctx, int32_t* rank_to_id, int64_t rank_cap, int32_t* tile_range,
+                     int64_t tiles_cap, int32_t* pair_rank, int64_t pair_cap);
+
+/* ---- losses (loss/losses.hpp:77-94) over the most recent render ----------------------- */
+int gsf_tracking_loss(gsf_ctx ctx, const float* target_rgb, const float* observed_depth,
+                      const gsf_loss_weights* w, gsf_loss_terms* out, float* d_color,
+                      float* d_alpha_depth);
+int gsf_mapping_loss(gsf_ctx ctx, const float* target_rgb, const float* observed_depth,
+                     const gsf_loss_weights* w, gsf_loss_terms* out, float* d_color,
+                     float* d_alpha_depth, float* d_median_depth, float* d_uncertainty,
+                     float* d_log_scale_direct);
+/* ssim / ssim_with_gradient (loss/ssim.hpp:11-14); d_x may be NULL. */
+int gsf_ssim(gsf_ctx ctx, const float* x, const float* y, int32_t w, int32_t h, double* value,
+             float* d_x);
+
+/* ---- frames resident on the device --------------------------------------------------- */
+/* Upload one RGB-D observation into slot `slot` (rgb 3*W*H, depth W*H, meters). */
+int gsf_frame_upload(gsf_ctx ctx, int32_t slot, const float* rgb, const float* depth,
+                     int32_t width, int32_t height);
+
+/* ---- track / map / bundle adjustment --------------------------------------------------- */
+/* track_frame (track/tracker.hpp:38-42, tracker.cpp:30-84) against frame slot `slot`. */
+int gsf_track_frame(gsf_ctx ctx, int32_t slot, const gsf_pose* initial, const gsf_intrinsics* K,
+                    const gsf_tracker_cfg* tcfg, const gsf_loss_weights* w,
+                    const gsf_raster_cfg* rcfg, gsf_track_result* out);
+/* Same call with host frame buffers: uploads rgb/depth into slot 0 first (e2e path). */
+int gsf_track_frame_host(gsf_ctx ctx, const float* rgb, const float* depth,
+                         const gsf_pose* initial, const gsf_intrinsics* K,
+                         const gsf_tracker_cfg* tcfg, const gsf_loss_weights* w,
+                         const gsf_raster_cfg* rcfg, gsf_track_result* out);
+/* map_step (map/mapper.hpp:101-103): window = frame slots + their poses; trace gets
+ * `iterations` loss values. */
+int gsf_map_step(gsf_ctx ctx, const int32_t* slots, const gsf_pose* poses, int32_t n,
+                 const gsf_intrinsics* K, const gsf_mapper_cfg* mcfg, int32_t iterations,
+                 double* trace);
+/* sliding_ba (track/tracker.hpp:55-57).  poses is updated in place; frame_ids pick the anchor.
+ * With a communicator set (gsf_comm_init), each rank passes the full window and renders
+ * only the keyframes it owns (k mod nranks == rank); Gaussian gradients are summed with one
+ * NCCL all-reduce per iteration; every rank returns the same map and all window poses. */
+int gsf_sliding_ba(gsf_ctx ctx, const int32_t* slots, gsf_pose* poses, const int32_t* frame_ids,
+                   int32_t n, const gsf_intrinsics* K, const gsf_tracker_cfg* tcfg,
+                   const gsf_mapper_cfg* mcfg, int32_t iterations, double* trace);
+
+/* accumulate_uncertainty / prune_unreliable (map/uncertainty.hpp:33-39).  Each view is
+ * rendered on the device from (slot depth, pose). */
+int gsf_accumulate_uncertainty(gsf_ctx ctx, const int32_t* slots, const gsf_pose* poses,
+                               int32_t n, const gsf_intrinsics* K, const gsf_raster_cfg* rcfg,
+                               int32_t* observed_count);
+int gsf_prune_unreliable(gsf_ctx ctx, double tau, double reduced_opacity, int32_t* reduced);
+
+/* ---- multi-GPU (keyframe-sharded sliding_ba) ----------------------------------------- */
+/* Which window keyframes rank `rank` of `nranks` renders: out[i] = 1 if owned.  Pure host
+ * logic, usable without a device (ctx may be NULL). */
+int gsf_ba_partition(int32_t n, int32_t nranks, int32_t rank, uint8_t* owned);
+int gsf_comm_unique_id(uint8_t id[128]);
+int gsf_comm_init(gsf_ctx ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
+
+/* ---- synthetic inputs (io/synthetic.cpp:56-186; support, not the hot path) ----------- */
+/* Room scene of SceneSpec{room, primitive_count, extent, wall_layers}, mt19937_64(seed).
+ * Call with map->mean == NULL to get map->count; then with arrays of that size (K = 1). */
+int gsf_synth_room(int32_t primitive_count, double extent, int32_t wall_layers, uint64_t seed,
+                   gsf_map_host* map);
+/* Orbit trajectory (synthetic.cpp:158-186) with TrajectorySpec defaults except frames/radius/height. */
+int gsf_synth_orbit(int32_t frames, double radius, double height, gsf_pose* poses);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSF_CUDA_H */

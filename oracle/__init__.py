@@ -1,0 +1,396 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU checker.
+
+ctypes bindings of oracle/liboracle.so: the fp64 restatement of the reference hot path
+(oracle/gsf_oracle.cpp, every function citing the /root/reference file:line it follows) and the
+fp32 mirror of the device decision path (oracle/mirror.cpp).  Only tests/, __graft_entry__.smoke()
+and bench.py's cpu_baseline / --impl reference legs may import this package, and only as the
+checker or the timed CPU baseline — never as the product.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from types import SimpleNamespace
+
+import numpy as np
+
+from paper_2403_16095_b200.abi import (Intrinsics, LossTerms, LossWeights, MapHost, MapperCfg, Pose, RasterCfg,
+                                       TrackerCfg, TrackResult)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+
+dp = C.POINTER(C.c_double)
+fp = C.POINTER(C.c_float)
+u8p = C.POINTER(C.c_uint8)
+i32p = C.POINTER(C.c_int32)
+
+
+class Maps(C.Structure):
+    _fields_ = [("color", dp), ("alpha_depth", dp), ("median_depth", dp), ("median_valid", u8p), ("opacity", dp),
+                ("uncertainty", dp), ("final_transmittance", dp), ("per_pixel_count", i32p), ("dominant", i32p),
+                ("median_prim", i32p), ("dominant_weight", dp), ("visible", u8p), ("has_uncertainty", C.c_int32)]
+
+
+class Upstream(C.Structure):
+    _fields_ = [("d_color", dp), ("d_alpha_depth", dp), ("d_median_depth", dp), ("d_opacity", dp),
+                ("d_uncertainty", dp)]
+
+
+class Grads(C.Structure):
+    _fields_ = [("d_mean", dp), ("d_log_scale", dp), ("d_quat", dp), ("d_opacity_logit", dp), ("d_sh", dp),
+                ("d_mean2d", dp), ("d_pose", C.c_double * 6)]
+
+
+class GradcheckReport(C.Structure):
+    _fields_ = [("total", C.c_int32), ("checked", C.c_int32), ("skipped", C.c_int32), ("max_rel_err", C.c_double),
+                ("worst_analytic", C.c_double), ("worst_fd", C.c_double), ("worst_index", C.c_int32)]
+
+
+class MirOut(C.Structure):
+    _fields_ = [("visible", u8p), ("rank_to_id", i32p), ("tile_range", i32p), ("pair_rank", i32p),
+                ("pair_capacity", C.c_int64), ("color", fp), ("alpha_depth", fp), ("median_depth", fp),
+                ("median_valid", u8p), ("opacity", fp), ("uncertainty", fp), ("final_transmittance", fp),
+                ("per_pixel_count", i32p), ("dominant", i32p), ("median_prim", i32p), ("dominant_weight", fp),
+                ("last_index", i32p), ("num_visible", C.c_int64), ("num_pairs", C.c_int64)]
+
+
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        build()
+    L = C.CDLL(LIB_PATH)
+    sig = {
+        "orc_last_error": (C.c_char_p, []),
+        "orc_threads": (C.c_int, []),
+        "orc_render": (C.c_int, [C.POINTER(MapHost), C.POINTER(Pose), C.POINTER(Intrinsics), dp, C.POINTER(RasterCfg),
+                                 C.c_int, C.POINTER(C.c_void_p)]),
+        "orc_result_free": (None, [C.c_void_p]),
+        "orc_result_maps": (C.c_int, [C.c_void_p, C.POINTER(Maps)]),
+        "orc_result_record_total": (C.c_int64, [C.c_void_p]),
+        "orc_result_record": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), i32p, dp, dp]),
+        "orc_render_backward": (C.c_int, [C.POINTER(MapHost), C.POINTER(Pose), C.POINTER(Intrinsics), C.c_void_p,
+                                          C.POINTER(Upstream), dp, C.POINTER(RasterCfg), C.POINTER(Grads)]),
+        "orc_tracking_loss": (C.c_int, [C.c_void_p, dp, dp, C.POINTER(Intrinsics), C.POINTER(LossWeights),
+                                        C.POINTER(LossTerms), dp, dp]),
+        "orc_mapping_loss": (C.c_int, [C.POINTER(MapHost), C.c_void_p, dp, dp, C.POINTER(Intrinsics),
+                                       C.POINTER(LossWeights), C.POINTER(LossTerms), dp, dp, dp, dp, dp]),
+        "orc_ssim": (C.c_int, [dp, dp, C.c_int, C.c_int, dp, dp]),
+        "orc_adam_step": (None, [dp, dp, dp, dp, C.c_int64, C.POINTER(C.c_uint64), C.c_double, C.c_double, C.c_double,
+                                 C.c_double]),
+        "orc_track_frame": (C.c_int, [C.POINTER(MapHost), dp, dp, C.POINTER(Pose), C.POINTER(Intrinsics),
+                                      C.POINTER(TrackerCfg), C.POINTER(LossWeights), C.POINTER(RasterCfg),
+                                      C.POINTER(TrackResult)]),
+        "orc_mapstate_create": (C.c_int, [C.POINTER(MapHost), C.POINTER(MapperCfg), C.POINTER(C.c_void_p)]),
+        "orc_mapstate_free": (None, [C.c_void_p]),
+        "orc_mapstate_count": (C.c_int64, [C.c_void_p]),
+        "orc_mapstate_get": (C.c_int, [C.c_void_p, C.POINTER(MapHost)]),
+        "orc_map_step": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(dp), C.POINTER(dp), C.POINTER(Pose),
+                                   C.POINTER(Intrinsics), C.POINTER(MapperCfg), C.c_int, dp]),
+        "orc_sliding_ba": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(dp), C.POINTER(dp), C.POINTER(Pose), i32p,
+                                     C.POINTER(Intrinsics), C.POINTER(TrackerCfg), C.POINTER(MapperCfg), C.c_int, dp]),
+        "orc_accumulate_uncertainty": (C.c_int, [C.POINTER(MapHost), C.c_int, C.POINTER(C.c_void_p), C.POINTER(dp),
+                                                 C.POINTER(Pose), C.POINTER(Intrinsics), i32p]),
+        "orc_prune_unreliable": (C.c_int, [C.POINTER(MapHost), C.c_double, C.c_double, i32p]),
+        "orc_gradcheck_linear": (C.c_int, [C.POINTER(MapHost), C.POINTER(Pose), C.POINTER(Intrinsics),
+                                           C.POINTER(RasterCfg), dp, dp, dp, dp, dp, dp, C.c_double, C.c_double,
+                                           C.POINTER(GradcheckReport)]),
+        "orc_random_scene": (C.c_int, [C.c_uint32, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                       C.POINTER(MapHost)]),
+        "orc_wavy_depth": (None, [C.c_int, C.c_int, C.c_double, C.c_int, dp]),
+        "mir_render": (C.c_int, [C.POINTER(MapHost), C.POINTER(Pose), C.POINTER(Intrinsics), fp, C.POINTER(RasterCfg),
+                                 C.POINTER(MirOut)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+class OracleError(Exception):
+    def __init__(self, status, msg):
+        super().__init__(msg)
+        self.status = status
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(rc, lib().orc_last_error().decode())
+
+
+def _d(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(dp)
+
+
+def host_of(m) -> MapHost:
+    """MapHost view of any object with mean/log_scale/quat/opacity_logit/sh(/uncertainty/observed) arrays."""
+    P = m.mean.shape[0]
+    K = m.sh.shape[1] if m.sh.ndim == 3 else m.sh.shape[1] // 3
+    unc = getattr(m, "uncertainty", None)
+    obs = getattr(m, "observed", None)
+    return MapHost(P, K, m.mean.ctypes.data_as(dp), m.log_scale.ctypes.data_as(dp), m.quat.ctypes.data_as(dp),
+                   m.opacity_logit.ctypes.data_as(dp), m.sh.ctypes.data_as(dp),
+                   None if unc is None else unc.ctypes.data_as(dp), None if obs is None else obs.ctypes.data_as(u8p))
+
+
+def empty_map(P, K=1):
+    q = np.zeros((P, 4))
+    q[:, 0] = 1.0
+    return SimpleNamespace(mean=np.zeros((P, 3)), log_scale=np.zeros((P, 3)), quat=q, opacity_logit=np.zeros(P),
+                           sh=np.zeros((P, K, 3)), uncertainty=np.zeros(P), observed=np.zeros(P, np.uint8))
+
+
+def threads() -> int:
+    return int(lib().orc_threads())
+
+
+def random_scene(seed, count, sh_coeffs=1, max_opacity=0.95, min_scale=0.02, max_scale=0.15):
+    """tests/test_utils.hpp:27-53 with std::mt19937(seed)."""
+    m = empty_map(count, sh_coeffs)
+    h = host_of(m)
+    _check(lib().orc_random_scene(seed, count, sh_coeffs, max_opacity, min_scale, max_scale, C.byref(h)))
+    return m
+
+
+def wavy_depth(w, h, base, hole_every=17):
+    out = np.zeros(w * h)
+    lib().orc_wavy_depth(w, h, base, hole_every, out.ctypes.data_as(dp))
+    return out.reshape(h, w)
+
+
+class Result:
+    """Owning wrapper of an orc_result (RenderResult)."""
+
+    def __init__(self, handle, W, H, P):
+        self.h, self.W, self.H, self.P = handle, W, H, P
+        n = W * H
+        self.color = np.zeros((H, W, 3))
+        self.alpha_depth = np.zeros((H, W))
+        self.median_depth = np.zeros((H, W))
+        self.median_valid = np.zeros((H, W), np.uint8)
+        self.opacity = np.zeros((H, W))
+        self.uncertainty = np.zeros((H, W))
+        self.final_transmittance = np.zeros((H, W))
+        self.per_pixel_count = np.zeros((H, W), np.int32)
+        self.dominant = np.zeros((H, W), np.int32)
+        self.median_prim = np.zeros((H, W), np.int32)
+        self.dominant_weight = np.zeros((H, W))
+        self.visible = np.zeros(max(P, 1), np.uint8)
+        m = Maps(self.color.ctypes.data_as(dp), self.alpha_depth.ctypes.data_as(dp), self.median_depth.ctypes.data_as(dp),
+                 self.median_valid.ctypes.data_as(u8p), self.opacity.ctypes.data_as(dp),
+                 self.uncertainty.ctypes.data_as(dp), self.final_transmittance.ctypes.data_as(dp),
+                 self.per_pixel_count.ctypes.data_as(i32p), self.dominant.ctypes.data_as(i32p),
+                 self.median_prim.ctypes.data_as(i32p), self.dominant_weight.ctypes.data_as(dp),
+                 self.visible.ctypes.data_as(u8p), 0)
+        _check(lib().orc_result_maps(handle, C.byref(m)))
+        self.visible = self.visible[:P]
+        self.has_uncertainty = bool(m.has_uncertainty)
+        _ = n
+
+    def record(self):
+        t = lib().orc_result_record_total(self.h)
+        rs = np.zeros(self.W * self.H + 1, np.uint32)
+        prim = np.zeros(max(t, 1), np.int32)
+        a = np.zeros(max(t, 1))
+        tr = np.zeros(max(t, 1))
+        _check(lib().orc_result_record(self.h, rs.ctypes.data_as(C.POINTER(C.c_uint32)), prim.ctypes.data_as(i32p),
+                                       a.ctypes.data_as(dp), tr.ctypes.data_as(dp)))
+        return rs, prim[:t], a[:t], tr[:t]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_result_free(self.h)
+            self.h = None
+
+
+def render(m, pose: Pose, K: Intrinsics, obs=None, cfg: RasterCfg = None, brute_force=False) -> Result:
+    from paper_2403_16095_b200.abi import defaults_raster
+    cfg = cfg or defaults_raster()
+    h = host_of(m)
+    out = C.c_void_p()
+    o = None if obs is None else np.ascontiguousarray(obs, dtype=np.float64)
+    _check(lib().orc_render(C.byref(h), C.byref(pose), C.byref(K), None if o is None else o.ctypes.data_as(dp),
+                            C.byref(cfg), 1 if brute_force else 0, C.byref(out)))
+    return Result(out, K.width, K.height, m.mean.shape[0])
+
+
+def render_backward(m, pose, K, res: Result, d_color=None, d_alpha_depth=None, d_median_depth=None, d_opacity=None,
+                    d_uncertainty=None, obs=None, cfg=None):
+    from paper_2403_16095_b200.abi import defaults_raster
+    cfg = cfg or defaults_raster()
+    keep = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in
+            (d_color, d_alpha_depth, d_median_depth, d_opacity, d_uncertainty)]
+    up = Upstream(*[None if a is None else a.ctypes.data_as(dp) for a in keep])
+    P = m.mean.shape[0]
+    K_ = m.sh.shape[1]
+    g = SimpleNamespace(d_mean=np.zeros((P, 3)), d_log_scale=np.zeros((P, 3)), d_quat=np.zeros((P, 4)),
+                        d_opacity_logit=np.zeros(P), d_sh=np.zeros((P, K_, 3)), d_mean2d=np.zeros((P, 2)))
+    go = Grads(g.d_mean.ctypes.data_as(dp), g.d_log_scale.ctypes.data_as(dp), g.d_quat.ctypes.data_as(dp),
+               g.d_opacity_logit.ctypes.data_as(dp), g.d_sh.ctypes.data_as(dp), g.d_mean2d.ctypes.data_as(dp))
+    o = None if obs is None else np.ascontiguousarray(obs, dtype=np.float64)
+    h = host_of(m)
+    _check(lib().orc_render_backward(C.byref(h), C.byref(pose), C.byref(K), res.h, C.byref(up),
+                                     None if o is None else o.ctypes.data_as(dp), C.byref(cfg), C.byref(go)))
+    g.d_pose = np.array(list(go.d_pose))
+    return g
+
+
+def tracking_loss(res: Result, target, obs, K, w):
+    t = np.ascontiguousarray(target, dtype=np.float64)
+    o = np.ascontiguousarray(obs, dtype=np.float64)
+    out = LossTerms()
+    n = K.width * K.height
+    dc, dd = np.zeros(3 * n), np.zeros(n)
+    _check(lib().orc_tracking_loss(res.h, t.ctypes.data_as(dp), o.ctypes.data_as(dp), C.byref(K), C.byref(w),
+                                   C.byref(out), dc.ctypes.data_as(dp), dd.ctypes.data_as(dp)))
+    return out, dc, dd
+
+
+def mapping_loss(m, res: Result, target, obs, K, w):
+    t = np.ascontiguousarray(target, dtype=np.float64)
+    o = np.ascontiguousarray(obs, dtype=np.float64)
+    out = LossTerms()
+    n = K.width * K.height
+    P = m.mean.shape[0]
+    bufs = [np.zeros(3 * n), np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(3 * max(P, 1))]
+    h = host_of(m)
+    _check(lib().orc_mapping_loss(C.byref(h), res.h, t.ctypes.data_as(dp), o.ctypes.data_as(dp), C.byref(K),
+                                  C.byref(w), C.byref(out), *[b.ctypes.data_as(dp) for b in bufs]))
+    return out, bufs
+
+
+def ssim(x, y, w, h, gradient=False):
+    xa = np.ascontiguousarray(x, dtype=np.float64)
+    ya = np.ascontiguousarray(y, dtype=np.float64)
+    v = C.c_double()
+    g = np.zeros(3 * w * h) if gradient else None
+    _check(lib().orc_ssim(xa.ctypes.data_as(dp), ya.ctypes.data_as(dp), w, h, C.byref(v),
+                          None if g is None else g.ctypes.data_as(dp)))
+    return (v.value, g) if gradient else v.value
+
+
+def track_frame(m, rgb, depth, initial: Pose, K, tcfg, w, raster) -> TrackResult:
+    r = np.ascontiguousarray(rgb, dtype=np.float64)
+    d = np.ascontiguousarray(depth, dtype=np.float64)
+    out = TrackResult()
+    h = host_of(m)
+    _check(lib().orc_track_frame(C.byref(h), r.ctypes.data_as(dp), d.ctypes.data_as(dp), C.byref(initial), C.byref(K),
+                                 C.byref(tcfg), C.byref(w), C.byref(raster), C.byref(out)))
+    return out
+
+
+class MapState:
+    def __init__(self, m, mcfg: MapperCfg):
+        self.K = m.sh.shape[1]
+        h = host_of(m)
+        s = C.c_void_p()
+        _check(lib().orc_mapstate_create(C.byref(h), C.byref(mcfg), C.byref(s)))
+        self.h = s
+
+    def get(self):
+        P = lib().orc_mapstate_count(self.h)
+        m = empty_map(P, self.K)
+        h = host_of(m)
+        _check(lib().orc_mapstate_get(self.h, C.byref(h)))
+        return m
+
+    def map_step(self, frames, poses, K, mcfg, iterations):
+        n = len(frames)
+        keep = [(np.ascontiguousarray(r, dtype=np.float64), np.ascontiguousarray(d, dtype=np.float64)) for r, d in frames]
+        rg = (dp * n)(*[k[0].ctypes.data_as(dp) for k in keep])
+        dg = (dp * n)(*[k[1].ctypes.data_as(dp) for k in keep])
+        ps = (Pose * n)(*poses)
+        trace = np.zeros(max(iterations, 1))
+        _check(lib().orc_map_step(self.h, n, rg, dg, ps, C.byref(K), C.byref(mcfg), iterations, trace.ctypes.data_as(dp)))
+        return trace[:iterations]
+
+    def sliding_ba(self, frames, poses, frame_ids, K, tcfg, mcfg, iterations):
+        n = len(frames)
+        keep = [(np.ascontiguousarray(r, dtype=np.float64), np.ascontiguousarray(d, dtype=np.float64)) for r, d in frames]
+        rg = (dp * n)(*[k[0].ctypes.data_as(dp) for k in keep])
+        dg = (dp * n)(*[k[1].ctypes.data_as(dp) for k in keep])
+        ps = (Pose * n)(*poses)
+        fid = (C.c_int32 * n)(*frame_ids)
+        trace = np.zeros(max(iterations, 1))
+        _check(lib().orc_sliding_ba(self.h, n, rg, dg, ps, fid, C.byref(K), C.byref(tcfg), C.byref(mcfg), iterations,
+                                    trace.ctypes.data_as(dp)))
+        return trace[:iterations], [ps[i] for i in range(n)]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_mapstate_free(self.h)
+            self.h = None
+
+
+def accumulate_uncertainty(m, results, depths, poses, K):
+    n = len(results)
+    keep = [np.ascontiguousarray(d, dtype=np.float64) for d in depths]
+    rh = (C.c_void_p * max(n, 1))(*[r.h for r in results])
+    dg = (dp * max(n, 1))(*[k.ctypes.data_as(dp) for k in keep])
+    ps = (Pose * max(n, 1))(*poses)
+    cnt = C.c_int32()
+    h = host_of(m)
+    _check(lib().orc_accumulate_uncertainty(C.byref(h), n, rh, dg, ps, C.byref(K), C.byref(cnt)))
+    return cnt.value
+
+
+def prune_unreliable(m, tau=0.025, reduced=0.005):
+    r = C.c_int32()
+    h = host_of(m)
+    _check(lib().orc_prune_unreliable(C.byref(h), tau, reduced, C.byref(r)))
+    return r.value
+
+
+def gradcheck_linear(m, pose, K, cfg, obs, a_color, a_depth, a_opacity, a_uncert, a_median, step=1e-4, floor=1e-3):
+    rep = GradcheckReport()
+    keep = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in
+            (obs, a_color, a_depth, a_opacity, a_uncert, a_median)]
+    h = host_of(m)
+    _check(lib().orc_gradcheck_linear(C.byref(h), C.byref(pose), C.byref(K), C.byref(cfg),
+                                      *[None if a is None else a.ctypes.data_as(dp) for a in keep], step, floor,
+                                      C.byref(rep)))
+    return rep
+
+
+def mirror_render(m, pose, K, obs=None, cfg=None, pair_capacity=1 << 22):
+    from paper_2403_16095_b200.abi import defaults_raster
+    cfg = cfg or defaults_raster()
+    P = m.mean.shape[0]
+    W, H = K.width, K.height
+    ntiles = ((W + 15) // 16) * ((H + 15) // 16)
+    o = SimpleNamespace(visible=np.zeros(max(P, 1), np.uint8), rank_to_id=np.zeros(max(P, 1), np.int32),
+                        tile_range=np.zeros(2 * ntiles, np.int32), pair_rank=np.zeros(pair_capacity, np.int32),
+                        color=np.zeros((H, W, 3), np.float32), alpha_depth=np.zeros((H, W), np.float32),
+                        median_depth=np.zeros((H, W), np.float32), median_valid=np.zeros((H, W), np.uint8),
+                        opacity=np.zeros((H, W), np.float32), uncertainty=np.zeros((H, W), np.float32),
+                        final_transmittance=np.zeros((H, W), np.float32), per_pixel_count=np.zeros((H, W), np.int32),
+                        dominant=np.zeros((H, W), np.int32), median_prim=np.zeros((H, W), np.int32),
+                        dominant_weight=np.zeros((H, W), np.float32), last_index=np.zeros((H, W), np.int32))
+    mo = MirOut(o.visible.ctypes.data_as(u8p), o.rank_to_id.ctypes.data_as(i32p), o.tile_range.ctypes.data_as(i32p),
+                o.pair_rank.ctypes.data_as(i32p), pair_capacity, o.color.ctypes.data_as(fp), o.alpha_depth.ctypes.data_as(fp),
+                o.median_depth.ctypes.data_as(fp), o.median_valid.ctypes.data_as(u8p), o.opacity.ctypes.data_as(fp),
+                o.uncertainty.ctypes.data_as(fp), o.final_transmittance.ctypes.data_as(fp),
+                o.per_pixel_count.ctypes.data_as(i32p), o.dominant.ctypes.data_as(i32p),
+                o.median_prim.ctypes.data_as(i32p), o.dominant_weight.ctypes.data_as(fp), o.last_index.ctypes.data_as(i32p),
+                0, 0)
+    ob = None if obs is None else np.ascontiguousarray(obs, dtype=np.float32)
+    h = host_of(m)
+    _check(lib().mir_render(C.byref(h), C.byref(pose), C.byref(K), None if ob is None else ob.ctypes.data_as(fp),
+                            C.byref(cfg), C.byref(mo)))
+    o.num_visible, o.num_pairs = int(mo.num_visible), int(mo.num_pairs)
+    o.visible = o.visible[:P]
+    o.rank_to_id = o.rank_to_id[: o.num_visible]
+    o.pair_rank = o.pair_rank[: o.num_pairs]
+    return o

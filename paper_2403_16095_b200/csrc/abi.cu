@@ -1,0 +1,1413 @@
+// abi.cu — the C-ABI (include/gsf_cuda.h): context, map residency, and the device-resident
+// render / render_backward / losses / track_frame / map_step / sliding_ba / uncertainty loops.
+//
+// Host responsibilities only: argument validation with the reference's exception messages,
+// buffer residency, kernel sequencing on one stream, and turning device-side status flags
+// (DevState) back into the reference's error semantics.  Every number is computed on the device.
+#include <dlfcn.h>
+
+#include <cstddef>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gsf_cuda.h"
+#include "kernels.h"
+
+using namespace gsfk;
+
+namespace {
+
+struct EInval : std::invalid_argument {
+  explicit EInval(const std::string& s) : std::invalid_argument(s) {}
+};
+struct ENonFinite : std::invalid_argument {
+  int64_t index;
+  ENonFinite(const std::string& s, int64_t i) : std::invalid_argument(s), index(i) {}
+};
+struct EDiverged : std::runtime_error {
+  explicit EDiverged(const std::string& s) : std::runtime_error(s) {}
+};
+struct EUnsupported : std::runtime_error {
+  explicit EUnsupported(const std::string& s) : std::runtime_error(s) {}
+};
+
+// NCCL is opened at run time so the library has no link-time dependency on it.
+struct NcclApi {
+  void* h = nullptr;
+  int (*get_unique_id)(void*) = nullptr;
+  int (*comm_init_rank)(void**, int, const void*, int) = nullptr;  // ncclUniqueId passed by value (128 B)
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  const char* (*get_error)(int) = nullptr;
+  bool load() {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclGetUniqueId"));
+    all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclAllReduce"));
+    comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+    get_error = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+    return get_unique_id && all_reduce && comm_destroy;
+  }
+};
+NcclApi g_nccl;
+struct NcclUid { char b[128]; };
+typedef int (*nccl_init_fn)(void**, int, NcclUid, int);
+
+struct Frame {
+  float* rgb = nullptr;
+  float* depth = nullptr;
+  int w = 0, h = 0;
+};
+
+// Per-keyframe pose + Adam state for sliding_ba / map_step, device resident.
+struct KfPose {
+  double rot[3], trans[3];
+  double m[6], v[6];
+  double t;
+  double grad[6];
+};
+
+}  // namespace
+
+struct gsf_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t err_index = -1;
+  int64_t launches = 0;
+  // map
+  int64_t P = 0;
+  int K = 1;
+  int D = 14;
+  int64_t map_cap = 0;
+  int64_t map_gen = 0;
+  float* params = nullptr;
+  float* grads = nullptr;
+  float* adam_m = nullptr;
+  float* adam_v = nullptr;
+  double adam_step = 0.0;
+  float* nu = nullptr;
+  uint8_t* observed = nullptr;
+  float* d_mean2d = nullptr;
+  float* grad_accum = nullptr;
+  int32_t* grad_count = nullptr;
+  int64_t map_iteration = 0;
+  // device workspace + scalars
+  Workspace ws;
+  DevState* ds = nullptr;
+  DevState* ds_host = nullptr;   // pinned shadow for staging / readback
+  KfPose* kf = nullptr;
+  KfPose* kf_host = nullptr;
+  int kf_cap = 0;
+  double* trace_dev = nullptr;
+  int trace_cap = 0;
+  double* unc_sum = nullptr;
+  uint32_t* unc_cnt = nullptr;
+  uint32_t* counters = nullptr;
+  int64_t unc_cap = 0;
+  std::vector<Frame> frames;
+  // last render (for render_backward / loss API)
+  bool have_render = false;
+  int64_t render_gen = -1;
+  gsf_intrinsics rK{};
+  gsf_raster_cfg rcfg{};
+  bool render_obs = false;
+  // staging for host inputs
+  float* stage = nullptr;
+  size_t stage_bytes = 0;
+  // comm
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
+  float* red_f = nullptr;   // allreduce scratch for the loss sum
+  Profiler prof;
+  cudaEvent_t ev[8] = {nullptr};
+};
+
+namespace {
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+template <class T>
+void dalloc(T*& p, size_t count) {
+  dfree(p);
+  if (count == 0) count = 1;
+  GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * count));
+}
+
+void check_intrinsics(const gsf_intrinsics& k) {   // camera.hpp:20-26
+  if (!(k.fx > 0.0) || !(k.fy > 0.0)) throw EInval("intrinsics: focal lengths must be positive");
+  if (k.width <= 0 || k.height <= 0) throw EInval("intrinsics: image size must be positive");
+  if (!(k.depth_scale > 0.0)) throw EInval("intrinsics: depth_scale must be positive");
+  if (!(k.near_plane > 0.0) || !(k.far_plane > k.near_plane)) throw EInval("intrinsics: need 0 < near < far");
+}
+
+void check_raster(const gsf_raster_cfg& c) {
+  if (c.tile_size != kTile)
+    throw EUnsupported("raster.tile_size " + std::to_string(c.tile_size) + " is not supported on the device path (16 only)");
+}
+
+void check_weights(const gsf_loss_weights& w) {   // losses.cpp:49-56
+  const double all[] = {w.w_color, w.w_ssim, w.w_geo, w.w_align, w.w_iso, w.w_var, w.t_color, w.t_geo};
+  for (double v : all)
+    if (!(v >= 0.0)) throw EInval("loss weights must be non-negative");
+  if (!(w.iso_epsilon >= 1.0)) throw EInval("iso epsilon must be >= 1");
+  if (!(w.opacity_floor >= 0.0 && w.opacity_floor <= 1.0)) throw EInval("opacity floor must lie in [0,1]");
+}
+
+RasterParams make_rp(const gsf_ctx_s* c, const gsf_intrinsics& k, const gsf_raster_cfg& cfg) {
+  RasterParams rp;
+  rp.footprint_sigma = cfg.footprint_sigma;
+  rp.dilation = cfg.dilation;
+  rp.alpha_clamp = cfg.alpha_clamp;
+  rp.alpha_skip = cfg.alpha_skip;
+  rp.termination = cfg.termination_threshold;
+  rp.tile = kTile;
+  rp.tiles_x = (k.width + kTile - 1) / kTile;
+  rp.tiles_y = (k.height + kTile - 1) / kTile;
+  rp.sh_coeffs = c->K;
+  return rp;
+}
+
+LossParams make_lp(int mode, const gsf_loss_weights* w, const gsf_raster_cfg& cfg) {
+  LossParams lp{};
+  lp.mode = mode;
+  lp.uncertainty_full_gradient = cfg.uncertainty_full_gradient;
+  if (w) {
+    lp.opacity_floor = static_cast<float>(w->opacity_floor);
+    lp.normalize_by_valid = w->normalize_by_valid;
+    lp.w_color = w->w_color; lp.w_ssim = w->w_ssim; lp.w_geo = w->w_geo; lp.w_align = w->w_align;
+    lp.w_iso = w->w_iso; lp.w_var = w->w_var; lp.t_color = w->t_color; lp.t_geo = w->t_geo;
+    lp.iso_epsilon = w->iso_epsilon;
+  }
+  return lp;
+}
+
+Cam host_cam(const gsf_pose& p, const gsf_intrinsics& k) {
+  return make_cam(p.rotation_tangent, p.translation, k.fx, k.fy, k.cx, k.cy, k.width, k.height, k.near_plane, k.far_plane);
+}
+
+void* stage(gsf_ctx_s* c, size_t bytes) {
+  if (bytes > c->stage_bytes) {
+    if (c->stage) cudaFreeHost(c->stage);
+    c->stage = nullptr;
+    GSF_CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&c->stage), bytes));
+    c->stage_bytes = bytes;
+  }
+  return c->stage;
+}
+
+void sync(gsf_ctx_s* c) {
+  GSF_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  c->prof.resolve();
+}
+
+void read_state(gsf_ctx_s* c) {
+  GSF_CUDA_CHECK(cudaMemcpyAsync(c->ds_host, c->ds, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+}
+
+// Reset the per-call scalars; cam is written from the host shadow.
+void reset_state(gsf_ctx_s* c, const Cam* cam) {
+  DevState& h = *c->ds_host;
+  std::memset(&h, 0, sizeof(DevState));
+  h.bad_index = std::numeric_limits<int32_t>::max();
+  if (cam) h.cam = *cam;
+  GSF_CUDA_CHECK(cudaMemcpyAsync(c->ds, &h, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+}
+
+void ensure_map(gsf_ctx_s* c, int64_t P, int K) {
+  const int D = kFieldsBase + 3 * K;
+  if (P * D > c->map_cap * c->D || P > c->map_cap || !c->params) {
+    const int64_t cap = std::max<int64_t>(P, 1);
+    dalloc(c->params, static_cast<size_t>(cap) * D);
+    dalloc(c->grads, static_cast<size_t>(cap) * D);
+    dalloc(c->adam_m, static_cast<size_t>(cap) * D);
+    dalloc(c->adam_v, static_cast<size_t>(cap) * D);
+    dalloc(c->nu, cap);
+    dalloc(c->observed, cap);
+    dalloc(c->d_mean2d, 2 * cap);
+    dalloc(c->grad_accum, cap);
+    dalloc(c->grad_count, cap);
+    c->map_cap = cap;
+  }
+  c->P = P;
+  c->K = K;
+  c->D = D;
+}
+
+void ensure_ws(gsf_ctx_s* c, int W, int H) {
+  Workspace& ws = c->ws;
+  const int64_t P = std::max<int64_t>(c->P, 1);
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  const int64_t tiles = static_cast<int64_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
+  if (P > ws.P_cap) {
+    dalloc(ws.flag, P); dalloc(ws.vis_off, P); dalloc(ws.key_id, P);
+    dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
+    for (int i = 0; i < 2; ++i) { dalloc(ws.skeys[i], P); dalloc(ws.svals[i], P); }
+    dalloc(ws.rank_to_id, P); dalloc(ws.bg, P); dalloc(ws.gg, P); dalloc(ws.rect, P); dalloc(ws.tile_cnt, P);
+    dalloc(ws.pair_off, P + 1);
+    dalloc(ws.pose_part, static_cast<size_t>(div_up(P, 256)) * 6);
+    ws.P_cap = P;
+  }
+  if (ws.pair_cap == 0) ws.pair_cap = std::max<int64_t>(1 << 20, 4 * P);
+  if (!ws.pkeys[0]) {
+    for (int i = 0; i < 2; ++i) { dalloc(ws.pkeys[i], ws.pair_cap); dalloc(ws.pvals[i], ws.pair_cap); }
+    dalloc(ws.pair_rank, ws.pair_cap);
+    dalloc(ws.partials, ws.pair_cap * 10);
+  }
+  if (npix > ws.npix_cap) {
+    dalloc(ws.color, 3 * npix); dalloc(ws.alpha_depth, npix); dalloc(ws.median_depth, npix); dalloc(ws.median_valid, npix);
+    dalloc(ws.opacity, npix); dalloc(ws.uncertainty, npix); dalloc(ws.final_T, npix); dalloc(ws.count, npix);
+    dalloc(ws.dominant, npix); dalloc(ws.median_prim, npix); dalloc(ws.dominant_w, npix); dalloc(ws.last, npix);
+    dalloc(ws.obs, npix); dalloc(ws.upstream, 7 * npix); dalloc(ws.dssim, 3 * npix); dalloc(ws.ssim_tmp, 24 * npix);
+    ws.npix_cap = npix;
+  }
+  if (tiles > ws.tiles_cap) {
+    dalloc(ws.ranges, tiles);
+    dalloc(ws.loss_part, tiles * LS_NUM);
+    ws.tiles_cap = tiles;
+  }
+  const int64_t scan_n = std::max<int64_t>(P, npix);
+  const size_t sb = scan_temp_bytes(static_cast<uint32_t>(scan_n));
+  const size_t rb = std::max(radix_temp_bytes(static_cast<uint32_t>(P), 4), radix_temp_bytes(static_cast<uint32_t>(ws.pair_cap), 4));
+  // scan state and radix temp are sized for the largest of P / npix / pair_cap
+  if (!ws.scan.state || ws.radix_temp_bytes < rb + sb) {
+    dfree(ws.scan.state);
+    dfree(ws.radix_temp);
+    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ws.scan.state), sb + 64));
+    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ws.radix_temp), rb));
+    ws.radix_temp_bytes = rb + sb;
+  }
+  const int64_t red = 2 * std::max<int64_t>(div_up(npix, 256), div_up(P, 256)) + 64;
+  if (!ws.red_part || ws.red_iso_offset * 2 < red) {
+    dalloc(ws.red_part, red);
+    ws.red_iso_offset = red / 2;
+  }
+  if (!c->counters) dalloc(c->counters, 16);
+}
+
+void grow_pairs(gsf_ctx_s* c, uint32_t needed) {
+  Workspace& ws = c->ws;
+  ws.pair_cap = static_cast<int64_t>(needed) + needed / 4 + 1024;
+  for (int i = 0; i < 2; ++i) { dalloc(ws.pkeys[i], ws.pair_cap); dalloc(ws.pvals[i], ws.pair_cap); }
+  dalloc(ws.pair_rank, ws.pair_cap);
+  dalloc(ws.partials, ws.pair_cap * 10);
+  const size_t rb = std::max(radix_temp_bytes(static_cast<uint32_t>(ws.P_cap), 4), radix_temp_bytes(static_cast<uint32_t>(ws.pair_cap), 4));
+  dfree(ws.radix_temp);
+  GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ws.radix_temp), rb));
+}
+
+FwdArgs fwd_args(gsf_ctx_s* c, const gsf_intrinsics& k, const gsf_raster_cfg& cfg, const float* obs, const float* loss_rgb,
+                 const float* loss_depth, const LossParams& lp, int iteration) {
+  FwdArgs a;
+  a.params = c->params;
+  a.P = c->P;
+  a.K = c->K;
+  a.rp = make_rp(c, k, cfg);
+  a.kc = make_blend_consts(a.rp);
+  a.W = k.width;
+  a.H = k.height;
+  a.near_plane = k.near_plane;
+  a.far_plane = k.far_plane;
+  a.obs = obs;
+  a.loss_rgb = loss_rgb;
+  a.loss_depth = loss_depth;
+  a.lp = lp;
+  a.iteration = iteration;
+  return a;
+}
+
+BwdArgs bwd_args(gsf_ctx_s* c, const gsf_intrinsics& k, const gsf_raster_cfg& cfg, const float* obs, const float* target,
+                 const LossParams& lp, int seed_mode, bool pose_only) {
+  BwdArgs b{};
+  b.params = c->params;
+  b.P = c->P;
+  b.K = c->K;
+  b.rp = make_rp(c, k, cfg);
+  b.kc = make_blend_consts(b.rp);
+  b.W = k.width;
+  b.H = k.height;
+  b.near_plane = k.near_plane;
+  b.far_plane = k.far_plane;
+  b.obs = obs;
+  b.target_rgb = target;
+  b.lp = lp;
+  b.seed_mode = seed_mode;
+  b.pose_only = pose_only;
+  b.grads = c->grads;
+  b.d_mean2d = c->d_mean2d;
+  return b;
+}
+
+void throw_nonfinite(int32_t idx) {
+  throw ENonFinite("render: primitive " + std::to_string(idx) + " has non-finite parameters", idx);
+}
+
+// One device render with the overflow-retry protocol (API path, synchronous).
+void render_sync(gsf_ctx_s* c, const gsf_pose& pose, const gsf_intrinsics& k, const gsf_raster_cfg& cfg, const float* obs_dev) {
+  ensure_ws(c, k.width, k.height);
+  const Cam cam = host_cam(pose, k);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    reset_state(c, &cam);
+    c->ds_host->has_obs = obs_dev ? 1 : 0;
+    GSF_CUDA_CHECK(cudaMemcpyAsync(&c->ds->has_obs, &c->ds_host->has_obs, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    run_forward(c->ws, c->ds, fwd_args(c, k, cfg, obs_dev, nullptr, nullptr, make_lp(0, nullptr, cfg), -1), c->stream, &c->launches);
+    read_state(c);
+    if (c->ds_host->bad_index != std::numeric_limits<int32_t>::max()) throw_nonfinite(c->ds_host->bad_index);
+    if (!c->ds_host->overflow) break;
+    grow_pairs(c, c->ds_host->M);
+  }
+  c->have_render = true;
+  c->render_gen = c->map_gen;
+  c->rK = k;
+  c->rcfg = cfg;
+  c->render_obs = obs_dev != nullptr;
+}
+
+void upload_floats(gsf_ctx_s* c, float* dst, const float* src, size_t n) {
+  GSF_CUDA_CHECK(cudaMemcpyAsync(dst, src, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+}
+
+template <class F>
+int guard(gsf_ctx c, F&& f) {
+  if (!c) return GSF_EINVAL;
+  c->err.clear();
+  c->err_index = -1;
+  try {
+    cudaSetDevice(c->device);
+    f();
+    return GSF_OK;
+  } catch (const ENonFinite& e) {
+    c->err = e.what();
+    c->err_index = e.index;
+    return GSF_ENONFINITE;
+  } catch (const EInval& e) {
+    c->err = e.what();
+    return GSF_EINVAL;
+  } catch (const EDiverged& e) {
+    c->err = e.what();
+    return GSF_EDIVERGED;
+  } catch (const EUnsupported& e) {
+    c->err = e.what();
+    return GSF_EUNSUPPORTED;
+  } catch (const CudaError& e) {
+    std::ostringstream m;
+    m << "CUDA error " << cudaGetErrorName(e.code) << " (" << cudaGetErrorString(e.code) << ") at " << e.file << ":"
+      << e.line << " in " << e.expr;
+    c->err = m.str();
+    return GSF_ECUDA;
+  } catch (const std::bad_alloc&) {
+    c->err = "host allocation failed";
+    return GSF_ENOMEM;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return GSF_EINVAL;
+  }
+}
+
+const Frame& get_frame(gsf_ctx_s* c, int slot, const gsf_intrinsics& k) {
+  if (slot < 0 || slot >= static_cast<int>(c->frames.size()) || !c->frames[slot].rgb)
+    throw EInval("frame slot " + std::to_string(slot) + " is empty");
+  const Frame& f = c->frames[slot];
+  if (f.w != k.width || f.h != k.height) throw EInval("loss: target rgb dimensions mismatch");
+  return f;
+}
+
+void ensure_kf(gsf_ctx_s* c, int n) {
+  if (n <= c->kf_cap) return;
+  dfree(c->kf);
+  if (c->kf_host) cudaFreeHost(c->kf_host);
+  dalloc(c->kf, n);
+  GSF_CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&c->kf_host), sizeof(KfPose) * n));
+  c->kf_cap = n;
+}
+
+void ensure_trace(gsf_ctx_s* c, int n) {
+  if (n <= c->trace_cap) return;
+  dalloc(c->trace_dev, n);
+  c->trace_cap = n;
+}
+
+}  // namespace
+
+// ---- small device helpers used by the loops ---------------------------------------------------
+namespace {
+
+__global__ void k_set_cam_from_kf(DevState* ds, const KfPose* kf, int k, int has_obs) {
+  const Cam old = ds->cam;
+  ds->cam = make_cam(kf[k].rot, kf[k].trans, old.fx, old.fy, old.cx, old.cy, old.width, old.height, old.near_plane,
+                     old.far_plane);
+  ds->has_obs = has_obs;
+}
+
+__global__ void k_kf_grab(DevState* ds, KfPose* kf, int k, double* loss_acc, double* trace, int it, int store_trace) {
+  for (int a = 0; a < 6; ++a) kf[k].grad[a] = ds->d_pose[a];
+  if (loss_acc) *loss_acc += ds->loss_total;
+  if (store_trace && trace) trace[it] = ds->loss_total;
+}
+
+__global__ void k_store(const double* src, double* dst) { *dst = *src; }
+
+// Pose Adam + perturbed for every non-anchor keyframe (tracker.cpp:168-179).
+__global__ void k_kf_update(DevState* ds, KfPose* kf, int n, int anchor, double lr_rot, double lr_trans) {
+  const int k = threadIdx.x;
+  if (k >= n || k == anchor || ds->halt) return;
+  KfPose& p = kf[k];
+  p.t += 1.0;
+  const double bc1 = 1.0 - pow(0.9, p.t), bc2 = 1.0 - pow(0.999, p.t);
+  double delta[6];
+  for (int a = 0; a < 6; ++a) {
+    const double g = p.grad[a];
+    p.m[a] = 0.9 * p.m[a] + (1.0 - 0.9) * g;
+    p.v[a] = 0.999 * p.v[a] + (1.0 - 0.999) * g * g;
+    delta[a] = 0.0 - (a < 3 ? lr_rot : lr_trans) * (p.m[a] / bc1) / (sqrt(p.v[a] / bc2) + 1e-8);
+  }
+  double dR[9], Rc[9], Rn[9];
+  exp_map_d(delta, dR);
+  exp_map_d(p.rot, Rc);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) Rn[3 * i + j] = dR[3 * i] * Rc[j] + dR[3 * i + 1] * Rc[3 + j] + dR[3 * i + 2] * Rc[6 + j];
+  double tn[3];
+  for (int i = 0; i < 3; ++i) tn[i] = dR[3 * i] * p.trans[0] + dR[3 * i + 1] * p.trans[1] + dR[3 * i + 2] * p.trans[2] + delta[3 + i];
+  // log_map (lie.cpp:30-52)
+  const double trace = Rn[0] + Rn[4] + Rn[8];
+  double ct = (trace - 1.0) * 0.5;
+  ct = ct < -1.0 ? -1.0 : (ct > 1.0 ? 1.0 : ct);
+  const double th = acos(ct);
+  const double vee[3] = {Rn[7] - Rn[5], Rn[2] - Rn[6], Rn[3] - Rn[1]};
+  double out[3];
+  if (th < 1e-8) {
+    const double f = 0.5 * (1.0 + th * th / 6.0);
+    for (int i = 0; i < 3; ++i) out[i] = f * vee[i];
+  } else if (th > M_PI - 1e-3) {
+    double o[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) o[3 * i + j] = (0.5 * (Rn[3 * i + j] + Rn[3 * j + i]) - ct * (i == j ? 1.0 : 0.0)) / (1.0 - ct);
+    int a = 0;
+    for (int i = 1; i < 3; ++i)
+      if (o[4 * i] > o[4 * a]) a = i;
+    const double sq = sqrt(o[4 * a]);
+    double ax[3] = {o[a] / sq, o[3 + a] / sq, o[6 + a] / sq};
+    if (ax[0] * vee[0] + ax[1] * vee[1] + ax[2] * vee[2] < 0.0)
+      for (int i = 0; i < 3; ++i) ax[i] = -ax[i];
+    for (int i = 0; i < 3; ++i) out[i] = th * ax[i];
+  } else {
+    const double f = th / (2.0 * sin(th));
+    for (int i = 0; i < 3; ++i) out[i] = f * vee[i];
+  }
+  for (int i = 0; i < 3; ++i) { p.rot[i] = out[i]; p.trans[i] = tn[i]; }
+}
+
+__global__ void k_gather_grads_aos(const float* __restrict__ g, int64_t P, int K, const float* __restrict__ m2d,
+                                   float* __restrict__ out) {
+  // out: per primitive [mean3, ls3, quat4, op1, sh 3K, mean2d 2] contiguous (AoS, for download)
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int D = kFieldsBase + 3 * K;
+  float* o = out + i * (D + 2);
+  for (int f = 0; f < D; ++f) o[f] = g[f * P + i];
+  o[D] = m2d[i];
+  o[D + 1] = m2d[P + i];
+}
+
+__global__ void k_scatter_map_soa(const double* __restrict__ in, int64_t P, int K, float* __restrict__ params) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int D = kFieldsBase + 3 * K;
+  for (int f = 0; f < D; ++f) params[f * P + i] = static_cast<float>(in[i * D + f]);
+}
+
+__global__ void k_gather_map_aos(const float* __restrict__ params, int64_t P, int K, double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int D = kFieldsBase + 3 * K;
+  for (int f = 0; f < D; ++f) out[i * D + f] = params[f * P + i];
+}
+
+__global__ void k_add_d(double* acc, const double* v) { *acc += *v; }
+
+// CSR record of the last render (rasterizer.cpp:240-259): per-pixel contributors front to back.
+__global__ void k_record(const int2* __restrict__ ranges, const uint32_t* __restrict__ sorted_orig,
+                         const uint32_t* __restrict__ pair_rank, const BlendG* __restrict__ bg,
+                         const GuardG* __restrict__ gg, const int32_t* __restrict__ rank_to_id,
+                         const int32_t* __restrict__ last, const uint32_t* __restrict__ row_start, int W, int H, int tiles_x,
+                         BlendConsts kc, int32_t* __restrict__ prim, float* __restrict__ alpha, float* __restrict__ trans) {
+  const int64_t pi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pi >= static_cast<int64_t>(W) * H) return;
+  const int x = static_cast<int>(pi % W), y = static_cast<int>(pi / W);
+  const int tile = (y / kTile) * tiles_x + (x / kTile);
+  const int2 rg = ranges[tile];
+  const int lim = last[pi];
+  const float px = x + 0.5f, py = y + 0.5f;
+  uint32_t out = row_start[pi];
+  float T = 1.0f;
+  for (int j = 0; j < lim; ++j) {
+    const int r = static_cast<int>(pair_rank[sorted_orig[rg.x + j]]);
+    const PairEval e = eval_pair(px, py, bg[r], gg + r, kc);
+    if (!e.code) continue;
+    prim[out] = rank_to_id[r];
+    alpha[out] = e.alpha;
+    trans[out] = T;
+    ++out;
+    T = fmul(T, fsub(1.0f, e.alpha));
+  }
+}
+
+}  // namespace
+
+// =================================================================================================
+extern "C" {
+
+int gsf_abi_version(void) { return GSF_ABI_VERSION; }
+
+int gsf_ctx_create(int device, gsf_ctx* out) {
+  if (!out) return GSF_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) return GSF_ECUDA;
+  auto* c = new gsf_ctx_s;
+  c->device = device;
+  const int rc = guard(c, [&] {
+    GSF_CUDA_CHECK(cudaSetDevice(device));
+    GSF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    dalloc(c->ds, 1);
+    GSF_CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&c->ds_host), sizeof(DevState)));
+    reset_state(c, nullptr);
+    sync(c);
+  });
+  if (rc != GSF_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return GSF_OK;
+}
+
+int gsf_ctx_destroy(gsf_ctx c) {
+  if (!c) return GSF_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
+  Workspace& ws = c->ws;
+  void* bufs[] = {ws.flag, ws.vis_off, ws.key_id, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id, ws.visible,
+                  ws.skeys[0], ws.skeys[1], ws.svals[0], ws.svals[1], ws.rank_to_id, ws.bg, ws.gg, ws.rect,
+                  ws.tile_cnt, ws.pair_off, ws.pkeys[0], ws.pkeys[1], ws.pvals[0], ws.pvals[1], ws.pair_rank,
+                  ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
+                  ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
+                  ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.scan.state, ws.radix_temp, ws.pose_part,
+                  ws.red_part, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
+                  c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
+                  c->red_f};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  for (Frame& f : c->frames) {
+    if (f.rgb) cudaFree(f.rgb);
+    if (f.depth) cudaFree(f.depth);
+  }
+  if (c->ds_host) cudaFreeHost(c->ds_host);
+  if (c->kf_host) cudaFreeHost(c->kf_host);
+  if (c->stage) cudaFreeHost(c->stage);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return GSF_OK;
+}
+
+const char* gsf_last_error(gsf_ctx c) { return c ? c->err.c_str() : "null context"; }
+int64_t gsf_last_error_index(gsf_ctx c) { return c ? c->err_index : -1; }
+int64_t gsf_kernel_launches(gsf_ctx c) { return c ? c->launches : 0; }
+int gsf_synchronize(gsf_ctx c) {
+  return guard(c, [&] { sync(c); });
+}
+
+int gsf_map_upload(gsf_ctx c, const gsf_map_host* m) {
+  return guard(c, [&] {
+    if (!m || m->count < 0) throw EInval("map: negative primitive count");
+    const int K = m->sh_coeffs;
+    if (K != 0 && K != 1 && K != 4 && K != 9 && K != 16) throw EInval("sh coefficient count must be 1, 4, 9 or 16");
+    const int64_t P = m->count;
+    ensure_map(c, P, K);
+    const int D = c->D;
+    double* h = static_cast<double*>(stage(c, sizeof(double) * std::max<int64_t>(P, 1) * D));
+    for (int64_t i = 0; i < P; ++i) {
+      double* o = h + i * D;
+      for (int a = 0; a < 3; ++a) o[a] = m->mean[3 * i + a];
+      for (int a = 0; a < 3; ++a) o[3 + a] = m->log_scale[3 * i + a];
+      for (int a = 0; a < 4; ++a) o[6 + a] = m->quat[4 * i + a];
+      o[10] = m->opacity_logit[i];
+      for (int b = 0; b < 3 * K; ++b) o[11 + b] = m->sh[3 * K * i + b];
+    }
+    if (P > 0) {
+      double* tmp = nullptr;
+      GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&tmp), sizeof(double) * P * D));
+      GSF_CUDA_CHECK(cudaMemcpyAsync(tmp, h, sizeof(double) * P * D, cudaMemcpyHostToDevice, c->stream));
+      k_scatter_map_soa<<<div_up(P, 256), 256, 0, c->stream>>>(tmp, P, K, c->params);
+      ++c->launches;
+      sync(c);
+      cudaFree(tmp);
+      std::vector<float> nu(P, 0.0f);
+      std::vector<uint8_t> ob(P, 0);
+      for (int64_t i = 0; i < P; ++i) {
+        if (m->uncertainty) nu[i] = static_cast<float>(m->uncertainty[i]);
+        if (m->observed) ob[i] = m->observed[i];
+      }
+      GSF_CUDA_CHECK(cudaMemcpy(c->nu, nu.data(), sizeof(float) * P, cudaMemcpyHostToDevice));
+      GSF_CUDA_CHECK(cudaMemcpy(c->observed, ob.data(), P, cudaMemcpyHostToDevice));
+      GSF_CUDA_CHECK(cudaMemset(c->adam_m, 0, sizeof(float) * P * D));
+      GSF_CUDA_CHECK(cudaMemset(c->adam_v, 0, sizeof(float) * P * D));
+      GSF_CUDA_CHECK(cudaMemset(c->grad_accum, 0, sizeof(float) * P));
+      GSF_CUDA_CHECK(cudaMemset(c->grad_count, 0, sizeof(int32_t) * P));
+    }
+    c->adam_step = 0.0;
+    c->map_iteration = 0;
+    ++c->map_gen;
+    c->have_render = false;
+  });
+}
+
+int gsf_map_download(gsf_ctx c, gsf_map_host* m) {
+  return guard(c, [&] {
+    if (!m || m->count != c->P) throw EInval("map_download: primitive count mismatch");
+    const int64_t P = c->P;
+    const int K = c->K, D = c->D;
+    if (P == 0) return;
+    double* tmp = nullptr;
+    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&tmp), sizeof(double) * P * D));
+    k_gather_map_aos<<<div_up(P, 256), 256, 0, c->stream>>>(c->params, P, K, tmp);
+    ++c->launches;
+    double* h = static_cast<double*>(stage(c, sizeof(double) * P * D));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(h, tmp, sizeof(double) * P * D, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<float> nu(P);
+    std::vector<uint8_t> ob(P);
+    GSF_CUDA_CHECK(cudaMemcpyAsync(nu.data(), c->nu, sizeof(float) * P, cudaMemcpyDeviceToHost, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(ob.data(), c->observed, P, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    cudaFree(tmp);
+    for (int64_t i = 0; i < P; ++i) {
+      const double* o = h + i * D;
+      if (m->mean) for (int a = 0; a < 3; ++a) m->mean[3 * i + a] = o[a];
+      if (m->log_scale) for (int a = 0; a < 3; ++a) m->log_scale[3 * i + a] = o[3 + a];
+      if (m->quat) for (int a = 0; a < 4; ++a) m->quat[4 * i + a] = o[6 + a];
+      if (m->opacity_logit) m->opacity_logit[i] = o[10];
+      if (m->sh && m->sh_coeffs == K) for (int b = 0; b < 3 * K; ++b) m->sh[3 * K * i + b] = o[11 + b];
+      if (m->uncertainty) m->uncertainty[i] = nu[i];
+      if (m->observed) m->observed[i] = ob[i];
+    }
+  });
+}
+
+int64_t gsf_map_count(gsf_ctx c) { return c ? c->P : -1; }
+
+int gsf_profile_enable(gsf_ctx c, int32_t on) {
+  return guard(c, [&] {
+    sync(c);
+    c->prof.on = on != 0;
+    c->ws.prof = on ? &c->prof : nullptr;
+    for (int i = 0; i < 16; ++i) { c->prof.total_ms[i] = 0.0; c->prof.count[i] = 0; }
+  });
+}
+
+int gsf_profile_read(gsf_ctx c, int32_t name, double* total_ms, int64_t* launches) {
+  return guard(c, [&] {
+    if (name < 0 || name >= PROF_NUM) throw EInval("profile_read: unknown kernel class");
+    sync(c);
+    *total_ms = c->prof.total_ms[name];
+    *launches = c->prof.count[name];
+  });
+}
+
+int gsf_event_record(gsf_ctx c, int32_t slot) {
+  return guard(c, [&] {
+    if (slot < 0 || slot >= 8) throw EInval("event slot out of range");
+    if (!c->ev[slot]) GSF_CUDA_CHECK(cudaEventCreate(&c->ev[slot]));
+    GSF_CUDA_CHECK(cudaEventRecord(c->ev[slot], c->stream));
+  });
+}
+
+int gsf_event_elapsed(gsf_ctx c, int32_t a, int32_t b, double* ms) {
+  return guard(c, [&] {
+    if (a < 0 || a >= 8 || b < 0 || b >= 8 || !c->ev[a] || !c->ev[b]) throw EInval("event slot not recorded");
+    GSF_CUDA_CHECK(cudaEventSynchronize(c->ev[b]));
+    float f = 0.0f;
+    GSF_CUDA_CHECK(cudaEventElapsedTime(&f, c->ev[a], c->ev[b]));
+    *ms = f;
+  });
+}
+
+int gsf_optimizer_reset(gsf_ctx c) {
+  return guard(c, [&] {
+    if (c->P > 0) {
+      GSF_CUDA_CHECK(cudaMemsetAsync(c->adam_m, 0, sizeof(float) * c->P * c->D, c->stream));
+      GSF_CUDA_CHECK(cudaMemsetAsync(c->adam_v, 0, sizeof(float) * c->P * c->D, c->stream));
+      GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_accum, 0, sizeof(float) * c->P, c->stream));
+      GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_count, 0, sizeof(int32_t) * c->P, c->stream));
+    }
+    c->adam_step = 0.0;
+    c->map_iteration = 0;
+    sync(c);
+  });
+}
+
+int gsf_render(gsf_ctx c, const gsf_pose* pose, const gsf_intrinsics* K, const float* obs, const gsf_raster_cfg* cfg,
+               gsf_render_out* out) {
+  return guard(c, [&] {
+    check_intrinsics(*K);
+    check_raster(*cfg);
+    const int W = K->width, H = K->height;
+    const int64_t npix = static_cast<int64_t>(W) * H;
+    ensure_ws(c, W, H);
+    if (obs) upload_floats(c, c->ws.obs, obs, npix);
+    render_sync(c, *pose, *K, *cfg, obs ? c->ws.obs : nullptr);
+    Workspace& ws = c->ws;
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      if (dst) GSF_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    };
+    if (out) {
+      d2h(out->color, ws.color, sizeof(float) * 3 * npix);
+      d2h(out->alpha_depth, ws.alpha_depth, sizeof(float) * npix);
+      d2h(out->median_depth, ws.median_depth, sizeof(float) * npix);
+      d2h(out->median_valid, ws.median_valid, npix);
+      d2h(out->opacity, ws.opacity, sizeof(float) * npix);
+      d2h(out->uncertainty, ws.uncertainty, sizeof(float) * npix);
+      d2h(out->final_transmittance, ws.final_T, sizeof(float) * npix);
+      d2h(out->per_pixel_count, ws.count, sizeof(int32_t) * npix);
+      d2h(out->dominant, ws.dominant, sizeof(int32_t) * npix);
+      d2h(out->median_prim, ws.median_prim, sizeof(int32_t) * npix);
+      d2h(out->dominant_weight, ws.dominant_w, sizeof(float) * npix);
+      if (c->P > 0) d2h(out->visible, ws.visible, c->P);
+      sync(c);
+      out->has_uncertainty = obs ? 1 : 0;
+      out->num_visible = c->ds_host->V;
+      out->num_pairs = c->ds_host->M;
+      if (!obs && out->uncertainty) std::memset(out->uncertainty, 0, sizeof(float) * npix);
+    }
+  });
+}
+
+int gsf_render_record(gsf_ctx c, uint32_t* row_start, int32_t* prim, float* alpha, float* trans, int64_t* total) {
+  return guard(c, [&] {
+    if (!c->have_render) throw EInval("render_record: no render on this context");
+    const int W = c->rK.width, H = c->rK.height;
+    const int64_t npix = static_cast<int64_t>(W) * H;
+    std::vector<int32_t> cnt(npix);
+    GSF_CUDA_CHECK(cudaMemcpy(cnt.data(), c->ws.count, sizeof(int32_t) * npix, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> rs(npix + 1);
+    uint64_t acc = 0;
+    for (int64_t i = 0; i < npix; ++i) {
+      rs[i] = static_cast<uint32_t>(acc);
+      acc += static_cast<uint64_t>(cnt[i]);
+    }
+    rs[npix] = static_cast<uint32_t>(acc);
+    *total = static_cast<int64_t>(acc);
+    if (row_start) std::memcpy(row_start, rs.data(), sizeof(uint32_t) * (npix + 1));
+    if (!prim) return;
+    uint32_t* d_rs = nullptr;
+    int32_t* d_prim = nullptr;
+    float *d_a = nullptr, *d_t = nullptr;
+    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d_rs), sizeof(uint32_t) * (npix + 1)));
+    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d_prim), sizeof(int32_t) * std::max<uint64_t>(acc, 1)));
+    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d_a), sizeof(float) * std::max<uint64_t>(acc, 1)));
+    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d_t), sizeof(float) * std::max<uint64_t>(acc, 1)));
+    GSF_CUDA_CHECK(cudaMemcpy(d_rs, rs.data(), sizeof(uint32_t) * (npix + 1), cudaMemcpyHostToDevice));
+    const RasterParams rp = make_rp(c, c->rK, c->rcfg);
+    k_record<<<div_up(npix, 256), 256, 0, c->stream>>>(c->ws.ranges, c->ws.pair_sorted_vals, c->ws.pair_rank, c->ws.bg,
+                                                        c->ws.gg, c->ws.rank_to_id, c->ws.last, d_rs, W, H, rp.tiles_x,
+                                                        make_blend_consts(rp), d_prim, d_a, d_t);
+    ++c->launches;
+    sync(c);
+    if (acc) {
+      GSF_CUDA_CHECK(cudaMemcpy(prim, d_prim, sizeof(int32_t) * acc, cudaMemcpyDeviceToHost));
+      if (alpha) GSF_CUDA_CHECK(cudaMemcpy(alpha, d_a, sizeof(float) * acc, cudaMemcpyDeviceToHost));
+      if (trans) GSF_CUDA_CHECK(cudaMemcpy(trans, d_t, sizeof(float) * acc, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(d_rs); cudaFree(d_prim); cudaFree(d_a); cudaFree(d_t);
+  });
+}
+
+int gsf_render_tiles(gsf_ctx c, int32_t* rank_to_id, int64_t rank_cap, int32_t* tile_range, int64_t tiles_cap,
+                     int32_t* pair_rank, int64_t pair_cap) {
+  return guard(c, [&] {
+    if (!c->have_render) throw EInval("render_tiles: no render on this context");
+    read_state(c);
+    const uint32_t V = c->ds_host->V, M = c->ds_host->M;
+    const int tiles = ((c->rK.width + kTile - 1) / kTile) * ((c->rK.height + kTile - 1) / kTile);
+    if (rank_to_id) {
+      if (rank_cap < V) throw EInval("render_tiles: rank capacity too small");
+      GSF_CUDA_CHECK(cudaMemcpy(rank_to_id, c->ws.rank_to_id, sizeof(int32_t) * V, cudaMemcpyDeviceToHost));
+    }
+    if (tile_range) {
+      if (tiles_cap < tiles) throw EInval("render_tiles: tile capacity too small");
+      GSF_CUDA_CHECK(cudaMemcpy(tile_range, c->ws.ranges, sizeof(int2) * tiles, cudaMemcpyDeviceToHost));
+    }
+    if (pair_rank) {
+      if (pair_cap < M) throw EInval("render_tiles: pair capacity too small");
+      std::vector<uint32_t> orig(M), pr(std::max<uint32_t>(M, 1));
+      if (M) {
+        GSF_CUDA_CHECK(cudaMemcpy(orig.data(), c->ws.pair_sorted_vals, sizeof(uint32_t) * M, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> rank_of(M);
+        GSF_CUDA_CHECK(cudaMemcpy(rank_of.data(), c->ws.pair_rank, sizeof(uint32_t) * M, cudaMemcpyDeviceToHost));
+        for (uint32_t s = 0; s < M; ++s) pair_rank[s] = static_cast<int32_t>(rank_of[orig[s]]);
+      }
+    }
+  });
+}
+
+static void download_grads(gsf_ctx_s* c, gsf_grads_out* out) {
+  const int64_t P = c->P;
+  const int K = c->K, D = c->D;
+  if (P > 0) {
+    float* tmp = nullptr;
+    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&tmp), sizeof(float) * P * (D + 2)));
+    k_gather_grads_aos<<<div_up(P, 256), 256, 0, c->stream>>>(c->grads, P, K, c->d_mean2d, tmp);
+    ++c->launches;
+    std::vector<float> h(static_cast<size_t>(P) * (D + 2));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(h.data(), tmp, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    cudaFree(tmp);
+    for (int64_t i = 0; i < P; ++i) {
+      const float* o = &h[i * (D + 2)];
+      if (out->d_mean) for (int a = 0; a < 3; ++a) out->d_mean[3 * i + a] = o[a];
+      if (out->d_log_scale) for (int a = 0; a < 3; ++a) out->d_log_scale[3 * i + a] = o[3 + a];
+      if (out->d_quat) for (int a = 0; a < 4; ++a) out->d_quat[4 * i + a] = o[6 + a];
+      if (out->d_opacity_logit) out->d_opacity_logit[i] = o[10];
+      if (out->d_sh) for (int b = 0; b < 3 * K; ++b) out->d_sh[3 * K * i + b] = o[11 + b];
+      if (out->d_mean2d) { out->d_mean2d[2 * i] = o[D]; out->d_mean2d[2 * i + 1] = o[D + 1]; }
+    }
+  }
+  read_state(c);
+  for (int a = 0; a < 6; ++a) out->d_pose[a] = c->ds_host->d_pose[a];
+}
+
+int gsf_render_backward(gsf_ctx c, const gsf_upstream* up, const float* obs, gsf_grads_out* out) {
+  return guard(c, [&] {
+    if (!c->have_render) throw EInval("render_backward: no render on this context");
+    if (c->render_gen != c->map_gen) throw EInval("render_backward: record does not match the primitive list");
+    const int W = c->rK.width, H = c->rK.height;
+    const int64_t npix = static_cast<int64_t>(W) * H;
+    const bool use_c = up && up->d_color, use_ad = up && up->d_alpha_depth, use_md = up && up->d_median_depth,
+               use_op = up && up->d_opacity, use_u = up && up->d_uncertainty && c->rcfg.uncertainty_full_gradient;
+    if (use_u && !obs) throw EInval("render_backward: uncertainty gradient needs observed depth");
+    if (c->P > 0) {
+      GSF_CUDA_CHECK(cudaMemsetAsync(c->grads, 0, sizeof(float) * c->P * c->D, c->stream));
+      GSF_CUDA_CHECK(cudaMemsetAsync(c->d_mean2d, 0, sizeof(float) * c->P * 2, c->stream));
+    }
+    GSF_CUDA_CHECK(cudaMemsetAsync(c->ds->d_pose, 0, sizeof(double) * 6, c->stream));
+    if (!(use_c || use_ad || use_md || use_op || use_u)) {
+      download_grads(c, out);
+      return;
+    }
+    Workspace& ws = c->ws;
+    float* u = ws.upstream;
+    if (use_c) upload_floats(c, u, up->d_color, 3 * npix);
+    if (use_ad) upload_floats(c, u + 3 * npix, up->d_alpha_depth, npix);
+    if (use_md) upload_floats(c, u + 4 * npix, up->d_median_depth, npix);
+    if (use_op) upload_floats(c, u + 5 * npix, up->d_opacity, npix);
+    if (use_u) upload_floats(c, u + 6 * npix, up->d_uncertainty, npix);
+    if (obs) upload_floats(c, ws.obs, obs, npix);
+    BwdArgs b = bwd_args(c, c->rK, c->rcfg, obs ? ws.obs : nullptr, nullptr, make_lp(0, nullptr, c->rcfg), SEED_EXPLICIT, false);
+    b.up_color = use_c ? u : nullptr;
+    b.up_adepth = use_ad ? u + 3 * npix : nullptr;
+    b.up_mdepth = use_md ? u + 4 * npix : nullptr;
+    b.up_opacity = use_op ? u + 5 * npix : nullptr;
+    b.up_uncert = use_u ? u + 6 * npix : nullptr;
+    run_backward(ws, c->ds, b, c->stream, &c->launches);
+    download_grads(c, out);
+  });
+}
+
+static void fill_terms(gsf_ctx_s* c, gsf_loss_terms* out) {
+  const DevState& h = *c->ds_host;
+  *out = gsf_loss_terms{};
+  out->color = h.term_color;
+  out->ssim = h.term_ssim;
+  out->geo = h.term_geo;
+  out->align = h.term_align;
+  out->iso = h.term_iso;
+  out->var = h.term_var;
+  out->total = h.loss_total;
+  out->valid_color = static_cast<int32_t>(h.loss[LS_COLOR_CNT]);
+  out->valid_geo = static_cast<int32_t>(h.loss[LS_GEO_CNT]);
+  out->any_empty_mask = h.any_empty;
+}
+
+int gsf_tracking_loss(gsf_ctx c, const float* target, const float* depth, const gsf_loss_weights* w, gsf_loss_terms* out,
+                      float* d_color, float* d_ad) {
+  return guard(c, [&] {
+    if (!c->have_render) throw EInval("tracking_loss: no render on this context");
+    check_weights(*w);
+    const gsf_intrinsics& k = c->rK;
+    const int64_t npix = static_cast<int64_t>(k.width) * k.height;
+    Workspace& ws = c->ws;
+    float* tgt = ws.upstream;             // reuse: 3 planes rgb
+    float* dep = ws.upstream + 3 * npix;  // 1 plane depth
+    upload_floats(c, tgt, target, 3 * npix);
+    upload_floats(c, dep, depth, npix);
+    const LossParams lp = make_lp(1, w, c->rcfg);
+    const int tiles = ((k.width + kTile - 1) / kTile) * ((k.height + kTile - 1) / kTile);
+    c->ds_host->halt = 0;
+    GSF_CUDA_CHECK(cudaMemsetAsync(&c->ds->halt, 0, sizeof(int32_t), c->stream));
+    run_loss_tiles(ws, 1, tgt, dep, c->render_obs, k.width, k.height, k.near_plane, k.far_plane, lp.opacity_floor, c->stream, &c->launches);
+    run_loss_finalize(ws, c->ds, lp, tiles, npix, -1, c->stream, &c->launches);
+    float* seeds = ws.upstream + 4 * npix;   // 3 planes free (4..6) + use dssim scratch for the rest
+    float* sout = ws.ssim_tmp;
+    run_seeds_out(ws, c->ds, 1, tgt, dep, lp, k.width, k.height, k.near_plane, k.far_plane, sout, c->stream, &c->launches);
+    (void)seeds;
+    read_state(c);
+    fill_terms(c, out);
+    if (d_color) GSF_CUDA_CHECK(cudaMemcpy(d_color, sout, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost));
+    if (d_ad) GSF_CUDA_CHECK(cudaMemcpy(d_ad, sout + 3 * npix, sizeof(float) * npix, cudaMemcpyDeviceToHost));
+  });
+}
+
+static double sum_blocks(gsf_ctx_s* c, const double* dev, int n) {
+  std::vector<double> h(n);
+  GSF_CUDA_CHECK(cudaMemcpy(h.data(), dev, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  double s = 0.0;
+  for (double v : h) s += v;
+  return s;
+}
+
+int gsf_mapping_loss(gsf_ctx c, const float* target, const float* depth, const gsf_loss_weights* w, gsf_loss_terms* out,
+                     float* d_color, float* d_ad, float* d_md, float* d_u, float* d_ls_direct) {
+  return guard(c, [&] {
+    if (!c->have_render) throw EInval("mapping_loss: no render on this context");
+    if (c->render_gen != c->map_gen) throw EInval("mapping_loss: render does not match the primitive list");
+    check_weights(*w);
+    const gsf_intrinsics& k = c->rK;
+    const int64_t npix = static_cast<int64_t>(k.width) * k.height;
+    Workspace& ws = c->ws;
+    // targets live in frame-sized scratch outside the SSIM buffers
+    float* tgt = ws.upstream;
+    float* dep = ws.upstream + 3 * npix;
+    upload_floats(c, tgt, target, 3 * npix);
+    upload_floats(c, dep, depth, npix);
+    const LossParams lp = make_lp(2, w, c->rcfg);
+    const int tiles = ((k.width + kTile - 1) / kTile) * ((k.height + kTile - 1) / kTile);
+    GSF_CUDA_CHECK(cudaMemsetAsync(&c->ds->halt, 0, sizeof(int32_t), c->stream));
+    const int32_t ho = c->render_obs ? 1 : 0;
+    c->ds_host->has_obs = ho;
+    GSF_CUDA_CHECK(cudaMemcpyAsync(&c->ds->has_obs, &c->ds_host->has_obs, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    run_loss_tiles(ws, 2, tgt, dep, c->render_obs, k.width, k.height, k.near_plane, k.far_plane, lp.opacity_floor, c->stream, &c->launches);
+    if (w->w_ssim > 0.0) run_ssim(ws, c->ds, ws.color, tgt, k.width, k.height, 1.0f, ws.dssim, c->stream, &c->launches);
+    run_iso(ws, c->ds, c->params, c->P, w->w_iso, w->iso_epsilon, nullptr, c->stream, &c->launches);
+    run_loss_finalize(ws, c->ds, lp, tiles, npix, -1, c->stream, &c->launches);
+    float* sout = ws.ssim_tmp + 15 * npix;   // 6 planes after the SSIM scratch's first 15 planes
+    run_seeds_out(ws, c->ds, 2, tgt, dep, lp, k.width, k.height, k.near_plane, k.far_plane, sout, c->stream, &c->launches);
+    if (d_ls_direct && c->P > 0) {
+      GSF_CUDA_CHECK(cudaMemsetAsync(c->grads, 0, sizeof(float) * c->P * c->D, c->stream));
+      if (w->w_iso > 0.0) run_iso(ws, c->ds, c->params, c->P, w->w_iso, w->iso_epsilon, c->grads, c->stream, &c->launches);
+    }
+    read_state(c);
+    fill_terms(c, out);
+    const bool have_c = w->w_color > 0.0 || w->w_ssim > 0.0;
+    if (d_color) {
+      if (have_c) GSF_CUDA_CHECK(cudaMemcpy(d_color, sout, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost));
+      else std::memset(d_color, 0, sizeof(float) * 3 * npix);
+    }
+    if (d_ad) GSF_CUDA_CHECK(cudaMemcpy(d_ad, sout + 3 * npix, sizeof(float) * npix, cudaMemcpyDeviceToHost));
+    if (d_md) GSF_CUDA_CHECK(cudaMemcpy(d_md, sout + 4 * npix, sizeof(float) * npix, cudaMemcpyDeviceToHost));
+    if (d_u) GSF_CUDA_CHECK(cudaMemcpy(d_u, sout + 5 * npix, sizeof(float) * npix, cudaMemcpyDeviceToHost));
+    if (d_ls_direct) {
+      const int64_t P = c->P;
+      std::vector<float> g(static_cast<size_t>(3) * P);
+      if (P > 0 && w->w_iso > 0.0 && c->ds_host->V > 0)
+        for (int a = 0; a < 3; ++a)
+          GSF_CUDA_CHECK(cudaMemcpy(g.data() + a * P, c->grads + (3 + a) * P, sizeof(float) * P, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < P; ++i)
+        for (int a = 0; a < 3; ++a) d_ls_direct[3 * i + a] = g[a * P + i];
+    }
+  });
+}
+
+int gsf_ssim(gsf_ctx c, const float* x, const float* y, int32_t w, int32_t h, double* value, float* d_x) {
+  return guard(c, [&] {
+    if (w <= 0 || h <= 0) throw EInval("ssim: empty image");
+    const int64_t npix = static_cast<int64_t>(w) * h;
+    ensure_ws(c, w, h);
+    Workspace& ws = c->ws;
+    upload_floats(c, ws.color, x, 3 * npix);
+    upload_floats(c, ws.upstream, y, 3 * npix);
+    run_ssim(ws, c->ds, ws.color, ws.upstream, w, h, 1.0f, d_x ? ws.dssim : nullptr, c->stream, &c->launches);
+    sync(c);
+    const double s = sum_blocks(c, ws.red_part, ws.ssim_blocks);
+    *value = s / (3.0 * static_cast<double>(npix));
+    if (d_x) GSF_CUDA_CHECK(cudaMemcpy(d_x, ws.dssim, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gsf_frame_upload(gsf_ctx c, int32_t slot, const float* rgb, const float* depth, int32_t w, int32_t h) {
+  return guard(c, [&] {
+    if (slot < 0 || slot > 4096) throw EInval("frame slot out of range");
+    if (w <= 0 || h <= 0) throw EInval("frame dimensions must be positive");
+    if (static_cast<int>(c->frames.size()) <= slot) c->frames.resize(slot + 1);
+    Frame& f = c->frames[slot];
+    const int64_t npix = static_cast<int64_t>(w) * h;
+    if (f.w * f.h != npix || !f.rgb) {
+      dfree(f.rgb);
+      dfree(f.depth);
+      dalloc(f.rgb, 3 * npix);
+      dalloc(f.depth, npix);
+    }
+    f.w = w;
+    f.h = h;
+    upload_floats(c, f.rgb, rgb, 3 * npix);
+    upload_floats(c, f.depth, depth, npix);
+  });
+}
+
+// ------------------------------------------------------------------------------------------------
+// track_frame (tracker.cpp:30-84)
+// ------------------------------------------------------------------------------------------------
+static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k, const gsf_tracker_cfg& tcfg,
+                          const gsf_loss_weights& w, const gsf_raster_cfg& rcfg) {
+  const LossParams lp = make_lp(1, &w, rcfg);
+  const int tiles = ((k.width + kTile - 1) / kTile) * ((k.height + kTile - 1) / kTile);
+  const int64_t npix = static_cast<int64_t>(k.width) * k.height;
+  for (int it = 0; it < tcfg.iterations; ++it) {
+    run_forward(c->ws, c->ds, fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it), c->stream, &c->launches);
+    run_loss_finalize(c->ws, c->ds, lp, tiles, npix, it, c->stream, &c->launches);
+    BwdArgs b = bwd_args(c, k, rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);
+    run_backward(c->ws, c->ds, b, c->stream, &c->launches);
+    run_track_update(c->ds, it, c->stream, &c->launches);
+  }
+  // final render + loss without gradients (tracker.cpp:74-76)
+  run_forward(c->ws, c->ds, fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, -1), c->stream, &c->launches);
+  run_loss_finalize(c->ws, c->ds, lp, tiles, npix, -1, c->stream, &c->launches);
+}
+
+int gsf_track_frame(gsf_ctx c, int32_t slot, const gsf_pose* initial, const gsf_intrinsics* K, const gsf_tracker_cfg* tcfg,
+                    const gsf_loss_weights* w, const gsf_raster_cfg* rcfg, gsf_track_result* out) {
+  return guard(c, [&] {
+    check_intrinsics(*K);
+    check_raster(*rcfg);
+    check_weights(*w);
+    const Frame& f = get_frame(c, slot, *K);
+    ensure_ws(c, K->width, K->height);
+    const Cam cam = host_cam(*initial, *K);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      reset_state(c, &cam);
+      DevState& h = *c->ds_host;
+      for (int a = 0; a < 3; ++a) { h.pose_rot[a] = initial->rotation_tangent[a]; h.pose_trans[a] = initial->translation[a]; }
+      h.lr_rot = tcfg->lr_rotation;
+      h.lr_trans = tcfg->lr_translation;
+      h.degraded_ratio = tcfg->degraded_loss_ratio;
+      GSF_CUDA_CHECK(cudaMemcpyAsync(c->ds, &h, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+      enqueue_track(c, f, *K, *tcfg, *w, *rcfg);
+      read_state(c);
+      if (!h.overflow) break;
+      grow_pairs(c, h.M);
+    }
+    const DevState& h = *c->ds_host;
+    if (h.bad_index != std::numeric_limits<int32_t>::max()) throw_nonfinite(h.bad_index);
+    *out = gsf_track_result{};
+    out->initial_loss = h.initial_loss;
+    if (h.halt == 1) {   // nothing to track at iteration 0: keep the prediction (tracker.cpp:46-53)
+      out->pose = *initial;
+      out->degraded = 1;
+      out->final_loss = h.final_loss;
+      out->iterations_run = 0;
+      return;
+    }
+    if (h.halt == 2) {
+      std::ostringstream m;
+      m << "tracking diverged at iteration " << h.halt_iter << ": total=" << h.loss_total << " color=" << h.term_color
+        << " geo=" << h.term_geo;
+      throw EDiverged(m.str());
+    }
+    for (int a = 0; a < 3; ++a) {
+      out->pose.rotation_tangent[a] = h.pose_rot[a];
+      out->pose.translation[a] = h.pose_trans[a];
+    }
+    out->final_loss = h.loss_total;
+    out->iterations_run = tcfg->iterations;
+    if (tcfg->iterations == 0)
+      out->degraded = (h.loss[LS_COLOR_CNT] == 0.0 && h.loss[LS_GEO_CNT] == 0.0) ? 1 : 0;
+    else if (h.loss_total > tcfg->degraded_loss_ratio * h.initial_loss)
+      out->degraded = 1;
+  });
+}
+
+int gsf_track_frame_host(gsf_ctx c, const float* rgb, const float* depth, const gsf_pose* initial, const gsf_intrinsics* K,
+                         const gsf_tracker_cfg* tcfg, const gsf_loss_weights* w, const gsf_raster_cfg* rcfg,
+                         gsf_track_result* out) {
+  const int rc = gsf_frame_upload(c, 0, rgb, depth, K->width, K->height);
+  if (rc != GSF_OK) return rc;
+  return gsf_track_frame(c, 0, initial, K, tcfg, w, rcfg, out);
+}
+
+// ------------------------------------------------------------------------------------------------
+// map_step (mapper.cpp:232-281) and sliding_ba (tracker.cpp:119-183)
+// ------------------------------------------------------------------------------------------------
+static AdamGroups groups_of(const gsf_mapper_cfg& m) {
+  AdamGroups g;
+  g.lr[0] = m.lr_mean * m.scene_extent;
+  g.lr[1] = m.lr_scale;
+  g.lr[2] = m.lr_rotation;
+  g.lr[3] = m.lr_opacity;
+  g.lr[4] = m.lr_sh;
+  return g;
+}
+
+// One mapping-objective forward/backward of keyframe k into c->grads (accumulating).
+static void enqueue_map_view(gsf_ctx_s* c, const Frame& f, int k, const gsf_intrinsics& K, const gsf_mapper_cfg& m, int it,
+                             double* loss_acc, int trace_index) {
+  const LossParams lp = make_lp(2, &m.weights, m.raster);
+  const int tiles = ((K.width + kTile - 1) / kTile) * ((K.height + kTile - 1) / kTile);
+  const int64_t npix = static_cast<int64_t>(K.width) * K.height;
+  k_set_cam_from_kf<<<1, 1, 0, c->stream>>>(c->ds, c->kf, k, 1);
+  ++c->launches;
+  run_forward(c->ws, c->ds, fwd_args(c, K, m.raster, f.depth, f.rgb, f.depth, lp, it), c->stream, &c->launches);
+  if (m.weights.w_ssim > 0.0) run_ssim(c->ws, c->ds, c->ws.color, f.rgb, K.width, K.height, 1.0f, c->ws.dssim, c->stream, &c->launches);
+  run_iso(c->ws, c->ds, c->params, c->P, m.weights.w_iso, m.weights.iso_epsilon, nullptr, c->stream, &c->launches);
+  run_loss_finalize(c->ws, c->ds, lp, tiles, npix, it, c->stream, &c->launches);
+  BwdArgs b = bwd_args(c, K, m.raster, f.depth, f.rgb, lp, SEED_MAP, false);
+  run_backward(c->ws, c->ds, b, c->stream, &c->launches);
+  if (m.weights.w_iso > 0.0)
+    run_iso(c->ws, c->ds, c->params, c->P, m.weights.w_iso, m.weights.iso_epsilon, c->grads, c->stream, &c->launches);
+  k_kf_grab<<<1, 1, 0, c->stream>>>(c->ds, c->kf, k, loss_acc, c->trace_dev, trace_index, trace_index >= 0 ? 1 : 0);
+  ++c->launches;
+}
+
+static void upload_kf(gsf_ctx_s* c, const gsf_pose* poses, int n) {
+  ensure_kf(c, n);
+  for (int i = 0; i < n; ++i) {
+    KfPose& p = c->kf_host[i];
+    std::memset(&p, 0, sizeof(KfPose));
+    for (int a = 0; a < 3; ++a) { p.rot[a] = poses[i].rotation_tangent[a]; p.trans[a] = poses[i].translation[a]; }
+  }
+  GSF_CUDA_CHECK(cudaMemcpyAsync(c->kf, c->kf_host, sizeof(KfPose) * n, cudaMemcpyHostToDevice, c->stream));
+}
+
+int gsf_map_step(gsf_ctx c, const int32_t* slots, const gsf_pose* poses, int32_t n, const gsf_intrinsics* K,
+                 const gsf_mapper_cfg* m, int32_t iterations, double* trace) {
+  return guard(c, [&] {
+    if (n <= 0) throw EInval("mapping window is empty");
+    check_intrinsics(*K);
+    check_raster(m->raster);
+    check_weights(m->weights);
+    std::vector<const Frame*> fr(n);
+    for (int i = 0; i < n; ++i) {
+      if (slots[i] < 0 || slots[i] >= static_cast<int>(c->frames.size()) || !c->frames[slots[i]].rgb)
+        throw EInval("mapping window observation missing rgb or depth");
+      fr[i] = &get_frame(c, slots[i], *K);
+    }
+    if (iterations <= 0) return;
+    if (m->densify_interval > 0) {
+      const int64_t first = (c->map_iteration / m->densify_interval + 1) * m->densify_interval;
+      if (first <= c->map_iteration + iterations)
+        throw EUnsupported("map_step: densify_and_cull would run at mapping iteration " + std::to_string(first) +
+                           "; structural map edits are not implemented on the device path");
+    }
+    ensure_ws(c, K->width, K->height);
+    ensure_trace(c, iterations);
+    const Cam cam = host_cam(poses[0], *K);
+    reset_state(c, &cam);
+    upload_kf(c, poses, n);
+    const AdamGroups g = groups_of(*m);
+    for (int it = 0; it < iterations; ++it) {
+      const int o = it % n;
+      if (c->P > 0) {
+        GSF_CUDA_CHECK(cudaMemsetAsync(c->grads, 0, sizeof(float) * c->P * c->D, c->stream));
+        GSF_CUDA_CHECK(cudaMemsetAsync(c->d_mean2d, 0, sizeof(float) * c->P * 2, c->stream));
+      }
+      enqueue_map_view(c, *fr[o], o, *K, *m, static_cast<int>(c->map_iteration) + it, nullptr, it);
+      run_densify_stats(c->ws.visible, c->d_mean2d, c->grad_accum, c->grad_count, c->P, K->width, K->height, c->stream, &c->launches);
+      c->adam_step += 1.0;
+      run_adam(c->params, c->grads, c->adam_m, c->adam_v, c->P, c->D, g, c->adam_step, c->stream, &c->launches);
+    }
+    read_state(c);
+    const DevState& h = *c->ds_host;
+    if (h.bad_index != std::numeric_limits<int32_t>::max()) throw_nonfinite(h.bad_index);
+    if (h.overflow) throw EUnsupported("map_step: pair capacity exceeded; rerun after a render at these poses");
+    if (h.halt == 2) {
+      std::ostringstream msg;
+      msg << "mapping diverged at iteration " << h.halt_iter << ": total=" << h.loss_total << " color=" << h.term_color
+          << " ssim=" << h.term_ssim << " geo=" << h.term_geo << " align=" << h.term_align << " iso=" << h.term_iso
+          << " var=" << h.term_var;
+      throw EDiverged(msg.str());
+    }
+    if (trace) GSF_CUDA_CHECK(cudaMemcpy(trace, c->trace_dev, sizeof(double) * iterations, cudaMemcpyDeviceToHost));
+    c->map_iteration += iterations;
+  });
+}
+
+int gsf_ba_partition(int32_t n, int32_t nranks, int32_t rank, uint8_t* owned) {
+  if (n < 0 || nranks <= 0 || rank < 0 || rank >= nranks || (!owned && n > 0)) return GSF_EINVAL;
+  for (int k = 0; k < n; ++k) owned[k] = (k % nranks == rank) ? 1 : 0;
+  return GSF_OK;
+}
+
+int gsf_comm_unique_id(uint8_t id[128]) {
+  if (!g_nccl.load()) return GSF_ECUDA;
+  return g_nccl.get_unique_id(id) == 0 ? GSF_OK : GSF_ECUDA;
+}
+
+int gsf_comm_init(gsf_ctx c, int32_t nranks, int32_t rank, const uint8_t id[128]) {
+  return guard(c, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw EInval("comm_init: bad rank/size");
+    c->nranks = nranks;
+    c->rank = rank;
+    if (nranks == 1) return;
+    if (!g_nccl.load()) throw EUnsupported("NCCL (libnccl.so.2) could not be loaded");
+    auto init = reinterpret_cast<nccl_init_fn>(dlsym(g_nccl.h, "ncclCommInitRank"));
+    if (!init) throw EUnsupported("ncclCommInitRank missing");
+    NcclUid uid;
+    std::memcpy(uid.b, id, 128);
+    const int r = init(&c->comm, nranks, uid, rank);
+    if (r != 0) throw EUnsupported(std::string("ncclCommInitRank failed: ") + (g_nccl.get_error ? g_nccl.get_error(r) : "?"));
+  });
+}
+
+static double* kf_grad(gsf_ctx_s* c, int k) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(c->kf + k) + offsetof(KfPose, grad));
+}
+
+static void allreduce(gsf_ctx_s* c, void* buf, size_t count, int dtype /*7 f32, 8 f64*/) {
+  if (c->nranks <= 1) return;
+  const int r = g_nccl.all_reduce(buf, buf, count, dtype, 0 /*sum*/, c->comm, c->stream);
+  if (r != 0) throw EUnsupported(std::string("ncclAllReduce failed: ") + (g_nccl.get_error ? g_nccl.get_error(r) : "?"));
+}
+
+int gsf_sliding_ba(gsf_ctx c, const int32_t* slots, gsf_pose* poses, const int32_t* frame_ids, int32_t n,
+                   const gsf_intrinsics* K, const gsf_tracker_cfg* tcfg, const gsf_mapper_cfg* m, int32_t iterations,
+                   double* trace) {
+  return guard(c, [&] {
+    if (n <= 0) throw EInval("adjustment window is empty");
+    check_intrinsics(*K);
+    check_raster(m->raster);
+    check_weights(m->weights);
+    std::vector<const Frame*> fr(n, nullptr);
+    std::vector<uint8_t> owned(n);
+    gsf_ba_partition(n, c->nranks, c->rank, owned.data());
+    for (int i = 0; i < n; ++i) {
+      if (!owned[i]) continue;
+      if (slots[i] < 0 || slots[i] >= static_cast<int>(c->frames.size()) || !c->frames[slots[i]].rgb)
+        throw EInval("adjustment window holds a null keyframe");
+      fr[i] = &get_frame(c, slots[i], *K);
+    }
+    int anchor = -1;
+    if (tcfg->freeze_oldest_pose) {
+      anchor = 0;
+      for (int i = 1; i < n; ++i)
+        if (frame_ids[i] < frame_ids[anchor]) anchor = i;
+    }
+    ensure_ws(c, K->width, K->height);
+    ensure_trace(c, std::max(iterations, 1) + 2);
+    const Cam cam = host_cam(poses[0], *K);
+    reset_state(c, &cam);
+    upload_kf(c, poses, n);
+    const AdamGroups g = groups_of(*m);
+    double* loss_acc = c->trace_dev + std::max(iterations, 1);  // scratch slot after the trace
+    for (int it = 0; it < iterations; ++it) {
+      if (c->P > 0) {
+        GSF_CUDA_CHECK(cudaMemsetAsync(c->grads, 0, sizeof(float) * c->P * c->D, c->stream));
+        GSF_CUDA_CHECK(cudaMemsetAsync(c->d_mean2d, 0, sizeof(float) * c->P * 2, c->stream));
+      }
+      GSF_CUDA_CHECK(cudaMemsetAsync(loss_acc, 0, sizeof(double), c->stream));
+      for (int k = 0; k < n; ++k) {
+        if (!owned[k]) {
+          GSF_CUDA_CHECK(cudaMemsetAsync(kf_grad(c, k), 0, sizeof(double) * 6, c->stream));
+          continue;
+        }
+        enqueue_map_view(c, *fr[k], k, *K, *m, it, loss_acc, -1);
+      }
+      if (c->nranks > 1) {
+        allreduce(c, c->grads, static_cast<size_t>(c->P) * c->D, 7);
+        allreduce(c, loss_acc, 1, 8);
+        for (int k = 0; k < n; ++k) allreduce(c, kf_grad(c, k), 6, 8);
+      }
+      k_store<<<1, 1, 0, c->stream>>>(loss_acc, c->trace_dev + it);
+      ++c->launches;
+      c->adam_step += 1.0;
+      run_adam(c->params, c->grads, c->adam_m, c->adam_v, c->P, c->D, g, c->adam_step, c->stream, &c->launches);
+      k_kf_update<<<1, 32 * div_up(n, 32), 0, c->stream>>>(c->ds, c->kf, n, anchor, tcfg->lr_rotation, tcfg->lr_translation);
+      ++c->launches;
+    }
+    read_state(c);
+    const DevState& h = *c->ds_host;
+    if (h.bad_index != std::numeric_limits<int32_t>::max()) throw_nonfinite(h.bad_index);
+    if (h.overflow) throw EUnsupported("sliding_ba: pair capacity exceeded; rerun after a render at these poses");
+    if (h.halt == 2) {
+      std::ostringstream msg;
+      msg << "bundle adjustment diverged at iteration " << h.halt_iter << ": total=" << h.loss_total;
+      throw EDiverged(msg.str());
+    }
+    GSF_CUDA_CHECK(cudaMemcpy(c->kf_host, c->kf, sizeof(KfPose) * n, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < n; ++k)
+      for (int a = 0; a < 3; ++a) {
+        poses[k].rotation_tangent[a] = c->kf_host[k].rot[a];
+        poses[k].translation[a] = c->kf_host[k].trans[a];
+      }
+    if (trace && iterations > 0) GSF_CUDA_CHECK(cudaMemcpy(trace, c->trace_dev, sizeof(double) * iterations, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gsf_accumulate_uncertainty(gsf_ctx c, const int32_t* slots, const gsf_pose* poses, int32_t n, const gsf_intrinsics* K,
+                               const gsf_raster_cfg* rcfg, int32_t* observed_count) {
+  return guard(c, [&] {
+    *observed_count = 0;
+    if (n == 0) return;
+    check_intrinsics(*K);
+    check_raster(*rcfg);
+    std::vector<const Frame*> fr(n);
+    for (int i = 0; i < n; ++i) {
+      if (slots[i] < 0 || slots[i] >= static_cast<int>(c->frames.size()) || !c->frames[slots[i]].rgb)
+        throw EInval("uncertainty view missing record or depth");
+      fr[i] = &c->frames[slots[i]];
+      if (fr[i]->w != K->width || fr[i]->h != K->height) throw EInval("uncertainty view depth dimensions mismatch");
+    }
+    ensure_ws(c, K->width, K->height);
+    if (c->P > c->unc_cap) {
+      dalloc(c->unc_sum, c->P);
+      dalloc(c->unc_cnt, c->P);
+      c->unc_cap = c->P;
+    }
+    const int64_t P = c->P;
+    if (P == 0) return;
+    GSF_CUDA_CHECK(cudaMemsetAsync(c->unc_sum, 0, sizeof(double) * P, c->stream));
+    GSF_CUDA_CHECK(cudaMemsetAsync(c->unc_cnt, 0, sizeof(uint32_t) * P, c->stream));
+    for (int v = 0; v < n; ++v) {
+      render_sync(c, poses[v], *K, *rcfg, fr[v]->depth);
+      run_uncertainty_view(c->ws, c->params, P, fr[v]->depth, K->width, K->height, K->near_plane, K->far_plane, c->ds,
+                           c->unc_sum, c->unc_cnt, c->stream, &c->launches);
+    }
+    GSF_CUDA_CHECK(cudaMemsetAsync(c->counters, 0, sizeof(uint32_t) * 16, c->stream));
+    run_uncertainty_finalize(c->unc_sum, c->unc_cnt, c->nu, c->observed, P, c->counters, c->stream, &c->launches);
+    uint32_t cnt = 0;
+    GSF_CUDA_CHECK(cudaMemcpyAsync(&cnt, c->counters, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    *observed_count = static_cast<int32_t>(cnt);
+  });
+}
+
+int gsf_prune_unreliable(gsf_ctx c, double tau, double reduced_opacity, int32_t* reduced) {
+  return guard(c, [&] {
+    if (!(tau > 0.0)) throw EInval("uncertainty threshold must be positive");
+    if (!(reduced_opacity > 0.0 && reduced_opacity < 0.1)) throw EInval("reduced opacity must lie in (0, 0.1)");
+    *reduced = 0;
+    if (c->P == 0) return;
+    if (!c->counters) dalloc(c->counters, 16);
+    const float target = static_cast<float>(std::log(reduced_opacity / (1.0 - reduced_opacity)));
+    GSF_CUDA_CHECK(cudaMemsetAsync(c->counters, 0, sizeof(uint32_t) * 16, c->stream));
+    run_prune(c->nu, c->params + 10 * c->P, c->P, static_cast<float>(tau), target, c->counters, c->stream, &c->launches);
+    uint32_t cnt = 0;
+    GSF_CUDA_CHECK(cudaMemcpyAsync(&cnt, c->counters, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    *reduced = static_cast<int32_t>(cnt);
+    ++c->map_gen;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,536 @@
+// gsf_shared.cuh — the decision-path arithmetic shared by the sm_100a kernels and the CPU
+// mirror (oracle/mirror.cpp).  Everything here is __host__ __device__ and written with
+// explicitly-rounded operations, so the device (which would otherwise contract a*b+c into
+// FFMA) and the host (compiled with -ffp-contract=off) produce identical bits.  That is what
+// makes tile keys, depth order, tile ranges, per-pixel contributor counts and ids bit-exact
+// between the GPU and the mirror.
+//
+// Reference semantics restated here:
+//   project_gaussian      projection.cpp:54-104 (+ axis_bounds :40-50, jacobian :26-33)
+//   project_all           rasterizer.cpp:46-67 (support radius, sigmoid, SH colour)
+//   eval_sh_color         sh.cpp:79-86, bases :21-42
+//   tile rectangle        rasterizer.cpp:199-208
+//   blend_pixel           rasterizer.cpp:96-140
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+#if !defined(__CUDACC__)
+#include <cmath>
+#endif
+
+#if defined(__CUDACC__)
+#define GSF_HD __host__ __device__ __forceinline__
+#else
+#define GSF_HD inline
+#endif
+
+namespace gsfk {
+
+// ---------------------------------------------------------------------------------------
+// Explicitly rounded arithmetic.
+// ---------------------------------------------------------------------------------------
+#if defined(__CUDA_ARCH__)
+GSF_HD float fmul(float a, float b) { return __fmul_rn(a, b); }
+GSF_HD float fadd(float a, float b) { return __fadd_rn(a, b); }
+GSF_HD float fsub(float a, float b) { return __fsub_rn(a, b); }
+GSF_HD float ffma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+GSF_HD double dmul(double a, double b) { return __dmul_rn(a, b); }
+GSF_HD double dadd(double a, double b) { return __dadd_rn(a, b); }
+GSF_HD double dsub(double a, double b) { return __dsub_rn(a, b); }
+GSF_HD double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+GSF_HD double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+GSF_HD double dsqrt(double a) { return __dsqrt_rn(a); }
+GSF_HD double drint(double a) { return rint(a); }
+GSF_HD float frint(float a) { return rintf(a); }
+GSF_HD int64_t dbits(double a) { return __double_as_longlong(a); }
+GSF_HD double bitsd(int64_t a) { return __longlong_as_double(a); }
+GSF_HD int32_t fbits(float a) { return __float_as_int(a); }
+GSF_HD float bitsf(int32_t a) { return __int_as_float(a); }
+#else
+GSF_HD float fmul(float a, float b) { return a * b; }
+GSF_HD float fadd(float a, float b) { return a + b; }
+GSF_HD float fsub(float a, float b) { return a - b; }
+GSF_HD float ffma(float a, float b, float c) { return fmaf(a, b, c); }
+GSF_HD double dmul(double a, double b) { return a * b; }
+GSF_HD double dadd(double a, double b) { return a + b; }
+GSF_HD double dsub(double a, double b) { return a - b; }
+GSF_HD double ddiv(double a, double b) { return a / b; }
+GSF_HD double dfma(double a, double b, double c) { return fma(a, b, c); }
+GSF_HD double dsqrt(double a) { return sqrt(a); }
+GSF_HD double drint(double a) { return rint(a); }
+GSF_HD float frint(float a) { return rintf(a); }
+GSF_HD int64_t dbits(double a) { int64_t r; memcpy(&r, &a, 8); return r; }
+GSF_HD double bitsd(int64_t a) { double r; memcpy(&r, &a, 8); return r; }
+GSF_HD int32_t fbits(float a) { int32_t r; memcpy(&r, &a, 4); return r; }
+GSF_HD float bitsf(int32_t a) { float r; memcpy(&r, &a, 4); return r; }
+#endif
+
+#if defined(__CUDA_ARCH__)
+GSF_HD bool disfinite(double a) { return isfinite(a); }
+#else
+GSF_HD bool disfinite(double a) { return std::isfinite(a); }
+#endif
+GSF_HD double dinf() { return bitsd(0x7ff0000000000000LL); }
+GSF_HD float finf() { return bitsf(0x7f800000); }
+
+GSF_HD double dmax(double a, double b) { return a > b ? a : b; }
+GSF_HD double dmin(double a, double b) { return a < b ? a : b; }
+GSF_HD float fminf_(float a, float b) { return a < b ? a : b; }
+
+// Deterministic exp (fp64): Cody-Waite reduction by ln2 then a degree-13 Taylor polynomial
+// on |r| <= 0.35, all in fused multiply-adds.  < 1 ulp from glibc on the ranges used here.
+GSF_HD double exp_d(double x) {
+  if (!(x == x)) return x;
+  if (x > 709.78) return dinf();
+  if (x < -745.2) return 0.0;
+  const double n = drint(dmul(x, 1.4426950408889634));
+  double r = dfma(n, -6.93147180369123816490e-01, x);
+  r = dfma(n, -1.90821492927058770002e-10, r);
+  double p = 1.0 / 6227020800.0;  // 1/13!
+  p = dfma(p, r, 1.0 / 479001600.0);
+  p = dfma(p, r, 1.0 / 39916800.0);
+  p = dfma(p, r, 1.0 / 3628800.0);
+  p = dfma(p, r, 1.0 / 362880.0);
+  p = dfma(p, r, 1.0 / 40320.0);
+  p = dfma(p, r, 1.0 / 5040.0);
+  p = dfma(p, r, 1.0 / 720.0);
+  p = dfma(p, r, 1.0 / 120.0);
+  p = dfma(p, r, 1.0 / 24.0);
+  p = dfma(p, r, 1.0 / 6.0);
+  p = dfma(p, r, 0.5);
+  p = dfma(p, r, 1.0);
+  p = dfma(p, r, 1.0);
+  int ni = static_cast<int>(n);
+  // scale by 2^n in two steps so subnormal results stay exact enough
+  if (ni < -1000) {
+    p = dmul(p, bitsd(static_cast<int64_t>(1023 - 1000) << 52));
+    ni += 1000;
+  }
+  if (ni > 1000) {
+    p = dmul(p, bitsd(static_cast<int64_t>(1023 + 1000) << 52));
+    ni -= 1000;
+  }
+  return dmul(p, bitsd(static_cast<int64_t>(1023 + ni) << 52));
+}
+
+// Deterministic exp (fp32) for the blend: reduction by ln2, degree-6 polynomial.
+// Inputs are -rho/2 in [-0.5*cutoff, 0]; values below -87 flush to zero.
+GSF_HD float exp_f(float x) {
+  if (x < -87.0f) return 0.0f;
+  if (x > 88.0f) return finf();
+  const float n = frint(fmul(x, 1.44269504f));
+  float r = ffma(n, -0.693145752f, x);
+  r = ffma(n, -1.42860677e-06f, r);
+  float p = 1.0f / 5040.0f;
+  p = ffma(p, r, 1.0f / 720.0f);
+  p = ffma(p, r, 1.0f / 120.0f);
+  p = ffma(p, r, 1.0f / 24.0f);
+  p = ffma(p, r, 1.0f / 6.0f);
+  p = ffma(p, r, 0.5f);
+  p = ffma(p, r, 1.0f);
+  p = ffma(p, r, 1.0f);
+  const int ni = static_cast<int>(n);
+  return fmul(p, bitsf((127 + ni) << 23));
+}
+
+// ---------------------------------------------------------------------------------------
+// Camera (fp64).  W is row-major world->camera rotation exp(rotation_tangent).
+// ---------------------------------------------------------------------------------------
+struct Cam {
+  double W[9];
+  double t[3];
+  double center[3];   // -W^T t
+  double fx, fy, cx, cy;
+  double near_plane, far_plane;
+  int32_t width, height;
+};
+
+struct RasterParams {
+  double footprint_sigma, dilation, alpha_clamp, alpha_skip, termination;
+  int32_t tile;        // 16
+  int32_t tiles_x, tiles_y;
+  int32_t sh_coeffs;
+};
+
+// ---------------------------------------------------------------------------------------
+// Preprocess of one primitive (fp64): project_all + project_gaussian + tile rectangle.
+// ---------------------------------------------------------------------------------------
+struct PreOut {
+  int visible;
+  double depth;
+  double mx, my;
+  double c00, c01, c11;   // conic (inverse screen covariance); conic(1,0) == conic(0,1)
+  double radius;
+  double sigma;
+  double color[3];
+  int32_t tx0, tx1, ty0, ty1;
+};
+
+GSF_HD void axis_bounds_d(double a, double z, double r, double f, double c, double& lo, double& hi) {
+  // projection.cpp:40-50: extremes over the corners of [a-r, a+r] x [z-r, z+r]
+  lo = dinf();
+  hi = -lo;
+  for (int i = 0; i < 2; ++i) {
+    const double da = i == 0 ? -r : r;
+    for (int j = 0; j < 2; ++j) {
+      const double dz = j == 0 ? -r : r;
+      const double u = dadd(c, ddiv(dmul(f, dadd(a, da)), dadd(z, dz)));
+      lo = dmin(lo, u);
+      hi = dmax(hi, u);
+    }
+  }
+}
+
+GSF_HD int tile_clamp(double v, int hi) {
+  const double f = floor(v);
+  if (f < 0.0) return 0;
+  if (f > static_cast<double>(hi)) return hi;
+  return static_cast<int>(f);
+}
+
+// SH bases, degree <= 3 (sh.cpp:21-42).
+GSF_HD void sh_basis(int degree, double x, double y, double z, double* b) {
+  const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+  b[0] = C0;
+  if (degree < 1) return;
+  b[1] = dmul(-C1, y);
+  b[2] = dmul(C1, z);
+  b[3] = dmul(-C1, x);
+  if (degree < 2) return;
+  const double xx = dmul(x, x), yy = dmul(y, y), zz = dmul(z, z);
+  b[4] = dmul(dmul(1.0925484305920792, x), y);
+  b[5] = dmul(dmul(-1.0925484305920792, y), z);
+  b[6] = dmul(0.31539156525252005, dsub(dsub(dmul(2.0, zz), xx), yy));
+  b[7] = dmul(dmul(-1.0925484305920792, x), z);
+  b[8] = dmul(0.5462742152960396, dsub(xx, yy));
+  if (degree < 3) return;
+  b[9] = dmul(dmul(-0.5900435899266435, y), dsub(dmul(3.0, xx), yy));
+  b[10] = dmul(dmul(dmul(2.890611442640554, x), y), z);
+  b[11] = dmul(dmul(-0.4570457994644658, y), dsub(dsub(dmul(4.0, zz), xx), yy));
+  b[12] = dmul(dmul(0.3731763325901154, z), dsub(dsub(dmul(2.0, zz), dmul(3.0, xx)), dmul(3.0, yy)));
+  b[13] = dmul(dmul(-0.4570457994644658, x), dsub(dsub(dmul(4.0, zz), xx), yy));
+  b[14] = dmul(dmul(1.445305721320277, z), dsub(xx, yy));
+  b[15] = dmul(dmul(-0.5900435899266435, x), dsub(xx, dmul(3.0, yy)));
+}
+
+GSF_HD int sh_degree(int K) { return K >= 16 ? 3 : (K >= 9 ? 2 : (K >= 4 ? 1 : 0)); }
+
+// One primitive.  p = pointer to field 0 of this primitive in a SoA [field][stride] fp32
+// block (mean 0-2, log_scale 3-5, quat 6-9, opacity_logit 10, sh 11+3b+c).
+GSF_HD PreOut preprocess_one(const float* p, int64_t stride, const Cam& cam, const RasterParams& rp) {
+  PreOut o;
+  o.visible = 0;
+  o.depth = 0.0;
+  o.mx = o.my = o.c00 = o.c01 = o.c11 = o.radius = o.sigma = 0.0;
+  o.color[0] = o.color[1] = o.color[2] = 0.0;
+  o.tx0 = o.tx1 = o.ty0 = o.ty1 = 0;
+  const double m0 = p[0 * stride], m1 = p[1 * stride], m2 = p[2 * stride];
+  const double l0 = p[3 * stride], l1 = p[4 * stride], l2 = p[5 * stride];
+  const double qw = p[6 * stride], qx = p[7 * stride], qy = p[8 * stride], qz = p[9 * stride];
+  const double* W = cam.W;
+  // p_cam = W * mean + t
+  const double pc0 = dadd(dadd(dadd(dmul(W[0], m0), dmul(W[1], m1)), dmul(W[2], m2)), cam.t[0]);
+  const double pc1 = dadd(dadd(dadd(dmul(W[3], m0), dmul(W[4], m1)), dmul(W[5], m2)), cam.t[1]);
+  const double pc2 = dadd(dadd(dadd(dmul(W[6], m0), dmul(W[7], m1)), dmul(W[8], m2)), cam.t[2]);
+  o.depth = pc2;
+  if (!(pc2 > cam.near_plane) || !(pc2 < cam.far_plane)) return o;
+  // support = footprint_sigma * exp(max log_scale)  (rasterizer.cpp:55)
+  const double lmax = dmax(dmax(l0, l1), l2);
+  const double support = dmul(rp.footprint_sigma, exp_d(lmax));
+  if (support > 0.0) {
+    if (!(dsub(pc2, support) > 0.0)) return o;
+    const double pad = dmul(rp.footprint_sigma, dsqrt(dmax(0.0, rp.dilation)));
+    double u_lo, u_hi, v_lo, v_hi;
+    axis_bounds_d(pc0, pc2, support, cam.fx, cam.cx, u_lo, u_hi);
+    axis_bounds_d(pc1, pc2, support, cam.fy, cam.cy, v_lo, v_hi);
+    if (dadd(u_hi, pad) < 0.0 || dsub(u_lo, pad) > static_cast<double>(cam.width) ||
+        dadd(v_hi, pad) < 0.0 || dsub(v_lo, pad) > static_cast<double>(cam.height))
+      return o;
+  }
+  o.mx = dadd(ddiv(dmul(cam.fx, pc0), pc2), cam.cx);
+  o.my = dadd(ddiv(dmul(cam.fy, pc1), pc2), cam.cy);
+  // world covariance R diag(exp(2 ls)) R^T (primitive.hpp:46-50)
+  const double qn = dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz)));
+  const double w = ddiv(qw, qn), x = ddiv(qx, qn), y = ddiv(qy, qn), z = ddiv(qz, qn);
+  double R[9];
+  R[0] = dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(z, z))));
+  R[1] = dmul(2.0, dsub(dmul(x, y), dmul(w, z)));
+  R[2] = dmul(2.0, dadd(dmul(x, z), dmul(w, y)));
+  R[3] = dmul(2.0, dadd(dmul(x, y), dmul(w, z)));
+  R[4] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(z, z))));
+  R[5] = dmul(2.0, dsub(dmul(y, z), dmul(w, x)));
+  R[6] = dmul(2.0, dsub(dmul(x, z), dmul(w, y)));
+  R[7] = dmul(2.0, dadd(dmul(y, z), dmul(w, x)));
+  R[8] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
+  const double s2[3] = {exp_d(dmul(2.0, l0)), exp_d(dmul(2.0, l1)), exp_d(dmul(2.0, l2))};
+  double S[9];  // (R diag(s2)) R^T
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      S[3 * i + j] = dadd(dadd(dmul(dmul(R[3 * i + 0], s2[0]), R[3 * j + 0]), dmul(dmul(R[3 * i + 1], s2[1]), R[3 * j + 1])),
+                          dmul(dmul(R[3 * i + 2], s2[2]), R[3 * j + 2]));
+  // J (projection.cpp:26-33)
+  const double iz = ddiv(1.0, pc2);
+  const double iz2 = dmul(iz, iz);
+  const double J[6] = {dmul(cam.fx, iz), 0.0, dmul(dmul(-cam.fx, pc0), iz2),
+                       0.0, dmul(cam.fy, iz), dmul(dmul(-cam.fy, pc1), iz2)};
+  // cov2d = ((((J W) S) W^T) J^T), left to right as projection.cpp:81
+  double A[6], B[6], C[6];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 3; ++j)
+      A[3 * i + j] = dadd(dadd(dmul(J[3 * i + 0], W[0 * 3 + j]), dmul(J[3 * i + 1], W[1 * 3 + j])), dmul(J[3 * i + 2], W[2 * 3 + j]));
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 3; ++j)
+      B[3 * i + j] = dadd(dadd(dmul(A[3 * i + 0], S[0 * 3 + j]), dmul(A[3 * i + 1], S[1 * 3 + j])), dmul(A[3 * i + 2], S[2 * 3 + j]));
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 3; ++j)  // times W^T: (W^T)(k,j) = W(j,k)
+      C[3 * i + j] = dadd(dadd(dmul(B[3 * i + 0], W[3 * j + 0]), dmul(B[3 * i + 1], W[3 * j + 1])), dmul(B[3 * i + 2], W[3 * j + 2]));
+  double cv[4];
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j)
+      cv[2 * i + j] = dadd(dadd(dmul(C[3 * i + 0], J[3 * j + 0]), dmul(C[3 * i + 1], J[3 * j + 1])), dmul(C[3 * i + 2], J[3 * j + 2]));
+  cv[0] = dadd(cv[0], rp.dilation);
+  cv[3] = dadd(cv[3], rp.dilation);
+  const double det = dsub(dmul(cv[0], cv[3]), dmul(cv[1], cv[2]));
+  const bool fin = disfinite(cv[0]) && disfinite(cv[1]) && disfinite(cv[2]) && disfinite(cv[3]);
+  if (!(det > 0.0) || !fin) return o;
+  const double inv_det = ddiv(1.0, det);
+  o.c00 = dmul(cv[3], inv_det);
+  o.c01 = dmul(-cv[1], inv_det);
+  o.c11 = dmul(cv[0], inv_det);
+  const double mid = dmul(0.5, dadd(cv[0], cv[3]));
+  const double lmax2 = dadd(mid, dsqrt(dmax(0.0, dsub(dmul(mid, mid), det))));
+  o.radius = dmul(rp.footprint_sigma, dsqrt(lmax2));
+  if (dadd(o.mx, o.radius) < 0.0 || dsub(o.mx, o.radius) > static_cast<double>(cam.width) ||
+      dadd(o.my, o.radius) < 0.0 || dsub(o.my, o.radius) > static_cast<double>(cam.height))
+    return o;
+  o.visible = 1;
+  // sigmoid(opacity_logit) (primitive.hpp:11,33)
+  o.sigma = ddiv(1.0, dadd(1.0, exp_d(-static_cast<double>(p[10 * stride]))));
+  // colour through SH along the normalized view direction (rasterizer.cpp:60-63)
+  const int K = rp.sh_coeffs;
+  const double d0 = dsub(m0, cam.center[0]), d1 = dsub(m1, cam.center[1]), d2 = dsub(m2, cam.center[2]);
+  const double len = dsqrt(dadd(dadd(dmul(d0, d0), dmul(d1, d1)), dmul(d2, d2)));
+  double dx = 0.0, dy = 0.0, dz = 1.0;
+  if (len > 1e-12) { dx = ddiv(d0, len); dy = ddiv(d1, len); dz = ddiv(d2, len); }
+  if (K <= 0) {
+    o.color[0] = o.color[1] = o.color[2] = 0.5;
+  } else {
+    double b[16];
+    sh_basis(sh_degree(K), dx, dy, dz, b);
+    for (int c = 0; c < 3; ++c) {
+      double acc = 0.5;
+      for (int k = 0; k < K; ++k) acc = dadd(acc, dmul(b[k], static_cast<double>(p[(11 + 3 * k + c) * stride])));
+      o.color[c] = dmax(acc, 0.0);
+    }
+  }
+  // inclusive tile rectangle (rasterizer.cpp:199-208)
+  const double ts = static_cast<double>(rp.tile);
+  o.tx0 = tile_clamp(ddiv(dsub(o.mx, o.radius), ts), rp.tiles_x - 1);
+  o.tx1 = tile_clamp(ddiv(dadd(o.mx, o.radius), ts), rp.tiles_x - 1);
+  o.ty0 = tile_clamp(ddiv(dsub(o.my, o.radius), ts), rp.tiles_y - 1);
+  o.ty1 = tile_clamp(ddiv(dadd(o.my, o.radius), ts), rp.tiles_y - 1);
+  return o;
+}
+
+// exp_map (lie.cpp:15-28) in explicit fp64; sin/cos are the platform's.
+GSF_HD void exp_map_d(const double* v, double* R) {
+  const double th2 = dadd(dadd(dmul(v[0], v[0]), dmul(v[1], v[1])), dmul(v[2], v[2]));
+  const double th = dsqrt(th2);
+  double a, b;
+  if (th < 1e-8) {
+    a = dsub(1.0, ddiv(th2, 6.0));
+    b = dsub(0.5, ddiv(th2, 24.0));
+  } else {
+    a = ddiv(sin(th), th);
+    b = ddiv(dsub(1.0, cos(th)), th2);
+  }
+  const double k[9] = {0.0, -v[2], v[1], v[2], 0.0, -v[0], -v[1], v[0], 0.0};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double kk = dadd(dadd(dmul(k[3 * i + 0], k[0 * 3 + j]), dmul(k[3 * i + 1], k[1 * 3 + j])), dmul(k[3 * i + 2], k[2 * 3 + j]));
+      R[3 * i + j] = dadd(dadd(i == j ? 1.0 : 0.0, dmul(a, k[3 * i + j])), dmul(b, kk));
+    }
+}
+
+// Camera from a pose tangent (pose.hpp:24,41) and intrinsics.
+GSF_HD Cam make_cam(const double* rot, const double* trans, double fx, double fy, double cx, double cy,
+                    int width, int height, double near_plane, double far_plane) {
+  Cam c;
+  exp_map_d(rot, c.W);
+  for (int i = 0; i < 3; ++i) c.t[i] = trans[i];
+  for (int i = 0; i < 3; ++i)
+    c.center[i] = -dadd(dadd(dmul(c.W[0 * 3 + i], trans[0]), dmul(c.W[1 * 3 + i], trans[1])), dmul(c.W[2 * 3 + i], trans[2]));
+  c.fx = fx; c.fy = fy; c.cx = cx; c.cy = cy;
+  c.width = width; c.height = height;
+  c.near_plane = near_plane; c.far_plane = far_plane;
+  return c;
+}
+
+// Depth sort key: IEEE bits of the fp32-rounded depth, offset by the near plane.  Rounding
+// is monotone so the key order agrees with the fp64 order up to ties, which the fixup pass
+// resolves with the exact (fp64 depth, id) comparison of rasterizer.cpp:74-77.
+GSF_HD uint32_t depth_key(double depth, uint32_t near_bits) {
+  return static_cast<uint32_t>(fbits(static_cast<float>(depth))) - near_bits;
+}
+
+// ---------------------------------------------------------------------------------------
+// Blend (fp32) with an fp64 guard band on the two discrete tests of blend_pixel.
+// ---------------------------------------------------------------------------------------
+struct BlendG {       // per visible primitive, rank order, 3 x float4 on the device
+  float mx, my, depth, sigma;
+  float c00, c01x2, c11, pad0;
+  float r, g, b, pad1;
+};
+struct GuardG {       // fp64 copies read only inside the guard band
+  double mx, my, c00, c01, c11, sigma;
+};
+GSF_HD BlendG make_blend_g(const PreOut& o) {
+  BlendG g;
+  g.mx = static_cast<float>(o.mx);
+  g.my = static_cast<float>(o.my);
+  g.depth = static_cast<float>(o.depth);
+  g.sigma = static_cast<float>(o.sigma);
+  g.c00 = static_cast<float>(o.c00);
+  g.c01x2 = static_cast<float>(dmul(2.0, o.c01));
+  g.c11 = static_cast<float>(o.c11);
+  g.pad0 = 0.0f;
+  g.r = static_cast<float>(o.color[0]);
+  g.g = static_cast<float>(o.color[1]);
+  g.b = static_cast<float>(o.color[2]);
+  g.pad1 = 0.0f;
+  return g;
+}
+GSF_HD GuardG make_guard_g(const PreOut& o) {
+  GuardG g;
+  g.mx = o.mx; g.my = o.my; g.c00 = o.c00; g.c01 = o.c01; g.c11 = o.c11; g.sigma = o.sigma;
+  return g;
+}
+
+struct BlendConsts {
+  float cutoff;       // footprint_sigma^2
+  float skip, clamp, term;
+  double cutoff_d, skip_d, clamp_d;
+  float rho_band, alpha_band;
+};
+
+GSF_HD BlendConsts make_blend_consts(const RasterParams& rp) {
+  BlendConsts k;
+  k.cutoff_d = dmul(rp.footprint_sigma, rp.footprint_sigma);
+  k.cutoff = static_cast<float>(k.cutoff_d);
+  k.skip_d = rp.alpha_skip;
+  k.clamp_d = rp.alpha_clamp;
+  k.skip = static_cast<float>(rp.alpha_skip);
+  k.clamp = static_cast<float>(rp.alpha_clamp);
+  k.term = static_cast<float>(rp.termination);
+  k.rho_band = static_cast<float>(4e-3 + 2e-4 * k.cutoff_d);
+  k.alpha_band = 5e-4f;
+  return k;
+}
+
+GSF_HD double guard_rho(double px, double py, const GuardG& g) {
+  const double dx = dsub(px, g.mx), dy = dsub(py, g.my);
+  // conic00*dx*dx + 2*conic01*dx*dy + conic11*dy*dy (rasterizer.cpp:108-109)
+  return dadd(dadd(dmul(dmul(g.c00, dx), dx), dmul(dmul(dmul(2.0, g.c01), dx), dy)), dmul(dmul(g.c11, dy), dy));
+}
+
+// Result of the per-pair test.  code: 0 = skip, 1 = contributes.
+struct PairEval {
+  int code;
+  int clamped;   // sigma*g > alpha_clamp (gradient stop, rasterizer.cpp:451)
+  float alpha;   // min(sigma*g, clamp)
+  float gval;    // exp(-rho/2)
+  float dx, dy;
+};
+
+// The guard is only consulted for values within a small band of a threshold, so the device
+// touches the fp64 copy for a tiny fraction of pairs.  `gp` points at the fp64 copy.
+GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
+  PairEval e;
+  e.dx = fsub(px, g.mx);
+  e.dy = fsub(py, g.my);
+  const float rho = ffma(fmul(g.c00, e.dx), e.dx, ffma(fmul(g.c01x2, e.dx), e.dy, fmul(fmul(g.c11, e.dy), e.dy)));
+  e.code = 0;
+  e.clamped = 0;
+  e.alpha = 0.0f;
+  e.gval = 0.0f;
+  double rho_d = -1.0;
+  bool have_d = false;
+  // rho > cutoff || rho < 0 -> skip
+  if (rho > fadd(k.cutoff, k.rho_band)) return e;
+  if (rho >= fsub(k.cutoff, k.rho_band) || rho < k.rho_band) {
+    rho_d = guard_rho(static_cast<double>(px), static_cast<double>(py), *gp);
+    have_d = true;
+    if (rho_d > k.cutoff_d || rho_d < 0.0) return e;
+  }
+  e.gval = exp_f(fmul(-0.5f, rho));
+  const float raw = fmul(g.sigma, e.gval);
+  // raw < alpha_skip -> skip
+  const float sb = fmul(k.skip, k.alpha_band);
+  if (raw < fsub(k.skip, sb)) return e;
+  if (raw <= fadd(k.skip, sb)) {
+    if (!have_d) { rho_d = guard_rho(static_cast<double>(px), static_cast<double>(py), *gp); have_d = true; }
+    const double raw_d = dmul(gp->sigma, exp_d(dmul(-0.5, rho_d)));
+    if (raw_d < k.skip_d) return e;
+  }
+  // alpha clamp decision
+  const float cb = fmul(k.clamp, k.alpha_band);
+  if (raw > fadd(k.clamp, cb)) {
+    e.clamped = 1;
+  } else if (raw >= fsub(k.clamp, cb)) {
+    if (!have_d) { rho_d = guard_rho(static_cast<double>(px), static_cast<double>(py), *gp); have_d = true; }
+    const double raw_d = dmul(gp->sigma, exp_d(dmul(-0.5, rho_d)));
+    e.clamped = raw_d > k.clamp_d ? 1 : 0;
+  }
+  e.alpha = e.clamped ? k.clamp : fminf_(raw, k.clamp);
+  e.code = 1;
+  return e;
+}
+
+struct PixelState {
+  float T;
+  float cr, cg, cb, ad, op, unc, best, med_depth;
+  int32_t count, dominant, median, last;   // last = list index + 1 of the last contributor
+  int32_t done;
+};
+
+GSF_HD void pixel_init(PixelState& s) {
+  s.T = 1.0f;
+  s.cr = s.cg = s.cb = s.ad = s.op = s.unc = s.best = s.med_depth = 0.0f;
+  s.count = 0;
+  s.dominant = -1;
+  s.median = -1;
+  s.last = 0;
+  s.done = 0;
+}
+
+// Accumulate one contributing pair (rasterizer.cpp:116-137).  `id` is the primitive id.
+GSF_HD void pixel_accumulate(PixelState& s, const BlendG& g, const PairEval& e, int32_t id, int32_t list_index,
+                             bool obs_valid, float obs, const BlendConsts& k) {
+  const float w = fmul(e.alpha, s.T);
+  s.cr = ffma(w, g.r, s.cr);
+  s.cg = ffma(w, g.g, s.cg);
+  s.cb = ffma(w, g.b, s.cb);
+  s.ad = ffma(w, g.depth, s.ad);
+  s.op = fadd(s.op, w);
+  if (obs_valid) {
+    const float d = fsub(g.depth, obs);
+    s.unc = ffma(fmul(w, d), d, s.unc);
+  }
+  if (w > s.best) {
+    s.best = w;
+    s.dominant = id;
+  }
+  s.count += 1;
+  s.last = list_index + 1;
+  const float t_next = fmul(s.T, fsub(1.0f, e.alpha));
+  if (s.median < 0 && s.T >= 0.5f && t_next < 0.5f) {
+    s.median = id;
+    s.med_depth = g.depth;
+  }
+  s.T = t_next;
+  if (s.T < k.term) s.done = 1;
+}
+
+}  // namespace gsfk

@@ -1,0 +1,206 @@
+// kernels.h — host-side launch wrappers of the sm_100a kernels and the device workspace.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gsfk {
+
+// Optional CUDA-event brackets around named kernels (bench / roofline evidence only).
+struct Profiler {
+  struct Mark { int name; cudaEvent_t a, b; };
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<Mark> pending;
+  double total_ms[16] = {0};
+  int64_t count[16] = {0};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void begin(int name, cudaStream_t st) {
+    if (!on) return;
+    Mark m{name, get(), get()};
+    cudaEventRecord(m.a, st);
+    pending.push_back(m);
+  }
+  void end(cudaStream_t st) {
+    if (!on || pending.empty()) return;
+    cudaEventRecord(pending.back().b, st);
+  }
+  void resolve() {   // after a stream sync
+    for (Mark& m : pending) {
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) {
+        total_ms[m.name] += ms;
+        count[m.name] += 1;
+      }
+      pool.push_back(m.a);
+      pool.push_back(m.b);
+    }
+    pending.clear();
+  }
+};
+enum ProfName { PROF_PREPROCESS = 0, PROF_SORT = 1, PROF_BLEND = 2, PROF_BACKWARD = 3, PROF_CHAIN = 4, PROF_SSIM = 5,
+                PROF_ADAM = 6, PROF_BINNING = 7, PROF_NUM = 8 };
+
+struct ScanTemp {
+  unsigned long long* state = nullptr;
+};
+
+// Device workspace of one context.  Capacities grow on demand (never shrink).
+struct Workspace {
+  int64_t P_cap = 0, pair_cap = 0, npix_cap = 0, tiles_cap = 0;
+  // per primitive, id-indexed
+  uint32_t* flag = nullptr;
+  uint32_t* vis_off = nullptr;
+  uint32_t* key_id = nullptr;
+  BlendG* bg_id = nullptr;
+  GuardG* gg_id = nullptr;
+  double* depth_id = nullptr;
+  int4* rect_id = nullptr;
+  uint8_t* visible = nullptr;
+  // per visible primitive, depth-rank-indexed
+  uint32_t* skeys[2] = {nullptr, nullptr};
+  uint32_t* svals[2] = {nullptr, nullptr};
+  int32_t* rank_to_id = nullptr;
+  BlendG* bg = nullptr;
+  GuardG* gg = nullptr;
+  int4* rect = nullptr;
+  uint32_t* tile_cnt = nullptr;
+  uint32_t* pair_off = nullptr;
+  // per (tile, primitive) pair
+  uint32_t* pkeys[2] = {nullptr, nullptr};
+  uint32_t* pvals[2] = {nullptr, nullptr};
+  uint32_t* pair_rank = nullptr;
+  float* partials = nullptr;   // pair_cap * 10
+  // per tile
+  int2* ranges = nullptr;
+  double* loss_part = nullptr;  // tiles * LS_NUM
+  // per pixel (render outputs + backward inputs)
+  float* color = nullptr;      // 3*npix, interleaved
+  float* alpha_depth = nullptr;
+  float* median_depth = nullptr;
+  uint8_t* median_valid = nullptr;
+  float* opacity = nullptr;
+  float* uncertainty = nullptr;
+  float* final_T = nullptr;
+  int32_t* count = nullptr;
+  int32_t* dominant = nullptr;
+  int32_t* median_prim = nullptr;
+  float* dominant_w = nullptr;
+  int32_t* last = nullptr;
+  float* obs = nullptr;         // observed depth of the API render (npix)
+  float* upstream = nullptr;    // explicit upstream maps for gsf_render_backward (7*npix)
+  float* dssim = nullptr;       // 3*npix: d(w_ssim * ssim loss)/d colour (mapping)
+  float* ssim_tmp = nullptr;    // SSIM scratch maps (see loss.cu)
+  // temporaries
+  ScanTemp scan;
+  uint32_t* radix_temp = nullptr;
+  size_t radix_temp_bytes = 0;
+  double* pose_part = nullptr;  // chain blocks * 6
+  double* red_part = nullptr;   // generic per-block fp64 partials (ssim, then iso)
+  int64_t red_iso_offset = 0;
+  int ssim_blocks = 0, iso_blocks = 0;
+  // final buffers of the two sorts (set by the pipeline)
+  uint32_t* depth_sorted_vals = nullptr;
+  uint32_t* pair_sorted_keys = nullptr;
+  uint32_t* pair_sorted_vals = nullptr;
+  Profiler* prof = nullptr;
+};
+
+// sort.cu
+void launch_scan_excl(const uint32_t* in, uint32_t* out, const uint32_t* n_dev, uint32_t n_max, uint32_t* total_out,
+                      ScanTemp& tmp, cudaStream_t st, int64_t* launches);
+size_t scan_temp_bytes(uint32_t n_max);
+size_t radix_temp_bytes(uint32_t n_max, int max_passes);
+int radix_sort_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
+                   uint32_t n_max, int begin_bit, int end_bit, bool vals_are_index, uint32_t* temp, cudaStream_t st,
+                   int64_t* launches);
+void launch_sort_fixup(const uint32_t* keys, uint32_t* vals, const double* depth_id, const uint32_t* n_dev,
+                       uint32_t n_max, cudaStream_t st, int64_t* launches);
+
+// raster_fwd.cu
+struct FwdArgs {
+  const float* params;   // [D][P]
+  int64_t P;
+  int32_t K;
+  RasterParams rp;
+  BlendConsts kc;
+  int32_t W, H;
+  double near_plane, far_plane;
+  const float* obs;          // observed depth for the U map (nullable)
+  const float* loss_rgb;     // target colour for the fused loss epilogue (nullable)
+  const float* loss_depth;   // sensor depth for the loss masks (nullable)
+  LossParams lp;
+  int iteration;             // loop iteration (for device-side checks), -1 outside loops
+};
+void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* launches);
+void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,
+                    double near_plane, double far_plane, float floor, cudaStream_t st, int64_t* launches);
+
+// raster_bwd.cu
+enum SeedMode { SEED_EXPLICIT = 0, SEED_TRACK = 1, SEED_MAP = 2 };
+struct BwdArgs {
+  const float* params;
+  int64_t P;
+  int32_t K;
+  RasterParams rp;
+  BlendConsts kc;
+  int32_t W, H;
+  double near_plane, far_plane;
+  const float* obs;          // sensor depth (U map gradient / loss masks), nullable
+  const float* target_rgb;   // loss target (tracking/mapping seeds)
+  const float* up_color;     // explicit seeds (SEED_EXPLICIT), nullable each
+  const float* up_adepth;
+  const float* up_mdepth;
+  const float* up_opacity;
+  const float* up_uncert;
+  LossParams lp;
+  int seed_mode;
+  bool pose_only;            // tracking: skip per-primitive parameter gradients
+  float* grads;              // [D][P] parameter gradients (full mode)
+  float* d_mean2d;           // [2][P] (full mode, nullable)
+};
+void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st, int64_t* launches);
+// seed maps (3 colour planes interleaved, then ad, md, u planes) of the last render's loss
+void run_seeds_out(Workspace& ws, DevState* ds, int mode, const float* target, const float* depth, const LossParams& lp,
+                   int W, int H, double near_plane, double far_plane, float* out, cudaStream_t st, int64_t* launches);
+
+// loss.cu
+void run_loss_finalize(Workspace& ws, DevState* ds, const LossParams& lp, int tiles, int64_t npix, int iteration,
+                       cudaStream_t st, int64_t* launches);
+void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W, int H, float weight_grad,
+              float* d_out, cudaStream_t st, int64_t* launches);
+void run_iso(Workspace& ws, DevState* ds, const float* params, int64_t P, double w_iso, double eps, float* grads,
+             cudaStream_t st, int64_t* launches);
+
+// optim.cu
+struct AdamGroups {
+  double lr[5];   // mean, log_scale, quat, opacity, sh
+};
+void run_adam(float* params, const float* grads, float* m, float* v, int64_t P, int D, const AdamGroups& g, double step,
+              cudaStream_t st, int64_t* launches);
+void run_track_update(DevState* ds, int iteration, cudaStream_t st, int64_t* launches);
+void run_densify_stats(const uint8_t* visible, const float* d_mean2d, float* accum, int32_t* cnt, int64_t P, int W,
+                       int H, cudaStream_t st, int64_t* launches);
+
+// uncert.cu
+void run_uncertainty_view(const Workspace& ws, const float* params, int64_t P, const float* obs, int W, int H,
+                          double near_plane, double far_plane, const DevState* ds, double* sum, uint32_t* cnt,
+                          cudaStream_t st, int64_t* launches);
+void run_uncertainty_finalize(const double* sum, const uint32_t* cnt, float* nu, uint8_t* observed, int64_t P,
+                              uint32_t* observed_count, cudaStream_t st, int64_t* launches);
+void run_prune(const float* nu, float* opacity_logit, int64_t P, float tau, float target, uint32_t* reduced,
+               cudaStream_t st, int64_t* launches);
+
+}  // namespace gsfk

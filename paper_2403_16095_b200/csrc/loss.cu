@@ -1,0 +1,383 @@
+// loss.cu — loss finalisation, SSIM forward/adjoint and the anisotropy (iso) term on sm_100a.
+//
+//   k_loss_finalize  the scalar tails of evaluate_tracking_loss (losses.cpp:284-339) and
+//                    evaluate_mapping_loss (:156-282): a fixed-order sum of the per-tile partials
+//                    written by the blend epilogue, the normalisers w/m of every seed map, and
+//                    the device-side loop checks of track_frame (tracker.cpp:45-60) / map_step
+//                    (mapper.cpp:247-254) so no host round trip is needed per iteration.
+//   SSIM             ssim.cpp:27-187: separable 11-tap blur with border renormalisation, fp64
+//                    per-pixel terms, and the adjoint blur for d(ssim)/dx.
+//   k_iso            iso term and its direct log-scale gradient (losses.cpp:195-216, 272-280).
+#include "kernels.h"
+
+namespace gsfk {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum one value per thread over a 256-thread block in a fixed tree; result valid in thread 0.
+__device__ __forceinline__ double block_sum_d(double v, double* s_red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  v = warp_sum_d(v);
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (tid == 0)
+    for (int w = 0; w < 8; ++w) t += s_red[w];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(256) k_loss_finalize(const double* __restrict__ loss_part, int tiles, int64_t npix,
+                                                       LossParams lp, int iteration, const double* __restrict__ ssim_part,
+                                                       int ssim_blocks, const double* __restrict__ iso_part,
+                                                       int iso_blocks, DevState* ds) {
+  __shared__ double s_red[8];
+  double tot[LS_NUM];
+  for (int q = 0; q < LS_NUM; ++q) {
+    double a = 0.0;
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) a += loss_part[static_cast<int64_t>(t) * LS_NUM + q];
+    tot[q] = block_sum_d(a, s_red);
+  }
+  double ssim_sum = 0.0, iso_sum = 0.0;
+  {
+    double a = 0.0;
+    for (int t = threadIdx.x; t < ssim_blocks; t += blockDim.x) a += ssim_part[t];
+    ssim_sum = block_sum_d(a, s_red);
+    a = 0.0;
+    for (int t = threadIdx.x; t < iso_blocks; t += blockDim.x) a += iso_part[t];
+    iso_sum = block_sum_d(a, s_red);
+  }
+  if (threadIdx.x != 0) return;
+  if (ds->halt) return;
+  for (int q = 0; q < LS_NUM; ++q) ds->loss[q] = tot[q];
+  const double hw = static_cast<double>(npix);
+  const bool nbv = lp.normalize_by_valid != 0;
+  const double cc = tot[LS_COLOR_CNT], cg = tot[LS_GEO_CNT], ca = tot[LS_ALIGN_CNT], cv = tot[LS_VAR_CNT];
+  if (lp.mode == 1) {
+    const double color = cc > 0.0 ? tot[LS_COLOR_SUM] / (3.0 * (nbv ? cc : hw)) : 0.0;
+    const double geo = cg > 0.0 ? tot[LS_GEO_SUM] / (nbv ? cg : hw) : 0.0;
+    const double total = lp.t_color * color + lp.t_geo * geo;
+    const double m_color = nbv ? cc : hw, m_geo = nbv ? cg : hw;
+    ds->term_color = color;
+    ds->term_geo = geo;
+    ds->term_align = ds->term_var = ds->term_ssim = ds->term_iso = 0.0;
+    ds->loss_total = total;
+    ds->seed_color = (lp.t_color > 0.0 && m_color > 0.0) ? lp.t_color / (3.0 * m_color) : 0.0;
+    ds->seed_geo = (lp.t_geo > 0.0 && m_geo > 0.0) ? lp.t_geo / m_geo : 0.0;
+    ds->any_empty = (cc == 0.0 || cg == 0.0) ? 1 : 0;
+    if (iteration == 0) {
+      ds->initial_loss = total;
+      if (cc == 0.0 && cg == 0.0) {   // tracker.cpp:46-53
+        ds->halt = 1;
+        ds->halt_iter = 0;
+        ds->final_loss = total;
+        ds->degraded = 1;
+        return;
+      }
+    }
+    if (iteration >= 0 && !isfinite(total)) {   // tracker.cpp:55-60
+      ds->halt = 2;
+      ds->halt_iter = iteration;
+    }
+  } else if (lp.mode == 2) {
+    bool warn = false;
+    const double color = hw > 0.0 ? tot[LS_COLOR_SUM] / (3.0 * hw) : 0.0;
+    auto masked = [&](double sum, double c) {
+      if (c == 0.0) { warn = true; return 0.0; }
+      return sum / (nbv ? c : hw);
+    };
+    const double geo = masked(tot[LS_GEO_SUM], cg);
+    const double align = masked(tot[LS_ALIGN_SUM], ca);
+    double var = 0.0;
+    if (ds->has_obs) var = masked(tot[LS_VAR_SUM], cv);
+    else warn = true;
+    const double ssim = lp.w_ssim > 0.0 ? 1.0 - ssim_sum / (3.0 * hw) : 0.0;
+    const double iso = ds->V > 0 ? iso_sum / static_cast<double>(ds->V) : 0.0;
+    const double total = lp.w_color * color + lp.w_ssim * ssim + lp.w_geo * geo + lp.w_align * align + lp.w_iso * iso +
+                         lp.w_var * var;
+    const double m_geo = nbv ? cg : hw, m_align = nbv ? ca : hw, m_var = nbv ? cv : hw;
+    ds->term_color = color;
+    ds->term_geo = geo;
+    ds->term_align = align;
+    ds->term_var = var;
+    ds->term_ssim = ssim;
+    ds->term_iso = iso;
+    ds->loss_total = total;
+    ds->any_empty = warn ? 1 : 0;
+    ds->seed_color = lp.w_color > 0.0 ? lp.w_color / (3.0 * hw) : 0.0;
+    ds->seed_geo = (lp.w_geo > 0.0 && m_geo > 0.0) ? lp.w_geo / m_geo : 0.0;
+    ds->seed_align = (lp.w_align > 0.0 && m_align > 0.0) ? lp.w_align / m_align : 0.0;
+    ds->seed_var = (lp.w_var > 0.0 && ds->has_obs && m_var > 0.0) ? lp.w_var / m_var : 0.0;
+    if (iteration >= 0 && !isfinite(total)) {
+      ds->halt = 2;
+      ds->halt_iter = iteration;
+    }
+  }
+}
+
+// ---- SSIM ------------------------------------------------------------------------------------
+constexpr int kR = 5;
+__constant__ float c_win[11];
+
+__device__ __forceinline__ float axis_norm(int p, int n) {
+  float z = 0.0f;
+#pragma unroll
+  for (int o = -kR; o <= kR; ++o)
+    if (p + o >= 0 && p + o < n) z += c_win[o + kR];
+  return z;
+}
+
+// horizontal pass over the 15 product maps (x, y, xx, yy, xy per channel), planar output
+__global__ void k_ssim_h(const float* __restrict__ x, const float* __restrict__ y, int W, int H, float* __restrict__ tmp) {
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  const int px = static_cast<int>(i % W);
+  const float zx = axis_norm(px, W);
+  float acc[15];
+#pragma unroll
+  for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
+#pragma unroll
+  for (int o = -kR; o <= kR; ++o) {
+    if (px + o < 0 || px + o >= W) continue;
+    const float w = c_win[o + kR];
+    const int64_t j = i + o;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float a = x[3 * j + c], b = y[3 * j + c];
+      acc[c] += w * a;
+      acc[3 + c] += w * b;
+      acc[6 + c] += w * (a * a);
+      acc[9 + c] += w * (b * b);
+      acc[12 + c] += w * (a * b);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 15; ++q) tmp[q * npix + i] = acc[q] / zx;
+}
+
+// vertical pass + per-pixel SSIM (fp64) + the three adjoint seed maps (ssim.cpp:139-176)
+__global__ void __launch_bounds__(256) k_ssim_v(const float* __restrict__ tmp, int W, int H, double weight,
+                                                float* __restrict__ u, double* __restrict__ part) {
+  __shared__ double s_red[8];
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double ssum = 0.0;
+  if (i < npix) {
+    const int py = static_cast<int>(i / W);
+    const float zy = axis_norm(py, H);
+    float acc[15];
+#pragma unroll
+    for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
+#pragma unroll
+    for (int o = -kR; o <= kR; ++o) {
+      if (py + o < 0 || py + o >= H) continue;
+      const float w = c_win[o + kR];
+      const int64_t j = i + static_cast<int64_t>(o) * W;
+#pragma unroll
+      for (int q = 0; q < 15; ++q) acc[q] += w * tmp[q * npix + j];
+    }
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double mx = acc[c] / zy, my = acc[3 + c] / zy, ex2 = acc[6 + c] / zy, ey2 = acc[9 + c] / zy,
+                   exy = acc[12 + c] / zy;
+      const double a1 = 2.0 * mx * my + C1;
+      const double a2 = 2.0 * (exy - mx * my) + C2;
+      const double b1 = mx * mx + my * my + C1;
+      const double b2 = (ex2 - mx * mx) + (ey2 - my * my) + C2;
+      const double denom = b1 * b2;
+      const double sv = a1 * a2 / denom;
+      ssum += sv;
+      if (u) {
+        const double d_a1 = a2 / denom, d_a2 = a1 / denom, d_b1 = -sv / b1, d_b2 = -sv / b2;
+        u[c * npix + i] = static_cast<float>((2.0 * my * d_a1 - 2.0 * my * d_a2 + 2.0 * mx * d_b1 - 2.0 * mx * d_b2) * weight);
+        u[(3 + c) * npix + i] = static_cast<float>(d_b2 * weight);
+        u[(6 + c) * npix + i] = static_cast<float>(2.0 * d_a2 * weight);
+      }
+    }
+  }
+  const double t = block_sum_d(ssum, s_red);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+// adjoint, vertical first: tmp(x,y) = sum_o w u(x,y+o) / zy(y+o)   (ssim.cpp:60-70)
+__global__ void k_ssim_adj_v(const float* __restrict__ u, int W, int H, float* __restrict__ t2) {
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  const int py = static_cast<int>(i / W);
+  float acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
+#pragma unroll
+  for (int o = -kR; o <= kR; ++o) {
+    if (py + o < 0 || py + o >= H) continue;
+    const float w = c_win[o + kR] / axis_norm(py + o, H);
+    const int64_t j = i + static_cast<int64_t>(o) * W;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] += w * u[q * npix + j];
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) t2[q * npix + i] = acc[q];
+}
+
+// then horizontal, and d_x = a_mu + 2 a_ex2 x + a_exy y   (ssim.cpp:72-80, 178-183)
+__global__ void k_ssim_adj_h(const float* __restrict__ t2, const float* __restrict__ x, const float* __restrict__ y, int W,
+                             int H, float* __restrict__ dx) {
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  const int px = static_cast<int>(i % W);
+  float acc[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
+#pragma unroll
+  for (int o = -kR; o <= kR; ++o) {
+    if (px + o < 0 || px + o >= W) continue;
+    const float w = c_win[o + kR] / axis_norm(px + o, W);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] += w * t2[q * npix + i + o];
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) dx[3 * i + c] = acc[c] + 2.0f * acc[3 + c] * x[3 * i + c] + acc[6 + c] * y[3 * i + c];
+}
+
+// small-image fallback: global statistics (ssim.cpp:117-144), one block
+__global__ void __launch_bounds__(256) k_ssim_global(const float* __restrict__ x, const float* __restrict__ y, int64_t n,
+                                                     float* __restrict__ dx, double* part) {
+  __shared__ double s_red[8];
+  __shared__ double s_stat[15];
+  __shared__ double s_part[9];
+  for (int q = 0; q < 15; ++q) {
+    const int c = q % 3, kind = q / 3;
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const double xv = x[3 * i + c], yv = y[3 * i + c];
+      a += kind == 0 ? xv : kind == 1 ? yv : kind == 2 ? xv * xv : kind == 3 ? yv * yv : xv * yv;
+    }
+    const double t = block_sum_d(a, s_red);
+    if (threadIdx.x == 0) s_stat[q] = t / static_cast<double>(n);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    double ssum = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      const double mx = s_stat[c], my = s_stat[3 + c], ex2 = s_stat[6 + c], ey2 = s_stat[9 + c], exy = s_stat[12 + c];
+      const double a1 = 2.0 * mx * my + C1, a2 = 2.0 * (exy - mx * my) + C2;
+      const double b1 = mx * mx + my * my + C1, b2 = (ex2 - mx * mx) + (ey2 - my * my) + C2;
+      const double denom = b1 * b2, sv = a1 * a2 / denom;
+      ssum += sv;
+      const double d_a1 = a2 / denom, d_a2 = a1 / denom, d_b1 = -sv / b1, d_b2 = -sv / b2;
+      s_part[c] = 2.0 * my * d_a1 - 2.0 * my * d_a2 + 2.0 * mx * d_b1 - 2.0 * mx * d_b2;
+      s_part[3 + c] = d_b2;
+      s_part[6 + c] = 2.0 * d_a2;
+    }
+    // reported as a per-pixel sum so the finaliser's 1 - sum/(3n) is the channel mean
+    part[0] = ssum * static_cast<double>(n);
+  }
+  __syncthreads();
+  if (dx) {
+    const double inv = 1.0 / static_cast<double>(n);
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      for (int c = 0; c < 3; ++c)
+        dx[3 * i + c] = static_cast<float>((s_part[c] + 2.0 * s_part[3 + c] * x[3 * i + c] + s_part[6 + c] * y[3 * i + c]) *
+                                           (inv / 3.0));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_iso(const float* __restrict__ params, int64_t P, const uint8_t* __restrict__ visible,
+                                             const DevState* ds, double w_iso, double eps, int add_grad,
+                                             float* __restrict__ grads, double* __restrict__ part) {
+  __shared__ double s_red[8];
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double term = 0.0;
+  if (i < P && visible[i] && !ds->halt) {
+    const double s[3] = {exp(static_cast<double>(params[3 * P + i])), exp(static_cast<double>(params[4 * P + i])),
+                         exp(static_cast<double>(params[5 * P + i]))};
+    int a = 0, b = 0;
+    for (int c = 1; c < 3; ++c) {
+      if (s[c] > s[a]) a = c;
+      if (s[c] < s[b]) b = c;
+    }
+    const double ratio = s[a] / s[b];
+    term = (ratio > eps ? ratio : eps) - eps;
+    if (add_grad && ratio > eps && w_iso > 0.0) {
+      const double g = w_iso * ratio / static_cast<double>(ds->V);
+      grads[(3 + a) * P + i] = static_cast<float>(static_cast<double>(grads[(3 + a) * P + i]) + g);
+      grads[(3 + b) * P + i] = static_cast<float>(static_cast<double>(grads[(3 + b) * P + i]) - g);
+    }
+  }
+  if (add_grad) return;
+  const double t = block_sum_d(term, s_red);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+}  // namespace
+
+static bool g_win_ready = false;
+
+static void ensure_window() {
+  if (g_win_ready) return;
+  float w[11];
+  for (int i = 0; i <= 10; ++i) {
+    const double d = i - 5;
+    w[i] = static_cast<float>(std::exp(-d * d / (2.0 * 1.5 * 1.5)));
+  }
+  GSF_CUDA_CHECK(cudaMemcpyToSymbol(c_win, w, sizeof(w)));
+  g_win_ready = true;
+}
+
+void run_loss_finalize(Workspace& ws, DevState* ds, const LossParams& lp, int tiles, int64_t npix, int iteration,
+                       cudaStream_t st, int64_t* L) {
+  // red_part layout: [0, 4096) ssim block partials, [4096, 8192+) iso block partials
+  const int ssim_blocks = lp.mode == 2 && lp.w_ssim > 0.0 ? ws.ssim_blocks : 0;
+  const int iso_blocks = lp.mode == 2 ? ws.iso_blocks : 0;
+  k_loss_finalize<<<1, 256, 0, st>>>(ws.loss_part, tiles, npix, lp, iteration, ws.red_part, ssim_blocks,
+                                     ws.red_part + ws.red_iso_offset, iso_blocks, ds);
+  ++*L;
+}
+
+void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W, int H, float /*unused*/, float* d_out,
+              cudaStream_t st, int64_t* L) {
+  (void)ds;
+  ensure_window();
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  if (W < 11 || H < 11) {
+    k_ssim_global<<<1, 256, 0, st>>>(x, y, npix, d_out, ws.red_part);
+    ++*L;
+    ws.ssim_blocks = 1;
+    return;
+  }
+  const int blocks = div_up(npix, 256);
+  float* tmp = ws.ssim_tmp;               // 15 planes
+  float* u = ws.ssim_tmp + 15 * npix;     // 9 planes
+  float* t2 = ws.ssim_tmp;                // reuse the first 9 planes after the forward
+  k_ssim_h<<<blocks, 256, 0, st>>>(x, y, W, H, tmp);
+  k_ssim_v<<<blocks, 256, 0, st>>>(tmp, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr, ws.red_part);
+  *L += 2;
+  ws.ssim_blocks = blocks;
+  if (d_out) {
+    k_ssim_adj_v<<<blocks, 256, 0, st>>>(u, W, H, t2);
+    k_ssim_adj_h<<<blocks, 256, 0, st>>>(t2, x, y, W, H, d_out);
+    *L += 2;
+  }
+}
+
+void run_iso(Workspace& ws, DevState* ds, const float* params, int64_t P, double w_iso, double eps, float* grads,
+             cudaStream_t st, int64_t* L) {
+  if (P <= 0) { ws.iso_blocks = 0; return; }
+  const int blocks = div_up(P, 256);
+  k_iso<<<blocks, 256, 0, st>>>(params, P, ws.visible, ds, w_iso, eps, grads ? 1 : 0, grads, ws.red_part + ws.red_iso_offset);
+  ++*L;
+  if (!grads) ws.iso_blocks = blocks;
+}
+
+}  // namespace gsfk

@@ -1,0 +1,565 @@
+// raster_bwd.cu — reverse-order backward of the tile rasterizer on sm_100a.
+//
+// k_backward  render_backward phase 1 (rasterizer.cpp:374-464).  One 256-thread CTA per 16x16
+//             tile walks the tile list back to front in batches staged through shared memory.
+//             Every thread re-evaluates its pixel's pair with the forward's exact decision
+//             arithmetic (gsf_shared.cuh), recovers T by division from the final transmittance
+//             and accumulates the screen-space adjoints.  The per-(tile, primitive) sum over
+//             the 256 pixels is a warp reduce-scatter (12 shuffles for 10 fields instead of 50)
+//             followed by a fixed-order cross-warp sum; the CTA writes it ONCE into the pair's
+//             unique slot.  No float atomics anywhere: results are bit-repeatable.
+// k_chain     phase 2 (rasterizer.cpp:480-570) in fp64, one thread per visible primitive: a
+//             fixed-order gather of its pair slots (= the reference's tile-order reduction,
+//             :466-478), the projection/covariance chain, the SE(3) pose pieces and the
+//             world-parameter gradients; the pose 6-vector is reduced block-wise in fp64.
+// k_pose_sum  fixed-order sum of the per-block pose partials (rasterizer.cpp:570).
+#include "kernels.h"
+#include "pixel_loss.cuh"
+
+namespace gsfk {
+
+namespace {
+
+// Field layout of a pair partial: 0,1 d_mean2d; 2,3,4 d_cov2d (00, 01=10, 11); 5 d_depth;
+// 6,7,8 d_color; 9 d_sigma.  Pose-only mode keeps the first 6 (or 9 with view-dependent SH).
+template <int N, int LO>
+__device__ __forceinline__ void rs_step(float* f, bool upper, int off) {
+#pragma unroll
+  for (int i = 0; i < LO; ++i) {
+    const float hi = (LO + i < N) ? f[LO + i] : 0.0f;
+    const float send = upper ? f[i] : hi;
+    const float keep = upper ? hi : f[i];
+    f[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+  }
+}
+
+template <int NF>
+__device__ __forceinline__ float warp_reduce_scatter(float* f, int lane) {
+  constexpr int n1 = (NF + 1) / 2, n2 = (n1 + 1) / 2, n3 = (n2 + 1) / 2, n4 = (n3 + 1) / 2, n5 = (n4 + 1) / 2;
+  rs_step<NF, n1>(f, lane & 16, 16);
+  rs_step<n1, n2>(f, lane & 8, 8);
+  rs_step<n2, n3>(f, lane & 4, 4);
+  rs_step<n3, n4>(f, lane & 2, 2);
+  rs_step<n4, n5>(f, lane & 1, 1);
+  return f[0];
+}
+
+__device__ __forceinline__ int rs_field(int nf, int lane, bool& valid) {
+  int base = 0, n = nf, end = nf;
+  for (int off = 16; off >= 1; off >>= 1) {
+    const int lo = (n + 1) / 2;
+    if (lane & off) {
+      end = min(end, base + n);
+      base += lo;
+    } else {
+      end = min(end, base + lo);
+    }
+    n = lo;
+  }
+  valid = base < end;
+  return base;
+}
+
+__device__ __forceinline__ float sgnf(float v) { return v > 0.0f ? 1.0f : (v < 0.0f ? -1.0f : 0.0f); }
+
+__device__ __forceinline__ bool dvalid(float d, double near_plane, double far_plane) {
+  const double v = d;
+  return isfinite(v) && v > near_plane && v < far_plane;
+}
+
+struct BwdPtrs {
+  const int2* ranges;
+  const uint32_t* sorted_orig;
+  const uint32_t* pair_rank;
+  const BlendG* bg;
+  const GuardG* gg;
+  const int32_t* rank_to_id;
+  const float* color;
+  const float* alpha_depth;
+  const float* median_depth;
+  const uint8_t* median_valid;
+  const float* opacity;
+  const float* final_T;
+  const int32_t* last;
+  const int32_t* median_prim;
+  const float* obs;
+  const float* target;
+  const float* up_color;
+  const float* up_adepth;
+  const float* up_mdepth;
+  const float* up_opacity;
+  const float* up_uncert;
+  const float* dssim;
+  float* partials;
+};
+
+constexpr int kBwdBatch = 64;
+
+template <int SEED, int NF>
+__global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc, double near_plane,
+                                                  double far_plane, LossParams lp, const DevState* ds) {
+  __shared__ BlendG s_g[kBwdBatch];
+  __shared__ int32_t s_rank[kBwdBatch];
+  __shared__ int32_t s_id[kBwdBatch];
+  __shared__ uint32_t s_orig[kBwdBatch];
+  __shared__ float s_part[8][kBwdBatch][NF];
+  __shared__ int s_wmax[8];
+  if (ds->halt) return;
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int x = tx * kTile + (tid & 15), y = ty * kTile + (tid >> 4);
+  const bool inside = x < W && y < H;
+  const int64_t pi = static_cast<int64_t>(y) * W + x;
+  const int2 rg = bp.ranges[tile];
+
+  float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gad = 0.f, gop = 0.f, gmd = 0.f, gu = 0.f, D = 0.f, T = 1.f;
+  int med = -1, last = 0;
+  if (inside) {
+    last = bp.last[pi];
+    T = bp.final_T[pi];
+    med = bp.median_prim[pi];
+    if (SEED == SEED_EXPLICIT) {
+      if (bp.up_color) { gc0 = bp.up_color[3 * pi]; gc1 = bp.up_color[3 * pi + 1]; gc2 = bp.up_color[3 * pi + 2]; }
+      if (bp.up_adepth) gad = bp.up_adepth[pi];
+      if (bp.up_opacity) gop = bp.up_opacity[pi];
+      if (bp.up_mdepth) gmd = bp.up_mdepth[pi];
+      if (bp.up_uncert && lp.uncertainty_full_gradient) gu = bp.up_uncert[pi];
+      if (bp.obs) {
+        D = bp.obs[pi];
+        if (!dvalid(D, near_plane, far_plane)) gu = 0.f;
+      } else {
+        gu = 0.f;
+      }
+    } else {
+      const PixSeeds sd = seeds_pixel<SEED == SEED_TRACK ? 1 : 2>(pi, bp.color, bp.alpha_depth[pi], bp.median_depth[pi],
+                                                                  bp.median_valid[pi] != 0, bp.opacity[pi], bp.target,
+                                                                  bp.obs, bp.dssim, ds, lp, near_plane, far_plane);
+      gc0 = sd.gc0; gc1 = sd.gc1; gc2 = sd.gc2; gad = sd.gad; gmd = sd.gmd;
+      gu = lp.uncertainty_full_gradient ? sd.gu : 0.0f;
+      if (SEED == SEED_MAP && bp.obs) D = bp.obs[pi];
+    }
+    if (med < 0) gmd = 0.f;
+    if (gc0 == 0.f && gc1 == 0.f && gc2 == 0.f && gad == 0.f && gop == 0.f && gmd == 0.f && gu == 0.f) last = 0;
+  }
+  int ml = __reduce_max_sync(0xffffffffu, last);
+  if (lane == 0) s_wmax[warp] = ml;
+  __syncthreads();
+  int maxlast = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) maxlast = max(maxlast, s_wmax[w]);
+  bool fvalid;
+  const int fidx = rs_field(NF, lane, fvalid);
+  const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
+  float S = 0.0f;
+  const int end = rg.x + maxlast;
+  for (int bend = end; bend > rg.x; bend -= kBwdBatch) {
+    const int bstart = max(rg.x, bend - kBwdBatch);
+    const int cnt = bend - bstart;
+    if (tid < cnt) {
+      const uint32_t orig = bp.sorted_orig[bstart + tid];
+      const int r = static_cast<int>(bp.pair_rank[orig]);
+      s_g[tid] = bp.bg[r];
+      s_rank[tid] = r;
+      s_id[tid] = bp.rank_to_id[r];
+      s_orig[tid] = orig;
+    }
+    __syncthreads();
+    for (int k = cnt - 1; k >= 0; --k) {
+      const int li = bstart + k - rg.x;
+      float f[NF];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) f[q] = 0.0f;
+      bool contrib = false;
+      if (li < last) {
+        const BlendG g = s_g[k];
+        const PairEval e = eval_pair(px, py, g, bp.gg + s_rank[k], kc);
+        if (e.code) {
+          contrib = true;
+          const float alpha = e.alpha;
+          const float inv = __frcp_rn(1.0f - alpha);
+          const float Tpre = T * inv;
+          const float derr = g.depth - D;
+          const float q = gc0 * g.r + gc1 * g.g + gc2 * g.b + gad * g.depth + gop + gu * derr * derr;
+          const float dal = Tpre * q - S * inv;
+          const float w = alpha * Tpre;
+          S += w * q;
+          if (NF >= 9) { f[6] = w * gc0; f[7] = w * gc1; f[8] = w * gc2; }
+          f[5] = w * (gad + 2.0f * gu * derr) + (s_id[k] == med ? gmd : 0.0f);
+          if (!e.clamped) {
+            if (NF >= 10) f[9] = dal * e.gval;
+            const float dg = dal * g.sigma;
+            const float c01 = 0.5f * g.c01x2;
+            const float ux = g.c00 * e.dx + c01 * e.dy, uy = c01 * e.dx + g.c11 * e.dy;
+            const float gdg = e.gval * dg;
+            f[0] = gdg * ux;
+            f[1] = gdg * uy;
+            const float h = 0.5f * gdg;
+            f[2] = h * ux * ux;
+            f[3] = h * ux * uy;
+            f[4] = h * uy * uy;
+          }
+          T = Tpre;
+        }
+      }
+      if (__any_sync(0xffffffffu, contrib)) {
+        const float val = warp_reduce_scatter<NF>(f, lane);
+        if (fvalid) s_part[warp][k][fidx] = val;
+      } else if (lane < NF) {
+        s_part[warp][k][lane] = 0.0f;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < cnt * NF; idx += 256) {
+      const int k = idx / NF, fi = idx - k * NF;
+      float sum = 0.0f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sum += s_part[w][k][fi];
+      bp.partials[static_cast<size_t>(s_orig[k]) * NF + fi] = sum;
+    }
+    __syncthreads();
+  }
+  for (int j = end + tid; j < rg.y; j += 256) {
+    const uint32_t orig = bp.sorted_orig[j];
+#pragma unroll
+    for (int fi = 0; fi < NF; ++fi) bp.partials[static_cast<size_t>(orig) * NF + fi] = 0.0f;
+  }
+}
+
+// SH basis gradients (sh.cpp:44-72), fp64.
+__device__ void sh_basis_grad(int degree, double x, double y, double z, double* g /*16*3*/) {
+  const double C1 = 0.4886025119029199;
+  for (int i = 0; i < 48; ++i) g[i] = 0.0;
+  if (degree < 1) return;
+  g[3 * 1 + 1] = -C1;
+  g[3 * 2 + 2] = C1;
+  g[3 * 3 + 0] = -C1;
+  if (degree < 2) return;
+  const double xx = x * x, yy = y * y, zz = z * z;
+  const double c20 = 1.0925484305920792, c21 = -1.0925484305920792, c22 = 0.31539156525252005, c23 = -1.0925484305920792,
+               c24 = 0.5462742152960396;
+  g[12] = c20 * y; g[13] = c20 * x; g[14] = 0.0;
+  g[15] = 0.0; g[16] = c21 * z; g[17] = c21 * y;
+  g[18] = c22 * (-2.0 * x); g[19] = c22 * (-2.0 * y); g[20] = c22 * (4.0 * z);
+  g[21] = c23 * z; g[22] = 0.0; g[23] = c23 * x;
+  g[24] = c24 * (2.0 * x); g[25] = c24 * (-2.0 * y); g[26] = 0.0;
+  if (degree < 3) return;
+  const double c30 = -0.5900435899266435, c31 = 2.890611442640554, c32 = -0.4570457994644658, c33 = 0.3731763325901154,
+               c34 = -0.4570457994644658, c35 = 1.445305721320277, c36 = -0.5900435899266435;
+  g[27] = c30 * (6.0 * x * y); g[28] = c30 * (3.0 * xx - 3.0 * yy); g[29] = 0.0;
+  g[30] = c31 * (y * z); g[31] = c31 * (x * z); g[32] = c31 * (x * y);
+  g[33] = c32 * (-2.0 * x * y); g[34] = c32 * (4.0 * zz - xx - 3.0 * yy); g[35] = c32 * (8.0 * y * z);
+  g[36] = c33 * (-6.0 * x * z); g[37] = c33 * (-6.0 * y * z); g[38] = c33 * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+  g[39] = c34 * (4.0 * zz - 3.0 * xx - yy); g[40] = c34 * (-2.0 * x * y); g[41] = c34 * (8.0 * x * z);
+  g[42] = c35 * (2.0 * x * z); g[43] = c35 * (-2.0 * y * z); g[44] = c35 * (xx - yy);
+  g[45] = c36 * (3.0 * xx - 3.0 * yy); g[46] = c36 * (-6.0 * x * y); g[47] = 0.0;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NF, bool FULL>
+__global__ void __launch_bounds__(256) k_chain(const uint32_t* __restrict__ pair_off, const float* __restrict__ partials,
+                                               const int32_t* __restrict__ rank_to_id, const DevState* ds, uint32_t Pcap,
+                                               uint32_t pair_cap, const float* __restrict__ params, int64_t P, int K,
+                                               float* __restrict__ grads, float* __restrict__ d_mean2d,
+                                               double* __restrict__ pose_part) {
+  __shared__ double s_red[8][6];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t r = blockIdx.x * blockDim.x + tid;
+  double pose[6] = {0, 0, 0, 0, 0, 0};
+  const uint32_t V = min(ds->V, Pcap);
+  if (r < V && !ds->halt) {
+    const uint32_t Mtot = min(ds->M, pair_cap);
+    const uint32_t beg = min(pair_off[r], Mtot);
+    const uint32_t end = r + 1 < V ? min(pair_off[r + 1], Mtot) : Mtot;
+    double sg[NF];
+#pragma unroll
+    for (int q = 0; q < NF; ++q) sg[q] = 0.0;
+    for (uint32_t p = beg; p < end; ++p) {
+#pragma unroll
+      for (int q = 0; q < NF; ++q) sg[q] += static_cast<double>(partials[static_cast<size_t>(p) * NF + q]);
+    }
+    bool zero = true;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) zero = zero && sg[q] == 0.0;
+    if (!zero) {
+      const int64_t id = rank_to_id[r];
+      const Cam& cam = ds->cam;
+      const double* Wr = cam.W;
+      const double m0 = params[0 * P + id], m1 = params[1 * P + id], m2 = params[2 * P + id];
+      const double pc[3] = {Wr[0] * m0 + Wr[1] * m1 + Wr[2] * m2 + cam.t[0], Wr[3] * m0 + Wr[4] * m1 + Wr[5] * m2 + cam.t[1],
+                            Wr[6] * m0 + Wr[7] * m1 + Wr[8] * m2 + cam.t[2]};
+      const double iz = 1.0 / pc[2], iz2 = iz * iz, z = pc[2];
+      const double J[2][3] = {{cam.fx * iz, 0.0, -cam.fx * pc[0] * iz2}, {0.0, cam.fy * iz, -cam.fy * pc[1] * iz2}};
+      const double qw0 = params[6 * P + id], qx0 = params[7 * P + id], qy0 = params[8 * P + id], qz0 = params[9 * P + id];
+      const double qlen = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
+      const double qn[4] = {qw0 / qlen, qx0 / qlen, qy0 / qlen, qz0 / qlen};
+      const double w = qn[0], x = qn[1], y = qn[2], zq = qn[3];
+      const double R[3][3] = {{1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq), 2 * (x * zq + w * y)},
+                              {2 * (x * y + w * zq), 1 - 2 * (x * x + zq * zq), 2 * (y * zq - w * x)},
+                              {2 * (x * zq - w * y), 2 * (y * zq + w * x), 1 - 2 * (x * x + y * y)}};
+      const double s[3] = {exp(static_cast<double>(params[3 * P + id])), exp(static_cast<double>(params[4 * P + id])),
+                           exp(static_cast<double>(params[5 * P + id]))};
+      double Cw[3][3], Cc[3][3], T1[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          Cw[a][b] = R[a][0] * (s[0] * s[0]) * R[b][0] + R[a][1] * (s[1] * s[1]) * R[b][1] + R[a][2] * (s[2] * s[2]) * R[b][2];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) T1[a][b] = Wr[3 * a + 0] * Cw[0][b] + Wr[3 * a + 1] * Cw[1][b] + Wr[3 * a + 2] * Cw[2][b];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Cc[a][b] = T1[a][0] * Wr[3 * b + 0] + T1[a][1] * Wr[3 * b + 1] + T1[a][2] * Wr[3 * b + 2];
+      const double dC[2][2] = {{sg[2], sg[3]}, {sg[3], sg[4]}};
+      // d_cov_cam = J^T dC J ; d_jac = 2 dC J Cc   (rasterizer.cpp:503-504)
+      double dCc[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+          const double t0 = J[0][a] * dC[0][0] + J[1][a] * dC[1][0];
+          const double t1 = J[0][a] * dC[0][1] + J[1][a] * dC[1][1];
+          dCc[a][b] = t0 * J[0][b] + t1 * J[1][b];
+        }
+      double dJ[2][3];
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b) {
+          double acc = 0.0;
+          for (int c = 0; c < 3; ++c) acc += (2.0 * dC[a][0] * J[0][c] + 2.0 * dC[a][1] * J[1][c]) * Cc[c][b];
+          dJ[a][b] = acc;
+        }
+      const double iz3 = iz2 / z;
+      double dp[3] = {0.0, 0.0, 0.0};
+      dp[0] += dJ[0][2] * (-cam.fx * iz2);
+      dp[1] += dJ[1][2] * (-cam.fy * iz2);
+      dp[2] += dJ[0][0] * (-cam.fx * iz2) + dJ[1][1] * (-cam.fy * iz2) + dJ[0][2] * (2.0 * cam.fx * pc[0] * iz3) +
+               dJ[1][2] * (2.0 * cam.fy * pc[1] * iz3);
+      for (int a = 0; a < 3; ++a) dp[a] += J[0][a] * sg[0] + J[1][a] * sg[1];
+      dp[2] += sg[5];
+      // pose (rasterizer.cpp:519-526)
+      pose[0] = pc[1] * dp[2] - pc[2] * dp[1];
+      pose[1] = pc[2] * dp[0] - pc[0] * dp[2];
+      pose[2] = pc[0] * dp[1] - pc[1] * dp[0];
+      pose[3] = dp[0];
+      pose[4] = dp[1];
+      pose[5] = dp[2];
+      for (int j = 0; j < 3; ++j) {
+        // E = skew(unit_j); sum dCc .* (E Cc - Cc E)
+        double E[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        if (j == 0) { E[1][2] = -1.0; E[2][1] = 1.0; }
+        if (j == 1) { E[0][2] = 1.0; E[2][0] = -1.0; }
+        if (j == 2) { E[0][1] = -1.0; E[1][0] = 1.0; }
+        double acc = 0.0;
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) {
+            double ec = 0.0, ce = 0.0;
+            for (int c = 0; c < 3; ++c) { ec += E[a][c] * Cc[c][b]; ce += Cc[a][c] * E[c][b]; }
+            acc += dCc[a][b] * (ec - ce);
+          }
+        pose[j] += acc;
+      }
+      double through[3] = {0.0, 0.0, 0.0};
+      double dcol[3] = {0.0, 0.0, 0.0};
+      if (NF >= 9) { dcol[0] = sg[6]; dcol[1] = sg[7]; dcol[2] = sg[8]; }
+      double dsh[48];
+      const bool need_sh = K > 0 && (FULL || K > 1);
+      if (need_sh) {
+        // eval_sh_color_backward (sh.cpp:88-108) along the view direction
+        const double d0 = m0 - cam.center[0], d1 = m1 - cam.center[1], d2 = m2 - cam.center[2];
+        const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+        double dir[3] = {0.0, 0.0, 1.0};
+        if (len > 1e-12) { dir[0] = d0 / len; dir[1] = d1 / len; dir[2] = d2 / len; }
+        const int deg = sh_degree(K);
+        double b[16];
+        sh_basis(deg, dir[0], dir[1], dir[2], b);
+        double masked[3];
+        for (int c = 0; c < 3; ++c) {
+          double raw = 0.5;
+          for (int k = 0; k < K; ++k) raw += b[k] * params[(11 + 3 * k + c) * P + id];
+          masked[c] = raw < 0.0 ? 0.0 : dcol[c];
+        }
+        for (int k = 0; k < K; ++k)
+          for (int c = 0; c < 3; ++c) dsh[3 * k + c] = b[k] * masked[c];
+        if (deg >= 1 && len > 1e-12) {
+          double gb[48];
+          sh_basis_grad(deg, dir[0], dir[1], dir[2], gb);
+          double dd[3] = {0.0, 0.0, 0.0};
+          for (int k = 1; k < K; ++k) {
+            const double md = masked[0] * params[(11 + 3 * k + 0) * P + id] + masked[1] * params[(11 + 3 * k + 1) * P + id] +
+                              masked[2] * params[(11 + 3 * k + 2) * P + id];
+            for (int a = 0; a < 3; ++a) dd[a] += gb[3 * k + a] * md;
+          }
+          const double dot = dir[0] * dd[0] + dir[1] * dd[1] + dir[2] * dd[2];
+          for (int a = 0; a < 3; ++a) through[a] = (dd[a] - dir[a] * dot) / len;
+          for (int a = 0; a < 3; ++a) pose[3 + a] += Wr[3 * a + 0] * through[0] + Wr[3 * a + 1] * through[1] + Wr[3 * a + 2] * through[2];
+        }
+      }
+      if (FULL) {
+        if (d_mean2d) { d_mean2d[id] = static_cast<float>(sg[0]); d_mean2d[P + id] = static_cast<float>(sg[1]); }
+        // world parameters (rasterizer.cpp:528-546)
+        for (int a = 0; a < 3; ++a) {
+          const double dm = Wr[0 * 3 + a] * dp[0] + Wr[1 * 3 + a] * dp[1] + Wr[2 * 3 + a] * dp[2] + through[a];
+          grads[a * P + id] = static_cast<float>(dm);
+        }
+        double dCw[3][3], T2[3][3];
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) T2[a][b] = Wr[0 * 3 + a] * dCc[0][b] + Wr[1 * 3 + a] * dCc[1][b] + Wr[2 * 3 + a] * dCc[2][b];
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) dCw[a][b] = T2[a][0] * Wr[0 * 3 + b] + T2[a][1] * Wr[1 * 3 + b] + T2[a][2] * Wr[2 * 3 + b];
+        double dM[3][3];  // 2 dCw (R diag(s))
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b)
+            dM[a][b] = 2.0 * (dCw[a][0] * R[0][b] * s[b] + dCw[a][1] * R[1][b] * s[b] + dCw[a][2] * R[2][b] * s[b]);
+        for (int a = 0; a < 3; ++a) {
+          const double ds_ = R[0][a] * dM[0][a] + R[1][a] * dM[1][a] + R[2][a] * dM[2][a];
+          grads[(3 + a) * P + id] = static_cast<float>(ds_ * s[a]);
+        }
+        double dR[3][3];
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) dR[a][b] = dM[a][b] * s[b];
+        // rotation_quat_jacobians (rasterizer.cpp:320-335)
+        const double jq[4][9] = {{0, -zq, y, zq, 0, -x, -y, x, 0},
+                                 {0, y, zq, y, -2 * x, -w, zq, w, -2 * x},
+                                 {-2 * y, x, w, x, 0, zq, -w, zq, -2 * y},
+                                 {-2 * zq, -w, x, w, -2 * zq, y, x, y, 0}};
+        double dqn[4];
+        for (int kq = 0; kq < 4; ++kq) {
+          double acc = 0.0;
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) acc += dR[a][b] * (2.0 * jq[kq][3 * a + b]);
+          dqn[kq] = acc;
+        }
+        const double qd = qn[0] * dqn[0] + qn[1] * dqn[1] + qn[2] * dqn[2] + qn[3] * dqn[3];
+        for (int a = 0; a < 4; ++a) grads[(6 + a) * P + id] = static_cast<float>((dqn[a] - qn[a] * qd) / qlen);
+        const double sig = 1.0 / (1.0 + exp(-static_cast<double>(params[10 * P + id])));
+        grads[10 * P + id] = static_cast<float>((NF >= 10 ? sg[9] : 0.0) * sig * (1.0 - sig));
+        if (K > 0)
+          for (int k = 0; k < 3 * K; ++k) grads[(11 + k) * P + id] = static_cast<float>(dsh[k]);
+      }
+    }
+  }
+  // deterministic block reduction of the pose pieces
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    const double t = warp_sum_d(pose[a]);
+    if (lane == 0) s_red[warp][a] = t;
+  }
+  __syncthreads();
+  if (tid < 6) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s_red[w][tid];
+    pose_part[static_cast<size_t>(blockIdx.x) * 6 + tid] = t;
+  }
+}
+
+__global__ void k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds) {
+  __shared__ double s_red[8][6];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = tid; b < blocks; b += blockDim.x)
+    for (int a = 0; a < 6; ++a) acc[a] += pose_part[static_cast<size_t>(b) * 6 + a];
+  for (int a = 0; a < 6; ++a) {
+    const double t = warp_sum_d(acc[a]);
+    if (lane == 0) s_red[warp][a] = t;
+  }
+  __syncthreads();
+  if (tid < 6) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += s_red[w][tid];
+    ds->d_pose[tid] = ds->halt ? 0.0 : t;
+  }
+}
+
+template <int SEED>
+__global__ void k_seeds_out(int64_t npix, const float* __restrict__ color, const float* __restrict__ ad,
+                            const float* __restrict__ md, const uint8_t* __restrict__ mv, const float* __restrict__ op,
+                            const float* __restrict__ target, const float* __restrict__ depth, const float* __restrict__ dssim,
+                            const DevState* ds, LossParams lp, double near_plane, double far_plane, float* __restrict__ out) {
+  const int64_t pi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (pi >= npix) return;
+  const PixSeeds s = seeds_pixel<SEED>(pi, color, ad[pi], md[pi], mv[pi] != 0, op[pi], target, depth, dssim, ds, lp,
+                                       near_plane, far_plane);
+  out[3 * pi] = s.gc0;
+  out[3 * pi + 1] = s.gc1;
+  out[3 * pi + 2] = s.gc2;
+  out[3 * npix + pi] = s.gad;
+  out[4 * npix + pi] = s.gmd;
+  out[5 * npix + pi] = s.gu;
+}
+
+}  // namespace
+
+void run_seeds_out(Workspace& ws, DevState* ds, int mode, const float* target, const float* depth, const LossParams& lp,
+                   int W, int H, double near_plane, double far_plane, float* out, cudaStream_t st, int64_t* L) {
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  const float* dssim = (mode == 2 && lp.w_ssim > 0.0) ? ws.dssim : nullptr;
+  if (mode == 1)
+    k_seeds_out<1><<<div_up(npix, 256), 256, 0, st>>>(npix, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
+                                                       ws.opacity, target, depth, dssim, ds, lp, near_plane, far_plane, out);
+  else
+    k_seeds_out<2><<<div_up(npix, 256), 256, 0, st>>>(npix, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
+                                                       ws.opacity, target, depth, dssim, ds, lp, near_plane, far_plane, out);
+  ++*L;
+}
+
+void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st, int64_t* L) {
+  const int ntiles = a.rp.tiles_x * a.rp.tiles_y;
+  BwdPtrs bp;
+  bp.ranges = ws.ranges;
+  bp.sorted_orig = ws.pair_sorted_vals;
+  bp.pair_rank = ws.pair_rank;
+  bp.bg = ws.bg;
+  bp.gg = ws.gg;
+  bp.rank_to_id = ws.rank_to_id;
+  bp.color = ws.color;
+  bp.alpha_depth = ws.alpha_depth;
+  bp.median_depth = ws.median_depth;
+  bp.median_valid = ws.median_valid;
+  bp.opacity = ws.opacity;
+  bp.final_T = ws.final_T;
+  bp.last = ws.last;
+  bp.median_prim = ws.median_prim;
+  bp.obs = a.obs;
+  bp.target = a.target_rgb;
+  bp.up_color = a.up_color;
+  bp.up_adepth = a.up_adepth;
+  bp.up_mdepth = a.up_mdepth;
+  bp.up_opacity = a.up_opacity;
+  bp.up_uncert = a.up_uncert;
+  bp.dssim = (a.seed_mode == SEED_MAP && a.lp.w_ssim > 0.0) ? ws.dssim : nullptr;
+  bp.partials = ws.partials;
+  const bool view_dep = a.K > 1;
+  const int nf = a.pose_only ? (view_dep ? 9 : 6) : 10;
+  if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
+#define GSF_BWD(SM, NFV) k_backward<SM, NFV><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds)
+  if (a.seed_mode == SEED_TRACK) {
+    if (nf == 6) GSF_BWD(SEED_TRACK, 6); else if (nf == 9) GSF_BWD(SEED_TRACK, 9); else GSF_BWD(SEED_TRACK, 10);
+  } else if (a.seed_mode == SEED_MAP) {
+    if (nf == 6) GSF_BWD(SEED_MAP, 6); else if (nf == 9) GSF_BWD(SEED_MAP, 9); else GSF_BWD(SEED_MAP, 10);
+  } else {
+    if (nf == 6) GSF_BWD(SEED_EXPLICIT, 6); else if (nf == 9) GSF_BWD(SEED_EXPLICIT, 9); else GSF_BWD(SEED_EXPLICIT, 10);
+  }
+#undef GSF_BWD
+  ++*L;
+  if (ws.prof) ws.prof->end(st);
+  if (ws.prof) ws.prof->begin(PROF_CHAIN, st);
+  const uint32_t Pcap = static_cast<uint32_t>(a.P);
+  const int blocks = std::max(1, div_up(a.P, 256));
+  const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
+  if (nf == 6)
+    k_chain<6, false><<<blocks, 256, 0, st>>>(ws.pair_off, ws.partials, ws.rank_to_id, ds, Pcap, pair_cap, a.params, a.P, a.K,
+                                             a.grads, a.d_mean2d, ws.pose_part);
+  else if (nf == 9)
+    k_chain<9, false><<<blocks, 256, 0, st>>>(ws.pair_off, ws.partials, ws.rank_to_id, ds, Pcap, pair_cap, a.params, a.P, a.K,
+                                             a.grads, a.d_mean2d, ws.pose_part);
+  else
+    k_chain<10, true><<<blocks, 256, 0, st>>>(ws.pair_off, ws.partials, ws.rank_to_id, ds, Pcap, pair_cap, a.params, a.P, a.K,
+                                             a.grads, a.d_mean2d, ws.pose_part);
+  ++*L;
+  k_pose_sum<<<1, 256, 0, st>>>(ws.pose_part, blocks, ds);
+  ++*L;
+  if (ws.prof) ws.prof->end(st);
+}
+
+}  // namespace gsfk

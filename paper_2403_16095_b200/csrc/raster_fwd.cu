@@ -1,0 +1,335 @@
+// raster_fwd.cu — forward pass of the tile rasterizer on sm_100a.
+//
+//   k_preprocess   project_all (rasterizer.cpp:46-67) + validate_primitives (:34-44), fp64,
+//                  one thread per primitive, SoA fp32 parameter reads (coalesced per field)
+//   scan/compact   visible ids in id order (input of the stable depth sort)
+//   sort + fixup   sorted_visible (:69-79)
+//   k_gather       rank-ordered blend records (3 x float4 per primitive) + tile counts
+//   scan           pair offsets; k_duplicate writes (tile id, rank) pairs in rank order
+//   sort           stable by tile id -> every tile list in global depth order (:193-212)
+//   k_ranges       [start, end) per tile
+//   k_blend        blend_pixel (:96-140) for a 16x16 tile per 256-thread CTA with the tile
+//                  list staged through shared memory, plus the fused loss epilogue
+//                  (losses.cpp:156-339: masks, residual sums and counts per tile)
+#include "kernels.h"
+#include "pixel_loss.cuh"
+
+namespace gsfk {
+
+namespace {
+
+__global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ params, int64_t P, const DevState* ds,
+                                                    RasterParams rp, uint32_t near_bits, uint32_t* __restrict__ flag,
+                                                    uint32_t* __restrict__ key_id, BlendG* __restrict__ bg_id,
+                                                    GuardG* __restrict__ gg_id, double* __restrict__ depth_id,
+                                                    int4* __restrict__ rect_id, uint8_t* __restrict__ visible,
+                                                    int32_t* bad_index) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  // validate_primitives (rasterizer.cpp:34-44): every field finite and |q| > 1e-12
+  const int D = kFieldsBase + 3 * rp.sh_coeffs;
+  bool ok = true;
+  for (int f = 0; f < D; ++f) ok = ok && isfinite(params[f * P + i]);
+  if (ok) {
+    const double qw = params[6 * P + i], qx = params[7 * P + i], qy = params[8 * P + i], qz = params[9 * P + i];
+    ok = dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz))) > 1e-12;
+  }
+  if (!ok) {
+    atomicMin(bad_index, static_cast<int32_t>(i));
+    flag[i] = 0u;
+    visible[i] = 0;
+    return;
+  }
+  const PreOut o = preprocess_one(params + i, P, ds->cam, rp);
+  visible[i] = static_cast<uint8_t>(o.visible);
+  flag[i] = static_cast<uint32_t>(o.visible);
+  if (!o.visible) return;
+  key_id[i] = depth_key(o.depth, near_bits);
+  bg_id[i] = make_blend_g(o);
+  gg_id[i] = make_guard_g(o);
+  depth_id[i] = o.depth;
+  rect_id[i] = make_int4(o.tx0, o.tx1, o.ty0, o.ty1);
+}
+
+__global__ void k_compact(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ off,
+                          const uint32_t* __restrict__ key_id, int64_t P, uint32_t* __restrict__ keys,
+                          uint32_t* __restrict__ vals) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P || !flag[i]) return;
+  const uint32_t pos = off[i];
+  keys[pos] = key_id[i];
+  vals[pos] = static_cast<uint32_t>(i);
+}
+
+__global__ void k_gather(const uint32_t* __restrict__ sorted_ids, const uint32_t* n_dev, uint32_t n_cap,
+                         const BlendG* __restrict__ bg_id, const GuardG* __restrict__ gg_id,
+                         const int4* __restrict__ rect_id, int32_t* __restrict__ rank_to_id, BlendG* __restrict__ bg,
+                         GuardG* __restrict__ gg, int4* __restrict__ rect, uint32_t* __restrict__ tile_cnt) {
+  const uint32_t n = min(*n_dev, n_cap);
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t id = sorted_ids[r];
+  rank_to_id[r] = static_cast<int32_t>(id);
+  bg[r] = bg_id[id];
+  gg[r] = gg_id[id];
+  const int4 q = rect_id[id];
+  rect[r] = q;
+  tile_cnt[r] = static_cast<uint32_t>((q.y - q.x + 1) * (q.w - q.z + 1));
+}
+
+__global__ void k_duplicate(const int4* __restrict__ rect, const uint32_t* __restrict__ pair_off, const uint32_t* n_dev,
+                            uint32_t n_cap, const uint32_t* m_dev, uint32_t pair_cap, int tiles_x,
+                            uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pair_rank, uint32_t* overflow) {
+  const uint32_t n = min(*n_dev, n_cap);
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0 && *m_dev > pair_cap) *overflow = 1u;
+  if (r >= n) return;
+  const int4 q = rect[r];
+  uint32_t pos = pair_off[r];
+  for (int ty = q.z; ty <= q.w; ++ty)
+    for (int tx = q.x; tx <= q.y; ++tx) {
+      if (pos < pair_cap) {
+        pkeys[pos] = static_cast<uint32_t>(ty * tiles_x + tx);
+        pair_rank[pos] = r;
+      }
+      ++pos;
+    }
+}
+
+__global__ void k_ranges(const uint32_t* __restrict__ keys, const uint32_t* m_dev, uint32_t cap, int2* ranges) {
+  const uint32_t n = min(*m_dev, cap);
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t t = keys[s];
+  if (s == 0 || keys[s - 1] != t) ranges[t].x = static_cast<int>(s);
+  if (s + 1 == n || keys[s + 1] != t) ranges[t].y = static_cast<int>(s + 1);
+}
+
+__device__ __forceinline__ bool depth_valid(float d, double near_plane, double far_plane) {
+  const double v = d;
+  return isfinite(v) && v > near_plane && v < far_plane;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int LMODE>
+__global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sorted_orig,
+                                               const uint32_t* __restrict__ pair_rank, const BlendG* __restrict__ bg,
+                                               const GuardG* __restrict__ gg, const int32_t* __restrict__ rank_to_id,
+                                               const float* __restrict__ obs, const float* __restrict__ loss_rgb,
+                                               const float* __restrict__ loss_depth, int W, int H, int tiles_x,
+                                               BlendConsts kc, double near_plane, double far_plane, LossParams lp,
+                                               const DevState* ds, float* __restrict__ o_color, float* __restrict__ o_ad,
+                                               float* __restrict__ o_md, uint8_t* __restrict__ o_mv,
+                                               float* __restrict__ o_op, float* __restrict__ o_unc,
+                                               float* __restrict__ o_T, int32_t* __restrict__ o_count,
+                                               int32_t* __restrict__ o_dom, int32_t* __restrict__ o_med,
+                                               float* __restrict__ o_domw, int32_t* __restrict__ o_last,
+                                               double* __restrict__ loss_part) {
+  __shared__ BlendG s_g[256];
+  __shared__ int32_t s_rank[256];
+  __shared__ int32_t s_id[256];
+  __shared__ double s_red[8][LS_NUM];
+  if (ds->halt) return;
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int x = tx * kTile + (tid & 15), y = ty * kTile + (tid >> 4);
+  const bool inside = x < W && y < H;
+  const int64_t pi = static_cast<int64_t>(y) * W + x;
+  const int2 rg = ranges[tile];
+  PixelState s;
+  pixel_init(s);
+  if (!inside) s.done = 1;
+  bool obs_valid = false;
+  float ov = 0.0f;
+  if (obs && inside) {
+    ov = obs[pi];
+    obs_valid = depth_valid(ov, near_plane, far_plane);
+  }
+  const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
+  for (int start = rg.x; start < rg.y; start += 256) {
+    if (__syncthreads_and(s.done)) break;
+    const int j = start + tid;
+    if (j < rg.y) {
+      const int r = static_cast<int>(pair_rank[sorted_orig[j]]);
+      s_g[tid] = bg[r];
+      s_rank[tid] = r;
+      s_id[tid] = rank_to_id[r];
+    }
+    __syncthreads();
+    const int cnt = min(256, rg.y - start);
+    for (int k = 0; k < cnt && !s.done; ++k) {
+      const BlendG g = s_g[k];
+      const PairEval e = eval_pair(px, py, g, gg + s_rank[k], kc);
+      if (e.code) pixel_accumulate(s, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+    }
+  }
+  if (inside) {
+    o_color[3 * pi + 0] = s.cr;
+    o_color[3 * pi + 1] = s.cg;
+    o_color[3 * pi + 2] = s.cb;
+    o_ad[pi] = s.ad;
+    o_md[pi] = s.med_depth;
+    o_mv[pi] = s.median >= 0 ? 1 : 0;
+    o_op[pi] = s.op;
+    o_unc[pi] = s.unc;
+    o_T[pi] = s.T;
+    o_count[pi] = s.count;
+    o_dom[pi] = s.dominant;
+    o_med[pi] = s.median;
+    o_domw[pi] = s.best;
+    o_last[pi] = s.last;
+  }
+  if (LMODE == 0) return;
+  // fused loss epilogue: per-tile residual sums and mask counts (deterministic tree)
+  double v[LS_NUM];
+#pragma unroll
+  for (int q = 0; q < LS_NUM; ++q) v[q] = 0.0;
+  if (inside)
+    loss_pixel<LMODE>(v, s.cr, s.cg, s.cb, s.ad, s.med_depth, s.median >= 0, s.op, s.unc, loss_rgb + 3 * pi, loss_depth, pi,
+                      obs != nullptr, near_plane, far_plane, lp.opacity_floor);
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int q = 0; q < LS_NUM; ++q) {
+    const double t = warp_sum_d(v[q]);
+    if (lane == 0) s_red[warp][q] = t;
+  }
+  __syncthreads();
+  if (tid < LS_NUM) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s_red[w][tid];
+    loss_part[static_cast<int64_t>(tile) * LS_NUM + tid] = t;
+  }
+}
+
+// Stand-alone loss partials over stored maps (evaluate_*_loss called on a RenderResult).
+template <int LMODE>
+__global__ void __launch_bounds__(256) k_loss_tiles(const float* __restrict__ color, const float* __restrict__ ad,
+                                                    const float* __restrict__ md, const uint8_t* __restrict__ mv,
+                                                    const float* __restrict__ op, const float* __restrict__ unc,
+                                                    const float* __restrict__ rgb, const float* __restrict__ depth, int W,
+                                                    int H, int tiles_x, bool has_unc, double near_plane, double far_plane,
+                                                    float floor, double* __restrict__ loss_part) {
+  __shared__ double s_red[8][LS_NUM];
+  const int tile = blockIdx.x, tid = threadIdx.x;
+  const int x = (tile % tiles_x) * kTile + (tid & 15), y = (tile / tiles_x) * kTile + (tid >> 4);
+  double v[LS_NUM];
+#pragma unroll
+  for (int q = 0; q < LS_NUM; ++q) v[q] = 0.0;
+  if (x < W && y < H) {
+    const int64_t pi = static_cast<int64_t>(y) * W + x;
+    loss_pixel<LMODE>(v, color[3 * pi], color[3 * pi + 1], color[3 * pi + 2], ad[pi], md[pi], mv[pi] != 0, op[pi], unc[pi],
+                      rgb + 3 * pi, depth, pi, has_unc, near_plane, far_plane, floor);
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int q = 0; q < LS_NUM; ++q) {
+    const double t = warp_sum_d(v[q]);
+    if (lane == 0) s_red[warp][q] = t;
+  }
+  __syncthreads();
+  if (tid < LS_NUM) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s_red[w][tid];
+    loss_part[static_cast<int64_t>(tile) * LS_NUM + tid] = t;
+  }
+}
+
+int bits_for(uint32_t max_value) {
+  int b = 0;
+  while (b < 32 && (max_value >> b) != 0) ++b;
+  return b;
+}
+
+}  // namespace
+
+void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* L) {
+  const int64_t P = a.P;
+  const uint32_t Pn = static_cast<uint32_t>(P);
+  const int tiles_x = a.rp.tiles_x, tiles_y = a.rp.tiles_y;
+  const int ntiles = tiles_x * tiles_y;
+  const uint32_t near_bits = static_cast<uint32_t>(fbits(static_cast<float>(a.near_plane)));
+  const uint32_t far_key = static_cast<uint32_t>(fbits(static_cast<float>(a.far_plane))) - near_bits;
+  const int depth_bits = std::max(1, bits_for(far_key));
+  const int tile_bits = std::max(1, bits_for(static_cast<uint32_t>(ntiles - 1)));
+  const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
+
+  Profiler* pf = ws.prof;
+  if (pf) pf->begin(PROF_PREPROCESS, st);
+  if (P > 0) {
+    k_preprocess<<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, near_bits, ws.flag, ws.key_id, ws.bg_id, ws.gg_id,
+                                                 ws.depth_id, ws.rect_id, ws.visible, &ds->bad_index);
+    ++*L;
+  }
+  if (pf) pf->end(st);
+  if (pf) pf->begin(PROF_SORT, st);
+  launch_scan_excl(ws.flag, ws.vis_off, nullptr, Pn, &ds->V, ws.scan, st, L);
+  if (P > 0) {
+    k_compact<<<div_up(P, 256), 256, 0, st>>>(ws.flag, ws.vis_off, ws.key_id, P, ws.skeys[0], ws.svals[0]);
+    ++*L;
+  }
+  const int dpass = radix_sort_u32(ws.skeys[0], ws.svals[0], ws.skeys[1], ws.svals[1], &ds->V, Pn, 0, depth_bits, false,
+                                   ws.radix_temp, st, L);
+  uint32_t* dkeys = (dpass & 1) ? ws.skeys[1] : ws.skeys[0];
+  uint32_t* dvals = (dpass & 1) ? ws.svals[1] : ws.svals[0];
+  ws.depth_sorted_vals = dvals;
+  launch_sort_fixup(dkeys, dvals, ws.depth_id, &ds->V, Pn, st, L);
+  if (P > 0) {
+    k_gather<<<div_up(P, 256), 256, 0, st>>>(dvals, &ds->V, Pn, ws.bg_id, ws.gg_id, ws.rect_id, ws.rank_to_id, ws.bg, ws.gg,
+                                             ws.rect, ws.tile_cnt);
+    ++*L;
+  }
+  launch_scan_excl(ws.tile_cnt, ws.pair_off, &ds->V, Pn, &ds->M, ws.scan, st, L);
+  if (P > 0) {
+    k_duplicate<<<div_up(P, 256), 256, 0, st>>>(ws.rect, ws.pair_off, &ds->V, Pn, &ds->M, pair_cap, tiles_x, ws.pkeys[0],
+                                                ws.pair_rank, &ds->overflow);
+    ++*L;
+  }
+  const int ppass = radix_sort_u32(ws.pkeys[0], ws.pvals[0], ws.pkeys[1], ws.pvals[1], &ds->M, pair_cap, 0, tile_bits, true,
+                                   ws.radix_temp, st, L);
+  ws.pair_sorted_keys = (ppass & 1) ? ws.pkeys[1] : ws.pkeys[0];
+  ws.pair_sorted_vals = (ppass & 1) ? ws.pvals[1] : ws.pvals[0];
+  if (pf) pf->end(st);
+  GSF_CUDA_CHECK(cudaMemsetAsync(ws.ranges, 0, sizeof(int2) * ntiles, st));
+  k_ranges<<<div_up(std::max<int64_t>(pair_cap, 1), 256), 256, 0, st>>>(ws.pair_sorted_keys, &ds->M, pair_cap, ws.ranges);
+  ++*L;
+  const float* loss_rgb = a.loss_rgb;
+#define GSF_BLEND_ARGS                                                                                                 \
+  ws.ranges, ws.pair_sorted_vals, ws.pair_rank, ws.bg, ws.gg, ws.rank_to_id, a.obs, loss_rgb, a.loss_depth, a.W, a.H, \
+      tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid, \
+      ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w, ws.last, ws.loss_part
+  if (pf) pf->begin(PROF_BLEND, st);
+  if (a.lp.mode == 1 && loss_rgb)
+    k_blend<1><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
+  else if (a.lp.mode == 2 && loss_rgb)
+    k_blend<2><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
+  else
+    k_blend<0><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
+#undef GSF_BLEND_ARGS
+  ++*L;
+  if (pf) pf->end(st);
+  (void)tiles_y;
+}
+
+void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,
+                    double near_plane, double far_plane, float floor, cudaStream_t st, int64_t* L) {
+  const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
+  if (mode == 1)
+    k_loss_tiles<1><<<tiles_x * tiles_y, 256, 0, st>>>(ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid, ws.opacity,
+                                                        ws.uncertainty, rgb, depth, W, H, tiles_x, has_unc, near_plane,
+                                                        far_plane, floor, ws.loss_part);
+  else
+    k_loss_tiles<2><<<tiles_x * tiles_y, 256, 0, st>>>(ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid, ws.opacity,
+                                                        ws.uncertainty, rgb, depth, W, H, tiles_x, has_unc, near_plane,
+                                                        far_plane, floor, ws.loss_part);
+  ++*L;
+}
+
+}  // namespace gsfk

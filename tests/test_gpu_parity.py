@@ -1,0 +1,348 @@
+"""GPU parity: the sm_100a path (libgsf_cuda.so through the C-ABI) against the CPU oracle.
+
+Bar:
+  * bit-exact vs the fp32 mirror (oracle/mirror.cpp): visible flags, global depth order, tile
+    ranges, tile lists, per-pixel contributor counts, dominant / median ids and the fp32 maps;
+  * vs the fp64 restatement (oracle/gsf_oracle.cpp): maps within 1e-4 (abs, values are O(1)),
+    integer outputs identical, gradients within |g - g_ref| <= 1e-4 * max(|g_ref|, 1e-3 * max|g_ref|)
+    and the pose 6-vector within 1e-4 relative.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2403_16095_b200 import api
+from paper_2403_16095_b200.abi import defaults_mapper, defaults_raster, defaults_tracker, defaults_weights
+from helpers import (axis_primitive, f32_round, golden, make_intrinsics, one_pixel_camera, perturbed, pose,
+                     rotation_error, scene, to_api_map, translation_error)
+
+pytestmark = pytest.mark.gpu
+
+MAP_TOL = 1e-4
+
+
+def _upload(ctx, m):
+    ctx.upload(to_api_map(m))
+
+
+def _grad_close(g, ref, rel=1e-4, name=""):
+    g = np.asarray(g, np.float64).ravel()
+    ref = np.asarray(ref, np.float64).ravel()
+    if ref.size == 0:
+        return
+    scale = np.maximum(np.abs(ref), 1e-3 * np.abs(ref).max() + 1e-30)
+    err = np.abs(g - ref) / scale
+    assert err.max() <= rel, f"{name}: worst rel err {err.max():.3e} at {err.argmax()} ({g[err.argmax()]} vs {ref[err.argmax()]})"
+
+
+def test_two_primitive_kat_on_gpu(gpu_ctx, orc):
+    """test_rasterizer.cpp:39-63 through the CUDA path."""
+    e = golden("reference_kats.json")["two_primitive_pixel"]["expect"]
+    m = scene([axis_primitive(1.0, 0.6, [1, 0, 0]), axis_primitive(2.0, 0.8, [0, 1, 0])])
+    _upload(gpu_ctx, m)
+    r = gpu_ctx.render(pose(), one_pixel_camera(), np.array([[1.0]]))
+    assert np.allclose(r.color[0, 0], e["color"], atol=1e-6)
+    assert r.opacity[0, 0] == pytest.approx(e["opacity"], abs=1e-6)
+    assert r.alpha_depth[0, 0] == pytest.approx(e["alpha_depth"], abs=1e-6)
+    assert r.uncertainty[0, 0] == pytest.approx(e["uncertainty"], abs=1e-6)
+    assert r.final_transmittance[0, 0] == pytest.approx(e["final_transmittance"], abs=1e-7)
+    assert r.median_valid[0, 0] == 1 and r.median_depth[0, 0] == pytest.approx(1.0)
+    assert r.per_pixel_count[0, 0] == 2 and r.dominant[0, 0] == 0 and r.median_prim[0, 0] == 0
+    rs, prim, alpha, tr = gpu_ctx.render_record_full(1)
+    assert list(prim) == [0, 1] and tr[1] == pytest.approx(0.4, abs=1e-7)
+
+
+def test_empty_and_errors(gpu_ctx, orc):
+    """test_rasterizer.cpp:65-99 + the EUNSUPPORTED path for non-16 tiles."""
+    _upload(gpu_ctx, scene([]))
+    r = gpu_ctx.render(pose(), make_intrinsics(16, 12, 20.0))
+    assert (r.opacity == 0).all() and (r.per_pixel_count == 0).all() and (r.final_transmittance == 1).all()
+    m = orc.random_scene(3, 5)
+    m.mean[3, 1] = float("nan")
+    _upload(gpu_ctx, m)
+    with pytest.raises(ValueError) as ei:
+        gpu_ctx.render(pose(), make_intrinsics(8, 8, 10.0))
+    assert "primitive 3 has non-finite" in str(ei.value) and ei.value.index == 3
+    _upload(gpu_ctx, orc.random_scene(4, 3))
+    with pytest.raises(ValueError):
+        gpu_ctx.render(pose(), make_intrinsics(8, 8, 10.0), np.ones((4, 4)))
+    cfg = defaults_raster()
+    cfg.tile_size = 8
+    with pytest.raises(NotImplementedError):
+        gpu_ctx.render(pose(), make_intrinsics(8, 8, 10.0), cfg=cfg)
+
+
+def _scene_cases(orc):
+    rng = np.random.default_rng(5)
+    for seed in range(12):
+        m = f32_round(orc.random_scene(100 + seed, 200, 4 if seed % 3 == 0 else 1))
+        K = make_intrinsics(64, 64, 60.0) if seed % 2 == 0 else make_intrinsics(50, 34, 40.0)
+        obs = orc.wavy_depth(K.width, K.height, 2.5).astype(np.float32)
+        p = pose(0.03 * rng.standard_normal(3), 0.05 * rng.standard_normal(3))
+        yield seed, m, K, obs, p
+
+
+def test_forward_bit_exact_vs_mirror(gpu_ctx, orc):
+    """Keys/order/ranges/lists/counts/ids and fp32 maps identical to the fp32 mirror."""
+    for seed, m, K, obs, p in _scene_cases(orc):
+        _upload(gpu_ctx, m)
+        r = gpu_ctx.render(p, K, obs)
+        mr = orc.mirror_render(m, p, K, obs)
+        assert r.num_visible == mr.num_visible and r.num_pairs == mr.num_pairs, seed
+        assert (r.visible == mr.visible).all()
+        ntiles = ((K.width + 15) // 16) * ((K.height + 15) // 16)
+        r2i, tr, pr = gpu_ctx.render_tiles(r.num_visible, ntiles, r.num_pairs)
+        assert (r2i == mr.rank_to_id).all(), seed
+        assert (tr.ravel() == mr.tile_range).all(), seed
+        assert (pr == mr.pair_rank).all(), seed
+        for k in ("per_pixel_count", "dominant", "median_prim", "median_valid"):
+            assert (getattr(r, k) == getattr(mr, k)).all(), (seed, k)
+        for k in ("color", "alpha_depth", "median_depth", "opacity", "uncertainty", "final_transmittance",
+                  "dominant_weight"):
+            assert np.array_equal(getattr(r, k), getattr(mr, k)), (seed, k)
+
+
+def test_forward_vs_fp64_oracle(gpu_ctx, orc):
+    """Maps within 1e-4 of the fp64 reference restatement; integer outputs identical."""
+    for seed, m, K, obs, p in _scene_cases(orc):
+        _upload(gpu_ctx, m)
+        r = gpu_ctx.render(p, K, obs)
+        o = orc.render(m, p, K, obs.astype(np.float64))
+        assert (r.visible == o.visible).all(), seed
+        for k in ("per_pixel_count", "dominant", "median_prim", "median_valid"):
+            mism = int((getattr(r, k) != getattr(o, k)).sum())
+            assert mism == 0, (seed, k, mism)
+        for k in ("color", "alpha_depth", "opacity", "uncertainty", "final_transmittance"):
+            assert np.abs(getattr(r, k) - getattr(o, k)).max() < MAP_TOL, (seed, k)
+        md = np.where(o.median_valid == 1, r.median_depth - o.median_depth, 0)
+        assert np.abs(md).max() < MAP_TOL
+
+
+def test_record_matches_oracle(gpu_ctx, orc):
+    """BlendRecord CSR (rasterizer.cpp:240-259) from the device equals the oracle's."""
+    seed, m, K, obs, p = next(iter(_scene_cases(orc)))
+    _upload(gpu_ctx, m)
+    gpu_ctx.render(p, K, obs)
+    rs, prim, alpha, tr = gpu_ctx.render_record_full(K.width * K.height)
+    o = orc.render(m, p, K, obs.astype(np.float64))
+    ors, oprim, oalpha, otr = o.record()
+    assert (rs == ors).all() and (prim == oprim).all()
+    assert np.abs(alpha - oalpha).max() < 1e-6 and np.abs(tr - otr).max() < 1e-5
+
+
+def _probe(rng, w, h, with_unc):
+    return (rng.standard_normal((h, w, 3)), rng.standard_normal((h, w)), rng.standard_normal((h, w)),
+            rng.standard_normal((h, w)) if with_unc else None, rng.standard_normal((h, w)))
+
+
+@pytest.mark.parametrize("sh", [1, 4, 16])
+def test_backward_vs_fp64_oracle(gpu_ctx, orc, sh):
+    """render_backward (rasterizer.cpp:339-572) with linear-probe upstream maps."""
+    rng = np.random.default_rng(sh)
+    for seed in range(4):
+        m = f32_round(orc.random_scene(2000 + seed, 150, sh))
+        K = make_intrinsics(48, 40, 45.0)
+        obs = orc.wavy_depth(48, 40, 2.5).astype(np.float32)
+        p = pose(0.02 * rng.standard_normal(3), 0.03 * rng.standard_normal(3))
+        a_c, a_d, a_o, a_u, a_m = [None if a is None else a.astype(np.float32).astype(np.float64)
+                                   for a in _probe(rng, 48, 40, True)]
+        _upload(gpu_ctx, m)
+        gpu_ctx.render(p, K, obs)
+        g = gpu_ctx.render_backward(a_c, a_d, a_m, a_o, a_u, obs)
+        o = orc.render(m, p, K, obs.astype(np.float64))
+        go = orc.render_backward(m, p, K, o, a_c, a_d, a_m, a_o, a_u, obs.astype(np.float64))
+        for k in ("d_mean", "d_log_scale", "d_quat", "d_opacity_logit", "d_sh", "d_mean2d"):
+            _grad_close(getattr(g, k), getattr(go, k), name=f"{k} seed {seed}")
+        _grad_close(g.d_pose, go.d_pose, name="d_pose")
+
+
+def test_backward_zero_upstream(gpu_ctx, orc):
+    _upload(gpu_ctx, f32_round(orc.random_scene(7, 10)))
+    gpu_ctx.render(pose(), make_intrinsics(16, 16, 15.0))
+    g = gpu_ctx.render_backward()
+    assert (g.d_pose == 0).all() and (g.d_mean == 0).all() and (g.d_quat == 0).all()
+
+
+def test_backward_deterministic(gpu_ctx, orc):
+    """test_gradients.cpp:181-206: bit-identical repeats (no float atomics on the device path)."""
+    m = f32_round(orc.random_scene(11, 80))
+    K = make_intrinsics(40, 28, 35.0)
+    obs = orc.wavy_depth(40, 28, 2.5).astype(np.float32)
+    rng = np.random.default_rng(12)
+    probe = _probe(rng, 40, 28, True)
+    _upload(gpu_ctx, m)
+    gpu_ctx.render(pose(), K, obs)
+    a = gpu_ctx.render_backward(*probe[:2], probe[4], probe[2], probe[3], obs)
+    gpu_ctx.render(pose(), K, obs)
+    b = gpu_ctx.render_backward(*probe[:2], probe[4], probe[2], probe[3], obs)
+    assert np.array_equal(a.d_pose, b.d_pose) and np.array_equal(a.d_mean, b.d_mean)
+    assert np.array_equal(a.d_quat, b.d_quat) and np.array_equal(a.d_opacity_logit, b.d_opacity_logit)
+
+
+def test_symmetric_scene_zero_lateral_pose_gradient(gpu_ctx, orc):
+    """test_gradients.cpp:164-179"""
+    m = scene([dict(mean=[0, 0, 2.0], scale=0.08, opacity=0.7, sh=[[0.3, 0.1, -0.2]])])
+    _upload(gpu_ctx, f32_round(m))
+    gpu_ctx.render(pose(), make_intrinsics(33, 33, 30.0))
+    g = gpu_ctx.render_backward(d_opacity=np.ones((33, 33)))
+    assert abs(g.d_pose[3]) < 1e-8 and abs(g.d_pose[4]) < 1e-8
+
+
+def test_tracking_loss_vs_oracle(gpu_ctx, orc):
+    """evaluate_tracking_loss (losses.cpp:284-339)"""
+    m = f32_round(orc.random_scene(41, 60))
+    K = make_intrinsics(48, 36, 40.0)
+    rng = np.random.default_rng(3)
+    target = rng.random((36, 48, 3)).astype(np.float32)
+    depth = orc.wavy_depth(48, 36, 2.5).astype(np.float32)
+    _upload(gpu_ctx, m)
+    gpu_ctx.render(pose(), K)
+    out, dc, dd = gpu_ctx.evaluate_tracking_loss(target, depth, defaults_weights(True))
+    o = orc.render(m, pose(), K)
+    oo, odc, odd = orc.tracking_loss(o, target.astype(np.float64), depth.astype(np.float64), K, defaults_weights(True))
+    assert out.valid_color == oo.valid_color and out.valid_geo == oo.valid_geo
+    assert out.total == pytest.approx(oo.total, rel=1e-5)
+    assert np.abs(dc - odc).max() < 1e-7 and np.abs(dd - odd).max() < 1e-7
+
+
+def test_mapping_loss_kat_on_gpu(gpu_ctx, orc):
+    """test_losses.cpp:169-198 through the CUDA path."""
+    e = golden("reference_kats.json")["mapping_loss_single_pixel"]["expect"]
+    m = scene([axis_primitive(1.0, 0.6, [1, 0, 0]), axis_primitive(2.0, 0.8, [0, 1, 0])])
+    _upload(gpu_ctx, m)
+    obs = np.array([[1.0]], np.float32)
+    r = gpu_ctx.render(pose(), one_pixel_camera(), obs)
+    out, (dc, dad, dmd, du, dls) = gpu_ctx.evaluate_mapping_loss(r.color, obs, defaults_weights())
+    assert out.geo == pytest.approx(e["geo"], abs=1e-6) and out.align == pytest.approx(e["align"], abs=1e-6)
+    assert out.var == pytest.approx(e["var"], abs=1e-6) and out.total == pytest.approx(e["total"], abs=1e-6)
+    assert dad[0] == pytest.approx(e["d_alpha_depth"], abs=1e-6) and dmd[0] == pytest.approx(e["d_median_depth"], abs=1e-6)
+    assert du[0] == pytest.approx(e["d_uncertainty"], abs=1e-6)
+
+
+def test_mapping_loss_vs_oracle(gpu_ctx, orc):
+    """evaluate_mapping_loss (losses.cpp:156-282) incl. SSIM and iso on a random scene."""
+    m = f32_round(orc.random_scene(37, 80))
+    K = make_intrinsics(48, 36, 40.0)
+    rng = np.random.default_rng(4)
+    target = rng.random((36, 48, 3)).astype(np.float32)
+    depth = orc.wavy_depth(48, 36, 2.5).astype(np.float32)
+    _upload(gpu_ctx, m)
+    gpu_ctx.render(pose(), K, depth)
+    out, (dc, dad, dmd, du, dls) = gpu_ctx.evaluate_mapping_loss(target, depth, defaults_weights())
+    o = orc.render(m, pose(), K, depth.astype(np.float64))
+    oo, (odc, odad, odmd, odu, odls) = orc.mapping_loss(m, o, target.astype(np.float64), depth.astype(np.float64), K,
+                                                        defaults_weights())
+    for k in ("color", "ssim", "geo", "align", "iso", "var", "total"):
+        assert getattr(out, k) == pytest.approx(getattr(oo, k), rel=1e-4, abs=1e-7), k
+    assert np.abs(dc - odc).max() < 1e-4 * np.abs(odc).max() + 1e-9
+    assert np.abs(dad - odad).max() < 1e-7 and np.abs(dmd - odmd).max() < 1e-7 and np.abs(du - odu).max() < 1e-7
+    _grad_close(dls, odls, name="iso direct")
+
+
+def test_ssim_vs_oracle(gpu_ctx, orc):
+    rng = np.random.default_rng(21)
+    for (w, h) in ((40, 30), (7, 5)):
+        x = rng.random((h, w, 3)).astype(np.float32)
+        y = rng.random((h, w, 3)).astype(np.float32)
+        v, g = gpu_ctx.ssim(x, y, w, h, want_gradient=True)
+        ov, og = orc.ssim(x.astype(np.float64), y.astype(np.float64), w, h, gradient=True)
+        assert v == pytest.approx(ov, rel=1e-5)
+        assert np.abs(g - og).max() < 1e-4 * np.abs(og).max()
+
+
+def _frames(ctx, orc, m, poses, K):
+    out = []
+    for i, p in enumerate(poses):
+        r = ctx.render(p, K)
+        out.append((r.color.copy(), r.alpha_depth.copy()))
+        ctx.frame_upload(i, r.color, r.alpha_depth, K.width, K.height)
+    return out
+
+
+def test_tracking_stationary_recovers_repeatable(gpu_ctx, orc):
+    """test_tracker.cpp:192-244 on the device loop, and the oracle's trajectory as a reference."""
+    K = make_intrinsics(48, 36, 40.0)
+    m = f32_round(orc.random_scene(7, 60))
+    _upload(gpu_ctx, m)
+    _frames(gpu_ctx, orc, m, [pose()], K)
+    tc = defaults_tracker()
+    tc.iterations = 10
+    res = gpu_ctx.track_frame(0, pose(), K, tc, defaults_weights(True))
+    assert np.linalg.norm(list(res.pose.rotation_tangent)) <= 1e-15 and res.final_loss == 0.0
+    assert not res.degraded and res.iterations_run == 10
+
+    K = make_intrinsics(64, 48, 55.0)
+    m = f32_round(orc.random_scene(19, 80))
+    _upload(gpu_ctx, m)
+    fr = _frames(gpu_ctx, orc, m, [pose()], K)
+    start = perturbed(pose(), [0.004, -0.003, 0.002, 0.008, -0.006, 0.004])
+    tc.iterations = 40
+    res = gpu_ctx.track_frame(0, start, K, tc, defaults_weights(True))
+    assert rotation_error(res.pose, pose()) < 0.35 * rotation_error(start, pose())
+    assert translation_error(res.pose, pose()) < 0.35 * translation_error(start, pose())
+    again = gpu_ctx.track_frame(0, start, K, tc, defaults_weights(True))
+    assert list(again.pose.translation) == list(res.pose.translation) and again.final_loss == res.final_loss
+    ores = orc.track_frame(m, fr[0][0], fr[0][1], start, K, tc, defaults_weights(True), defaults_raster())
+    assert rotation_error(res.pose, ores.pose) < 1e-4 and translation_error(res.pose, ores.pose) < 1e-4
+
+
+def test_tracking_empty_view_degraded(gpu_ctx, orc):
+    """test_tracker.cpp:246-263"""
+    _upload(gpu_ctx, f32_round(orc.random_scene(3, 30)))
+    K = make_intrinsics(32, 24, 28.0)
+    gpu_ctx.frame_upload(0, np.full((24, 32, 3), 0.5), orc.wavy_depth(32, 24, 2.0), 32, 24)
+    away = pose((math.pi, 0, 0))
+    res = gpu_ctx.track_frame(0, away, K, defaults_tracker(), defaults_weights(True))
+    assert res.degraded and res.iterations_run == 0
+
+
+def test_ba_noop_and_map_step(gpu_ctx, orc):
+    """test_tracker.cpp:319-363 (BA exact no-op at the optimum) and test_map.cpp:391-423."""
+    m = f32_round(orc.random_scene(31, 50))
+    K = make_intrinsics(48, 36, 40.0)
+    mc = defaults_mapper()
+    mc.weights.w_ssim = mc.weights.w_align = mc.weights.w_iso = mc.weights.w_var = 0.0
+    poses = [pose(), perturbed(pose(), [0.02, -0.01, 0.03, 0.05, 0.02, -0.04]),
+             perturbed(pose(), [-0.03, 0.02, -0.01, -0.04, 0.03, 0.05])]
+    _upload(gpu_ctx, m)
+    _frames(gpu_ctx, orc, m, poses, K)
+    trace, out_poses = gpu_ctx.sliding_ba([0, 1, 2], poses, [0, 10, 20], K, defaults_tracker(), mc, 5)
+    assert (trace == 0).all()
+    m2 = gpu_ctx.download()
+    assert np.array_equal(m2.mean, m.mean) and np.array_equal(m2.opacity_logit, m.opacity_logit)
+
+    K = make_intrinsics(48, 36, 40.0)
+    truth = f32_round(orc.random_scene(83, 40, 1, 0.95, 0.05, 0.2))
+    _upload(gpu_ctx, truth)
+    gt = gpu_ctx.render(pose(), K)
+    obs = np.where(gt.opacity > 0.5, gt.alpha_depth, 0.0).astype(np.float32)
+    gpu_ctx.frame_upload(0, gt.color, obs, 48, 36)
+    rng = np.random.default_rng(83)
+    pert = f32_round(truth)
+    pert.mean = (pert.mean + 0.02 * rng.standard_normal(pert.mean.shape)).astype(np.float32).astype(np.float64)
+    pert.sh[:, 0] = (pert.sh[:, 0] + 0.15 * rng.standard_normal((40, 3))).astype(np.float32).astype(np.float64)
+    mc = defaults_mapper()
+    mc.densify_interval = 0
+    _upload(gpu_ctx, pert)
+    trace = gpu_ctx.map_step([0], [pose()], K, mc, 60)
+    assert trace[-1] < 0.7 * trace[0]
+    st = orc.MapState(pert, mc)
+    otrace = st.map_step([(gt.color.astype(np.float64), obs.astype(np.float64))], [pose()], K, mc, 60)
+    assert trace[0] == pytest.approx(otrace[0], rel=1e-4)
+    assert trace[-1] == pytest.approx(otrace[-1], rel=2e-2)
+
+
+def test_uncertainty_kats_on_gpu(gpu_ctx, orc):
+    """test_map.cpp:118-155, 189-211 through the device uncertainty pass."""
+    K = one_pixel_camera()
+    m = scene([dict(mean=[0, 0, 1.5], scale=0.05, opacity=0.9, color=[0.5, 0.5, 0.5])])
+    _upload(gpu_ctx, m)
+    gpu_ctx.frame_upload(0, np.zeros(3), np.array([2.0]), 1, 1)
+    assert gpu_ctx.accumulate_uncertainty([0], [pose()], K) == 1
+    d = gpu_ctx.download()
+    assert d.uncertainty[0] == pytest.approx(0.225, rel=1e-6) and d.observed[0] == 1
+    assert gpu_ctx.prune_unreliable() == 1
+    d = gpu_ctx.download()
+    assert 1 / (1 + math.exp(-d.opacity_logit[0])) == pytest.approx(0.005, rel=1e-5)
+    assert gpu_ctx.prune_unreliable() == 0
