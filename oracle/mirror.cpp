@@ -72,9 +72,9 @@ extern "C" int mir_render(const gsf_map_host* map, const gsf_pose* pose, const g
   }
   int64_t total = 0;
   for (int t = 0; t < ntiles; ++t) {
-    if (out->tile_range) {
-      out->tile_range[2 * t] = static_cast<int32_t>(total);
-      out->tile_range[2 * t + 1] = static_cast<int32_t>(total + lists[t].size());
+    if (out->tile_range) {   // empty tiles are [0, 0), as the device's memset leaves them
+      out->tile_range[2 * t] = lists[t].empty() ? 0 : static_cast<int32_t>(total);
+      out->tile_range[2 * t + 1] = lists[t].empty() ? 0 : static_cast<int32_t>(total + lists[t].size());
     }
     for (size_t j = 0; j < lists[t].size(); ++j) {
       if (out->pair_rank && total + static_cast<int64_t>(j) < out->pair_capacity) out->pair_rank[total + j] = lists[t][j];

@@ -68,7 +68,9 @@ class GaussianMap:
         self.log_scale = np.ascontiguousarray(self.log_scale, dtype=np.float64).reshape(P, 3)
         self.quat = np.ascontiguousarray(self.quat, dtype=np.float64).reshape(P, 4)
         self.opacity_logit = np.ascontiguousarray(self.opacity_logit, dtype=np.float64).reshape(P)
-        self.sh = np.ascontiguousarray(self.sh, dtype=np.float64).reshape(P, -1, 3)
+        sh = np.ascontiguousarray(self.sh, dtype=np.float64)
+        k = sh.shape[1] if sh.ndim == 3 else (sh.size // max(P, 1) // 3 if P else 1)
+        self.sh = sh.reshape(P, k, 3)
         if self.uncertainty is None:
             self.uncertainty = np.zeros(P)
         self.uncertainty = np.ascontiguousarray(self.uncertainty, dtype=np.float64).reshape(P)
