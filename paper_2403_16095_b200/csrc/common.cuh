@@ -12,6 +12,12 @@ constexpr int kTile = 16;             // tile edge (RasterConfig::tile_size, con
 constexpr int kTilePixels = kTile * kTile;
 constexpr int kFieldsBase = 11;       // mean 3, log_scale 3, quat 4, opacity 1; then 3*K SH
 
+// Pixel of thread `tid` inside a 16x16 tile: each warp owns an 8x4 block (warp w -> block
+// column w & 1, block row w >> 1), which keeps a warp's pixels compact so that footprint
+// edges split fewer warps than 16x2 rows would.
+__host__ __device__ __forceinline__ int tile_lx(int tid) { return ((tid >> 5) & 1) * 8 + (tid & 7); }
+__host__ __device__ __forceinline__ int tile_ly(int tid) { return (tid >> 6) * 4 + ((tid >> 3) & 3); }
+
 // Loss partial slots written per tile by the fused blend epilogue (fixed order reduction).
 enum LossSlot {
   LS_COLOR_SUM = 0,   // sum |c - I| over the colour mask (tracking: opacity mask, mapping: all)

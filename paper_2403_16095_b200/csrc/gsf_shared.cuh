@@ -413,6 +413,10 @@ struct BlendConsts {
   float skip, clamp, term;
   double cutoff_d, skip_d, clamp_d;
   float rho_band, alpha_band;
+  // precomputed decision thresholds (same explicit ops as the full path below)
+  float rho_hi, rho_lo, rho_min;      // cutoff + band, cutoff - band, band
+  float skip_lo, skip_hi, clamp_lo, clamp_hi;
+  int32_t fast_ok;                    // exp_f needs no range checks on the fast path
 };
 
 GSF_HD BlendConsts make_blend_consts(const RasterParams& rp) {
@@ -426,6 +430,15 @@ GSF_HD BlendConsts make_blend_consts(const RasterParams& rp) {
   k.term = static_cast<float>(rp.termination);
   k.rho_band = static_cast<float>(4e-3 + 2e-4 * k.cutoff_d);
   k.alpha_band = 5e-4f;
+  k.rho_hi = fadd(k.cutoff, k.rho_band);
+  k.rho_lo = fsub(k.cutoff, k.rho_band);
+  k.rho_min = k.rho_band;
+  const float sb = fmul(k.skip, k.alpha_band), cb = fmul(k.clamp, k.alpha_band);
+  k.skip_lo = fsub(k.skip, sb);
+  k.skip_hi = fadd(k.skip, sb);
+  k.clamp_lo = fsub(k.clamp, cb);
+  k.clamp_hi = fadd(k.clamp, cb);
+  k.fast_ok = k.cutoff_d < 170.0 ? 1 : 0;
   return k;
 }
 
@@ -444,41 +457,44 @@ struct PairEval {
   float dx, dy;
 };
 
-// The guard is only consulted for values within a small band of a threshold, so the device
-// touches the fp64 copy for a tiny fraction of pairs.  `gp` points at the fp64 copy.
-GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
+GSF_HD float pair_rho(float dx, float dy, const BlendG& g) {
+  return ffma(fmul(g.c00, dx), dx, ffma(fmul(g.c01x2, dx), dy, fmul(fmul(g.c11, dy), dy)));
+}
+
+// Full decision (rasterizer.cpp:106-114) with the fp64 guard band around both thresholds.
+#if defined(__CUDA_ARCH__)
+__device__ __noinline__
+#else
+inline
+#endif
+PairEval eval_pair_full(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
   PairEval e;
   e.dx = fsub(px, g.mx);
   e.dy = fsub(py, g.my);
-  const float rho = ffma(fmul(g.c00, e.dx), e.dx, ffma(fmul(g.c01x2, e.dx), e.dy, fmul(fmul(g.c11, e.dy), e.dy)));
+  const float rho = pair_rho(e.dx, e.dy, g);
   e.code = 0;
   e.clamped = 0;
   e.alpha = 0.0f;
   e.gval = 0.0f;
   double rho_d = -1.0;
   bool have_d = false;
-  // rho > cutoff || rho < 0 -> skip
-  if (rho > fadd(k.cutoff, k.rho_band)) return e;
-  if (rho >= fsub(k.cutoff, k.rho_band) || rho < k.rho_band) {
+  if (rho > k.rho_hi) return e;                       // rho > cutoff || rho < 0 -> skip
+  if (rho >= k.rho_lo || rho < k.rho_min) {
     rho_d = guard_rho(static_cast<double>(px), static_cast<double>(py), *gp);
     have_d = true;
     if (rho_d > k.cutoff_d || rho_d < 0.0) return e;
   }
   e.gval = exp_f(fmul(-0.5f, rho));
   const float raw = fmul(g.sigma, e.gval);
-  // raw < alpha_skip -> skip
-  const float sb = fmul(k.skip, k.alpha_band);
-  if (raw < fsub(k.skip, sb)) return e;
-  if (raw <= fadd(k.skip, sb)) {
+  if (raw < k.skip_lo) return e;                      // raw < alpha_skip -> skip
+  if (raw <= k.skip_hi) {
     if (!have_d) { rho_d = guard_rho(static_cast<double>(px), static_cast<double>(py), *gp); have_d = true; }
     const double raw_d = dmul(gp->sigma, exp_d(dmul(-0.5, rho_d)));
     if (raw_d < k.skip_d) return e;
   }
-  // alpha clamp decision
-  const float cb = fmul(k.clamp, k.alpha_band);
-  if (raw > fadd(k.clamp, cb)) {
+  if (raw > k.clamp_hi) {                             // alpha clamp decision
     e.clamped = 1;
-  } else if (raw >= fsub(k.clamp, cb)) {
+  } else if (raw >= k.clamp_lo) {
     if (!have_d) { rho_d = guard_rho(static_cast<double>(px), static_cast<double>(py), *gp); have_d = true; }
     const double raw_d = dmul(gp->sigma, exp_d(dmul(-0.5, rho_d)));
     e.clamped = raw_d > k.clamp_d ? 1 : 0;
@@ -486,6 +502,38 @@ GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp,
   e.alpha = e.clamped ? k.clamp : fminf_(raw, k.clamp);
   e.code = 1;
   return e;
+}
+
+// Same decisions as eval_pair_full; the common cases (clearly outside, clearly inside and away
+// from the alpha thresholds) are resolved inline and only band cases take the fp64 path.
+// `gp` is only dereferenced on that path.
+GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
+  PairEval e;
+  e.dx = fsub(px, g.mx);
+  e.dy = fsub(py, g.my);
+  const float rho = pair_rho(e.dx, e.dy, g);
+  e.code = 0;
+  e.clamped = 0;
+  e.alpha = 0.0f;
+  e.gval = 0.0f;
+  if (rho > k.rho_hi) return e;
+  if (k.fast_ok && rho < k.rho_lo && rho >= k.rho_min) {
+    e.gval = exp_f(fmul(-0.5f, rho));
+    const float raw = fmul(g.sigma, e.gval);
+    if (raw < k.skip_lo) return e;
+    if (raw > k.skip_hi && raw < k.clamp_lo) {
+      e.alpha = raw;
+      e.code = 1;
+      return e;
+    }
+    if (raw > k.clamp_hi && raw > k.skip_hi) {
+      e.alpha = k.clamp;
+      e.clamped = 1;
+      e.code = 1;
+      return e;
+    }
+  }
+  return eval_pair_full(px, py, g, gp, k);
 }
 
 struct PixelState {

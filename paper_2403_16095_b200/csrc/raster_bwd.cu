@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
   const int tile = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int x = tx * kTile + (tid & 15), y = ty * kTile + (tid >> 4);
+  const int x = tx * kTile + tile_lx(tid), y = ty * kTile + tile_ly(tid);
   const bool inside = x < W && y < H;
   const int64_t pi = static_cast<int64_t>(y) * W + x;
   const int2 rg = bp.ranges[tile];

@@ -27,12 +27,18 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ pa
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= P) return;
   // validate_primitives (rasterizer.cpp:34-44): every field finite and |q| > 1e-12
+  // (all loads issued before any test: no short-circuit chain of dependent memory latencies)
   const int D = kFieldsBase + 3 * rp.sh_coeffs;
+  float v[kFieldsBase];
+#pragma unroll
+  for (int f = 0; f < kFieldsBase; ++f) v[f] = params[f * P + i];
   bool ok = true;
-  for (int f = 0; f < D; ++f) ok = ok && isfinite(params[f * P + i]);
-  if (ok) {
-    const double qw = params[6 * P + i], qx = params[7 * P + i], qy = params[8 * P + i], qz = params[9 * P + i];
-    ok = dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz))) > 1e-12;
+#pragma unroll
+  for (int f = 0; f < kFieldsBase; ++f) ok &= isfinite(v[f]);
+  for (int f = kFieldsBase; f < D; ++f) ok &= isfinite(params[f * P + i]);
+  {
+    const double qw = v[6], qx = v[7], qy = v[8], qz = v[9];
+    ok &= dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz))) > 1e-12;
   }
   if (!ok) {
     atomicMin(bad_index, static_cast<int32_t>(i));
@@ -77,23 +83,41 @@ __global__ void k_gather(const uint32_t* __restrict__ sorted_ids, const uint32_t
   tile_cnt[r] = static_cast<uint32_t>((q.y - q.x + 1) * (q.w - q.z + 1));
 }
 
+// One warp expands 32 consecutive ranks cooperatively (lanes stride over each rank's tile
+// rectangle), so a few very large footprints cannot serialise a thread; writes are coalesced.
 __global__ void k_duplicate(const int4* __restrict__ rect, const uint32_t* __restrict__ pair_off, const uint32_t* n_dev,
                             uint32_t n_cap, const uint32_t* m_dev, uint32_t pair_cap, int tiles_x,
                             uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pair_rank, uint32_t* overflow) {
   const uint32_t n = min(*n_dev, n_cap);
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r == 0 && *m_dev > pair_cap) *overflow = 1u;
-  if (r >= n) return;
-  const int4 q = rect[r];
-  uint32_t pos = pair_off[r];
-  for (int ty = q.z; ty <= q.w; ++ty)
-    for (int tx = q.x; tx <= q.y; ++tx) {
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  if (gtid == 0 && *m_dev > pair_cap) *overflow = 1u;
+  const uint32_t r0 = gtid & ~31u;
+  if (r0 >= n) return;
+  int4 q = make_int4(0, -1, 0, -1);
+  uint32_t off = 0;
+  if (r0 + lane < n) {
+    q = rect[r0 + lane];
+    off = pair_off[r0 + lane];
+  }
+  const int nj = static_cast<int>(min(32u, n - r0));
+  for (int j = 0; j < nj; ++j) {
+    const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qx1 = __shfl_sync(0xffffffffu, q.y, j);
+    const int qy0 = __shfl_sync(0xffffffffu, q.z, j), qy1 = __shfl_sync(0xffffffffu, q.w, j);
+    const uint32_t base = __shfl_sync(0xffffffffu, off, j);
+    const int w = qx1 - qx0 + 1;
+    const int c = w * (qy1 - qy0 + 1);
+    const float inv_w = 1.0f / static_cast<float>(w);
+    for (int k = lane; k < c; k += 32) {
+      const int row = __float2int_rz((static_cast<float>(k) + 0.5f) * inv_w);   // exact for c < 4M
+      const int col = k - row * w;
+      const uint32_t pos = base + static_cast<uint32_t>(k);
       if (pos < pair_cap) {
-        pkeys[pos] = static_cast<uint32_t>(ty * tiles_x + tx);
-        pair_rank[pos] = r;
+        pkeys[pos] = static_cast<uint32_t>((qy0 + row) * tiles_x + qx0 + col);
+        pair_rank[pos] = r0 + static_cast<uint32_t>(j);
       }
-      ++pos;
     }
+  }
 }
 
 __global__ void k_ranges(const uint32_t* __restrict__ keys, const uint32_t* m_dev, uint32_t cap, int2* ranges) {
@@ -138,7 +162,7 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
   const int tile = blockIdx.x;
   const int tid = threadIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int x = tx * kTile + (tid & 15), y = ty * kTile + (tid >> 4);
+  const int x = tx * kTile + tile_lx(tid), y = ty * kTile + tile_ly(tid);
   const bool inside = x < W && y < H;
   const int64_t pi = static_cast<int64_t>(y) * W + x;
   const int2 rg = ranges[tile];
@@ -218,7 +242,7 @@ __global__ void __launch_bounds__(256) k_loss_tiles(const float* __restrict__ co
                                                     float floor, double* __restrict__ loss_part) {
   __shared__ double s_red[8][LS_NUM];
   const int tile = blockIdx.x, tid = threadIdx.x;
-  const int x = (tile % tiles_x) * kTile + (tid & 15), y = (tile / tiles_x) * kTile + (tid >> 4);
+  const int x = (tile % tiles_x) * kTile + tile_lx(tid), y = (tile / tiles_x) * kTile + tile_ly(tid);
   double v[LS_NUM];
 #pragma unroll
   for (int q = 0; q < LS_NUM; ++q) v[q] = 0.0;

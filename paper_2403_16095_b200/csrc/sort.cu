@@ -89,11 +89,22 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(const uint32_t* __rest
       atomicExch(&state[0], (2ull << 32) | btotal);
     } else {
       atomicExch(&state[tile], (1ull << 32) | btotal);
-      for (int p = static_cast<int>(tile) - 1;; --p) {
-        unsigned long long s;
-        do { s = ld_vol64(&state[p]); } while ((s >> 32) == 0);
-        excl += static_cast<uint32_t>(s);
-        if ((s >> 32) == 2) break;
+      int p = static_cast<int>(tile) - 1;
+      bool done = false;
+      while (!done) {
+        unsigned long long s[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[j] = (p - j >= 0) ? ld_vol64(&state[p - j]) : (2ull << 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (!done) {
+            unsigned long long v = s[j];
+            while ((v >> 32) == 0) v = ld_vol64(&state[p - j]);
+            excl += static_cast<uint32_t>(v);
+            if ((v >> 32) == 2) done = true;
+          }
+        }
+        p -= 8;
       }
       atomicExch(&state[tile], (2ull << 32) | (excl + btotal));
     }
@@ -145,11 +156,12 @@ __global__ void __launch_bounds__(kRsBlock) k_onesweep(const uint32_t* __restric
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = n_dev ? min(*n_dev, n_host) : n_host;
   if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int i = tid; i < kRsWarps * (kRadix + 1); i += kRsBlock) (&s_whist[0][0])[i] = 0u;
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint32_t base = tile * kRsTile;
   if (base >= n) return;
+  for (int i = tid; i < kRsWarps * (kRadix + 1); i += kRsBlock) (&s_whist[0][0])[i] = 0u;
+  __syncthreads();
   const uint32_t wbase = base + warp * 32 * kRsIpt;
   uint32_t k[kRsIpt], v[kRsIpt], rank[kRsIpt];
 #pragma unroll
@@ -193,11 +205,23 @@ __global__ void __launch_bounds__(kRsBlock) k_onesweep(const uint32_t* __restric
       st_vol(&lb[d], kFlagP | cnt);
     } else {
       st_vol(&lb[d], kFlagA | cnt);
-      for (int p = static_cast<int>(tile) - 1;; --p) {
-        uint32_t s;
-        do { s = ld_vol(&lookback[static_cast<size_t>(p) * kRadix + d]); } while ((s & ~kValMask) == 0);
-        excl += s & kValMask;
-        if (s & kFlagP) break;
+      // batched look-back: 8 predecessor words in flight per round instead of a serial chain
+      int p = static_cast<int>(tile) - 1;
+      bool done = false;
+      while (!done) {
+        uint32_t s[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[j] = (p - j >= 0) ? ld_vol(&lookback[static_cast<size_t>(p - j) * kRadix + d]) : kFlagP;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (!done) {
+            uint32_t v = s[j];
+            while ((v & ~kValMask) == 0) v = ld_vol(&lookback[static_cast<size_t>(p - j) * kRadix + d]);
+            excl += v & kValMask;
+            if (v & kFlagP) done = true;
+          }
+        }
+        p -= 8;
       }
       st_vol(&lb[d], kFlagP | (excl + cnt));
     }
