@@ -259,8 +259,9 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     for (int i = 0; i < 2; ++i) { dalloc(ws.skeys[i], P); dalloc(ws.svals[i], P); }
     dalloc(ws.rank_to_id, P); dalloc(ws.bg, P); dalloc(ws.gg, P); dalloc(ws.rect, P); dalloc(ws.tile_cnt, P);
     dalloc(ws.pair_off, P + 1);
-    dalloc(ws.pose_part, static_cast<size_t>(div_up(P, 256)) * 6);
+    dalloc(ws.pj_id, static_cast<size_t>(P) * 36);
     ws.P_cap = P;
+    dfree(ws.pose_part);
   }
   if (ws.pair_cap == 0) ws.pair_cap = std::max<int64_t>(1 << 20, 4 * P);
   if (!ws.pkeys[0]) {
@@ -279,7 +280,9 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     dalloc(ws.ranges, tiles);
     dalloc(ws.loss_part, tiles * LS_NUM);
     ws.tiles_cap = tiles;
+    dfree(ws.pose_part);
   }
+  if (!ws.pose_part) dalloc(ws.pose_part, static_cast<size_t>(std::max<int64_t>(div_up(ws.P_cap, 256), ws.tiles_cap)) * 6);
   const int64_t scan_n = std::max<int64_t>(P, npix);
   const size_t sb = scan_temp_bytes(static_cast<uint32_t>(scan_n));
   const size_t rb = std::max(radix_temp_bytes(static_cast<uint32_t>(P), 4), radix_temp_bytes(static_cast<uint32_t>(ws.pair_cap), 4));
@@ -607,7 +610,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
                   ws.tile_cnt, ws.pair_off, ws.pkeys[0], ws.pkeys[1], ws.pvals[0], ws.pvals[1], ws.pair_rank,
                   ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
-                  ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.scan.state, ws.radix_temp, ws.pose_part,
+                  ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.scan.state, ws.radix_temp, ws.pose_part, ws.pj_id,
                   ws.red_part, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
                   c->red_f};
@@ -1076,9 +1079,12 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
   const int tiles = ((k.width + kTile - 1) / kTile) * ((k.height + kTile - 1) / kTile);
   const int64_t npix = static_cast<int64_t>(k.width) * k.height;
   for (int it = 0; it < tcfg.iterations; ++it) {
-    run_forward(c->ws, c->ds, fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it), c->stream, &c->launches);
+    FwdArgs fa = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it);
+    fa.want_posejac = true;
+    run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
     run_loss_finalize(c->ws, c->ds, lp, tiles, npix, it, c->stream, &c->launches);
     BwdArgs b = bwd_args(c, k, rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);
+    b.fused_pose = true;
     run_backward(c->ws, c->ds, b, c->stream, &c->launches);
     run_track_update(c->ds, it, c->stream, &c->launches);
   }

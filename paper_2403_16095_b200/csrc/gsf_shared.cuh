@@ -215,6 +215,35 @@ GSF_HD void sh_basis(int degree, double x, double y, double z, double* b) {
   b[15] = dmul(dmul(-0.5900435899266435, x), dsub(xx, dmul(3.0, yy)));
 }
 
+// Direction gradients of the SH bases (sh.cpp:44-72), g[3*k + axis].
+GSF_HD void sh_basis_grad_d(int degree, double x, double y, double z, double* g) {
+  for (int i = 0; i < 48; ++i) g[i] = 0.0;
+  if (degree < 1) return;
+  const double C1 = 0.4886025119029199;
+  g[4] = -C1;
+  g[8] = C1;
+  g[9] = -C1;
+  if (degree < 2) return;
+  const double xx = x * x, yy = y * y, zz = z * z;
+  const double c20 = 1.0925484305920792, c21 = -1.0925484305920792, c22 = 0.31539156525252005, c23 = -1.0925484305920792,
+               c24 = 0.5462742152960396;
+  g[12] = c20 * y; g[13] = c20 * x;
+  g[16] = c21 * z; g[17] = c21 * y;
+  g[18] = c22 * (-2.0 * x); g[19] = c22 * (-2.0 * y); g[20] = c22 * (4.0 * z);
+  g[21] = c23 * z; g[23] = c23 * x;
+  g[24] = c24 * (2.0 * x); g[25] = c24 * (-2.0 * y);
+  if (degree < 3) return;
+  const double c30 = -0.5900435899266435, c31 = 2.890611442640554, c32 = -0.4570457994644658, c33 = 0.3731763325901154,
+               c34 = -0.4570457994644658, c35 = 1.445305721320277, c36 = -0.5900435899266435;
+  g[27] = c30 * (6.0 * x * y); g[28] = c30 * (3.0 * xx - 3.0 * yy);
+  g[30] = c31 * (y * z); g[31] = c31 * (x * z); g[32] = c31 * (x * y);
+  g[33] = c32 * (-2.0 * x * y); g[34] = c32 * (4.0 * zz - xx - 3.0 * yy); g[35] = c32 * (8.0 * y * z);
+  g[36] = c33 * (-6.0 * x * z); g[37] = c33 * (-6.0 * y * z); g[38] = c33 * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+  g[39] = c34 * (4.0 * zz - 3.0 * xx - yy); g[40] = c34 * (-2.0 * x * y); g[41] = c34 * (8.0 * x * z);
+  g[42] = c35 * (2.0 * x * z); g[43] = c35 * (-2.0 * y * z); g[44] = c35 * (xx - yy);
+  g[45] = c36 * (3.0 * xx - 3.0 * yy); g[46] = c36 * (-6.0 * x * y);
+}
+
 GSF_HD int sh_degree(int K) { return K >= 16 ? 3 : (K >= 9 ? 2 : (K >= 4 ? 1 : 0)); }
 
 // One primitive.  p = pointer to field 0 of this primitive in a SoA [field][stride] fp32
@@ -462,12 +491,7 @@ GSF_HD float pair_rho(float dx, float dy, const BlendG& g) {
 }
 
 // Full decision (rasterizer.cpp:106-114) with the fp64 guard band around both thresholds.
-#if defined(__CUDA_ARCH__)
-__device__ __noinline__
-#else
-inline
-#endif
-PairEval eval_pair_full(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
+GSF_HD PairEval eval_pair_full(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
   PairEval e;
   e.dx = fsub(px, g.mx);
   e.dy = fsub(py, g.my);

@@ -107,7 +107,8 @@ struct Workspace {
   ScanTemp scan;
   uint32_t* radix_temp = nullptr;
   size_t radix_temp_bytes = 0;
-  double* pose_part = nullptr;  // chain blocks * 6
+  double* pose_part = nullptr;  // chain blocks * 6 (or tiles * 6 for the fused tracking backward)
+  float* pj_id = nullptr;       // P * 36: per-visible-primitive pose Jacobians, rank order (tracking)
   double* red_part = nullptr;   // generic per-block fp64 partials (ssim, then iso)
   int64_t red_iso_offset = 0;
   int ssim_blocks = 0, iso_blocks = 0;
@@ -143,6 +144,7 @@ struct FwdArgs {
   const float* loss_depth;   // sensor depth for the loss masks (nullable)
   LossParams lp;
   int iteration;             // loop iteration (for device-side checks), -1 outside loops
+  bool want_posejac = false; // tracking: emit the per-primitive pose Jacobians (ws.pj_id)
 };
 void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* launches);
 void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,
@@ -168,6 +170,7 @@ struct BwdArgs {
   LossParams lp;
   int seed_mode;
   bool pose_only;            // tracking: skip per-primitive parameter gradients
+  bool fused_pose = false;   // pose_only + ws.pj_id valid: pose through per-primitive Jacobians
   float* grads;              // [D][P] parameter gradients (full mode)
   float* d_mean2d;           // [2][P] (full mode, nullable)
 };

@@ -18,6 +18,113 @@ namespace gsfk {
 
 namespace {
 
+// Per-primitive linear map from the six screen-space partials of one (tile, primitive) pair
+// (d_mean2d x/y, d_cov2d 00/01/11, d_depth [+ d_color for view-dependent SH]) to the SE(3)
+// pose gradient: the camera part of render_backward phase 2 (rasterizer.cpp:495-526, 548-558)
+// linearised per primitive in fp64, so the tracking backward can apply it right after its
+// per-tile reduction instead of round-tripping every pair partial through memory.
+// Layout (36 floats): J00 J02 J11 J12 | Bc[3][3] | Cr[3][3] | p_cam[3] | Tc[3][3] | pad pad
+__device__ void compute_posejac(const float* __restrict__ p, int64_t stride, const Cam& cam, int K, float* out) {
+  const double m0 = p[0], m1 = p[stride], m2 = p[2 * stride];
+  const double* W = cam.W;
+  const double pc[3] = {W[0] * m0 + W[1] * m1 + W[2] * m2 + cam.t[0], W[3] * m0 + W[4] * m1 + W[5] * m2 + cam.t[1],
+                        W[6] * m0 + W[7] * m1 + W[8] * m2 + cam.t[2]};
+  const double iz = 1.0 / pc[2], iz2 = iz * iz, iz3 = iz2 * iz;
+  const double J00 = cam.fx * iz, J02 = -cam.fx * pc[0] * iz2, J11 = cam.fy * iz, J12 = -cam.fy * pc[1] * iz2;
+  const double qw0 = p[6 * stride], qx0 = p[7 * stride], qy0 = p[8 * stride], qz0 = p[9 * stride];
+  const double ql = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
+  const double w = qw0 / ql, x = qx0 / ql, y = qy0 / ql, z = qz0 / ql;
+  const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                          {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                          {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+  double s2[3];
+  for (int a = 0; a < 3; ++a) {
+    const double sa = exp(static_cast<double>(p[(3 + a) * stride]));
+    s2[a] = sa * sa;
+  }
+  double Cw[3][3], T1[3][3], V[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) Cw[a][b] = R[a][0] * s2[0] * R[b][0] + R[a][1] * s2[1] * R[b][1] + R[a][2] * s2[2] * R[b][2];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) T1[a][b] = W[3 * a] * Cw[0][b] + W[3 * a + 1] * Cw[1][b] + W[3 * a + 2] * Cw[2][b];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) V[a][b] = T1[a][0] * W[3 * b] + T1[a][1] * W[3 * b + 1] + T1[a][2] * W[3 * b + 2];
+  double G[2][3];
+  for (int b = 0; b < 3; ++b) {
+    G[0][b] = J00 * V[0][b] + J02 * V[2][b];
+    G[1][b] = J11 * V[1][b] + J12 * V[2][b];
+  }
+  const double ax = -cam.fx * iz2, ay = -cam.fy * iz2, bx = 2.0 * cam.fx * pc[0] * iz3, by = 2.0 * cam.fy * pc[1] * iz3;
+  // d_p_cam from (s2, s3, s4) via d_jac = 2 dC J V (rasterizer.cpp:504-513)
+  const double Bc[3][3] = {{2.0 * G[0][2] * ax, 2.0 * G[1][2] * ax, 0.0},
+                           {0.0, 2.0 * G[0][2] * ay, 2.0 * G[1][2] * ay},
+                           {2.0 * (ax * G[0][0] + bx * G[0][2]),
+                            2.0 * (ax * G[1][0] + ay * G[0][1] + bx * G[1][2] + by * G[0][2]),
+                            2.0 * (ay * G[1][1] + by * G[1][2])}};
+  // rot += sum dCc .* (E_j V - V E_j) = -2 vee(V dCc - dCc V), dCc = s2 J0J0^T + s3 (J0J1^T + J1J0^T) + s4 J1J1^T
+  const double J0[3] = {J00, 0.0, J02}, J1[3] = {0.0, J11, J12};
+  double Cr[3][3];
+  for (int k = 0; k < 3; ++k) {
+    double Dk[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b)
+        Dk[a][b] = k == 0 ? J0[a] * J0[b] : (k == 1 ? J0[a] * J1[b] + J1[a] * J0[b] : J1[a] * J1[b]);
+    double M[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double vd = 0.0, dv = 0.0;
+        for (int c = 0; c < 3; ++c) { vd += V[a][c] * Dk[c][b]; dv += Dk[a][c] * V[c][b]; }
+        M[a][b] = vd - dv;
+      }
+    Cr[0][k] = -2.0 * M[2][1];
+    Cr[1][k] = -2.0 * M[0][2];
+    Cr[2][k] = -2.0 * M[1][0];
+  }
+  double Tc[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  if (K > 1) {   // view-dependent colour: trans += W (I - dir dir^T)/len * dDir/dColour (sh.cpp:88-108)
+    const double d0 = m0 - cam.center[0], d1 = m1 - cam.center[1], d2 = m2 - cam.center[2];
+    const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    if (len > 1e-12) {
+      const double dir[3] = {d0 / len, d1 / len, d2 / len};
+      const int deg = sh_degree(K);
+      double b[16], gb[48];
+      sh_basis(deg, dir[0], dir[1], dir[2], b);
+      sh_basis_grad_d(deg, dir[0], dir[1], dir[2], gb);
+      double Dm[3][3];   // d_dir = Dm * d_colour
+      for (int c = 0; c < 3; ++c) {
+        double raw = 0.5;
+        for (int k = 0; k < K; ++k) raw += b[k] * p[(11 + 3 * k + c) * stride];
+        const double mask = raw < 0.0 ? 0.0 : 1.0;
+        for (int a = 0; a < 3; ++a) {
+          double acc = 0.0;
+          for (int k = 1; k < K; ++k) acc += gb[3 * k + a] * p[(11 + 3 * k + c) * stride];
+          Dm[a][c] = mask * acc;
+        }
+      }
+      double Pm[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) Pm[a][c] = ((a == c ? 1.0 : 0.0) - dir[a] * dir[c]) / len;
+      double PD[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) PD[a][c] = Pm[a][0] * Dm[0][c] + Pm[a][1] * Dm[1][c] + Pm[a][2] * Dm[2][c];
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) Tc[a][c] = W[3 * a] * PD[0][c] + W[3 * a + 1] * PD[1][c] + W[3 * a + 2] * PD[2][c];
+    }
+  }
+  out[0] = static_cast<float>(J00);
+  out[1] = static_cast<float>(J02);
+  out[2] = static_cast<float>(J11);
+  out[3] = static_cast<float>(J12);
+  for (int a = 0; a < 3; ++a)
+    for (int c = 0; c < 3; ++c) {
+      out[4 + 3 * a + c] = static_cast<float>(Bc[a][c]);
+      out[13 + 3 * a + c] = static_cast<float>(Cr[a][c]);
+      out[25 + 3 * a + c] = static_cast<float>(Tc[a][c]);
+    }
+  for (int a = 0; a < 3; ++a) out[22 + a] = static_cast<float>(pc[a]);
+  out[34] = out[35] = 0.0f;
+}
+
 __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ params, int64_t P, const DevState* ds,
                                                     RasterParams rp, uint32_t near_bits, uint32_t* __restrict__ flag,
                                                     uint32_t* __restrict__ key_id, BlendG* __restrict__ bg_id,
@@ -55,6 +162,17 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ pa
   gg_id[i] = make_guard_g(o);
   depth_id[i] = o.depth;
   rect_id[i] = make_int4(o.tx0, o.tx1, o.ty0, o.ty1);
+}
+
+// Pose Jacobians of the visible primitives in depth-rank order (tracking only).
+__global__ void __launch_bounds__(256) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
+                                                 const int32_t* __restrict__ rank_to_id, const uint32_t* n_dev,
+                                                 uint32_t n_cap, float* __restrict__ pj) {
+  const uint32_t n = min(*n_dev, n_cap);
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || ds->halt) return;
+  const int64_t id = rank_to_id[r];
+  compute_posejac(params + id, P, ds->cam, K, pj + 36 * static_cast<size_t>(r));
 }
 
 __global__ void k_compact(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ off,
@@ -308,6 +426,10 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   if (P > 0) {
     k_gather<<<div_up(P, 256), 256, 0, st>>>(dvals, &ds->V, Pn, ws.bg_id, ws.gg_id, ws.rect_id, ws.rank_to_id, ws.bg, ws.gg,
                                              ws.rect, ws.tile_cnt);
+    ++*L;
+  }
+  if (a.want_posejac && P > 0) {
+    k_posejac<<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.K, ws.rank_to_id, &ds->V, Pn, ws.pj_id);
     ++*L;
   }
   launch_scan_excl(ws.tile_cnt, ws.pair_off, &ds->V, Pn, &ds->M, ws.scan, st, L);
