@@ -234,6 +234,12 @@ int gsf_frame_upload(gsf_ctx ctx, int32_t slot, const float* rgb, const float* d
 int gsf_track_frame(gsf_ctx ctx, int32_t slot, const gsf_pose* initial, const gsf_intrinsics* K,
                     const gsf_tracker_cfg* tcfg, const gsf_loss_weights* w,
                     const gsf_raster_cfg* rcfg, gsf_track_result* out);
+/* One tracking iteration's objective and pose gradient at `pose` against frame slot `slot`:
+ * render -> evaluate_tracking_loss -> render_backward (pose part) of tracker.cpp:42-63, on the
+ * fused device path track_frame uses (per-primitive SE(3) Jacobians, no chain pass). */
+int gsf_tracking_gradient(gsf_ctx ctx, int32_t slot, const gsf_pose* pose, const gsf_intrinsics* K,
+                          const gsf_loss_weights* w, const gsf_raster_cfg* rcfg, gsf_loss_terms* terms,
+                          double d_pose[6]);
 /* Same call with host frame buffers: uploads rgb/depth into slot 0 first (e2e path). */
 int gsf_track_frame_host(gsf_ctx ctx, const float* rgb, const float* depth,
                          const gsf_pose* initial, const gsf_intrinsics* K,

@@ -130,6 +130,9 @@ SIGNATURES = {
     "gsf_track_frame": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Pose), C.POINTER(Intrinsics),
                                   C.POINTER(TrackerCfg), C.POINTER(LossWeights),
                                   C.POINTER(RasterCfg), C.POINTER(TrackResult)]),
+    "gsf_tracking_gradient": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Pose), C.POINTER(Intrinsics),
+                                        C.POINTER(LossWeights), C.POINTER(RasterCfg), C.POINTER(LossTerms),
+                                        C.POINTER(C.c_double * 6)]),
     "gsf_track_frame_host": (C.c_int, [C.c_void_p, fp, fp, C.POINTER(Pose), C.POINTER(Intrinsics),
                                        C.POINTER(TrackerCfg), C.POINTER(LossWeights),
                                        C.POINTER(RasterCfg), C.POINTER(TrackResult)]),

@@ -313,6 +313,17 @@ class Context:
                                              C.byref(raster), C.byref(out)))
         return out
 
+    def tracking_gradient(self, slot: int, pose: Pose, K: Intrinsics, w: LossWeights = None,
+                          raster: RasterCfg = None):
+        """Tracking objective and its pose gradient at `pose` (one track_frame iteration)."""
+        w = w or abi.defaults_weights()
+        raster = raster or abi.defaults_raster()
+        terms = abi.LossTerms()
+        g = (C.c_double * 6)()
+        self._check(self.lib.gsf_tracking_gradient(self.h, slot, C.byref(pose), C.byref(K), C.byref(w), C.byref(raster),
+                                                   C.byref(terms), C.byref(g)))
+        return terms, np.array(list(g))
+
     def map_step(self, slots: Sequence[int], poses: Sequence[Pose], K: Intrinsics, mcfg: MapperCfg = None,
                  iterations: int = 60):
         mcfg = mcfg or abi.defaults_mapper()

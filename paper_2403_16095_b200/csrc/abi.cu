@@ -1145,6 +1145,43 @@ int gsf_track_frame(gsf_ctx c, int32_t slot, const gsf_pose* initial, const gsf_
   });
 }
 
+int gsf_tracking_gradient(gsf_ctx c, int32_t slot, const gsf_pose* pose, const gsf_intrinsics* K,
+                          const gsf_loss_weights* w, const gsf_raster_cfg* rcfg, gsf_loss_terms* terms,
+                          double d_pose[6]) {
+  return guard(c, [&] {
+    check_intrinsics(*K);
+    check_raster(*rcfg);
+    check_weights(*w);
+    const Frame& f = get_frame(c, slot, *K);
+    ensure_ws(c, K->width, K->height);
+    const Cam cam = host_cam(*pose, *K);
+    const LossParams lp = make_lp(1, w, *rcfg);
+    const int tiles = ((K->width + kTile - 1) / kTile) * ((K->height + kTile - 1) / kTile);
+    const int64_t npix = static_cast<int64_t>(K->width) * K->height;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      reset_state(c, &cam);
+      FwdArgs fa = fwd_args(c, *K, *rcfg, nullptr, f.rgb, f.depth, lp, -1);
+      fa.want_posejac = true;
+      run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
+      run_loss_finalize(c->ws, c->ds, lp, tiles, npix, -1, c->stream, &c->launches);
+      BwdArgs b = bwd_args(c, *K, *rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);
+      b.fused_pose = true;
+      run_backward(c->ws, c->ds, b, c->stream, &c->launches);
+      read_state(c);
+      if (!c->ds_host->overflow) break;
+      grow_pairs(c, c->ds_host->M);
+    }
+    if (c->ds_host->bad_index != std::numeric_limits<int32_t>::max()) throw_nonfinite(c->ds_host->bad_index);
+    fill_terms(c, terms);
+    for (int a = 0; a < 6; ++a) d_pose[a] = c->ds_host->d_pose[a];
+    c->have_render = true;
+    c->render_gen = c->map_gen;
+    c->rK = *K;
+    c->rcfg = *rcfg;
+    c->render_obs = false;
+  });
+}
+
 int gsf_track_frame_host(gsf_ctx c, const float* rgb, const float* depth, const gsf_pose* initial, const gsf_intrinsics* K,
                          const gsf_tracker_cfg* tcfg, const gsf_loss_weights* w, const gsf_raster_cfg* rcfg,
                          gsf_track_result* out) {

@@ -284,6 +284,175 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
   }
 }
 
+// Per-pixel backward inputs (rasterizer.cpp:395-413): seeds, final T and the contributor limit.
+struct PixBwd {
+  float gc0, gc1, gc2, gad, gop, gmd, gu, D, T;
+  int med, last;
+};
+
+template <int SEED>
+__device__ __forceinline__ PixBwd load_pixel_bwd(const BwdPtrs& bp, int64_t pi, bool inside, const LossParams& lp,
+                                                 const DevState* ds, double near_plane, double far_plane) {
+  PixBwd p;
+  p.gc0 = p.gc1 = p.gc2 = p.gad = p.gop = p.gmd = p.gu = p.D = 0.0f;
+  p.T = 1.0f;
+  p.med = -1;
+  p.last = 0;
+  if (!inside) return p;
+  p.last = bp.last[pi];
+  p.T = bp.final_T[pi];
+  p.med = bp.median_prim[pi];
+  if (SEED == SEED_EXPLICIT) {
+    if (bp.up_color) { p.gc0 = bp.up_color[3 * pi]; p.gc1 = bp.up_color[3 * pi + 1]; p.gc2 = bp.up_color[3 * pi + 2]; }
+    if (bp.up_adepth) p.gad = bp.up_adepth[pi];
+    if (bp.up_opacity) p.gop = bp.up_opacity[pi];
+    if (bp.up_mdepth) p.gmd = bp.up_mdepth[pi];
+    if (bp.up_uncert && lp.uncertainty_full_gradient) p.gu = bp.up_uncert[pi];
+    if (bp.obs) {
+      p.D = bp.obs[pi];
+      if (!dvalid(p.D, near_plane, far_plane)) p.gu = 0.f;
+    } else {
+      p.gu = 0.f;
+    }
+  } else {
+    const PixSeeds sd = seeds_pixel<SEED == SEED_TRACK ? 1 : 2>(pi, bp.color, bp.alpha_depth[pi], bp.median_depth[pi],
+                                                                bp.median_valid[pi] != 0, bp.opacity[pi], bp.target,
+                                                                bp.obs, bp.dssim, ds, lp, near_plane, far_plane);
+    p.gc0 = sd.gc0; p.gc1 = sd.gc1; p.gc2 = sd.gc2; p.gad = sd.gad; p.gmd = sd.gmd;
+    p.gu = lp.uncertainty_full_gradient ? sd.gu : 0.0f;
+    if (SEED == SEED_MAP && bp.obs) p.D = bp.obs[pi];
+  }
+  if (p.med < 0) p.gmd = 0.f;
+  if (p.gc0 == 0.f && p.gc1 == 0.f && p.gc2 == 0.f && p.gad == 0.f && p.gop == 0.f && p.gmd == 0.f && p.gu == 0.f)
+    p.last = 0;
+  return p;
+}
+
+// Tracking backward (pose only).  The pose gradient is linear in every pair's screen-space
+// gradient, so each lane pushes its own pixel's screen gradient through the primitive's SE(3)
+// Jacobian (compute_posejac) and accumulates the 6-vector in registers: no per-(tile, primitive)
+// cross-lane reduction, no pair partials in memory, no per-primitive chain kernel.  Lane sums
+// are fp32 within a batch and fp64 across batches; the CTA reduces them in a fixed tree.
+constexpr int kPoseBatch = 128;
+
+template <int SEED, bool VIEWDEP>
+__global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc,
+                                                       double near_plane, double far_plane, LossParams lp,
+                                                       const DevState* ds) {
+  __shared__ BlendG s_g[kPoseBatch];
+  __shared__ float4 s_pj[kPoseBatch][9];
+  __shared__ int32_t s_rank[kPoseBatch];
+  __shared__ int32_t s_id[kPoseBatch];
+  __shared__ int s_wmax[8];
+  __shared__ double s_pred[8][6];
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (ds->halt) {
+    if (tid < 6) bp.tile_pose[static_cast<size_t>(tile) * 6 + tid] = 0.0;
+    return;
+  }
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int x = tx * kTile + tile_lx(tid), y = ty * kTile + tile_ly(tid);
+  const bool inside = x < W && y < H;
+  const int64_t pi = static_cast<int64_t>(y) * W + x;
+  const int2 rg = bp.ranges[tile];
+  PixBwd pb = load_pixel_bwd<SEED>(bp, pi, inside, lp, ds, near_plane, far_plane);
+  const int ml = __reduce_max_sync(0xffffffffu, pb.last);
+  if (lane == 0) s_wmax[warp] = ml;
+  __syncthreads();
+  int maxlast = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) maxlast = max(maxlast, s_wmax[w]);
+  const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
+  float T = pb.T, S = 0.0f;
+  double pd[6] = {0, 0, 0, 0, 0, 0};
+  const int end = rg.x + maxlast;
+  for (int bend = end; bend > rg.x; bend -= kPoseBatch) {
+    const int bstart = max(rg.x, bend - kPoseBatch);
+    const int cnt = bend - bstart;
+    if (tid < cnt) {
+      const int r = static_cast<int>(bp.pair_rank[bp.sorted_orig[bstart + tid]]);
+      s_g[tid] = bp.bg[r];
+      s_rank[tid] = r;
+      s_id[tid] = bp.rank_to_id[r];
+    }
+    __syncthreads();
+    for (int i = tid; i < cnt * 9; i += 256) {
+      const int k = i / 9, j = i - 9 * k;
+      s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[9 * static_cast<size_t>(s_rank[k]) + j];
+    }
+    __syncthreads();
+    float pf0 = 0.f, pf1 = 0.f, pf2 = 0.f, pf3 = 0.f, pf4 = 0.f, pf5 = 0.f;
+    for (int k = cnt - 1; k >= 0; --k) {
+      const int li = bstart + k - rg.x;
+      if (li >= pb.last) continue;
+      const BlendG g = s_g[k];
+      const PairEval e = eval_pair(px, py, g, bp.gg + s_rank[k], kc);
+      if (!e.code) continue;
+      const float alpha = e.alpha;
+      const float inv = __frcp_rn(1.0f - alpha);
+      const float Tpre = T * inv;
+      const float derr = g.depth - pb.D;
+      const float q = pb.gc0 * g.r + pb.gc1 * g.g + pb.gc2 * g.b + pb.gad * g.depth + pb.gop + pb.gu * derr * derr;
+      const float dal = Tpre * q - S * inv;
+      const float w = alpha * Tpre;
+      S += w * q;
+      T = Tpre;
+      const float s5 = w * (pb.gad + 2.0f * pb.gu * derr) + (s_id[k] == pb.med ? pb.gmd : 0.0f);
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+      if (!e.clamped) {
+        const float dg = dal * g.sigma;
+        const float c01 = 0.5f * g.c01x2;
+        const float ux = g.c00 * e.dx + c01 * e.dy, uy = c01 * e.dx + g.c11 * e.dy;
+        const float gdg = e.gval * dg;
+        const float h = 0.5f * gdg;
+        s0 = gdg * ux;
+        s1 = gdg * uy;
+        s2 = h * ux * ux;
+        s3 = h * ux * uy;
+        s4 = h * uy * uy;
+      }
+      // layout: J00 J02 J11 J12 | Bc | Cr | p_cam | Tc (compute_posejac)
+      const float4 a0 = s_pj[k][0], a1 = s_pj[k][1], a2 = s_pj[k][2], a3 = s_pj[k][3], a4 = s_pj[k][4],
+                   a5 = s_pj[k][5], a6 = s_pj[k][6];
+      const float d0 = a0.x * s0 + a1.x * s2 + a1.y * s3 + a1.z * s4;
+      const float d1 = a0.z * s1 + a1.w * s2 + a2.x * s3 + a2.y * s4;
+      const float d2 = a0.y * s0 + a0.w * s1 + a2.z * s2 + a2.w * s3 + a3.x * s4 + s5;
+      const float pc0 = a5.z, pc1 = a5.w, pc2 = a6.x;
+      pf0 += pc1 * d2 - pc2 * d1 + a3.y * s2 + a3.z * s3 + a3.w * s4;
+      pf1 += pc2 * d0 - pc0 * d2 + a4.x * s2 + a4.y * s3 + a4.z * s4;
+      pf2 += pc0 * d1 - pc1 * d0 + a4.w * s2 + a5.x * s3 + a5.y * s4;
+      float t0 = d0, t1 = d1, t2 = d2;
+      if (VIEWDEP) {
+        const float4 a7 = s_pj[k][7], a8 = s_pj[k][8];
+        const float c0 = w * pb.gc0, c1 = w * pb.gc1, c2 = w * pb.gc2;
+        t0 += a6.y * c0 + a6.z * c1 + a6.w * c2;
+        t1 += a7.x * c0 + a7.y * c1 + a7.z * c2;
+        t2 += a7.w * c0 + a8.x * c1 + a8.y * c2;
+      }
+      pf3 += t0;
+      pf4 += t1;
+      pf5 += t2;
+    }
+    pd[0] += pf0; pd[1] += pf1; pd[2] += pf2; pd[3] += pf3; pd[4] += pf4; pd[5] += pf5;
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    double v = pd[a];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) s_pred[warp][a] = v;
+  }
+  __syncthreads();
+  if (tid < 6) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s_pred[w][tid];
+    bp.tile_pose[static_cast<size_t>(tile) * 6 + tid] = t;
+  }
+}
+
 // SH basis gradients (sh.cpp:44-72), fp64.
 __device__ void sh_basis_grad(int degree, double x, double y, double z, double* g /*16*3*/) {
   const double C1 = 0.4886025119029199;
@@ -597,11 +766,11 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     bp.tile_pose = ws.pose_part;
     if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
     if (a.seed_mode == SEED_TRACK) {
-      if (nf == 6) k_backward<SEED_TRACK, 6, true><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
-      else k_backward<SEED_TRACK, 9, true><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
+      if (nf == 6) k_backward_pose<SEED_TRACK, false><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
+      else k_backward_pose<SEED_TRACK, true><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
     } else {
-      if (nf == 6) k_backward<SEED_EXPLICIT, 6, true><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
-      else k_backward<SEED_EXPLICIT, 9, true><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
+      if (nf == 6) k_backward_pose<SEED_EXPLICIT, false><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
+      else k_backward_pose<SEED_EXPLICIT, true><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
     }
     ++*L;
     if (ws.prof) ws.prof->end(st);

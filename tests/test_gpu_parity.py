@@ -215,6 +215,27 @@ def test_tracking_loss_vs_oracle(gpu_ctx, orc):
     assert np.abs(dc - odc).max() < 1e-7 and np.abs(dd - odd).max() < 1e-7
 
 
+@pytest.mark.parametrize("sh", [1, 4])
+def test_tracking_pose_gradient_vs_oracle(gpu_ctx, orc, sh):
+    """The fused tracking backward (per-primitive SE(3) Jacobians, lane-level pose accumulation)
+    against render -> evaluate_tracking_loss -> render_backward of the fp64 oracle."""
+    rng = np.random.default_rng(40 + sh)
+    for seed in range(4):
+        m = f32_round(orc.random_scene(3000 + seed, 200, sh))
+        K = make_intrinsics(64, 48, 55.0)
+        _upload(gpu_ctx, m)
+        gt = gpu_ctx.render(pose(), K)
+        gpu_ctx.frame_upload(0, gt.color, gt.alpha_depth, 64, 48)
+        p = perturbed(pose(), 0.01 * rng.standard_normal(6))
+        w = defaults_weights(True)
+        terms, g = gpu_ctx.tracking_gradient(0, p, K, w)
+        o = orc.render(m, p, K)
+        ot, odc, odd = orc.tracking_loss(o, gt.color.astype(np.float64), gt.alpha_depth.astype(np.float64), K, w)
+        go = orc.render_backward(m, p, K, o, d_color=odc.reshape(48, 64, 3), d_alpha_depth=odd.reshape(48, 64))
+        assert terms.total == pytest.approx(ot.total, rel=1e-5)
+        _pose_close(g, go.d_pose)
+
+
 def test_mapping_loss_kat_on_gpu(gpu_ctx, orc):
     """test_losses.cpp:169-198 through the CUDA path."""
     e = golden("reference_kats.json")["mapping_loss_single_pixel"]["expect"]
