@@ -18,6 +18,46 @@ constexpr int kFieldsBase = 11;       // mean 3, log_scale 3, quat 4, opacity 1;
 __host__ __device__ __forceinline__ int tile_lx(int tid) { return ((tid >> 5) & 1) * 8 + (tid & 7); }
 __host__ __device__ __forceinline__ int tile_ly(int tid) { return (tid >> 6) * 4 + ((tid >> 3) & 3); }
 
+// Conservative footprint test of one staged tile-list entry against the eight 8x4 warp blocks
+// of its tile.  Bit w is set unless every pixel centre of warp block w is certainly rejected by
+// the per-pair test (rho > cutoff + band, or sigma*exp(-rho/2) below the alpha skip); the
+// margins dwarf fp32 rounding, so the mask only removes work that would produce nothing and
+// never changes a result.  min over a rectangle of a x^2 + 2 b x y + c y^2 is attained at the
+// origin (if inside) or on an edge at the clamped stationary point.
+__device__ __forceinline__ float quad_min_rect(float a, float b, float c, float x0, float x1, float y0, float y1) {
+  if (x0 <= 0.0f && x1 >= 0.0f && y0 <= 0.0f && y1 >= 0.0f) return 0.0f;
+  float m = 3.0e38f;
+  const float ia = 1.0f / a, ic = 1.0f / c;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const float X = e ? x1 : x0;
+    const float y = fminf(fmaxf(-b * X * ic, y0), y1);
+    m = fminf(m, a * X * X + 2.0f * b * X * y + c * y * y);
+    const float Y = e ? y1 : y0;
+    const float x = fminf(fmaxf(-b * Y * ia, x0), x1);
+    m = fminf(m, a * x * x + 2.0f * b * x * Y + c * Y * Y);
+  }
+  return m;
+}
+
+__device__ __forceinline__ uint32_t warp_block_mask(const BlendG& g, float tile_x0, float tile_y0, const BlendConsts& kc) {
+  const float a = g.c00, b = 0.5f * g.c01x2, c = g.c11;
+  if (!(a > 0.0f) || !(c > 0.0f) || !(a * c > b * b)) return 0xffu;
+  if (g.sigma < kc.skip_lo) return 0u;   // sigma * g <= sigma < skip: nothing can contribute
+  float thr = kc.rho_hi;
+  const float ra = 2.0f * __logf(g.sigma / kc.skip_lo);   // rho beyond which alpha < skip
+  thr = fminf(thr, ra);
+  thr = thr * 1.002f + 2e-3f;
+  uint32_t mask = 0u;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const float bx0 = tile_x0 + static_cast<float>(8 * (w & 1)) + 0.5f - g.mx;
+    const float by0 = tile_y0 + static_cast<float>(4 * (w >> 1)) + 0.5f - g.my;
+    if (quad_min_rect(a, b, c, bx0, bx0 + 7.0f, by0, by0 + 3.0f) <= thr) mask |= 1u << w;
+  }
+  return mask;
+}
+
 // Loss partial slots written per tile by the fused blend epilogue (fixed order reduction).
 enum LossSlot {
   LS_COLOR_SUM = 0,   // sum |c - I| over the colour mask (tracking: opacity mask, mapping: all)

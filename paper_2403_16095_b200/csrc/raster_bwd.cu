@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
   __shared__ BlendG s_g[kBwdBatch];
   __shared__ int32_t s_rank[kBwdBatch];
   __shared__ int32_t s_id[kBwdBatch];
+  __shared__ uint8_t s_mask[kBwdBatch];
   __shared__ uint32_t s_orig[kBwdBatch];
   __shared__ float s_part[8][kBwdBatch][NF];
   __shared__ int s_wmax[8];
@@ -167,13 +168,19 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
     if (tid < cnt) {
       const uint32_t orig = bp.sorted_orig[bstart + tid];
       const int r = static_cast<int>(bp.pair_rank[orig]);
-      s_g[tid] = bp.bg[r];
+      const BlendG gj = bp.bg[r];
+      s_g[tid] = gj;
       s_rank[tid] = r;
       s_id[tid] = bp.rank_to_id[r];
       s_orig[tid] = orig;
+      s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, static_cast<float>(tx * kTile), static_cast<float>(ty * kTile), kc));
     }
     __syncthreads();
     for (int k = cnt - 1; k >= 0; --k) {
+      if (!((s_mask[k] >> warp) & 1u)) {   // footprint cannot reach this warp's block
+        if (lane < NF) s_part[warp][k][lane] = 0.0f;
+        continue;
+      }
       const int li = bstart + k - rg.x;
       float f[NF];
 #pragma unroll
@@ -343,6 +350,7 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
   __shared__ float4 s_pj[kPoseBatch][9];
   __shared__ int32_t s_rank[kPoseBatch];
   __shared__ int32_t s_id[kPoseBatch];
+  __shared__ uint8_t s_mask[kPoseBatch];
   __shared__ int s_wmax[8];
   __shared__ double s_pred[8][6];
   const int tile = blockIdx.x;
@@ -364,6 +372,7 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
 #pragma unroll
   for (int w = 0; w < 8; ++w) maxlast = max(maxlast, s_wmax[w]);
   const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
+  const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
   float T = pb.T, S = 0.0f;
   double pd[6] = {0, 0, 0, 0, 0, 0};
   const int end = rg.x + maxlast;
@@ -372,9 +381,11 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
     const int cnt = bend - bstart;
     if (tid < cnt) {
       const int r = static_cast<int>(bp.pair_rank[bp.sorted_orig[bstart + tid]]);
-      s_g[tid] = bp.bg[r];
+      const BlendG gj = bp.bg[r];
+      s_g[tid] = gj;
       s_rank[tid] = r;
       s_id[tid] = bp.rank_to_id[r];
+      s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, tile_x0, tile_y0, kc));
     }
     __syncthreads();
     for (int i = tid; i < cnt * 9; i += 256) {
@@ -383,7 +394,14 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
     }
     __syncthreads();
     float pf0 = 0.f, pf1 = 0.f, pf2 = 0.f, pf3 = 0.f, pf4 = 0.f, pf5 = 0.f;
-    for (int k = cnt - 1; k >= 0; --k) {
+    // back to front over only the entries whose footprint can reach this warp's block
+    for (int c0 = ((cnt - 1) >> 5) << 5; c0 >= 0; c0 -= 32) {
+     const int kk = c0 + lane;
+     uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
+     while (bits) {
+      const int j = 31 - __clz(bits);
+      bits &= ~(1u << j);
+      const int k = c0 + j;
       const int li = bstart + k - rg.x;
       if (li >= pb.last) continue;
       const BlendG g = s_g[k];
@@ -433,6 +451,7 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
       pf3 += t0;
       pf4 += t1;
       pf5 += t2;
+     }
     }
     pd[0] += pf0; pd[1] += pf1; pd[2] += pf2; pd[3] += pf3; pd[4] += pf4; pd[5] += pf5;
     __syncthreads();

@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
   __shared__ BlendG s_g[256];
   __shared__ int32_t s_rank[256];
   __shared__ int32_t s_id[256];
+  __shared__ uint8_t s_mask[256];
   __shared__ double s_red[8][LS_NUM];
   if (ds->halt) return;
   const int tile = blockIdx.x;
@@ -294,21 +295,33 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
     obs_valid = depth_valid(ov, near_plane, far_plane);
   }
   const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
+  const int lane = tid & 31, warp = tid >> 5;
+  const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
   for (int start = rg.x; start < rg.y; start += 256) {
     if (__syncthreads_and(s.done)) break;
     const int j = start + tid;
     if (j < rg.y) {
       const int r = static_cast<int>(pair_rank[sorted_orig[j]]);
-      s_g[tid] = bg[r];
+      const BlendG gj = bg[r];
+      s_g[tid] = gj;
       s_rank[tid] = r;
       s_id[tid] = rank_to_id[r];
+      s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, tile_x0, tile_y0, kc));
     }
     __syncthreads();
     const int cnt = min(256, rg.y - start);
-    for (int k = 0; k < cnt && !s.done; ++k) {
-      const BlendG g = s_g[k];
-      const PairEval e = eval_pair(px, py, g, gg + s_rank[k], kc);
-      if (e.code) pixel_accumulate(s, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+    // each warp walks only the entries whose footprint can reach its 8x4 block, in list order
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int kk = c0 + lane;
+      uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
+      while (bits) {
+        const int k = c0 + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        if (s.done) continue;
+        const BlendG g = s_g[k];
+        const PairEval e = eval_pair(px, py, g, gg + s_rank[k], kc);
+        if (e.code) pixel_accumulate(s, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+      }
     }
   }
   if (inside) {
@@ -335,7 +348,6 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
   if (inside)
     loss_pixel<LMODE>(v, s.cr, s.cg, s.cb, s.ad, s.med_depth, s.median >= 0, s.op, s.unc, loss_rgb + 3 * pi, loss_depth, pi,
                       obs != nullptr, near_plane, far_plane, lp.opacity_floor);
-  const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
   for (int q = 0; q < LS_NUM; ++q) {
     const double t = warp_sum_d(v[q]);
