@@ -84,11 +84,12 @@ extern "C" int mir_render(const gsf_map_host* map, const gsf_pose* pose, const g
   out->num_pairs = total;
   std::vector<BlendG> bg(V);
   std::vector<GuardG> gg(V);
+  const BlendConsts kc = make_blend_consts(rp);
   for (int r = 0; r < V; ++r) {
     bg[r] = make_blend_g(pre[vis[r]]);
+    bg[r].pad0 = blend_rho_fast(bg[r].sigma, kc);
     gg[r] = make_guard_g(pre[vis[r]]);
   }
-  const BlendConsts kc = make_blend_consts(rp);
   for (int t = 0; t < ntiles; ++t) {
     const int tx = t % rp.tiles_x, ty = t / rp.tiles_x;
     for (int y = ty * ts; y < std::min(H, (ty + 1) * ts); ++y)

@@ -424,7 +424,7 @@ GSF_HD BlendG make_blend_g(const PreOut& o) {
   g.c00 = static_cast<float>(o.c00);
   g.c01x2 = static_cast<float>(dmul(2.0, o.c01));
   g.c11 = static_cast<float>(o.c11);
-  g.pad0 = 0.0f;
+  g.pad0 = -1.0f;   // rho_fast, filled by blend_rho_fast once the raster constants are known
   g.r = static_cast<float>(o.color[0]);
   g.g = static_cast<float>(o.color[1]);
   g.b = static_cast<float>(o.color[2]);
@@ -528,9 +528,39 @@ GSF_HD PairEval eval_pair_full(float px, float py, const BlendG& g, const GuardG
   return e;
 }
 
-// Same decisions as eval_pair_full; the common cases (clearly outside, clearly inside and away
-// from the alpha thresholds) are resolved inline and only band cases take the fp64 path.
-// `gp` is only dereferenced on that path.
+// exp_f without the range guards: only called on the fast path, where -rho/2 lies in
+// (-cutoff/2, 0] and cutoff < 170, so the guards of exp_f can never trigger.  Same bits.
+GSF_HD float exp_f_inrange(float x) {
+  const float n = frint(fmul(x, 1.44269504f));
+  float r = ffma(n, -0.693145752f, x);
+  r = ffma(n, -1.42860677e-06f, r);
+  float p = 1.0f / 5040.0f;
+  p = ffma(p, r, 1.0f / 720.0f);
+  p = ffma(p, r, 1.0f / 120.0f);
+  p = ffma(p, r, 1.0f / 24.0f);
+  p = ffma(p, r, 1.0f / 6.0f);
+  p = ffma(p, r, 0.5f);
+  p = ffma(p, r, 1.0f);
+  p = ffma(p, r, 1.0f);
+  const int ni = static_cast<int>(n);
+  return fmul(p, bitsf((127 + ni) << 23));
+}
+
+// Per-primitive fast-path bound (stored in BlendG::pad0): for rho in [rho_min, rho_fast) the full
+// decision is certainly "contributes, unclamped, alpha = sigma*exp_f(-rho/2)" — rho is below the
+// guard band, alpha is above the skip band (margin 1e-5 in log space, >> exp_f's 1-ulp error)
+// and sigma is below the clamp band.  -1 disables the fast path.  Only selects the evaluation
+// path, never a result, so the mirror and the kernels stay bit-identical either way.
+GSF_HD float blend_rho_fast(float sigma, const BlendConsts& k) {
+  if (!k.fast_ok || !(static_cast<double>(sigma) * (1.0 + 1e-6) < static_cast<double>(k.clamp_lo))) return -1.0f;
+  if (!(sigma > k.skip_hi)) return -1.0f;
+  const double ra = 2.0 * (log(static_cast<double>(sigma) / static_cast<double>(k.skip_hi)) - 1e-5);
+  const double r = ra < static_cast<double>(k.rho_lo) ? ra : static_cast<double>(k.rho_lo);
+  return r > 0.0 ? static_cast<float>(r * (1.0 - 1e-6)) : -1.0f;
+}
+
+// Same decisions as eval_pair_full; the common cases are resolved inline and only band cases
+// take the fp64 path.  `gp` is only dereferenced on that path.
 GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
   PairEval e;
   e.dx = fsub(px, g.mx);
@@ -541,21 +571,11 @@ GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp,
   e.alpha = 0.0f;
   e.gval = 0.0f;
   if (rho > k.rho_hi) return e;
-  if (k.fast_ok && rho < k.rho_lo && rho >= k.rho_min) {
-    e.gval = exp_f(fmul(-0.5f, rho));
-    const float raw = fmul(g.sigma, e.gval);
-    if (raw < k.skip_lo) return e;
-    if (raw > k.skip_hi && raw < k.clamp_lo) {
-      e.alpha = raw;
-      e.code = 1;
-      return e;
-    }
-    if (raw > k.clamp_hi && raw > k.skip_hi) {
-      e.alpha = k.clamp;
-      e.clamped = 1;
-      e.code = 1;
-      return e;
-    }
+  if (rho < g.pad0 && rho >= k.rho_min) {
+    e.gval = exp_f_inrange(fmul(-0.5f, rho));
+    e.alpha = fmul(g.sigma, e.gval);
+    e.code = 1;
+    return e;
   }
   return eval_pair_full(px, py, g, gp, k);
 }
@@ -602,6 +622,22 @@ GSF_HD void pixel_accumulate(PixelState& s, const BlendG& g, const PairEval& e, 
     s.med_depth = g.depth;
   }
   s.T = t_next;
+  if (s.T < k.term) s.done = 1;
+}
+
+// Tracking variant: only the maps the tracking loss and the pose backward read (colour, alpha
+// depth, opacity, T, last contributor).  Same operations in the same order as pixel_accumulate
+// for those fields, so the values are identical to a full render's.
+GSF_HD void pixel_accumulate_min(PixelState& s, const BlendG& g, const PairEval& e, int32_t list_index,
+                                 const BlendConsts& k) {
+  const float w = fmul(e.alpha, s.T);
+  s.cr = ffma(w, g.r, s.cr);
+  s.cg = ffma(w, g.g, s.cg);
+  s.cb = ffma(w, g.b, s.cb);
+  s.ad = ffma(w, g.depth, s.ad);
+  s.op = fadd(s.op, w);
+  s.last = list_index + 1;
+  s.T = fmul(s.T, fsub(1.0f, e.alpha));
   if (s.T < k.term) s.done = 1;
 }
 

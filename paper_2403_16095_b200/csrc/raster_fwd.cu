@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ pa
                                                     uint32_t* __restrict__ key_id, BlendG* __restrict__ bg_id,
                                                     GuardG* __restrict__ gg_id, double* __restrict__ depth_id,
                                                     int4* __restrict__ rect_id, uint8_t* __restrict__ visible,
-                                                    int32_t* bad_index) {
+                                                    int32_t* bad_index, BlendConsts kc) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= P) return;
   // validate_primitives (rasterizer.cpp:34-44): every field finite and |q| > 1e-12
@@ -158,7 +158,9 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ pa
   flag[i] = static_cast<uint32_t>(o.visible);
   if (!o.visible) return;
   key_id[i] = depth_key(o.depth, near_bits);
-  bg_id[i] = make_blend_g(o);
+  BlendG g = make_blend_g(o);
+  g.pad0 = blend_rho_fast(g.sigma, kc);
+  bg_id[i] = g;
   gg_id[i] = make_guard_g(o);
   depth_id[i] = o.depth;
   rect_id[i] = make_int4(o.tx0, o.tx1, o.ty0, o.ty1);
@@ -320,7 +322,12 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
         if (s.done) continue;
         const BlendG g = s_g[k];
         const PairEval e = eval_pair(px, py, g, gg + s_rank[k], kc);
-        if (e.code) pixel_accumulate(s, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+        if (e.code) {
+          if (LMODE == 1)
+            pixel_accumulate_min(s, g, e, start + k - rg.x, kc);
+          else
+            pixel_accumulate(s, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+        }
       }
     }
   }
@@ -329,16 +336,18 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
     o_color[3 * pi + 1] = s.cg;
     o_color[3 * pi + 2] = s.cb;
     o_ad[pi] = s.ad;
-    o_md[pi] = s.med_depth;
-    o_mv[pi] = s.median >= 0 ? 1 : 0;
     o_op[pi] = s.op;
-    o_unc[pi] = s.unc;
     o_T[pi] = s.T;
-    o_count[pi] = s.count;
-    o_dom[pi] = s.dominant;
-    o_med[pi] = s.median;
-    o_domw[pi] = s.best;
     o_last[pi] = s.last;
+    if (LMODE != 1) {   // tracking reads none of these
+      o_md[pi] = s.med_depth;
+      o_mv[pi] = s.median >= 0 ? 1 : 0;
+      o_unc[pi] = s.unc;
+      o_count[pi] = s.count;
+      o_dom[pi] = s.dominant;
+      o_med[pi] = s.median;
+      o_domw[pi] = s.best;
+    }
   }
   if (LMODE == 0) return;
   // fused loss epilogue: per-tile residual sums and mask counts (deterministic tree)
@@ -419,7 +428,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   if (pf) pf->begin(PROF_PREPROCESS, st);
   if (P > 0) {
     k_preprocess<<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, near_bits, ws.flag, ws.key_id, ws.bg_id, ws.gg_id,
-                                                 ws.depth_id, ws.rect_id, ws.visible, &ds->bad_index);
+                                                 ws.depth_id, ws.rect_id, ws.visible, &ds->bad_index, a.kc);
     ++*L;
   }
   if (pf) pf->end(st);
