@@ -340,10 +340,7 @@ def run_mapping(args, ctx, rank, world, device):
         c, d = noisy(r.color, r.alpha_depth, f)
         mctx.frame_upload(j, c, d, W, H)
     if world > 1:
-        uid = api.comm_unique_id() if rank == 0 else bytes(128)
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        mctx.comm_init(world, rank, obj[0])
+        mctx.comm_setup()
     mc = abi.defaults_mapper()
     mc.densify_interval = 0
     tc = abi.defaults_tracker()

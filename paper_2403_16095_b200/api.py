@@ -367,6 +367,13 @@ class Context:
         arr = (C.c_uint8 * 128)(*uid)
         self._check(self.lib.gsf_comm_init(self.h, nranks, rank, C.byref(arr)))
 
+    def comm_setup(self, group=None):
+        """Join this context to the torch.distributed job: rank 0 draws the NCCL unique id, it is
+        broadcast over `group` (any backend), then every rank calls gsf_comm_init."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.comm_init(world, rank, exchange_unique_id(group))
+
 
 def comm_unique_id() -> bytes:
     lib = abi.load()
@@ -375,6 +382,19 @@ def comm_unique_id() -> bytes:
     if rc != GSF_OK:
         raise GsfError(rc, "ncclGetUniqueId failed")
     return bytes(arr)
+
+
+def exchange_unique_id(group=None) -> bytes:
+    """Rank 0's NCCL unique id, broadcast to every rank of `group` over torch.distributed."""
+    import torch.distributed as dist
+    if dist.get_world_size(group) == 1:
+        return bytes(128)
+    obj = [comm_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    uid = obj[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise GsfError(GSF_EINVAL, "comm_setup: malformed NCCL unique id")
+    return bytes(uid)
 
 
 def ba_partition(n: int, nranks: int, rank: int) -> np.ndarray:
