@@ -190,7 +190,7 @@ def run_ours(args):
     stat = ctx.render(starts[1], K)
     npix = W * H
     tiles_x, tiles_y = (W + 15) // 16, (H + 15) // 16
-    r2i, tr, pr = ctx.render_tiles(stat.num_visible, tiles_x * tiles_y, stat.num_pairs)
+    tr, _ = ctx.render_tiles(tiles_x * tiles_y, stat.num_pairs)
     tile_len = (tr[:, 1] - tr[:, 0]).astype(np.float64)
     tile_pix = np.array([min(16, W - (t % tiles_x) * 16) * min(16, H - (t // tiles_x) * 16)
                          for t in range(tiles_x * tiles_y)], np.float64)
@@ -299,7 +299,7 @@ def run_ours(args):
         "config": {"workload": "configs[1]: tracking loop, Replica-shaped 1200x680, ~500k Gaussians, "
                                "uncertainty-based primitive selection, 1 B200",
                    "primitives": int(m.count), "iterations_per_frame": args.iters, "width": W, "height": H,
-                   "visible": int(stat.num_visible), "pairs": int(stat.num_pairs),
+                   "visible": int(stat.num_visible), "pairs": int(stat.num_pairs), "max_tile_list": int(tile_len.max()),
                    "traversed_pairs": traversed, "contributors": contributors,
                    "uncertainty_observed": observed, "uncertainty_pruned": pruned,
                    "l2": "working set (~0.1 GB) is L2-resident across steps; no flush (latency-bound loop)",

@@ -205,12 +205,13 @@ int gsf_render_backward(gsf_ctx ctx, const gsf_upstream* up, const float* observ
 int gsf_render_record(gsf_ctx ctx, uint32_t* row_start, int32_t* prim, float* alpha,
                       float* transmittance, int64_t* total);
 
-/* Tile binning of the most recent render, for bit-exact checks of the hand-written sort:
- * rank_to_id[V] (global (depth, id) order, rasterizer.cpp:69-79), tile_range[2*tiles]
- * ([start, end) into the pair list) and pair_rank[M] (tile lists, rasterizer.cpp:199-212).
+/* Tile binning of the most recent render, for bit-exact checks of the binning:
+ * tile_range[2*tiles] ([start, end) into the pair list; [0, 0) for an empty tile) and
+ * pair_prim[M] (every tile list as primitive ids in (depth, id) order: the tile_lists of
+ * rasterizer.cpp:193-212 built from sorted_visible, :69-79).
  * Any pointer may be NULL; capacities are checked against the counts of gsf_render_out. */
-int gsf_render_tiles(gsf_ctx ctx, int32_t* rank_to_id, int64_t rank_cap, int32_t* tile_range,
-                     int64_t tiles_cap, int32_t* pair_rank, int64_t pair_cap);
+int gsf_render_tiles(gsf_ctx ctx, int32_t* tile_range, int64_t tiles_cap, int32_t* pair_prim,
+                     int64_t pair_cap);
 
 /* ---- losses (loss/losses.hpp:77-94) over the most recent render ----------------------- */
 int gsf_tracking_loss(gsf_ctx ctx, const float* target_rgb, const float* observed_depth,

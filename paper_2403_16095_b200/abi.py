@@ -120,7 +120,7 @@ SIGNATURES = {
                              C.POINTER(RasterCfg), C.POINTER(RenderOut)]),
     "gsf_render_backward": (C.c_int, [C.c_void_p, C.POINTER(Upstream), fp, C.POINTER(GradsOut)]),
     "gsf_render_record": (C.c_int, [C.c_void_p, u32p, i32p, fp, fp, i64p]),
-    "gsf_render_tiles": (C.c_int, [C.c_void_p, i32p, C.c_int64, i32p, C.c_int64, i32p, C.c_int64]),
+    "gsf_render_tiles": (C.c_int, [C.c_void_p, i32p, C.c_int64, i32p, C.c_int64]),
     "gsf_tracking_loss": (C.c_int, [C.c_void_p, fp, fp, C.POINTER(LossWeights),
                                     C.POINTER(LossTerms), fp, fp]),
     "gsf_mapping_loss": (C.c_int, [C.c_void_p, fp, fp, C.POINTER(LossWeights),

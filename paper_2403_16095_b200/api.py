@@ -229,14 +229,12 @@ class Context:
         return RenderResult(**o, has_uncertainty=bool(ro.has_uncertainty), num_visible=int(ro.num_visible),
                             num_pairs=int(ro.num_pairs))
 
-    def render_tiles(self, num_visible: int, num_tiles: int, num_pairs: int):
-        """(rank_to_id, tile_range (tiles,2), pair_rank) of the last render (bit-exact binning checks)."""
-        r2i = np.zeros(max(num_visible, 1), np.int32)
+    def render_tiles(self, num_tiles: int, num_pairs: int):
+        """(tile_range (tiles, 2), pair_prim) of the last render: every tile list as primitive ids."""
         tr = np.zeros(2 * max(num_tiles, 1), np.int32)
-        pr = np.zeros(max(num_pairs, 1), np.int32)
-        self._check(self.lib.gsf_render_tiles(self.h, _ptr(r2i, C.c_int32), r2i.size, _ptr(tr, C.c_int32), num_tiles,
-                                              _ptr(pr, C.c_int32), pr.size))
-        return r2i[:num_visible], tr[: 2 * num_tiles].reshape(-1, 2), pr[:num_pairs]
+        pp = np.zeros(max(num_pairs, 1), np.int32)
+        self._check(self.lib.gsf_render_tiles(self.h, _ptr(tr, C.c_int32), num_tiles, _ptr(pp, C.c_int32), pp.size))
+        return tr[: 2 * num_tiles].reshape(-1, 2), pp[:num_pairs]
 
     def render_record(self):
         """CSR BlendRecord of the last render: (row_start, prim, alpha, transmittance)."""

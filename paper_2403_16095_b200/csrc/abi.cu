@@ -248,27 +248,26 @@ void ensure_map(gsf_ctx_s* c, int64_t P, int K) {
   c->D = D;
 }
 
+void alloc_pairs(Workspace& ws) {
+  dalloc(ws.ukey, ws.pair_cap);
+  dalloc(ws.skey, ws.pair_cap); dalloc(ws.sid, ws.pair_cap);
+  dalloc(ws.partials, ws.pair_cap * 10);
+}
+
 void ensure_ws(gsf_ctx_s* c, int W, int H) {
   Workspace& ws = c->ws;
   const int64_t P = std::max<int64_t>(c->P, 1);
   const int64_t npix = static_cast<int64_t>(W) * H;
   const int64_t tiles = static_cast<int64_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
   if (P > ws.P_cap) {
-    dalloc(ws.flag, P); dalloc(ws.vis_off, P); dalloc(ws.key_id, P);
     dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
-    for (int i = 0; i < 2; ++i) { dalloc(ws.skeys[i], P); dalloc(ws.svals[i], P); }
-    dalloc(ws.rank_to_id, P); dalloc(ws.bg, P); dalloc(ws.gg, P); dalloc(ws.rect, P); dalloc(ws.tile_cnt, P);
-    dalloc(ws.pair_off, P + 1);
     dalloc(ws.pj_id, static_cast<size_t>(P) * 36);
+    dalloc(ws.big_ids, P);
     ws.P_cap = P;
     dfree(ws.pose_part);
   }
   if (ws.pair_cap == 0) ws.pair_cap = std::max<int64_t>(1 << 20, 4 * P);
-  if (!ws.pkeys[0]) {
-    for (int i = 0; i < 2; ++i) { dalloc(ws.pkeys[i], ws.pair_cap); dalloc(ws.pvals[i], ws.pair_cap); }
-    dalloc(ws.pair_rank, ws.pair_cap);
-    dalloc(ws.partials, ws.pair_cap * 10);
-  }
+  if (!ws.ukey) alloc_pairs(ws);
   if (npix > ws.npix_cap) {
     dalloc(ws.color, 3 * npix); dalloc(ws.alpha_depth, npix); dalloc(ws.median_depth, npix); dalloc(ws.median_valid, npix);
     dalloc(ws.opacity, npix); dalloc(ws.uncertainty, npix); dalloc(ws.final_T, npix); dalloc(ws.count, npix);
@@ -278,22 +277,16 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   }
   if (tiles > ws.tiles_cap) {
     dalloc(ws.ranges, tiles);
+    dalloc(ws.bins, tiles * std::max(kBinStride, 2) + kCntNum);
+    dalloc(ws.tile_start, tiles);
+    ws.tile_cnt = ws.bins;
+    ws.tile_fill = kBinStride == 1 ? ws.bins + tiles : ws.bins + 1;
+    ws.bin_counters = ws.bins + tiles * std::max(kBinStride, 2);
     dalloc(ws.loss_part, tiles * LS_NUM);
     ws.tiles_cap = tiles;
     dfree(ws.pose_part);
   }
   if (!ws.pose_part) dalloc(ws.pose_part, static_cast<size_t>(std::max<int64_t>(div_up(ws.P_cap, 256), ws.tiles_cap)) * 6);
-  const int64_t scan_n = std::max<int64_t>(P, npix);
-  const size_t sb = scan_temp_bytes(static_cast<uint32_t>(scan_n));
-  const size_t rb = std::max(radix_temp_bytes(static_cast<uint32_t>(P), 4), radix_temp_bytes(static_cast<uint32_t>(ws.pair_cap), 4));
-  // scan state and radix temp are sized for the largest of P / npix / pair_cap
-  if (!ws.scan.state || ws.radix_temp_bytes < rb + sb) {
-    dfree(ws.scan.state);
-    dfree(ws.radix_temp);
-    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ws.scan.state), sb + 64));
-    GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ws.radix_temp), rb));
-    ws.radix_temp_bytes = rb + sb;
-  }
   const int64_t red = 2 * std::max<int64_t>(div_up(npix, 256), div_up(P, 256)) + 64;
   if (!ws.red_part || ws.red_iso_offset * 2 < red) {
     dalloc(ws.red_part, red);
@@ -305,12 +298,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
 void grow_pairs(gsf_ctx_s* c, uint32_t needed) {
   Workspace& ws = c->ws;
   ws.pair_cap = static_cast<int64_t>(needed) + needed / 4 + 1024;
-  for (int i = 0; i < 2; ++i) { dalloc(ws.pkeys[i], ws.pair_cap); dalloc(ws.pvals[i], ws.pair_cap); }
-  dalloc(ws.pair_rank, ws.pair_cap);
-  dalloc(ws.partials, ws.pair_cap * 10);
-  const size_t rb = std::max(radix_temp_bytes(static_cast<uint32_t>(ws.P_cap), 4), radix_temp_bytes(static_cast<uint32_t>(ws.pair_cap), 4));
-  dfree(ws.radix_temp);
-  GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&ws.radix_temp), rb));
+  alloc_pairs(ws);
 }
 
 FwdArgs fwd_args(gsf_ctx_s* c, const gsf_intrinsics& k, const gsf_raster_cfg& cfg, const float* obs, const float* loss_rgb,
@@ -543,10 +531,8 @@ __global__ void k_gather_map_aos(const float* __restrict__ params, int64_t P, in
 __global__ void k_add_d(double* acc, const double* v) { *acc += *v; }
 
 // CSR record of the last render (rasterizer.cpp:240-259): per-pixel contributors front to back.
-__global__ void k_record(const int2* __restrict__ ranges, const uint32_t* __restrict__ sorted_orig,
-                         const uint32_t* __restrict__ pair_rank, const BlendG* __restrict__ bg,
-                         const GuardG* __restrict__ gg, const int32_t* __restrict__ rank_to_id,
-                         const int32_t* __restrict__ last, const uint32_t* __restrict__ row_start, int W, int H, int tiles_x,
+__global__ void k_record(const int2* __restrict__ ranges, const uint32_t* __restrict__ sid,
+                         const BlendG* __restrict__ bg, const GuardG* __restrict__ gg, const int32_t* __restrict__ last, const uint32_t* __restrict__ row_start, int W, int H, int tiles_x,
                          BlendConsts kc, int32_t* __restrict__ prim, float* __restrict__ alpha, float* __restrict__ trans) {
   const int64_t pi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (pi >= static_cast<int64_t>(W) * H) return;
@@ -558,10 +544,10 @@ __global__ void k_record(const int2* __restrict__ ranges, const uint32_t* __rest
   uint32_t out = row_start[pi];
   float T = 1.0f;
   for (int j = 0; j < lim; ++j) {
-    const int r = static_cast<int>(pair_rank[sorted_orig[rg.x + j]]);
-    const PairEval e = eval_pair(px, py, bg[r], gg + r, kc);
+    const int id = static_cast<int>(sid[rg.x + j]);
+    const PairEval e = eval_pair(px, py, bg[id], gg + id, kc);
     if (!e.code) continue;
-    prim[out] = rank_to_id[r];
+    prim[out] = id;
     alpha[out] = e.alpha;
     trans[out] = T;
     ++out;
@@ -605,12 +591,10 @@ int gsf_ctx_destroy(gsf_ctx c) {
   cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   Workspace& ws = c->ws;
-  void* bufs[] = {ws.flag, ws.vis_off, ws.key_id, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id, ws.visible,
-                  ws.skeys[0], ws.skeys[1], ws.svals[0], ws.svals[1], ws.rank_to_id, ws.bg, ws.gg, ws.rect,
-                  ws.tile_cnt, ws.pair_off, ws.pkeys[0], ws.pkeys[1], ws.pvals[0], ws.pvals[1], ws.pair_rank,
-                  ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
+  void* bufs[] = {ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
+                  ws.ukey, ws.skey, ws.sid, ws.big_ids, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
-                  ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.scan.state, ws.radix_temp, ws.pose_part, ws.pj_id,
+                  ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.pj_id,
                   ws.red_part, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
                   c->red_f};
@@ -825,8 +809,8 @@ int gsf_render_record(gsf_ctx c, uint32_t* row_start, int32_t* prim, float* alph
     GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&d_t), sizeof(float) * std::max<uint64_t>(acc, 1)));
     GSF_CUDA_CHECK(cudaMemcpy(d_rs, rs.data(), sizeof(uint32_t) * (npix + 1), cudaMemcpyHostToDevice));
     const RasterParams rp = make_rp(c, c->rK, c->rcfg);
-    k_record<<<div_up(npix, 256), 256, 0, c->stream>>>(c->ws.ranges, c->ws.pair_sorted_vals, c->ws.pair_rank, c->ws.bg,
-                                                        c->ws.gg, c->ws.rank_to_id, c->ws.last, d_rs, W, H, rp.tiles_x,
+    k_record<<<div_up(npix, 256), 256, 0, c->stream>>>(c->ws.ranges, c->ws.sid, c->ws.bg_id, c->ws.gg_id, c->ws.last, d_rs, W, H,
+                                                        rp.tiles_x,
                                                         make_blend_consts(rp), d_prim, d_a, d_t);
     ++c->launches;
     sync(c);
@@ -839,30 +823,19 @@ int gsf_render_record(gsf_ctx c, uint32_t* row_start, int32_t* prim, float* alph
   });
 }
 
-int gsf_render_tiles(gsf_ctx c, int32_t* rank_to_id, int64_t rank_cap, int32_t* tile_range, int64_t tiles_cap,
-                     int32_t* pair_rank, int64_t pair_cap) {
+int gsf_render_tiles(gsf_ctx c, int32_t* tile_range, int64_t tiles_cap, int32_t* pair_prim, int64_t pair_cap) {
   return guard(c, [&] {
     if (!c->have_render) throw EInval("render_tiles: no render on this context");
     read_state(c);
-    const uint32_t V = c->ds_host->V, M = c->ds_host->M;
+    const uint32_t M = c->ds_host->M;
     const int tiles = ((c->rK.width + kTile - 1) / kTile) * ((c->rK.height + kTile - 1) / kTile);
-    if (rank_to_id) {
-      if (rank_cap < V) throw EInval("render_tiles: rank capacity too small");
-      GSF_CUDA_CHECK(cudaMemcpy(rank_to_id, c->ws.rank_to_id, sizeof(int32_t) * V, cudaMemcpyDeviceToHost));
-    }
     if (tile_range) {
       if (tiles_cap < tiles) throw EInval("render_tiles: tile capacity too small");
       GSF_CUDA_CHECK(cudaMemcpy(tile_range, c->ws.ranges, sizeof(int2) * tiles, cudaMemcpyDeviceToHost));
     }
-    if (pair_rank) {
+    if (pair_prim && M) {
       if (pair_cap < M) throw EInval("render_tiles: pair capacity too small");
-      std::vector<uint32_t> orig(M), pr(std::max<uint32_t>(M, 1));
-      if (M) {
-        GSF_CUDA_CHECK(cudaMemcpy(orig.data(), c->ws.pair_sorted_vals, sizeof(uint32_t) * M, cudaMemcpyDeviceToHost));
-        std::vector<uint32_t> rank_of(M);
-        GSF_CUDA_CHECK(cudaMemcpy(rank_of.data(), c->ws.pair_rank, sizeof(uint32_t) * M, cudaMemcpyDeviceToHost));
-        for (uint32_t s = 0; s < M; ++s) pair_rank[s] = static_cast<int32_t>(rank_of[orig[s]]);
-      }
+      GSF_CUDA_CHECK(cudaMemcpy(pair_prim, c->ws.sid, sizeof(int32_t) * M, cudaMemcpyDeviceToHost));
     }
   });
 }
@@ -1078,19 +1051,24 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
   const LossParams lp = make_lp(1, &w, rcfg);
   const int tiles = ((k.width + kTile - 1) / kTile) * ((k.height + kTile - 1) / kTile);
   const int64_t npix = static_cast<int64_t>(k.width) * k.height;
+  // per iteration: forward (its last CTA finalises the loss), pose backward (its last CTA sums
+  // the pose gradient) and the single-thread pose step
   for (int it = 0; it < tcfg.iterations; ++it) {
     FwdArgs fa = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it);
     fa.want_posejac = true;
+    fa.fuse_loss_final = true;
     run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
-    run_loss_finalize(c->ws, c->ds, lp, tiles, npix, it, c->stream, &c->launches);
     BwdArgs b = bwd_args(c, k, rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);
     b.fused_pose = true;
     run_backward(c->ws, c->ds, b, c->stream, &c->launches);
     run_track_update(c->ds, it, c->stream, &c->launches);
   }
   // final render + loss without gradients (tracker.cpp:74-76)
-  run_forward(c->ws, c->ds, fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, -1), c->stream, &c->launches);
-  run_loss_finalize(c->ws, c->ds, lp, tiles, npix, -1, c->stream, &c->launches);
+  FwdArgs fin = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, -1);
+  fin.fuse_loss_final = true;
+  run_forward(c->ws, c->ds, fin, c->stream, &c->launches);
+  (void)tiles;
+  (void)npix;
 }
 
 int gsf_track_frame(gsf_ctx c, int32_t slot, const gsf_pose* initial, const gsf_intrinsics* K, const gsf_tracker_cfg* tcfg,

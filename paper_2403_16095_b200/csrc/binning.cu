@@ -1,0 +1,306 @@
+// binning.cu — per-tile lists of the visible primitives in exact (depth, id) order.
+//
+// The reference sorts the visible ids globally by (fp64 depth, id) (sorted_visible,
+// rasterizer.cpp:69-79) and appends each one to every tile its footprint rectangle overlaps
+// (rasterizer.cpp:193-212), so every tile list is in global depth order.  Only the per-tile
+// order is observable, so the device bins first and sorts each tile's (short) list:
+//
+//   k_preprocess    (raster_fwd.cu) counts the visible primitives, histograms their tile
+//                   rectangles and lists the few primitives with more than kBigPairs tiles
+//   k_tile_scan     one CTA: exclusive scan of the tile counts -> list starts, pair total M
+//   k_scatter       every (tile, primitive) pair claims a slot of its tile; a warp flattens the
+//                   pairs of its 32 primitives over its lanes (order inside a tile is arbitrary)
+//   k_scatter_big   one 1024-thread CTA per listed large-footprint primitive, so a primitive
+//                   covering a thousand tiles does not serialise one warp
+//   k_tile_sort     one CTA per tile: 32-key runs sorted in registers (warp bitonic), then
+//                   pairwise run merges by rank (binary search in the partner run) in shared
+//                   memory; lists longer than kSortChunk are chunk-sorted and merged (merge path)
+//                   through global memory by the same CTA.  A final pass re-orders the rare runs
+//                   whose fp32 depths tie by the exact fp64 depth (then id).
+//
+// Sort key: (fp32 bits of the depth) << 32 | id, one 64-bit integer.  Positive floats order like
+// their bit patterns and fp32 rounding is monotone, so this is the reference order except inside
+// runs of equal fp32 depth, which the fix-up resolves with the fp64 depth.  Keys are unique (id),
+// so the result does not depend on the scatter order: deterministic.
+#include "kernels.h"
+
+namespace gsfk {
+
+namespace {
+
+constexpr int kSortChunk = 2048;   // longest list sorted entirely in shared memory (2 x 16 KB)
+
+__device__ __forceinline__ unsigned long long pair_key(double depth, uint32_t id) {
+  return (static_cast<unsigned long long>(static_cast<uint32_t>(__float_as_int(static_cast<float>(depth)))) << 32) | id;
+}
+
+__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__ cnt, int ntiles,
+                                                    uint32_t* __restrict__ start, const uint32_t* counters,
+                                                    uint32_t pair_cap, DevState* ds) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < ntiles; base += 1024) {
+    const int t = base + tid;
+    const uint32_t v = t < ntiles ? cnt[static_cast<int64_t>(t) * kBinStride] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = s_warp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      s_warp[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t incl = s_carry + (warp ? s_warp[warp - 1] : 0u) + x;
+    if (t < ntiles) start[t] = incl - v;
+    __syncthreads();
+    if (tid == 1023) s_carry = incl;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    ds->M = s_carry;
+    ds->V = counters[kCntVisible];
+    if (s_carry > pair_cap) ds->overflow = 1u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scatter(const uint8_t* __restrict__ visible, const int4* __restrict__ rect_id,
+                                                 const double* __restrict__ depth_id, int64_t P, int tiles_x,
+                                                 const uint32_t* __restrict__ start, uint32_t* __restrict__ fill,
+                                                 uint32_t pair_cap, unsigned long long* __restrict__ ukey) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool vis = i < P && visible[i];
+  int4 q = make_int4(0, -1, 0, -1);
+  unsigned long long key = 0ull;
+  if (vis) {
+    q = rect_id[i];
+    key = pair_key(depth_id[i], static_cast<uint32_t>(i));
+  }
+  const int w = q.y - q.x + 1;
+  int c = vis ? w * (q.w - q.z + 1) : 0;
+  if (c > kBigPairs) c = 0;   // listed by k_preprocess for k_scatter_big
+  const int excl = warp_excl_scan(c);
+  const int total = __shfl_sync(0xffffffffu, excl + c, 31);
+  for (int base = 0; base < total; base += 32) {
+    const int k = base + lane;
+    const int j = warp_owner(excl, k);   // lane whose pair range holds k
+    const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qy0 = __shfl_sync(0xffffffffu, q.z, j);
+    const int wj = __shfl_sync(0xffffffffu, w, j), ej = __shfl_sync(0xffffffffu, excl, j);
+    const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
+    if (k < total) {
+      const int r = k - ej;
+      const int row = r / wj;
+      const int64_t t = (qy0 + row) * tiles_x + qx0 + (r - row * wj);
+      const uint32_t pos = start[t] + atomicAdd(&fill[t * kBinStride], 1u);
+      if (pos < pair_cap) ukey[pos] = kj;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scatter_big(const uint32_t* __restrict__ big_ids, const uint32_t* counters,
+                                                      const int4* __restrict__ rect_id, const double* __restrict__ depth_id,
+                                                      int tiles_x, const uint32_t* __restrict__ start,
+                                                      uint32_t* __restrict__ fill, uint32_t pair_cap,
+                                                      unsigned long long* __restrict__ ukey) {
+  const uint32_t nbig = counters[kCntBig];
+  for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+    const uint32_t id = big_ids[b];
+    const int4 q = rect_id[id];
+    const unsigned long long key = pair_key(depth_id[id], id);
+    const int w = q.y - q.x + 1;
+    const int c = w * (q.w - q.z + 1);
+    for (int r = threadIdx.x; r < c; r += blockDim.x) {
+      const int row = r / w;
+      const int64_t t = (q.z + row) * tiles_x + q.x + (r - row * w);
+      const uint32_t pos = start[t] + atomicAdd(&fill[t * kBinStride], 1u);
+      if (pos < pair_cap) ukey[pos] = key;
+    }
+  }
+}
+
+// Ascending bitonic sort of 32 keys, one per lane, in registers.
+__device__ __forceinline__ unsigned long long warp_sort32(unsigned long long k) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      const unsigned long long p = __shfl_xor_sync(0xffffffffu, k, j);
+      const bool keep_min = ((lane & j) == 0) == ((lane & size) == 0 || size == 32);
+      k = keep_min ? min(k, p) : max(k, p);
+    }
+  }
+  return k;
+}
+
+// Number of keys of the sorted run r[0, len) below k (upper: at or below).
+__device__ __forceinline__ int run_rank(const unsigned long long* r, int len, unsigned long long k, bool upper) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int m = (lo + hi) >> 1;
+    const unsigned long long v = r[m];
+    if (upper ? v <= k : v < k)
+      lo = m + 1;
+    else
+      hi = m;
+  }
+  return lo;
+}
+
+// Sort n <= kSortChunk keys (src) into dst: register-sorted 32-runs, then pairwise merges by rank
+// in shared memory.  Padding (~0) sorts to the end; equal padding keys are separated by the
+// lower/upper rank rule of the two runs, so every element gets a distinct slot.
+__device__ void sort_chunk(const unsigned long long* src, unsigned long long* dst, int n,
+                           unsigned long long (*s_k)[kSortChunk]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int nruns = (n + 31) >> 5;
+  const int N = nruns << 5;
+  for (int r = warp; r < nruns; r += nwarps) {
+    const int i = (r << 5) + lane;
+    const unsigned long long k = warp_sort32(i < n ? src[i] : ~0ull);
+    if (nruns == 1) {
+      if (i < n) dst[i] = k;
+    } else {
+      s_k[0][i] = k;
+    }
+  }
+  if (nruns == 1) return;
+  __syncthreads();
+  int buf = 0;
+  for (int w = 32; w < N; w <<= 1) {
+    const bool last_pass = (w << 1) >= N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const int r = i / w;
+      const int own = i - r * w;
+      const int pbeg = (r ^ 1) * w;
+      const int base = (r & ~1) * w;
+      const unsigned long long k = s_k[buf][i];
+      int pos = i;
+      if (pbeg < N) pos = base + own + run_rank(&s_k[buf][pbeg], min(w, N - pbeg), k, (r & 1) != 0);
+      if (last_pass) {
+        if (pos < n) dst[pos] = k;
+      } else {
+        s_k[buf ^ 1][pos] = k;
+      }
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+}
+
+// One merge pass over a segment of n keys: runs of width w in a -> runs of 2w in b.
+__device__ void merge_pass(const unsigned long long* a, unsigned long long* b, int n, int w) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  int o = threadIdx.x * per;
+  const int o1 = min(n, o + per);
+  while (o < o1) {
+    const int plo = (o / (2 * w)) * (2 * w);
+    const int mid = min(plo + w, n), phi = min(plo + 2 * w, n);
+    const int la = mid - plo, lb = phi - mid;
+    const unsigned long long* A = a + plo;
+    const unsigned long long* B = a + mid;
+    const int d = o - plo;
+    int lo = max(0, d - lb), hi = min(d, la);
+    while (lo < hi) {   // merge path: number of A keys among the first d outputs
+      const int m = (lo + hi) >> 1;
+      if (B[d - 1 - m] < A[m])
+        hi = m;
+      else
+        lo = m + 1;
+    }
+    int ia = lo, ib = d - lo;
+    const int pend = min(o1, phi);
+    for (; o < pend; ++o) b[o] = (ia < la && (ib >= lb || A[ia] < B[ib])) ? A[ia++] : B[ib++];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ start,
+                                                   uint32_t pair_cap, unsigned long long* ukey, unsigned long long* skey,
+                                                   uint32_t* __restrict__ sid, const double* __restrict__ depth_id,
+                                                   int2* __restrict__ ranges) {
+  __shared__ unsigned long long s_k[2][kSortChunk];
+  const int t = blockIdx.x;
+  const uint32_t s0 = min(start[t], pair_cap);
+  const int n = static_cast<int>(min(cnt[static_cast<int64_t>(t) * kBinStride], pair_cap - s0));
+  if (threadIdx.x == 0) ranges[t] = n ? make_int2(static_cast<int>(s0), static_cast<int>(s0) + n) : make_int2(0, 0);
+  if (n == 0) return;
+  unsigned long long* uk = ukey + s0;
+  unsigned long long* sk = skey + s0;
+  if (n <= kSortChunk) {
+    sort_chunk(uk, sk, n, s_k);
+  } else {
+    // long list: sorted chunks, then merge passes ping-ponging between the two buffers
+    for (int c = 0; c < n; c += kSortChunk) {
+      sort_chunk(uk + c, sk + c, min(kSortChunk, n - c), s_k);
+      __syncthreads();
+    }
+    bool in_s = true;
+    for (int w = kSortChunk; w < n; w *= 2) {
+      merge_pass(in_s ? sk : uk, in_s ? uk : sk, n, w);
+      in_s = !in_s;
+    }
+    if (!in_s)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = uk[i];
+  }
+  __syncthreads();
+  // fix-up: runs of equal fp32 depth in (fp64 depth, id) order (rasterizer.cpp:74-77); the
+  // first thread of each run insertion-sorts it (runs are a handful of keys)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t hi = static_cast<uint32_t>(sk[i] >> 32);
+    const bool starts = (i == 0 || static_cast<uint32_t>(sk[i - 1] >> 32) != hi) && i + 1 < n &&
+                        static_cast<uint32_t>(sk[i + 1] >> 32) == hi;
+    if (!starts) continue;
+    int e = i + 2;
+    while (e < n && static_cast<uint32_t>(sk[e] >> 32) == hi) ++e;
+    for (int a = i + 1; a < e; ++a) {
+      const unsigned long long ka = sk[a];
+      const uint32_t ida = static_cast<uint32_t>(ka);
+      const double da = depth_id[ida];
+      int b = a - 1;
+      while (b >= i) {
+        const uint32_t idb = static_cast<uint32_t>(sk[b]);
+        const double db = depth_id[idb];
+        if (db < da || (db == da && idb < ida)) break;
+        sk[b + 1] = sk[b];
+        --b;
+      }
+      sk[b + 1] = ka;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sid[s0 + i] = static_cast<uint32_t>(sk[i]);
+}
+
+}  // namespace
+
+void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles, cudaStream_t st, int64_t* L) {
+  const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
+  k_tile_scan<<<1, 1024, 0, st>>>(ws.tile_cnt, ntiles, ws.tile_start, ws.bin_counters, pair_cap, ds);
+  ++*L;
+  if (P > 0) {
+    k_scatter<<<div_up(P, 256), 256, 0, st>>>(ws.visible, ws.rect_id, ws.depth_id, P, tiles_x, ws.tile_start, ws.tile_fill,
+                                              pair_cap, ws.ukey);
+    ++*L;
+    k_scatter_big<<<128, 1024, 0, st>>>(ws.big_ids, ws.bin_counters, ws.rect_id, ws.depth_id, tiles_x, ws.tile_start,
+                                        ws.tile_fill, pair_cap, ws.ukey);
+    ++*L;
+  }
+  k_tile_sort<<<ntiles, 256, 0, st>>>(ws.tile_cnt, ws.tile_start, pair_cap, ws.ukey, ws.skey, ws.sid, ws.depth_id, ws.ranges);
+  ++*L;
+}
+
+}  // namespace gsfk

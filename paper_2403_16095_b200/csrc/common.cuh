@@ -8,7 +8,12 @@
 
 namespace gsfk {
 
-constexpr int kTile = 16;             // tile edge (RasterConfig::tile_size, config.hpp:10)
+constexpr int kTile = 16;
+// Binning: per-tile counters (stride kBinStride u32), primitives with more than kBigPairs tiles
+// go to the one-CTA-per-primitive scatter, and the slots of Workspace::bin_counters.
+constexpr int kBinStride = 1;
+constexpr int kBigPairs = 128;
+enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
 constexpr int kTilePixels = kTile * kTile;
 constexpr int kFieldsBase = 11;       // mean 3, log_scale 3, quat 4, opacity 1; then 3*K SH
 
@@ -107,6 +112,29 @@ struct LossParams {       // what the fused epilogues need (constant per loop)
   double w_color, w_ssim, w_geo, w_align, w_iso, w_var, t_color, t_geo, iso_epsilon;
   int32_t uncertainty_full_gradient;
 };
+
+// Warp-wide exclusive prefix sum of one int per lane.
+__device__ __forceinline__ int warp_excl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x - v;
+}
+
+// Largest lane j with excl_j <= k (excl non-decreasing over the lanes, excl_0 == 0).
+__device__ __forceinline__ int warp_owner(int excl, int k) {
+  int lo = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int e = __shfl_sync(0xffffffffu, excl, lo + step);
+    if (e <= k) lo += step;
+  }
+  return lo;
+}
 
 #define GSF_CUDA_CHECK(expr)                                                        \
   do {                                                                              \

@@ -53,39 +53,30 @@ struct Profiler {
 enum ProfName { PROF_PREPROCESS = 0, PROF_SORT = 1, PROF_BLEND = 2, PROF_BACKWARD = 3, PROF_CHAIN = 4, PROF_SSIM = 5,
                 PROF_ADAM = 6, PROF_BINNING = 7, PROF_NUM = 8 };
 
-struct ScanTemp {
-  unsigned long long* state = nullptr;
-};
-
 // Device workspace of one context.  Capacities grow on demand (never shrink).
 struct Workspace {
   int64_t P_cap = 0, pair_cap = 0, npix_cap = 0, tiles_cap = 0;
-  // per primitive, id-indexed
-  uint32_t* flag = nullptr;
-  uint32_t* vis_off = nullptr;
-  uint32_t* key_id = nullptr;
+  // per primitive, id-indexed (written by k_preprocess for the visible ones)
   BlendG* bg_id = nullptr;
   GuardG* gg_id = nullptr;
   double* depth_id = nullptr;
   int4* rect_id = nullptr;
   uint8_t* visible = nullptr;
-  // per visible primitive, depth-rank-indexed
-  uint32_t* skeys[2] = {nullptr, nullptr};
-  uint32_t* svals[2] = {nullptr, nullptr};
-  int32_t* rank_to_id = nullptr;
-  BlendG* bg = nullptr;
-  GuardG* gg = nullptr;
-  int4* rect = nullptr;
+  float* pj_id = nullptr;       // P * 36: pose Jacobians of the visible primitives (tracking)
+  // per tile: bins[t * kBinStride + {0, 1}] = (count, fill cursor), then the counters; one memset
+  uint32_t* bins = nullptr;
   uint32_t* tile_cnt = nullptr;
-  uint32_t* pair_off = nullptr;
-  // per (tile, primitive) pair
-  uint32_t* pkeys[2] = {nullptr, nullptr};
-  uint32_t* pvals[2] = {nullptr, nullptr};
-  uint32_t* pair_rank = nullptr;
-  float* partials = nullptr;   // pair_cap * 10
-  // per tile
+  uint32_t* tile_fill = nullptr;
+  uint32_t* bin_counters = nullptr;   // BinCounter slots
+  uint32_t* big_ids = nullptr;        // P: primitives with more than kBigPairs tiles
+  uint32_t* tile_start = nullptr;
   int2* ranges = nullptr;
   double* loss_part = nullptr;  // tiles * LS_NUM
+  // per (tile, primitive) pair: scattered keys/ids, then each tile's list sorted by (depth, id)
+  unsigned long long* ukey = nullptr;   // (fp32 depth bits << 32 | id), scatter order
+  unsigned long long* skey = nullptr;   // the same keys, each tile's list in (depth, id) order
+  uint32_t* sid = nullptr;
+  float* partials = nullptr;   // pair_cap * 10, at sorted list positions (generic backward)
   // per pixel (render outputs + backward inputs)
   float* color = nullptr;      // 3*npix, interleaved
   float* alpha_depth = nullptr;
@@ -104,31 +95,15 @@ struct Workspace {
   float* dssim = nullptr;       // 3*npix: d(w_ssim * ssim loss)/d colour (mapping)
   float* ssim_tmp = nullptr;    // SSIM scratch maps (see loss.cu)
   // temporaries
-  ScanTemp scan;
-  uint32_t* radix_temp = nullptr;
-  size_t radix_temp_bytes = 0;
   double* pose_part = nullptr;  // chain blocks * 6 (or tiles * 6 for the fused tracking backward)
-  float* pj_id = nullptr;       // P * 36: per-visible-primitive pose Jacobians, rank order (tracking)
   double* red_part = nullptr;   // generic per-block fp64 partials (ssim, then iso)
   int64_t red_iso_offset = 0;
   int ssim_blocks = 0, iso_blocks = 0;
-  // final buffers of the two sorts (set by the pipeline)
-  uint32_t* depth_sorted_vals = nullptr;
-  uint32_t* pair_sorted_keys = nullptr;
-  uint32_t* pair_sorted_vals = nullptr;
   Profiler* prof = nullptr;
 };
 
-// sort.cu
-void launch_scan_excl(const uint32_t* in, uint32_t* out, const uint32_t* n_dev, uint32_t n_max, uint32_t* total_out,
-                      ScanTemp& tmp, cudaStream_t st, int64_t* launches);
-size_t scan_temp_bytes(uint32_t n_max);
-size_t radix_temp_bytes(uint32_t n_max, int max_passes);
-int radix_sort_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
-                   uint32_t n_max, int begin_bit, int end_bit, bool vals_are_index, uint32_t* temp, cudaStream_t st,
-                   int64_t* launches);
-void launch_sort_fixup(const uint32_t* keys, uint32_t* vals, const double* depth_id, const uint32_t* n_dev,
-                       uint32_t n_max, cudaStream_t st, int64_t* launches);
+// binning.cu
+void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles, cudaStream_t st, int64_t* launches);
 
 // raster_fwd.cu
 struct FwdArgs {
@@ -145,6 +120,7 @@ struct FwdArgs {
   LossParams lp;
   int iteration;             // loop iteration (for device-side checks), -1 outside loops
   bool want_posejac = false; // tracking: emit the per-primitive pose Jacobians (ws.pj_id)
+  bool fuse_loss_final = false;  // tracking: the blend's last CTA runs the loss finalize
 };
 void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* launches);
 void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,

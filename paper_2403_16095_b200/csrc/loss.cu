@@ -9,6 +9,7 @@
 //                    per-pixel terms, and the adjoint blur for d(ssim)/dx.
 //   k_iso            iso term and its direct log-scale gradient (losses.cpp:195-216, 272-280).
 #include "kernels.h"
+#include "finalize.cuh"
 
 namespace gsfk {
 
@@ -37,88 +38,14 @@ __global__ void __launch_bounds__(256) k_loss_finalize(const double* __restrict_
                                                        LossParams lp, int iteration, const double* __restrict__ ssim_part,
                                                        int ssim_blocks, const double* __restrict__ iso_part,
                                                        int iso_blocks, DevState* ds) {
-  __shared__ double s_red[8];
-  double tot[LS_NUM];
-  for (int q = 0; q < LS_NUM; ++q) {
-    double a = 0.0;
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x) a += loss_part[static_cast<int64_t>(t) * LS_NUM + q];
-    tot[q] = block_sum_d(a, s_red);
-  }
-  double ssim_sum = 0.0, iso_sum = 0.0;
-  {
-    double a = 0.0;
-    for (int t = threadIdx.x; t < ssim_blocks; t += blockDim.x) a += ssim_part[t];
-    ssim_sum = block_sum_d(a, s_red);
-    a = 0.0;
-    for (int t = threadIdx.x; t < iso_blocks; t += blockDim.x) a += iso_part[t];
-    iso_sum = block_sum_d(a, s_red);
-  }
-  if (threadIdx.x != 0) return;
-  if (ds->halt) return;
-  for (int q = 0; q < LS_NUM; ++q) ds->loss[q] = tot[q];
-  const double hw = static_cast<double>(npix);
-  const bool nbv = lp.normalize_by_valid != 0;
-  const double cc = tot[LS_COLOR_CNT], cg = tot[LS_GEO_CNT], ca = tot[LS_ALIGN_CNT], cv = tot[LS_VAR_CNT];
-  if (lp.mode == 1) {
-    const double color = cc > 0.0 ? tot[LS_COLOR_SUM] / (3.0 * (nbv ? cc : hw)) : 0.0;
-    const double geo = cg > 0.0 ? tot[LS_GEO_SUM] / (nbv ? cg : hw) : 0.0;
-    const double total = lp.t_color * color + lp.t_geo * geo;
-    const double m_color = nbv ? cc : hw, m_geo = nbv ? cg : hw;
-    ds->term_color = color;
-    ds->term_geo = geo;
-    ds->term_align = ds->term_var = ds->term_ssim = ds->term_iso = 0.0;
-    ds->loss_total = total;
-    ds->seed_color = (lp.t_color > 0.0 && m_color > 0.0) ? lp.t_color / (3.0 * m_color) : 0.0;
-    ds->seed_geo = (lp.t_geo > 0.0 && m_geo > 0.0) ? lp.t_geo / m_geo : 0.0;
-    ds->any_empty = (cc == 0.0 || cg == 0.0) ? 1 : 0;
-    if (iteration == 0) {
-      ds->initial_loss = total;
-      if (cc == 0.0 && cg == 0.0) {   // tracker.cpp:46-53
-        ds->halt = 1;
-        ds->halt_iter = 0;
-        ds->final_loss = total;
-        ds->degraded = 1;
-        return;
-      }
-    }
-    if (iteration >= 0 && !isfinite(total)) {   // tracker.cpp:55-60
-      ds->halt = 2;
-      ds->halt_iter = iteration;
-    }
-  } else if (lp.mode == 2) {
-    bool warn = false;
-    const double color = hw > 0.0 ? tot[LS_COLOR_SUM] / (3.0 * hw) : 0.0;
-    auto masked = [&](double sum, double c) {
-      if (c == 0.0) { warn = true; return 0.0; }
-      return sum / (nbv ? c : hw);
-    };
-    const double geo = masked(tot[LS_GEO_SUM], cg);
-    const double align = masked(tot[LS_ALIGN_SUM], ca);
-    double var = 0.0;
-    if (ds->has_obs) var = masked(tot[LS_VAR_SUM], cv);
-    else warn = true;
-    const double ssim = lp.w_ssim > 0.0 ? 1.0 - ssim_sum / (3.0 * hw) : 0.0;
-    const double iso = ds->V > 0 ? iso_sum / static_cast<double>(ds->V) : 0.0;
-    const double total = lp.w_color * color + lp.w_ssim * ssim + lp.w_geo * geo + lp.w_align * align + lp.w_iso * iso +
-                         lp.w_var * var;
-    const double m_geo = nbv ? cg : hw, m_align = nbv ? ca : hw, m_var = nbv ? cv : hw;
-    ds->term_color = color;
-    ds->term_geo = geo;
-    ds->term_align = align;
-    ds->term_var = var;
-    ds->term_ssim = ssim;
-    ds->term_iso = iso;
-    ds->loss_total = total;
-    ds->any_empty = warn ? 1 : 0;
-    ds->seed_color = lp.w_color > 0.0 ? lp.w_color / (3.0 * hw) : 0.0;
-    ds->seed_geo = (lp.w_geo > 0.0 && m_geo > 0.0) ? lp.w_geo / m_geo : 0.0;
-    ds->seed_align = (lp.w_align > 0.0 && m_align > 0.0) ? lp.w_align / m_align : 0.0;
-    ds->seed_var = (lp.w_var > 0.0 && ds->has_obs && m_var > 0.0) ? lp.w_var / m_var : 0.0;
-    if (iteration >= 0 && !isfinite(total)) {
-      ds->halt = 2;
-      ds->halt_iter = iteration;
-    }
-  }
+  __shared__ double s_red[8][LS_NUM];
+  __shared__ double s_red1[8][1];
+  __shared__ double s_tot[LS_NUM];
+  __shared__ double s_ssim[1], s_iso[1];
+  block_reduce_rows<LS_NUM>(loss_part, tiles, s_tot, s_red);
+  block_reduce_rows<1>(ssim_part, ssim_blocks, s_ssim, s_red1);
+  block_reduce_rows<1>(iso_part, iso_blocks, s_iso, s_red1);
+  if (threadIdx.x == 0) loss_scalars(ds, lp, s_tot, s_ssim[0], s_iso[0], npix, iteration);
 }
 
 // ---- SSIM ------------------------------------------------------------------------------------

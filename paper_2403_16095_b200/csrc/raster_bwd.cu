@@ -15,6 +15,7 @@
 // k_pose_sum  fixed-order sum of the per-block pose partials (rasterizer.cpp:570).
 #include "kernels.h"
 #include "pixel_loss.cuh"
+#include "finalize.cuh"
 
 namespace gsfk {
 
@@ -69,11 +70,9 @@ __device__ __forceinline__ bool dvalid(float d, double near_plane, double far_pl
 
 struct BwdPtrs {
   const int2* ranges;
-  const uint32_t* sorted_orig;
-  const uint32_t* pair_rank;
-  const BlendG* bg;
+  const uint32_t* sid;      // tile lists (primitive ids) in (depth, id) order
+  const BlendG* bg;         // id-indexed
   const GuardG* gg;
-  const int32_t* rank_to_id;
   const float* color;
   const float* alpha_depth;
   const float* median_depth;
@@ -91,7 +90,7 @@ struct BwdPtrs {
   const float* up_uncert;
   const float* dssim;
   float* partials;
-  const float* pj;       // per-primitive pose Jacobians (fused tracking mode), rank-indexed, 36 floats
+  const float* pj;       // per-primitive pose Jacobians (fused tracking mode), id-indexed, 36 floats
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
 };
 
@@ -104,10 +103,8 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
   __shared__ double s_pred[8][6];
   double pacc[6] = {0, 0, 0, 0, 0, 0};
   __shared__ BlendG s_g[kBwdBatch];
-  __shared__ int32_t s_rank[kBwdBatch];
   __shared__ int32_t s_id[kBwdBatch];
   __shared__ uint8_t s_mask[kBwdBatch];
-  __shared__ uint32_t s_orig[kBwdBatch];
   __shared__ float s_part[8][kBwdBatch][NF];
   __shared__ int s_wmax[8];
   const int tile = blockIdx.x;
@@ -166,13 +163,10 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
     const int bstart = max(rg.x, bend - kBwdBatch);
     const int cnt = bend - bstart;
     if (tid < cnt) {
-      const uint32_t orig = bp.sorted_orig[bstart + tid];
-      const int r = static_cast<int>(bp.pair_rank[orig]);
-      const BlendG gj = bp.bg[r];
+      const int id = static_cast<int>(bp.sid[bstart + tid]);
+      const BlendG gj = bp.bg[id];
       s_g[tid] = gj;
-      s_rank[tid] = r;
-      s_id[tid] = bp.rank_to_id[r];
-      s_orig[tid] = orig;
+      s_id[tid] = id;
       s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, static_cast<float>(tx * kTile), static_cast<float>(ty * kTile), kc));
     }
     __syncthreads();
@@ -188,7 +182,7 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
       bool contrib = false;
       if (li < last) {
         const BlendG g = s_g[k];
-        const PairEval e = eval_pair(px, py, g, bp.gg + s_rank[k], kc);
+        const PairEval e = eval_pair(px, py, g, bp.gg + s_id[k], kc);
         if (e.code) {
           contrib = true;
           const float alpha = e.alpha;
@@ -233,12 +227,12 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
       if (POSEJ)
         s_sum[k][fi] = sum;
       else
-        bp.partials[static_cast<size_t>(s_orig[k]) * NF + fi] = sum;
+        bp.partials[static_cast<size_t>(bstart + k) * NF + fi] = sum;
     }
     __syncthreads();
     if (POSEJ && tid < cnt) {
       // pose contribution of this (tile, primitive) pair through its Jacobian (rasterizer.cpp:495-526)
-      const float4* q4 = reinterpret_cast<const float4*>(bp.pj + 36 * static_cast<size_t>(s_rank[tid]));
+      const float4* q4 = reinterpret_cast<const float4*>(bp.pj + 36 * static_cast<size_t>(s_id[tid]));
       float pjv[36];
 #pragma unroll
       for (int i = 0; i < 9; ++i) {
@@ -285,9 +279,8 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
     return;
   }
   for (int j = end + tid; j < rg.y; j += 256) {
-    const uint32_t orig = bp.sorted_orig[j];
 #pragma unroll
-    for (int fi = 0; fi < NF; ++fi) bp.partials[static_cast<size_t>(orig) * NF + fi] = 0.0f;
+    for (int fi = 0; fi < NF; ++fi) bp.partials[static_cast<size_t>(j) * NF + fi] = 0.0f;
   }
 }
 
@@ -345,18 +338,18 @@ constexpr int kPoseBatch = 128;
 template <int SEED, bool VIEWDEP>
 __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc,
                                                        double near_plane, double far_plane, LossParams lp,
-                                                       const DevState* ds) {
+                                                       DevState* ds, uint32_t* ticket) {
   __shared__ BlendG s_g[kPoseBatch];
   __shared__ float4 s_pj[kPoseBatch][9];
-  __shared__ int32_t s_rank[kPoseBatch];
   __shared__ int32_t s_id[kPoseBatch];
   __shared__ uint8_t s_mask[kPoseBatch];
   __shared__ int s_wmax[8];
   __shared__ double s_pred[8][6];
   const int tile = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (ds->halt) {
-    if (tid < 6) bp.tile_pose[static_cast<size_t>(tile) * 6 + tid] = 0.0;
+  if (ds->halt) {   // halted loop: zero gradient, no update (k_pose_sum semantics)
+    __shared__ int s_last0;
+    if (last_cta(ticket, &s_last0, false) && tid < 6) ds->d_pose[tid] = 0.0;
     return;
   }
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -380,17 +373,16 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
     const int bstart = max(rg.x, bend - kPoseBatch);
     const int cnt = bend - bstart;
     if (tid < cnt) {
-      const int r = static_cast<int>(bp.pair_rank[bp.sorted_orig[bstart + tid]]);
-      const BlendG gj = bp.bg[r];
+      const int id = static_cast<int>(bp.sid[bstart + tid]);
+      const BlendG gj = bp.bg[id];
       s_g[tid] = gj;
-      s_rank[tid] = r;
-      s_id[tid] = bp.rank_to_id[r];
+      s_id[tid] = id;
       s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, tile_x0, tile_y0, kc));
     }
     __syncthreads();
     for (int i = tid; i < cnt * 9; i += 256) {
       const int k = i / 9, j = i - 9 * k;
-      s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[9 * static_cast<size_t>(s_rank[k]) + j];
+      s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[9 * static_cast<size_t>(s_id[k]) + j];
     }
     __syncthreads();
     float pf0 = 0.f, pf1 = 0.f, pf2 = 0.f, pf3 = 0.f, pf4 = 0.f, pf5 = 0.f;
@@ -405,7 +397,7 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
       const int li = bstart + k - rg.x;
       if (li >= pb.last) continue;
       const BlendG g = s_g[k];
-      const PairEval e = eval_pair(px, py, g, bp.gg + s_rank[k], kc);
+      const PairEval e = eval_pair(px, py, g, bp.gg + s_id[k], kc);
       if (!e.code) continue;
       const float alpha = e.alpha;
       const float inv = __frcp_rn(1.0f - alpha);
@@ -470,6 +462,13 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
     for (int w = 0; w < 8; ++w) t += s_pred[w][tid];
     bp.tile_pose[static_cast<size_t>(tile) * 6 + tid] = t;
   }
+  // the last tile CTA sums the tile partials in a fixed order (k_pose_sum without a launch)
+  __shared__ int s_last;
+  __shared__ double s_pose[6];
+  if (last_cta(ticket, &s_last, tid < 6)) {
+    block_reduce_rows<6>(bp.tile_pose, gridDim.x, s_pose, s_pred);
+    if (tid < 6) ds->d_pose[tid] = s_pose[tid];
+  }
 }
 
 // SH basis gradients (sh.cpp:44-72), fp64.
@@ -507,33 +506,55 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// Position of primitive `id` in tile list [lo, hi) (keys (fp32 depth bits << 32 | id), runs of
+// equal fp32 depth in fp64 order): lower bound of its fp32 depth, then a walk along that run.
+// Returns -1 if absent (pair dropped by a pair-capacity overflow).
+__device__ __forceinline__ int find_in_list(const unsigned long long* __restrict__ skey, int lo, int hi, uint32_t dbits,
+                                            uint32_t id) {
+  const unsigned long long k0 = static_cast<unsigned long long>(dbits) << 32;
+  int a = lo, b = hi;
+  while (a < b) {
+    const int m = (a + b) >> 1;
+    if (skey[m] < k0)
+      a = m + 1;
+    else
+      b = m;
+  }
+  for (; a < hi && static_cast<uint32_t>(skey[a] >> 32) == dbits; ++a)
+    if (static_cast<uint32_t>(skey[a]) == id) return a;
+  return -1;
+}
+
 template <int NF, bool FULL>
-__global__ void __launch_bounds__(256) k_chain(const uint32_t* __restrict__ pair_off, const float* __restrict__ partials,
-                                               const int32_t* __restrict__ rank_to_id, const DevState* ds, uint32_t Pcap,
-                                               uint32_t pair_cap, const float* __restrict__ params, int64_t P, int K,
+__global__ void __launch_bounds__(256) k_chain(const uint8_t* __restrict__ visible, const int4* __restrict__ rect_id,
+                                               const double* __restrict__ depth_id, const int2* __restrict__ ranges,
+                                               const unsigned long long* __restrict__ skey, int tiles_x, const float* __restrict__ partials, const DevState* ds,
+                                               const float* __restrict__ params, int64_t P, int K,
                                                float* __restrict__ grads, float* __restrict__ d_mean2d,
                                                double* __restrict__ pose_part) {
   __shared__ double s_red[8][6];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t r = blockIdx.x * blockDim.x + tid;
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
   double pose[6] = {0, 0, 0, 0, 0, 0};
-  const uint32_t V = min(ds->V, Pcap);
-  if (r < V && !ds->halt) {
-    const uint32_t Mtot = min(ds->M, pair_cap);
-    const uint32_t beg = min(pair_off[r], Mtot);
-    const uint32_t end = r + 1 < V ? min(pair_off[r + 1], Mtot) : Mtot;
+  if (id < P && visible[id] && !ds->halt) {
+    // fixed-order gather of the primitive's pair partials, tiles in row-major rectangle order
+    const int4 q = rect_id[id];
+    const uint32_t dbits = static_cast<uint32_t>(__float_as_int(static_cast<float>(depth_id[id])));
     double sg[NF];
 #pragma unroll
-    for (int q = 0; q < NF; ++q) sg[q] = 0.0;
-    for (uint32_t p = beg; p < end; ++p) {
+    for (int f = 0; f < NF; ++f) sg[f] = 0.0;
+    for (int ty = q.z; ty <= q.w; ++ty)
+      for (int tx = q.x; tx <= q.y; ++tx) {
+        const int2 rg = ranges[ty * tiles_x + tx];
+        const int pos = find_in_list(skey, rg.x, rg.y, dbits, static_cast<uint32_t>(id));
+        if (pos < 0) continue;
 #pragma unroll
-      for (int q = 0; q < NF; ++q) sg[q] += static_cast<double>(partials[static_cast<size_t>(p) * NF + q]);
-    }
+        for (int f = 0; f < NF; ++f) sg[f] += static_cast<double>(partials[static_cast<size_t>(pos) * NF + f]);
+      }
     bool zero = true;
 #pragma unroll
-    for (int q = 0; q < NF; ++q) zero = zero && sg[q] == 0.0;
+    for (int f = 0; f < NF; ++f) zero = zero && sg[f] == 0.0;
     if (!zero) {
-      const int64_t id = rank_to_id[r];
       const Cam& cam = ds->cam;
       const double* Wr = cam.W;
       const double m0 = params[0 * P + id], m1 = params[1 * P + id], m2 = params[2 * P + id];
@@ -753,11 +774,9 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   const int ntiles = a.rp.tiles_x * a.rp.tiles_y;
   BwdPtrs bp;
   bp.ranges = ws.ranges;
-  bp.sorted_orig = ws.pair_sorted_vals;
-  bp.pair_rank = ws.pair_rank;
-  bp.bg = ws.bg;
-  bp.gg = ws.gg;
-  bp.rank_to_id = ws.rank_to_id;
+  bp.sid = ws.sid;
+  bp.bg = ws.bg_id;
+  bp.gg = ws.gg_id;
   bp.color = ws.color;
   bp.alpha_depth = ws.alpha_depth;
   bp.median_depth = ws.median_depth;
@@ -780,21 +799,20 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   const bool view_dep = a.K > 1;
   const int nf = a.pose_only ? (view_dep ? 9 : 6) : 10;
   if (a.pose_only && a.fused_pose) {
-    // tracking: per-tile pose partials through the per-primitive Jacobians, no chain kernel
+    // tracking: per-tile pose partials through the per-primitive Jacobians; the last CTA reduces
+    // them, so neither a chain nor a pose-sum launch follows
     bp.pj = ws.pj_id;
     bp.tile_pose = ws.pose_part;
+    uint32_t* ticket = ws.bin_counters + kCntBwdTicket;
     if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
+#define GSF_BWDP(SM, VD) \
+  k_backward_pose<SM, VD><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ticket)
     if (a.seed_mode == SEED_TRACK) {
-      if (nf == 6) k_backward_pose<SEED_TRACK, false><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
-      else k_backward_pose<SEED_TRACK, true><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
+      if (nf == 6) GSF_BWDP(SEED_TRACK, false); else GSF_BWDP(SEED_TRACK, true);
     } else {
-      if (nf == 6) k_backward_pose<SEED_EXPLICIT, false><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
-      else k_backward_pose<SEED_EXPLICIT, true><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds);
+      if (nf == 6) GSF_BWDP(SEED_EXPLICIT, false); else GSF_BWDP(SEED_EXPLICIT, true);
     }
-    ++*L;
-    if (ws.prof) ws.prof->end(st);
-    if (ws.prof) ws.prof->begin(PROF_CHAIN, st);
-    k_pose_sum<<<1, 256, 0, st>>>(ws.pose_part, ntiles, ds);
+#undef GSF_BWDP
     ++*L;
     if (ws.prof) ws.prof->end(st);
     return;
@@ -812,18 +830,17 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   ++*L;
   if (ws.prof) ws.prof->end(st);
   if (ws.prof) ws.prof->begin(PROF_CHAIN, st);
-  const uint32_t Pcap = static_cast<uint32_t>(a.P);
   const int blocks = std::max(1, div_up(a.P, 256));
-  const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
+#define GSF_CHAIN(NFV, FULLV)                                                                                            \
+  k_chain<NFV, FULLV><<<blocks, 256, 0, st>>>(ws.visible, ws.rect_id, ws.depth_id, ws.ranges, ws.skey, a.rp.tiles_x, \
+                                              ws.partials, ds, a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part)
   if (nf == 6)
-    k_chain<6, false><<<blocks, 256, 0, st>>>(ws.pair_off, ws.partials, ws.rank_to_id, ds, Pcap, pair_cap, a.params, a.P, a.K,
-                                             a.grads, a.d_mean2d, ws.pose_part);
+    GSF_CHAIN(6, false);
   else if (nf == 9)
-    k_chain<9, false><<<blocks, 256, 0, st>>>(ws.pair_off, ws.partials, ws.rank_to_id, ds, Pcap, pair_cap, a.params, a.P, a.K,
-                                             a.grads, a.d_mean2d, ws.pose_part);
+    GSF_CHAIN(9, false);
   else
-    k_chain<10, true><<<blocks, 256, 0, st>>>(ws.pair_off, ws.partials, ws.rank_to_id, ds, Pcap, pair_cap, a.params, a.P, a.K,
-                                             a.grads, a.d_mean2d, ws.pose_part);
+    GSF_CHAIN(10, true);
+#undef GSF_CHAIN
   ++*L;
   k_pose_sum<<<1, 256, 0, st>>>(ws.pose_part, blocks, ds);
   ++*L;

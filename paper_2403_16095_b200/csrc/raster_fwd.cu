@@ -1,18 +1,16 @@
 // raster_fwd.cu — forward pass of the tile rasterizer on sm_100a.
 //
 //   k_preprocess   project_all (rasterizer.cpp:46-67) + validate_primitives (:34-44), fp64,
-//                  one thread per primitive, SoA fp32 parameter reads (coalesced per field)
-//   scan/compact   visible ids in id order (input of the stable depth sort)
-//   sort + fixup   sorted_visible (:69-79)
-//   k_gather       rank-ordered blend records (3 x float4 per primitive) + tile counts
-//   scan           pair offsets; k_duplicate writes (tile id, rank) pairs in rank order
-//   sort           stable by tile id -> every tile list in global depth order (:193-212)
-//   k_ranges       [start, end) per tile
+//                  one thread per primitive, SoA fp32 parameter reads (coalesced per field);
+//                  also counts the visible primitives, histograms their tile rectangles
+//                  (warp-cooperative atomics) and, for tracking, emits the pose Jacobians
+//   binning        (binning.cu) per-tile lists in exact (depth, id) order (:69-79, :193-212)
 //   k_blend        blend_pixel (:96-140) for a 16x16 tile per 256-thread CTA with the tile
 //                  list staged through shared memory, plus the fused loss epilogue
 //                  (losses.cpp:156-339: masks, residual sums and counts per tile)
 #include "kernels.h"
 #include "pixel_loss.cuh"
+#include "finalize.cuh"
 
 namespace gsfk {
 
@@ -125,128 +123,79 @@ __device__ void compute_posejac(const float* __restrict__ p, int64_t stride, con
   out[34] = out[35] = 0.0f;
 }
 
+template <bool PJ>
 __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ params, int64_t P, const DevState* ds,
-                                                    RasterParams rp, uint32_t near_bits, uint32_t* __restrict__ flag,
-                                                    uint32_t* __restrict__ key_id, BlendG* __restrict__ bg_id,
-                                                    GuardG* __restrict__ gg_id, double* __restrict__ depth_id,
-                                                    int4* __restrict__ rect_id, uint8_t* __restrict__ visible,
-                                                    int32_t* bad_index, BlendConsts kc) {
+                                                    RasterParams rp, BlendG* __restrict__ bg_id, GuardG* __restrict__ gg_id,
+                                                    double* __restrict__ depth_id, int4* __restrict__ rect_id,
+                                                    uint8_t* __restrict__ visible, int32_t* bad_index, BlendConsts kc,
+                                                    uint32_t* __restrict__ tile_cnt, uint32_t* counters,
+                                                    uint32_t* __restrict__ big_ids, float* __restrict__ pj) {
+  __shared__ uint32_t s_vis[8];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= P) return;
-  // validate_primitives (rasterizer.cpp:34-44): every field finite and |q| > 1e-12
-  // (all loads issued before any test: no short-circuit chain of dependent memory latencies)
-  const int D = kFieldsBase + 3 * rp.sh_coeffs;
-  float v[kFieldsBase];
-#pragma unroll
-  for (int f = 0; f < kFieldsBase; ++f) v[f] = params[f * P + i];
-  bool ok = true;
-#pragma unroll
-  for (int f = 0; f < kFieldsBase; ++f) ok &= isfinite(v[f]);
-  for (int f = kFieldsBase; f < D; ++f) ok &= isfinite(params[f * P + i]);
-  {
-    const double qw = v[6], qx = v[7], qy = v[8], qz = v[9];
-    ok &= dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz))) > 1e-12;
-  }
-  if (!ok) {
-    atomicMin(bad_index, static_cast<int32_t>(i));
-    flag[i] = 0u;
-    visible[i] = 0;
-    return;
-  }
-  const PreOut o = preprocess_one(params + i, P, ds->cam, rp);
-  visible[i] = static_cast<uint8_t>(o.visible);
-  flag[i] = static_cast<uint32_t>(o.visible);
-  if (!o.visible) return;
-  key_id[i] = depth_key(o.depth, near_bits);
-  BlendG g = make_blend_g(o);
-  g.pad0 = blend_rho_fast(g.sigma, kc);
-  bg_id[i] = g;
-  gg_id[i] = make_guard_g(o);
-  depth_id[i] = o.depth;
-  rect_id[i] = make_int4(o.tx0, o.tx1, o.ty0, o.ty1);
-}
-
-// Pose Jacobians of the visible primitives in depth-rank order (tracking only).
-__global__ void __launch_bounds__(256) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
-                                                 const int32_t* __restrict__ rank_to_id, const uint32_t* n_dev,
-                                                 uint32_t n_cap, float* __restrict__ pj) {
-  const uint32_t n = min(*n_dev, n_cap);
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n || ds->halt) return;
-  const int64_t id = rank_to_id[r];
-  compute_posejac(params + id, P, ds->cam, K, pj + 36 * static_cast<size_t>(r));
-}
-
-__global__ void k_compact(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ off,
-                          const uint32_t* __restrict__ key_id, int64_t P, uint32_t* __restrict__ keys,
-                          uint32_t* __restrict__ vals) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= P || !flag[i]) return;
-  const uint32_t pos = off[i];
-  keys[pos] = key_id[i];
-  vals[pos] = static_cast<uint32_t>(i);
-}
-
-__global__ void k_gather(const uint32_t* __restrict__ sorted_ids, const uint32_t* n_dev, uint32_t n_cap,
-                         const BlendG* __restrict__ bg_id, const GuardG* __restrict__ gg_id,
-                         const int4* __restrict__ rect_id, int32_t* __restrict__ rank_to_id, BlendG* __restrict__ bg,
-                         GuardG* __restrict__ gg, int4* __restrict__ rect, uint32_t* __restrict__ tile_cnt) {
-  const uint32_t n = min(*n_dev, n_cap);
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const uint32_t id = sorted_ids[r];
-  rank_to_id[r] = static_cast<int32_t>(id);
-  bg[r] = bg_id[id];
-  gg[r] = gg_id[id];
-  const int4 q = rect_id[id];
-  rect[r] = q;
-  tile_cnt[r] = static_cast<uint32_t>((q.y - q.x + 1) * (q.w - q.z + 1));
-}
-
-// One warp expands 32 consecutive ranks cooperatively (lanes stride over each rank's tile
-// rectangle), so a few very large footprints cannot serialise a thread; writes are coalesced.
-__global__ void k_duplicate(const int4* __restrict__ rect, const uint32_t* __restrict__ pair_off, const uint32_t* n_dev,
-                            uint32_t n_cap, const uint32_t* m_dev, uint32_t pair_cap, int tiles_x,
-                            uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pair_rank, uint32_t* overflow) {
-  const uint32_t n = min(*n_dev, n_cap);
-  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  if (gtid == 0 && *m_dev > pair_cap) *overflow = 1u;
-  const uint32_t r0 = gtid & ~31u;
-  if (r0 >= n) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  bool vis = false;
   int4 q = make_int4(0, -1, 0, -1);
-  uint32_t off = 0;
-  if (r0 + lane < n) {
-    q = rect[r0 + lane];
-    off = pair_off[r0 + lane];
-  }
-  const int nj = static_cast<int>(min(32u, n - r0));
-  for (int j = 0; j < nj; ++j) {
-    const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qx1 = __shfl_sync(0xffffffffu, q.y, j);
-    const int qy0 = __shfl_sync(0xffffffffu, q.z, j), qy1 = __shfl_sync(0xffffffffu, q.w, j);
-    const uint32_t base = __shfl_sync(0xffffffffu, off, j);
-    const int w = qx1 - qx0 + 1;
-    const int c = w * (qy1 - qy0 + 1);
-    const float inv_w = 1.0f / static_cast<float>(w);
-    for (int k = lane; k < c; k += 32) {
-      const int row = __float2int_rz((static_cast<float>(k) + 0.5f) * inv_w);   // exact for c < 4M
-      const int col = k - row * w;
-      const uint32_t pos = base + static_cast<uint32_t>(k);
-      if (pos < pair_cap) {
-        pkeys[pos] = static_cast<uint32_t>((qy0 + row) * tiles_x + qx0 + col);
-        pair_rank[pos] = r0 + static_cast<uint32_t>(j);
+  if (i < P) {
+    // validate_primitives (rasterizer.cpp:34-44): every field finite and |q| > 1e-12
+    // (all loads issued before any test: no short-circuit chain of dependent memory latencies)
+    const int D = kFieldsBase + 3 * rp.sh_coeffs;
+    float v[kFieldsBase];
+#pragma unroll
+    for (int f = 0; f < kFieldsBase; ++f) v[f] = params[f * P + i];
+    bool ok = true;
+#pragma unroll
+    for (int f = 0; f < kFieldsBase; ++f) ok &= isfinite(v[f]);
+    for (int f = kFieldsBase; f < D; ++f) ok &= isfinite(params[f * P + i]);
+    {
+      const double qw = v[6], qx = v[7], qy = v[8], qz = v[9];
+      ok &= dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz))) > 1e-12;
+    }
+    if (!ok) {
+      atomicMin(bad_index, static_cast<int32_t>(i));
+      visible[i] = 0;
+    } else {
+      const PreOut o = preprocess_one(params + i, P, ds->cam, rp);
+      visible[i] = static_cast<uint8_t>(o.visible);
+      if (o.visible) {
+        vis = true;
+        BlendG g = make_blend_g(o);
+        g.pad0 = blend_rho_fast(g.sigma, kc);
+        bg_id[i] = g;
+        gg_id[i] = make_guard_g(o);
+        depth_id[i] = o.depth;
+        q = make_int4(o.tx0, o.tx1, o.ty0, o.ty1);
+        rect_id[i] = q;
+        if (PJ) compute_posejac(params + i, P, ds->cam, rp.sh_coeffs, pj + 36 * static_cast<size_t>(i));
       }
     }
   }
-}
-
-__global__ void k_ranges(const uint32_t* __restrict__ keys, const uint32_t* m_dev, uint32_t cap, int2* ranges) {
-  const uint32_t n = min(*m_dev, cap);
-  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const uint32_t t = keys[s];
-  if (s == 0 || keys[s - 1] != t) ranges[t].x = static_cast<int>(s);
-  if (s + 1 == n || keys[s + 1] != t) ranges[t].y = static_cast<int>(s + 1);
+  // tile histogram: the warp's (tile, primitive) pairs are flattened over its lanes
+  const uint32_t bits = __ballot_sync(0xffffffffu, vis);
+  if (lane == 0) s_vis[warp] = static_cast<uint32_t>(__popc(bits));
+  const int tiles_x = rp.tiles_x;
+  const int w = q.y - q.x + 1;
+  const int c = vis ? w * (q.w - q.z + 1) : 0;
+  if (c > kBigPairs) big_ids[atomicAdd(&counters[kCntBig], 1u)] = static_cast<uint32_t>(i);
+  const int excl = warp_excl_scan(c);
+  const int total = __shfl_sync(0xffffffffu, excl + c, 31);
+  for (int base = 0; base < total; base += 32) {
+    const int k = base + lane;
+    const int j = warp_owner(excl, k);
+    const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qy0 = __shfl_sync(0xffffffffu, q.z, j);
+    const int wj = __shfl_sync(0xffffffffu, w, j), ej = __shfl_sync(0xffffffffu, excl, j);
+    if (k < total) {
+      const int r = k - ej;
+      const int row = r / wj;
+      atomicAdd(&tile_cnt[static_cast<int64_t>((qy0 + row) * tiles_x + qx0 + (r - row * wj)) * kBinStride], 1u);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t n = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) n += s_vis[w];
+    if (n) atomicAdd(&counters[kCntVisible], n);
+  }
 }
 
 __device__ __forceinline__ bool depth_valid(float d, double near_plane, double far_plane) {
@@ -261,21 +210,20 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 template <int LMODE>
-__global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sorted_orig,
-                                               const uint32_t* __restrict__ pair_rank, const BlendG* __restrict__ bg,
-                                               const GuardG* __restrict__ gg, const int32_t* __restrict__ rank_to_id,
+__global__ void __launch_bounds__(256, LMODE == 1 ? 5 : 4) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sid,
+                                               const BlendG* __restrict__ bg, const GuardG* __restrict__ gg,
                                                const float* __restrict__ obs, const float* __restrict__ loss_rgb,
                                                const float* __restrict__ loss_depth, int W, int H, int tiles_x,
                                                BlendConsts kc, double near_plane, double far_plane, LossParams lp,
-                                               const DevState* ds, float* __restrict__ o_color, float* __restrict__ o_ad,
+                                               DevState* ds, float* __restrict__ o_color, float* __restrict__ o_ad,
                                                float* __restrict__ o_md, uint8_t* __restrict__ o_mv,
                                                float* __restrict__ o_op, float* __restrict__ o_unc,
                                                float* __restrict__ o_T, int32_t* __restrict__ o_count,
                                                int32_t* __restrict__ o_dom, int32_t* __restrict__ o_med,
                                                float* __restrict__ o_domw, int32_t* __restrict__ o_last,
-                                               double* __restrict__ loss_part) {
+                                               double* __restrict__ loss_part, int fuse_final, int iteration,
+                                               uint32_t* ticket) {
   __shared__ BlendG s_g[256];
-  __shared__ int32_t s_rank[256];
   __shared__ int32_t s_id[256];
   __shared__ uint8_t s_mask[256];
   __shared__ double s_red[8][LS_NUM];
@@ -303,11 +251,10 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
     if (__syncthreads_and(s.done)) break;
     const int j = start + tid;
     if (j < rg.y) {
-      const int r = static_cast<int>(pair_rank[sorted_orig[j]]);
-      const BlendG gj = bg[r];
+      const int id = static_cast<int>(sid[j]);
+      const BlendG gj = bg[id];
       s_g[tid] = gj;
-      s_rank[tid] = r;
-      s_id[tid] = rank_to_id[r];
+      s_id[tid] = id;
       s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, tile_x0, tile_y0, kc));
     }
     __syncthreads();
@@ -321,7 +268,7 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
         bits &= bits - 1u;
         if (s.done) continue;
         const BlendG g = s_g[k];
-        const PairEval e = eval_pair(px, py, g, gg + s_rank[k], kc);
+        const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
         if (e.code) {
           if (LMODE == 1)
             pixel_accumulate_min(s, g, e, start + k - rg.x, kc);
@@ -369,6 +316,15 @@ __global__ void __launch_bounds__(256) k_blend(const int2* __restrict__ ranges, 
     for (int w = 0; w < 8; ++w) t += s_red[w][tid];
     loss_part[static_cast<int64_t>(tile) * LS_NUM + tid] = t;
   }
+  if (LMODE == 1 && fuse_final) {
+    // the last tile CTA finalises the loss (k_loss_finalize without its own launch)
+    __shared__ int s_last;
+    __shared__ double s_tot[LS_NUM];
+    if (last_cta(ticket, &s_last, tid < LS_NUM)) {
+      block_reduce_rows<LS_NUM>(loss_part, gridDim.x, s_tot, s_red);
+      if (tid == 0) loss_scalars(ds, lp, s_tot, 0.0, 0.0, static_cast<int64_t>(W) * H, iteration);
+    }
+  }
 }
 
 // Stand-alone loss partials over stored maps (evaluate_*_loss called on a RenderResult).
@@ -405,73 +361,36 @@ __global__ void __launch_bounds__(256) k_loss_tiles(const float* __restrict__ co
   }
 }
 
-int bits_for(uint32_t max_value) {
-  int b = 0;
-  while (b < 32 && (max_value >> b) != 0) ++b;
-  return b;
-}
-
 }  // namespace
 
 void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* L) {
   const int64_t P = a.P;
-  const uint32_t Pn = static_cast<uint32_t>(P);
   const int tiles_x = a.rp.tiles_x, tiles_y = a.rp.tiles_y;
   const int ntiles = tiles_x * tiles_y;
-  const uint32_t near_bits = static_cast<uint32_t>(fbits(static_cast<float>(a.near_plane)));
-  const uint32_t far_key = static_cast<uint32_t>(fbits(static_cast<float>(a.far_plane))) - near_bits;
-  const int depth_bits = std::max(1, bits_for(far_key));
-  const int tile_bits = std::max(1, bits_for(static_cast<uint32_t>(ntiles - 1)));
-  const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
-
   Profiler* pf = ws.prof;
+  GSF_CUDA_CHECK(cudaMemsetAsync(ws.bins, 0, sizeof(uint32_t) * (ws.tiles_cap * std::max(kBinStride, 2) + kCntNum), st));
   if (pf) pf->begin(PROF_PREPROCESS, st);
   if (P > 0) {
-    k_preprocess<<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, near_bits, ws.flag, ws.key_id, ws.bg_id, ws.gg_id,
-                                                 ws.depth_id, ws.rect_id, ws.visible, &ds->bad_index, a.kc);
+    if (a.want_posejac)
+      k_preprocess<true><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,
+                                                         ws.visible, &ds->bad_index, a.kc, ws.tile_cnt, ws.bin_counters,
+                                                         ws.big_ids, ws.pj_id);
+    else
+      k_preprocess<false><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,
+                                                          ws.visible, &ds->bad_index, a.kc, ws.tile_cnt, ws.bin_counters,
+                                                          ws.big_ids, ws.pj_id);
     ++*L;
   }
   if (pf) pf->end(st);
   if (pf) pf->begin(PROF_SORT, st);
-  launch_scan_excl(ws.flag, ws.vis_off, nullptr, Pn, &ds->V, ws.scan, st, L);
-  if (P > 0) {
-    k_compact<<<div_up(P, 256), 256, 0, st>>>(ws.flag, ws.vis_off, ws.key_id, P, ws.skeys[0], ws.svals[0]);
-    ++*L;
-  }
-  const int dpass = radix_sort_u32(ws.skeys[0], ws.svals[0], ws.skeys[1], ws.svals[1], &ds->V, Pn, 0, depth_bits, false,
-                                   ws.radix_temp, st, L);
-  uint32_t* dkeys = (dpass & 1) ? ws.skeys[1] : ws.skeys[0];
-  uint32_t* dvals = (dpass & 1) ? ws.svals[1] : ws.svals[0];
-  ws.depth_sorted_vals = dvals;
-  launch_sort_fixup(dkeys, dvals, ws.depth_id, &ds->V, Pn, st, L);
-  if (P > 0) {
-    k_gather<<<div_up(P, 256), 256, 0, st>>>(dvals, &ds->V, Pn, ws.bg_id, ws.gg_id, ws.rect_id, ws.rank_to_id, ws.bg, ws.gg,
-                                             ws.rect, ws.tile_cnt);
-    ++*L;
-  }
-  if (a.want_posejac && P > 0) {
-    k_posejac<<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.K, ws.rank_to_id, &ds->V, Pn, ws.pj_id);
-    ++*L;
-  }
-  launch_scan_excl(ws.tile_cnt, ws.pair_off, &ds->V, Pn, &ds->M, ws.scan, st, L);
-  if (P > 0) {
-    k_duplicate<<<div_up(P, 256), 256, 0, st>>>(ws.rect, ws.pair_off, &ds->V, Pn, &ds->M, pair_cap, tiles_x, ws.pkeys[0],
-                                                ws.pair_rank, &ds->overflow);
-    ++*L;
-  }
-  const int ppass = radix_sort_u32(ws.pkeys[0], ws.pvals[0], ws.pkeys[1], ws.pvals[1], &ds->M, pair_cap, 0, tile_bits, true,
-                                   ws.radix_temp, st, L);
-  ws.pair_sorted_keys = (ppass & 1) ? ws.pkeys[1] : ws.pkeys[0];
-  ws.pair_sorted_vals = (ppass & 1) ? ws.pvals[1] : ws.pvals[0];
+  run_binning(ws, ds, P, tiles_x, ntiles, st, L);
   if (pf) pf->end(st);
-  GSF_CUDA_CHECK(cudaMemsetAsync(ws.ranges, 0, sizeof(int2) * ntiles, st));
-  k_ranges<<<div_up(std::max<int64_t>(pair_cap, 1), 256), 256, 0, st>>>(ws.pair_sorted_keys, &ds->M, pair_cap, ws.ranges);
-  ++*L;
   const float* loss_rgb = a.loss_rgb;
 #define GSF_BLEND_ARGS                                                                                                 \
-  ws.ranges, ws.pair_sorted_vals, ws.pair_rank, ws.bg, ws.gg, ws.rank_to_id, a.obs, loss_rgb, a.loss_depth, a.W, a.H, \
+  ws.ranges, ws.sid, ws.bg_id, ws.gg_id, a.obs, loss_rgb, a.loss_depth, a.W, a.H,                                     \
       tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid, \
-      ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w, ws.last, ws.loss_part
+      ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w, ws.last, ws.loss_part, \
+      a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket
   if (pf) pf->begin(PROF_BLEND, st);
   if (a.lp.mode == 1 && loss_rgb)
     k_blend<1><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);

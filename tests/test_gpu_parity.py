@@ -101,15 +101,37 @@ def test_forward_bit_exact_vs_mirror(gpu_ctx, orc):
         assert r.num_visible == mr.num_visible and r.num_pairs == mr.num_pairs, seed
         assert (r.visible == mr.visible).all()
         ntiles = ((K.width + 15) // 16) * ((K.height + 15) // 16)
-        r2i, tr, pr = gpu_ctx.render_tiles(r.num_visible, ntiles, r.num_pairs)
-        assert (r2i == mr.rank_to_id).all(), seed
+        tr, pp = gpu_ctx.render_tiles(ntiles, r.num_pairs)
+        assert r.num_visible == len(mr.rank_to_id), seed
         assert (tr.ravel() == mr.tile_range).all(), seed
-        assert (pr == mr.pair_rank).all(), seed
+        assert (pp == mr.rank_to_id[mr.pair_rank]).all(), seed
         for k in ("per_pixel_count", "dominant", "median_prim", "median_valid"):
             assert (getattr(r, k) == getattr(mr, k)).all(), (seed, k)
         for k in ("color", "alpha_depth", "median_depth", "opacity", "uncertainty", "final_transmittance",
                   "dominant_weight"):
             assert np.array_equal(getattr(r, k), getattr(mr, k)), (seed, k)
+
+
+@pytest.mark.parametrize("count", [700, 1500, 5000])
+def test_long_tile_lists_bit_exact(gpu_ctx, orc, count):
+    """Tile lists longer than one shared-memory chunk (chunk sort + merge passes) and exact
+    fp64 depth ties (broken by id, rasterizer.cpp:74-77) match the mirror's std::sort order."""
+    m = orc.random_scene(7 + count, count)
+    rng = np.random.default_rng(count)
+    m.mean[:, :2] = rng.uniform(-0.15, 0.15, (count, 2))
+    m.mean[:, 2] = np.round(rng.uniform(1.5, 3.0, count), 2)   # many identical depths
+    m = f32_round(m)
+    K = make_intrinsics(32, 32, 30.0)
+    _upload(gpu_ctx, m)
+    r = gpu_ctx.render(pose(), K)
+    mr = orc.mirror_render(m, pose(), K)
+    tr, pp = gpu_ctx.render_tiles(4, r.num_pairs)
+    assert (tr[:, 1] - tr[:, 0]).max() > count // 2
+    assert (tr.ravel() == mr.tile_range).all()
+    assert (pp == mr.rank_to_id[mr.pair_rank]).all()
+    for k in ("per_pixel_count", "dominant", "median_prim"):
+        assert (getattr(r, k) == getattr(mr, k)).all(), k
+    assert np.array_equal(r.color, mr.color)
 
 
 def test_forward_vs_fp64_oracle(gpu_ctx, orc):
