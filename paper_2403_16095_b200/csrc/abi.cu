@@ -249,7 +249,7 @@ void ensure_map(gsf_ctx_s* c, int64_t P, int K) {
 }
 
 void alloc_pairs(Workspace& ws) {
-  dalloc(ws.ukey, ws.pair_cap);
+
   dalloc(ws.skey, ws.pair_cap); dalloc(ws.sid, ws.pair_cap);
   dalloc(ws.partials, ws.pair_cap * 10);
 }
@@ -263,11 +263,14 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
     dalloc(ws.pj_id, static_cast<size_t>(P) * 36);
     dalloc(ws.big_ids, P);
+    dalloc(ws.vis_list, P);
+    dalloc(ws.world, P);
+    dalloc(ws.support, P);
     ws.P_cap = P;
     dfree(ws.pose_part);
   }
   if (ws.pair_cap == 0) ws.pair_cap = std::max<int64_t>(1 << 20, 4 * P);
-  if (!ws.ukey) alloc_pairs(ws);
+  if (!ws.skey) alloc_pairs(ws);
   if (npix > ws.npix_cap) {
     dalloc(ws.color, 3 * npix); dalloc(ws.alpha_depth, npix); dalloc(ws.median_depth, npix); dalloc(ws.median_valid, npix);
     dalloc(ws.opacity, npix); dalloc(ws.uncertainty, npix); dalloc(ws.final_T, npix); dalloc(ws.count, npix);
@@ -277,15 +280,17 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   }
   if (tiles > ws.tiles_cap) {
     dalloc(ws.ranges, tiles);
-    dalloc(ws.bins, tiles * std::max(kBinStride, 2) + kCntNum);
+    dalloc(ws.bins, tiles * kBinStride + kCntNum);
     dalloc(ws.tile_start, tiles);
-    ws.tile_cnt = ws.bins;
-    ws.tile_fill = kBinStride == 1 ? ws.bins + tiles : ws.bins + 1;
-    ws.bin_counters = ws.bins + tiles * std::max(kBinStride, 2);
+    ws.tile_fill = ws.bins;
+    ws.bin_counters = ws.bins + tiles * kBinStride;
+    dfree(ws.bucket);
     dalloc(ws.loss_part, tiles * LS_NUM);
     ws.tiles_cap = tiles;
     dfree(ws.pose_part);
   }
+  if (ws.bucket_cap == 0) ws.bucket_cap = 2048;
+  if (!ws.bucket) dalloc(ws.bucket, static_cast<size_t>(ws.tiles_cap) * ws.bucket_cap);
   if (!ws.pose_part) dalloc(ws.pose_part, static_cast<size_t>(std::max<int64_t>(div_up(ws.P_cap, 256), ws.tiles_cap)) * 6);
   const int64_t red = 2 * std::max<int64_t>(div_up(npix, 256), div_up(P, 256)) + 64;
   if (!ws.red_part || ws.red_iso_offset * 2 < red) {
@@ -295,10 +300,18 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   if (!c->counters) dalloc(c->counters, 16);
 }
 
+// After an overflow: grow the pair lists and/or the per-tile buckets to fit the last render.
 void grow_pairs(gsf_ctx_s* c, uint32_t needed) {
   Workspace& ws = c->ws;
-  ws.pair_cap = static_cast<int64_t>(needed) + needed / 4 + 1024;
-  alloc_pairs(ws);
+  if (needed > ws.pair_cap) {
+    ws.pair_cap = static_cast<int64_t>(needed) + needed / 4 + 1024;
+    alloc_pairs(ws);
+  }
+  const int64_t longest = c->ds_host->max_tile;
+  if (longest > ws.bucket_cap) {
+    while (ws.bucket_cap < longest + longest / 4) ws.bucket_cap *= 2;
+    dalloc(ws.bucket, static_cast<size_t>(ws.tiles_cap) * ws.bucket_cap);
+  }
 }
 
 FwdArgs fwd_args(gsf_ctx_s* c, const gsf_intrinsics& k, const gsf_raster_cfg& cfg, const float* obs, const float* loss_rgb,
@@ -592,7 +605,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   Workspace& ws = c->ws;
   void* bufs[] = {ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
-                  ws.ukey, ws.skey, ws.sid, ws.big_ids, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
+                  ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
                   ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.pj_id,
                   ws.red_part, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
@@ -1053,10 +1066,13 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
   const int64_t npix = static_cast<int64_t>(k.width) * k.height;
   // per iteration: forward (its last CTA finalises the loss), pose backward (its last CTA sums
   // the pose gradient) and the single-thread pose step
+  // the map is constant during track_frame: validate it and cache its view-independent part once
+  run_world(c->ws, c->ds, c->params, c->P, make_rp(c, k, rcfg), c->stream, &c->launches);
   for (int it = 0; it < tcfg.iterations; ++it) {
     FwdArgs fa = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it);
     fa.want_posejac = true;
     fa.fuse_loss_final = true;
+    fa.use_world = true;
     run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
     BwdArgs b = bwd_args(c, k, rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);
     b.fused_pose = true;
@@ -1066,6 +1082,7 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
   // final render + loss without gradients (tracker.cpp:74-76)
   FwdArgs fin = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, -1);
   fin.fuse_loss_final = true;
+  fin.use_world = true;
   run_forward(c->ws, c->ds, fin, c->stream, &c->launches);
   (void)tiles;
   (void)npix;

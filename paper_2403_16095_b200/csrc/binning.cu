@@ -5,13 +5,14 @@
 // (rasterizer.cpp:193-212), so every tile list is in global depth order.  Only the per-tile
 // order is observable, so the device bins first and sorts each tile's (short) list:
 //
-//   k_preprocess    (raster_fwd.cu) counts the visible primitives, histograms their tile
-//                   rectangles and lists the few primitives with more than kBigPairs tiles
-//   k_tile_scan     one CTA: exclusive scan of the tile counts -> list starts, pair total M
-//   k_scatter       every (tile, primitive) pair claims a slot of its tile; a warp flattens the
-//                   pairs of its 32 primitives over its lanes (order inside a tile is arbitrary)
+//   k_scatter       every (tile, primitive) pair claims a slot of its tile's bucket with one
+//                   atomic on the tile's fill counter (one counter per L2 sector); a warp flattens
+//                   the pairs of its 32 primitives over its lanes, and lists the few primitives
+//                   with more than kBigPairs tiles (order inside a bucket is arbitrary)
 //   k_scatter_big   one 1024-thread CTA per listed large-footprint primitive, so a primitive
 //                   covering a thousand tiles does not serialise one warp
+//   k_tile_scan     one CTA: exclusive scan of the tile counts -> list starts, pair total M,
+//                   longest list (a bucket overflow makes the host grow the buckets and re-run)
 //   k_tile_sort     one CTA per tile: 32-key runs sorted in registers (warp bitonic), then
 //                   pairwise run merges by rank (binary search in the partner run) in shared
 //                   memory; lists longer than kSortChunk are chunk-sorted and merged (merge path)
@@ -28,30 +29,34 @@ namespace gsfk {
 
 namespace {
 
-constexpr int kSortChunk = 2048;   // longest list sorted entirely in shared memory (2 x 16 KB)
+constexpr int kSortChunk = 1024;   // longest list sorted entirely in shared memory (2 x 8 KB)
 
 __device__ __forceinline__ unsigned long long pair_key(double depth, uint32_t id) {
   return (static_cast<unsigned long long>(static_cast<uint32_t>(__float_as_int(static_cast<float>(depth)))) << 32) | id;
 }
 
-__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__ cnt, int ntiles,
+__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__ fill, int ntiles, uint32_t bucket_cap,
                                                     uint32_t* __restrict__ start, const uint32_t* counters,
                                                     uint32_t pair_cap, DevState* ds) {
   __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_carry;
+  __shared__ uint32_t s_max[32];
+  __shared__ uint32_t s_carry, s_mx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = 0;
+  if (tid == 0) s_carry = s_mx = 0;
   __syncthreads();
   for (int base = 0; base < ntiles; base += 1024) {
     const int t = base + tid;
-    const uint32_t v = t < ntiles ? cnt[static_cast<int64_t>(t) * kBinStride] : 0u;
+    const uint32_t f = t < ntiles ? fill[static_cast<int64_t>(t) * kBinStride] : 0u;
+    const uint32_t v = min(f, bucket_cap);
     uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
+    const uint32_t wm = __reduce_max_sync(0xffffffffu, f);
     if (lane == 31) s_warp[warp] = x;
+    if (lane == 0) s_max[warp] = wm;
     __syncthreads();
     if (warp == 0) {
       uint32_t w = s_warp[lane];
@@ -61,6 +66,8 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__
         if (lane >= o) w += y;
       }
       s_warp[lane] = w;
+      const uint32_t m = __reduce_max_sync(0xffffffffu, s_max[lane]);
+      if (lane == 0) s_mx = max(s_mx, m);
     }
     __syncthreads();
     const uint32_t incl = s_carry + (warp ? s_warp[warp - 1] : 0u) + x;
@@ -72,14 +79,22 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__
   if (tid == 0) {
     ds->M = s_carry;
     ds->V = counters[kCntVisible];
-    if (s_carry > pair_cap) ds->overflow = 1u;
+    ds->max_tile = s_mx;
+    if (s_carry > pair_cap || s_mx > bucket_cap) ds->overflow = 1u;
   }
+}
+
+__device__ __forceinline__ void bucket_put(uint32_t* fill, unsigned long long* bucket, uint32_t bucket_cap, int64_t t,
+                                           unsigned long long key) {
+  const uint32_t slot = atomicAdd(&fill[t * kBinStride], 1u);
+  if (slot < bucket_cap) bucket[t * bucket_cap + slot] = key;
 }
 
 __global__ void __launch_bounds__(256) k_scatter(const uint8_t* __restrict__ visible, const int4* __restrict__ rect_id,
                                                  const double* __restrict__ depth_id, int64_t P, int tiles_x,
-                                                 const uint32_t* __restrict__ start, uint32_t* __restrict__ fill,
-                                                 uint32_t pair_cap, unsigned long long* __restrict__ ukey) {
+                                                 uint32_t* __restrict__ fill, uint32_t bucket_cap,
+                                                 unsigned long long* __restrict__ bucket, uint32_t* counters,
+                                                 uint32_t* __restrict__ big_ids) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool vis = i < P && visible[i];
@@ -91,7 +106,10 @@ __global__ void __launch_bounds__(256) k_scatter(const uint8_t* __restrict__ vis
   }
   const int w = q.y - q.x + 1;
   int c = vis ? w * (q.w - q.z + 1) : 0;
-  if (c > kBigPairs) c = 0;   // listed by k_preprocess for k_scatter_big
+  if (c > kBigPairs) {   // k_scatter_big's
+    big_ids[atomicAdd(&counters[kCntBig], 1u)] = static_cast<uint32_t>(i);
+    c = 0;
+  }
   const int excl = warp_excl_scan(c);
   const int total = __shfl_sync(0xffffffffu, excl + c, 31);
   for (int base = 0; base < total; base += 32) {
@@ -103,18 +121,15 @@ __global__ void __launch_bounds__(256) k_scatter(const uint8_t* __restrict__ vis
     if (k < total) {
       const int r = k - ej;
       const int row = r / wj;
-      const int64_t t = (qy0 + row) * tiles_x + qx0 + (r - row * wj);
-      const uint32_t pos = start[t] + atomicAdd(&fill[t * kBinStride], 1u);
-      if (pos < pair_cap) ukey[pos] = kj;
+      bucket_put(fill, bucket, bucket_cap, (qy0 + row) * tiles_x + qx0 + (r - row * wj), kj);
     }
   }
 }
 
 __global__ void __launch_bounds__(1024) k_scatter_big(const uint32_t* __restrict__ big_ids, const uint32_t* counters,
                                                       const int4* __restrict__ rect_id, const double* __restrict__ depth_id,
-                                                      int tiles_x, const uint32_t* __restrict__ start,
-                                                      uint32_t* __restrict__ fill, uint32_t pair_cap,
-                                                      unsigned long long* __restrict__ ukey) {
+                                                      int tiles_x, uint32_t* __restrict__ fill, uint32_t bucket_cap,
+                                                      unsigned long long* __restrict__ bucket) {
   const uint32_t nbig = counters[kCntBig];
   for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
     const uint32_t id = big_ids[b];
@@ -124,9 +139,7 @@ __global__ void __launch_bounds__(1024) k_scatter_big(const uint32_t* __restrict
     const int c = w * (q.w - q.z + 1);
     for (int r = threadIdx.x; r < c; r += blockDim.x) {
       const int row = r / w;
-      const int64_t t = (q.z + row) * tiles_x + q.x + (r - row * w);
-      const uint32_t pos = start[t] + atomicAdd(&fill[t * kBinStride], 1u);
-      if (pos < pair_cap) ukey[pos] = key;
+      bucket_put(fill, bucket, bucket_cap, (q.z + row) * tiles_x + q.x + (r - row * w), key);
     }
   }
 }
@@ -160,45 +173,61 @@ __device__ __forceinline__ int run_rank(const unsigned long long* r, int len, un
   return lo;
 }
 
-// Sort n <= kSortChunk keys (src) into dst: register-sorted 32-runs, then pairwise merges by rank
-// in shared memory.  Padding (~0) sorts to the end; equal padding keys are separated by the
-// lower/upper rank rule of the two runs, so every element gets a distinct slot.
-__device__ void sort_chunk(const unsigned long long* src, unsigned long long* dst, int n,
-                           unsigned long long (*s_k)[kSortChunk]) {
+// Sort n <= kSortChunk keys of src (global) in shared memory: register-sorted 32-runs, then
+// pairwise merges by rank.  Returns the s_k buffer holding the sorted keys (first n; the padding
+// ~0 sorts to the end, and equal padding keys are separated by the lower/upper rank rule of the
+// two runs, so every element gets a distinct slot).
+__device__ int sort_chunk(const unsigned long long* src, int n, unsigned long long (*s_k)[kSortChunk]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int nruns = (n + 31) >> 5;
   const int N = nruns << 5;
   for (int r = warp; r < nruns; r += nwarps) {
     const int i = (r << 5) + lane;
-    const unsigned long long k = warp_sort32(i < n ? src[i] : ~0ull);
-    if (nruns == 1) {
-      if (i < n) dst[i] = k;
-    } else {
-      s_k[0][i] = k;
-    }
+    s_k[0][i] = warp_sort32(i < n ? src[i] : ~0ull);
   }
-  if (nruns == 1) return;
   __syncthreads();
   int buf = 0;
   for (int w = 32; w < N; w <<= 1) {
-    const bool last_pass = (w << 1) >= N;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       const int r = i / w;
-      const int own = i - r * w;
       const int pbeg = (r ^ 1) * w;
-      const int base = (r & ~1) * w;
       const unsigned long long k = s_k[buf][i];
       int pos = i;
-      if (pbeg < N) pos = base + own + run_rank(&s_k[buf][pbeg], min(w, N - pbeg), k, (r & 1) != 0);
-      if (last_pass) {
-        if (pos < n) dst[pos] = k;
-      } else {
-        s_k[buf ^ 1][pos] = k;
-      }
+      if (pbeg < N) pos = (r & ~1) * w + (i - r * w) + run_rank(&s_k[buf][pbeg], min(w, N - pbeg), k, (r & 1) != 0);
+      s_k[buf ^ 1][pos] = k;
     }
     __syncthreads();
     buf ^= 1;
   }
+  return buf;
+}
+
+// Runs of equal fp32 depth in (fp64 depth, id) order (rasterizer.cpp:74-77): the first thread of
+// each run insertion-sorts it (runs are a handful of keys).  Ends with a __syncthreads().
+__device__ void fix_ties(unsigned long long* k, int n, const double* __restrict__ depth_id) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t hi = static_cast<uint32_t>(k[i] >> 32);
+    const bool starts = (i == 0 || static_cast<uint32_t>(k[i - 1] >> 32) != hi) && i + 1 < n &&
+                        static_cast<uint32_t>(k[i + 1] >> 32) == hi;
+    if (!starts) continue;
+    int e = i + 2;
+    while (e < n && static_cast<uint32_t>(k[e] >> 32) == hi) ++e;
+    for (int a = i + 1; a < e; ++a) {
+      const unsigned long long ka = k[a];
+      const uint32_t ida = static_cast<uint32_t>(ka);
+      const double da = depth_id[ida];
+      int b = a - 1;
+      while (b >= i) {
+        const uint32_t idb = static_cast<uint32_t>(k[b]);
+        const double db = depth_id[idb];
+        if (db < da || (db == da && idb < ida)) break;
+        k[b + 1] = k[b];
+        --b;
+      }
+      k[b + 1] = ka;
+    }
+  }
+  __syncthreads();
 }
 
 // One merge pass over a segment of n keys: runs of width w in a -> runs of 2w in b.
@@ -228,60 +257,45 @@ __device__ void merge_pass(const unsigned long long* a, unsigned long long* b, i
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ start,
-                                                   uint32_t pair_cap, unsigned long long* ukey, unsigned long long* skey,
-                                                   uint32_t* __restrict__ sid, const double* __restrict__ depth_id,
-                                                   int2* __restrict__ ranges) {
+__global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ fill, const uint32_t* __restrict__ start,
+                                                   uint32_t pair_cap, unsigned long long* bucket, uint32_t bucket_cap,
+                                                   unsigned long long* skey, uint32_t* __restrict__ sid,
+                                                   const double* __restrict__ depth_id, int2* __restrict__ ranges) {
   __shared__ unsigned long long s_k[2][kSortChunk];
   const int t = blockIdx.x;
   const uint32_t s0 = min(start[t], pair_cap);
-  const int n = static_cast<int>(min(cnt[static_cast<int64_t>(t) * kBinStride], pair_cap - s0));
+  const int n = static_cast<int>(min(min(fill[static_cast<int64_t>(t) * kBinStride], bucket_cap), pair_cap - s0));
   if (threadIdx.x == 0) ranges[t] = n ? make_int2(static_cast<int>(s0), static_cast<int>(s0) + n) : make_int2(0, 0);
   if (n == 0) return;
-  unsigned long long* uk = ukey + s0;
+  unsigned long long* bk = bucket + static_cast<int64_t>(t) * bucket_cap;
   unsigned long long* sk = skey + s0;
   if (n <= kSortChunk) {
-    sort_chunk(uk, sk, n, s_k);
-  } else {
-    // long list: sorted chunks, then merge passes ping-ponging between the two buffers
-    for (int c = 0; c < n; c += kSortChunk) {
-      sort_chunk(uk + c, sk + c, min(kSortChunk, n - c), s_k);
-      __syncthreads();
+    unsigned long long* k = s_k[sort_chunk(bk, n, s_k)];
+    fix_ties(k, n, depth_id);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long v = k[i];
+      sk[i] = v;
+      sid[s0 + i] = static_cast<uint32_t>(v);
     }
-    bool in_s = true;
-    for (int w = kSortChunk; w < n; w *= 2) {
-      merge_pass(in_s ? sk : uk, in_s ? uk : sk, n, w);
-      in_s = !in_s;
-    }
-    if (!in_s)
-      for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = uk[i];
+    return;
   }
-  __syncthreads();
-  // fix-up: runs of equal fp32 depth in (fp64 depth, id) order (rasterizer.cpp:74-77); the
-  // first thread of each run insertion-sorts it (runs are a handful of keys)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint32_t hi = static_cast<uint32_t>(sk[i] >> 32);
-    const bool starts = (i == 0 || static_cast<uint32_t>(sk[i - 1] >> 32) != hi) && i + 1 < n &&
-                        static_cast<uint32_t>(sk[i + 1] >> 32) == hi;
-    if (!starts) continue;
-    int e = i + 2;
-    while (e < n && static_cast<uint32_t>(sk[e] >> 32) == hi) ++e;
-    for (int a = i + 1; a < e; ++a) {
-      const unsigned long long ka = sk[a];
-      const uint32_t ida = static_cast<uint32_t>(ka);
-      const double da = depth_id[ida];
-      int b = a - 1;
-      while (b >= i) {
-        const uint32_t idb = static_cast<uint32_t>(sk[b]);
-        const double db = depth_id[idb];
-        if (db < da || (db == da && idb < ida)) break;
-        sk[b + 1] = sk[b];
-        --b;
-      }
-      sk[b + 1] = ka;
-    }
+  // long list: sorted chunks into skey, then merge passes ping-ponging with the (consumed) bucket
+  for (int c = 0; c < n; c += kSortChunk) {
+    const int m = min(kSortChunk, n - c);
+    const unsigned long long* k = s_k[sort_chunk(bk + c, m, s_k)];
+    for (int i = threadIdx.x; i < m; i += blockDim.x) sk[c + i] = k[i];
+    __syncthreads();
   }
-  __syncthreads();
+  bool in_s = true;
+  for (int w = kSortChunk; w < n; w *= 2) {
+    merge_pass(in_s ? sk : bk, in_s ? bk : sk, n, w);
+    in_s = !in_s;
+  }
+  if (!in_s) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sk[i] = bk[i];
+    __syncthreads();
+  }
+  fix_ties(sk, n, depth_id);
   for (int i = threadIdx.x; i < n; i += blockDim.x) sid[s0 + i] = static_cast<uint32_t>(sk[i]);
 }
 
@@ -289,17 +303,19 @@ __global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ 
 
 void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles, cudaStream_t st, int64_t* L) {
   const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
-  k_tile_scan<<<1, 1024, 0, st>>>(ws.tile_cnt, ntiles, ws.tile_start, ws.bin_counters, pair_cap, ds);
-  ++*L;
+  const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
   if (P > 0) {
-    k_scatter<<<div_up(P, 256), 256, 0, st>>>(ws.visible, ws.rect_id, ws.depth_id, P, tiles_x, ws.tile_start, ws.tile_fill,
-                                              pair_cap, ws.ukey);
+    k_scatter<<<div_up(P, 256), 256, 0, st>>>(ws.visible, ws.rect_id, ws.depth_id, P, tiles_x, ws.tile_fill, bcap, ws.bucket,
+                                              ws.bin_counters, ws.big_ids);
     ++*L;
-    k_scatter_big<<<128, 1024, 0, st>>>(ws.big_ids, ws.bin_counters, ws.rect_id, ws.depth_id, tiles_x, ws.tile_start,
-                                        ws.tile_fill, pair_cap, ws.ukey);
+    k_scatter_big<<<128, 1024, 0, st>>>(ws.big_ids, ws.bin_counters, ws.rect_id, ws.depth_id, tiles_x, ws.tile_fill, bcap,
+                                        ws.bucket);
     ++*L;
   }
-  k_tile_sort<<<ntiles, 256, 0, st>>>(ws.tile_cnt, ws.tile_start, pair_cap, ws.ukey, ws.skey, ws.sid, ws.depth_id, ws.ranges);
+  k_tile_scan<<<1, 1024, 0, st>>>(ws.tile_fill, ntiles, bcap, ws.tile_start, ws.bin_counters, pair_cap, ds);
+  ++*L;
+  k_tile_sort<<<ntiles, 256, 0, st>>>(ws.tile_fill, ws.tile_start, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id,
+                                      ws.ranges);
   ++*L;
 }
 

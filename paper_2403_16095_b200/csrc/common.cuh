@@ -9,9 +9,11 @@
 namespace gsfk {
 
 constexpr int kTile = 16;
-// Binning: per-tile counters (stride kBinStride u32), primitives with more than kBigPairs tiles
-// go to the one-CTA-per-primitive scatter, and the slots of Workspace::bin_counters.
-constexpr int kBinStride = 1;
+// Binning: one fill counter per 32-byte L2 sector (the L2 serialises atomics per sector:
+// measured 35 us for the 563k pair increments of configs[1] packed vs 12 us one per sector),
+// primitives with more than kBigPairs tiles go to the one-CTA-per-primitive scatter, and the
+// slots of Workspace::bin_counters.
+constexpr int kBinStride = 8;
 constexpr int kBigPairs = 128;
 enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
 constexpr int kTilePixels = kTile * kTile;
@@ -80,7 +82,8 @@ enum LossSlot {
 struct DevState {
   uint32_t V;              // visible primitives of the current render
   uint32_t M;              // (tile, primitive) pairs of the current render
-  uint32_t overflow;       // pair capacity exceeded (host grows and re-runs)
+  uint32_t overflow;       // pair / tile-bucket capacity exceeded (host grows and re-runs)
+  uint32_t max_tile;       // longest tile list of the current render
   int32_t bad_index;       // smallest non-finite primitive index, INT32_MAX if none
   int32_t halt;            // 0 run, 1 nothing to track at it 0, 2 diverged, 3 non-finite map
   int32_t halt_iter;

@@ -246,18 +246,111 @@ GSF_HD void sh_basis_grad_d(int degree, double x, double y, double z, double* g)
 
 GSF_HD int sh_degree(int K) { return K >= 16 ? 3 : (K >= 9 ? 2 : (K >= 4 ? 1 : 0)); }
 
-// One primitive.  p = pointer to field 0 of this primitive in a SoA [field][stride] fp32
-// block (mean 0-2, log_scale 3-5, quat 6-9, opacity_logit 10, sh 11+3b+c).
-GSF_HD PreOut preprocess_one(const float* p, int64_t stride, const Cam& cam, const RasterParams& rp) {
+// View-independent part of one primitive, cached per map version by the tracking loop (the
+// map is constant during track_frame): exactly the values project_core would compute.
+struct WorldG {
+  double S[9];       // world covariance R diag(exp(2 ls)) R^T (primitive.hpp:46-50)
+  double sigma;      // sigmoid(opacity_logit) (primitive.hpp:11,33)
+  double color[3];   // SH colour; view-independent when sh_coeffs <= 1
+  double pad;
+};
+
+// support = footprint_sigma * exp(max log_scale)  (rasterizer.cpp:55)
+GSF_HD double world_support(const float* p, int64_t stride, const RasterParams& rp) {
+  const double l0 = p[3 * stride], l1 = p[4 * stride], l2 = p[5 * stride];
+  return dmul(rp.footprint_sigma, exp_d(dmax(dmax(l0, l1), l2)));
+}
+
+// Parameters read straight from the SoA [field][stride] fp32 block (mean 0-2, log_scale 3-5,
+// quat 6-9, opacity_logit 10, sh 11+3b+c); p points at field 0 of this primitive.
+struct ParamSrc {
+  const float* p;
+  int64_t stride;
+  int K;
+  GSF_HD void cov(double* S) const {
+    const double l0 = p[3 * stride], l1 = p[4 * stride], l2 = p[5 * stride];
+    const double qw = p[6 * stride], qx = p[7 * stride], qy = p[8 * stride], qz = p[9 * stride];
+    const double qn = dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz)));
+    const double w = ddiv(qw, qn), x = ddiv(qx, qn), y = ddiv(qy, qn), z = ddiv(qz, qn);
+    double R[9];
+    R[0] = dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(z, z))));
+    R[1] = dmul(2.0, dsub(dmul(x, y), dmul(w, z)));
+    R[2] = dmul(2.0, dadd(dmul(x, z), dmul(w, y)));
+    R[3] = dmul(2.0, dadd(dmul(x, y), dmul(w, z)));
+    R[4] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(z, z))));
+    R[5] = dmul(2.0, dsub(dmul(y, z), dmul(w, x)));
+    R[6] = dmul(2.0, dsub(dmul(x, z), dmul(w, y)));
+    R[7] = dmul(2.0, dadd(dmul(y, z), dmul(w, x)));
+    R[8] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
+    const double s2[3] = {exp_d(dmul(2.0, l0)), exp_d(dmul(2.0, l1)), exp_d(dmul(2.0, l2))};
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        S[3 * i + j] = dadd(dadd(dmul(dmul(R[3 * i + 0], s2[0]), R[3 * j + 0]), dmul(dmul(R[3 * i + 1], s2[1]), R[3 * j + 1])),
+                            dmul(dmul(R[3 * i + 2], s2[2]), R[3 * j + 2]));
+  }
+  GSF_HD double sigma() const { return ddiv(1.0, dadd(1.0, exp_d(-static_cast<double>(p[10 * stride])))); }
+  // colour through SH along the normalized view direction (rasterizer.cpp:60-63)
+  GSF_HD void color(const Cam& cam, double m0, double m1, double m2, double* out) const {
+    const double d0 = dsub(m0, cam.center[0]), d1 = dsub(m1, cam.center[1]), d2 = dsub(m2, cam.center[2]);
+    const double len = dsqrt(dadd(dadd(dmul(d0, d0), dmul(d1, d1)), dmul(d2, d2)));
+    double dx = 0.0, dy = 0.0, dz = 1.0;
+    if (len > 1e-12) { dx = ddiv(d0, len); dy = ddiv(d1, len); dz = ddiv(d2, len); }
+    if (K <= 0) {
+      out[0] = out[1] = out[2] = 0.5;
+      return;
+    }
+    double b[16];
+    sh_basis(sh_degree(K), dx, dy, dz, b);
+    for (int c = 0; c < 3; ++c) {
+      double acc = 0.5;
+      for (int k = 0; k < K; ++k) acc = dadd(acc, dmul(b[k], static_cast<double>(p[(11 + 3 * k + c) * stride])));
+      out[c] = dmax(acc, 0.0);
+    }
+  }
+};
+
+// The world part from the cache (colour from the parameters when it is view-dependent).
+struct CachedSrc {
+  const WorldG* w;
+  ParamSrc ps;
+  GSF_HD void cov(double* S) const {
+    for (int i = 0; i < 9; ++i) S[i] = w->S[i];
+  }
+  GSF_HD double sigma() const { return w->sigma; }
+  GSF_HD void color(const Cam& cam, double m0, double m1, double m2, double* out) const {
+    if (ps.K <= 1) {
+      out[0] = w->color[0]; out[1] = w->color[1]; out[2] = w->color[2];
+    } else {
+      ps.color(cam, m0, m1, m2, out);
+    }
+  }
+};
+
+// WorldG of one primitive (the colour is evaluated along +z: exact when sh_coeffs <= 1).
+GSF_HD WorldG make_world(const float* p, int64_t stride, int K) {
+  WorldG g;
+  const ParamSrc ps{p, stride, K};
+  ps.cov(g.S);
+  g.sigma = ps.sigma();
+  g.color[0] = g.color[1] = g.color[2] = 0.5;
+  if (K == 1) {
+    for (int c = 0; c < 3; ++c) g.color[c] = dmax(dadd(0.5, dmul(0.28209479177387814, static_cast<double>(p[(11 + c) * stride]))), 0.0);
+  }
+  g.pad = 0.0;
+  return g;
+}
+
+// Camera part of project_all + project_gaussian + tile rectangle for one primitive; the world
+// quantities are pulled from src only once the cheap culling tests have passed.
+template <class Src>
+GSF_HD PreOut project_core(double m0, double m1, double m2, double support, const Src& src, const Cam& cam,
+                           const RasterParams& rp) {
   PreOut o;
   o.visible = 0;
   o.depth = 0.0;
   o.mx = o.my = o.c00 = o.c01 = o.c11 = o.radius = o.sigma = 0.0;
   o.color[0] = o.color[1] = o.color[2] = 0.0;
   o.tx0 = o.tx1 = o.ty0 = o.ty1 = 0;
-  const double m0 = p[0 * stride], m1 = p[1 * stride], m2 = p[2 * stride];
-  const double l0 = p[3 * stride], l1 = p[4 * stride], l2 = p[5 * stride];
-  const double qw = p[6 * stride], qx = p[7 * stride], qy = p[8 * stride], qz = p[9 * stride];
   const double* W = cam.W;
   // p_cam = W * mean + t
   const double pc0 = dadd(dadd(dadd(dmul(W[0], m0), dmul(W[1], m1)), dmul(W[2], m2)), cam.t[0]);
@@ -265,9 +358,6 @@ GSF_HD PreOut preprocess_one(const float* p, int64_t stride, const Cam& cam, con
   const double pc2 = dadd(dadd(dadd(dmul(W[6], m0), dmul(W[7], m1)), dmul(W[8], m2)), cam.t[2]);
   o.depth = pc2;
   if (!(pc2 > cam.near_plane) || !(pc2 < cam.far_plane)) return o;
-  // support = footprint_sigma * exp(max log_scale)  (rasterizer.cpp:55)
-  const double lmax = dmax(dmax(l0, l1), l2);
-  const double support = dmul(rp.footprint_sigma, exp_d(lmax));
   if (support > 0.0) {
     if (!(dsub(pc2, support) > 0.0)) return o;
     const double pad = dmul(rp.footprint_sigma, dsqrt(dmax(0.0, rp.dilation)));
@@ -280,25 +370,8 @@ GSF_HD PreOut preprocess_one(const float* p, int64_t stride, const Cam& cam, con
   }
   o.mx = dadd(ddiv(dmul(cam.fx, pc0), pc2), cam.cx);
   o.my = dadd(ddiv(dmul(cam.fy, pc1), pc2), cam.cy);
-  // world covariance R diag(exp(2 ls)) R^T (primitive.hpp:46-50)
-  const double qn = dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz)));
-  const double w = ddiv(qw, qn), x = ddiv(qx, qn), y = ddiv(qy, qn), z = ddiv(qz, qn);
-  double R[9];
-  R[0] = dsub(1.0, dmul(2.0, dadd(dmul(y, y), dmul(z, z))));
-  R[1] = dmul(2.0, dsub(dmul(x, y), dmul(w, z)));
-  R[2] = dmul(2.0, dadd(dmul(x, z), dmul(w, y)));
-  R[3] = dmul(2.0, dadd(dmul(x, y), dmul(w, z)));
-  R[4] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(z, z))));
-  R[5] = dmul(2.0, dsub(dmul(y, z), dmul(w, x)));
-  R[6] = dmul(2.0, dsub(dmul(x, z), dmul(w, y)));
-  R[7] = dmul(2.0, dadd(dmul(y, z), dmul(w, x)));
-  R[8] = dsub(1.0, dmul(2.0, dadd(dmul(x, x), dmul(y, y))));
-  const double s2[3] = {exp_d(dmul(2.0, l0)), exp_d(dmul(2.0, l1)), exp_d(dmul(2.0, l2))};
-  double S[9];  // (R diag(s2)) R^T
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j)
-      S[3 * i + j] = dadd(dadd(dmul(dmul(R[3 * i + 0], s2[0]), R[3 * j + 0]), dmul(dmul(R[3 * i + 1], s2[1]), R[3 * j + 1])),
-                          dmul(dmul(R[3 * i + 2], s2[2]), R[3 * j + 2]));
+  double S[9];
+  src.cov(S);
   // J (projection.cpp:26-33)
   const double iz = ddiv(1.0, pc2);
   const double iz2 = dmul(iz, iz);
@@ -335,25 +408,8 @@ GSF_HD PreOut preprocess_one(const float* p, int64_t stride, const Cam& cam, con
       dadd(o.my, o.radius) < 0.0 || dsub(o.my, o.radius) > static_cast<double>(cam.height))
     return o;
   o.visible = 1;
-  // sigmoid(opacity_logit) (primitive.hpp:11,33)
-  o.sigma = ddiv(1.0, dadd(1.0, exp_d(-static_cast<double>(p[10 * stride]))));
-  // colour through SH along the normalized view direction (rasterizer.cpp:60-63)
-  const int K = rp.sh_coeffs;
-  const double d0 = dsub(m0, cam.center[0]), d1 = dsub(m1, cam.center[1]), d2 = dsub(m2, cam.center[2]);
-  const double len = dsqrt(dadd(dadd(dmul(d0, d0), dmul(d1, d1)), dmul(d2, d2)));
-  double dx = 0.0, dy = 0.0, dz = 1.0;
-  if (len > 1e-12) { dx = ddiv(d0, len); dy = ddiv(d1, len); dz = ddiv(d2, len); }
-  if (K <= 0) {
-    o.color[0] = o.color[1] = o.color[2] = 0.5;
-  } else {
-    double b[16];
-    sh_basis(sh_degree(K), dx, dy, dz, b);
-    for (int c = 0; c < 3; ++c) {
-      double acc = 0.5;
-      for (int k = 0; k < K; ++k) acc = dadd(acc, dmul(b[k], static_cast<double>(p[(11 + 3 * k + c) * stride])));
-      o.color[c] = dmax(acc, 0.0);
-    }
-  }
+  o.sigma = src.sigma();
+  src.color(cam, m0, m1, m2, o.color);
   // inclusive tile rectangle (rasterizer.cpp:199-208)
   const double ts = static_cast<double>(rp.tile);
   o.tx0 = tile_clamp(ddiv(dsub(o.mx, o.radius), ts), rp.tiles_x - 1);
@@ -361,6 +417,12 @@ GSF_HD PreOut preprocess_one(const float* p, int64_t stride, const Cam& cam, con
   o.ty0 = tile_clamp(ddiv(dsub(o.my, o.radius), ts), rp.tiles_y - 1);
   o.ty1 = tile_clamp(ddiv(dadd(o.my, o.radius), ts), rp.tiles_y - 1);
   return o;
+}
+
+// One primitive from its parameters: project_all + project_gaussian + tile rectangle.
+GSF_HD PreOut preprocess_one(const float* p, int64_t stride, const Cam& cam, const RasterParams& rp) {
+  const double m0 = p[0 * stride], m1 = p[1 * stride], m2 = p[2 * stride];
+  return project_core(m0, m1, m2, world_support(p, stride, rp), ParamSrc{p, stride, rp.sh_coeffs}, cam, rp);
 }
 
 // exp_map (lie.cpp:15-28) in explicit fp64; sin/cos are the platform's.

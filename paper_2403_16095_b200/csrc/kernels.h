@@ -63,17 +63,20 @@ struct Workspace {
   int4* rect_id = nullptr;
   uint8_t* visible = nullptr;
   float* pj_id = nullptr;       // P * 36: pose Jacobians of the visible primitives (tracking)
-  // per tile: bins[t * kBinStride + {0, 1}] = (count, fill cursor), then the counters; one memset
+  WorldG* world = nullptr;      // P: view-independent part, cached per tracked frame (k_world)
+  double* support = nullptr;    // P: footprint support of the same cache (NaN = invalid primitive)
+  // per tile: bins[t * kBinStride] = fill cursor of the tile's bucket, then the counters; one memset
   uint32_t* bins = nullptr;
-  uint32_t* tile_cnt = nullptr;
   uint32_t* tile_fill = nullptr;
   uint32_t* bin_counters = nullptr;   // BinCounter slots
   uint32_t* big_ids = nullptr;        // P: primitives with more than kBigPairs tiles
+  uint32_t* vis_list = nullptr;       // P: visible ids (any order), for the pose Jacobians
   uint32_t* tile_start = nullptr;
   int2* ranges = nullptr;
   double* loss_part = nullptr;  // tiles * LS_NUM
   // per (tile, primitive) pair: scattered keys/ids, then each tile's list sorted by (depth, id)
-  unsigned long long* ukey = nullptr;   // (fp32 depth bits << 32 | id), scatter order
+  unsigned long long* bucket = nullptr; // tiles * bucket_cap keys (fp32 depth bits << 32 | id), scatter order
+  int64_t bucket_cap = 0;
   unsigned long long* skey = nullptr;   // the same keys, each tile's list in (depth, id) order
   uint32_t* sid = nullptr;
   float* partials = nullptr;   // pair_cap * 10, at sorted list positions (generic backward)
@@ -121,8 +124,12 @@ struct FwdArgs {
   int iteration;             // loop iteration (for device-side checks), -1 outside loops
   bool want_posejac = false; // tracking: emit the per-primitive pose Jacobians (ws.pj_id)
   bool fuse_loss_final = false;  // tracking: the blend's last CTA runs the loss finalize
+  bool use_world = false;        // preprocess from ws.world / ws.support (run_world ran for this map)
 };
 void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* launches);
+// per-primitive validation + view-independent cache (ws.world, ws.support)
+void run_world(Workspace& ws, DevState* ds, const float* params, int64_t P, const RasterParams& rp, cudaStream_t st,
+               int64_t* launches);
 void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,
                     double near_plane, double far_plane, float floor, cudaStream_t st, int64_t* launches);
 

@@ -22,27 +22,33 @@ namespace {
 // linearised per primitive in fp64, so the tracking backward can apply it right after its
 // per-tile reduction instead of round-tripping every pair partial through memory.
 // Layout (36 floats): J00 J02 J11 J12 | Bc[3][3] | Cr[3][3] | p_cam[3] | Tc[3][3] | pad pad
-__device__ void compute_posejac(const float* __restrict__ p, int64_t stride, const Cam& cam, int K, float* out) {
+__device__ void compute_posejac(const float* __restrict__ p, int64_t stride, const Cam& cam, int K, float* out,
+                                const double* Sw) {
   const double m0 = p[0], m1 = p[stride], m2 = p[2 * stride];
   const double* W = cam.W;
   const double pc[3] = {W[0] * m0 + W[1] * m1 + W[2] * m2 + cam.t[0], W[3] * m0 + W[4] * m1 + W[5] * m2 + cam.t[1],
                         W[6] * m0 + W[7] * m1 + W[8] * m2 + cam.t[2]};
   const double iz = 1.0 / pc[2], iz2 = iz * iz, iz3 = iz2 * iz;
   const double J00 = cam.fx * iz, J02 = -cam.fx * pc[0] * iz2, J11 = cam.fy * iz, J12 = -cam.fy * pc[1] * iz2;
-  const double qw0 = p[6 * stride], qx0 = p[7 * stride], qy0 = p[8 * stride], qz0 = p[9 * stride];
-  const double ql = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
-  const double w = qw0 / ql, x = qx0 / ql, y = qy0 / ql, z = qz0 / ql;
-  const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
-                          {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
-                          {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
-  double s2[3];
-  for (int a = 0; a < 3; ++a) {
-    const double sa = exp(static_cast<double>(p[(3 + a) * stride]));
-    s2[a] = sa * sa;
-  }
   double Cw[3][3], T1[3][3], V[3][3];
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) Cw[a][b] = R[a][0] * s2[0] * R[b][0] + R[a][1] * s2[1] * R[b][1] + R[a][2] * s2[2] * R[b][2];
+  if (Sw) {   // world covariance from the per-frame cache
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) Cw[a][b] = Sw[3 * a + b];
+  } else {
+    const double qw0 = p[6 * stride], qx0 = p[7 * stride], qy0 = p[8 * stride], qz0 = p[9 * stride];
+    const double ql = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
+    const double w = qw0 / ql, x = qx0 / ql, y = qy0 / ql, z = qz0 / ql;
+    const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                            {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                            {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+    double s2[3];
+    for (int a = 0; a < 3; ++a) {
+      const double sa = exp(static_cast<double>(p[(3 + a) * stride]));
+      s2[a] = sa * sa;
+    }
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) Cw[a][b] = R[a][0] * s2[0] * R[b][0] + R[a][1] * s2[1] * R[b][1] + R[a][2] * s2[2] * R[b][2];
+  }
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) T1[a][b] = W[3 * a] * Cw[0][b] + W[3 * a + 1] * Cw[1][b] + W[3 * a + 2] * Cw[2][b];
   for (int a = 0; a < 3; ++a)
@@ -123,38 +129,84 @@ __device__ void compute_posejac(const float* __restrict__ p, int64_t stride, con
   out[34] = out[35] = 0.0f;
 }
 
-template <bool PJ>
-__global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ params, int64_t P, const DevState* ds,
+// Validation + view-independent part of every primitive, once per tracked frame (the map is
+// constant inside track_frame).  Invalid primitives get a NaN support and report bad_index.
+__global__ void __launch_bounds__(256) k_world(const float* __restrict__ params, int64_t P, RasterParams rp,
+                                               WorldG* __restrict__ world, double* __restrict__ support,
+                                               int32_t* bad_index) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int D = kFieldsBase + 3 * rp.sh_coeffs;
+  float v[kFieldsBase];
+#pragma unroll
+  for (int f = 0; f < kFieldsBase; ++f) v[f] = params[f * P + i];
+  bool ok = true;
+#pragma unroll
+  for (int f = 0; f < kFieldsBase; ++f) ok &= isfinite(v[f]);
+  for (int f = kFieldsBase; f < D; ++f) ok &= isfinite(params[f * P + i]);
+  {
+    const double qw = v[6], qx = v[7], qy = v[8], qz = v[9];
+    ok &= dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz))) > 1e-12;
+  }
+  if (!ok) {
+    atomicMin(bad_index, static_cast<int32_t>(i));
+    support[i] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  support[i] = world_support(params + i, P, rp);
+  world[i] = make_world(params + i, P, rp.sh_coeffs);
+}
+
+// CACHED: the world part comes from k_world (tracking loop); otherwise every primitive is
+// validated and projected from its parameters (validate_primitives + project_all).
+template <bool CACHED>
+__global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float* __restrict__ params, int64_t P, const DevState* ds,
                                                     RasterParams rp, BlendG* __restrict__ bg_id, GuardG* __restrict__ gg_id,
                                                     double* __restrict__ depth_id, int4* __restrict__ rect_id,
                                                     uint8_t* __restrict__ visible, int32_t* bad_index, BlendConsts kc,
-                                                    uint32_t* __restrict__ tile_cnt, uint32_t* counters,
-                                                    uint32_t* __restrict__ big_ids, float* __restrict__ pj) {
+                                                    uint32_t* counters, uint32_t* __restrict__ vis_list,
+                                                    const WorldG* __restrict__ world, const double* __restrict__ support) {
   __shared__ uint32_t s_vis[8];
+  __shared__ uint32_t s_base;
+  __shared__ Cam s_cam;   // read through shared memory: 20 doubles need not live in registers
+  if (threadIdx.x < sizeof(Cam) / 4)
+    reinterpret_cast<uint32_t*>(&s_cam)[threadIdx.x] = reinterpret_cast<const uint32_t*>(&ds->cam)[threadIdx.x];
+  __syncthreads();
+  const Cam& cam = s_cam;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   bool vis = false;
   int4 q = make_int4(0, -1, 0, -1);
   if (i < P) {
-    // validate_primitives (rasterizer.cpp:34-44): every field finite and |q| > 1e-12
-    // (all loads issued before any test: no short-circuit chain of dependent memory latencies)
-    const int D = kFieldsBase + 3 * rp.sh_coeffs;
-    float v[kFieldsBase];
-#pragma unroll
-    for (int f = 0; f < kFieldsBase; ++f) v[f] = params[f * P + i];
+    PreOut o;
     bool ok = true;
+    if (CACHED) {
+      const double sup = support[i];
+      ok = !isnan(sup);
+      if (ok) {
+        const double m0 = params[i], m1 = params[P + i], m2 = params[2 * P + i];
+        o = project_core(m0, m1, m2, sup, CachedSrc{world + i, ParamSrc{params + i, P, rp.sh_coeffs}}, cam, rp);
+      }
+    } else {
+      // validate_primitives (rasterizer.cpp:34-44): every field finite and |q| > 1e-12
+      // (all loads issued before any test: no short-circuit chain of dependent memory latencies)
+      const int D = kFieldsBase + 3 * rp.sh_coeffs;
+      float v[kFieldsBase];
 #pragma unroll
-    for (int f = 0; f < kFieldsBase; ++f) ok &= isfinite(v[f]);
-    for (int f = kFieldsBase; f < D; ++f) ok &= isfinite(params[f * P + i]);
-    {
-      const double qw = v[6], qx = v[7], qy = v[8], qz = v[9];
-      ok &= dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz))) > 1e-12;
+      for (int f = 0; f < kFieldsBase; ++f) v[f] = params[f * P + i];
+#pragma unroll
+      for (int f = 0; f < kFieldsBase; ++f) ok &= isfinite(v[f]);
+      for (int f = kFieldsBase; f < D; ++f) ok &= isfinite(params[f * P + i]);
+      {
+        const double qw = v[6], qx = v[7], qy = v[8], qz = v[9];
+        ok &= dsqrt(dadd(dadd(dadd(dmul(qw, qw), dmul(qx, qx)), dmul(qy, qy)), dmul(qz, qz))) > 1e-12;
+      }
+      if (!ok) atomicMin(bad_index, static_cast<int32_t>(i));
+      else o = preprocess_one(params + i, P, cam, rp);
     }
     if (!ok) {
-      atomicMin(bad_index, static_cast<int32_t>(i));
       visible[i] = 0;
     } else {
-      const PreOut o = preprocess_one(params + i, P, ds->cam, rp);
       visible[i] = static_cast<uint8_t>(o.visible);
       if (o.visible) {
         vis = true;
@@ -165,37 +217,35 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ pa
         depth_id[i] = o.depth;
         q = make_int4(o.tx0, o.tx1, o.ty0, o.ty1);
         rect_id[i] = q;
-        if (PJ) compute_posejac(params + i, P, ds->cam, rp.sh_coeffs, pj + 36 * static_cast<size_t>(i));
       }
     }
   }
-  // tile histogram: the warp's (tile, primitive) pairs are flattened over its lanes
   const uint32_t bits = __ballot_sync(0xffffffffu, vis);
   if (lane == 0) s_vis[warp] = static_cast<uint32_t>(__popc(bits));
-  const int tiles_x = rp.tiles_x;
-  const int w = q.y - q.x + 1;
-  const int c = vis ? w * (q.w - q.z + 1) : 0;
-  if (c > kBigPairs) big_ids[atomicAdd(&counters[kCntBig], 1u)] = static_cast<uint32_t>(i);
-  const int excl = warp_excl_scan(c);
-  const int total = __shfl_sync(0xffffffffu, excl + c, 31);
-  for (int base = 0; base < total; base += 32) {
-    const int k = base + lane;
-    const int j = warp_owner(excl, k);
-    const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qy0 = __shfl_sync(0xffffffffu, q.z, j);
-    const int wj = __shfl_sync(0xffffffffu, w, j), ej = __shfl_sync(0xffffffffu, excl, j);
-    if (k < total) {
-      const int r = k - ej;
-      const int row = r / wj;
-      atomicAdd(&tile_cnt[static_cast<int64_t>((qy0 + row) * tiles_x + qx0 + (r - row * wj)) * kBinStride], 1u);
-    }
-  }
+  // visible count (one atomic per CTA) and, for the pose Jacobians, the list of visible ids
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t n = 0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) n += s_vis[w];
-    if (n) atomicAdd(&counters[kCntVisible], n);
+    s_base = n ? atomicAdd(&counters[kCntVisible], n) : 0u;
   }
+  __syncthreads();
+  if (vis_list && vis) {
+    uint32_t off = s_base;
+    for (int w = 0; w < warp; ++w) off += s_vis[w];
+    vis_list[off + __popc(bits & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+  }
+}
+
+// Pose Jacobians of the visible primitives (tracking), one thread per listed id.
+__global__ void __launch_bounds__(256) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
+                                                 const uint32_t* __restrict__ vis_list, const uint32_t* counters,
+                                                 const WorldG* __restrict__ world, float* __restrict__ pj) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= counters[kCntVisible] || ds->halt) return;
+  const uint32_t id = vis_list[r];
+  compute_posejac(params + id, P, ds->cam, K, pj + 36 * static_cast<size_t>(id), world ? world[id].S : nullptr);
 }
 
 __device__ __forceinline__ bool depth_valid(float d, double near_plane, double far_plane) {
@@ -368,18 +418,21 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   const int tiles_x = a.rp.tiles_x, tiles_y = a.rp.tiles_y;
   const int ntiles = tiles_x * tiles_y;
   Profiler* pf = ws.prof;
-  GSF_CUDA_CHECK(cudaMemsetAsync(ws.bins, 0, sizeof(uint32_t) * (ws.tiles_cap * std::max(kBinStride, 2) + kCntNum), st));
+  GSF_CUDA_CHECK(cudaMemsetAsync(ws.bins, 0, sizeof(uint32_t) * (ws.tiles_cap * kBinStride + kCntNum), st));
   if (pf) pf->begin(PROF_PREPROCESS, st);
   if (P > 0) {
-    if (a.want_posejac)
-      k_preprocess<true><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,
-                                                         ws.visible, &ds->bad_index, a.kc, ws.tile_cnt, ws.bin_counters,
-                                                         ws.big_ids, ws.pj_id);
-    else
-      k_preprocess<false><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,
-                                                          ws.visible, &ds->bad_index, a.kc, ws.tile_cnt, ws.bin_counters,
-                                                          ws.big_ids, ws.pj_id);
+#define GSF_PRE(CV)                                                                                                    \
+  k_preprocess<CV><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,   \
+                                                   ws.visible, &ds->bad_index, a.kc, ws.bin_counters,                    \
+                                                   a.want_posejac ? ws.vis_list : nullptr, ws.world, ws.support)
+    if (a.use_world) GSF_PRE(true); else GSF_PRE(false);
+#undef GSF_PRE
     ++*L;
+    if (a.want_posejac) {
+      k_posejac<<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.K, ws.vis_list, ws.bin_counters,
+                                                a.use_world ? ws.world : nullptr, ws.pj_id);
+      ++*L;
+    }
   }
   if (pf) pf->end(st);
   if (pf) pf->begin(PROF_SORT, st);
@@ -402,6 +455,13 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   ++*L;
   if (pf) pf->end(st);
   (void)tiles_y;
+}
+
+void run_world(Workspace& ws, DevState* ds, const float* params, int64_t P, const RasterParams& rp, cudaStream_t st,
+               int64_t* L) {
+  if (P <= 0) return;
+  k_world<<<div_up(P, 256), 256, 0, st>>>(params, P, rp, ws.world, ws.support, &ds->bad_index);
+  ++*L;
 }
 
 void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,
