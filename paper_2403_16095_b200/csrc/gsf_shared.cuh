@@ -623,7 +623,23 @@ GSF_HD float blend_rho_fast(float sigma, const BlendConsts& k) {
 
 // Same decisions as eval_pair_full; the common cases are resolved inline and only band cases
 // take the fp64 path.  `gp` is only dereferenced on that path.
-GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
+// exp(-rho/2) on the hardware exp2 unit (|rel err| < 2^-21): used by the pose backward only
+// where the decision is already certain (the rho_fast path).  Its alpha then differs from the
+// forward's in the last bits, which only perturbs the recovered T at the 1e-7 level; every
+// forward stays on the exact polynomial (bit-identical to the mirror, and a track_frame at the
+// optimum sees exactly zero residuals, test_tracker.cpp:192-244).
+GSF_HD float exp_neg_half_fast(float rho) {
+#ifdef __CUDA_ARCH__
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(rho * -0.72134752044448170f));
+  return y;
+#else
+  return exp_f_inrange(fmul(-0.5f, rho));
+#endif
+}
+
+template <bool FAST>
+GSF_HD PairEval eval_pair_t(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
   PairEval e;
   e.dx = fsub(px, g.mx);
   e.dy = fsub(py, g.my);
@@ -634,12 +650,16 @@ GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp,
   e.gval = 0.0f;
   if (rho > k.rho_hi) return e;
   if (rho < g.pad0 && rho >= k.rho_min) {
-    e.gval = exp_f_inrange(fmul(-0.5f, rho));
+    e.gval = FAST ? exp_neg_half_fast(rho) : exp_f_inrange(fmul(-0.5f, rho));
     e.alpha = fmul(g.sigma, e.gval);
     e.code = 1;
     return e;
   }
   return eval_pair_full(px, py, g, gp, k);
+}
+
+GSF_HD PairEval eval_pair(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
+  return eval_pair_t<false>(px, py, g, gp, k);
 }
 
 struct PixelState {

@@ -336,7 +336,7 @@ __device__ __forceinline__ PixBwd load_pixel_bwd(const BwdPtrs& bp, int64_t pi, 
 constexpr int kPoseBatch = 128;
 
 template <int SEED, bool VIEWDEP>
-__global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc,
+__global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc,
                                                        double near_plane, double far_plane, LossParams lp,
                                                        DevState* ds, uint32_t* ticket) {
   __shared__ BlendG s_g[kPoseBatch];
@@ -397,10 +397,10 @@ __global__ void __launch_bounds__(256) k_backward_pose(BwdPtrs bp, int W, int H,
       const int li = bstart + k - rg.x;
       if (li >= pb.last) continue;
       const BlendG g = s_g[k];
-      const PairEval e = eval_pair(px, py, g, bp.gg + s_id[k], kc);
+      const PairEval e = eval_pair_t<true>(px, py, g, bp.gg + s_id[k], kc);
       if (!e.code) continue;
       const float alpha = e.alpha;
-      const float inv = __frcp_rn(1.0f - alpha);
+      const float inv = __fdividef(1.0f, 1.0f - alpha);
       const float Tpre = T * inv;
       const float derr = g.depth - pb.D;
       const float q = pb.gc0 * g.r + pb.gc1 * g.g + pb.gc2 * g.b + pb.gad * g.depth + pb.gop + pb.gu * derr * derr;
