@@ -61,6 +61,12 @@ __device__ __forceinline__ int rs_field(int nf, int lane, bool& valid) {
   return base;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float sgnf(float v) { return v > 0.0f ? 1.0f : (v < 0.0f ? -1.0f : 0.0f); }
 
 __device__ __forceinline__ bool dvalid(float d, double near_plane, double far_plane) {
@@ -400,15 +406,20 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
       const PairEval e = eval_pair_t<true>(px, py, g, bp.gg + s_id[k], kc);
       if (!e.code) continue;
       const float alpha = e.alpha;
-      const float inv = __fdividef(1.0f, 1.0f - alpha);
+      const float inv = rcp_approx(1.0f - alpha);
       const float Tpre = T * inv;
-      const float derr = g.depth - pb.D;
-      const float q = pb.gc0 * g.r + pb.gc1 * g.g + pb.gc2 * g.b + pb.gad * g.depth + pb.gop + pb.gu * derr * derr;
+      // the tracking loss seeds colour and alpha depth only (losses.cpp:284-339): no opacity,
+      // median-depth or uncertainty seeds on that path
+      constexpr bool kTrack = SEED == SEED_TRACK;
+      const float derr = kTrack ? 0.0f : g.depth - pb.D;
+      float q = pb.gc0 * g.r + pb.gc1 * g.g + pb.gc2 * g.b + pb.gad * g.depth;
+      if (!kTrack) q += pb.gop + pb.gu * derr * derr;
       const float dal = Tpre * q - S * inv;
       const float w = alpha * Tpre;
       S += w * q;
       T = Tpre;
-      const float s5 = w * (pb.gad + 2.0f * pb.gu * derr) + (s_id[k] == pb.med ? pb.gmd : 0.0f);
+      const float s5 = kTrack ? w * pb.gad
+                              : w * (pb.gad + 2.0f * pb.gu * derr) + (s_id[k] == pb.med ? pb.gmd : 0.0f);
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
       if (!e.clamped) {
         const float dg = dal * g.sigma;
