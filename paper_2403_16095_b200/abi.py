@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgsf_cuda.so")
+# GSF_LIB: an alternative in-tree build of the same library (kernel-variant A/B measurements)
+LIB_PATH = os.environ.get("GSF_LIB") or os.path.join(HERE, "libgsf_cuda.so")
 
 GSF_OK, GSF_EINVAL, GSF_ENONFINITE, GSF_EDIVERGED, GSF_ECUDA, GSF_EUNSUPPORTED, GSF_ENOMEM = range(7)
 

@@ -96,18 +96,16 @@ struct BwdPtrs {
   const float* up_uncert;
   const float* dssim;
   float* partials;
-  const float* pj;       // per-primitive pose Jacobians (fused tracking mode), id-indexed, 36 floats
+  const float* pj;          // pose Jacobians (fused tracking mode), 36 floats at the primitive's slot
+  const uint32_t* pj_slot;  // id -> slot in pj (position in the visible list)
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
 };
 
 constexpr int kBwdBatch = 64;
 
-template <int SEED, int NF, bool POSEJ>
+template <int SEED, int NF>
 __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc, double near_plane,
                                                   double far_plane, LossParams lp, const DevState* ds) {
-  __shared__ float s_sum[POSEJ ? kBwdBatch : 1][NF];
-  __shared__ double s_pred[8][6];
-  double pacc[6] = {0, 0, 0, 0, 0, 0};
   __shared__ BlendG s_g[kBwdBatch];
   __shared__ int32_t s_id[kBwdBatch];
   __shared__ uint8_t s_mask[kBwdBatch];
@@ -115,10 +113,7 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
   __shared__ int s_wmax[8];
   const int tile = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (ds->halt) {
-    if (POSEJ && tid < 6) bp.tile_pose[static_cast<size_t>(tile) * 6 + tid] = 0.0;
-    return;
-  }
+  if (ds->halt) return;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x = tx * kTile + tile_lx(tid), y = ty * kTile + tile_ly(tid);
   const bool inside = x < W && y < H;
@@ -230,59 +225,9 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
       float sum = 0.0f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) sum += s_part[w][k][fi];
-      if (POSEJ)
-        s_sum[k][fi] = sum;
-      else
-        bp.partials[static_cast<size_t>(bstart + k) * NF + fi] = sum;
+      bp.partials[static_cast<size_t>(bstart + k) * NF + fi] = sum;
     }
     __syncthreads();
-    if (POSEJ && tid < cnt) {
-      // pose contribution of this (tile, primitive) pair through its Jacobian (rasterizer.cpp:495-526)
-      const float4* q4 = reinterpret_cast<const float4*>(bp.pj + 36 * static_cast<size_t>(s_id[tid]));
-      float pjv[36];
-#pragma unroll
-      for (int i = 0; i < 9; ++i) {
-        const float4 t4 = q4[i];
-        pjv[4 * i] = t4.x; pjv[4 * i + 1] = t4.y; pjv[4 * i + 2] = t4.z; pjv[4 * i + 3] = t4.w;
-      }
-      const float sv0 = s_sum[tid][0], sv1 = s_sum[tid][1], sv2 = s_sum[tid][2], sv3 = s_sum[tid][3],
-                  sv4 = s_sum[tid][4], sv5 = s_sum[tid][5];
-      float d[3];
-      d[0] = pjv[0] * sv0 + pjv[4] * sv2 + pjv[5] * sv3 + pjv[6] * sv4;
-      d[1] = pjv[2] * sv1 + pjv[7] * sv2 + pjv[8] * sv3 + pjv[9] * sv4;
-      d[2] = pjv[1] * sv0 + pjv[3] * sv1 + pjv[10] * sv2 + pjv[11] * sv3 + pjv[12] * sv4 + sv5;
-      const float* pc = pjv + 22;
-      const float rot0 = pc[1] * d[2] - pc[2] * d[1] + pjv[13] * sv2 + pjv[14] * sv3 + pjv[15] * sv4;
-      const float rot1 = pc[2] * d[0] - pc[0] * d[2] + pjv[16] * sv2 + pjv[17] * sv3 + pjv[18] * sv4;
-      const float rot2 = pc[0] * d[1] - pc[1] * d[0] + pjv[19] * sv2 + pjv[20] * sv3 + pjv[21] * sv4;
-      float tr0 = d[0], tr1 = d[1], tr2 = d[2];
-      if (NF >= 9) {
-        const float c0 = s_sum[tid][NF >= 9 ? 6 : 0], c1 = s_sum[tid][NF >= 9 ? 7 : 0], c2 = s_sum[tid][NF >= 9 ? 8 : 0];
-        tr0 += pjv[25] * c0 + pjv[26] * c1 + pjv[27] * c2;
-        tr1 += pjv[28] * c0 + pjv[29] * c1 + pjv[30] * c2;
-        tr2 += pjv[31] * c0 + pjv[32] * c1 + pjv[33] * c2;
-      }
-      pacc[0] += rot0; pacc[1] += rot1; pacc[2] += rot2;
-      pacc[3] += tr0; pacc[4] += tr1; pacc[5] += tr2;
-    }
-  }
-  if (POSEJ) {
-    // fixed-order block reduction of the per-thread pose sums -> one partial per tile
-#pragma unroll
-    for (int a = 0; a < 6; ++a) {
-      double v = pacc[a];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-      if (lane == 0) s_pred[warp][a] = v;
-    }
-    __syncthreads();
-    if (tid < 6) {
-      double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) t += s_pred[w][tid];
-      bp.tile_pose[static_cast<size_t>(tile) * 6 + tid] = t;
-    }
-    return;
   }
   for (int j = end + tid; j < rg.y; j += 256) {
 #pragma unroll
@@ -388,7 +333,7 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
     __syncthreads();
     for (int i = tid; i < cnt * 9; i += 256) {
       const int k = i / 9, j = i - 9 * k;
-      s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[9 * static_cast<size_t>(s_id[k]) + j];
+      s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[9 * static_cast<size_t>(bp.pj_slot[s_id[k]]) + j];
     }
     __syncthreads();
     float pf0 = 0.f, pf1 = 0.f, pf2 = 0.f, pf3 = 0.f, pf4 = 0.f, pf5 = 0.f;
@@ -806,6 +751,7 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.dssim = (a.seed_mode == SEED_MAP && a.lp.w_ssim > 0.0) ? ws.dssim : nullptr;
   bp.partials = ws.partials;
   bp.pj = nullptr;
+  bp.pj_slot = nullptr;
   bp.tile_pose = nullptr;
   const bool view_dep = a.K > 1;
   const int nf = a.pose_only ? (view_dep ? 9 : 6) : 10;
@@ -813,6 +759,7 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     // tracking: per-tile pose partials through the per-primitive Jacobians; the last CTA reduces
     // them, so neither a chain nor a pose-sum launch follows
     bp.pj = ws.pj_id;
+    bp.pj_slot = ws.pj_slot;
     bp.tile_pose = ws.pose_part;
     uint32_t* ticket = ws.bin_counters + kCntBwdTicket;
     if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
@@ -829,7 +776,7 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     return;
   }
   if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
-#define GSF_BWD(SM, NFV) k_backward<SM, NFV, false><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds)
+#define GSF_BWD(SM, NFV) k_backward<SM, NFV><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds)
   if (a.seed_mode == SEED_TRACK) {
     if (nf == 6) GSF_BWD(SEED_TRACK, 6); else if (nf == 9) GSF_BWD(SEED_TRACK, 9); else GSF_BWD(SEED_TRACK, 10);
   } else if (a.seed_mode == SEED_MAP) {

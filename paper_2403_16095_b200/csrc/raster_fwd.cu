@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
                                                     double* __restrict__ depth_id, int4* __restrict__ rect_id,
                                                     uint8_t* __restrict__ visible, int32_t* bad_index, BlendConsts kc,
                                                     uint32_t* counters, uint32_t* __restrict__ vis_list,
+                                                    uint32_t* __restrict__ pj_slot,
                                                     const WorldG* __restrict__ world, const double* __restrict__ support) {
   __shared__ uint32_t s_vis[8];
   __shared__ uint32_t s_base;
@@ -234,18 +235,34 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
   if (vis_list && vis) {
     uint32_t off = s_base;
     for (int w = 0; w < warp; ++w) off += s_vis[w];
-    vis_list[off + __popc(bits & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+    const uint32_t r = off + __popc(bits & ((1u << lane) - 1u));
+    vis_list[r] = static_cast<uint32_t>(i);
+    pj_slot[i] = r;
   }
 }
 
-// Pose Jacobians of the visible primitives (tracking), one thread per listed id.
+// Pose Jacobians of the visible primitives (tracking), one thread per listed id; slot r of the
+// list owns pj[36 r, 36 r + 36), staged through shared memory so the CTA writes one contiguous,
+// coalesced block.
 __global__ void __launch_bounds__(256) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
                                                  const uint32_t* __restrict__ vis_list, const uint32_t* counters,
                                                  const WorldG* __restrict__ world, float* __restrict__ pj) {
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= counters[kCntVisible] || ds->halt) return;
-  const uint32_t id = vis_list[r];
-  compute_posejac(params + id, P, ds->cam, K, pj + 36 * static_cast<size_t>(id), world ? world[id].S : nullptr);
+  __shared__ float s_out[256 * 37];
+  const uint32_t n = counters[kCntVisible];
+  const uint32_t r0 = blockIdx.x * blockDim.x;
+  if (r0 >= n || ds->halt) return;
+  const uint32_t r = r0 + threadIdx.x;
+  if (r < n) {
+    const uint32_t id = vis_list[r];
+    float v[36];
+    compute_posejac(params + id, P, ds->cam, K, v, world ? world[id].S : nullptr);
+#pragma unroll
+    for (int q = 0; q < 36; ++q) s_out[threadIdx.x * 37 + q] = v[q];
+  }
+  __syncthreads();
+  const uint32_t cnt = min(256u, n - r0);
+  float* dst = pj + 36 * static_cast<size_t>(r0);
+  for (uint32_t e = threadIdx.x; e < 36 * cnt; e += 256) dst[e] = s_out[(e / 36) * 37 + e % 36];
 }
 
 __device__ __forceinline__ bool depth_valid(float d, double near_plane, double far_plane) {
@@ -260,7 +277,10 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 template <int LMODE>
-__global__ void __launch_bounds__(256, LMODE == 1 ? 5 : 4) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sid,
+#ifndef GSF_BLEND_MINB
+#define GSF_BLEND_MINB 5
+#endif
+__global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sid,
                                                const BlendG* __restrict__ bg, const GuardG* __restrict__ gg,
                                                const float* __restrict__ obs, const float* __restrict__ loss_rgb,
                                                const float* __restrict__ loss_depth, int W, int H, int tiles_x,
@@ -424,7 +444,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
 #define GSF_PRE(CV)                                                                                                    \
   k_preprocess<CV><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,   \
                                                    ws.visible, &ds->bad_index, a.kc, ws.bin_counters,                    \
-                                                   a.want_posejac ? ws.vis_list : nullptr, ws.world, ws.support)
+                                                   a.want_posejac ? ws.vis_list : nullptr, ws.pj_slot, ws.world, ws.support)
     if (a.use_world) GSF_PRE(true); else GSF_PRE(false);
 #undef GSF_PRE
     ++*L;
