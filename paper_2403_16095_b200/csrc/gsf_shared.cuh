@@ -115,24 +115,26 @@ GSF_HD double exp_d(double x) {
   return dmul(p, bitsd(static_cast<int64_t>(1023 + ni) << 52));
 }
 
-// Deterministic exp (fp32) for the blend: reduction by ln2, degree-6 polynomial.
-// Inputs are -rho/2 in [-0.5*cutoff, 0]; values below -87 flush to zero.
-GSF_HD float exp_f(float x) {
-  if (x < -87.0f) return 0.0f;
-  if (x > 88.0f) return finf();
-  const float n = frint(fmul(x, 1.44269504f));
-  float r = ffma(n, -0.693145752f, x);
-  r = ffma(n, -1.42860677e-06f, r);
-  float p = 1.0f / 5040.0f;
-  p = ffma(p, r, 1.0f / 720.0f);
-  p = ffma(p, r, 1.0f / 120.0f);
-  p = ffma(p, r, 1.0f / 24.0f);
-  p = ffma(p, r, 1.0f / 6.0f);
-  p = ffma(p, r, 0.5f);
-  p = ffma(p, r, 1.0f);
-  p = ffma(p, r, 1.0f);
-  const int ni = static_cast<int>(n);
-  return fmul(p, bitsf((127 + ni) << 23));
+// Deterministic exp(-rho/2) (fp32) for the blend, rho >= -tiny: 2^y with y = rho * (-log2(e)/2)
+// split as y = n + f, |f| <= 1/2, and 2^f by its degree-6 Taylor polynomial in Horner form.
+// |relative error| < 3e-7 (truncation 1.2e-7 + roundings), far inside the 5e-4 alpha guard band;
+// 12 instructions.  The in-range form skips the underflow test (fast path: rho < cutoff < 170).
+GSF_HD float exp_neg_half_inrange(float rho) {
+  const float y = fmul(rho, -0.72134752044448170368f);
+  const float n = frint(y);
+  const float f = fsub(y, n);
+  float p = 1.5403530393381606e-4f;
+  p = ffma(p, f, 1.3333558146428443e-3f);
+  p = ffma(p, f, 9.6181291076284772e-3f);
+  p = ffma(p, f, 5.5504108664821580e-2f);
+  p = ffma(p, f, 2.4022650695910071e-1f);
+  p = ffma(p, f, 6.9314718055994531e-1f);
+  p = ffma(p, f, 1.0f);
+  return fmul(p, bitsf((127 + static_cast<int>(n)) << 23));
+}
+GSF_HD float exp_neg_half(float rho) {
+  if (fmul(rho, -0.72134752044448170368f) < -126.0f) return 0.0f;   // 2^n must stay normal
+  return exp_neg_half_inrange(rho);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -507,7 +509,7 @@ struct BlendConsts {
   // precomputed decision thresholds (same explicit ops as the full path below)
   float rho_hi, rho_lo, rho_min;      // cutoff + band, cutoff - band, band
   float skip_lo, skip_hi, clamp_lo, clamp_hi;
-  int32_t fast_ok;                    // exp_f needs no range checks on the fast path
+  int32_t fast_ok;                    // exp_neg_half needs no range check on the fast path
 };
 
 GSF_HD BlendConsts make_blend_consts(const RasterParams& rp) {
@@ -570,7 +572,7 @@ GSF_HD PairEval eval_pair_full(float px, float py, const BlendG& g, const GuardG
     have_d = true;
     if (rho_d > k.cutoff_d || rho_d < 0.0) return e;
   }
-  e.gval = exp_f(fmul(-0.5f, rho));
+  e.gval = exp_neg_half(rho);
   const float raw = fmul(g.sigma, e.gval);
   if (raw < k.skip_lo) return e;                      // raw < alpha_skip -> skip
   if (raw <= k.skip_hi) {
@@ -590,27 +592,9 @@ GSF_HD PairEval eval_pair_full(float px, float py, const BlendG& g, const GuardG
   return e;
 }
 
-// exp_f without the range guards: only called on the fast path, where -rho/2 lies in
-// (-cutoff/2, 0] and cutoff < 170, so the guards of exp_f can never trigger.  Same bits.
-GSF_HD float exp_f_inrange(float x) {
-  const float n = frint(fmul(x, 1.44269504f));
-  float r = ffma(n, -0.693145752f, x);
-  r = ffma(n, -1.42860677e-06f, r);
-  float p = 1.0f / 5040.0f;
-  p = ffma(p, r, 1.0f / 720.0f);
-  p = ffma(p, r, 1.0f / 120.0f);
-  p = ffma(p, r, 1.0f / 24.0f);
-  p = ffma(p, r, 1.0f / 6.0f);
-  p = ffma(p, r, 0.5f);
-  p = ffma(p, r, 1.0f);
-  p = ffma(p, r, 1.0f);
-  const int ni = static_cast<int>(n);
-  return fmul(p, bitsf((127 + ni) << 23));
-}
-
 // Per-primitive fast-path bound (stored in BlendG::pad0): for rho in [rho_min, rho_fast) the full
-// decision is certainly "contributes, unclamped, alpha = sigma*exp_f(-rho/2)" — rho is below the
-// guard band, alpha is above the skip band (margin 1e-5 in log space, >> exp_f's 1-ulp error)
+// decision is certainly "contributes, unclamped, alpha = sigma*exp(-rho/2)" — rho is below the
+// guard band, alpha is above the skip band (margin 1e-5 in log space, >> the exp error of 3e-7)
 // and sigma is below the clamp band.  -1 disables the fast path.  Only selects the evaluation
 // path, never a result, so the mirror and the kernels stay bit-identical either way.
 GSF_HD float blend_rho_fast(float sigma, const BlendConsts& k) {
@@ -621,8 +605,6 @@ GSF_HD float blend_rho_fast(float sigma, const BlendConsts& k) {
   return r > 0.0 ? static_cast<float>(r * (1.0 - 1e-6)) : -1.0f;
 }
 
-// Same decisions as eval_pair_full; the common cases are resolved inline and only band cases
-// take the fp64 path.  `gp` is only dereferenced on that path.
 // exp(-rho/2) on the hardware exp2 unit (|rel err| < 2^-21): used by the pose backward only
 // where the decision is already certain (the rho_fast path).  Its alpha then differs from the
 // forward's in the last bits, which only perturbs the recovered T at the 1e-7 level; every
@@ -634,10 +616,12 @@ GSF_HD float exp_neg_half_fast(float rho) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(rho * -0.72134752044448170f));
   return y;
 #else
-  return exp_f_inrange(fmul(-0.5f, rho));
+  return exp_neg_half_inrange(rho);
 #endif
 }
 
+// Same decisions as eval_pair_full; the common cases are resolved inline and only band cases
+// take the fp64 path.  `gp` is only dereferenced on that path.
 template <bool FAST>
 GSF_HD PairEval eval_pair_t(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
   PairEval e;
@@ -650,7 +634,7 @@ GSF_HD PairEval eval_pair_t(float px, float py, const BlendG& g, const GuardG* g
   e.gval = 0.0f;
   if (rho > k.rho_hi) return e;
   if (rho < g.pad0 && rho >= k.rho_min) {
-    e.gval = FAST ? exp_neg_half_fast(rho) : exp_f_inrange(fmul(-0.5f, rho));
+    e.gval = FAST ? exp_neg_half_fast(rho) : exp_neg_half_inrange(rho);
     e.alpha = fmul(g.sigma, e.gval);
     e.code = 1;
     return e;
