@@ -264,6 +264,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     dalloc(ws.pj_id, static_cast<size_t>(P) * 36);
     dalloc(ws.big_ids, P);
     dalloc(ws.vis_list, P);
+    dalloc(ws.pair_base, P);
     dalloc(ws.pj_slot, P);
     dalloc(ws.world, P);
     dalloc(ws.support, P);
@@ -606,7 +607,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   Workspace& ws = c->ws;
   void* bufs[] = {ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
-                  ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
+                  ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
                   ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.pj_id,
                   ws.red_part, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_scatter(const uint8_t* __restrict__ vis
                                                  const double* __restrict__ depth_id, int64_t P, int tiles_x,
                                                  uint32_t* __restrict__ fill, uint32_t bucket_cap,
                                                  unsigned long long* __restrict__ bucket, uint32_t* counters,
-                                                 uint32_t* __restrict__ big_ids) {
+                                                 uint32_t* __restrict__ big_ids, uint32_t* __restrict__ pair_base) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool vis = i < P && visible[i];
@@ -106,6 +106,28 @@ __global__ void __launch_bounds__(256) k_scatter(const uint8_t* __restrict__ vis
   }
   const int w = q.y - q.x + 1;
   int c = vis ? w * (q.w - q.z + 1) : 0;
+  {
+    // primitive-major pair slots (pair_base[id] + rectangle index) for the mapping backward and
+    // its chain: a CTA scan of the pair counts plus one atomic per CTA (any order is fine: the
+    // chain reads each primitive's own slots in rectangle order)
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_cta;
+    const int warp = threadIdx.x >> 5;
+    const int ex = warp_excl_scan(c);
+    if (lane == 31) s_w[warp] = static_cast<uint32_t>(ex + c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int k = 0; k < 8; ++k) t += s_w[k];
+      s_cta = t ? atomicAdd(&counters[kCntPairAlloc], t) : 0u;
+    }
+    __syncthreads();
+    if (vis) {
+      uint32_t b = s_cta + static_cast<uint32_t>(ex);
+      for (int k = 0; k < warp; ++k) b += s_w[k];
+      pair_base[i] = b;
+    }
+  }
   if (c > kBigPairs) {   // k_scatter_big's
     big_ids[atomicAdd(&counters[kCntBig], 1u)] = static_cast<uint32_t>(i);
     c = 0;
@@ -306,7 +328,7 @@ void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles
   const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
   if (P > 0) {
     k_scatter<<<div_up(P, 256), 256, 0, st>>>(ws.visible, ws.rect_id, ws.depth_id, P, tiles_x, ws.tile_fill, bcap, ws.bucket,
-                                              ws.bin_counters, ws.big_ids);
+                                              ws.bin_counters, ws.big_ids, ws.pair_base);
     ++*L;
     k_scatter_big<<<128, 1024, 0, st>>>(ws.big_ids, ws.bin_counters, ws.rect_id, ws.depth_id, tiles_x, ws.tile_fill, bcap,
                                         ws.bucket);

@@ -15,7 +15,7 @@ constexpr int kTile = 16;
 // slots of Workspace::bin_counters.
 constexpr int kBinStride = 8;
 constexpr int kBigPairs = 128;
-enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
+enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntPairAlloc = 4, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
 constexpr int kTilePixels = kTile * kTile;
 constexpr int kFieldsBase = 11;       // mean 3, log_scale 3, quat 4, opacity 1; then 3*K SH
 

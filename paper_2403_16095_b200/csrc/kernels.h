@@ -71,7 +71,8 @@ struct Workspace {
   uint32_t* tile_fill = nullptr;
   uint32_t* bin_counters = nullptr;   // BinCounter slots
   uint32_t* big_ids = nullptr;        // P: primitives with more than kBigPairs tiles
-  uint32_t* vis_list = nullptr;       // P: visible ids (any order), for the pose Jacobians
+  uint32_t* vis_list = nullptr;       // P: visible ids (any order): pose Jacobians, chain
+  uint32_t* pair_base = nullptr;      // P: first primitive-major pair slot of a visible primitive
   uint32_t* tile_start = nullptr;
   int2* ranges = nullptr;
   double* loss_part = nullptr;  // tiles * LS_NUM
@@ -80,7 +81,7 @@ struct Workspace {
   int64_t bucket_cap = 0;
   unsigned long long* skey = nullptr;   // the same keys, each tile's list in (depth, id) order
   uint32_t* sid = nullptr;
-  float* partials = nullptr;   // pair_cap * 10, at sorted list positions (generic backward)
+  float* partials = nullptr;   // pair_cap * 10, primitive-major: pair_base[id] + rectangle index
   // per pixel (render outputs + backward inputs)
   float* color = nullptr;      // 3*npix, interleaved
   float* alpha_depth = nullptr;

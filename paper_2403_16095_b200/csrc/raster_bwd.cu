@@ -96,6 +96,8 @@ struct BwdPtrs {
   const float* up_uncert;
   const float* dssim;
   float* partials;
+  const int4* rect;         // id-indexed tile rectangles
+  const uint32_t* pair_base;  // id -> first primitive-major partial slot
   const float* pj;          // pose Jacobians (fused tracking mode), 36 floats at the primitive's slot
   const uint32_t* pj_slot;  // id -> slot in pj (position in the visible list)
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
                                                   double far_plane, LossParams lp, const DevState* ds) {
   __shared__ BlendG s_g[kBwdBatch];
   __shared__ int32_t s_id[kBwdBatch];
+  __shared__ uint32_t s_slot[kBwdBatch];
   __shared__ uint8_t s_mask[kBwdBatch];
   __shared__ float s_part[8][kBwdBatch][NF];
   __shared__ int s_wmax[8];
@@ -168,6 +171,8 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
       const BlendG gj = bp.bg[id];
       s_g[tid] = gj;
       s_id[tid] = id;
+      const int4 q = bp.rect[id];
+      s_slot[tid] = bp.pair_base[id] + static_cast<uint32_t>((ty - q.z) * (q.y - q.x + 1) + (tx - q.x));
       s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, static_cast<float>(tx * kTile), static_cast<float>(ty * kTile), kc));
     }
     __syncthreads();
@@ -183,11 +188,11 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
       bool contrib = false;
       if (li < last) {
         const BlendG g = s_g[k];
-        const PairEval e = eval_pair(px, py, g, bp.gg + s_id[k], kc);
+        const PairEval e = eval_pair_t<true>(px, py, g, bp.gg + s_id[k], kc);
         if (e.code) {
           contrib = true;
           const float alpha = e.alpha;
-          const float inv = __frcp_rn(1.0f - alpha);
+          const float inv = rcp_approx(1.0f - alpha);
           const float Tpre = T * inv;
           const float derr = g.depth - D;
           const float q = gc0 * g.r + gc1 * g.g + gc2 * g.b + gad * g.depth + gop + gu * derr * derr;
@@ -225,13 +230,16 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
       float sum = 0.0f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) sum += s_part[w][k][fi];
-      bp.partials[static_cast<size_t>(bstart + k) * NF + fi] = sum;
+      bp.partials[static_cast<size_t>(s_slot[k]) * NF + fi] = sum;
     }
     __syncthreads();
   }
-  for (int j = end + tid; j < rg.y; j += 256) {
+  for (int j = end + tid; j < rg.y; j += 256) {   // entries behind every pixel's last contributor
+    const int id = static_cast<int>(bp.sid[j]);
+    const int4 q = bp.rect[id];
+    const size_t slot = bp.pair_base[id] + static_cast<uint32_t>((ty - q.z) * (q.y - q.x + 1) + (tx - q.x));
 #pragma unroll
-    for (int fi = 0; fi < NF; ++fi) bp.partials[static_cast<size_t>(j) * NF + fi] = 0.0f;
+    for (int fi = 0; fi < NF; ++fi) bp.partials[slot * NF + fi] = 0.0f;
   }
 }
 
@@ -462,51 +470,70 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Position of primitive `id` in tile list [lo, hi) (keys (fp32 depth bits << 32 | id), runs of
-// equal fp32 depth in fp64 order): lower bound of its fp32 depth, then a walk along that run.
-// Returns -1 if absent (pair dropped by a pair-capacity overflow).
-__device__ __forceinline__ int find_in_list(const unsigned long long* __restrict__ skey, int lo, int hi, uint32_t dbits,
-                                            uint32_t id) {
-  const unsigned long long k0 = static_cast<unsigned long long>(dbits) << 32;
-  int a = lo, b = hi;
-  while (a < b) {
-    const int m = (a + b) >> 1;
-    if (skey[m] < k0)
-      a = m + 1;
-    else
-      b = m;
+// eval_sh_color_backward (sh.cpp:88-108) along the view direction for sh_coeffs > 1, fp64:
+// writes d sh into grads (if non-null) and returns d mean through the view direction.
+static __device__ __noinline__ void sh_backward(const float* __restrict__ params, int64_t P, int64_t id, int K,
+                                                const Cam& cam, double m0, double m1, double m2, const double* dcol,
+                                                float* __restrict__ grads, double* through) {
+  const double d0 = m0 - cam.center[0], d1 = m1 - cam.center[1], d2 = m2 - cam.center[2];
+  const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+  double dir[3] = {0.0, 0.0, 1.0};
+  if (len > 1e-12) { dir[0] = d0 / len; dir[1] = d1 / len; dir[2] = d2 / len; }
+  const int deg = sh_degree(K);
+  double b[16];
+  sh_basis(deg, dir[0], dir[1], dir[2], b);
+  double masked[3];
+  for (int c = 0; c < 3; ++c) {
+    double raw = 0.5;
+    for (int k = 0; k < K; ++k) raw += b[k] * params[(11 + 3 * k + c) * P + id];
+    masked[c] = raw < 0.0 ? 0.0 : dcol[c];
   }
-  for (; a < hi && static_cast<uint32_t>(skey[a] >> 32) == dbits; ++a)
-    if (static_cast<uint32_t>(skey[a]) == id) return a;
-  return -1;
+  if (grads)
+    for (int k = 0; k < K; ++k)
+      for (int c = 0; c < 3; ++c) grads[(11 + 3 * k + c) * P + id] = static_cast<float>(b[k] * masked[c]);
+  through[0] = through[1] = through[2] = 0.0;
+  if (deg >= 1 && len > 1e-12) {
+    double gb[48];
+    sh_basis_grad(deg, dir[0], dir[1], dir[2], gb);
+    double dd[3] = {0.0, 0.0, 0.0};
+    for (int k = 1; k < K; ++k) {
+      const double md = masked[0] * params[(11 + 3 * k + 0) * P + id] + masked[1] * params[(11 + 3 * k + 1) * P + id] +
+                        masked[2] * params[(11 + 3 * k + 2) * P + id];
+      for (int a = 0; a < 3; ++a) dd[a] += gb[3 * k + a] * md;
+    }
+    const double dot = dir[0] * dd[0] + dir[1] * dd[1] + dir[2] * dd[2];
+    for (int a = 0; a < 3; ++a) through[a] = (dd[a] - dir[a] * dot) / len;
+  }
 }
 
 template <int NF, bool FULL>
-__global__ void __launch_bounds__(256) k_chain(const uint8_t* __restrict__ visible, const int4* __restrict__ rect_id,
-                                               const double* __restrict__ depth_id, const int2* __restrict__ ranges,
-                                               const unsigned long long* __restrict__ skey, int tiles_x, const float* __restrict__ partials, const DevState* ds,
+#ifndef GSF_CHAIN_MINB
+#define GSF_CHAIN_MINB 2
+#endif
+__global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* __restrict__ vis_list, const uint32_t* counters,
+                                               const int4* __restrict__ rect_id, const uint32_t* __restrict__ pair_base,
+                                               const float* __restrict__ partials, const DevState* ds,
                                                const float* __restrict__ params, int64_t P, int K,
                                                float* __restrict__ grads, float* __restrict__ d_mean2d,
                                                double* __restrict__ pose_part) {
   __shared__ double s_red[8][6];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
+  const uint32_t r = blockIdx.x * blockDim.x + tid;
   double pose[6] = {0, 0, 0, 0, 0, 0};
-  if (id < P && visible[id] && !ds->halt) {
-    // fixed-order gather of the primitive's pair partials, tiles in row-major rectangle order
+  if (r < counters[kCntVisible] && !ds->halt) {
+    const int64_t id = vis_list[r];
+    // fixed-order gather of the primitive's pair partials: its slots hold the tiles of its
+    // rectangle in row-major order (the reference's tile-order reduction, rasterizer.cpp:466-478)
     const int4 q = rect_id[id];
-    const uint32_t dbits = static_cast<uint32_t>(__float_as_int(static_cast<float>(depth_id[id])));
+    const int c = (q.y - q.x + 1) * (q.w - q.z + 1);
+    const float* pp = partials + static_cast<size_t>(pair_base[id]) * NF;
     double sg[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) sg[f] = 0.0;
-    for (int ty = q.z; ty <= q.w; ++ty)
-      for (int tx = q.x; tx <= q.y; ++tx) {
-        const int2 rg = ranges[ty * tiles_x + tx];
-        const int pos = find_in_list(skey, rg.x, rg.y, dbits, static_cast<uint32_t>(id));
-        if (pos < 0) continue;
+    for (int k = 0; k < c; ++k) {
 #pragma unroll
-        for (int f = 0; f < NF; ++f) sg[f] += static_cast<double>(partials[static_cast<size_t>(pos) * NF + f]);
-      }
+      for (int f = 0; f < NF; ++f) sg[f] += static_cast<double>(pp[k * NF + f]);
+    }
     bool zero = true;
 #pragma unroll
     for (int f = 0; f < NF; ++f) zero = zero && sg[f] == 0.0;
@@ -584,38 +611,15 @@ __global__ void __launch_bounds__(256) k_chain(const uint8_t* __restrict__ visib
       double through[3] = {0.0, 0.0, 0.0};
       double dcol[3] = {0.0, 0.0, 0.0};
       if (NF >= 9) { dcol[0] = sg[6]; dcol[1] = sg[7]; dcol[2] = sg[8]; }
-      double dsh[48];
-      const bool need_sh = K > 0 && (FULL || K > 1);
-      if (need_sh) {
-        // eval_sh_color_backward (sh.cpp:88-108) along the view direction
-        const double d0 = m0 - cam.center[0], d1 = m1 - cam.center[1], d2 = m2 - cam.center[2];
-        const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-        double dir[3] = {0.0, 0.0, 1.0};
-        if (len > 1e-12) { dir[0] = d0 / len; dir[1] = d1 / len; dir[2] = d2 / len; }
-        const int deg = sh_degree(K);
-        double b[16];
-        sh_basis(deg, dir[0], dir[1], dir[2], b);
-        double masked[3];
+      if (K == 1 && FULL) {
+        // degree 0: colour_c = max(0.5 + C0 sh_c, 0), no view-direction gradient (sh.cpp:88-108)
         for (int c = 0; c < 3; ++c) {
-          double raw = 0.5;
-          for (int k = 0; k < K; ++k) raw += b[k] * params[(11 + 3 * k + c) * P + id];
-          masked[c] = raw < 0.0 ? 0.0 : dcol[c];
+          const double raw = 0.5 + 0.28209479177387814 * params[(11 + c) * P + id];
+          grads[(11 + c) * P + id] = static_cast<float>(raw < 0.0 ? 0.0 : 0.28209479177387814 * dcol[c]);
         }
-        for (int k = 0; k < K; ++k)
-          for (int c = 0; c < 3; ++c) dsh[3 * k + c] = b[k] * masked[c];
-        if (deg >= 1 && len > 1e-12) {
-          double gb[48];
-          sh_basis_grad(deg, dir[0], dir[1], dir[2], gb);
-          double dd[3] = {0.0, 0.0, 0.0};
-          for (int k = 1; k < K; ++k) {
-            const double md = masked[0] * params[(11 + 3 * k + 0) * P + id] + masked[1] * params[(11 + 3 * k + 1) * P + id] +
-                              masked[2] * params[(11 + 3 * k + 2) * P + id];
-            for (int a = 0; a < 3; ++a) dd[a] += gb[3 * k + a] * md;
-          }
-          const double dot = dir[0] * dd[0] + dir[1] * dd[1] + dir[2] * dd[2];
-          for (int a = 0; a < 3; ++a) through[a] = (dd[a] - dir[a] * dot) / len;
-          for (int a = 0; a < 3; ++a) pose[3 + a] += Wr[3 * a + 0] * through[0] + Wr[3 * a + 1] * through[1] + Wr[3 * a + 2] * through[2];
-        }
+      } else if (K > 1) {
+        sh_backward(params, P, id, K, cam, m0, m1, m2, dcol, FULL ? grads : nullptr, through);
+        for (int a = 0; a < 3; ++a) pose[3 + a] += Wr[3 * a + 0] * through[0] + Wr[3 * a + 1] * through[1] + Wr[3 * a + 2] * through[2];
       }
       if (FULL) {
         if (d_mean2d) { d_mean2d[id] = static_cast<float>(sg[0]); d_mean2d[P + id] = static_cast<float>(sg[1]); }
@@ -656,8 +660,6 @@ __global__ void __launch_bounds__(256) k_chain(const uint8_t* __restrict__ visib
         for (int a = 0; a < 4; ++a) grads[(6 + a) * P + id] = static_cast<float>((dqn[a] - qn[a] * qd) / qlen);
         const double sig = 1.0 / (1.0 + exp(-static_cast<double>(params[10 * P + id])));
         grads[10 * P + id] = static_cast<float>((NF >= 10 ? sg[9] : 0.0) * sig * (1.0 - sig));
-        if (K > 0)
-          for (int k = 0; k < 3 * K; ++k) grads[(11 + k) * P + id] = static_cast<float>(dsh[k]);
       }
     }
   }
@@ -752,6 +754,8 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.partials = ws.partials;
   bp.pj = nullptr;
   bp.pj_slot = nullptr;
+  bp.rect = ws.rect_id;
+  bp.pair_base = ws.pair_base;
   bp.tile_pose = nullptr;
   const bool view_dep = a.K > 1;
   const int nf = a.pose_only ? (view_dep ? 9 : 6) : 10;
@@ -790,8 +794,8 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   if (ws.prof) ws.prof->begin(PROF_CHAIN, st);
   const int blocks = std::max(1, div_up(a.P, 256));
 #define GSF_CHAIN(NFV, FULLV)                                                                                            \
-  k_chain<NFV, FULLV><<<blocks, 256, 0, st>>>(ws.visible, ws.rect_id, ws.depth_id, ws.ranges, ws.skey, a.rp.tiles_x, \
-                                              ws.partials, ds, a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part)
+  k_chain<NFV, FULLV><<<blocks, 256, 0, st>>>(ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base, ws.partials, ds, \
+                                              a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part)
   if (nf == 6)
     GSF_CHAIN(6, false);
   else if (nf == 9)

@@ -444,7 +444,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
 #define GSF_PRE(CV)                                                                                                    \
   k_preprocess<CV><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,   \
                                                    ws.visible, &ds->bad_index, a.kc, ws.bin_counters,                    \
-                                                   a.want_posejac ? ws.vis_list : nullptr, ws.pj_slot, ws.world, ws.support)
+                                                   ws.vis_list, ws.pj_slot, ws.world, ws.support)
     if (a.use_world) GSF_PRE(true); else GSF_PRE(false);
 #undef GSF_PRE
     ++*L;
