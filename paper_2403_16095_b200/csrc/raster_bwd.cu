@@ -506,6 +506,8 @@ static __device__ __noinline__ void sh_backward(const float* __restrict__ params
   }
 }
 
+constexpr int kChainCoop = 64;
+
 template <int NF, bool FULL>
 #ifndef GSF_CHAIN_MINB
 #define GSF_CHAIN_MINB 2
@@ -520,20 +522,52 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t r = blockIdx.x * blockDim.x + tid;
   double pose[6] = {0, 0, 0, 0, 0, 0};
-  if (r < counters[kCntVisible] && !ds->halt) {
-    const int64_t id = vis_list[r];
-    // fixed-order gather of the primitive's pair partials: its slots hold the tiles of its
-    // rectangle in row-major order (the reference's tile-order reduction, rasterizer.cpp:466-478)
+  const bool active = r < counters[kCntVisible] && !ds->halt;
+  int64_t id = 0;
+  int c = 0;
+  const float* pp = partials;
+  if (active) {
+    id = vis_list[r];
     const int4 q = rect_id[id];
-    const int c = (q.y - q.x + 1) * (q.w - q.z + 1);
-    const float* pp = partials + static_cast<size_t>(pair_base[id]) * NF;
-    double sg[NF];
+    c = (q.y - q.x + 1) * (q.w - q.z + 1);
+    pp = partials + static_cast<size_t>(pair_base[id]) * NF;
+  }
+  // fixed-order gather of the primitive's pair partials: its slots hold the tiles of its
+  // rectangle in row-major order (the reference's tile-order reduction, rasterizer.cpp:466-478).
+  // Short lists are summed by their own lane; a list longer than kChainCoop is summed by the
+  // whole warp (lane-strided, then a fixed shuffle tree) so one huge footprint cannot leave a
+  // single thread walking thousands of L2 round trips.
+  double sg[NF];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) sg[f] = 0.0;
+  for (int f = 0; f < NF; ++f) sg[f] = 0.0;
+  const bool coop = c > kChainCoop;
+  if (!coop)
     for (int k = 0; k < c; ++k) {
 #pragma unroll
       for (int f = 0; f < NF; ++f) sg[f] += static_cast<double>(pp[k * NF + f]);
     }
+  uint32_t big = __ballot_sync(0xffffffffu, coop);
+  while (big) {
+    const int j = __ffs(big) - 1;
+    big &= big - 1u;
+    const int cj = __shfl_sync(0xffffffffu, c, j);
+    const float* pj = reinterpret_cast<const float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(pp), j));
+    double acc[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) acc[f] = 0.0;
+    for (int k = lane; k < cj; k += 32) {
+#pragma unroll
+      for (int f = 0; f < NF; ++f) acc[f] += static_cast<double>(pj[k * NF + f]);
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      double v = acc[f];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == j) sg[f] = v;
+    }
+  }
+  if (active) {
     bool zero = true;
 #pragma unroll
     for (int f = 0; f < NF; ++f) zero = zero && sg[f] == 0.0;
