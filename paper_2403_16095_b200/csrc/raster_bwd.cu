@@ -103,7 +103,10 @@ struct BwdPtrs {
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
 };
 
-constexpr int kBwdBatch = 64;
+#ifndef GSF_BWD_BATCH
+#define GSF_BWD_BATCH 96
+#endif
+constexpr int kBwdBatch = GSF_BWD_BATCH;
 
 template <int SEED, int NF>
 __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc, double near_plane,
@@ -176,11 +179,15 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
       s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, static_cast<float>(tx * kTile), static_cast<float>(ty * kTile), kc));
     }
     __syncthreads();
-    for (int k = cnt - 1; k >= 0; --k) {
-      if (!((s_mask[k] >> warp) & 1u)) {   // footprint cannot reach this warp's block
-        if (lane < NF) s_part[warp][k][lane] = 0.0f;
-        continue;
-      }
+    // back to front over only the entries whose footprint can reach this warp's block; the
+    // cross-warp sum below skips the (warp, entry) slots this loop never writes
+    for (int c0 = ((cnt - 1) >> 5) << 5; c0 >= 0; c0 -= 32) {
+     const int kk = c0 + lane;
+     uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
+     while (bits) {
+      const int jb = 31 - __clz(bits);
+      bits &= ~(1u << jb);
+      const int k = c0 + jb;
       const int li = bstart + k - rg.x;
       float f[NF];
 #pragma unroll
@@ -223,13 +230,16 @@ __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int 
       } else if (lane < NF) {
         s_part[warp][k][lane] = 0.0f;
       }
+     }
     }
     __syncthreads();
     for (int idx = tid; idx < cnt * NF; idx += 256) {
       const int k = idx / NF, fi = idx - k * NF;
+      const uint32_t m = s_mask[k];
       float sum = 0.0f;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) sum += s_part[w][k][fi];
+      for (int w = 0; w < 8; ++w)
+        if ((m >> w) & 1u) sum += s_part[w][k][fi];
       bp.partials[static_cast<size_t>(s_slot[k]) * NF + fi] = sum;
     }
     __syncthreads();
