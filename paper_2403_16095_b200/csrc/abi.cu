@@ -1202,13 +1202,15 @@ static AdamGroups groups_of(const gsf_mapper_cfg& m) {
 
 // One mapping-objective forward/backward of keyframe k into c->grads (accumulating).
 static void enqueue_map_view(gsf_ctx_s* c, const Frame& f, int k, const gsf_intrinsics& K, const gsf_mapper_cfg& m, int it,
-                             double* loss_acc, int trace_index) {
+                             double* loss_acc, int trace_index, bool use_world = false) {
   const LossParams lp = make_lp(2, &m.weights, m.raster);
   const int tiles = ((K.width + kTile - 1) / kTile) * ((K.height + kTile - 1) / kTile);
   const int64_t npix = static_cast<int64_t>(K.width) * K.height;
   k_set_cam_from_kf<<<1, 1, 0, c->stream>>>(c->ds, c->kf, k, 1);
   ++c->launches;
-  run_forward(c->ws, c->ds, fwd_args(c, K, m.raster, f.depth, f.rgb, f.depth, lp, it), c->stream, &c->launches);
+  FwdArgs fa = fwd_args(c, K, m.raster, f.depth, f.rgb, f.depth, lp, it);
+  fa.use_world = use_world;
+  run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
   if (m.weights.w_ssim > 0.0) run_ssim(c->ws, c->ds, c->ws.color, f.rgb, K.width, K.height, 1.0f, c->ws.dssim, c->stream, &c->launches);
   run_iso(c->ws, c->ds, c->params, c->P, m.weights.w_iso, m.weights.iso_epsilon, nullptr, c->stream, &c->launches);
   run_loss_finalize(c->ws, c->ds, lp, tiles, npix, it, c->stream, &c->launches);
@@ -1356,12 +1358,14 @@ int gsf_sliding_ba(gsf_ctx c, const int32_t* slots, gsf_pose* poses, const int32
         GSF_CUDA_CHECK(cudaMemsetAsync(c->d_mean2d, 0, sizeof(float) * c->P * 2, c->stream));
       }
       GSF_CUDA_CHECK(cudaMemsetAsync(loss_acc, 0, sizeof(double), c->stream));
+      // the map is constant across this iteration's keyframes: validate + cache it once
+      run_world(c->ws, c->ds, c->params, c->P, make_rp(c, *K, m->raster), c->stream, &c->launches);
       for (int k = 0; k < n; ++k) {
         if (!owned[k]) {
           GSF_CUDA_CHECK(cudaMemsetAsync(kf_grad(c, k), 0, sizeof(double) * 6, c->stream));
           continue;
         }
-        enqueue_map_view(c, *fr[k], k, *K, *m, it, loss_acc, -1);
+        enqueue_map_view(c, *fr[k], k, *K, *m, it, loss_acc, -1, true);
       }
       if (c->nranks > 1) {
         allreduce(c, c->grads, static_cast<size_t>(c->P) * c->D, 7);
