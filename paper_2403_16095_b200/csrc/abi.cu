@@ -261,7 +261,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   const int64_t tiles = static_cast<int64_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
   if (P > ws.P_cap) {
     dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
-    dalloc(ws.pj_id, static_cast<size_t>(P) * 36);
+    dalloc(ws.pj_id, static_cast<size_t>(P) * kPjFloats);
     dalloc(ws.big_ids, P);
     dalloc(ws.vis_list, P);
     dalloc(ws.pair_base, P);

@@ -62,7 +62,7 @@ struct Workspace {
   double* depth_id = nullptr;
   int4* rect_id = nullptr;
   uint8_t* visible = nullptr;
-  float* pj_id = nullptr;       // P * 36: pose Jacobians of the visible primitives at their list slot (tracking)
+  float* pj_id = nullptr;       // P * kPjFloats: pose matrices of the visible primitives at their list slot
   uint32_t* pj_slot = nullptr;  // P: id -> slot of its pose Jacobian
   WorldG* world = nullptr;      // P: view-independent part, cached per tracked frame (k_world)
   double* support = nullptr;    // P: footprint support of the same cache (NaN = invalid primitive)

@@ -308,8 +308,9 @@ template <int SEED, bool VIEWDEP>
 __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc,
                                                        double near_plane, double far_plane, LossParams lp,
                                                        DevState* ds, uint32_t* ticket) {
+  constexpr int kM4 = VIEWDEP ? 14 : 9;   // float4s of the pose matrix the kernel needs
   __shared__ BlendG s_g[kPoseBatch];
-  __shared__ float4 s_pj[kPoseBatch][9];
+  __shared__ float4 s_pj[kPoseBatch][kM4];
   __shared__ int32_t s_id[kPoseBatch];
   __shared__ uint8_t s_mask[kPoseBatch];
   __shared__ int s_wmax[8];
@@ -349,12 +350,13 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
       s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, tile_x0, tile_y0, kc));
     }
     __syncthreads();
-    for (int i = tid; i < cnt * 9; i += 256) {
-      const int k = i / 9, j = i - 9 * k;
-      s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[9 * static_cast<size_t>(bp.pj_slot[s_id[k]]) + j];
+    for (int i = tid; i < cnt * kM4; i += 256) {
+      const int k = i / kM4, j = i - kM4 * k;
+      s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[(kPjFloats / 4) * static_cast<size_t>(bp.pj_slot[s_id[k]]) + j];
     }
     __syncthreads();
-    float pf0 = 0.f, pf1 = 0.f, pf2 = 0.f, pf3 = 0.f, pf4 = 0.f, pf5 = 0.f;
+    // (rot0, rot1), (rot2, trans0), (trans1, trans2) of this batch, accumulated with FFMA2
+    float2 pa = make_float2(0.f, 0.f), pb2 = make_float2(0.f, 0.f), pc2 = make_float2(0.f, 0.f);
     // back to front over only the entries whose footprint can reach this warp's block
     for (int c0 = ((cnt - 1) >> 5) << 5; c0 >= 0; c0 -= 32) {
      const int kk = c0 + lane;
@@ -383,43 +385,42 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
       T = Tpre;
       const float s5 = kTrack ? w * pb.gad
                               : w * (pb.gad + 2.0f * pb.gu * derr) + (s_id[k] == pb.med ? pb.gmd : 0.0f);
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+      float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+      float s4 = 0.f;
       if (!e.clamped) {
-        const float dg = dal * g.sigma;
+        const float gdg = e.gval * (dal * g.sigma);
         const float c01 = 0.5f * g.c01x2;
         const float ux = g.c00 * e.dx + c01 * e.dy, uy = c01 * e.dx + g.c11 * e.dy;
-        const float gdg = e.gval * dg;
-        const float h = 0.5f * gdg;
-        s0 = gdg * ux;
-        s1 = gdg * uy;
-        s2 = h * ux * ux;
-        s3 = h * ux * uy;
-        s4 = h * uy * uy;
+        s01 = __fmul2_rn(make_float2(gdg, gdg), make_float2(ux, uy));   // d_mean2d
+        s23 = __fmul2_rn(make_float2(s01.x, s01.x), make_float2(ux, uy)); // 2 x d_cov 00, 01
+        s4 = s01.y * uy;                                                 // 2 x d_cov 11
       }
-      // layout: J00 J02 J11 J12 | Bc | Cr | p_cam | Tc (compute_posejac)
-      const float4 a0 = s_pj[k][0], a1 = s_pj[k][1], a2 = s_pj[k][2], a3 = s_pj[k][3], a4 = s_pj[k][4],
-                   a5 = s_pj[k][5], a6 = s_pj[k][6];
-      const float d0 = a0.x * s0 + a1.x * s2 + a1.y * s3 + a1.z * s4;
-      const float d1 = a0.z * s1 + a1.w * s2 + a2.x * s3 + a2.y * s4;
-      const float d2 = a0.y * s0 + a0.w * s1 + a2.z * s2 + a2.w * s3 + a3.x * s4 + s5;
-      const float pc0 = a5.z, pc1 = a5.w, pc2 = a6.x;
-      pf0 += pc1 * d2 - pc2 * d1 + a3.y * s2 + a3.z * s3 + a3.w * s4;
-      pf1 += pc2 * d0 - pc0 * d2 + a4.x * s2 + a4.y * s3 + a4.z * s4;
-      pf2 += pc0 * d1 - pc1 * d0 + a4.w * s2 + a5.x * s3 + a5.y * s4;
-      float t0 = d0, t1 = d1, t2 = d2;
+      // pose += M s, M column-major (compute_posejac): columns 0..5, then the colour columns
+      const float4* M = s_pj[k];
+#define GSF_COL(F4A, F4B, F4C, SV)                                                    \
+      {                                                                               \
+        const float2 sv = make_float2(SV, SV);                                        \
+        pa = __ffma2_rn(sv, F4A, pa);                                                 \
+        pb2 = __ffma2_rn(sv, F4B, pb2);                                               \
+        pc2 = __ffma2_rn(sv, F4C, pc2);                                               \
+      }
+      const float4 m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3], m4 = M[4], m5 = M[5], m6 = M[6], m7 = M[7], m8 = M[8];
+      GSF_COL(make_float2(m0.x, m0.y), make_float2(m0.z, m0.w), make_float2(m1.x, m1.y), s01.x)
+      GSF_COL(make_float2(m1.z, m1.w), make_float2(m2.x, m2.y), make_float2(m2.z, m2.w), s01.y)
+      GSF_COL(make_float2(m3.x, m3.y), make_float2(m3.z, m3.w), make_float2(m4.x, m4.y), s23.x)
+      GSF_COL(make_float2(m4.z, m4.w), make_float2(m5.x, m5.y), make_float2(m5.z, m5.w), s23.y)
+      GSF_COL(make_float2(m6.x, m6.y), make_float2(m6.z, m6.w), make_float2(m7.x, m7.y), s4)
+      GSF_COL(make_float2(m7.z, m7.w), make_float2(m8.x, m8.y), make_float2(m8.z, m8.w), s5)
       if (VIEWDEP) {
-        const float4 a7 = s_pj[k][7], a8 = s_pj[k][8];
-        const float c0 = w * pb.gc0, c1 = w * pb.gc1, c2 = w * pb.gc2;
-        t0 += a6.y * c0 + a6.z * c1 + a6.w * c2;
-        t1 += a7.x * c0 + a7.y * c1 + a7.z * c2;
-        t2 += a7.w * c0 + a8.x * c1 + a8.y * c2;
+        const float4 m9 = M[9], m10 = M[10], m11 = M[11], m12 = M[12], m13 = M[13];
+        GSF_COL(make_float2(m9.x, m9.y), make_float2(m9.z, m9.w), make_float2(m10.x, m10.y), w * pb.gc0)
+        GSF_COL(make_float2(m10.z, m10.w), make_float2(m11.x, m11.y), make_float2(m11.z, m11.w), w * pb.gc1)
+        GSF_COL(make_float2(m12.x, m12.y), make_float2(m12.z, m12.w), make_float2(m13.x, m13.y), w * pb.gc2)
       }
-      pf3 += t0;
-      pf4 += t1;
-      pf5 += t2;
+#undef GSF_COL
      }
     }
-    pd[0] += pf0; pd[1] += pf1; pd[2] += pf2; pd[3] += pf3; pd[4] += pf4; pd[5] += pf5;
+    pd[0] += pa.x; pd[1] += pa.y; pd[2] += pb2.x; pd[3] += pb2.y; pd[4] += pc2.x; pd[5] += pc2.y;
     __syncthreads();
   }
 #pragma unroll

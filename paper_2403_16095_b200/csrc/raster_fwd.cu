@@ -21,7 +21,11 @@ namespace {
 // pose gradient: the camera part of render_backward phase 2 (rasterizer.cpp:495-526, 548-558)
 // linearised per primitive in fp64, so the tracking backward can apply it right after its
 // per-tile reduction instead of round-tripping every pair partial through memory.
-// Layout (36 floats): J00 J02 J11 J12 | Bc[3][3] | Cr[3][3] | p_cam[3] | Tc[3][3] | pad pad
+// Output: the 6 x 9 matrix M with pose = sum_j M[:, j] s_j, column-major (kPjFloats floats):
+// columns j = 0..5 take the screen partials s = (d_mean2d x, y, d_cov2d 00, 01, 11 without the
+// 1/2 of d_conic, d_depth); columns 6..8 the view-dependent colour partials (zero unless K > 1).
+// Rows: rot0 rot1 rot2 trans0 trans1 trans2, so the kernel accumulates three float2 pairs with
+// packed FFMA2s.  In fp64: d = A s (A from J, Bc), rot = p_cam x d + Cr s_cov, trans = d.
 __device__ void compute_posejac(const float* __restrict__ p, int64_t stride, const Cam& cam, int K, float* out,
                                 const double* Sw) {
   const double m0 = p[0], m1 = p[stride], m2 = p[2 * stride];
@@ -115,18 +119,20 @@ __device__ void compute_posejac(const float* __restrict__ p, int64_t stride, con
         for (int c = 0; c < 3; ++c) Tc[a][c] = W[3 * a] * PD[0][c] + W[3 * a + 1] * PD[1][c] + W[3 * a + 2] * PD[2][c];
     }
   }
-  out[0] = static_cast<float>(J00);
-  out[1] = static_cast<float>(J02);
-  out[2] = static_cast<float>(J11);
-  out[3] = static_cast<float>(J12);
-  for (int a = 0; a < 3; ++a)
-    for (int c = 0; c < 3; ++c) {
-      out[4 + 3 * a + c] = static_cast<float>(Bc[a][c]);
-      out[13 + 3 * a + c] = static_cast<float>(Cr[a][c]);
-      out[25 + 3 * a + c] = static_cast<float>(Tc[a][c]);
-    }
-  for (int a = 0; a < 3; ++a) out[22 + a] = static_cast<float>(pc[a]);
-  out[34] = out[35] = 0.0f;
+  const double A[3][6] = {{J00, 0.0, Bc[0][0], Bc[0][1], Bc[0][2], 0.0},
+                          {0.0, J11, Bc[1][0], Bc[1][1], Bc[1][2], 0.0},
+                          {J02, J12, Bc[2][0], Bc[2][1], Bc[2][2], 1.0}};
+  for (int j = 0; j < 6; ++j) {
+    const double d0 = A[0][j], d1 = A[1][j], d2 = A[2][j];
+    double col[6] = {pc[1] * d2 - pc[2] * d1, pc[2] * d0 - pc[0] * d2, pc[0] * d1 - pc[1] * d0, d0, d1, d2};
+    if (j >= 2 && j <= 4)
+      for (int a = 0; a < 3; ++a) col[a] += Cr[a][j - 2];
+    const double scale = (j >= 2 && j <= 4) ? 0.5 : 1.0;   // the kernel's s_cov carries no 1/2
+    for (int a = 0; a < 6; ++a) out[6 * j + a] = static_cast<float>(scale * col[a]);
+  }
+  for (int c = 0; c < 3; ++c)
+    for (int a = 0; a < 6; ++a) out[36 + 6 * c + a] = a < 3 ? 0.0f : static_cast<float>(Tc[a - 3][c]);
+  out[54] = out[55] = 0.0f;
 }
 
 // Validation + view-independent part of every primitive, once per tracked frame (the map is
@@ -242,27 +248,29 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
 }
 
 // Pose Jacobians of the visible primitives (tracking), one thread per listed id; slot r of the
-// list owns pj[36 r, 36 r + 36), staged through shared memory so the CTA writes one contiguous,
+// list owns pj[kPjFloats r, kPjFloats (r + 1)), staged through shared memory so the CTA writes one contiguous,
 // coalesced block.
-__global__ void __launch_bounds__(256) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
+constexpr int kPjThreads = 128;
+__global__ void __launch_bounds__(kPjThreads) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
                                                  const uint32_t* __restrict__ vis_list, const uint32_t* counters,
                                                  const WorldG* __restrict__ world, float* __restrict__ pj) {
-  __shared__ float s_out[256 * 37];
+  __shared__ float s_out[kPjThreads * (kPjFloats + 1)];
   const uint32_t n = counters[kCntVisible];
   const uint32_t r0 = blockIdx.x * blockDim.x;
   if (r0 >= n || ds->halt) return;
   const uint32_t r = r0 + threadIdx.x;
   if (r < n) {
     const uint32_t id = vis_list[r];
-    float v[36];
+    float v[kPjFloats];
     compute_posejac(params + id, P, ds->cam, K, v, world ? world[id].S : nullptr);
 #pragma unroll
-    for (int q = 0; q < 36; ++q) s_out[threadIdx.x * 37 + q] = v[q];
+    for (int q = 0; q < kPjFloats; ++q) s_out[threadIdx.x * (kPjFloats + 1) + q] = v[q];
   }
   __syncthreads();
-  const uint32_t cnt = min(256u, n - r0);
-  float* dst = pj + 36 * static_cast<size_t>(r0);
-  for (uint32_t e = threadIdx.x; e < 36 * cnt; e += 256) dst[e] = s_out[(e / 36) * 37 + e % 36];
+  const uint32_t cnt = min(static_cast<uint32_t>(kPjThreads), n - r0);
+  float* dst = pj + kPjFloats * static_cast<size_t>(r0);
+  for (uint32_t e = threadIdx.x; e < kPjFloats * cnt; e += kPjThreads)
+    dst[e] = s_out[(e / kPjFloats) * (kPjFloats + 1) + e % kPjFloats];
 }
 
 __device__ __forceinline__ bool depth_valid(float d, double near_plane, double far_plane) {
@@ -449,7 +457,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
 #undef GSF_PRE
     ++*L;
     if (a.want_posejac) {
-      k_posejac<<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.K, ws.vis_list, ws.bin_counters,
+      k_posejac<<<div_up(P, kPjThreads), kPjThreads, 0, st>>>(a.params, P, ds, a.K, ws.vis_list, ws.bin_counters,
                                                 a.use_world ? ws.world : nullptr, ws.pj_id);
       ++*L;
     }
