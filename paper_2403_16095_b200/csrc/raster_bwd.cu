@@ -302,17 +302,26 @@ __device__ __forceinline__ PixBwd load_pixel_bwd(const BwdPtrs& bp, int64_t pi, 
 // Jacobian (compute_posejac) and accumulates the 6-vector in registers: no per-(tile, primitive)
 // cross-lane reduction, no pair partials in memory, no per-primitive chain kernel.  Lane sums
 // are fp32 within a batch and fp64 across batches; the CTA reduces them in a fixed tree.
-constexpr int kPoseBatch = 128;
+#ifndef GSF_POSE_BATCH
+#define GSF_POSE_BATCH 256
+#endif
+constexpr int kPoseBatch = GSF_POSE_BATCH;   // one batch covers most tile lists: one staging barrier
+
+template <bool VIEWDEP>
+constexpr size_t pose_smem_bytes() {
+  return static_cast<size_t>(kPoseBatch) * (sizeof(BlendG) + (VIEWDEP ? 14 : 9) * sizeof(float4) + sizeof(int32_t) + 1);
+}
 
 template <int SEED, bool VIEWDEP>
 __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc,
                                                        double near_plane, double far_plane, LossParams lp,
                                                        DevState* ds, uint32_t* ticket) {
   constexpr int kM4 = VIEWDEP ? 14 : 9;   // float4s of the pose matrix the kernel needs
-  __shared__ BlendG s_g[kPoseBatch];
-  __shared__ float4 s_pj[kPoseBatch][kM4];
-  __shared__ int32_t s_id[kPoseBatch];
-  __shared__ uint8_t s_mask[kPoseBatch];
+  extern __shared__ float4 s_dyn[];         // pose_smem_bytes<VIEWDEP>()
+  float4 (*s_pj)[kM4] = reinterpret_cast<float4 (*)[kM4]>(s_dyn);
+  BlendG* s_g = reinterpret_cast<BlendG*>(s_dyn + kPoseBatch * kM4);
+  int32_t* s_id = reinterpret_cast<int32_t*>(s_g + kPoseBatch);
+  uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_id + kPoseBatch);
   __shared__ int s_wmax[8];
   __shared__ double s_pred[8][6];
   const int tile = blockIdx.x;
@@ -352,7 +361,8 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
     __syncthreads();
     for (int i = tid; i < cnt * kM4; i += 256) {
       const int k = i / kM4, j = i - kM4 * k;
-      s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[(kPjFloats / 4) * static_cast<size_t>(bp.pj_slot[s_id[k]]) + j];
+      if (s_mask[k])   // entries no warp block can see are never read
+        s_pj[k][j] = reinterpret_cast<const float4*>(bp.pj)[(kPjFloats / 4) * static_cast<size_t>(bp.pj_slot[s_id[k]]) + j];
     }
     __syncthreads();
     // (rot0, rot1), (rot2, trans0), (trans1, trans2) of this batch, accumulated with FFMA2
@@ -812,8 +822,17 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     bp.tile_pose = ws.pose_part;
     uint32_t* ticket = ws.bin_counters + kCntBwdTicket;
     if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
-#define GSF_BWDP(SM, VD) \
-  k_backward_pose<SM, VD><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ticket)
+#define GSF_BWDP(SM, VD)                                                                                        \
+  do {                                                                                                          \
+    static bool attr_set = false;                                                                               \
+    if (!attr_set) {                                                                                            \
+      GSF_CUDA_CHECK(cudaFuncSetAttribute(k_backward_pose<SM, VD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                          static_cast<int>(pose_smem_bytes<VD>())));                          \
+      attr_set = true;                                                                                          \
+    }                                                                                                           \
+    k_backward_pose<SM, VD><<<ntiles, 256, pose_smem_bytes<VD>(), st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc,      \
+                                                                       a.near_plane, a.far_plane, a.lp, ds, ticket); \
+  } while (0)
     if (a.seed_mode == SEED_TRACK) {
       if (nf == 6) GSF_BWDP(SEED_TRACK, false); else GSF_BWDP(SEED_TRACK, true);
     } else {
