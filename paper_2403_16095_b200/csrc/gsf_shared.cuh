@@ -474,7 +474,7 @@ GSF_HD uint32_t depth_key(double depth, uint32_t near_bits) {
 struct BlendG {       // per visible primitive, rank order, 3 x float4 on the device
   float mx, my, depth, sigma;
   float c00, c01x2, c11, pad0;
-  float r, g, b, pad1;
+  float r, g, b, depth_b;   // depth_b = depth again: (b, depth) pair for packed FMAs
 };
 struct GuardG {       // fp64 copies read only inside the guard band
   double mx, my, c00, c01, c11, sigma;
@@ -492,7 +492,7 @@ GSF_HD BlendG make_blend_g(const PreOut& o) {
   g.r = static_cast<float>(o.color[0]);
   g.g = static_cast<float>(o.color[1]);
   g.b = static_cast<float>(o.color[2]);
-  g.pad1 = 0.0f;
+  g.depth_b = g.depth;
   return g;
 }
 GSF_HD GuardG make_guard_g(const PreOut& o) {
@@ -625,8 +625,16 @@ GSF_HD float exp_neg_half_fast(float rho) {
 template <bool FAST>
 GSF_HD PairEval eval_pair_t(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts& k) {
   PairEval e;
+#ifdef __CUDA_ARCH__
+  {   // one packed FADD2; p - m == p + (-m) exactly, so the bits equal the two fsub's
+    const float2 d = __fadd2_rn(make_float2(px, py), make_float2(-g.mx, -g.my));
+    e.dx = d.x;
+    e.dy = d.y;
+  }
+#else
   e.dx = fsub(px, g.mx);
   e.dy = fsub(py, g.my);
+#endif
   const float rho = pair_rho(e.dx, e.dy, g);
   e.code = 0;
   e.clamped = 0;

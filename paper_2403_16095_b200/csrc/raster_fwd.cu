@@ -284,6 +284,27 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// Tracking forward pixel state: the fields pixel_accumulate_min keeps, with the colour and
+// alpha-depth sums as two float2 pairs so each contributor costs two packed FFMA2s; __ffma2_rn
+// rounds each lane exactly like __fmaf_rn, so the values equal the scalar (mirror) ones.
+struct TrackPix {
+  float2 rg, bd;   // (colour r, g), (colour b, alpha depth)
+  float op, T;
+  int last, done;
+};
+
+__device__ __forceinline__ void track_accumulate(TrackPix& s, const BlendG& g, float alpha, int list_index,
+                                                 const BlendConsts& k) {
+  const float w = fmul(alpha, s.T);
+  const float2 ww = make_float2(w, w);
+  s.rg = __ffma2_rn(ww, make_float2(g.r, g.g), s.rg);
+  s.bd = __ffma2_rn(ww, make_float2(g.b, g.depth_b), s.bd);
+  s.op = fadd(s.op, w);
+  s.last = list_index + 1;
+  s.T = fmul(s.T, fsub(1.0f, alpha));
+  if (s.T < k.term) s.done = 1;
+}
+
 template <int LMODE>
 #ifndef GSF_BLEND_MINB
 #define GSF_BLEND_MINB 5
@@ -316,6 +337,12 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
   PixelState s;
   pixel_init(s);
   if (!inside) s.done = 1;
+  TrackPix t;   // LMODE 1 state (the PixelState is then unused)
+  t.rg = t.bd = make_float2(0.0f, 0.0f);
+  t.op = 0.0f;
+  t.T = 1.0f;
+  t.last = 0;
+  t.done = inside ? 0 : 1;
   bool obs_valid = false;
   float ov = 0.0f;
   if (obs && inside) {
@@ -326,7 +353,7 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
   const int lane = tid & 31, warp = tid >> 5;
   const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
   for (int start = rg.x; start < rg.y; start += 256) {
-    if (__syncthreads_and(s.done)) break;
+    if (__syncthreads_and(LMODE == 1 ? t.done : s.done)) break;
     const int j = start + tid;
     if (j < rg.y) {
       const int id = static_cast<int>(sid[j]);
@@ -344,17 +371,27 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
       while (bits) {
         const int k = c0 + __ffs(bits) - 1;
         bits &= bits - 1u;
-        if (s.done) continue;
-        const BlendG g = s_g[k];
-        const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
-        if (e.code) {
-          if (LMODE == 1)
-            pixel_accumulate_min(s, g, e, start + k - rg.x, kc);
-          else
-            pixel_accumulate(s, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+        if constexpr (LMODE == 1) {   // finished lanes ride along predicated instead of branching
+          const BlendG g = s_g[k];
+          const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
+          if (e.code && !t.done) track_accumulate(t, g, e.alpha, start + k - rg.x, kc);
+        } else {
+          if (s.done) continue;
+          const BlendG g = s_g[k];
+          const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
+          if (e.code) pixel_accumulate(s, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
         }
       }
     }
+  }
+  if (LMODE == 1) {
+    s.cr = t.rg.x;
+    s.cg = t.rg.y;
+    s.cb = t.bd.x;
+    s.ad = t.bd.y;
+    s.op = t.op;
+    s.T = t.T;
+    s.last = t.last;
   }
   if (inside) {
     o_color[3 * pi + 0] = s.cr;
