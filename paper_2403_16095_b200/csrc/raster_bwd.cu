@@ -387,7 +387,9 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
       // median-depth or uncertainty seeds on that path
       constexpr bool kTrack = SEED == SEED_TRACK;
       const float derr = kTrack ? 0.0f : g.depth - pb.D;
-      float q = pb.gc0 * g.r + pb.gc1 * g.g + pb.gc2 * g.b + pb.gad * g.depth;
+      const float2 q2 = __ffma2_rn(make_float2(pb.gc2, pb.gad), make_float2(g.b, g.depth_b),
+                                   __fmul2_rn(make_float2(pb.gc0, pb.gc1), make_float2(g.r, g.g)));
+      float q = q2.x + q2.y;
       if (!kTrack) q += pb.gop + pb.gu * derr * derr;
       const float dal = Tpre * q - S * inv;
       const float w = alpha * Tpre;
@@ -400,8 +402,10 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
       if (!e.clamped) {
         const float gdg = e.gval * (dal * g.sigma);
         const float c01 = 0.5f * g.c01x2;
-        const float ux = g.c00 * e.dx + c01 * e.dy, uy = c01 * e.dx + g.c11 * e.dy;
-        s01 = __fmul2_rn(make_float2(gdg, gdg), make_float2(ux, uy));   // d_mean2d
+        const float2 u = __ffma2_rn(make_float2(c01, g.c11), make_float2(e.dy, e.dy),
+                                    __fmul2_rn(make_float2(g.c00, c01), make_float2(e.dx, e.dx)));
+        const float ux = u.x, uy = u.y;
+        s01 = __fmul2_rn(make_float2(gdg, gdg), u);   // d_mean2d
         s23 = __fmul2_rn(make_float2(s01.x, s01.x), make_float2(ux, uy)); // 2 x d_cov 00, 01
         s4 = s01.y * uy;                                                 // 2 x d_cov 11
       }
