@@ -1075,6 +1075,7 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
     fa.want_posejac = true;
     fa.fuse_loss_final = true;
     fa.use_world = true;
+    fa.want_pair_base = false;
     run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
     BwdArgs b = bwd_args(c, k, rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);
     b.fused_pose = true;
@@ -1085,6 +1086,7 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
   FwdArgs fin = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, -1);
   fin.fuse_loss_final = true;
   fin.use_world = true;
+  fin.want_pair_base = false;
   run_forward(c->ws, c->ds, fin, c->stream, &c->launches);
   (void)tiles;
   (void)npix;

@@ -5,10 +5,10 @@
 // (rasterizer.cpp:193-212), so every tile list is in global depth order.  Only the per-tile
 // order is observable, so the device bins first and sorts each tile's (short) list:
 //
-//   k_scatter       every (tile, primitive) pair claims a slot of its tile's bucket with one
-//                   atomic on the tile's fill counter (one counter per L2 sector); a warp flattens
-//                   the pairs of its 32 primitives over its lanes, and lists the few primitives
-//                   with more than kBigPairs tiles (order inside a bucket is arbitrary)
+//   k_preprocess    (raster_fwd.cu) scatters every (tile, primitive) pair into its tile's bucket
+//                   with one atomic on the tile's fill counter (one counter per L2 sector); a warp
+//                   flattens the pairs of its 32 primitives over its lanes, and lists the few
+//                   primitives with more than kBigPairs tiles (order inside a bucket is arbitrary)
 //   k_scatter_big   one 1024-thread CTA per listed large-footprint primitive, so a primitive
 //                   covering a thousand tiles does not serialise one warp
 //   k_tile_scan     one CTA: exclusive scan of the tile counts -> list starts, pair total M,
@@ -30,10 +30,6 @@ namespace gsfk {
 namespace {
 
 constexpr int kSortChunk = 1024;   // longest list sorted entirely in shared memory (2 x 8 KB)
-
-__device__ __forceinline__ unsigned long long pair_key(double depth, uint32_t id) {
-  return (static_cast<unsigned long long>(static_cast<uint32_t>(__float_as_int(static_cast<float>(depth)))) << 32) | id;
-}
 
 __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__ fill, int ntiles, uint32_t bucket_cap,
                                                     uint32_t* __restrict__ start, const uint32_t* counters,
@@ -81,70 +77,6 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__
     ds->V = counters[kCntVisible];
     ds->max_tile = s_mx;
     if (s_carry > pair_cap || s_mx > bucket_cap) ds->overflow = 1u;
-  }
-}
-
-__device__ __forceinline__ void bucket_put(uint32_t* fill, unsigned long long* bucket, uint32_t bucket_cap, int64_t t,
-                                           unsigned long long key) {
-  const uint32_t slot = atomicAdd(&fill[t * kBinStride], 1u);
-  if (slot < bucket_cap) bucket[t * bucket_cap + slot] = key;
-}
-
-__global__ void __launch_bounds__(256) k_scatter(const uint8_t* __restrict__ visible, const int4* __restrict__ rect_id,
-                                                 const double* __restrict__ depth_id, int64_t P, int tiles_x,
-                                                 uint32_t* __restrict__ fill, uint32_t bucket_cap,
-                                                 unsigned long long* __restrict__ bucket, uint32_t* counters,
-                                                 uint32_t* __restrict__ big_ids, uint32_t* __restrict__ pair_base) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const bool vis = i < P && visible[i];
-  int4 q = make_int4(0, -1, 0, -1);
-  unsigned long long key = 0ull;
-  if (vis) {
-    q = rect_id[i];
-    key = pair_key(depth_id[i], static_cast<uint32_t>(i));
-  }
-  const int w = q.y - q.x + 1;
-  int c = vis ? w * (q.w - q.z + 1) : 0;
-  {
-    // primitive-major pair slots (pair_base[id] + rectangle index) for the mapping backward and
-    // its chain: a CTA scan of the pair counts plus one atomic per CTA (any order is fine: the
-    // chain reads each primitive's own slots in rectangle order)
-    __shared__ uint32_t s_w[8];
-    __shared__ uint32_t s_cta;
-    const int warp = threadIdx.x >> 5;
-    const int ex = warp_excl_scan(c);
-    if (lane == 31) s_w[warp] = static_cast<uint32_t>(ex + c);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t t = 0;
-      for (int k = 0; k < 8; ++k) t += s_w[k];
-      s_cta = t ? atomicAdd(&counters[kCntPairAlloc], t) : 0u;
-    }
-    __syncthreads();
-    if (vis) {
-      uint32_t b = s_cta + static_cast<uint32_t>(ex);
-      for (int k = 0; k < warp; ++k) b += s_w[k];
-      pair_base[i] = b;
-    }
-  }
-  if (c > kBigPairs) {   // k_scatter_big's
-    big_ids[atomicAdd(&counters[kCntBig], 1u)] = static_cast<uint32_t>(i);
-    c = 0;
-  }
-  const int excl = warp_excl_scan(c);
-  const int total = __shfl_sync(0xffffffffu, excl + c, 31);
-  for (int base = 0; base < total; base += 32) {
-    const int k = base + lane;
-    const int j = warp_owner(excl, k);   // lane whose pair range holds k
-    const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qy0 = __shfl_sync(0xffffffffu, q.z, j);
-    const int wj = __shfl_sync(0xffffffffu, w, j), ej = __shfl_sync(0xffffffffu, excl, j);
-    const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
-    if (k < total) {
-      const int r = k - ej;
-      const int row = r / wj;
-      bucket_put(fill, bucket, bucket_cap, (qy0 + row) * tiles_x + qx0 + (r - row * wj), kj);
-    }
   }
 }
 
@@ -326,10 +258,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ 
 void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles, cudaStream_t st, int64_t* L) {
   const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
   const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
-  if (P > 0) {
-    k_scatter<<<div_up(P, 256), 256, 0, st>>>(ws.visible, ws.rect_id, ws.depth_id, P, tiles_x, ws.tile_fill, bcap, ws.bucket,
-                                              ws.bin_counters, ws.big_ids, ws.pair_base);
-    ++*L;
+  if (P > 0) {   // the regular pairs were scattered by k_preprocess
     k_scatter_big<<<128, 1024, 0, st>>>(ws.big_ids, ws.bin_counters, ws.rect_id, ws.depth_id, tiles_x, ws.tile_fill, bcap,
                                         ws.bucket);
     ++*L;

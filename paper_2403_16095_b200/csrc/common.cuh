@@ -140,6 +140,18 @@ __device__ __forceinline__ int warp_owner(int excl, int k) {
   return lo;
 }
 
+// Tile-list sort key: (fp32 bits of the depth) << 32 | id (binning.cu).
+__device__ __forceinline__ unsigned long long pair_key(double depth, uint32_t id) {
+  return (static_cast<unsigned long long>(static_cast<uint32_t>(__float_as_int(static_cast<float>(depth)))) << 32) | id;
+}
+
+// One (tile, primitive) pair into its tile's bucket (binning.cu).
+__device__ __forceinline__ void bucket_put(uint32_t* fill, unsigned long long* bucket, uint32_t bucket_cap, int64_t t,
+                                           unsigned long long key) {
+  const uint32_t slot = atomicAdd(&fill[t * kBinStride], 1u);
+  if (slot < bucket_cap) bucket[t * bucket_cap + slot] = key;
+}
+
 #define GSF_CUDA_CHECK(expr)                                                        \
   do {                                                                              \
     cudaError_t _e = (expr);                                                        \

@@ -127,6 +127,7 @@ struct FwdArgs {
   bool want_posejac = false; // tracking: emit the per-primitive pose Jacobians (ws.pj_id)
   bool fuse_loss_final = false;  // tracking: the blend's last CTA runs the loss finalize
   bool use_world = false;        // preprocess from ws.world / ws.support (run_world ran for this map)
+  bool want_pair_base = true;    // primitive-major pair slots for a parameter-gradient backward
 };
 void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* launches);
 // per-primitive validation + view-independent cache (ws.world, ws.support)

@@ -171,7 +171,9 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
                                                     double* __restrict__ depth_id, int4* __restrict__ rect_id,
                                                     uint8_t* __restrict__ visible, int32_t* bad_index, BlendConsts kc,
                                                     uint32_t* counters, uint32_t* __restrict__ vis_list,
-                                                    uint32_t* __restrict__ pj_slot,
+                                                    uint32_t* __restrict__ pj_slot, uint32_t* __restrict__ fill,
+                                                    uint32_t bucket_cap, unsigned long long* __restrict__ bucket,
+                                                    uint32_t* __restrict__ big_ids, uint32_t* __restrict__ pair_base,
                                                     const WorldG* __restrict__ world, const double* __restrict__ support) {
   __shared__ uint32_t s_vis[8];
   __shared__ uint32_t s_base;
@@ -229,6 +231,52 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
   }
   const uint32_t bits = __ballot_sync(0xffffffffu, vis);
   if (lane == 0) s_vis[warp] = static_cast<uint32_t>(__popc(bits));
+  // tile binning (binning.cu): every (tile, primitive) pair into its tile's bucket
+  {
+    const int tiles_x = rp.tiles_x;
+    const int w = q.y - q.x + 1;
+    int c = vis ? w * (q.w - q.z + 1) : 0;
+    if (pair_base) {
+      // primitive-major pair slots (pair_base[id] + rectangle index) for the mapping backward and
+      // its chain: a CTA scan of the pair counts plus one atomic per CTA (any order is fine: the
+      // chain reads each primitive's own slots in rectangle order)
+      __shared__ uint32_t s_w[8];
+      __shared__ uint32_t s_cta;
+      const int ex = warp_excl_scan(c);
+      if (lane == 31) s_w[warp] = static_cast<uint32_t>(ex + c);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < 8; ++k) t += s_w[k];
+        s_cta = t ? atomicAdd(&counters[kCntPairAlloc], t) : 0u;
+      }
+      __syncthreads();
+      if (vis) {
+        uint32_t b = s_cta + static_cast<uint32_t>(ex);
+        for (int k = 0; k < warp; ++k) b += s_w[k];
+        pair_base[i] = b;
+      }
+    }
+    if (c > kBigPairs) {   // k_scatter_big's
+      big_ids[atomicAdd(&counters[kCntBig], 1u)] = static_cast<uint32_t>(i);
+      c = 0;
+    }
+    const unsigned long long key = vis ? pair_key(depth_id[i], static_cast<uint32_t>(i)) : 0ull;
+    const int excl = warp_excl_scan(c);
+    const int total = __shfl_sync(0xffffffffu, excl + c, 31);
+    for (int base = 0; base < total; base += 32) {
+      const int k = base + lane;
+      const int j = warp_owner(excl, k);   // lane whose pair range holds k
+      const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qy0 = __shfl_sync(0xffffffffu, q.z, j);
+      const int wj = __shfl_sync(0xffffffffu, w, j), ej = __shfl_sync(0xffffffffu, excl, j);
+      const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
+      if (k < total) {
+        const int r = k - ej;
+        const int row = r / wj;
+        bucket_put(fill, bucket, bucket_cap, (qy0 + row) * tiles_x + qx0 + (r - row * wj), kj);
+      }
+    }
+  }
   // visible count (one atomic per CTA) and, for the pose Jacobians, the list of visible ids
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -489,7 +537,9 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
 #define GSF_PRE(CV)                                                                                                    \
   k_preprocess<CV><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,   \
                                                    ws.visible, &ds->bad_index, a.kc, ws.bin_counters,                    \
-                                                   ws.vis_list, ws.pj_slot, ws.world, ws.support)
+                                                   ws.vis_list, ws.pj_slot, ws.tile_fill,                                 \
+                                                   static_cast<uint32_t>(ws.bucket_cap), ws.bucket, ws.big_ids,           \
+                                                   a.want_pair_base ? ws.pair_base : nullptr, ws.world, ws.support)
     if (a.use_world) GSF_PRE(true); else GSF_PRE(false);
 #undef GSF_PRE
     ++*L;
