@@ -78,6 +78,26 @@ struct KfPose {
 
 }  // namespace
 
+// A captured track_frame (all iterations + the final render) replayed while its inputs match.
+struct TrackGraphKey {
+  const float* rgb;
+  const float* depth;
+  const float* params;
+  gsf_intrinsics K;
+  gsf_raster_cfg rcfg;
+  gsf_loss_weights w;
+  int32_t iterations;
+  int64_t P;
+  int32_t sh;
+  int64_t alloc_gen;
+};
+struct TrackGraph {
+  bool valid = false;
+  TrackGraphKey key{};
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;   // kernel launches one replay performs
+};
+
 struct gsf_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -121,6 +141,10 @@ struct gsf_ctx_s {
   gsf_intrinsics rK{};
   gsf_raster_cfg rcfg{};
   bool render_obs = false;
+  // captured track_frame graphs (small round-robin cache)
+  TrackGraph track_graphs[8];
+  int track_graph_next = 0;
+  bool use_graphs = true;
   // staging for host inputs
   float* stage = nullptr;
   size_t stage_bytes = 0;
@@ -140,11 +164,15 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
+// Bumped by every device (re)allocation: captured CUDA graphs hold raw buffer pointers.
+int64_t g_alloc_gen = 0;
+
 template <class T>
 void dalloc(T*& p, size_t count) {
   dfree(p);
   if (count == 0) count = 1;
   GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * count));
+  ++g_alloc_gen;
 }
 
 void check_intrinsics(const gsf_intrinsics& k) {   // camera.hpp:20-26
@@ -604,6 +632,8 @@ int gsf_ctx_destroy(gsf_ctx c) {
   if (!c) return GSF_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  for (TrackGraph& g : c->track_graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   Workspace& ws = c->ws;
   void* bufs[] = {ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
@@ -1092,6 +1122,60 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
   (void)npix;
 }
 
+// The ~10 launches per iteration of a track_frame replayed as one CUDA graph: the loop is
+// captured once per (frame buffers, camera, configuration, map, allocation generation) and
+// replayed while those match; profiling (per-kernel events) and the first attempt after a
+// capacity growth run eagerly.
+static void run_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k, const gsf_tracker_cfg& tcfg,
+                      const gsf_loss_weights& w, const gsf_raster_cfg& rcfg) {
+  if (!c->use_graphs || (c->ws.prof && c->ws.prof->on)) {
+    enqueue_track(c, f, k, tcfg, w, rcfg);
+    return;
+  }
+  TrackGraphKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.rgb = f.rgb;
+  key.depth = f.depth;
+  key.params = c->params;
+  key.K = k;
+  key.rcfg = rcfg;
+  key.w = w;
+  key.iterations = tcfg.iterations;
+  key.P = c->P;
+  key.sh = c->K;
+  key.alloc_gen = g_alloc_gen;
+  for (TrackGraph& g : c->track_graphs)
+    if (g.valid && std::memcmp(&g.key, &key, sizeof(key)) == 0) {
+      GSF_CUDA_CHECK(cudaGraphLaunch(g.exec, c->stream));
+      c->launches += g.launches;
+      return;
+    }
+  TrackGraph& g = c->track_graphs[c->track_graph_next];
+  c->track_graph_next = (c->track_graph_next + 1) % 8;
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  g.exec = nullptr;
+  g.valid = false;
+  const int64_t l0 = c->launches;
+  GSF_CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_track(c, f, k, tcfg, w, rcfg);
+  } catch (...) {
+    cudaGraph_t dummy = nullptr;
+    cudaStreamEndCapture(c->stream, &dummy);
+    if (dummy) cudaGraphDestroy(dummy);
+    throw;
+  }
+  cudaGraph_t graph = nullptr;
+  GSF_CUDA_CHECK(cudaStreamEndCapture(c->stream, &graph));
+  const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  GSF_CUDA_CHECK(ie);
+  g.key = key;
+  g.launches = c->launches - l0;
+  g.valid = true;
+  GSF_CUDA_CHECK(cudaGraphLaunch(g.exec, c->stream));
+}
+
 int gsf_track_frame(gsf_ctx c, int32_t slot, const gsf_pose* initial, const gsf_intrinsics* K, const gsf_tracker_cfg* tcfg,
                     const gsf_loss_weights* w, const gsf_raster_cfg* rcfg, gsf_track_result* out) {
   return guard(c, [&] {
@@ -1109,7 +1193,7 @@ int gsf_track_frame(gsf_ctx c, int32_t slot, const gsf_pose* initial, const gsf_
       h.lr_trans = tcfg->lr_translation;
       h.degraded_ratio = tcfg->degraded_loss_ratio;
       GSF_CUDA_CHECK(cudaMemcpyAsync(c->ds, &h, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
-      enqueue_track(c, f, *K, *tcfg, *w, *rcfg);
+      run_track(c, f, *K, *tcfg, *w, *rcfg);
       read_state(c);
       if (!h.overflow) break;
       grow_pairs(c, h.M);
