@@ -10,6 +10,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <sstream>
@@ -612,6 +613,7 @@ int gsf_ctx_create(int device, gsf_ctx* out) {
   if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) return GSF_ECUDA;
   auto* c = new gsf_ctx_s;
   c->device = device;
+  c->use_graphs = std::getenv("GSF_NO_GRAPHS") == nullptr;   // eager launches for debugging
   const int rc = guard(c, [&] {
     GSF_CUDA_CHECK(cudaSetDevice(device));
     GSF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

@@ -13,7 +13,10 @@ constexpr int kTile = 16;
 // measured 35 us for the 563k pair increments of configs[1] packed vs 12 us one per sector),
 // primitives with more than kBigPairs tiles go to the one-CTA-per-primitive scatter, and the
 // slots of Workspace::bin_counters.
-constexpr int kBinStride = 8;
+#ifndef GSF_BIN_STRIDE
+#define GSF_BIN_STRIDE 8
+#endif
+constexpr int kBinStride = GSF_BIN_STRIDE;
 constexpr int kPjFloats = 56;   // per-primitive pose matrix: 9 columns x 6 rows + 2 pad (k_posejac)
 constexpr int kBigPairs = 128;
 enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntPairAlloc = 4, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
