@@ -14,21 +14,29 @@ namespace gsfk {
 
 namespace {
 
+// One field per blockIdx.y, so the group and learning rate are uniform per CTA (no per-element
+// 64-bit division to find the field); each thread streams kAdamPer elements of that field.
+constexpr int kAdamPer = 4;
 __global__ void __launch_bounds__(256) k_adam(float* __restrict__ params, const float* __restrict__ grads,
-                                              float* __restrict__ m, float* __restrict__ v, int64_t P, int D, AdamGroups g,
+                                              float* __restrict__ m, float* __restrict__ v, int64_t P, AdamGroups g,
                                               double bc1, double bc2) {
-  const int64_t n = static_cast<int64_t>(D) * P;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int f = static_cast<int>(i / P);
-    const int grp = f < 3 ? 0 : (f < 6 ? 1 : (f < 10 ? 2 : (f < 11 ? 3 : 4)));
-    const double gr = grads[i];
-    const double mm = 0.9 * static_cast<double>(m[i]) + (1.0 - 0.9) * gr;
-    const double vv = 0.999 * static_cast<double>(v[i]) + (1.0 - 0.999) * gr * gr;
-    m[i] = static_cast<float>(mm);
-    v[i] = static_cast<float>(vv);
-    const double upd = g.lr[grp] * (mm / bc1) / (sqrt(vv / bc2) + 1e-8);
-    params[i] = static_cast<float>(static_cast<double>(params[i]) - upd);
+  const int f = blockIdx.y;
+  const int grp = f < 3 ? 0 : (f < 6 ? 1 : (f < 10 ? 2 : (f < 11 ? 3 : 4)));
+  const double lr = g.lr[grp];
+  const int64_t base = static_cast<int64_t>(f) * P;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x * kAdamPer + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < kAdamPer; ++u) {
+    const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+    if (i >= P) break;
+    const int64_t e = base + i;
+    const double gr = grads[e];
+    const double mm = 0.9 * static_cast<double>(m[e]) + (1.0 - 0.9) * gr;
+    const double vv = 0.999 * static_cast<double>(v[e]) + (1.0 - 0.999) * gr * gr;
+    m[e] = static_cast<float>(mm);
+    v[e] = static_cast<float>(vv);
+    const double upd = lr * (mm / bc1) / (sqrt(vv / bc2) + 1e-8);
+    params[e] = static_cast<float>(static_cast<double>(params[e]) - upd);
   }
 }
 
@@ -53,8 +61,8 @@ void run_adam(float* params, const float* grads, float* m, float* v, int64_t P, 
   if (n == 0) return;
   const double bc1 = 1.0 - std::pow(0.9, step);
   const double bc2 = 1.0 - std::pow(0.999, step);
-  const int blocks = static_cast<int>(std::min<int64_t>(div_up(n, 256), 148 * 16));
-  k_adam<<<blocks, 256, 0, st>>>(params, grads, m, v, P, D, g, bc1, bc2);
+  const dim3 grid(static_cast<unsigned>(div_up(P, 256 * kAdamPer)), static_cast<unsigned>(D));
+  k_adam<<<grid, 256, 0, st>>>(params, grads, m, v, P, g, bc1, bc2);
   ++*L;
 }
 

@@ -104,18 +104,24 @@ struct BwdPtrs {
 };
 
 #ifndef GSF_BWD_BATCH
-#define GSF_BWD_BATCH 96
+#define GSF_BWD_BATCH 192
 #endif
 constexpr int kBwdBatch = GSF_BWD_BATCH;
+
+template <int NF>
+constexpr size_t bwd_smem_bytes() {
+  return static_cast<size_t>(kBwdBatch) * (8 * NF * sizeof(float) + sizeof(BlendG) + 2 * sizeof(int32_t) + 1);
+}
 
 template <int SEED, int NF>
 __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc, double near_plane,
                                                   double far_plane, LossParams lp, const DevState* ds) {
-  __shared__ BlendG s_g[kBwdBatch];
-  __shared__ int32_t s_id[kBwdBatch];
-  __shared__ uint32_t s_slot[kBwdBatch];
-  __shared__ uint8_t s_mask[kBwdBatch];
-  __shared__ float s_part[8][kBwdBatch][NF];
+  extern __shared__ float4 s_dyn[];   // bwd_smem_bytes<NF>()
+  float (*s_part)[kBwdBatch][NF] = reinterpret_cast<float (*)[kBwdBatch][NF]>(s_dyn);
+  BlendG* s_g = reinterpret_cast<BlendG*>(&s_part[8][0][0]);
+  int32_t* s_id = reinterpret_cast<int32_t*>(s_g + kBwdBatch);
+  uint32_t* s_slot = reinterpret_cast<uint32_t*>(s_id + kBwdBatch);
+  uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_slot + kBwdBatch);
   __shared__ int s_wmax[8];
   const int tile = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -848,7 +854,17 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     return;
   }
   if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
-#define GSF_BWD(SM, NFV) k_backward<SM, NFV><<<ntiles, 256, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds)
+#define GSF_BWD(SM, NFV)                                                                                          \
+  do {                                                                                                            \
+    static bool attr_set = false;                                                                                 \
+    if (!attr_set) {                                                                                              \
+      GSF_CUDA_CHECK(cudaFuncSetAttribute(k_backward<SM, NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                          static_cast<int>(bwd_smem_bytes<NFV>())));                             \
+      attr_set = true;                                                                                            \
+    }                                                                                                             \
+    k_backward<SM, NFV><<<ntiles, 256, bwd_smem_bytes<NFV>(), st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, \
+                                                                     a.far_plane, a.lp, ds);                    \
+  } while (0)
   if (a.seed_mode == SEED_TRACK) {
     if (nf == 6) GSF_BWD(SEED_TRACK, 6); else if (nf == 9) GSF_BWD(SEED_TRACK, 9); else GSF_BWD(SEED_TRACK, 10);
   } else if (a.seed_mode == SEED_MAP) {

@@ -353,6 +353,35 @@ __device__ __forceinline__ void track_accumulate(TrackPix& s, const BlendG& g, f
   if (s.T < k.term) s.done = 1;
 }
 
+// pixel_accumulate (gsf_shared.cuh) with the colour / alpha-depth sums as two packed FFMA2s;
+// every lane rounds like __fmaf_rn, so the state equals the mirror's bit for bit.
+__device__ __forceinline__ void full_accumulate(PixelState& s, float2& rg, float2& bd, const BlendG& g, const PairEval& e,
+                                                int32_t id, int32_t list_index, bool obs_valid, float obs,
+                                                const BlendConsts& k) {
+  const float w = fmul(e.alpha, s.T);
+  const float2 ww = make_float2(w, w);
+  rg = __ffma2_rn(ww, make_float2(g.r, g.g), rg);
+  bd = __ffma2_rn(ww, make_float2(g.b, g.depth_b), bd);
+  s.op = fadd(s.op, w);
+  if (obs_valid) {
+    const float d = fsub(g.depth, obs);
+    s.unc = ffma(fmul(w, d), d, s.unc);
+  }
+  if (w > s.best) {
+    s.best = w;
+    s.dominant = id;
+  }
+  s.count += 1;
+  s.last = list_index + 1;
+  const float t_next = fmul(s.T, fsub(1.0f, e.alpha));
+  if (s.median < 0 && s.T >= 0.5f && t_next < 0.5f) {
+    s.median = id;
+    s.med_depth = g.depth;
+  }
+  s.T = t_next;
+  if (s.T < k.term) s.done = 1;
+}
+
 template <int LMODE>
 #ifndef GSF_BLEND_MINB
 #define GSF_BLEND_MINB 5
@@ -385,6 +414,7 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
   PixelState s;
   pixel_init(s);
   if (!inside) s.done = 1;
+  float2 frg = make_float2(0.0f, 0.0f), fbd = make_float2(0.0f, 0.0f);   // LMODE 0/2 colour, alpha depth
   TrackPix t;   // LMODE 1 state (the PixelState is then unused)
   t.rg = t.bd = make_float2(0.0f, 0.0f);
   t.op = 0.0f;
@@ -427,10 +457,16 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
           if (s.done) continue;
           const BlendG g = s_g[k];
           const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
-          if (e.code) pixel_accumulate(s, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+          if (e.code) full_accumulate(s, frg, fbd, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
         }
       }
     }
+  }
+  if (LMODE != 1) {
+    s.cr = frg.x;
+    s.cg = frg.y;
+    s.cb = fbd.x;
+    s.ad = fbd.y;
   }
   if (LMODE == 1) {
     s.cr = t.rg.x;
