@@ -188,6 +188,38 @@ def test_backward_vs_fp64_oracle(gpu_ctx, orc, sh):
         _pose_close(g.d_pose, go.d_pose)
 
 
+def test_large_footprints_forward_and_backward(gpu_ctx, orc):
+    """Primitives covering hundreds of tiles: the one-CTA-per-primitive scatter (> 128 tiles) and
+    the warp-cooperative gather of the chain (> 64 tiles) against the mirror / fp64 oracle."""
+    rng = np.random.default_rng(77)
+    m = orc.random_scene(77, 60)
+    m.log_scale[:4] = np.log([0.6, 0.45, 0.8, 0.5])[:, None] + 0.1 * rng.standard_normal((4, 3))
+    m.mean[:4] = [[0.1, 0.0, 2.2], [-0.2, 0.1, 2.6], [0.0, -0.1, 3.0], [0.3, 0.2, 2.4]]
+    m = f32_round(m)
+    K = make_intrinsics(320, 240, 200.0)
+    obs = orc.wavy_depth(320, 240, 2.5).astype(np.float32)
+    p = pose(0.01 * rng.standard_normal(3), 0.02 * rng.standard_normal(3))
+    _upload(gpu_ctx, m)
+    r = gpu_ctx.render(p, K, obs)
+    mr = orc.mirror_render(m, p, K, obs)
+    ntiles = 20 * 15
+    tr, pp = gpu_ctx.render_tiles(ntiles, r.num_pairs)
+    spans = (tr[:, 1] - tr[:, 0])
+    assert (spans > 0).sum() > 200
+    assert (tr.ravel() == mr.tile_range).all() and (pp == mr.rank_to_id[mr.pair_rank]).all()
+    for k in ("per_pixel_count", "dominant", "median_prim"):
+        assert (getattr(r, k) == getattr(mr, k)).all(), k
+    assert np.array_equal(r.color, mr.color)
+    a_c, a_d, a_o, a_u, a_m = [None if a is None else a.astype(np.float32).astype(np.float64)
+                               for a in _probe(rng, 320, 240, True)]
+    g = gpu_ctx.render_backward(a_c, a_d, a_m, a_o, a_u, obs)
+    o = orc.render(m, p, K, obs.astype(np.float64))
+    go = orc.render_backward(m, p, K, o, a_c, a_d, a_m, a_o, a_u, obs.astype(np.float64))
+    for k in ("d_mean", "d_log_scale", "d_quat", "d_opacity_logit", "d_sh", "d_mean2d"):
+        _grad_close(getattr(g, k), getattr(go, k), name=k)
+    _pose_close(g.d_pose, go.d_pose)
+
+
 def test_backward_zero_upstream(gpu_ctx, orc):
     _upload(gpu_ctx, f32_round(orc.random_scene(7, 10)))
     gpu_ctx.render(pose(), make_intrinsics(16, 16, 15.0))
