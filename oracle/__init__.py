@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
                                    C.POINTER(Intrinsics), C.POINTER(MapperCfg), C.c_int, dp]),
         "orc_sliding_ba": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(dp), C.POINTER(dp), C.POINTER(Pose), i32p,
                                      C.POINTER(Intrinsics), C.POINTER(TrackerCfg), C.POINTER(MapperCfg), C.c_int, dp]),
+        "orc_uncertainty_partials": (C.c_int, [C.POINTER(MapHost), C.c_int, C.POINTER(C.c_void_p), C.POINTER(dp),
+                                               C.POINTER(Pose), C.POINTER(Intrinsics), dp, i32p]),
         "orc_accumulate_uncertainty": (C.c_int, [C.POINTER(MapHost), C.c_int, C.POINTER(C.c_void_p), C.POINTER(dp),
                                                  C.POINTER(Pose), C.POINTER(Intrinsics), i32p]),
         "orc_prune_unreliable": (C.c_int, [C.POINTER(MapHost), C.c_double, C.c_double, i32p]),
@@ -344,6 +346,21 @@ def accumulate_uncertainty(m, results, depths, poses, K):
     h = host_of(m)
     _check(lib().orc_accumulate_uncertainty(C.byref(h), n, rh, dg, ps, C.byref(K), C.byref(cnt)))
     return cnt.value
+
+
+def uncertainty_partials(m, results, depths, poses, K):
+    """Per-primitive (sum, count) of Eq. 13 over the given views (uncertainty.cpp:35-73)."""
+    n = len(results)
+    keep = [np.ascontiguousarray(d, dtype=np.float64) for d in depths]
+    rh = (C.c_void_p * max(n, 1))(*[r.h for r in results])
+    dg = (dp * max(n, 1))(*[k.ctypes.data_as(dp) for k in keep])
+    ps = (Pose * max(n, 1))(*poses)
+    P = m.mean.shape[0]
+    s = np.zeros(max(P, 1))
+    c = np.zeros(max(P, 1), np.int32)
+    h = host_of(m)
+    _check(lib().orc_uncertainty_partials(C.byref(h), n, rh, dg, ps, C.byref(K), s.ctypes.data_as(dp), c.ctypes.data_as(i32p)))
+    return s[:P], c[:P]
 
 
 def prune_unreliable(m, tau=0.025, reduced=0.005):

@@ -1817,6 +1817,53 @@ int orc_sliding_ba(orc_mapstate* st, int n, const double* const* rgbs, const dou
   });
 }
 
+// uncertainty.cpp:35-73: per-view (sum, count) partials of Eq. 13 reduced in window order
+static void uncertainty_partials(const std::vector<Prim>& prims, int n, const orc_result* const* records,
+                                 const double* const* depths, const gsf_pose* poses, const gsf_intrinsics* K,
+                                 std::vector<double>& total, std::vector<int>& pixels) {
+  const size_t np = prims.size();
+  total.assign(np, 0.0);
+  pixels.assign(np, 0);
+  for (int v = 0; v < n; ++v) {
+    const Record& rec = records[v]->r.record;
+    if (rec.num_primitives != static_cast<int>(np))
+      throw std::invalid_argument("uncertainty view was rendered from a different primitive set");
+    const M3 rot = to_pose(&poses[v]).rotation();
+    const V3 t = to_pose(&poses[v]).trans;
+    std::vector<double> depth_in_view(np);
+    for (size_t i = 0; i < np; ++i) depth_in_view[i] = (mul(rot, prims[i].mean) + t)[2];
+    std::vector<double> sum(np, 0.0);
+    std::vector<int> count(np, 0);
+    for (int y = 0; y < rec.height; ++y)
+      for (int x = 0; x < rec.width; ++x) {
+        const size_t pi = static_cast<size_t>(y) * rec.width + x;
+        const int32_t owner = rec.dominant[pi];
+        if (owner < 0) continue;
+        const double d_obs = depths[v][pi];
+        if (!std::isfinite(d_obs) || d_obs <= K->near_plane || d_obs >= K->far_plane) continue;
+        for (uint32_t e = rec.row_start[pi]; e < rec.row_start[pi + 1]; ++e) {
+          if (rec.prim[e] != owner) continue;
+          const double resid = d_obs - depth_in_view[owner];
+          sum[owner] += rec.alpha[e] * rec.transmittance[e] * resid * resid;
+          ++count[owner];
+          break;
+        }
+      }
+    for (size_t i = 0; i < np; ++i) { total[i] += sum[i]; pixels[i] += count[i]; }
+  }
+}
+
+int orc_uncertainty_partials(const gsf_map_host* map, int n, const orc_result* const* records, const double* const* depths,
+                             const gsf_pose* poses, const gsf_intrinsics* K, double* sum_out, int32_t* count_out) {
+  return guarded([&] {
+    const std::vector<Prim> prims = load_map(map);
+    std::vector<double> total;
+    std::vector<int> pixels;
+    uncertainty_partials(prims, n, records, depths, poses, K, total, pixels);
+    for (size_t i = 0; i < prims.size(); ++i) { sum_out[i] = total[i]; count_out[i] = pixels[i]; }
+  });
+}
+
 // uncertainty.cpp:17-87
 int orc_accumulate_uncertainty(gsf_map_host* map, int n, const orc_result* const* records, const double* const* depths,
                                const gsf_pose* poses, const gsf_intrinsics* K, int32_t* observed_count) {
@@ -1825,35 +1872,9 @@ int orc_accumulate_uncertainty(gsf_map_host* map, int n, const orc_result* const
     if (n == 0) return;
     std::vector<Prim> prims = load_map(map);
     const size_t np = prims.size();
-    std::vector<double> total(np, 0.0);
-    std::vector<int> pixels(np, 0);
-    for (int v = 0; v < n; ++v) {
-      const Record& rec = records[v]->r.record;
-      if (rec.num_primitives != static_cast<int>(np))
-        throw std::invalid_argument("uncertainty view was rendered from a different primitive set");
-      const M3 rot = to_pose(&poses[v]).rotation();
-      const V3 t = to_pose(&poses[v]).trans;
-      std::vector<double> depth_in_view(np);
-      for (size_t i = 0; i < np; ++i) depth_in_view[i] = (mul(rot, prims[i].mean) + t)[2];
-      std::vector<double> sum(np, 0.0);
-      std::vector<int> count(np, 0);
-      for (int y = 0; y < rec.height; ++y)
-        for (int x = 0; x < rec.width; ++x) {
-          const size_t pi = static_cast<size_t>(y) * rec.width + x;
-          const int32_t owner = rec.dominant[pi];
-          if (owner < 0) continue;
-          const double d_obs = depths[v][pi];
-          if (!std::isfinite(d_obs) || d_obs <= K->near_plane || d_obs >= K->far_plane) continue;
-          for (uint32_t e = rec.row_start[pi]; e < rec.row_start[pi + 1]; ++e) {
-            if (rec.prim[e] != owner) continue;
-            const double resid = d_obs - depth_in_view[owner];
-            sum[owner] += rec.alpha[e] * rec.transmittance[e] * resid * resid;
-            ++count[owner];
-            break;
-          }
-        }
-      for (size_t i = 0; i < np; ++i) { total[i] += sum[i]; pixels[i] += count[i]; }
-    }
+    std::vector<double> total;
+    std::vector<int> pixels;
+    uncertainty_partials(prims, n, records, depths, poses, K, total, pixels);
     int observed = 0;
     for (size_t i = 0; i < np; ++i) {
       if (pixels[i] > 0) {

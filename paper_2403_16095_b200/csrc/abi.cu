@@ -1510,10 +1510,17 @@ int gsf_accumulate_uncertainty(gsf_ctx c, const int32_t* slots, const gsf_pose* 
     if (P == 0) return;
     GSF_CUDA_CHECK(cudaMemsetAsync(c->unc_sum, 0, sizeof(double) * P, c->stream));
     GSF_CUDA_CHECK(cudaMemsetAsync(c->unc_cnt, 0, sizeof(uint32_t) * P, c->stream));
+    // multi-GPU: rank g accumulates the views v = g (mod nranks) and the (sum, count) partials
+    // are all-reduced before the division (Eq. 13 is order-invariant)
     for (int v = 0; v < n; ++v) {
+      if (c->nranks > 1 && v % c->nranks != c->rank) continue;
       render_sync(c, poses[v], *K, *rcfg, fr[v]->depth);
       run_uncertainty_view(c->ws, c->params, P, fr[v]->depth, K->width, K->height, K->near_plane, K->far_plane, c->ds,
                            c->unc_sum, c->unc_cnt, c->stream, &c->launches);
+    }
+    if (c->nranks > 1) {
+      allreduce(c, c->unc_sum, static_cast<size_t>(P), 8 /*f64*/);
+      allreduce(c, c->unc_cnt, static_cast<size_t>(P), 3 /*u32*/);
     }
     GSF_CUDA_CHECK(cudaMemsetAsync(c->counters, 0, sizeof(uint32_t) * 16, c->stream));
     run_uncertainty_finalize(c->unc_sum, c->unc_cnt, c->nu, c->observed, P, c->counters, c->stream, &c->launches);

@@ -1,4 +1,5 @@
-"""World-size-2 CPU tests (gloo) of the keyframe-sharded sliding_ba host logic.
+"""World-size-2 CPU tests (gloo) of the multi-GPU host logic: keyframe-sharded sliding_ba and
+view-sharded accumulate_uncertainty.
 
 The device path (`gsf_sliding_ba` with nranks > 1, csrc/abi.cu) renders only the keyframes
 `gsf_ba_partition` assigns to its rank, sums their bundles locally, all-reduces the flat gradient,
@@ -6,7 +7,8 @@ the loss and the per-keyframe pose gradients, then runs identical Adam updates o
 These tests replay exactly that decomposition with the fp64 oracle as the per-keyframe gradient
 (reference: track/tracker.cpp sliding_ba, the loop the oracle restates in orc_sliding_ba) and
 torch.distributed/gloo as the all-reduce, and check it against the unsharded sum.  They also cover
-the NCCL unique-id exchange `Context.comm_setup` performs.
+the NCCL unique-id exchange `Context.comm_setup` performs, and the (sum, count) all-reduce of the
+uncertainty pass.
 """
 import os
 import socket
@@ -95,6 +97,47 @@ def _worker(rank, world, port, n, out_dir):
                  uid_len=np.array(len(uid)))
     finally:
         dist.destroy_process_group()
+
+
+def _unc_window():
+    import oracle as orc
+    K = make_intrinsics(40, 30, 35.0)
+    m = orc.random_scene(123, 70, 1, 0.95, 0.05, 0.2)
+    poses = [perturbed(pose(), [0.01 * k, -0.01 * k, 0.005, 0.02 * k, 0.0, -0.01]) for k in range(5)]
+    depths = [orc.wavy_depth(40, 30, 2.0 + 0.1 * k) for k in range(5)]
+    renders = [orc.render(m, p, K, d) for p, d in zip(poses, depths)]
+    return orc, m, K, poses, depths, renders
+
+
+def _unc_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc, m, K, poses, depths, renders = _unc_window()
+        mine = [v for v in range(len(poses)) if v % world == rank]   # gsf_accumulate_uncertainty's split
+        s, c = orc.uncertainty_partials(m, [renders[v] for v in mine], [depths[v] for v in mine],
+                                        [poses[v] for v in mine], K)
+        ts, tc = torch.from_numpy(s.copy()), torch.from_numpy(c.astype(np.int64))
+        dist.all_reduce(ts)
+        dist.all_reduce(tc)
+        np.savez(os.path.join(out_dir, f"unc{rank}.npz"), s=ts.numpy(), c=tc.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_uncertainty_matches_unsharded(tmp_path):
+    """accumulate_uncertainty over a window split by view across two ranks (uncertainty.cpp:35-85):
+    the all-reduced (sum, count) partials give the single-process nu and observed flags."""
+    mp.spawn(_unc_worker, args=(WORLD, _free_port(), str(tmp_path)), nprocs=WORLD, join=True)
+    orc, m, K, poses, depths, renders = _unc_window()
+    observed = orc.accumulate_uncertainty(m, renders, depths, poses, K)
+    for r in range(WORLD):
+        z = np.load(tmp_path / f"unc{r}.npz")
+        seen = z["c"] > 0
+        assert int(seen.sum()) == observed > 0
+        assert (seen == (m.observed[: len(seen)] != 0)).all()
+        nu = np.where(seen, z["s"] / np.maximum(z["c"], 1), 0.0)
+        np.testing.assert_allclose(nu[seen], m.uncertainty[seen], rtol=1e-12, atol=1e-15)
 
 
 @pytest.mark.parametrize("n", [5, 1])
