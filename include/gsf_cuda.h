@@ -39,7 +39,8 @@ typedef enum {
   GSF_EDIVERGED = 3,     /* std::runtime_error("... diverged ...") */
   GSF_ECUDA = 4,         /* device / launch failure (no fallback exists) */
   GSF_EUNSUPPORTED = 5,  /* a runtime value the device path does not implement (e.g. tile_size != 16) */
-  GSF_ENOMEM = 6
+  GSF_ENOMEM = 6,
+  GSF_ERUNTIME = 7       /* any other std::runtime_error of the reference (e.g. an empty first frame) */
 } gsf_status;
 
 typedef struct gsf_ctx_s* gsf_ctx;
@@ -92,6 +93,8 @@ typedef struct {
   uint64_t seed;
   gsf_raster_cfg raster;
   gsf_loss_weights weights;
+  int32_t init_stride, spawn_stride;          /* pixel sampling strides of initialize / spawn */
+  double spawn_opacity_threshold, init_opacity;
 } gsf_mapper_cfg;
 
 /* Host view of a primitive list (std::vector<GaussianPrimitive>). */
@@ -258,6 +261,21 @@ int gsf_map_step(gsf_ctx ctx, const int32_t* slots, const gsf_pose* poses, int32
 int gsf_sliding_ba(gsf_ctx ctx, const int32_t* slots, gsf_pose* poses, const int32_t* frame_ids,
                    int32_t n, const gsf_intrinsics* K, const gsf_tracker_cfg* tcfg,
                    const gsf_mapper_cfg* mcfg, int32_t iterations, double* trace);
+
+/* initialize_map (map/mapper.hpp:84-87, mapper.cpp:125-148): replaces the context's map with
+ * one backprojected primitive per init_stride-sampled valid-depth pixel of frame `slot` seen from
+ * `pose` (row-major pixel order) and resets the optimizer state (a fresh MapState).  An empty
+ * frame fails with GSF_ERUNTIME ("cannot initialize a map: first frame has no usable depth"). */
+int gsf_initialize_map(gsf_ctx ctx, int32_t slot, const gsf_pose* pose, const gsf_intrinsics* K,
+                       const gsf_mapper_cfg* mcfg, int64_t* count);
+
+/* spawn_gaussians (map/mapper.hpp:89-93, mapper.cpp:150-170): appends one primitive per
+ * spawn_stride-sampled pixel of frame `slot` with valid depth where the most recent render on
+ * this context (the reference's `rendered` argument; same intrinsics) has accumulated opacity
+ * below spawn_opacity_threshold.  Adam moments and densify statistics of the new primitives
+ * start at zero. */
+int gsf_spawn_gaussians(gsf_ctx ctx, int32_t slot, const gsf_pose* pose, const gsf_intrinsics* K,
+                        const gsf_mapper_cfg* mcfg, int32_t* spawned);
 
 /* accumulate_uncertainty / prune_unreliable (map/uncertainty.hpp:33-39).  Each view is
  * rendered on the device from (slot depth, pose). */

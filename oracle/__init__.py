@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
                                    C.POINTER(Intrinsics), C.POINTER(MapperCfg), C.c_int, dp]),
         "orc_sliding_ba": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(dp), C.POINTER(dp), C.POINTER(Pose), i32p,
                                      C.POINTER(Intrinsics), C.POINTER(TrackerCfg), C.POINTER(MapperCfg), C.c_int, dp]),
+        "orc_backproject": (C.c_int, [dp, dp, dp, C.POINTER(Pose), C.POINTER(Intrinsics), C.POINTER(MapperCfg),
+                                      C.c_int, C.POINTER(MapHost), C.POINTER(C.c_int64)]),
         "orc_uncertainty_partials": (C.c_int, [C.POINTER(MapHost), C.c_int, C.POINTER(C.c_void_p), C.POINTER(dp),
                                                C.POINTER(Pose), C.POINTER(Intrinsics), dp, i32p]),
         "orc_accumulate_uncertainty": (C.c_int, [C.POINTER(MapHost), C.c_int, C.POINTER(C.c_void_p), C.POINTER(dp),
@@ -346,6 +348,21 @@ def accumulate_uncertainty(m, results, depths, poses, K):
     h = host_of(m)
     _check(lib().orc_accumulate_uncertainty(C.byref(h), n, rh, dg, ps, C.byref(K), C.byref(cnt)))
     return cnt.value
+
+
+def backproject(rgb, depth, pose: Pose, K, mcfg, stride, opacity=None):
+    """initialize_map / spawn_gaussians candidates (mapper.cpp:12-26, 125-170) as a new map."""
+    r = np.ascontiguousarray(rgb, dtype=np.float64)
+    d = np.ascontiguousarray(depth, dtype=np.float64)
+    o = None if opacity is None else np.ascontiguousarray(opacity, dtype=np.float64)
+    n = C.c_int64()
+    _check(lib().orc_backproject(r.ctypes.data_as(dp), d.ctypes.data_as(dp), None if o is None else o.ctypes.data_as(dp),
+                                 C.byref(pose), C.byref(K), C.byref(mcfg), stride, None, C.byref(n)))
+    m = empty_map(n.value, mcfg.sh_coeffs)
+    h = host_of(m)
+    _check(lib().orc_backproject(r.ctypes.data_as(dp), d.ctypes.data_as(dp), None if o is None else o.ctypes.data_as(dp),
+                                 C.byref(pose), C.byref(K), C.byref(mcfg), stride, C.byref(h), C.byref(n)))
+    return m
 
 
 def uncertainty_partials(m, results, depths, poses, K):

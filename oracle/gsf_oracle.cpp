@@ -1817,6 +1817,43 @@ int orc_sliding_ba(orc_mapstate* st, int n, const double* const* rgbs, const dou
   });
 }
 
+// mapper.cpp:12-26 (backprojected_primitive) over the loops of initialize_map (:125-148) and
+// spawn_gaussians (:150-170): stride-sampled pixels in row-major order, sensor_valid_mask
+// (losses.cpp:141-148), and for spawn rendered.opacity < spawn_opacity_threshold (opacity != NULL).
+// Writes the new primitives (capacity out->count) and their number.
+int orc_backproject(const double* rgb, const double* depth, const double* opacity, const gsf_pose* pose,
+                    const gsf_intrinsics* K, const gsf_mapper_cfg* cfg, int stride, gsf_map_host* out, int64_t* count) {
+  return guarded([&] {
+    const Pose ps = to_pose(pose);
+    const M3 rinv = exp_map(V3(-ps.rot[0], -ps.rot[1], -ps.rot[2]));     // pose.inverse(): exp(-rot)
+    const M3 rt = tr(ps.rotation());
+    const V3 tinv = -(mul(rt, ps.trans));                                 // -(R^T t)
+    const double kC0 = 0.28209479177387814;
+    std::vector<Prim> made;
+    for (int y = 0; y < K->height; y += stride)
+      for (int x = 0; x < K->width; x += stride) {
+        const size_t pi = static_cast<size_t>(y) * K->width + x;
+        const double d = depth[pi];
+        if (!(std::isfinite(d) && d > K->near_plane && d < K->far_plane)) continue;
+        if (opacity && opacity[pi] >= cfg->spawn_opacity_threshold) continue;
+        Prim p;
+        const V3 pc((x + 0.5 - K->cx) / K->fx * d, (y + 0.5 - K->cy) / K->fy * d, d);   // camera.hpp:33-35
+        p.mean = mul(rinv, pc) + tinv;
+        const double ls = std::log((d / K->fx) * stride * 0.5);
+        p.log_scale = V3(ls, ls, ls);
+        p.quat = V4(1, 0, 0, 0);
+        p.opacity_logit = std::log(cfg->init_opacity / (1.0 - cfg->init_opacity));
+        p.sh.assign(cfg->sh_coeffs, V3(0, 0, 0));
+        for (int c = 0; c < 3; ++c) p.sh[0][c] = (rgb[3 * pi + c] - 0.5) / kC0;
+        p.uncertainty = 0.0;
+        p.observed = true;
+        made.push_back(p);
+      }
+    *count = static_cast<int64_t>(made.size());
+    if (out && out->mean && static_cast<int64_t>(made.size()) <= out->count) store_map(made, out);
+  });
+}
+
 // uncertainty.cpp:35-73: per-view (sum, count) partials of Eq. 13 reduced in window order
 static void uncertainty_partials(const std::vector<Prim>& prims, int n, const orc_result* const* records,
                                  const double* const* depths, const gsf_pose* poses, const gsf_intrinsics* K,
@@ -2062,6 +2099,10 @@ void orc_default_mapper(gsf_mapper_cfg* c) {
   c->seed = 0;
   orc_default_raster(&c->raster);
   orc_default_weights(&c->weights, 0);
+  c->init_stride = 2;
+  c->spawn_stride = 2;
+  c->spawn_opacity_threshold = 0.5;
+  c->init_opacity = 0.5;
 }
 
 }  // extern "C"

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # GSF_LIB: an alternative in-tree build of the same library (kernel-variant A/B measurements)
 LIB_PATH = os.environ.get("GSF_LIB") or os.path.join(HERE, "libgsf_cuda.so")
 
-GSF_OK, GSF_EINVAL, GSF_ENONFINITE, GSF_EDIVERGED, GSF_ECUDA, GSF_EUNSUPPORTED, GSF_ENOMEM = range(7)
+GSF_OK, GSF_EINVAL, GSF_ENONFINITE, GSF_EDIVERGED, GSF_ECUDA, GSF_EUNSUPPORTED, GSF_ENOMEM, GSF_ERUNTIME = range(8)
 
 dp = C.POINTER(C.c_double)
 fp = C.POINTER(C.c_float)
@@ -61,7 +61,9 @@ class MapperCfg(C.Structure):
                 ("densify_grad_threshold", C.c_double), ("densify_split_factor", C.c_double),
                 ("densify_size_fraction", C.c_double), ("densify_cull_opacity", C.c_double),
                 ("uncertainty_tau", C.c_double), ("uncertainty_reduced_opacity", C.c_double),
-                ("seed", C.c_uint64), ("raster", RasterCfg), ("weights", LossWeights)]
+                ("seed", C.c_uint64), ("raster", RasterCfg), ("weights", LossWeights),
+                ("init_stride", C.c_int32), ("spawn_stride", C.c_int32),
+                ("spawn_opacity_threshold", C.c_double), ("init_opacity", C.c_double)]
 
 
 class MapHost(C.Structure):
@@ -142,6 +144,10 @@ SIGNATURES = {
     "gsf_sliding_ba": (C.c_int, [C.c_void_p, i32p, C.POINTER(Pose), i32p, C.c_int32,
                                  C.POINTER(Intrinsics), C.POINTER(TrackerCfg), C.POINTER(MapperCfg),
                                  C.c_int32, dp]),
+    "gsf_initialize_map": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Pose), C.POINTER(Intrinsics),
+                                     C.POINTER(MapperCfg), C.POINTER(C.c_int64)]),
+    "gsf_spawn_gaussians": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Pose), C.POINTER(Intrinsics),
+                                      C.POINTER(MapperCfg), C.POINTER(C.c_int32)]),
     "gsf_accumulate_uncertainty": (C.c_int, [C.c_void_p, i32p, C.POINTER(Pose), C.c_int32,
                                              C.POINTER(Intrinsics), C.POINTER(RasterCfg), i32p]),
     "gsf_prune_unreliable": (C.c_int, [C.c_void_p, C.c_double, C.c_double, i32p]),
@@ -204,4 +210,4 @@ def defaults_tracker() -> TrackerCfg:
 def defaults_mapper() -> MapperCfg:
     """MapperConfig defaults (map/mapper.hpp:21-41)."""
     return MapperCfg(1, 4.0, 1.6e-4, 2.5e-3, 5e-2, 5e-3, 1e-3, 100, 2e-4, 1.6, 0.01, 0.005, 0.025,
-                     0.005, 0, defaults_raster(), defaults_weights())
+                     0.005, 0, defaults_raster(), defaults_weights(), 2, 2, 0.5, 0.5)

@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import abi
-from .abi import (GSF_EDIVERGED, GSF_EINVAL, GSF_ENONFINITE, GSF_EUNSUPPORTED, GSF_OK, GsfError,
+from .abi import (GSF_EDIVERGED, GSF_EINVAL, GSF_ENONFINITE, GSF_ERUNTIME, GSF_EUNSUPPORTED, GSF_OK, GsfError,
                   Intrinsics, LossWeights, MapperCfg, Pose, RasterCfg, TrackerCfg)
 
 
@@ -143,7 +143,7 @@ def _raise(status: int, msg: str, index: int = -1):
         e = ValueError(msg)
         e.index = index
         raise e
-    if status == GSF_EDIVERGED:
+    if status in (GSF_EDIVERGED, GSF_ERUNTIME):
         raise RuntimeError(msg)
     if status == GSF_EUNSUPPORTED:
         raise NotImplementedError(msg)
@@ -355,6 +355,25 @@ class Context:
         cnt = C.c_int32()
         self._check(self.lib.gsf_accumulate_uncertainty(self.h, s, ps, n, C.byref(K), C.byref(raster), C.byref(cnt)))
         return cnt.value
+
+    def _sync_count(self, sh_coeffs: int):
+        self.P, self.K = int(self.lib.gsf_map_count(self.h)), sh_coeffs
+
+    def initialize_map(self, slot: int, pose: Pose, K: Intrinsics, mcfg: MapperCfg = None) -> int:
+        """initialize_map (mapper.cpp:125-148) from frame `slot`: replaces the map, resets the optimizer."""
+        mcfg = mcfg or abi.defaults_mapper()
+        n = C.c_int64()
+        self._check(self.lib.gsf_initialize_map(self.h, slot, C.byref(pose), C.byref(K), C.byref(mcfg), C.byref(n)))
+        self._sync_count(mcfg.sh_coeffs)
+        return n.value
+
+    def spawn_gaussians(self, slot: int, pose: Pose, K: Intrinsics, mcfg: MapperCfg = None) -> int:
+        """spawn_gaussians (mapper.cpp:150-170) against the most recent render on this context."""
+        mcfg = mcfg or abi.defaults_mapper()
+        n = C.c_int32()
+        self._check(self.lib.gsf_spawn_gaussians(self.h, slot, C.byref(pose), C.byref(K), C.byref(mcfg), C.byref(n)))
+        self._sync_count(mcfg.sh_coeffs)
+        return n.value
 
     def prune_unreliable(self, tau: float = 0.025, reduced_opacity: float = 0.005) -> int:
         r = C.c_int32()

@@ -35,6 +35,9 @@ struct ENonFinite : std::invalid_argument {
 struct EDiverged : std::runtime_error {
   explicit EDiverged(const std::string& s) : std::runtime_error(s) {}
 };
+struct ERuntime : std::runtime_error {
+  explicit ERuntime(const std::string& s) : std::runtime_error(s) {}
+};
 struct EUnsupported : std::runtime_error {
   explicit EUnsupported(const std::string& s) : std::runtime_error(s) {}
 };
@@ -142,6 +145,9 @@ struct gsf_ctx_s {
   gsf_intrinsics rK{};
   gsf_raster_cfg rcfg{};
   bool render_obs = false;
+  // initialize / spawn scratch (per-CTA candidate counts and offsets + total)
+  uint32_t* bp_scratch = nullptr;
+  int64_t bp_cap = 0;
   // captured track_frame graphs (small round-robin cache)
   TrackGraph track_graphs[8];
   int track_graph_next = 0;
@@ -438,6 +444,9 @@ int guard(gsf_ctx c, F&& f) {
   } catch (const EUnsupported& e) {
     c->err = e.what();
     return GSF_EUNSUPPORTED;
+  } catch (const ERuntime& e) {
+    c->err = e.what();
+    return GSF_ERUNTIME;
   } catch (const CudaError& e) {
     std::ostringstream m;
     m << "CUDA error " << cudaGetErrorName(e.code) << " (" << cudaGetErrorString(e.code) << ") at " << e.file << ":"
@@ -642,7 +651,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
                   ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.pj_id,
-                  ws.red_part, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
+                  ws.red_part, c->bp_scratch, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
                   c->red_f};
   for (void* p : bufs)
@@ -1483,6 +1492,153 @@ int gsf_sliding_ba(gsf_ctx c, const int32_t* slots, gsf_pose* poses, const int32
         poses[k].translation[a] = c->kf_host[k].trans[a];
       }
     if (trace && iterations > 0) GSF_CUDA_CHECK(cudaMemcpy(trace, c->trace_dev, sizeof(double) * iterations, cudaMemcpyDeviceToHost));
+  });
+}
+
+// MapperConfig::validate (mapper.cpp:28-45) for the fields the device path reads.
+static void check_mapper(const gsf_mapper_cfg& m) {
+  if (m.sh_coeffs != 1 && m.sh_coeffs != 4 && m.sh_coeffs != 9 && m.sh_coeffs != 16)
+    throw EInval("sh coefficient count must be 1, 4, 9 or 16");
+  if (m.init_stride < 1 || m.spawn_stride < 1) throw EInval("sampling strides must be at least 1");
+  if (!(m.spawn_opacity_threshold > 0.0 && m.spawn_opacity_threshold <= 1.0))
+    throw EInval("spawn opacity threshold must lie in (0, 1]");
+  if (!(m.init_opacity > 0.0 && m.init_opacity < 1.0)) throw EInval("initial opacity must lie in (0, 1)");
+  if (!(m.scene_extent > 0.0)) throw EInval("scene extent must be positive");
+  if (!(m.densify_split_factor > 1.0)) throw EInval("split factor must exceed 1");
+}
+
+// Candidate pass of initialize / spawn: count the accepted stride-sampled pixels (blocking).
+static uint32_t backproject_count(gsf_ctx_s* c, BackprojectArgs& a, const Frame& f, const gsf_pose& pose,
+                                  const gsf_intrinsics& K, const gsf_mapper_cfg& m, int stride, const float* opacity) {
+  a.depth = f.depth;
+  a.rgb = f.rgb;
+  a.opacity = opacity;
+  a.threshold = m.spawn_opacity_threshold;
+  a.fx = K.fx; a.fy = K.fy; a.cx = K.cx; a.cy = K.cy;
+  a.near_plane = K.near_plane;
+  a.far_plane = K.far_plane;
+  // pose.inverse() (pose.hpp:35-38): rotation exp(-rot), translation -(R^T t)
+  double R[9], nrot[3];
+  exp_map_d(pose.rotation_tangent, R);
+  for (int i = 0; i < 3; ++i) nrot[i] = -pose.rotation_tangent[i];
+  exp_map_d(nrot, a.Rinv);
+  for (int i = 0; i < 3; ++i)
+    a.tinv[i] = -(R[0 * 3 + i] * pose.translation[0] + R[1 * 3 + i] * pose.translation[1] + R[2 * 3 + i] * pose.translation[2]);
+  a.logit0 = std::log(m.init_opacity / (1.0 - m.init_opacity));
+  a.W = K.width;
+  a.H = K.height;
+  a.stride = stride;
+  a.K = m.sh_coeffs;
+  a.cells_x = (K.width + stride - 1) / stride;
+  a.cells = static_cast<int64_t>(a.cells_x) * ((K.height + stride - 1) / stride);
+  const int64_t blocks = std::max<int64_t>(1, div_up(a.cells, 256));
+  if (2 * blocks + 1 > c->bp_cap) {
+    dalloc(c->bp_scratch, 2 * blocks + 1);
+    c->bp_cap = 2 * blocks + 1;
+  }
+  run_backproject_count(a, c->bp_scratch, c->bp_scratch + blocks, c->bp_scratch + 2 * blocks, c->stream, &c->launches);
+  uint32_t total = 0;
+  GSF_CUDA_CHECK(cudaMemcpyAsync(&total, c->bp_scratch + 2 * blocks, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  return total;
+}
+
+// Re-lay the SoA map [field][P] out for P_new >= P primitives: parameters, Adam moments, nu,
+// observed and the densify statistics are kept; the new tail of the moments and statistics is
+// zero (AdamState::append, MapState resize).
+static void grow_map_soa(gsf_ctx_s* c, int64_t P_new) {
+  const int64_t P_old = c->P;
+  const int D = c->D;
+  float *params = nullptr, *m = nullptr, *v = nullptr, *nu = nullptr, *acc = nullptr;
+  uint8_t* obs = nullptr;
+  int32_t* cnt = nullptr;
+  dalloc(params, static_cast<size_t>(P_new) * D);
+  dalloc(m, static_cast<size_t>(P_new) * D);
+  dalloc(v, static_cast<size_t>(P_new) * D);
+  dalloc(nu, P_new);
+  dalloc(obs, P_new);
+  dalloc(acc, P_new);
+  dalloc(cnt, P_new);
+  const size_t wb = sizeof(float) * static_cast<size_t>(P_new), ob = sizeof(float) * static_cast<size_t>(P_old);
+  GSF_CUDA_CHECK(cudaMemset2DAsync(m, wb, 0, wb, D, c->stream));
+  GSF_CUDA_CHECK(cudaMemset2DAsync(v, wb, 0, wb, D, c->stream));
+  GSF_CUDA_CHECK(cudaMemsetAsync(acc, 0, wb, c->stream));
+  GSF_CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * P_new, c->stream));
+  if (P_old > 0) {
+    GSF_CUDA_CHECK(cudaMemcpy2DAsync(params, wb, c->params, ob, ob, D, cudaMemcpyDeviceToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpy2DAsync(m, wb, c->adam_m, ob, ob, D, cudaMemcpyDeviceToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpy2DAsync(v, wb, c->adam_v, ob, ob, D, cudaMemcpyDeviceToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(nu, c->nu, ob, cudaMemcpyDeviceToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(obs, c->observed, P_old, cudaMemcpyDeviceToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(acc, c->grad_accum, ob, cudaMemcpyDeviceToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(cnt, c->grad_count, sizeof(int32_t) * P_old, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  sync(c);
+  dfree(c->params); dfree(c->adam_m); dfree(c->adam_v); dfree(c->nu); dfree(c->observed); dfree(c->grad_accum);
+  dfree(c->grad_count);
+  c->params = params; c->adam_m = m; c->adam_v = v; c->nu = nu; c->observed = obs; c->grad_accum = acc;
+  c->grad_count = cnt;
+  dalloc(c->grads, static_cast<size_t>(P_new) * D);
+  dalloc(c->d_mean2d, 2 * static_cast<size_t>(P_new));
+  c->map_cap = P_new;
+  c->P = P_new;
+  ++c->map_gen;
+}
+
+int gsf_initialize_map(gsf_ctx c, int32_t slot, const gsf_pose* pose, const gsf_intrinsics* K, const gsf_mapper_cfg* mcfg,
+                       int64_t* count) {
+  return guard(c, [&] {
+    check_mapper(*mcfg);
+    check_intrinsics(*K);
+    if (slot < 0 || slot >= static_cast<int>(c->frames.size()) || !c->frames[slot].rgb ||
+        c->frames[slot].w != K->width || c->frames[slot].h != K->height)
+      throw EInval("first frame dimensions do not match the intrinsics");
+    const Frame& f = c->frames[slot];
+    BackprojectArgs a;
+    const uint32_t total = backproject_count(c, a, f, *pose, *K, *mcfg, mcfg->init_stride, nullptr);
+    if (total == 0) throw ERuntime("cannot initialize a map: first frame has no usable depth");
+    // a fresh MapState: the new primitives only, zero optimizer state and statistics
+    c->P = 0;
+    c->K = mcfg->sh_coeffs;
+    c->D = kFieldsBase + 3 * c->K;
+    grow_map_soa(c, total);
+    run_backproject_write(a, c->bp_scratch + std::max<int64_t>(1, div_up(a.cells, 256)), 0, total, c->params, c->nu,
+                          c->observed, c->stream, &c->launches);
+    sync(c);
+    c->adam_step = 0.0;
+    c->map_iteration = 0;
+    c->have_render = false;
+    *count = total;
+  });
+}
+
+int gsf_spawn_gaussians(gsf_ctx c, int32_t slot, const gsf_pose* pose, const gsf_intrinsics* K, const gsf_mapper_cfg* mcfg,
+                        int32_t* spawned) {
+  return guard(c, [&] {
+    check_mapper(*mcfg);
+    check_intrinsics(*K);
+    *spawned = 0;
+    if (!c->have_render || c->rK.width != K->width || c->rK.height != K->height)
+      throw EInval("spawn render dimensions do not match the intrinsics");
+    if (c->P > 0 && c->K != mcfg->sh_coeffs) throw EInval("spawn: sh coefficient count differs from the map's");
+    if (slot < 0 || slot >= static_cast<int>(c->frames.size()) || !c->frames[slot].rgb ||
+        c->frames[slot].w != K->width || c->frames[slot].h != K->height)
+      throw EInval("spawn frame dimensions do not match the intrinsics");
+    const Frame& f = c->frames[slot];
+    BackprojectArgs a;
+    const uint32_t total = backproject_count(c, a, f, *pose, *K, *mcfg, mcfg->spawn_stride, c->ws.opacity);
+    if (total == 0) return;
+    const int64_t P_old = c->P;
+    if (P_old == 0) {
+      c->K = mcfg->sh_coeffs;
+      c->D = kFieldsBase + 3 * c->K;
+    }
+    grow_map_soa(c, P_old + total);
+    run_backproject_write(a, c->bp_scratch + std::max<int64_t>(1, div_up(a.cells, 256)), P_old, P_old + total, c->params,
+                          c->nu, c->observed, c->stream, &c->launches);
+    sync(c);
+    c->have_render = false;   // the render no longer describes this map
+    *spawned = static_cast<int32_t>(total);
   });
 }
 

@@ -183,6 +183,24 @@ void run_track_update(DevState* ds, int iteration, cudaStream_t st, int64_t* lau
 void run_densify_stats(const uint8_t* visible, const float* d_mean2d, float* accum, int32_t* cnt, int64_t P, int W,
                        int H, cudaStream_t st, int64_t* launches);
 
+// spawn.cu: initialize_map / spawn_gaussians candidates (one per stride-sampled pixel)
+struct BackprojectArgs {
+  const float* depth;     // sensor depth of the frame (W*H)
+  const float* rgb;       // frame colour, interleaved (3*W*H)
+  const float* opacity;   // current render's accumulated opacity (spawn) or nullptr (initialize)
+  double threshold;       // spawn_opacity_threshold
+  double fx, fy, cx, cy, near_plane, far_plane;
+  double Rinv[9], tinv[3];   // pose.inverse(): exp(-rot), -(R^T t)
+  double logit0;          // logit(init_opacity)
+  int W, H, stride, K;
+  int cells_x;
+  int64_t cells;
+};
+int64_t run_backproject_count(const BackprojectArgs& a, uint32_t* blk_cnt, uint32_t* blk_off, uint32_t* total,
+                              cudaStream_t st, int64_t* launches);
+void run_backproject_write(const BackprojectArgs& a, const uint32_t* blk_off, int64_t P_old, int64_t P_new, float* params,
+                           float* nu, uint8_t* observed, cudaStream_t st, int64_t* launches);
+
 // uncert.cu
 void run_uncertainty_view(const Workspace& ws, const float* params, int64_t P, const float* obs, int W, int H,
                           double near_plane, double far_plane, const DevState* ds, double* sum, uint32_t* cnt,

@@ -431,3 +431,62 @@ def test_uncertainty_kats_on_gpu(gpu_ctx, orc):
     d = gpu_ctx.download()
     assert 1 / (1 + math.exp(-d.opacity_logit[0])) == pytest.approx(0.005, rel=1e-5)
     assert gpu_ctx.prune_unreliable() == 0
+
+
+def _frame_of(orc, m, p, K, hole_every=13):
+    r = orc.render(m, p, K)
+    depth = np.where(r.opacity > 0.3, r.alpha_depth, 0.0).astype(np.float32)
+    depth.ravel()[::hole_every] = 0.0
+    return r.color.astype(np.float32), depth
+
+
+def test_initialize_map_matches_oracle(gpu_ctx, orc):
+    """initialize_map (mapper.cpp:125-148) on the device vs the fp64 restatement, same frame."""
+    m = orc.random_scene(321, 120)
+    K = make_intrinsics(64, 48, 50.0)
+    p = pose([0.02, -0.01, 0.03], [0.05, -0.02, 0.1])
+    rgb, depth = _frame_of(orc, m, p, K)
+    gpu_ctx.frame_upload(0, rgb, depth, 64, 48)
+    mc = defaults_mapper()
+    for stride in (1, 2, 3):
+        mc.init_stride = stride
+        n = gpu_ctx.initialize_map(0, p, K, mc)
+        ref = orc.backproject(rgb, depth, p, K, mc, stride)
+        assert n == ref.mean.shape[0] > 0, stride
+        g = gpu_ctx.download()
+        assert np.abs(g.mean - ref.mean).max() < 2e-6
+        assert np.abs(g.log_scale - ref.log_scale).max() < 2e-6
+        assert (g.quat == [1, 0, 0, 0]).all() and np.allclose(g.opacity_logit, ref.opacity_logit, atol=1e-7)
+        assert np.abs(g.sh - ref.sh.reshape(g.sh.shape)).max() < 2e-6
+    with pytest.raises(RuntimeError, match="no usable depth"):
+        gpu_ctx.frame_upload(1, rgb, np.zeros_like(depth), 64, 48)
+        gpu_ctx.initialize_map(1, p, K, mc)
+
+
+def test_spawn_gaussians_matches_oracle(gpu_ctx, orc):
+    """spawn_gaussians (mapper.cpp:150-170): thin pixels of the current render get new primitives;
+    the existing map is untouched and the new ones follow in row-major pixel order."""
+    truth = orc.random_scene(654, 150)
+    K = make_intrinsics(64, 48, 50.0)
+    p0, p1 = pose(), pose([0.0, 0.15, 0.0], [0.2, 0.0, 0.0])
+    rgb0, d0 = _frame_of(orc, truth, p0, K)
+    rgb1, d1 = _frame_of(orc, truth, p1, K)
+    gpu_ctx.frame_upload(0, rgb0, d0, 64, 48)
+    gpu_ctx.frame_upload(1, rgb1, d1, 64, 48)
+    mc = defaults_mapper()
+    mc.init_stride = 4
+    n0 = gpu_ctx.initialize_map(0, p0, K, mc)
+    before = gpu_ctx.download()
+    r = gpu_ctx.render(p1, K)
+    spawned = gpu_ctx.spawn_gaussians(1, p1, K, mc)
+    ref = orc.backproject(rgb1, d1, p1, K, mc, mc.spawn_stride, opacity=r.opacity.astype(np.float64))
+    assert spawned == ref.mean.shape[0] > 0
+    after = gpu_ctx.download()
+    assert after.mean.shape[0] == n0 + spawned
+    assert np.array_equal(after.mean[:n0], before.mean[:n0]) and np.array_equal(after.sh[:n0], before.sh[:n0])
+    assert np.abs(after.mean[n0:] - ref.mean).max() < 2e-6
+    assert np.abs(after.sh[n0:] - ref.sh.reshape(after.sh[n0:].shape)).max() < 2e-6
+    # the grown map renders and steps
+    mc.densify_interval = 0
+    gpu_ctx.render(p1, K)
+    gpu_ctx.map_step([1], [p1], K, mc, 3)

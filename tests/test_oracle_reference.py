@@ -327,3 +327,46 @@ def test_map_step_reduces_loss(orc):
     st = orc.MapState(pert, mc)
     trace = st.map_step([(gt.color.copy(), obs)], [pose()], K, mc, 60)
     assert trace[-1] < 0.7 * trace[0]
+
+
+def _tiny_camera(w, h):
+    """test_map.cpp:17-27"""
+    from paper_2403_16095_b200 import api
+    return api.intrinsics(10.0, 10.0, 0.5 * w, 0.5 * h, w, h, near_plane=0.1, far_plane=100.0)
+
+
+def test_backproject_initialize_kats(orc):
+    """test_map.cpp:246-283 (initialize_map): stride sampling, footprint scale, colour decode, axis pixel."""
+    from paper_2403_16095_b200.abi import defaults_mapper
+    mc = defaults_mapper()
+    K = _tiny_camera(4, 4)
+    rgb = np.tile(np.array([0.2, 0.4, 0.6]), (4, 4, 1))
+    depth = np.full((4, 4), 2.0)
+    assert orc.backproject(rgb, depth, pose(), K, mc, 1).mean.shape[0] == 16
+    half = orc.backproject(rgb, depth, pose(), K, mc, 2)
+    assert half.mean.shape[0] == 4
+    assert half.log_scale[0, 0] == pytest.approx(math.log((2.0 / 10.0) * 2 * 0.5))
+    assert half.sh[0, 0, 0] * 0.28209479177387814 + 0.5 == pytest.approx(0.2, rel=1e-12)
+    assert 1.0 / (1.0 + math.exp(-half.opacity_logit[0])) == pytest.approx(0.5)
+    K3 = _tiny_camera(3, 3)
+    d3 = np.zeros((3, 3))
+    d3[1, 1] = 2.0
+    one = orc.backproject(np.full((3, 3, 3), 0.5), d3, pose(), K3, mc, 1)
+    assert one.mean.shape[0] == 1 and np.linalg.norm(one.mean[0] - [0, 0, 2]) < 1e-12
+    assert orc.backproject(np.full((3, 3, 3), 0.5), np.zeros((3, 3)), pose(), K3, mc, 1).mean.shape[0] == 0
+
+
+def test_backproject_spawn_kats(orc):
+    """test_map.cpp:285-315 (spawn_gaussians): thin pixels with valid depth only."""
+    from paper_2403_16095_b200.abi import defaults_mapper
+    mc = defaults_mapper()
+    K = _tiny_camera(4, 3)
+    rgb = np.full((3, 4, 3), 0.3)
+    depth = np.full((3, 4), 1.5)
+    assert orc.backproject(rgb, depth, pose(), K, mc, 1, opacity=np.ones((3, 4))).mean.shape[0] == 0
+    depth[1, 2] = 0.0
+    spawned = orc.backproject(rgb, depth, pose(), K, mc, 1, opacity=np.zeros((3, 4)))
+    assert spawned.mean.shape[0] == 11 and np.allclose(spawned.mean[:, 2], 1.5)
+    partial = np.full((3, 4), 0.8)
+    partial[1, 1] = 0.4
+    assert orc.backproject(rgb, np.full((3, 4), 1.5), pose(), K, mc, 1, opacity=partial).mean.shape[0] == 1
