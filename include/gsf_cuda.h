@@ -277,6 +277,24 @@ int gsf_initialize_map(gsf_ctx ctx, int32_t slot, const gsf_pose* pose, const gs
 int gsf_spawn_gaussians(gsf_ctx ctx, int32_t slot, const gsf_pose* pose, const gsf_intrinsics* K,
                         const gsf_mapper_cfg* mcfg, int32_t* spawned);
 
+/* StructuralChange (map/mapper.hpp:66-70). */
+typedef struct {
+  int32_t split, cloned, removed;
+} gsf_structural_change;
+
+/* densify_and_cull (map/mapper.hpp:96-98, mapper.cpp:172-230) on the context's map and its
+ * densification statistics: decisions on the device, the split offsets drawn on the host from the
+ * map state's std::mt19937_64 (seeded with mcfg->seed the first time after the map state was
+ * created: gsf_map_upload, gsf_initialize_map or gsf_optimizer_reset), one std::normal_distribution
+ * per split parent, exactly as the reference.  gsf_map_step runs it every densify_interval
+ * mapping iterations. */
+int gsf_densify_and_cull(gsf_ctx ctx, const gsf_mapper_cfg* mcfg, gsf_structural_change* out);
+
+/* MapState::grad_accum / grad_count (map/mapper.hpp:76-77): the densification statistics of the
+ * context's map (count entries each). */
+int gsf_map_stats_upload(gsf_ctx ctx, const double* grad_accum, const int32_t* grad_count);
+int gsf_map_stats_download(gsf_ctx ctx, double* grad_accum, int32_t* grad_count);
+
 /* accumulate_uncertainty / prune_unreliable (map/uncertainty.hpp:33-39).  Each view is
  * rendered on the device from (slot depth, pose). */
 int gsf_accumulate_uncertainty(gsf_ctx ctx, const int32_t* slots, const gsf_pose* poses,

@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
                                    C.POINTER(Intrinsics), C.POINTER(MapperCfg), C.c_int, dp]),
         "orc_sliding_ba": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(dp), C.POINTER(dp), C.POINTER(Pose), i32p,
                                      C.POINTER(Intrinsics), C.POINTER(TrackerCfg), C.POINTER(MapperCfg), C.c_int, dp]),
+        "orc_mapstate_set_stats": (C.c_int, [C.c_void_p, dp, i32p]),
+        "orc_mapstate_densify": (C.c_int, [C.c_void_p, C.POINTER(MapperCfg), i32p]),
         "orc_backproject": (C.c_int, [dp, dp, dp, C.POINTER(Pose), C.POINTER(Intrinsics), C.POINTER(MapperCfg),
                                       C.c_int, C.POINTER(MapHost), C.POINTER(C.c_int64)]),
         "orc_uncertainty_partials": (C.c_int, [C.POINTER(MapHost), C.c_int, C.POINTER(C.c_void_p), C.POINTER(dp),
@@ -331,6 +333,17 @@ class MapState:
         _check(lib().orc_sliding_ba(self.h, n, rg, dg, ps, fid, C.byref(K), C.byref(tcfg), C.byref(mcfg), iterations,
                                     trace.ctypes.data_as(dp)))
         return trace[:iterations], [ps[i] for i in range(n)]
+
+    def set_stats(self, accum, count):
+        a = np.ascontiguousarray(accum, dtype=np.float64)
+        c = np.ascontiguousarray(count, dtype=np.int32)
+        _check(lib().orc_mapstate_set_stats(self.h, a.ctypes.data_as(dp), c.ctypes.data_as(i32p)))
+
+    def densify(self, mcfg):
+        """densify_and_cull (mapper.cpp:172-230): (split, cloned, removed)."""
+        ch = np.zeros(3, np.int32)
+        _check(lib().orc_mapstate_densify(self.h, C.byref(mcfg), ch.ctypes.data_as(i32p)))
+        return tuple(int(x) for x in ch)
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -1480,8 +1480,12 @@ uint64_t fingerprint_record(const Record& rec, double alpha_clamp) {
   return h;
 }
 
+struct DensifyCounts {
+  int split, cloned, removed;
+};
+
 // mapper.cpp:172-230
-void densify_and_cull(orc_mapstate& st, const gsf_mapper_cfg& cfg) {
+DensifyCounts densify_and_cull(orc_mapstate& st, const gsf_mapper_cfg& cfg) {
   const size_t n = st.prims.size();
   const double size_boundary = cfg.densify_size_fraction * cfg.scene_extent;
   std::vector<uint8_t> keep(n, 1);
@@ -1517,7 +1521,7 @@ void densify_and_cull(orc_mapstate& st, const gsf_mapper_cfg& cfg) {
   if (removed == 0 && split == 0 && cloned == 0) {
     st.grad_accum.assign(n, 0.0);
     st.grad_count.assign(n, 0);
-    return;
+    return DensifyCounts{0, 0, 0};
   }
   std::vector<Prim> next;
   for (size_t i = 0; i < n; ++i)
@@ -1528,6 +1532,7 @@ void densify_and_cull(orc_mapstate& st, const gsf_mapper_cfg& cfg) {
   st.prims = std::move(next);
   st.grad_accum.assign(st.prims.size(), 0.0);
   st.grad_count.assign(st.prims.size(), 0);
+  return DensifyCounts{split, cloned, removed};
 }
 
 }  // namespace
@@ -1851,6 +1856,23 @@ int orc_backproject(const double* rgb, const double* depth, const double* opacit
       }
     *count = static_cast<int64_t>(made.size());
     if (out && out->mean && static_cast<int64_t>(made.size()) <= out->count) store_map(made, out);
+  });
+}
+
+int orc_mapstate_set_stats(orc_mapstate* st, const double* accum, const int32_t* count) {
+  return guarded([&] {
+    for (size_t i = 0; i < st->prims.size(); ++i) { st->grad_accum[i] = accum[i]; st->grad_count[i] = count[i]; }
+  });
+}
+
+int orc_mapstate_densify(orc_mapstate* st, const gsf_mapper_cfg* cfg, int32_t* change /*split, cloned, removed*/) {
+  return guarded([&] {
+    const size_t before = st->prims.size();
+    (void)before;
+    const DensifyCounts c = densify_and_cull(*st, *cfg);
+    change[0] = c.split;
+    change[1] = c.cloned;
+    change[2] = c.removed;
   });
 }
 

@@ -92,6 +92,8 @@ int orc_sliding_ba(orc_mapstate* s, int n, const double* const* rgbs, const doub
 
 /* accumulate_uncertainty / prune_unreliable (uncertainty.cpp:17-100).  The map's
  * uncertainty/observed arrays are updated in place. */
+int orc_mapstate_set_stats(orc_mapstate* st, const double* accum, const int32_t* count);
+int orc_mapstate_densify(orc_mapstate* st, const gsf_mapper_cfg* cfg, int32_t* change);
 int orc_backproject(const double* rgb, const double* depth, const double* opacity, const gsf_pose* pose,
                     const gsf_intrinsics* K, const gsf_mapper_cfg* cfg, int stride, gsf_map_host* out, int64_t* count);
 int orc_uncertainty_partials(const gsf_map_host* map, int n, const orc_result* const* records,

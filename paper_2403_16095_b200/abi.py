@@ -66,6 +66,10 @@ class MapperCfg(C.Structure):
                 ("spawn_opacity_threshold", C.c_double), ("init_opacity", C.c_double)]
 
 
+class StructuralChange(C.Structure):
+    _fields_ = [("split", C.c_int32), ("cloned", C.c_int32), ("removed", C.c_int32)]
+
+
 class MapHost(C.Structure):
     _fields_ = [("count", C.c_int64), ("sh_coeffs", C.c_int32), ("mean", dp), ("log_scale", dp),
                 ("quat", dp), ("opacity_logit", dp), ("sh", dp), ("uncertainty", dp),
@@ -148,6 +152,9 @@ SIGNATURES = {
                                      C.POINTER(MapperCfg), C.POINTER(C.c_int64)]),
     "gsf_spawn_gaussians": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Pose), C.POINTER(Intrinsics),
                                       C.POINTER(MapperCfg), C.POINTER(C.c_int32)]),
+    "gsf_densify_and_cull": (C.c_int, [C.c_void_p, C.POINTER(MapperCfg), C.POINTER(StructuralChange)]),
+    "gsf_map_stats_upload": (C.c_int, [C.c_void_p, dp, i32p]),
+    "gsf_map_stats_download": (C.c_int, [C.c_void_p, dp, i32p]),
     "gsf_accumulate_uncertainty": (C.c_int, [C.c_void_p, i32p, C.POINTER(Pose), C.c_int32,
                                              C.POINTER(Intrinsics), C.POINTER(RasterCfg), i32p]),
     "gsf_prune_unreliable": (C.c_int, [C.c_void_p, C.c_double, C.c_double, i32p]),

@@ -331,6 +331,7 @@ class Context:
         trace = np.zeros(max(iterations, 1), np.float64)
         self._check(self.lib.gsf_map_step(self.h, s, ps, n, C.byref(K), C.byref(mcfg), iterations,
                                           trace.ctypes.data_as(C.POINTER(C.c_double))))
+        self._sync_count(self.K)   # densify_and_cull may have resized the map
         return trace[:iterations]
 
     def sliding_ba(self, slots: Sequence[int], poses: Sequence[Pose], frame_ids: Sequence[int], K: Intrinsics,
@@ -374,6 +375,29 @@ class Context:
         self._check(self.lib.gsf_spawn_gaussians(self.h, slot, C.byref(pose), C.byref(K), C.byref(mcfg), C.byref(n)))
         self._sync_count(mcfg.sh_coeffs)
         return n.value
+
+    def densify_and_cull(self, mcfg: MapperCfg = None):
+        """densify_and_cull (mapper.cpp:172-230): returns (split, cloned, removed)."""
+        mcfg = mcfg or abi.defaults_mapper()
+        ch = abi.StructuralChange()
+        self._check(self.lib.gsf_densify_and_cull(self.h, C.byref(mcfg), C.byref(ch)))
+        self._sync_count(self.K)
+        return ch.split, ch.cloned, ch.removed
+
+    def map_stats(self):
+        """(grad_accum, grad_count) densification statistics of the map (MapState, mapper.hpp:76-77)."""
+        a = np.zeros(max(self.P, 1))
+        c = np.zeros(max(self.P, 1), np.int32)
+        self._check(self.lib.gsf_map_stats_download(self.h, a.ctypes.data_as(C.POINTER(C.c_double)),
+                                                    c.ctypes.data_as(C.POINTER(C.c_int32))))
+        return a[: self.P], c[: self.P]
+
+    def set_map_stats(self, grad_accum, grad_count):
+        a = np.ascontiguousarray(grad_accum, dtype=np.float64)
+        c = np.ascontiguousarray(grad_count, dtype=np.int32)
+        assert a.size == self.P and c.size == self.P
+        self._check(self.lib.gsf_map_stats_upload(self.h, a.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  c.ctypes.data_as(C.POINTER(C.c_int32))))
 
     def prune_unreliable(self, tau: float = 0.025, reduced_opacity: float = 0.005) -> int:
         r = C.c_int32()

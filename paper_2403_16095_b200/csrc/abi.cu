@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <random>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -122,8 +123,10 @@ struct gsf_ctx_s {
   float* nu = nullptr;
   uint8_t* observed = nullptr;
   float* d_mean2d = nullptr;
-  float* grad_accum = nullptr;
+  double* grad_accum = nullptr;   // MapState::grad_accum (fp64 like the reference)
   int32_t* grad_count = nullptr;
+  std::mt19937_64 rng;            // MapState::rng, seeded with the mapper seed at the first densify
+  bool rng_seeded = false;
   int64_t map_iteration = 0;
   // device workspace + scalars
   Workspace ws;
@@ -710,10 +713,11 @@ int gsf_map_upload(gsf_ctx c, const gsf_map_host* m) {
       GSF_CUDA_CHECK(cudaMemcpy(c->observed, ob.data(), P, cudaMemcpyHostToDevice));
       GSF_CUDA_CHECK(cudaMemset(c->adam_m, 0, sizeof(float) * P * D));
       GSF_CUDA_CHECK(cudaMemset(c->adam_v, 0, sizeof(float) * P * D));
-      GSF_CUDA_CHECK(cudaMemset(c->grad_accum, 0, sizeof(float) * P));
+      GSF_CUDA_CHECK(cudaMemset(c->grad_accum, 0, sizeof(double) * P));
       GSF_CUDA_CHECK(cudaMemset(c->grad_count, 0, sizeof(int32_t) * P));
     }
     c->adam_step = 0.0;
+    c->rng_seeded = false;   // a fresh MapState: its rng restarts from the mapper seed
     c->map_iteration = 0;
     ++c->map_gen;
     c->have_render = false;
@@ -794,10 +798,11 @@ int gsf_optimizer_reset(gsf_ctx c) {
     if (c->P > 0) {
       GSF_CUDA_CHECK(cudaMemsetAsync(c->adam_m, 0, sizeof(float) * c->P * c->D, c->stream));
       GSF_CUDA_CHECK(cudaMemsetAsync(c->adam_v, 0, sizeof(float) * c->P * c->D, c->stream));
-      GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_accum, 0, sizeof(float) * c->P, c->stream));
+      GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_accum, 0, sizeof(double) * c->P, c->stream));
       GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_count, 0, sizeof(int32_t) * c->P, c->stream));
     }
     c->adam_step = 0.0;
+    c->rng_seeded = false;   // a fresh MapState: its rng restarts from the mapper seed
     c->map_iteration = 0;
     sync(c);
   });
@@ -1329,6 +1334,9 @@ static void upload_kf(gsf_ctx_s* c, const gsf_pose* poses, int n) {
   GSF_CUDA_CHECK(cudaMemcpyAsync(c->kf, c->kf_host, sizeof(KfPose) * n, cudaMemcpyHostToDevice, c->stream));
 }
 
+static void check_mapper(const gsf_mapper_cfg& m);
+static gsf_structural_change densify_and_cull(gsf_ctx_s* c, const gsf_mapper_cfg& m);
+
 int gsf_map_step(gsf_ctx c, const int32_t* slots, const gsf_pose* poses, int32_t n, const gsf_intrinsics* K,
                  const gsf_mapper_cfg* m, int32_t iterations, double* trace) {
   return guard(c, [&] {
@@ -1343,12 +1351,7 @@ int gsf_map_step(gsf_ctx c, const int32_t* slots, const gsf_pose* poses, int32_t
       fr[i] = &get_frame(c, slots[i], *K);
     }
     if (iterations <= 0) return;
-    if (m->densify_interval > 0) {
-      const int64_t first = (c->map_iteration / m->densify_interval + 1) * m->densify_interval;
-      if (first <= c->map_iteration + iterations)
-        throw EUnsupported("map_step: densify_and_cull would run at mapping iteration " + std::to_string(first) +
-                           "; structural map edits are not implemented on the device path");
-    }
+    check_mapper(*m);
     ensure_ws(c, K->width, K->height);
     ensure_trace(c, iterations);
     const Cam cam = host_cam(poses[0], *K);
@@ -1365,6 +1368,16 @@ int gsf_map_step(gsf_ctx c, const int32_t* slots, const gsf_pose* poses, int32_t
       run_densify_stats(c->ws.visible, c->d_mean2d, c->grad_accum, c->grad_count, c->P, K->width, K->height, c->stream, &c->launches);
       c->adam_step += 1.0;
       run_adam(c->params, c->grads, c->adam_m, c->adam_v, c->P, c->D, g, c->adam_step, c->stream, &c->launches);
+      // densify_and_cull every `interval` mapping iterations (mapper.cpp:278-279)
+      const int64_t done = c->map_iteration + it + 1;
+      if (m->densify_interval > 0 && done % m->densify_interval == 0) {
+        read_state(c);
+        if (c->ds_host->halt || c->ds_host->overflow ||
+            c->ds_host->bad_index != std::numeric_limits<int32_t>::max())
+          break;   // reported below
+        densify_and_cull(c, *m);
+        ensure_ws(c, K->width, K->height);
+      }
     }
     read_state(c);
     const DevState& h = *c->ds_host;
@@ -1549,7 +1562,8 @@ static uint32_t backproject_count(gsf_ctx_s* c, BackprojectArgs& a, const Frame&
 static void grow_map_soa(gsf_ctx_s* c, int64_t P_new) {
   const int64_t P_old = c->P;
   const int D = c->D;
-  float *params = nullptr, *m = nullptr, *v = nullptr, *nu = nullptr, *acc = nullptr;
+  float *params = nullptr, *m = nullptr, *v = nullptr, *nu = nullptr;
+  double* acc = nullptr;
   uint8_t* obs = nullptr;
   int32_t* cnt = nullptr;
   dalloc(params, static_cast<size_t>(P_new) * D);
@@ -1562,7 +1576,7 @@ static void grow_map_soa(gsf_ctx_s* c, int64_t P_new) {
   const size_t wb = sizeof(float) * static_cast<size_t>(P_new), ob = sizeof(float) * static_cast<size_t>(P_old);
   GSF_CUDA_CHECK(cudaMemset2DAsync(m, wb, 0, wb, D, c->stream));
   GSF_CUDA_CHECK(cudaMemset2DAsync(v, wb, 0, wb, D, c->stream));
-  GSF_CUDA_CHECK(cudaMemsetAsync(acc, 0, wb, c->stream));
+  GSF_CUDA_CHECK(cudaMemsetAsync(acc, 0, sizeof(double) * P_new, c->stream));
   GSF_CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * P_new, c->stream));
   if (P_old > 0) {
     GSF_CUDA_CHECK(cudaMemcpy2DAsync(params, wb, c->params, ob, ob, D, cudaMemcpyDeviceToDevice, c->stream));
@@ -1570,7 +1584,7 @@ static void grow_map_soa(gsf_ctx_s* c, int64_t P_new) {
     GSF_CUDA_CHECK(cudaMemcpy2DAsync(v, wb, c->adam_v, ob, ob, D, cudaMemcpyDeviceToDevice, c->stream));
     GSF_CUDA_CHECK(cudaMemcpyAsync(nu, c->nu, ob, cudaMemcpyDeviceToDevice, c->stream));
     GSF_CUDA_CHECK(cudaMemcpyAsync(obs, c->observed, P_old, cudaMemcpyDeviceToDevice, c->stream));
-    GSF_CUDA_CHECK(cudaMemcpyAsync(acc, c->grad_accum, ob, cudaMemcpyDeviceToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(acc, c->grad_accum, sizeof(double) * P_old, cudaMemcpyDeviceToDevice, c->stream));
     GSF_CUDA_CHECK(cudaMemcpyAsync(cnt, c->grad_count, sizeof(int32_t) * P_old, cudaMemcpyDeviceToDevice, c->stream));
   }
   sync(c);
@@ -1606,6 +1620,7 @@ int gsf_initialize_map(gsf_ctx c, int32_t slot, const gsf_pose* pose, const gsf_
                           c->observed, c->stream, &c->launches);
     sync(c);
     c->adam_step = 0.0;
+    c->rng_seeded = false;   // a fresh MapState: its rng restarts from the mapper seed
     c->map_iteration = 0;
     c->have_render = false;
     *count = total;
@@ -1639,6 +1654,149 @@ int gsf_spawn_gaussians(gsf_ctx c, int32_t slot, const gsf_pose* pose, const gsf
     sync(c);
     c->have_render = false;   // the render no longer describes this map
     *spawned = static_cast<int32_t>(total);
+  });
+}
+
+// densify_and_cull (mapper.cpp:172-230) on the context's map: the per-primitive decisions run on
+// the device, the host walks the codes in index order exactly like the reference loop (counts,
+// output order, and the split offsets from the map state's std::mt19937_64 with one fresh
+// std::normal_distribution per split parent), and the device builds the new SoA map.
+static void draw3(double a, double b, double c, double* out) {
+  out[0] = a;
+  out[1] = b;
+  out[2] = c;
+}
+
+static gsf_structural_change densify_and_cull(gsf_ctx_s* c, const gsf_mapper_cfg& m) {
+  gsf_structural_change ch{0, 0, 0};
+  const int64_t P = c->P;
+  if (!c->rng_seeded) {
+    c->rng.seed(m.seed);
+    c->rng_seeded = true;
+  }
+  if (P == 0) return ch;
+  uint8_t* d_code = nullptr;
+  dalloc(d_code, P);
+  run_densify_codes(c->params, P, c->grad_accum, c->grad_count, m.densify_cull_opacity, m.densify_grad_threshold,
+                    m.densify_size_fraction * m.scene_extent, d_code, c->stream, &c->launches);
+  std::vector<uint8_t> code(P);
+  GSF_CUDA_CHECK(cudaMemcpyAsync(code.data(), d_code, P, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  dfree(d_code);
+  std::vector<int32_t> src, zidx;
+  std::vector<uint8_t> kind;
+  std::vector<int32_t> app_src, app_z;
+  std::vector<uint8_t> app_kind;
+  std::vector<double> z;
+  src.reserve(P);
+  for (int64_t i = 0; i < P; ++i) {
+    switch (code[i]) {
+      case 0:
+        ++ch.removed;
+        break;
+      case 2: {
+        ++ch.split;
+        std::normal_distribution<double> gauss(0.0, 1.0);
+        for (int child = 0; child < 2; ++child) {
+          // the reference draws with `Vec3 z(gauss(rng), gauss(rng), gauss(rng))` (mapper.cpp:199):
+          // the order of those argument evaluations is the compiler's; draw through a 3-argument
+          // call as well so this build consumes the stream the way the reference's build does
+          double zz[3];
+          draw3(gauss(c->rng), gauss(c->rng), gauss(c->rng), zz);
+          app_src.push_back(static_cast<int32_t>(i));
+          app_kind.push_back(2);
+          app_z.push_back(static_cast<int32_t>(z.size() / 3));
+          z.insert(z.end(), zz, zz + 3);
+        }
+        break;
+      }
+      case 3:
+        ++ch.cloned;
+        src.push_back(static_cast<int32_t>(i));
+        kind.push_back(0);
+        zidx.push_back(0);
+        app_src.push_back(static_cast<int32_t>(i));
+        app_kind.push_back(1);
+        app_z.push_back(0);
+        break;
+      default:
+        src.push_back(static_cast<int32_t>(i));
+        kind.push_back(0);
+        zidx.push_back(0);
+    }
+  }
+  if (ch.removed == 0 && ch.split == 0 && ch.cloned == 0) {
+    GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_accum, 0, sizeof(double) * P, c->stream));
+    GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_count, 0, sizeof(int32_t) * P, c->stream));
+    return ch;
+  }
+  src.insert(src.end(), app_src.begin(), app_src.end());
+  kind.insert(kind.end(), app_kind.begin(), app_kind.end());
+  zidx.insert(zidx.end(), app_z.begin(), app_z.end());
+  const int64_t P_new = static_cast<int64_t>(src.size());
+  const int D = c->D;
+  int32_t *d_src = nullptr, *d_zi = nullptr;
+  uint8_t* d_kind = nullptr;
+  double* d_z = nullptr;
+  dalloc(d_src, std::max<int64_t>(P_new, 1));
+  dalloc(d_zi, std::max<int64_t>(P_new, 1));
+  dalloc(d_kind, std::max<int64_t>(P_new, 1));
+  dalloc(d_z, std::max<size_t>(z.size(), 3));
+  if (P_new > 0) {
+    GSF_CUDA_CHECK(cudaMemcpyAsync(d_src, src.data(), sizeof(int32_t) * P_new, cudaMemcpyHostToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(d_zi, zidx.data(), sizeof(int32_t) * P_new, cudaMemcpyHostToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(d_kind, kind.data(), P_new, cudaMemcpyHostToDevice, c->stream));
+  }
+  if (!z.empty())
+    GSF_CUDA_CHECK(cudaMemcpyAsync(d_z, z.data(), sizeof(double) * z.size(), cudaMemcpyHostToDevice, c->stream));
+  float *params = nullptr, *mm = nullptr, *vv = nullptr, *nu = nullptr;
+  uint8_t* obs = nullptr;
+  const int64_t cap = std::max<int64_t>(P_new, 1);
+  dalloc(params, static_cast<size_t>(cap) * D);
+  dalloc(mm, static_cast<size_t>(cap) * D);
+  dalloc(vv, static_cast<size_t>(cap) * D);
+  dalloc(nu, cap);
+  dalloc(obs, cap);
+  run_densify_build(c->params, c->adam_m, c->adam_v, c->nu, c->observed, P, D, d_src, d_kind, d_zi, d_z,
+                    std::log(m.densify_split_factor), P_new, params, mm, vv, nu, obs, c->stream, &c->launches);
+  sync(c);
+  dfree(d_src); dfree(d_zi); dfree(d_kind); dfree(d_z);
+  dfree(c->params); dfree(c->adam_m); dfree(c->adam_v); dfree(c->nu); dfree(c->observed);
+  c->params = params; c->adam_m = mm; c->adam_v = vv; c->nu = nu; c->observed = obs;
+  dalloc(c->grads, static_cast<size_t>(cap) * D);
+  dalloc(c->d_mean2d, 2 * static_cast<size_t>(cap));
+  dalloc(c->grad_accum, cap);
+  dalloc(c->grad_count, cap);
+  GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_accum, 0, sizeof(double) * cap, c->stream));
+  GSF_CUDA_CHECK(cudaMemsetAsync(c->grad_count, 0, sizeof(int32_t) * cap, c->stream));
+  c->map_cap = cap;
+  c->P = P_new;
+  ++c->map_gen;
+  c->have_render = false;
+  return ch;
+}
+
+int gsf_densify_and_cull(gsf_ctx c, const gsf_mapper_cfg* mcfg, gsf_structural_change* out) {
+  return guard(c, [&] {
+    check_mapper(*mcfg);
+    *out = densify_and_cull(c, *mcfg);
+  });
+}
+
+int gsf_map_stats_upload(gsf_ctx c, const double* grad_accum, const int32_t* grad_count) {
+  return guard(c, [&] {
+    if (c->P == 0) return;
+    GSF_CUDA_CHECK(cudaMemcpy(c->grad_accum, grad_accum, sizeof(double) * c->P, cudaMemcpyHostToDevice));
+    GSF_CUDA_CHECK(cudaMemcpy(c->grad_count, grad_count, sizeof(int32_t) * c->P, cudaMemcpyHostToDevice));
+  });
+}
+
+int gsf_map_stats_download(gsf_ctx c, double* grad_accum, int32_t* grad_count) {
+  return guard(c, [&] {
+    if (c->P == 0) return;
+    sync(c);
+    if (grad_accum) GSF_CUDA_CHECK(cudaMemcpy(grad_accum, c->grad_accum, sizeof(double) * c->P, cudaMemcpyDeviceToHost));
+    if (grad_count) GSF_CUDA_CHECK(cudaMemcpy(grad_count, c->grad_count, sizeof(int32_t) * c->P, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -180,8 +180,16 @@ struct AdamGroups {
 void run_adam(float* params, const float* grads, float* m, float* v, int64_t P, int D, const AdamGroups& g, double step,
               cudaStream_t st, int64_t* launches);
 void run_track_update(DevState* ds, int iteration, cudaStream_t st, int64_t* launches);
-void run_densify_stats(const uint8_t* visible, const float* d_mean2d, float* accum, int32_t* cnt, int64_t P, int W,
-                       int H, cudaStream_t st, int64_t* launches);
+
+// densify.cu (mapper.cpp:172-230, 261-269)
+void run_densify_stats(const uint8_t* visible, const float* d_mean2d, double* accum, int32_t* cnt, int64_t P, int W, int H,
+                       cudaStream_t st, int64_t* launches);
+void run_densify_codes(const float* params, int64_t P, const double* accum, const int32_t* cnt, double cull_opacity,
+                       double grad_threshold, double size_boundary, uint8_t* code, cudaStream_t st, int64_t* launches);
+void run_densify_build(const float* params, const float* m, const float* v, const float* nu, const uint8_t* observed,
+                       int64_t P_old, int D, const int32_t* src, const uint8_t* kind, const int32_t* zidx, const double* z,
+                       double log_split, int64_t P_new, float* params_n, float* m_n, float* v_n, float* nu_n,
+                       uint8_t* observed_n, cudaStream_t st, int64_t* launches);
 
 // spawn.cu: initialize_map / spawn_gaussians candidates (one per stride-sampled pixel)
 struct BackprojectArgs {

@@ -1,4 +1,4 @@
-// optim.cu — fused Adam over the SoA map, the fp64 pose update of track_frame, densify stats.
+// optim.cu — fused Adam over the SoA map and the fp64 pose update of track_frame.
 //
 //   k_adam          AdamState::step (adam.cpp:40-53) for all five parameter groups of
 //                   PrimitiveOptimizer::step (mapper.cpp:72-117) in one pass over [D][P]; fp32
@@ -6,7 +6,6 @@
 //   k_track_update  tracker.cpp:62-70: the two pose AdamStates on zero-initialised deltas, then
 //                   CameraPose::perturbed (pose.hpp:44-48) and the next iteration's camera, all
 //                   on the device so a whole track_frame can be one CUDA graph.
-//   k_densify_stats mapper.cpp:261-269 (screen-space gradient norms in NDC units).
 #include "kernels.h"
 #include "finalize.cuh"
 
@@ -44,15 +43,6 @@ __global__ void k_track_update(DevState* ds, int iteration, double bc1, double b
   if (threadIdx.x == 0 && blockIdx.x == 0) track_update(ds, iteration, bc1, bc2);
 }
 
-__global__ void k_densify_stats(const uint8_t* __restrict__ visible, const float* __restrict__ d_mean2d,
-                                float* __restrict__ accum, int32_t* __restrict__ cnt, int64_t P, double hw, double hh) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= P || !visible[i]) return;
-  const double nx = d_mean2d[i] * hw, ny = d_mean2d[P + i] * hh;
-  accum[i] = static_cast<float>(static_cast<double>(accum[i]) + sqrt(nx * nx + ny * ny));
-  cnt[i] += 1;
-}
-
 }  // namespace
 
 void run_adam(float* params, const float* grads, float* m, float* v, int64_t P, int D, const AdamGroups& g, double step,
@@ -70,13 +60,6 @@ void run_track_update(DevState* ds, int iteration, cudaStream_t st, int64_t* L) 
   // AdamState bias corrections at step t = iteration + 1 (adam.cpp:40-53), host std::pow
   const double t = static_cast<double>(iteration + 1);
   k_track_update<<<1, 32, 0, st>>>(ds, iteration, 1.0 - std::pow(0.9, t), 1.0 - std::pow(0.999, t));
-  ++*L;
-}
-
-void run_densify_stats(const uint8_t* visible, const float* d_mean2d, float* accum, int32_t* cnt, int64_t P, int W, int H,
-                       cudaStream_t st, int64_t* L) {
-  if (P <= 0) return;
-  k_densify_stats<<<div_up(P, 256), 256, 0, st>>>(visible, d_mean2d, accum, cnt, P, 0.5 * W, 0.5 * H);
   ++*L;
 }
 

@@ -490,3 +490,60 @@ def test_spawn_gaussians_matches_oracle(gpu_ctx, orc):
     mc.densify_interval = 0
     gpu_ctx.render(p1, K)
     gpu_ctx.map_step([1], [p1], K, mc, 3)
+
+
+def _plane_scene(specs):
+    from helpers import logit
+    return scene([dict(mean=[x, y, z], scale=sc, opacity=op, sh=[[0.0, 0.0, 0.0]]) for (x, y, z, sc, op) in specs])
+
+
+def test_densify_kat_on_device(gpu_ctx, orc):
+    """test_map.cpp:317-350 through gsf_densify_and_cull, and the split children equal the fp64
+    restatement's (same mt19937_64 seed, one normal_distribution per split parent)."""
+    mc = defaults_mapper()
+    mc.scene_extent = 4.0
+    mc.seed = 9
+    specs = [(0, 0, 2, 0.10, 0.9), (1, 0, 2, 0.01, 0.9), (0, 1, 2, 0.02, 1e-4), (1, 1, 2, 0.02, 0.9)]
+    m = f32_round(_plane_scene(specs))
+    _upload(gpu_ctx, m)
+    gpu_ctx.set_map_stats([1.0, 1.0, 0.0, 0.0], [1, 1, 0, 1])
+    assert gpu_ctx.densify_and_cull(mc) == (1, 1, 1)
+    g = gpu_ctx.download()
+    assert g.mean.shape[0] == 5
+    assert g.mean[0, 0] == pytest.approx(1.0) and g.mean[1, 1] == pytest.approx(1.0) and g.mean[4, 0] == pytest.approx(1.0)
+    assert math.exp(g.log_scale[2, 0]) == pytest.approx(0.10 / 1.6, rel=1e-6)
+    st = orc.MapState(m, mc)
+    st.set_stats([1.0, 1.0, 0.0, 0.0], [1, 1, 0, 1])
+    assert st.densify(mc) == (1, 1, 1)
+    ref = st.get()
+    assert np.abs(g.mean - ref.mean).max() < 1e-6 and np.abs(g.log_scale - ref.log_scale).max() < 1e-6
+    a, c = gpu_ctx.map_stats()
+    assert (a == 0).all() and (c == 0).all()
+    assert gpu_ctx.densify_and_cull(mc) == (0, 0, 0) and gpu_ctx.download().mean.shape[0] == 5
+    # a second split continues the same generator stream on both sides
+    gpu_ctx.set_map_stats([1.0] * 5, [1] * 5)
+    st.set_stats([1.0] * 5, [1] * 5)
+    assert gpu_ctx.densify_and_cull(mc) == st.densify(mc)
+    assert np.abs(gpu_ctx.download().mean - st.get().mean).max() < 1e-6
+
+
+def test_map_step_with_densification(gpu_ctx, orc):
+    """map_step runs densify_and_cull every `interval` iterations (mapper.cpp:278-279): the map
+    is resized on the device, its statistics restart and the loop keeps optimising."""
+    truth = orc.random_scene(83, 60, 1, 0.95, 0.05, 0.2)
+    K = make_intrinsics(48, 36, 40.0)
+    gt = orc.render(truth, pose(), K)
+    obs = np.where(gt.opacity > 0.5, gt.alpha_depth, 0.0)
+    m = f32_round(truth)
+    m.opacity_logit[:5] = -8.0            # faded: culled at the first pass
+    _upload(gpu_ctx, m)
+    gpu_ctx.frame_upload(0, gt.color.astype(np.float32), obs.astype(np.float32), 48, 36)
+    mc = defaults_mapper()
+    mc.densify_interval = 4
+    mc.densify_grad_threshold = 1e-9      # every primitive seen with any gradient strains
+    trace = gpu_ctx.map_step([0], [pose()], K, mc, 9)
+    assert np.isfinite(trace).all()
+    P = gpu_ctx.download().mean.shape[0]
+    assert P != 60 and P == gpu_ctx.P
+    a, c = gpu_ctx.map_stats()
+    assert a.shape[0] == P and (c <= 1).all()   # restarted at iteration 8, one pass since

@@ -370,3 +370,31 @@ def test_backproject_spawn_kats(orc):
     partial = np.full((3, 4), 0.8)
     partial[1, 1] = 0.4
     assert orc.backproject(rgb, np.full((3, 4), 1.5), pose(), K, mc, 1, opacity=partial).mean.shape[0] == 1
+
+
+def _plane_map(orc, specs):
+    """test_map.cpp:44-51 plane_primitive(x, y, z, scale, opacity)."""
+    from helpers import logit
+    m = orc.empty_map(len(specs), 1)
+    for i, (x, y, z, sc, op) in enumerate(specs):
+        m.mean[i] = [x, y, z]
+        m.log_scale[i] = math.log(sc)
+        m.opacity_logit[i] = logit(op)
+    return m
+
+
+def test_densify_kat(orc):
+    """test_map.cpp:317-350: split large, clone small, cull faded, order of survivors."""
+    from paper_2403_16095_b200.abi import defaults_mapper
+    mc = defaults_mapper()
+    mc.scene_extent = 4.0
+    m = _plane_map(orc, [(0, 0, 2, 0.10, 0.9), (1, 0, 2, 0.01, 0.9), (0, 1, 2, 0.02, 1e-4), (1, 1, 2, 0.02, 0.9)])
+    st = orc.MapState(m, mc)
+    st.set_stats([1.0, 1.0, 0.0, 0.0], [1, 1, 0, 1])
+    assert st.densify(mc) == (1, 1, 1)
+    g = st.get()
+    assert g.mean.shape[0] == 5
+    assert g.mean[0, 0] == pytest.approx(1.0) and g.mean[1, 1] == pytest.approx(1.0)
+    assert math.exp(g.log_scale[2, 0]) == pytest.approx(0.10 / 1.6, rel=1e-12)
+    assert g.mean[4, 0] == pytest.approx(1.0)
+    assert st.densify(mc) == (0, 0, 0) and st.get().mean.shape[0] == 5
