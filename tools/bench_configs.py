@@ -1,0 +1,167 @@
+"""Per-config measurements of SURVEY.md §8(d) beside the headline bench.py line (not bench lines):
+
+  cfg1  100k Gaussians, 640x480 (f=525): one render + render_backward with mapping-loss seeds
+        (all five maps, observed depth given) -> device ms per kernel class; CPU oracle median of 3
+  cfg3  TUM-shaped 640x480 (fx 517.3), 200k, handheld_real weights: 30 frames, track_frame(25) each,
+        map_step(45) over the last keyframes every 15 frames -> tracked frames/s, mapping it/s
+  cfg5  ScanNet-shaped 640x480 (fx 577.6), P in {10k .. 4M}: render + render_backward ms (device
+        event brackets), and the workload statistics V / M / longest tile list
+
+Run on the GPU box:  python tools/bench_configs.py > gpurun_out/configs.json
+Inputs are the reference room generator (synthetic.cpp:56-104, mt19937_64 seed 0) with the seeded
+anisotropy of SURVEY §8(d) and orbit poses; targets are device renders of the ground truth plus the
+NoiseSpec noise (as bench.py)."""
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402  (scene, noise and pose helpers shared with the headline bench)
+
+
+def cam(fx, fy, cx, cy, w, h):
+    from paper_2403_16095_b200.abi import Intrinsics
+    return Intrinsics(fx, fy, cx, cy, w, h, 1.0, 0.1, 10.0)
+
+
+def profile(ctx, fn, reps=5):
+    """Median device ms per kernel class over `reps` calls of fn (CUDA events on the library stream)."""
+    classes = ("preprocess", "sort_binning", "blend", "backward", "chain")
+    rows = []
+    for _ in range(reps):
+        ctx.lib.gsf_profile_enable(ctx.h, 1)
+        ctx.lib.gsf_event_record(ctx.h, 0)
+        fn()
+        ctx.lib.gsf_event_record(ctx.h, 1)
+        ms = C.c_double()
+        ctx.lib.gsf_event_elapsed(ctx.h, 0, 1, C.byref(ms))
+        row = {"wall_ms": ms.value}
+        for k, name in enumerate(classes):
+            t, n = C.c_double(), C.c_int64()
+            ctx.lib.gsf_profile_read(ctx.h, k, C.byref(t), C.byref(n))
+            row[name] = t.value
+        ctx.lib.gsf_profile_enable(ctx.h, 0)
+        rows.append(row)
+    return {k: float(np.median([r[k] for r in rows])) for k in rows[0]}
+
+
+def cfg1(out):
+    from paper_2403_16095_b200 import abi, api
+    import oracle
+    K = cam(525.0, 525.0, 319.5, 239.5, 640, 480)
+    m, poses = bench.build_scene(100000)
+    ctx = api.Context(0)
+    ctx.upload(m)
+    r = ctx.render(poses[3], K)
+    tgt, obs = bench.noisy(r.color, r.alpha_depth, 3)
+    p = bench.perturbed(poses[3], bench.OFFSET)
+    w = abi.defaults_weights()
+
+    def fwd_bwd():
+        ctx.render(p, K, obs)
+        _, (dc, dad, dmd, du, _) = ctx.evaluate_mapping_loss(tgt, obs, w)
+        ctx.render_backward(dc.reshape(480, 640, 3), dad.reshape(480, 640), dmd.reshape(480, 640), None,
+                            du.reshape(480, 640), obs)
+
+    fwd_bwd()
+    dev = profile(ctx, fwd_bwd)
+    cpu = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        o = oracle.render(m, p, K, obs.astype(np.float64))
+        loss, (dc, dad, dmd, du, dls) = oracle.mapping_loss(m, o, tgt.astype(np.float64), obs.astype(np.float64), K, w)
+        oracle.render_backward(m, p, K, o, dc, dad, dmd, None, du, obs.astype(np.float64))
+        cpu.append(time.perf_counter() - t0)
+    out["cfg1"] = {"workload": "100k Gaussians, 640x480 f=525: render + mapping loss + render_backward (all maps)",
+                   "primitives": int(m.count), "device_ms": dev, "cpu_oracle_s_median3": float(np.median(cpu)),
+                   "cpu_threads": oracle.threads()}
+    ctx.close()
+
+
+def cfg3(out):
+    from paper_2403_16095_b200 import abi, api
+    K = cam(517.3, 516.5, 318.6, 255.3, 640, 480)
+    m, poses = bench.build_scene(200000)
+    ctx = api.Context(0)
+    ctx.upload(m)
+    frames = []
+    for f in range(30):
+        r = ctx.render(poses[f], K)
+        c, d = bench.noisy(r.color, r.alpha_depth, f)
+        ctx.frame_upload(f, c, d, 640, 480)
+        frames.append((c, d))
+    tc = abi.defaults_tracker()
+    tc.iterations = 25
+    w = abi.defaults_weights(True)        # LossWeights::handheld_real (losses.cpp:35-46)
+    mc = abi.defaults_mapper()
+    mc.densify_interval = 0
+    mc.weights = abi.defaults_weights(True)
+    rc = abi.defaults_raster()
+    ctx.track_frame(0, poses[0], K, tc, w, rc)   # warm-up
+    track_ms, map_ms, map_its = 0.0, 0.0, 0
+    est = [poses[0]]
+    for f in range(1, 30):
+        ctx.lib.gsf_synchronize(ctx.h)
+        t0 = time.perf_counter()
+        res = ctx.track_frame(f, bench.perturbed(est[-1], [0, 0, 0, 0, 0, 0]), K, tc, w, rc)
+        track_ms += (time.perf_counter() - t0) * 1e3
+        est.append(res.pose)
+        if f % 15 == 0:
+            win = list(range(max(0, f - 3), f + 1))
+            t0 = time.perf_counter()
+            ctx.map_step(win, [est[k] for k in win], K, mc, 45)
+            map_ms += (time.perf_counter() - t0) * 1e3
+            map_its += 45
+    out["cfg3"] = {"workload": "TUM-shaped 640x480, 200k, handheld_real weights: 29 tracked frames x 25 iterations, "
+                               "map_step(45) every 15 frames (4-keyframe window)",
+                   "primitives": int(m.count), "tracking_frames_per_s": 29 / (track_ms / 1e3),
+                   "tracking_ms_per_iter": track_ms / (29 * 25), "mapping_it_per_s": map_its / (map_ms / 1e3)}
+    ctx.close()
+
+
+def cfg5(out):
+    from paper_2403_16095_b200 import api
+    K = cam(577.6, 578.7, 318.9, 242.7, 640, 480)
+    rows = []
+    rng = np.random.default_rng(5)
+    for P in (10000, 30000, 100000, 300000, 1000000, 2000000, 4000000):
+        m, poses = bench.build_scene(P)
+        ctx = api.Context(0)
+        ctx.upload(m)
+        p = poses[5]
+        up = [rng.standard_normal((480, 640, 3)).astype(np.float32), rng.standard_normal((480, 640)).astype(np.float32)]
+
+        def fwd_bwd():
+            ctx.render(p, K)
+            ctx.render_backward(up[0], up[1])
+
+        fwd_bwd()
+        r = ctx.render(p, K)
+        tiles = 40 * 30
+        tr, _ = ctx.render_tiles(tiles, r.num_pairs)
+        dev = profile(ctx, fwd_bwd)
+        rows.append({"primitives": int(m.count), "visible": int(r.num_visible), "pairs": int(r.num_pairs),
+                     "max_tile_list": int((tr[:, 1] - tr[:, 0]).max()), "device_ms": dev})
+        ctx.close()
+    out["cfg5"] = {"workload": "ScanNet-shaped 640x480 sweep: render + render_backward (explicit upstream colour "
+                               "and alpha-depth maps)", "rows": rows}
+
+
+def main():
+    out = {"note": "SURVEY.md §8(d) per-config measurements; device_ms = CUDA-event brackets per kernel class "
+                   "(median of 5 calls, wall_ms includes the API's host transfers)"}
+    for fn in (cfg1, cfg3, cfg5):
+        t0 = time.perf_counter()
+        fn(out)
+        out.setdefault("elapsed_s", {})[fn.__name__] = time.perf_counter() - t0
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
