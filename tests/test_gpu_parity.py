@@ -547,3 +547,16 @@ def test_map_step_with_densification(gpu_ctx, orc):
     assert P != 60 and P == gpu_ctx.P
     a, c = gpu_ctx.map_stats()
     assert a.shape[0] == P and (c <= 1).all()   # restarted at iteration 8, one pass since
+
+
+def test_cabi_client_from_cpp():
+    """The drop-in boundary from plain C++ (tools/cabi_client.cpp: include/gsf_cuda.h + the .so):
+    upload, render, frame upload, track_frame, map_step and the CSR record in one process."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "cabi_client")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["final_loss"] < r["initial_loss"] and r["record_entries"] > 0 and r["kernel_launches"] > 0
