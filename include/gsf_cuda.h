@@ -191,6 +191,8 @@ int gsf_event_elapsed(gsf_ctx ctx, int32_t a, int32_t b, double* ms);  /* waits 
 int gsf_map_upload(gsf_ctx ctx, const gsf_map_host* map);
 int gsf_map_download(gsf_ctx ctx, gsf_map_host* map);   /* map->count must match */
 int64_t gsf_map_count(gsf_ctx ctx);
+/* SH coefficients per colour channel of the context's map (K of GaussianPrimitive::sh). */
+int32_t gsf_map_sh_coeffs(gsf_ctx ctx);
 /* Reset the Adam moments/step counts of the primitive optimizer (PrimitiveOptimizer,
  * map/mapper.hpp:92-105) — a fresh MapState. */
 int gsf_optimizer_reset(gsf_ctx ctx);
@@ -276,6 +278,16 @@ int gsf_initialize_map(gsf_ctx ctx, int32_t slot, const gsf_pose* pose, const gs
  * start at zero. */
 int gsf_spawn_gaussians(gsf_ctx ctx, int32_t slot, const gsf_pose* pose, const gsf_intrinsics* K,
                         const gsf_mapper_cfg* mcfg, int32_t* spawned);
+
+/* render_reference (raster/rasterizer.hpp:24-28, rasterizer.cpp:263-296): the brute-force oracle
+ * render — every pixel blends its whole depth-ordered list without early termination. */
+int gsf_render_reference(gsf_ctx ctx, const gsf_pose* pose, const gsf_intrinsics* K, const float* observed_depth,
+                         const gsf_raster_cfg* cfg, gsf_render_out* out);
+
+/* save_checkpoint / load_checkpoint (io/checkpoint.hpp:16-20): the GSFMAP01 file of the context's
+ * map with intrinsics K.  Loading replaces the map (a fresh MapState) and returns its intrinsics. */
+int gsf_checkpoint_save(gsf_ctx ctx, const char* path, const gsf_intrinsics* K);
+int gsf_checkpoint_load(gsf_ctx ctx, const char* path, gsf_intrinsics* K);
 
 /* StructuralChange (map/mapper.hpp:66-70). */
 typedef struct {

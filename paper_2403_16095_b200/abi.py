@@ -122,6 +122,7 @@ SIGNATURES = {
     "gsf_map_upload": (C.c_int, [C.c_void_p, C.POINTER(MapHost)]),
     "gsf_map_download": (C.c_int, [C.c_void_p, C.POINTER(MapHost)]),
     "gsf_map_count": (C.c_int64, [C.c_void_p]),
+    "gsf_map_sh_coeffs": (C.c_int32, [C.c_void_p]),
     "gsf_optimizer_reset": (C.c_int, [C.c_void_p]),
     "gsf_render": (C.c_int, [C.c_void_p, C.POINTER(Pose), C.POINTER(Intrinsics), fp,
                              C.POINTER(RasterCfg), C.POINTER(RenderOut)]),
@@ -152,6 +153,10 @@ SIGNATURES = {
                                      C.POINTER(MapperCfg), C.POINTER(C.c_int64)]),
     "gsf_spawn_gaussians": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Pose), C.POINTER(Intrinsics),
                                       C.POINTER(MapperCfg), C.POINTER(C.c_int32)]),
+    "gsf_render_reference": (C.c_int, [C.c_void_p, C.POINTER(Pose), C.POINTER(Intrinsics), fp, C.POINTER(RasterCfg),
+                                       C.POINTER(RenderOut)]),
+    "gsf_checkpoint_save": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(Intrinsics)]),
+    "gsf_checkpoint_load": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(Intrinsics)]),
     "gsf_densify_and_cull": (C.c_int, [C.c_void_p, C.POINTER(MapperCfg), C.POINTER(StructuralChange)]),
     "gsf_map_stats_upload": (C.c_int, [C.c_void_p, dp, i32p]),
     "gsf_map_stats_download": (C.c_int, [C.c_void_p, dp, i32p]),

@@ -12,6 +12,7 @@ implement as ``NotImplementedError``.  All arithmetic runs in libgsf_cuda.so on 
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -198,7 +199,9 @@ class Context:
         self._check(self.lib.gsf_optimizer_reset(self.h))
 
     # ---- forward / backward ----------------------------------------------------------------
-    def render(self, pose: Pose, K: Intrinsics, observed_depth=None, cfg: RasterCfg = None) -> RenderResult:
+    def render(self, pose: Pose, K: Intrinsics, observed_depth=None, cfg: RasterCfg = None,
+               reference: bool = False) -> RenderResult:
+        """render (rasterizer.cpp:168-261); reference=True: render_reference (:263-296, no termination)."""
         cfg = cfg or abi.defaults_raster()
         W, H = K.width, K.height
         n = max(W, 0) * max(H, 0)
@@ -224,7 +227,8 @@ class Context:
             obs = _f32(observed_depth)
             if obs.size != n:
                 raise ValueError("render: observed depth dimensions do not match intrinsics")
-        self._check(self.lib.gsf_render(self.h, C.byref(pose), C.byref(K), _ptr(obs), C.byref(cfg), C.byref(ro)))
+        fn = self.lib.gsf_render_reference if reference else self.lib.gsf_render
+        self._check(fn(self.h, C.byref(pose), C.byref(K), _ptr(obs), C.byref(cfg), C.byref(ro)))
         o["visible"] = o["visible"][: self.P]
         return RenderResult(**o, has_uncertainty=bool(ro.has_uncertainty), num_visible=int(ro.num_visible),
                             num_pairs=int(ro.num_pairs))
@@ -375,6 +379,21 @@ class Context:
         self._check(self.lib.gsf_spawn_gaussians(self.h, slot, C.byref(pose), C.byref(K), C.byref(mcfg), C.byref(n)))
         self._sync_count(mcfg.sh_coeffs)
         return n.value
+
+    def save_checkpoint(self, path: str, K: Intrinsics):
+        """save_checkpoint (io/checkpoint.cpp:36-60): GSFMAP01 file of the device map."""
+        self._check(self.lib.gsf_checkpoint_save(self.h, os.fsencode(path), C.byref(K)))
+
+    def load_checkpoint(self, path: str) -> Intrinsics:
+        """load_checkpoint (io/checkpoint.cpp:62-100): replaces the map; returns the intrinsics."""
+        K = abi.Intrinsics()
+        self._check(self.lib.gsf_checkpoint_load(self.h, os.fsencode(path), C.byref(K)))
+        self.P = int(self.lib.gsf_map_count(self.h))
+        self.K = self.download_sh_coeffs()
+        return K
+
+    def download_sh_coeffs(self) -> int:
+        return int(self.lib.gsf_map_sh_coeffs(self.h))
 
     def densify_and_cull(self, mcfg: MapperCfg = None):
         """densify_and_cull (mapper.cpp:172-230): returns (split, cloned, removed)."""

@@ -756,6 +756,7 @@ int gsf_map_download(gsf_ctx c, gsf_map_host* m) {
 }
 
 int64_t gsf_map_count(gsf_ctx c) { return c ? c->P : -1; }
+int32_t gsf_map_sh_coeffs(gsf_ctx c) { return c ? c->K : -1; }
 
 int gsf_profile_enable(gsf_ctx c, int32_t on) {
   return guard(c, [&] {
@@ -1797,6 +1798,108 @@ int gsf_map_stats_download(gsf_ctx c, double* grad_accum, int32_t* grad_count) {
     sync(c);
     if (grad_accum) GSF_CUDA_CHECK(cudaMemcpy(grad_accum, c->grad_accum, sizeof(double) * c->P, cudaMemcpyDeviceToHost));
     if (grad_count) GSF_CUDA_CHECK(cudaMemcpy(grad_count, c->grad_count, sizeof(int32_t) * c->P, cudaMemcpyDeviceToHost));
+  });
+}
+
+// render_reference (rasterizer.cpp:263-296): every pixel walks the full depth-sorted list with no
+// early termination.  Every primitive a pixel can see (rho <= footprint_sigma^2) lies in that
+// pixel's tile list (the tile rectangle bounds the same footprint disc), so this is the tiled
+// render with the termination test disabled.
+int gsf_render_reference(gsf_ctx c, const gsf_pose* pose, const gsf_intrinsics* K, const float* obs,
+                         const gsf_raster_cfg* cfg, gsf_render_out* out) {
+  gsf_raster_cfg nt = *cfg;
+  nt.termination_threshold = 0.0;   // T < 0 never holds: no pixel terminates
+  return gsf_render(c, pose, K, obs, &nt, out);
+}
+
+// GSFMAP01 checkpoint (io/checkpoint.cpp:11-100): little-endian; magic, 9 doubles of intrinsics,
+// u32 SH bands, u64 count, per primitive mean 3, log_scale 3, quat 4, opacity logit, uncertainty
+// (f64), observed (u8), SH bands x 3 (f64).  The device map is fp32, so a saved map is exact and a
+// loaded fp64 map is rounded to fp32.
+int gsf_checkpoint_save(gsf_ctx c, const char* path, const gsf_intrinsics* K) {
+  return guard(c, [&] {
+    if (!path || !K) throw EInval("checkpoint: null argument");
+    const int64_t P = c->P;
+    const int Ks = c->K;
+    std::vector<double> mean(3 * P), ls(3 * P), quat(4 * P), op(P), sh(3 * Ks * std::max<int64_t>(P, 1)), nu(P);
+    std::vector<uint8_t> ob(P);
+    if (P > 0) {
+      gsf_map_host m{P, Ks, mean.data(), ls.data(), quat.data(), op.data(), sh.data(), nu.data(), ob.data()};
+      const int rc = gsf_map_download(c, &m);
+      if (rc != GSF_OK) throw ERuntime(c->err);
+    }
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) throw ERuntime(std::string("cannot open checkpoint for writing: ") + path);
+    const char magic[8] = {'G', 'S', 'F', 'M', 'A', 'P', '0', '1'};
+    const double header[9] = {K->fx, K->fy, K->cx, K->cy, double(K->width), double(K->height), K->depth_scale,
+                              K->near_plane, K->far_plane};
+    const uint32_t bands = static_cast<uint32_t>(std::max(Ks, 1));
+    const uint64_t count = static_cast<uint64_t>(P);
+    bool ok = std::fwrite(magic, 1, 8, f) == 8 && std::fwrite(header, sizeof(double), 9, f) == 9 &&
+              std::fwrite(&bands, 4, 1, f) == 1 && std::fwrite(&count, 8, 1, f) == 1;
+    for (int64_t i = 0; ok && i < P; ++i) {
+      const uint8_t o = ob[i] ? 1 : 0;
+      ok = std::fwrite(&mean[3 * i], sizeof(double), 3, f) == 3 && std::fwrite(&ls[3 * i], sizeof(double), 3, f) == 3 &&
+           std::fwrite(&quat[4 * i], sizeof(double), 4, f) == 4 && std::fwrite(&op[i], sizeof(double), 1, f) == 1 &&
+           std::fwrite(&nu[i], sizeof(double), 1, f) == 1 && std::fwrite(&o, 1, 1, f) == 1 &&
+           std::fwrite(&sh[3 * Ks * i], sizeof(double), 3 * Ks, f) == static_cast<size_t>(3 * Ks);
+    }
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw ERuntime(std::string("failed writing checkpoint: ") + path);
+  });
+}
+
+int gsf_checkpoint_load(gsf_ctx c, const char* path, gsf_intrinsics* K) {
+  return guard(c, [&] {
+    if (!path) throw EInval("checkpoint: null path");
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) throw ERuntime(std::string("cannot open checkpoint: ") + path);
+    auto rd = [&](void* dst, size_t bytes) {
+      if (std::fread(dst, 1, bytes, f) != bytes) {
+        std::fclose(f);
+        throw ERuntime("checkpoint truncated");
+      }
+    };
+    char magic[8];
+    rd(magic, 8);
+    if (std::memcmp(magic, "GSFMAP01", 8) != 0) {
+      std::fclose(f);
+      throw ERuntime(std::string("not a map checkpoint (bad magic): ") + path);
+    }
+    double header[9];
+    rd(header, sizeof(header));
+    uint32_t bands = 0;
+    uint64_t count = 0;
+    rd(&bands, 4);
+    rd(&count, 8);
+    if (bands == 0 || bands > 16) {
+      std::fclose(f);
+      throw ERuntime("checkpoint has invalid SH band count");
+    }
+    const int64_t P = static_cast<int64_t>(count);
+    const int Ks = static_cast<int>(bands);
+    std::vector<double> mean(3 * P), ls(3 * P), quat(4 * P), op(P), sh(3 * Ks * std::max<int64_t>(P, 1)), nu(P);
+    std::vector<uint8_t> ob(P);
+    for (int64_t i = 0; i < P; ++i) {
+      rd(&mean[3 * i], 24);
+      rd(&ls[3 * i], 24);
+      rd(&quat[4 * i], 32);
+      rd(&op[i], 8);
+      rd(&nu[i], 8);
+      rd(&ob[i], 1);
+      rd(&sh[3 * Ks * i], sizeof(double) * 3 * Ks);
+    }
+    std::fclose(f);
+    if (Ks != 1 && Ks != 4 && Ks != 9 && Ks != 16) throw EInval("sh coefficient count must be 1, 4, 9 or 16");
+    gsf_map_host m{P, Ks, mean.data(), ls.data(), quat.data(), op.data(), sh.data(), nu.data(), ob.data()};
+    const int rc = gsf_map_upload(c, &m);
+    if (rc != GSF_OK) throw ERuntime(c->err);
+    if (K) {
+      K->fx = header[0]; K->fy = header[1]; K->cx = header[2]; K->cy = header[3];
+      K->width = static_cast<int32_t>(header[4]);
+      K->height = static_cast<int32_t>(header[5]);
+      K->depth_scale = header[6]; K->near_plane = header[7]; K->far_plane = header[8];
+    }
   });
 }
 
