@@ -314,6 +314,44 @@ int gsf_accumulate_uncertainty(gsf_ctx ctx, const int32_t* slots, const gsf_pose
                                int32_t* observed_count);
 int gsf_prune_unreliable(gsf_ctx ctx, double tau, double reduced_opacity, int32_t* reduced);
 
+/* ---- SLAM pipeline (slam/system.hpp, system.cpp:31-154) on the context's map ------------ */
+typedef struct gsf_slam_s* gsf_slam;
+
+/* RunConfig fields the pipeline reads (io/config.hpp:16-35). */
+typedef struct {
+  gsf_intrinsics intrinsics;
+  gsf_tracker_cfg tracker;
+  gsf_mapper_cfg mapper;      /* mapper.seed is replaced by `seed` (system.cpp:20-24) */
+  int32_t map_iterations;     /* MapperConfig::iterations per keyframe window (60) */
+  int32_t init_iterations;    /* MapperConfig::init_iterations of the bootstrap (120) */
+  uint64_t seed;
+} gsf_slam_cfg;
+
+/* FrameLog (slam/system.hpp:17-34) plus the frame's trajectory pose.  The *_ms fields are
+ * wall-clock milliseconds of each stage (device work included). */
+typedef struct {
+  int32_t frame;
+  double timestamp;
+  double track_loss;
+  int32_t track_iterations, track_degraded, keyframe;
+  int64_t primitives;
+  double track_ms, map_ms, ba_ms, uncertainty_ms, spawn_ms;
+  double kf_psnr_db, kf_depth_l1_cm;
+  gsf_pose pose;
+} gsf_frame_log;
+
+/* SlamSystem over the context: the first processed frame bootstraps the map (initialize_map +
+ * map_step(init_iterations)); every later frame is tracked from the constant-velocity prediction,
+ * and every keyframe_interval-th frame runs map_step over the selected window, sliding_ba,
+ * accumulate_uncertainty + prune_unreliable and spawn_gaussians.  Frames use device slot 0 and
+ * keyframe k slot 1 + k of the context.  Host rgb (3*W*H) / depth (W*H) in stream order. */
+int gsf_slam_create(gsf_ctx ctx, const gsf_slam_cfg* cfg, gsf_slam* out);
+int gsf_slam_destroy(gsf_slam slam);
+int gsf_slam_process(gsf_slam slam, int32_t index, double timestamp, const float* rgb, const float* depth,
+                     gsf_frame_log* log);
+int32_t gsf_slam_keyframes(gsf_slam slam);
+int32_t gsf_slam_degraded_frames(gsf_slam slam);
+
 /* ---- multi-GPU (keyframe-sharded sliding_ba) ----------------------------------------- */
 /* Which window keyframes rank `rank` of `nranks` renders: out[i] = 1 if owned.  Pure host
  * logic, usable without a device (ctx may be NULL). */

@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
                                    C.POINTER(Intrinsics), C.POINTER(MapperCfg), C.c_int, dp]),
         "orc_sliding_ba": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(dp), C.POINTER(dp), C.POINTER(Pose), i32p,
                                      C.POINTER(Intrinsics), C.POINTER(TrackerCfg), C.POINTER(MapperCfg), C.c_int, dp]),
+        "orc_mapstate_put": (C.c_int, [C.c_void_p, C.POINTER(MapHost)]),
+        "orc_mapstate_append": (C.c_int, [C.c_void_p, C.POINTER(MapHost)]),
         "orc_mapstate_set_stats": (C.c_int, [C.c_void_p, dp, i32p]),
         "orc_mapstate_densify": (C.c_int, [C.c_void_p, C.POINTER(MapperCfg), i32p]),
         "orc_backproject": (C.c_int, [dp, dp, dp, C.POINTER(Pose), C.POINTER(Intrinsics), C.POINTER(MapperCfg),
@@ -333,6 +335,14 @@ class MapState:
         _check(lib().orc_sliding_ba(self.h, n, rg, dg, ps, fid, C.byref(K), C.byref(tcfg), C.byref(mcfg), iterations,
                                     trace.ctypes.data_as(dp)))
         return trace[:iterations], [ps[i] for i in range(n)]
+
+    def put(self, m):
+        h = host_of(m)
+        _check(lib().orc_mapstate_put(self.h, C.byref(h)))
+
+    def append(self, m):
+        h = host_of(m)
+        _check(lib().orc_mapstate_append(self.h, C.byref(h)))
 
     def set_stats(self, accum, count):
         a = np.ascontiguousarray(accum, dtype=np.float64)

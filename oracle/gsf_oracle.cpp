@@ -1734,6 +1734,26 @@ int orc_mapstate_get(const orc_mapstate* s, gsf_map_host* out) {
   return GSF_OK;
 }
 
+// Overwrite the primitives of a MapState (same count): what accumulate_uncertainty / prune_unreliable
+// do to MapState::primitives in place (system.cpp:130-132).
+int orc_mapstate_put(orc_mapstate* s, const gsf_map_host* map) {
+  return guarded([&] {
+    if (map->count != static_cast<int64_t>(s->prims.size())) throw std::invalid_argument("count mismatch");
+    s->prims = load_map(map);
+  });
+}
+
+// spawn_gaussians' tail (mapper.cpp:163-169): append primitives, zero Adam moments and statistics.
+int orc_mapstate_append(orc_mapstate* s, const gsf_map_host* map) {
+  return guarded([&] {
+    const std::vector<Prim> add = load_map(map);
+    s->prims.insert(s->prims.end(), add.begin(), add.end());
+    s->opt.append(add.size());
+    s->grad_accum.resize(s->prims.size(), 0.0);
+    s->grad_count.resize(s->prims.size(), 0);
+  });
+}
+
 // mapper.cpp:232-281
 int orc_map_step(orc_mapstate* st, int n, const double* const* rgbs, const double* const* depths, const gsf_pose* poses,
                  const gsf_intrinsics* K, const gsf_mapper_cfg* cfg, int iterations, double* trace) {

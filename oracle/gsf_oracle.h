@@ -92,6 +92,8 @@ int orc_sliding_ba(orc_mapstate* s, int n, const double* const* rgbs, const doub
 
 /* accumulate_uncertainty / prune_unreliable (uncertainty.cpp:17-100).  The map's
  * uncertainty/observed arrays are updated in place. */
+int orc_mapstate_put(orc_mapstate* st, const gsf_map_host* map);
+int orc_mapstate_append(orc_mapstate* st, const gsf_map_host* map);
 int orc_mapstate_set_stats(orc_mapstate* st, const double* accum, const int32_t* count);
 int orc_mapstate_densify(orc_mapstate* st, const gsf_mapper_cfg* cfg, int32_t* change);
 int orc_backproject(const double* rgb, const double* depth, const double* opacity, const gsf_pose* pose,

@@ -70,6 +70,19 @@ class StructuralChange(C.Structure):
     _fields_ = [("split", C.c_int32), ("cloned", C.c_int32), ("removed", C.c_int32)]
 
 
+class SlamCfg(C.Structure):
+    _fields_ = [("intrinsics", Intrinsics), ("tracker", TrackerCfg), ("mapper", MapperCfg),
+                ("map_iterations", C.c_int32), ("init_iterations", C.c_int32), ("seed", C.c_uint64)]
+
+
+class FrameLog(C.Structure):
+    _fields_ = [("frame", C.c_int32), ("timestamp", C.c_double), ("track_loss", C.c_double),
+                ("track_iterations", C.c_int32), ("track_degraded", C.c_int32), ("keyframe", C.c_int32),
+                ("primitives", C.c_int64), ("track_ms", C.c_double), ("map_ms", C.c_double), ("ba_ms", C.c_double),
+                ("uncertainty_ms", C.c_double), ("spawn_ms", C.c_double), ("kf_psnr_db", C.c_double),
+                ("kf_depth_l1_cm", C.c_double), ("pose", Pose)]
+
+
 class MapHost(C.Structure):
     _fields_ = [("count", C.c_int64), ("sh_coeffs", C.c_int32), ("mean", dp), ("log_scale", dp),
                 ("quat", dp), ("opacity_logit", dp), ("sh", dp), ("uncertainty", dp),
@@ -157,6 +170,11 @@ SIGNATURES = {
                                        C.POINTER(RenderOut)]),
     "gsf_checkpoint_save": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(Intrinsics)]),
     "gsf_checkpoint_load": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(Intrinsics)]),
+    "gsf_slam_create": (C.c_int, [C.c_void_p, C.POINTER(SlamCfg), C.POINTER(C.c_void_p)]),
+    "gsf_slam_destroy": (C.c_int, [C.c_void_p]),
+    "gsf_slam_process": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, fp, fp, C.POINTER(FrameLog)]),
+    "gsf_slam_keyframes": (C.c_int32, [C.c_void_p]),
+    "gsf_slam_degraded_frames": (C.c_int32, [C.c_void_p]),
     "gsf_densify_and_cull": (C.c_int, [C.c_void_p, C.POINTER(MapperCfg), C.POINTER(StructuralChange)]),
     "gsf_map_stats_upload": (C.c_int, [C.c_void_p, dp, i32p]),
     "gsf_map_stats_download": (C.c_int, [C.c_void_p, dp, i32p]),
@@ -217,6 +235,11 @@ def defaults_weights(handheld_real: bool = False) -> LossWeights:
 def defaults_tracker() -> TrackerCfg:
     """TrackerConfig defaults (track/tracker.hpp:11-22)."""
     return TrackerCfg(0.0015, 0.00215, 15, 4, 10, 30, 2, 1, 2.0)
+
+
+def defaults_slam(K: Intrinsics) -> SlamCfg:
+    """RunConfig defaults (io/config.hpp:16-35) with intrinsics K: tracker, mapper, 60 / 120 mapping iterations."""
+    return SlamCfg(K, defaults_tracker(), defaults_mapper(), 60, 120, 0)
 
 
 def defaults_mapper() -> MapperCfg:

@@ -489,3 +489,45 @@ def synth_orbit(frames: int, radius: float = 1.0, height: float = 0.0):
     if rc != GSF_OK:
         raise ValueError("synth_orbit failed")
     return [poses[i] for i in range(frames)]
+
+
+class SlamSystem:
+    """SlamSystem (slam/system.hpp) on a Context's device map: process() frames in stream order."""
+
+    def __init__(self, ctx: Context, cfg: "abi.SlamCfg"):
+        self.ctx = ctx
+        self.cfg = cfg
+        h = C.c_void_p()
+        rc = ctx.lib.gsf_slam_create(ctx.h, C.byref(cfg), C.byref(h))
+        if rc != GSF_OK:
+            raise ValueError("invalid SLAM configuration")
+        self.h = h
+        self.logs = []
+
+    def process(self, index: int, timestamp: float, rgb, depth) -> "abi.FrameLog":
+        log = abi.FrameLog()
+        r, d = _f32(rgb), _f32(depth)
+        self.ctx._check(self.ctx.lib.gsf_slam_process(self.h, index, timestamp, _ptr(r), _ptr(d), C.byref(log)))
+        self.ctx.P = int(self.ctx.lib.gsf_map_count(self.ctx.h))
+        self.ctx.K = int(self.ctx.lib.gsf_map_sh_coeffs(self.ctx.h))
+        self.logs.append(log)
+        return log
+
+    @property
+    def keyframes(self) -> int:
+        return int(self.ctx.lib.gsf_slam_keyframes(self.h))
+
+    @property
+    def degraded_frames(self) -> int:
+        return int(self.ctx.lib.gsf_slam_degraded_frames(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.gsf_slam_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -611,3 +611,93 @@ def test_checkpoint_roundtrip_and_format(gpu_ctx, orc, tmp_path):
     bad.write_bytes(b"NOTAMAP!" + raw[8:])
     with pytest.raises(RuntimeError, match="bad magic"):
         gpu_ctx.load_checkpoint(str(bad))
+
+
+def _room_frames(ctx, n, K, orbit=1440):
+    truth = api.synth_room(30000, 4.0, 3, 0)
+    ctx.upload(truth)
+    poses = api.synth_orbit(orbit, 1.0, 0.0)
+    frames = []
+    for f in range(n):
+        r = ctx.render(poses[f], K)
+        frames.append((r.color.copy(), np.where(r.opacity > 0.5, r.alpha_depth, 0.0).astype(np.float32)))
+    return frames, poses
+
+
+def _gt_relative(poses, n):
+    """pose_n o pose_0^-1: the world frame of a SLAM run is its first camera (system.cpp:69)."""
+    from scipy.spatial.transform import Rotation as R
+    R0 = R.from_rotvec(list(poses[0].rotation_tangent)).as_matrix()
+    Rn = R.from_rotvec(list(poses[n].rotation_tangent)).as_matrix()
+    Rr = Rn @ R0.T
+    return api.pose_of(R.from_matrix(Rr).as_rotvec(), np.array(list(poses[n].translation)) - Rr @ list(poses[0].translation))
+
+
+def test_slam_matches_oracle_orchestration(gpu_ctx, orc):
+    """SlamSystem::process (system.cpp:31-154) through gsf_slam_process vs the same sequence run by
+    oracle/slam.py over the fp64 oracle (bootstrap, velocity-model tracking, keyframe cycles with
+    map_step, sliding_ba, uncertainty pruning and spawning): same keyframes, same decisions, poses
+    within fp32-vs-fp64 drift of ~100 chained Adam steps."""
+    from paper_2403_16095_b200 import abi
+    from oracle.slam import OracleSlam
+    K = make_intrinsics(48, 36, 40.0, near=0.1, far=10.0)
+    frames, _ = _room_frames(gpu_ctx, 7, K)
+
+    def cfg():
+        c = abi.defaults_slam(K)
+        c.tracker.keyframe_interval = 3
+        c.tracker.iterations = 20
+        c.tracker.ba_iterations = 3
+        c.map_iterations = 10
+        c.init_iterations = 30
+        c.mapper.densify_interval = 0
+        c.seed = 5
+        return c
+    slam = api.SlamSystem(gpu_ctx, cfg())
+    ref = OracleSlam(cfg())
+    for f, (c, d) in enumerate(frames):
+        log = slam.process(f, f / 30.0, c, d)
+        p = ref.process(f, c, d)
+        assert log.keyframe == (1 if f % 3 == 0 else 0)
+        if f == 0:
+            assert log.primitives == ref.primitives    # the bootstrap back-projection is exact
+        else:
+            assert abs(log.primitives - ref.primitives) <= max(2, ref.primitives // 100), f
+        # fp32 vs fp64 over 15-20 chained Adam steps per frame: 1e-3 after the first tracked frame,
+        # growing to a few mm after two keyframe cycles (both arms sit ~0.1 m from the ground truth
+        # here: the alpha-depth geo term is biased while the young map is semi-transparent)
+        tol = 1e-3 if f <= 1 else 1e-2
+        assert translation_error(log.pose, p) < tol and rotation_error(log.pose, p) < tol / 2, f
+    assert slam.keyframes == len(ref.keyframes) == 3
+    slam.close()
+
+
+def test_slam_pipeline_on_synthetic_sequence(gpu_ctx, orc):
+    """SlamSystem end to end on a rendered orbit at the reference defaults (RunConfig, config.hpp:16-35):
+    the bootstrap map reproduces the first frame, tracking follows the ground-truth relative motion
+    over the first keyframe cycles, every stage reports its time."""
+    from paper_2403_16095_b200 import abi
+    K = make_intrinsics(96, 72, 80.0, near=0.1, far=10.0)
+    frames, poses = _room_frames(gpu_ctx, 11, K)
+    cfg = abi.defaults_slam(K)
+    cfg.tracker.keyframe_interval = 5
+    slam = api.SlamSystem(gpu_ctx, cfg)
+    for f, (c, d) in enumerate(frames):
+        log = slam.process(f, f / 30.0, c, d)
+        assert log.frame == f and log.primitives == gpu_ctx.P > 0
+    logs = slam.logs
+    assert slam.keyframes == 3 and [l.keyframe for l in logs] == [1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1]
+    assert logs[0].kf_psnr_db > 30.0 and logs[0].kf_depth_l1_cm < 5.0
+    assert all(np.isfinite(l.track_loss) and l.track_iterations == 15 for l in logs[1:])
+    for k in (5, 10):
+        assert logs[k].map_ms > 0 and logs[k].ba_ms > 0 and logs[k].uncertainty_ms > 0 and logs[k].spawn_ms > 0
+        assert logs[k].kf_psnr_db > 28.0 and logs[k].kf_depth_l1_cm < 3.0
+    assert logs[10].primitives > logs[5].primitives     # spawning filled the newly seen pixels
+    for f in range(1, 11):
+        gt = _gt_relative(poses, f)
+        assert translation_error(logs[f].pose, gt) < 0.12 and rotation_error(logs[f].pose, gt) < 0.03, f
+    with pytest.raises(ValueError):
+        bad = abi.defaults_slam(K)
+        bad.tracker.ba_window = 1                       # TrackerConfig::validate (tracker.cpp:12-24)
+        api.SlamSystem(gpu_ctx, bad)
+    slam.close()
