@@ -331,7 +331,12 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   }
   if (ws.bucket_cap == 0) ws.bucket_cap = 2048;
   if (!ws.bucket) dalloc(ws.bucket, static_cast<size_t>(ws.tiles_cap) * ws.bucket_cap);
-  if (!ws.pose_part) dalloc(ws.pose_part, static_cast<size_t>(std::max<int64_t>(div_up(ws.P_cap, 256), ws.tiles_cap)) * 6);
+  if (!ws.pose_part) {
+    dalloc(ws.pose_part, static_cast<size_t>(std::max<int64_t>(div_up(ws.P_cap, 256), 5 * ws.tiles_cap + 64)) * 6);
+    ws.wtickets_half = ws.tiles_cap / 8 + 8;   // groups of 32 rows over 4 rows per tile, + the top ticket
+    dalloc(ws.wtickets, 2 * ws.wtickets_half);
+    GSF_CUDA_CHECK(cudaMemset(ws.wtickets, 0, sizeof(uint32_t) * 2 * ws.wtickets_half));
+  }
   const int64_t red = 2 * std::max<int64_t>(div_up(npix, 256), div_up(P, 256)) + 64;
   if (!ws.red_part || ws.red_iso_offset * 2 < red) {
     dalloc(ws.red_part, red);
@@ -653,7 +658,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
   void* bufs[] = {ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
-                  ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.pj_id,
+                  ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
                   ws.red_part, c->bp_scratch, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
                   c->red_f};

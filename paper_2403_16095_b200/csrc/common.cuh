@@ -69,6 +69,73 @@ __device__ __forceinline__ uint32_t warp_block_mask(const BlendG& g, float tile_
   return mask;
 }
 
+// 8x8 variant for the two-pixels-per-lane tracking kernels: bit w (w < 4) says whether the
+// primitive can reach the 8x8 block (8 (w & 1), 8 (w >> 1)) of the tile.
+__device__ __forceinline__ uint32_t warp_block_mask8(const BlendG& g, float tile_x0, float tile_y0, const BlendConsts& kc) {
+  const float a = g.c00, b = 0.5f * g.c01x2, c = g.c11;
+  if (!(a > 0.0f) || !(c > 0.0f) || !(a * c > b * b)) return 0xfu;
+  if (g.sigma < kc.skip_lo) return 0u;
+  float thr = kc.rho_hi;
+  const float ra = 2.0f * __logf(g.sigma / kc.skip_lo);
+  thr = fminf(thr, ra);
+  thr = thr * 1.002f + 2e-3f;
+  uint32_t mask = 0u;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const float bx0 = tile_x0 + static_cast<float>(8 * (w & 1)) + 0.5f - g.mx;
+    const float by0 = tile_y0 + static_cast<float>(8 * (w >> 1)) + 0.5f - g.my;
+    if (quad_min_rect(a, b, c, bx0, bx0 + 7.0f, by0, by0 + 7.0f) <= thr) mask |= 1u << w;
+  }
+  return mask;
+}
+
+// One 8x8 block at pixel origin (bx0, by0): warp_block_mask8's test for a single block.
+__device__ __forceinline__ bool block_hit8(const BlendG& g, float bx0, float by0, const BlendConsts& kc) {
+  const float a = g.c00, b = 0.5f * g.c01x2, c = g.c11;
+  if (!(a > 0.0f) || !(c > 0.0f) || !(a * c > b * b)) return true;
+  if (g.sigma < kc.skip_lo) return false;
+  float thr = kc.rho_hi;
+  const float ra = 2.0f * __logf(g.sigma / kc.skip_lo);
+  thr = fminf(thr, ra);
+  thr = thr * 1.002f + 2e-3f;
+  const float x0 = bx0 + 0.5f - g.mx, y0 = by0 + 0.5f - g.my;
+  return quad_min_rect(a, b, c, x0, x0 + 7.0f, y0, y0 + 7.0f) <= thr;
+}
+
+// Ampere-style asynchronous global -> shared copies (cp.async, 16 bytes, L1-allocating).
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// pair_rho for two pixels in one column (same dx, dy = (dy_a, dy_b)) on packed FP32x2: each lane
+// performs pair_rho's operations in pair_rho's order, so rho.x / rho.y equal the scalar values.
+__device__ __forceinline__ float2 pair_rho2(float dx, float2 dy, const BlendG& g) {
+  const float a1 = __fmul_rn(g.c00, dx), b1 = __fmul_rn(g.c01x2, dx);
+  float2 t = __fmul2_rn(make_float2(g.c11, g.c11), dy);
+  t = __fmul2_rn(t, dy);
+  t = __ffma2_rn(make_float2(b1, b1), dy, t);
+  return __ffma2_rn(make_float2(a1, a1), make_float2(dx, dx), t);
+}
+
+// exp_neg_half_inrange (gsf_shared.cuh) of two values on packed FP32x2, bit-identical per lane.
+__device__ __forceinline__ float2 exp_neg_half_inrange2(float2 rho) {
+  const float2 y = __fmul2_rn(rho, make_float2(-0.72134752044448170368f, -0.72134752044448170368f));
+  const float nx = rintf(y.x), ny = rintf(y.y);
+  const float2 f = __fadd2_rn(y, make_float2(-nx, -ny));   // y - n, exactly fsub's result
+  float2 p = make_float2(1.5403530393381606e-4f, 1.5403530393381606e-4f);
+  p = __ffma2_rn(p, f, make_float2(1.3333558146428443e-3f, 1.3333558146428443e-3f));
+  p = __ffma2_rn(p, f, make_float2(9.6181291076284772e-3f, 9.6181291076284772e-3f));
+  p = __ffma2_rn(p, f, make_float2(5.5504108664821580e-2f, 5.5504108664821580e-2f));
+  p = __ffma2_rn(p, f, make_float2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
+  p = __ffma2_rn(p, f, make_float2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  return __fmul2_rn(p, make_float2(__int_as_float((127 + static_cast<int>(nx)) << 23),
+                                   __int_as_float((127 + static_cast<int>(ny)) << 23)));
+}
+
 // Loss partial slots written per tile by the fused blend epilogue (fixed order reduction).
 enum LossSlot {
   LS_COLOR_SUM = 0,   // sum |c - I| over the colour mask (tracking: opacity mask, mapping: all)

@@ -18,16 +18,16 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;
 }
 
-// out[0..NV) (shared) = column sums of part[rows][NV]; thread t owns rows t, t+256, ... so the
-// summation order is fixed.  Requires blockDim.x == 256; ends with a __syncthreads().
-template <int NV>
+// out[0..NV) (shared) = column sums of part[rows][NV]; thread t owns rows t, t+NT, ... so the
+// summation order is fixed.  Requires blockDim.x == NT; ends with a __syncthreads().
+template <int NV, int NT = 256>
 __device__ __forceinline__ void block_reduce_rows(const double* part, int rows, double* out, double (*s_red)[NV]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double acc[NV];
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = 0.0;
 #pragma unroll 4
-  for (int r = tid; r < rows; r += 256) {
+  for (int r = tid; r < rows; r += NT) {
     const double* row = part + static_cast<int64_t>(r) * NV;
 #pragma unroll
     for (int q = 0; q < NV; ++q) acc[q] += __ldcg(row + q);
@@ -41,7 +41,7 @@ __device__ __forceinline__ void block_reduce_rows(const double* part, int rows, 
   if (tid < NV) {
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += s_red[w][tid];
+    for (int w = 0; w < NT / 32; ++w) t += s_red[w][tid];
     out[tid] = t;
   }
   __syncthreads();
@@ -62,6 +62,53 @@ __device__ __forceinline__ bool last_cta(uint32_t* counter, int* s_flag, bool wr
   __syncthreads();
   if (*s_flag) __threadfence();
   return *s_flag != 0;
+}
+
+// Two-level fixed-order reduction for grids of single-warp CTAs (blockDim.x == 32): CTA r wrote
+// row part[r][NV].  The last CTA of each group of 32 consecutive rows sums the group (lane l takes
+// row l, then a fixed shuffle tree) into gpart[g]; the last group sums gpart the same way.  Returns
+// true in exactly one CTA, whose lane 0 then holds the totals in out[NV].  gt[] (one ticket per
+// group) and *top must be zero before the launch; they are re-zeroed here.
+template <int NV>
+__device__ __forceinline__ bool warp_grid_reduce(const double* part, double* gpart, int rows, uint32_t* gt, uint32_t* top,
+                                                 double* out, bool wrote) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x, g = r >> 5, g0 = g << 5, gn = min(32, rows - g0);
+  const int ngroups = (rows + 31) >> 5;
+  if (wrote) __threadfence();
+  __syncwarp();
+  unsigned last = 0;
+  if (lane == 0) {
+    last = atomicAdd(&gt[g], 1u) == static_cast<unsigned>(gn - 1);
+    if (last) gt[g] = 0u;
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return false;
+  __threadfence();
+  double v[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = lane < gn ? __ldcg(part + static_cast<int64_t>(g0 + lane) * NV + q) : 0.0;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum_f64(v[q]);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) gpart[static_cast<int64_t>(g) * NV + q] = v[q];
+    __threadfence();
+    last = atomicAdd(top, 1u) == static_cast<unsigned>(ngroups - 1);
+    if (last) *top = 0u;
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return false;
+  __threadfence();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = 0.0;
+  for (int i = lane; i < ngroups; i += 32)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] += __ldcg(gpart + static_cast<int64_t>(i) * NV + q);
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    v[q] = warp_sum_f64(v[q]);
+    if (lane == 0) out[q] = v[q];
+  }
+  return true;
 }
 
 // Scalar tails of the tracking (mode 1) and mapping (mode 2) losses; thread 0 only.

@@ -473,7 +473,7 @@ GSF_HD uint32_t depth_key(double depth, uint32_t near_bits) {
 // ---------------------------------------------------------------------------------------
 struct BlendG {       // per visible primitive, rank order, 3 x float4 on the device
   float mx, my, depth, sigma;
-  float c00, c01x2, c11, pad0;
+  float c00, c01x2, c11, rho_fast;   // rho_fast: blend_rho_fast
   float r, g, b, depth_b;   // depth_b = depth again: (b, depth) pair for packed FMAs
 };
 struct GuardG {       // fp64 copies read only inside the guard band
@@ -488,7 +488,7 @@ GSF_HD BlendG make_blend_g(const PreOut& o) {
   g.c00 = static_cast<float>(o.c00);
   g.c01x2 = static_cast<float>(dmul(2.0, o.c01));
   g.c11 = static_cast<float>(o.c11);
-  g.pad0 = -1.0f;   // rho_fast, filled by blend_rho_fast once the raster constants are known
+  g.rho_fast = -1.0f;   // filled by blend_rho_fast once the raster constants are known
   g.r = static_cast<float>(o.color[0]);
   g.g = static_cast<float>(o.color[1]);
   g.b = static_cast<float>(o.color[2]);
@@ -592,14 +592,20 @@ GSF_HD PairEval eval_pair_full(float px, float py, const BlendG& g, const GuardG
   return e;
 }
 
-// Per-primitive fast-path bound (stored in BlendG::pad0): for rho in [rho_min, rho_fast) the full
-// decision is certainly "contributes, unclamped, alpha = sigma*exp(-rho/2)" — rho is below the
-// guard band, alpha is above the skip band (margin 1e-5 in log space, >> the exp error of 3e-7)
-// and sigma is below the clamp band.  -1 disables the fast path.  Only selects the evaluation
-// path, never a result, so the mirror and the kernels stay bit-identical either way.
-GSF_HD float blend_rho_fast(float sigma, const BlendConsts& k) {
+// Per-primitive fast-path bound (BlendG::rho_fast): for rho < rho_fast the full decision is
+// certainly "contributes, unclamped, alpha = sigma*exp(-rho/2)" — rho is below the cutoff guard
+// band, alpha is above the skip band (margin 1e-5 in log space, >> the exp error of 3e-7) and
+// sigma is below the clamp band.  No lower bound is needed: the fp64 guard for rho < rho_min only
+// rejects rho_d < 0, and for a conic with det >= 1e-5 c00 c11 (condition number < 4e5, in fp32 and
+// hence in fp64) the fp64 quadratic form is non-negative everywhere (its rounding error is < 1e-15
+// of its largest term), so there the guard never fires.  -1 disables the fast path.  Only selects
+// the evaluation path, never a result, so the mirror and the kernels stay bit-identical either way.
+GSF_HD float blend_rho_fast(const BlendG& g, const BlendConsts& k) {
+  const float sigma = g.sigma;
   if (!k.fast_ok || !(static_cast<double>(sigma) * (1.0 + 1e-6) < static_cast<double>(k.clamp_lo))) return -1.0f;
   if (!(sigma > k.skip_hi)) return -1.0f;
+  const double a = g.c00, b = 0.5 * static_cast<double>(g.c01x2), c = g.c11;
+  if (!(a > 0.0 && c > 0.0 && a * c - b * b >= 1e-5 * a * c)) return -1.0f;
   const double ra = 2.0 * (log(static_cast<double>(sigma) / static_cast<double>(k.skip_hi)) - 1e-5);
   const double r = ra < static_cast<double>(k.rho_lo) ? ra : static_cast<double>(k.rho_lo);
   return r > 0.0 ? static_cast<float>(r * (1.0 - 1e-6)) : -1.0f;
@@ -641,7 +647,7 @@ GSF_HD PairEval eval_pair_t(float px, float py, const BlendG& g, const GuardG* g
   e.alpha = 0.0f;
   e.gval = 0.0f;
   if (rho > k.rho_hi) return e;
-  if (rho < g.pad0 && rho >= k.rho_min) {
+  if (rho < g.rho_fast) {
     e.gval = FAST ? exp_neg_half_fast(rho) : exp_neg_half_inrange(rho);
     e.alpha = fmul(g.sigma, e.gval);
     e.code = 1;

@@ -100,7 +100,9 @@ struct Workspace {
   float* dssim = nullptr;       // 3*npix: d(w_ssim * ssim loss)/d colour (mapping)
   float* ssim_tmp = nullptr;    // SSIM scratch maps (see loss.cu)
   // temporaries
-  double* pose_part = nullptr;  // chain blocks * 6 (or tiles * 6 for the fused tracking backward)
+  double* pose_part = nullptr;  // chain blocks * 6 (or 4 tiles * 6 + group rows for the tracking backward)
+  uint32_t* wtickets = nullptr; // zeroed group tickets of the single-warp grid reductions (self-resetting)
+  int64_t wtickets_half = 0;    // entries per region: [0, half) blend, [half, 2 half) backward
   double* red_part = nullptr;   // generic per-block fp64 partials (ssim, then iso)
   int64_t red_iso_offset = 0;
   int ssim_blocks = 0, iso_blocks = 0;

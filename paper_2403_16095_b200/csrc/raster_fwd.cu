@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
       if (o.visible) {
         vis = true;
         BlendG g = make_blend_g(o);
-        g.pad0 = blend_rho_fast(g.sigma, kc);
+        g.rho_fast = blend_rho_fast(g, kc);
         bg_id[i] = g;
         gg_id[i] = make_guard_g(o);
         depth_id[i] = o.depth;
@@ -526,6 +526,158 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
   }
 }
 
+// Tracking forward (k_blend<1>'s maps and fused loss) with two pixels per lane: warp w of the
+// 128-thread CTA owns the 8x8 block (8 (w & 1), 8 (w >> 1)) of the tile and lane l the pixels
+// (l & 7, l >> 3) and (l & 7, (l >> 3) + 4).  Both pixels share dx, so rho and exp run on packed
+// FP32x2 and every per-entry cost (ballot walk, staging reads) is paid once for two pixels; an
+// 8x8 block meets ~0.6x as many (block, entry) pairs as two 8x4 blocks.  Each packed lane rounds
+// like the scalar op in the scalar order, and a pixel that does not take an entry sees alpha 0
+// (w = 0, T * 1): the maps equal k_blend<1>'s, and the mirror's, bit for bit.
+constexpr int kTrkThreads = 128;
+constexpr int kTrkBatch = 256;
+
+// guard-band entries (rare): eval_pair's full decision out of line, keeping the hot loop's registers
+// (g is re-read from shared memory and kc read through a pointer, so the hot loop keeps no stack copies)
+static __device__ __noinline__ float guard_alpha(float px, float py, const BlendG* gs, const GuardG* gp, const BlendConsts* kc) {
+  const PairEval e = eval_pair_full(px, py, *gs, gp, *kc);
+  return e.code ? e.alpha : -1.0f;
+}
+
+#ifndef GSF_TRK_MINB
+#define GSF_TRK_MINB 8
+#endif
+__global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
+    const int2* __restrict__ ranges, const uint32_t* __restrict__ sid, const BlendG* __restrict__ bg,
+    const GuardG* __restrict__ gg, const float* __restrict__ loss_rgb, const float* __restrict__ loss_depth, int W, int H,
+    int tiles_x, BlendConsts kc, double near_plane, double far_plane, LossParams lp, DevState* ds,
+    float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_op, float* __restrict__ o_T,
+    int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket) {
+  __shared__ BlendG s_g[kTrkBatch];
+  __shared__ int32_t s_id[kTrkBatch];
+  __shared__ uint8_t s_mask[kTrkBatch];
+  __shared__ double s_red[kTrkThreads / 32][LS_NUM];
+  if (ds->halt) return;
+  const int tile = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int x = tx * kTile + 8 * (warp & 1) + (lane & 7);
+  const int ya = ty * kTile + 8 * (warp >> 1) + (lane >> 3), yb = ya + 4;
+  const bool in_a = x < W && ya < H, in_b = x < W && yb < H;
+  const int2 rg = ranges[tile];
+  float2 rg_a = make_float2(0.f, 0.f), bd_a = rg_a, rg_b = rg_a, bd_b = rg_a;
+  float2 op = make_float2(0.f, 0.f), T = make_float2(1.f, 1.f);
+  int last_a = 0, last_b = 0;
+  bool done_a = !in_a, done_b = !in_b;
+  const float px = static_cast<float>(x) + 0.5f;
+  const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
+  const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
+  for (int start = rg.x; start < rg.y; start += kTrkBatch) {
+    if (__syncthreads_and(done_a && done_b)) break;
+#pragma unroll
+    for (int h = 0; h < kTrkBatch / kTrkThreads; ++h) {
+      const int e = tid + h * kTrkThreads, j = start + e;
+      if (j < rg.y) {
+        const int id = static_cast<int>(sid[j]);
+        const BlendG gj = bg[id];
+        s_g[e] = gj;
+        s_id[e] = id;
+        s_mask[e] = static_cast<uint8_t>(warp_block_mask8(gj, tile_x0, tile_y0, kc));
+      }
+    }
+    __syncthreads();
+    const int cnt = min(kTrkBatch, rg.y - start);
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      if (__all_sync(0xffffffffu, done_a && done_b)) break;
+      const int kk = c0 + lane;
+      uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
+      while (bits) {
+        const int k = c0 + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const BlendG g = s_g[k];
+        const float dx = __fadd_rn(px, -g.mx);
+        const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
+        const float2 rho = pair_rho2(dx, dy, g);
+        const bool skip_a = done_a || rho.x > kc.rho_hi, skip_b = done_b || rho.y > kc.rho_hi;
+        if (skip_a && skip_b) continue;
+        const bool fast_a = rho.x < g.rho_fast, fast_b = rho.y < g.rho_fast;
+        float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), exp_neg_half_inrange2(rho));
+        bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
+        if (!skip_a && !fast_a) {   // guard band: eval_pair's full decision
+          al.x = guard_alpha(px, py.x, s_g + k, gg + s_id[k], &kc);
+          ca = al.x >= 0.0f;
+        }
+        if (!skip_b && !fast_b) {
+          al.y = guard_alpha(px, py.y, s_g + k, gg + s_id[k], &kc);
+          cb = al.y >= 0.0f;
+        }
+        const float2 am = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
+        const float2 w = __fmul2_rn(am, T);
+        rg_a = __ffma2_rn(make_float2(w.x, w.x), make_float2(g.r, g.g), rg_a);
+        bd_a = __ffma2_rn(make_float2(w.x, w.x), make_float2(g.b, g.depth_b), bd_a);
+        rg_b = __ffma2_rn(make_float2(w.y, w.y), make_float2(g.r, g.g), rg_b);
+        bd_b = __ffma2_rn(make_float2(w.y, w.y), make_float2(g.b, g.depth_b), bd_b);
+        op = __fadd2_rn(op, w);
+        T = __fmul2_rn(T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-am.x, -am.y)));
+        const int li = start + k - rg.x + 1;
+        if (ca) last_a = li;
+        if (cb) last_b = li;
+        done_a = done_a || T.x < kc.term;
+        done_b = done_b || T.y < kc.term;
+      }
+    }
+  }
+  double v[LS_NUM], vb[LS_NUM];
+#pragma unroll
+  for (int q = 0; q < LS_NUM; ++q) v[q] = vb[q] = 0.0;
+  if (in_a) {
+    const int64_t pi = static_cast<int64_t>(ya) * W + x;
+    o_color[3 * pi + 0] = rg_a.x;
+    o_color[3 * pi + 1] = rg_a.y;
+    o_color[3 * pi + 2] = bd_a.x;
+    o_ad[pi] = bd_a.y;
+    o_op[pi] = op.x;
+    o_T[pi] = T.x;
+    o_last[pi] = last_a;
+    if (loss_rgb)
+      loss_pixel<1>(v, rg_a.x, rg_a.y, bd_a.x, bd_a.y, 0.0f, false, op.x, 0.0f, loss_rgb + 3 * pi, loss_depth, pi, false,
+                    near_plane, far_plane, lp.opacity_floor);
+  }
+  if (in_b) {
+    const int64_t pi = static_cast<int64_t>(yb) * W + x;
+    o_color[3 * pi + 0] = rg_b.x;
+    o_color[3 * pi + 1] = rg_b.y;
+    o_color[3 * pi + 2] = bd_b.x;
+    o_ad[pi] = bd_b.y;
+    o_op[pi] = op.y;
+    o_T[pi] = T.y;
+    o_last[pi] = last_b;
+    if (loss_rgb)
+      loss_pixel<1>(vb, rg_b.x, rg_b.y, bd_b.x, bd_b.y, 0.0f, false, op.y, 0.0f, loss_rgb + 3 * pi, loss_depth, pi, false,
+                    near_plane, far_plane, lp.opacity_floor);
+  }
+  if (!loss_rgb) return;
+#pragma unroll
+  for (int q = 0; q < LS_NUM; ++q) {
+    const double t = warp_sum_d(v[q] + vb[q]);
+    if (lane == 0) s_red[warp][q] = t;
+  }
+  __syncthreads();
+  if (tid < LS_NUM) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kTrkThreads / 32; ++w) t += s_red[w][tid];
+    loss_part[static_cast<int64_t>(tile) * LS_NUM + tid] = t;
+  }
+  if (fuse_final) {
+    __shared__ int s_last;
+    __shared__ double s_tot[LS_NUM];
+    if (last_cta(ticket, &s_last, tid < LS_NUM)) {
+      block_reduce_rows<LS_NUM, kTrkThreads>(loss_part, gridDim.x, s_tot, s_red);
+      if (tid == 0) loss_scalars(ds, lp, s_tot, 0.0, 0.0, static_cast<int64_t>(W) * H, iteration);
+    }
+  }
+}
+
 // Stand-alone loss partials over stored maps (evaluate_*_loss called on a RenderResult).
 template <int LMODE>
 __global__ void __launch_bounds__(256) k_loss_tiles(const float* __restrict__ color, const float* __restrict__ ad,
@@ -596,8 +748,11 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
       ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w, ws.last, ws.loss_part, \
       a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket
   if (pf) pf->begin(PROF_BLEND, st);
-  if (a.lp.mode == 1 && loss_rgb)
-    k_blend<1><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
+  if (a.lp.mode == 1 && loss_rgb)   // k_blend<1>'s outputs, two pixels per lane
+    k_blend_track<<<ntiles, kTrkThreads, 0, st>>>(ws.ranges, ws.sid, ws.bg_id, ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,
+                                                  tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color,
+                                                  ws.alpha_depth, ws.opacity, ws.final_T, ws.last, ws.loss_part,
+                                                  a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket);
   else if (a.lp.mode == 2 && loss_rgb)
     k_blend<2><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
   else

@@ -290,6 +290,30 @@ def test_tracking_pose_gradient_vs_oracle(gpu_ctx, orc, sh):
         _pose_close(g, go.d_pose)
 
 
+def test_tracking_forward_maps_equal_plain_render(gpu_ctx, orc):
+    """The tracking loop's forward (two pixels per lane, packed FP32x2, fused loss) leaves colour,
+    alpha depth and opacity maps bit-identical to the plain render's (itself bit-exact vs the
+    mirror): the tracking loss and its adjoint maps evaluated on either are equal."""
+    rng = np.random.default_rng(77)
+    for seed, (P, w_, h_, f) in enumerate([(150, 64, 48, 55.0), (2500, 150, 110, 120.0), (6000, 97, 61, 70.0)]):
+        m = f32_round(orc.random_scene(5000 + seed, P, 1, 0.95, 0.01, 0.3))
+        K = make_intrinsics(w_, h_, f)
+        _upload(gpu_ctx, m)
+        gt = gpu_ctx.render(pose(), K)
+        depth = gt.alpha_depth.copy()
+        depth.ravel()[::7] = 0.0
+        gpu_ctx.frame_upload(0, gt.color, depth, w_, h_)
+        p = perturbed(pose(), 0.02 * rng.standard_normal(6))
+        w = defaults_weights(True)
+        terms, _ = gpu_ctx.tracking_gradient(0, p, K, w)
+        a, dca, dda = gpu_ctx.evaluate_tracking_loss(gt.color, depth, w)
+        gpu_ctx.render(p, K)
+        b, dcb, ddb = gpu_ctx.evaluate_tracking_loss(gt.color, depth, w)
+        assert (a.total, a.color, a.geo, a.valid_color, a.valid_geo) == (b.total, b.color, b.geo, b.valid_color, b.valid_geo)
+        assert np.array_equal(dca, dcb) and np.array_equal(dda, ddb)
+        assert terms.total == pytest.approx(b.total, rel=1e-12) and terms.valid_color == b.valid_color
+
+
 def test_mapping_loss_kat_on_gpu(gpu_ctx, orc):
     """test_losses.cpp:169-198 through the CUDA path."""
     e = golden("reference_kats.json")["mapping_loss_single_pixel"]["expect"]
