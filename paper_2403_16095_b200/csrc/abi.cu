@@ -325,7 +325,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     ws.tile_fill = ws.bins;
     ws.bin_counters = ws.bins + tiles * kBinStride;
     dfree(ws.bucket);
-    dalloc(ws.loss_part, tiles * LS_NUM);
+    dalloc(ws.loss_part, (5 * tiles + 64) * LS_NUM);
     ws.tiles_cap = tiles;
     dfree(ws.pose_part);
   }

@@ -110,6 +110,24 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Guard-band entries (rare) of the two-pixel kernels: eval_pair_full out of line.  Takes the
+// record's geometry by value (the caller's registers; nothing is materialised on the hot path) and
+// kc through a pointer.  alpha < 0: no contribution.
+struct GuardOut {
+  float alpha, gval;
+  int clamped;
+};
+static __device__ __noinline__ GuardOut guard_full(float px, float py, float mx, float my, float c00, float c01x2,
+                                                   float c11, float sigma, const GuardG* gp, const BlendConsts* kc) {
+  BlendG g;
+  g.mx = mx; g.my = my; g.c00 = c00; g.c01x2 = c01x2; g.c11 = c11; g.sigma = sigma;
+  const PairEval e = eval_pair_full(px, py, g, gp, *kc);
+  return GuardOut{e.code ? e.alpha : -1.0f, e.gval, e.clamped};
+}
+__device__ __forceinline__ GuardOut guard_decide(float px, float py, const BlendG& g, const GuardG* gp, const BlendConsts* kc) {
+  return guard_full(px, py, g.mx, g.my, g.c00, g.c01x2, g.c11, g.sigma, gp, kc);
+}
+
 // pair_rho for two pixels in one column (same dx, dy = (dy_a, dy_b)) on packed FP32x2: each lane
 // performs pair_rho's operations in pair_rho's order, so rho.x / rho.y equal the scalar values.
 __device__ __forceinline__ float2 pair_rho2(float dx, float2 dy, const BlendG& g) {

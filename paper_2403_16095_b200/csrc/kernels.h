@@ -75,7 +75,8 @@ struct Workspace {
   uint32_t* pair_base = nullptr;      // P: first primitive-major pair slot of a visible primitive
   uint32_t* tile_start = nullptr;
   int2* ranges = nullptr;
-  double* loss_part = nullptr;  // tiles * LS_NUM
+  double* loss_part = nullptr;  // rows * LS_NUM (+ group rows of the single-warp tracking blend)
+  int loss_rows = 0;            // rows the last loss-partial producer wrote (tiles, or 4 tiles)
   // per (tile, primitive) pair: scattered keys/ids, then each tile's list sorted by (depth, id)
   unsigned long long* bucket = nullptr; // tiles * bucket_cap keys (fp32 depth bits << 32 | id), scatter order
   int64_t bucket_cap = 0;

@@ -267,6 +267,7 @@ void run_loss_finalize(Workspace& ws, DevState* ds, const LossParams& lp, int ti
   // red_part layout: [0, 4096) ssim block partials, [4096, 8192+) iso block partials
   const int ssim_blocks = lp.mode == 2 && lp.w_ssim > 0.0 ? ws.ssim_blocks : 0;
   const int iso_blocks = lp.mode == 2 ? ws.iso_blocks : 0;
+  if (ws.loss_rows > 0) tiles = ws.loss_rows;   // the producer's row count (4 per tile for k_blend_track_w)
   k_loss_finalize<<<1, 256, 0, st>>>(ws.loss_part, tiles, npix, lp, iteration, ws.red_part, ssim_blocks,
                                      ws.red_part + ws.red_iso_offset, iso_blocks, ds);
   ++*L;

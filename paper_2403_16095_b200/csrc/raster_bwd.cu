@@ -481,17 +481,6 @@ constexpr int kTbThreads = 128;
 constexpr int kTbBatch = GSF_TB_BATCH;
 constexpr size_t kTbSmem = static_cast<size_t>(kTbBatch) * (sizeof(BlendG) + 9 * sizeof(float4) + sizeof(int32_t) + 1);
 
-// guard-band entries (rare), out of line: alpha (or -1: no contribution), gval, clamped.  g is
-// re-read from shared memory and kc read through a pointer, so the hot loop keeps no stack copies.
-struct GuardOut {
-  float alpha, gval;
-  int clamped;
-};
-static __device__ __noinline__ GuardOut guard_eval(float px, float py, const BlendG* gs, const GuardG* gp, const BlendConsts* kc) {
-  const PairEval e = eval_pair_full(px, py, *gs, gp, *kc);
-  return GuardOut{e.code ? e.alpha : -1.0f, e.gval, e.clamped};
-}
-
 #ifndef GSF_TB_MINB
 #define GSF_TB_MINB 8
 #endif
@@ -578,14 +567,14 @@ __global__ void __launch_bounds__(kTbThreads, GSF_TB_MINB) k_backward_track(BwdP
         bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
         int cl_a = 0, cl_b = 0;
         if (!skip_a && !fast_a) {
-          const GuardOut o = guard_eval(px, py.x, s_g + k, bp.gg + s_id[k], &kc);
+          const GuardOut o = guard_decide(px, py.x, g, bp.gg + s_id[k], &kc);
           al.x = o.alpha;
           gv.x = o.gval;
           cl_a = o.clamped;
           ca = al.x >= 0.0f;
         }
         if (!skip_b && !fast_b) {
-          const GuardOut o = guard_eval(px, py.y, s_g + k, bp.gg + s_id[k], &kc);
+          const GuardOut o = guard_decide(px, py.y, g, bp.gg + s_id[k], &kc);
           al.y = o.alpha;
           gv.y = o.gval;
           cl_b = o.clamped;
@@ -733,14 +722,14 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
         int cl_a = 0, cl_b = 0;
         if (!skip_a && !fast_a) {
-          const GuardOut o = guard_eval(px, py.x, s_g + k, bp.gg + s_id[k], &kc);
+          const GuardOut o = guard_decide(px, py.x, g, bp.gg + s_id[k], &kc);
           al.x = o.alpha;
           gv.x = o.gval;
           cl_a = o.clamped;
           ca = al.x >= 0.0f;
         }
         if (!skip_b && !fast_b) {
-          const GuardOut o = guard_eval(px, py.y, s_g + k, bp.gg + s_id[k], &kc);
+          const GuardOut o = guard_decide(px, py.y, g, bp.gg + s_id[k], &kc);
           al.y = o.alpha;
           gv.y = o.gval;
           cl_b = o.clamped;
@@ -788,179 +777,6 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       pd[0] += pa.x; pd[1] += pa.y; pd[2] += pb2.x; pd[3] += pb2.y; pd[4] += pc2.x; pd[5] += pc2.y;
       __syncwarp();
     }
-  }
-#pragma unroll
-  for (int a = 0; a < 6; ++a) pd[a] = warp_sum_f64(pd[a]);
-  if (lane == 0)
-#pragma unroll
-    for (int a = 0; a < 6; ++a) bp.tile_pose[static_cast<size_t>(blockIdx.x) * 6 + a] = pd[a];
-  double tot[6];
-  if (warp_grid_reduce<6>(bp.tile_pose, bp.tile_pose + static_cast<size_t>(rows) * 6, rows, gtickets,
-                          gtickets + (rows + 31) / 32, tot, lane == 0) && lane == 0)
-#pragma unroll
-    for (int a = 0; a < 6; ++a) ds->d_pose[a] = ds->halt ? 0.0 : tot[a];
-}
-
-// k_backward_track_w with its staging software-pipelined through cp.async: while chunk c is
-// processed, the pose matrices of chunk c+1 (whose entries were tested against the block one
-// iteration earlier) and the BlendG records of chunk c+2 are in flight, and the list ids of chunk
-// c+3 and pose-matrix slots of chunk c+2 are loading into registers.  One cp.async.wait_all per
-// chunk; the four dependent global reads (id -> record, id -> slot -> matrix) never stall a chunk.
-#ifndef GSF_TBP_MINB
-#define GSF_TBP_MINB 16
-#endif
-__global__ void __launch_bounds__(32, GSF_TBP_MINB) k_backward_track_p(BwdPtrs bp, int W, int H, int tiles_x,
-                                                                      BlendConsts kc, double near_plane,
-                                                                      double far_plane, LossParams lp, DevState* ds,
-                                                                      uint32_t* gtickets, int rows) {
-  __shared__ BlendG s_g[3][32];
-  __shared__ int32_t s_id[3][32];
-  __shared__ float4 s_pj[2][32][9];
-  const int lane = threadIdx.x;
-  const int tile = blockIdx.x >> 2, qd = blockIdx.x & 3;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int x = tx * kTile + 8 * (qd & 1) + (lane & 7);
-  const int ya = ty * kTile + 8 * (qd >> 1) + (lane >> 3), yb = ya + 4;
-  const bool in_a = x < W && ya < H, in_b = x < W && yb < H;
-  double pd[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  if (!ds->halt) {
-    const int2 rg = bp.ranges[tile];
-    const PixBwd qa = load_pixel_bwd<SEED_TRACK>(bp, static_cast<int64_t>(ya) * W + x, in_a, lp, ds, near_plane, far_plane);
-    const PixBwd qb = load_pixel_bwd<SEED_TRACK>(bp, static_cast<int64_t>(yb) * W + x, in_b, lp, ds, near_plane, far_plane);
-    const int last_a = qa.last, last_b = qb.last;
-    const int maxlast = __reduce_max_sync(0xffffffffu, max(last_a, last_b));
-    const int nch = (maxlast + 31) >> 5;
-    const int top = rg.x + maxlast;   // chunk c = entries [max(rg.x, top - 32 (c + 1)), top - 32 c)
-    auto cstart = [&](int c) { return max(rg.x, top - 32 * (c + 1)); };
-    auto ccnt = [&](int c) { return c < nch ? top - 32 * c - max(rg.x, top - 32 * (c + 1)) : 0; };
-    const float2 gc0 = make_float2(qa.gc0, qb.gc0), gc1 = make_float2(qa.gc1, qb.gc1), gc2 = make_float2(qa.gc2, qb.gc2),
-                 gad = make_float2(qa.gad, qb.gad);
-    const float px = static_cast<float>(x) + 0.5f;
-    const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
-    const float bx0 = static_cast<float>(tx * kTile + 8 * (qd & 1)), by0 = static_cast<float>(ty * kTile + 8 * (qd >> 1));
-    auto issue_bg = [&](int c, int id) {
-      if (lane < ccnt(c)) {
-        const float4* src = reinterpret_cast<const float4*>(bp.bg + id);
-        float4* dst = reinterpret_cast<float4*>(&s_g[c % 3][lane]);
-        cp_async16(dst, src);
-        cp_async16(dst + 1, src + 1);
-        cp_async16(dst + 2, src + 2);
-        s_id[c % 3][lane] = id;
-      }
-    };
-    auto issue_pj = [&](int c, uint32_t hit, uint32_t slot) {
-      if ((hit >> lane) & 1u) {
-        const float4* src = reinterpret_cast<const float4*>(bp.pj) + (kPjFloats / 4) * static_cast<size_t>(slot);
-#pragma unroll
-        for (int j = 0; j < 9; ++j) cp_async16(&s_pj[c & 1][lane][j], src + j);
-      }
-    };
-    auto test_hits = [&](int c) {
-      return __ballot_sync(0xffffffffu, lane < ccnt(c) && block_hit8(s_g[c % 3][lane], bx0, by0, kc));
-    };
-    // prologue: chunks 0 and 1 staged, matrices of chunk 0 requested
-    int id0 = lane < ccnt(0) ? static_cast<int>(bp.sid[cstart(0) + lane]) : 0;
-    int id1 = lane < ccnt(1) ? static_cast<int>(bp.sid[cstart(1) + lane]) : 0;
-    int idA = lane < ccnt(2) ? static_cast<int>(bp.sid[cstart(2) + lane]) : 0;   // chunk c + 2
-    const uint32_t slot0 = lane < ccnt(0) ? bp.pj_slot[id0] : 0u;
-    uint32_t slotA = lane < ccnt(1) ? bp.pj_slot[id1] : 0u;                      // chunk c + 1
-    issue_bg(0, id0);
-    issue_bg(1, id1);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncwarp();
-    uint32_t hit = test_hits(0);
-    issue_pj(0, hit, slot0);
-    cp_async_commit();
-    float2 T = make_float2(qa.T, qb.T), S = make_float2(0.f, 0.f);
-    for (int c = 0; c < nch; ++c) {
-      cp_async_wait_all();   // matrices of chunk c, records of chunk c + 1
-      __syncwarp();
-      const uint32_t hit_n = test_hits(c + 1);
-      issue_pj(c + 1, hit_n, slotA);
-      const uint32_t slotB = lane < ccnt(c + 2) ? bp.pj_slot[idA] : 0u;
-      const int idB = lane < ccnt(c + 3) ? static_cast<int>(bp.sid[cstart(c + 3) + lane]) : 0;
-      issue_bg(c + 2, idA);
-      cp_async_commit();
-      const int bstart = cstart(c);
-      const BlendG* sg = s_g[c % 3];
-      const int32_t* sidc = s_id[c % 3];
-      float2 pa = make_float2(0.f, 0.f), pb2 = make_float2(0.f, 0.f), pc2 = make_float2(0.f, 0.f);
-      uint32_t bits = hit;
-      while (bits) {
-        const int k = 31 - __clz(bits);
-        bits &= ~(1u << k);
-        const int li = bstart + k - rg.x;
-        const BlendG g = sg[k];
-        const float dx = __fadd_rn(px, -g.mx);
-        const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
-        const float2 rho = pair_rho2(dx, dy, g);
-        const bool skip_a = li >= last_a || rho.x > kc.rho_hi, skip_b = li >= last_b || rho.y > kc.rho_hi;
-        if (skip_a && skip_b) continue;
-        const bool fast_a = rho.x < g.rho_fast, fast_b = rho.y < g.rho_fast;
-        float2 gv = make_float2(exp_neg_half_fast(rho.x), exp_neg_half_fast(rho.y));
-        float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), gv);
-        bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
-        int cl_a = 0, cl_b = 0;
-        if (!skip_a && !fast_a) {
-          const GuardOut o = guard_eval(px, py.x, sg + k, bp.gg + sidc[k], &kc);
-          al.x = o.alpha;
-          gv.x = o.gval;
-          cl_a = o.clamped;
-          ca = al.x >= 0.0f;
-        }
-        if (!skip_b && !fast_b) {
-          const GuardOut o = guard_eval(px, py.y, sg + k, bp.gg + sidc[k], &kc);
-          al.y = o.alpha;
-          gv.y = o.gval;
-          cl_b = o.clamped;
-          cb = al.y >= 0.0f;
-        }
-        if (!ca && !cb) continue;
-        const float2 am = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
-        const float2 inv = make_float2(rcp_approx(1.0f - am.x), rcp_approx(1.0f - am.y));
-        const float2 Tpre = __fmul2_rn(T, inv);
-        float2 q = __fmul2_rn(gc0, make_float2(g.r, g.r));
-        q = __ffma2_rn(gc1, make_float2(g.g, g.g), q);
-        q = __ffma2_rn(gc2, make_float2(g.b, g.b), q);
-        q = __ffma2_rn(gad, make_float2(g.depth, g.depth), q);
-        const float2 dal = __ffma2_rn(Tpre, q, __fmul2_rn(make_float2(-S.x, -S.y), inv));
-        const float2 w = __fmul2_rn(am, Tpre);
-        S = __ffma2_rn(w, q, S);
-        T = make_float2(ca ? Tpre.x : T.x, cb ? Tpre.y : T.y);
-        float2 gdg = __fmul2_rn(__fmul2_rn(gv, dal), make_float2(g.sigma, g.sigma));
-        gdg = make_float2(ca && !cl_a ? gdg.x : 0.0f, cb && !cl_b ? gdg.y : 0.0f);
-        const float c01 = 0.5f * g.c01x2;
-        const float2 ux = __ffma2_rn(make_float2(c01, c01), dy, make_float2(g.c00 * dx, g.c00 * dx));
-        const float2 uy = __ffma2_rn(make_float2(g.c11, g.c11), dy, make_float2(c01 * dx, c01 * dx));
-        const float2 s0 = __fmul2_rn(gdg, ux), s1 = __fmul2_rn(gdg, uy);
-        const float2 s2 = __fmul2_rn(s0, ux), s3 = __fmul2_rn(s0, uy), s4 = __fmul2_rn(s1, uy);
-        const float2 s5 = __fmul2_rn(w, gad);
-        const float f0 = s0.x + s0.y, f1 = s1.x + s1.y, f2 = s2.x + s2.y, f3 = s3.x + s3.y, f4 = s4.x + s4.y,
-                    f5 = s5.x + s5.y;
-        const float4* M = s_pj[c & 1][k];
-#define GSF_COL(F4A, F4B, F4C, SV)                   \
-        {                                            \
-          const float2 sv = make_float2(SV, SV);     \
-          pa = __ffma2_rn(sv, F4A, pa);              \
-          pb2 = __ffma2_rn(sv, F4B, pb2);            \
-          pc2 = __ffma2_rn(sv, F4C, pc2);            \
-        }
-        const float4 m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3], m4 = M[4], m5 = M[5], m6 = M[6], m7 = M[7], m8 = M[8];
-        GSF_COL(make_float2(m0.x, m0.y), make_float2(m0.z, m0.w), make_float2(m1.x, m1.y), f0)
-        GSF_COL(make_float2(m1.z, m1.w), make_float2(m2.x, m2.y), make_float2(m2.z, m2.w), f1)
-        GSF_COL(make_float2(m3.x, m3.y), make_float2(m3.z, m3.w), make_float2(m4.x, m4.y), f2)
-        GSF_COL(make_float2(m4.z, m4.w), make_float2(m5.x, m5.y), make_float2(m5.z, m5.w), f3)
-        GSF_COL(make_float2(m6.x, m6.y), make_float2(m6.z, m6.w), make_float2(m7.x, m7.y), f4)
-        GSF_COL(make_float2(m7.z, m7.w), make_float2(m8.x, m8.y), make_float2(m8.z, m8.w), f5)
-#undef GSF_COL
-      }
-      pd[0] += pa.x; pd[1] += pa.y; pd[2] += pb2.x; pd[3] += pb2.y; pd[4] += pc2.x; pd[5] += pc2.y;
-      hit = hit_n;
-      slotA = slotB;
-      idA = idB;
-    }
-    cp_async_wait_all();
   }
 #pragma unroll
   for (int a = 0; a < 6; ++a) pd[a] = warp_sum_f64(pd[a]);
@@ -1364,11 +1180,8 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
 #if GSF_TB_VARIANT == 0
       k_backward_track<<<ntiles, kTbThreads, kTbSmem, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane,
                                                             a.lp, ds, ticket);
-#elif GSF_TB_VARIANT == 1
-      k_backward_track_w<<<4 * ntiles, 32, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
-                                                     ws.wtickets + ws.wtickets_half, 4 * ntiles);
 #else
-      k_backward_track_p<<<4 * ntiles, 32, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
+      k_backward_track_w<<<4 * ntiles, 32, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
                                                      ws.wtickets + ws.wtickets_half, 4 * ntiles);
 #endif
     } else if (a.seed_mode == SEED_TRACK) {

@@ -536,13 +536,6 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
 constexpr int kTrkThreads = 128;
 constexpr int kTrkBatch = 256;
 
-// guard-band entries (rare): eval_pair's full decision out of line, keeping the hot loop's registers
-// (g is re-read from shared memory and kc read through a pointer, so the hot loop keeps no stack copies)
-static __device__ __noinline__ float guard_alpha(float px, float py, const BlendG* gs, const GuardG* gp, const BlendConsts* kc) {
-  const PairEval e = eval_pair_full(px, py, *gs, gp, *kc);
-  return e.code ? e.alpha : -1.0f;
-}
-
 #ifndef GSF_TRK_MINB
 #define GSF_TRK_MINB 8
 #endif
@@ -565,14 +558,14 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   const bool in_a = x < W && ya < H, in_b = x < W && yb < H;
   const int2 rg = ranges[tile];
   float2 rg_a = make_float2(0.f, 0.f), bd_a = rg_a, rg_b = rg_a, bd_b = rg_a;
-  float2 op = make_float2(0.f, 0.f), T = make_float2(1.f, 1.f);
+  // a pixel is done once T < term (T never grows); pixels outside the image start done (T = 0)
+  float2 op = make_float2(0.f, 0.f), T = make_float2(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);
   int last_a = 0, last_b = 0;
-  bool done_a = !in_a, done_b = !in_b;
   const float px = static_cast<float>(x) + 0.5f;
   const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
   const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
   for (int start = rg.x; start < rg.y; start += kTrkBatch) {
-    if (__syncthreads_and(done_a && done_b)) break;
+    if (__syncthreads_and(T.x < kc.term && T.y < kc.term)) break;
 #pragma unroll
     for (int h = 0; h < kTrkBatch / kTrkThreads; ++h) {
       const int e = tid + h * kTrkThreads, j = start + e;
@@ -587,7 +580,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     __syncthreads();
     const int cnt = min(kTrkBatch, rg.y - start);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
-      if (__all_sync(0xffffffffu, done_a && done_b)) break;
+      if (__all_sync(0xffffffffu, T.x < kc.term && T.y < kc.term)) break;
       const int kk = c0 + lane;
       uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
       while (bits) {
@@ -597,17 +590,17 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         const float dx = __fadd_rn(px, -g.mx);
         const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
         const float2 rho = pair_rho2(dx, dy, g);
-        const bool skip_a = done_a || rho.x > kc.rho_hi, skip_b = done_b || rho.y > kc.rho_hi;
+        const bool skip_a = T.x < kc.term || rho.x > kc.rho_hi, skip_b = T.y < kc.term || rho.y > kc.rho_hi;
         if (skip_a && skip_b) continue;
         const bool fast_a = rho.x < g.rho_fast, fast_b = rho.y < g.rho_fast;
         float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), exp_neg_half_inrange2(rho));
         bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
         if (!skip_a && !fast_a) {   // guard band: eval_pair's full decision
-          al.x = guard_alpha(px, py.x, s_g + k, gg + s_id[k], &kc);
+          al.x = guard_decide(px, py.x, g, gg + s_id[k], &kc).alpha;
           ca = al.x >= 0.0f;
         }
         if (!skip_b && !fast_b) {
-          al.y = guard_alpha(px, py.y, s_g + k, gg + s_id[k], &kc);
+          al.y = guard_decide(px, py.y, g, gg + s_id[k], &kc).alpha;
           cb = al.y >= 0.0f;
         }
         const float2 am = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
@@ -621,8 +614,6 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         const int li = start + k - rg.x + 1;
         if (ca) last_a = li;
         if (cb) last_b = li;
-        done_a = done_a || T.x < kc.term;
-        done_b = done_b || T.y < kc.term;
       }
     }
   }
@@ -748,11 +739,13 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
       ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w, ws.last, ws.loss_part, \
       a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket
   if (pf) pf->begin(PROF_BLEND, st);
-  if (a.lp.mode == 1 && loss_rgb)   // k_blend<1>'s outputs, two pixels per lane
+  ws.loss_rows = ntiles;
+  if (a.lp.mode == 1 && loss_rgb) {   // k_blend<1>'s outputs, two pixels per lane
     k_blend_track<<<ntiles, kTrkThreads, 0, st>>>(ws.ranges, ws.sid, ws.bg_id, ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,
                                                   tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color,
                                                   ws.alpha_depth, ws.opacity, ws.final_T, ws.last, ws.loss_part,
                                                   a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket);
+  }
   else if (a.lp.mode == 2 && loss_rgb)
     k_blend<2><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
   else
@@ -773,6 +766,7 @@ void run_world(Workspace& ws, DevState* ds, const float* params, int64_t P, cons
 void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,
                     double near_plane, double far_plane, float floor, cudaStream_t st, int64_t* L) {
   const int tiles_x = (W + kTile - 1) / kTile, tiles_y = (H + kTile - 1) / kTile;
+  ws.loss_rows = tiles_x * tiles_y;
   if (mode == 1)
     k_loss_tiles<1><<<tiles_x * tiles_y, 256, 0, st>>>(ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid, ws.opacity,
                                                         ws.uncertainty, rgb, depth, W, H, tiles_x, has_unc, near_plane,
