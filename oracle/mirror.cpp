@@ -87,7 +87,7 @@ extern "C" int mir_render(const gsf_map_host* map, const gsf_pose* pose, const g
   const BlendConsts kc = make_blend_consts(rp);
   for (int r = 0; r < V; ++r) {
     bg[r] = make_blend_g(pre[vis[r]]);
-    bg[r].pad0 = blend_rho_fast(bg[r].sigma, kc);
+    bg[r].rho_fast = blend_rho_fast(bg[r], kc);
     gg[r] = make_guard_g(pre[vis[r]]);
   }
   for (int t = 0; t < ntiles; ++t) {

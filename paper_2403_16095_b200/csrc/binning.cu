@@ -156,9 +156,24 @@ __device__ int sort_chunk(const unsigned long long* src, int n, unsigned long lo
   return buf;
 }
 
-// Runs of equal fp32 depth in (fp64 depth, id) order (rasterizer.cpp:74-77): the first thread of
-// each run insertion-sorts it (runs are a handful of keys).  Ends with a __syncthreads().
+// Runs of equal fp32 depth in (fp64 depth, id) order (rasterizer.cpp:74-77).  Inside such a run
+// the keys are already in id order, so the list is in reference order iff no adjacent pair of equal
+// fp32 depth has a smaller fp64 depth behind it: one parallel round of depth reads settles the
+// common case (duplicate layers share their fp64 depth); otherwise the first thread of each run
+// insertion-sorts it (runs are a handful of keys).  Ends with a __syncthreads().
 __device__ void fix_ties(unsigned long long* k, int n, const double* __restrict__ depth_id) {
+  __shared__ int s_inv;
+  if (threadIdx.x == 0) s_inv = 0;
+  __syncthreads();
+  bool inv = false;
+  for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) {
+    const unsigned long long a = k[i], b = k[i + 1];
+    if ((a >> 32) == (b >> 32) && __ldg(depth_id + static_cast<uint32_t>(b)) < __ldg(depth_id + static_cast<uint32_t>(a)))
+      inv = true;
+  }
+  if (inv) s_inv = 1;
+  __syncthreads();
+  if (!s_inv) return;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const uint32_t hi = static_cast<uint32_t>(k[i] >> 32);
     const bool starts = (i == 0 || static_cast<uint32_t>(k[i - 1] >> 32) != hi) && i + 1 < n &&
@@ -226,11 +241,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ 
   if (n <= kSortChunk) {
     unsigned long long* k = s_k[sort_chunk(bk, n, s_k)];
     fix_ties(k, n, depth_id);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const unsigned long long v = k[i];
-      sk[i] = v;
-      sid[s0 + i] = static_cast<uint32_t>(v);
-    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sid[s0 + i] = static_cast<uint32_t>(k[i]);
     return;
   }
   // long list: sorted chunks into skey, then merge passes ping-ponging with the (consumed) bucket
