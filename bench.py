@@ -311,7 +311,7 @@ def run_ours(args):
     achieved = flops[dom] / (per_launch[dom] * 1e-3) / 1e12
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     pre_bytes = P * (56 + 52)
-    kname = {"blend": "k_blend<1>", "backward": "k_backward_pose"}[dom]
+    kname = {"blend": "k_blend_track", "backward": "k_backward_track_w"}[dom]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:

@@ -153,6 +153,7 @@ struct gsf_ctx_s {
   int64_t bp_cap = 0;
   // captured track_frame graphs (small round-robin cache)
   TrackGraph track_graphs[8];
+  Frame track_in;   // graph-owned copy of the frame being tracked (one graph serves every frame slot)
   int track_graph_next = 0;
   bool use_graphs = true;
   // staging for host inputs
@@ -664,6 +665,8 @@ int gsf_ctx_destroy(gsf_ctx c) {
                   c->red_f};
   for (void* p : bufs)
     if (p) cudaFree(p);
+  if (c->track_in.rgb) cudaFree(c->track_in.rgb);
+  if (c->track_in.depth) cudaFree(c->track_in.depth);
   for (Frame& f : c->frames) {
     if (f.rgb) cudaFree(f.rgb);
     if (f.depth) cudaFree(f.depth);
@@ -1154,10 +1157,23 @@ static void run_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k, con
     enqueue_track(c, f, k, tcfg, w, rcfg);
     return;
   }
+  // the captured loop reads the frame from a context-owned buffer, so a new frame (or another slot)
+  // costs one device-to-device copy instead of a re-capture
+  const int64_t npix = static_cast<int64_t>(f.w) * f.h;
+  Frame& tin = c->track_in;
+  if (tin.w * tin.h != npix || !tin.rgb) {
+    dalloc(tin.rgb, 3 * npix);
+    dalloc(tin.depth, npix);
+  }
+  tin.w = f.w;
+  tin.h = f.h;
+  GSF_CUDA_CHECK(cudaMemcpyAsync(tin.rgb, f.rgb, sizeof(float) * 3 * npix, cudaMemcpyDeviceToDevice, c->stream));
+  GSF_CUDA_CHECK(cudaMemcpyAsync(tin.depth, f.depth, sizeof(float) * npix, cudaMemcpyDeviceToDevice, c->stream));
+  const Frame& fr = tin;
   TrackGraphKey key;
   std::memset(&key, 0, sizeof(key));
-  key.rgb = f.rgb;
-  key.depth = f.depth;
+  key.rgb = fr.rgb;
+  key.depth = fr.depth;
   key.params = c->params;
   key.K = k;
   key.rcfg = rcfg;
@@ -1180,7 +1196,7 @@ static void run_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k, con
   const int64_t l0 = c->launches;
   GSF_CUDA_CHECK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
-    enqueue_track(c, f, k, tcfg, w, rcfg);
+    enqueue_track(c, fr, k, tcfg, w, rcfg);
   } catch (...) {
     cudaGraph_t dummy = nullptr;
     cudaStreamEndCapture(c->stream, &dummy);
