@@ -290,6 +290,7 @@ void ensure_map(gsf_ctx_s* c, int64_t P, int K) {
 void alloc_pairs(Workspace& ws) {
 
   dalloc(ws.skey, ws.pair_cap); dalloc(ws.sid, ws.pair_cap);
+  dalloc(ws.sslot, ws.pair_cap); dalloc(ws.emask, ws.pair_cap);
   dalloc(ws.partials, ws.pair_cap * 10);
 }
 
@@ -299,7 +300,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   const int64_t npix = static_cast<int64_t>(W) * H;
   const int64_t tiles = static_cast<int64_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
   if (P > ws.P_cap) {
-    dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
+    dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.bg_slot, P); dalloc(ws.gg_slot, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
     dalloc(ws.pj_id, static_cast<size_t>(P) * kPjFloats);
     dalloc(ws.big_ids, P);
     dalloc(ws.vis_list, P);
@@ -656,7 +657,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   Workspace& ws = c->ws;
-  void* bufs[] = {ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
+  void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
                   ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,

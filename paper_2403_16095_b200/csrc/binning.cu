@@ -229,7 +229,8 @@ __device__ void merge_pass(const unsigned long long* a, unsigned long long* b, i
 __global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ fill, const uint32_t* __restrict__ start,
                                                    uint32_t pair_cap, unsigned long long* bucket, uint32_t bucket_cap,
                                                    unsigned long long* skey, uint32_t* __restrict__ sid,
-                                                   const double* __restrict__ depth_id, int2* __restrict__ ranges) {
+                                                   const double* __restrict__ depth_id, int2* __restrict__ ranges,
+                                                   const uint32_t* __restrict__ pj_slot, uint32_t* __restrict__ sslot) {
   __shared__ unsigned long long s_k[2][kSortChunk];
   const int t = blockIdx.x;
   const uint32_t s0 = min(start[t], pair_cap);
@@ -241,7 +242,11 @@ __global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ 
   if (n <= kSortChunk) {
     unsigned long long* k = s_k[sort_chunk(bk, n, s_k)];
     fix_ties(k, n, depth_id);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sid[s0 + i] = static_cast<uint32_t>(k[i]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t id = static_cast<uint32_t>(k[i]);
+      sid[s0 + i] = id;
+      if (sslot) sslot[s0 + i] = pj_slot[id];
+    }
     return;
   }
   // long list: sorted chunks into skey, then merge passes ping-ponging with the (consumed) bucket
@@ -261,12 +266,17 @@ __global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ 
     __syncthreads();
   }
   fix_ties(sk, n, depth_id);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sid[s0 + i] = static_cast<uint32_t>(sk[i]);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t id = static_cast<uint32_t>(sk[i]);
+    sid[s0 + i] = id;
+    if (sslot) sslot[s0 + i] = pj_slot[id];
+  }
 }
 
 }  // namespace
 
-void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles, cudaStream_t st, int64_t* L) {
+void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles, cudaStream_t st, int64_t* L,
+                 bool want_slots) {
   const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
   const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
   if (P > 0) {   // the regular pairs were scattered by k_preprocess
@@ -277,7 +287,7 @@ void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles
   k_tile_scan<<<1, 1024, 0, st>>>(ws.tile_fill, ntiles, bcap, ws.tile_start, ws.bin_counters, pair_cap, ds);
   ++*L;
   k_tile_sort<<<ntiles, 256, 0, st>>>(ws.tile_fill, ws.tile_start, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id,
-                                      ws.ranges);
+                                      ws.ranges, ws.pj_slot, want_slots ? ws.sslot : nullptr);
   ++*L;
 }
 

@@ -59,6 +59,10 @@ struct Workspace {
   // per primitive, id-indexed (written by k_preprocess for the visible ones)
   BlendG* bg_id = nullptr;
   GuardG* gg_id = nullptr;
+  BlendG* bg_slot = nullptr;   // tracking: the same records indexed by visible slot (compact)
+  GuardG* gg_slot = nullptr;
+  uint32_t* sslot = nullptr;   // tracking: tile lists as visible slots (beside sid)
+  uint8_t* emask = nullptr;    // tracking: per list entry, the 8x8 blocks of its tile it can reach (k_blend_track)
   double* depth_id = nullptr;
   int4* rect_id = nullptr;
   uint8_t* visible = nullptr;
@@ -111,7 +115,8 @@ struct Workspace {
 };
 
 // binning.cu
-void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles, cudaStream_t st, int64_t* launches);
+void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles, cudaStream_t st, int64_t* launches,
+                 bool want_slots = false);
 
 // raster_fwd.cu
 struct FwdArgs {

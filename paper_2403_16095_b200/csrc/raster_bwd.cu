@@ -101,6 +101,10 @@ struct BwdPtrs {
   const float* pj;          // pose Jacobians (fused tracking mode), 36 floats at the primitive's slot
   const uint32_t* pj_slot;  // id -> slot in pj (position in the visible list)
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
+  const uint32_t* sslot;    // tracking: tile lists as visible slots
+  const uint8_t* emask;     // tracking: per entry, the 8x8 blocks it can reach (k_blend_track)
+  const BlendG* bg_slot;    // tracking: records by visible slot
+  const GuardG* gg_slot;
 };
 
 #ifndef GSF_BWD_BATCH
@@ -682,23 +686,24 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
                  gad = make_float2(qa.gad, qb.gad);
     const float px = static_cast<float>(x) + 0.5f;
     const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
-    const float bx0 = static_cast<float>(tx * kTile + 8 * (qd & 1)), by0 = static_cast<float>(ty * kTile + 8 * (qd >> 1));
     float2 T = make_float2(qa.T, qb.T), S = make_float2(0.f, 0.f);
     for (int bend = rg.x + maxlast; bend > rg.x; bend -= 32) {
       const int bstart = max(rg.x, bend - 32);
       const int cnt = bend - bstart;
+      // the entry's slot and the forward's block mask arrive together; only entries that can reach
+      // this block fetch their record and pose matrix (both indexed by slot)
       bool hit = false;
       if (lane < cnt) {
-        const int id = static_cast<int>(bp.sid[bstart + lane]);
-        const BlendG gj = bp.bg[id];
-        hit = block_hit8(gj, bx0, by0, kc);
+        hit = (__ldg(bp.emask + bstart + lane) >> qd) & 1u;
         if (hit) {
-          s_g[lane] = gj;
-          s_id[lane] = id;
-          const float4* src = reinterpret_cast<const float4*>(bp.pj) + (kPjFloats / 4) * static_cast<size_t>(bp.pj_slot[id]);
+          const uint32_t sl = __ldg(bp.sslot + bstart + lane);
+          const float4* src = reinterpret_cast<const float4*>(bp.pj) + (kPjFloats / 4) * static_cast<size_t>(sl);
+          const BlendG gj = bp.bg_slot[sl];
           float4 r[9];
 #pragma unroll
           for (int j = 0; j < 9; ++j) r[j] = __ldg(src + j);
+          s_g[lane] = gj;
+          s_id[lane] = static_cast<int32_t>(sl);
 #pragma unroll
           for (int j = 0; j < 9; ++j) s_pj[lane][j] = r[j];
         }
@@ -722,14 +727,14 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
         int cl_a = 0, cl_b = 0;
         if (!skip_a && !fast_a) {
-          const GuardOut o = guard_decide(px, py.x, g, bp.gg + s_id[k], &kc);
+          const GuardOut o = guard_decide(px, py.x, g, bp.gg_slot + s_id[k], &kc);
           al.x = o.alpha;
           gv.x = o.gval;
           cl_a = o.clamped;
           ca = al.x >= 0.0f;
         }
         if (!skip_b && !fast_b) {
-          const GuardOut o = guard_decide(px, py.y, g, bp.gg + s_id[k], &kc);
+          const GuardOut o = guard_decide(px, py.y, g, bp.gg_slot + s_id[k], &kc);
           al.y = o.alpha;
           gv.y = o.gval;
           cl_b = o.clamped;
@@ -1146,6 +1151,10 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.rect = ws.rect_id;
   bp.pair_base = ws.pair_base;
   bp.tile_pose = nullptr;
+  bp.sslot = ws.sslot;
+  bp.emask = ws.emask;
+  bp.bg_slot = ws.bg_slot;
+  bp.gg_slot = ws.gg_slot;
   const bool view_dep = a.K > 1;
   const int nf = a.pose_only ? (view_dep ? 9 : 6) : 10;
   if (a.pose_only && a.fused_pose) {

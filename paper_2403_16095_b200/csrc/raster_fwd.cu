@@ -301,7 +301,9 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
 constexpr int kPjThreads = 128;
 __global__ void __launch_bounds__(kPjThreads) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
                                                  const uint32_t* __restrict__ vis_list, const uint32_t* counters,
-                                                 const WorldG* __restrict__ world, float* __restrict__ pj) {
+                                                 const WorldG* __restrict__ world, float* __restrict__ pj,
+                                                 const BlendG* __restrict__ bg_id, const GuardG* __restrict__ gg_id,
+                                                 BlendG* __restrict__ bg_slot, GuardG* __restrict__ gg_slot) {
   __shared__ float s_out[kPjThreads * (kPjFloats + 1)];
   const uint32_t n = counters[kCntVisible];
   const uint32_t r0 = blockIdx.x * blockDim.x;
@@ -309,6 +311,8 @@ __global__ void __launch_bounds__(kPjThreads) k_posejac(const float* __restrict_
   const uint32_t r = r0 + threadIdx.x;
   if (r < n) {
     const uint32_t id = vis_list[r];
+    bg_slot[r] = bg_id[id];   // the tracking kernels read records by visible slot (compact, no id hop)
+    gg_slot[r] = gg_id[id];
     float v[kPjFloats];
     compute_posejac(params + id, P, ds->cam, K, v, world ? world[id].S : nullptr);
 #pragma unroll
@@ -544,7 +548,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     const GuardG* __restrict__ gg, const float* __restrict__ loss_rgb, const float* __restrict__ loss_depth, int W, int H,
     int tiles_x, BlendConsts kc, double near_plane, double far_plane, LossParams lp, DevState* ds,
     float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_op, float* __restrict__ o_T,
-    int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket) {
+    int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
+    uint8_t* __restrict__ emask) {
   __shared__ BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
@@ -574,7 +579,9 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         const BlendG gj = bg[id];
         s_g[e] = gj;
         s_id[e] = id;
-        s_mask[e] = static_cast<uint8_t>(warp_block_mask8(gj, tile_x0, tile_y0, kc));
+        const uint8_t mk = static_cast<uint8_t>(warp_block_mask8(gj, tile_x0, tile_y0, kc));
+        s_mask[e] = mk;
+        if (emask) emask[j] = mk;   // the pose backward's block test
       }
     }
     __syncthreads();
@@ -724,13 +731,14 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     ++*L;
     if (a.want_posejac) {
       k_posejac<<<div_up(P, kPjThreads), kPjThreads, 0, st>>>(a.params, P, ds, a.K, ws.vis_list, ws.bin_counters,
-                                                a.use_world ? ws.world : nullptr, ws.pj_id);
+                                                a.use_world ? ws.world : nullptr, ws.pj_id, ws.bg_id, ws.gg_id,
+                                                ws.bg_slot, ws.gg_slot);
       ++*L;
     }
   }
   if (pf) pf->end(st);
   if (pf) pf->begin(PROF_SORT, st);
-  run_binning(ws, ds, P, tiles_x, ntiles, st, L);
+  run_binning(ws, ds, P, tiles_x, ntiles, st, L, a.want_posejac);
   if (pf) pf->end(st);
   const float* loss_rgb = a.loss_rgb;
 #define GSF_BLEND_ARGS                                                                                                 \
@@ -741,10 +749,15 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   if (pf) pf->begin(PROF_BLEND, st);
   ws.loss_rows = ntiles;
   if (a.lp.mode == 1 && loss_rgb) {   // k_blend<1>'s outputs, two pixels per lane
-    k_blend_track<<<ntiles, kTrkThreads, 0, st>>>(ws.ranges, ws.sid, ws.bg_id, ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,
+    // with pose Jacobians (a pose backward follows) the lists and records are read by visible slot
+    // and the entries' block masks are kept for the backward
+    const bool sl = a.want_posejac;
+    k_blend_track<<<ntiles, kTrkThreads, 0, st>>>(ws.ranges, sl ? ws.sslot : ws.sid, sl ? ws.bg_slot : ws.bg_id,
+                                                  sl ? ws.gg_slot : ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,
                                                   tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color,
                                                   ws.alpha_depth, ws.opacity, ws.final_T, ws.last, ws.loss_part,
-                                                  a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket);
+                                                  a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket,
+                                                  sl ? ws.emask : nullptr);
   }
   else if (a.lp.mode == 2 && loss_rgb)
     k_blend<2><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
