@@ -300,7 +300,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   const int64_t npix = static_cast<int64_t>(W) * H;
   const int64_t tiles = static_cast<int64_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
   if (P > ws.P_cap) {
-    dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.bg_slot, P); dalloc(ws.gg_slot, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
+    dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.bg_slot, P); dalloc(ws.gg_slot, P); dalloc(ws.cand, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
     dalloc(ws.pj_id, static_cast<size_t>(P) * kPjFloats);
     dalloc(ws.big_ids, P);
     dalloc(ws.vis_list, P);
@@ -657,7 +657,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   Workspace& ws = c->ws;
-  void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
+  void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
                   ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
@@ -1117,6 +1117,10 @@ int gsf_frame_upload(gsf_ctx c, int32_t slot, const float* rgb, const float* dep
 // ------------------------------------------------------------------------------------------------
 // track_frame (tracker.cpp:30-84)
 // ------------------------------------------------------------------------------------------------
+// tracking trust region (rad, m): wide enough for a tracked frame's pose correction, small enough
+// that the candidate list stays close to the visible set
+constexpr double kTrustTheta = 0.03, kTrustDist = 0.05;
+
 static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k, const gsf_tracker_cfg& tcfg,
                           const gsf_loss_weights& w, const gsf_raster_cfg& rcfg) {
   const LossParams lp = make_lp(1, &w, rcfg);
@@ -1126,8 +1130,12 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
   // the pose gradient) and the single-thread pose step
   // the map is constant during track_frame: validate it and cache its view-independent part once
   run_world(c->ws, c->ds, c->params, c->P, make_rp(c, k, rcfg), c->stream, &c->launches);
+  // primitives that can be visible while the camera stays within kTrustTheta / kTrustDist of the
+  // starting pose; the iterations preprocess only those until a step leaves the region
+  run_candidates(c->ws, c->ds, c->params, c->P, make_rp(c, k, rcfg), kTrustTheta, kTrustDist, c->stream, &c->launches);
   for (int it = 0; it < tcfg.iterations; ++it) {
     FwdArgs fa = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it);
+    fa.cand = c->ws.cand;
     fa.want_posejac = true;
     fa.fuse_loss_final = true;
     fa.use_world = true;

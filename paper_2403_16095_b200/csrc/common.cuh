@@ -195,6 +195,12 @@ struct DevState {
   int32_t iterations_run, degraded;
   double lr_rot, lr_trans, degraded_ratio;
   Cam cam;                 // camera of the current render
+  // tracking trust region (k_candidates / track_update): the candidate list holds every primitive
+  // that can be visible while the camera stays within (theta, dist) of the frame's first camera
+  double cand_W0[9], cand_t0[3];
+  double cand_cos_min, cand_dist_max;
+  uint32_t ncand;
+  int32_t cand_ok;         // 1 while the current camera is inside the trust region
 };
 
 struct LossParams {       // what the fused epilogues need (constant per loop)

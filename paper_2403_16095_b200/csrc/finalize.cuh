@@ -250,6 +250,19 @@ static __device__ __noinline__ void track_update(DevState* ds, int iteration, do
   }
   ds->iterations_run = iteration + 1;
   ds->cam = nc;
+  if (ds->cand_ok) {   // leave the trust region -> later iterations preprocess every primitive
+    // p' = Q p + (t' - Q t0) with Q = W' W0^T: |p' - p| <= angle(Q) |p| + |t' - Q t0|
+    double tr = 0.0, u[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < 9; ++a) tr += nc.W[a] * ds->cand_W0[a];
+    for (int j = 0; j < 3; ++j)
+      for (int i = 0; i < 3; ++i) u[j] += ds->cand_W0[3 * i + j] * ds->cand_t0[i];
+    double d2 = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      const double e = nc.t[i] - (nc.W[3 * i] * u[0] + nc.W[3 * i + 1] * u[1] + nc.W[3 * i + 2] * u[2]);
+      d2 += e * e;
+    }
+    if (!(0.5 * (tr - 1.0) >= ds->cand_cos_min) || !(sqrt(d2) <= ds->cand_dist_max)) ds->cand_ok = 0;
+  }
 }
 
 }  // namespace gsfk

@@ -63,6 +63,7 @@ struct Workspace {
   GuardG* gg_slot = nullptr;
   uint32_t* sslot = nullptr;   // tracking: tile lists as visible slots (beside sid)
   uint8_t* emask = nullptr;    // tracking: per list entry, the 8x8 blocks of its tile it can reach (k_blend_track)
+  uint32_t* cand = nullptr;    // tracking: trust-region candidate ids (k_candidates)
   double* depth_id = nullptr;
   int4* rect_id = nullptr;
   uint8_t* visible = nullptr;
@@ -135,12 +136,16 @@ struct FwdArgs {
   bool want_posejac = false; // tracking: emit the per-primitive pose Jacobians (ws.pj_id)
   bool fuse_loss_final = false;  // tracking: the blend's last CTA runs the loss finalize
   bool use_world = false;        // preprocess from ws.world / ws.support (run_world ran for this map)
+  const uint32_t* cand = nullptr;  // tracking: candidate ids (run_candidates), used while ds->cand_ok
   bool want_pair_base = true;    // primitive-major pair slots for a parameter-gradient backward
 };
 void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* launches);
 // per-primitive validation + view-independent cache (ws.world, ws.support)
 void run_world(Workspace& ws, DevState* ds, const float* params, int64_t P, const RasterParams& rp, cudaStream_t st,
                int64_t* launches);
+// trust-region candidate list of the tracking loop (once per frame, after run_world, at its first camera)
+void run_candidates(Workspace& ws, DevState* ds, const float* params, int64_t P, const RasterParams& rp,
+                    double theta_max, double dist_max, cudaStream_t st, int64_t* launches);
 void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,
                     double near_plane, double far_plane, float floor, cudaStream_t st, int64_t* launches);
 

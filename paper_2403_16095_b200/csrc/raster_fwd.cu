@@ -139,8 +139,9 @@ __device__ void compute_posejac(const float* __restrict__ p, int64_t stride, con
 // constant inside track_frame).  Invalid primitives get a NaN support and report bad_index.
 __global__ void __launch_bounds__(256) k_world(const float* __restrict__ params, int64_t P, RasterParams rp,
                                                WorldG* __restrict__ world, double* __restrict__ support,
-                                               int32_t* bad_index) {
+                                               int32_t* bad_index, uint32_t* ncand) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i == 0 && ncand) *ncand = 0u;
   if (i >= P) return;
   const int D = kFieldsBase + 3 * rp.sh_coeffs;
   float v[kFieldsBase];
@@ -163,6 +164,67 @@ __global__ void __launch_bounds__(256) k_world(const float* __restrict__ params,
   world[i] = make_world(params + i, P, rp.sh_coeffs);
 }
 
+// Candidates of the tracking loop (once per frame, after k_world).  While the camera stays within
+// (theta_max, dist_max) of the frame's first camera, a primitive's camera-space centre moves by at
+// most eps = theta_max |p| + dist_max (p at the first camera; track_update checks the region after
+// every step), so its support ball stays inside B(p, r + eps).  project_gaussian's necessary tests
+// (projection.cpp:62-76: depth range, support ball in front of the camera, padded support box on
+// the image; the box test is monotone in the radius) evaluated for that larger ball can only keep
+// more primitives, never fewer: the lists the preprocess builds from the candidates are the full
+// ones, bit for bit.  Margins of 1e-9 relative cover the rounding of this fp64 test.
+__device__ __forceinline__ void axis_bounds_d(double a, double z, double r, double f, double c, double& lo, double& hi) {
+  lo = 1e300;
+  hi = -1e300;
+  for (int e = 0; e < 4; ++e) {
+    const double u = c + f * (a + ((e & 1) ? r : -r)) / (z + ((e & 2) ? r : -r));
+    lo = fmin(lo, u);
+    hi = fmax(hi, u);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_candidates(int64_t P, DevState* ds, RasterParams rp,
+                                                    const float* __restrict__ params, const double* __restrict__ support,
+                                                    double theta_max, double dist_max, uint32_t* __restrict__ cand) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const Cam& cam = ds->cam;
+  if (i == 0) {
+    for (int a = 0; a < 9; ++a) ds->cand_W0[a] = cam.W[a];
+    for (int a = 0; a < 3; ++a) ds->cand_t0[a] = cam.t[a];
+    ds->cand_cos_min = cos(theta_max);
+    ds->cand_dist_max = dist_max;
+    ds->cand_ok = 1;
+  }
+  bool keep = false;
+  if (i < P) {
+    const double r = support[i];
+    if (!isnan(r)) {
+      const double m0 = params[i], m1 = params[P + i], m2 = params[2 * P + i];
+      double p[3];
+      for (int a = 0; a < 3; ++a) p[a] = cam.W[3 * a] * m0 + cam.W[3 * a + 1] * m1 + cam.W[3 * a + 2] * m2 + cam.t[a];
+      const double n = sqrt(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+      const double eps = (theta_max * n + dist_max) * (1.0 + 1e-9) + 1e-9 * (1.0 + n);
+      keep = p[2] + eps > cam.near_plane && p[2] - eps < cam.far_plane;   // depth range
+      if (keep && r > 0.0) {
+        keep = p[2] + eps - r > 0.0;                                      // ball in front
+        const double R = r + eps;
+        if (keep && p[2] - R > 0.0) {                                     // padded support box
+          const double pad = rp.footprint_sigma * sqrt(fmax(0.0, rp.dilation)) + 1e-6;
+          double ulo, uhi, vlo, vhi;
+          axis_bounds_d(p[0], p[2], R, cam.fx, cam.cx, ulo, uhi);
+          axis_bounds_d(p[1], p[2], R, cam.fy, cam.cy, vlo, vhi);
+          keep = !(uhi + pad < 0.0 || ulo - pad > cam.width || vhi + pad < 0.0 || vlo - pad > cam.height);
+        }
+      }
+    }
+  }
+  const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == 0 && bits) base = atomicAdd(&ds->ncand, static_cast<uint32_t>(__popc(bits)));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (keep) cand[base + __popc(bits & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+}
+
 // CACHED: the world part comes from k_world (tracking loop); otherwise every primitive is
 // validated and projected from its parameters (validate_primitives + project_all).
 template <bool CACHED>
@@ -174,7 +236,8 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
                                                     uint32_t* __restrict__ pj_slot, uint32_t* __restrict__ fill,
                                                     uint32_t bucket_cap, unsigned long long* __restrict__ bucket,
                                                     uint32_t* __restrict__ big_ids, uint32_t* __restrict__ pair_base,
-                                                    const WorldG* __restrict__ world, const double* __restrict__ support) {
+                                                    const WorldG* __restrict__ world, const double* __restrict__ support,
+                                                    const uint32_t* __restrict__ cand) {
   __shared__ uint32_t s_vis[8];
   __shared__ uint32_t s_base;
   __shared__ Cam s_cam;   // read through shared memory: 20 doubles need not live in registers
@@ -182,7 +245,12 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
     reinterpret_cast<uint32_t*>(&s_cam)[threadIdx.x] = reinterpret_cast<const uint32_t*>(&ds->cam)[threadIdx.x];
   __syncthreads();
   const Cam& cam = s_cam;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (cand && ds->cand_ok) {   // inside the trust region: only the frame's candidates (k_candidates)
+    const uint32_t n = ds->ncand;
+    if (static_cast<uint32_t>(blockIdx.x) * blockDim.x >= n) return;   // whole CTA: no barrier follows
+    i = i < n ? static_cast<int64_t>(cand[i]) : P;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   bool vis = false;
   int4 q = make_int4(0, -1, 0, -1);
@@ -725,7 +793,8 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
                                                    ws.visible, &ds->bad_index, a.kc, ws.bin_counters,                    \
                                                    ws.vis_list, ws.pj_slot, ws.tile_fill,                                 \
                                                    static_cast<uint32_t>(ws.bucket_cap), ws.bucket, ws.big_ids,           \
-                                                   a.want_pair_base ? ws.pair_base : nullptr, ws.world, ws.support)
+                                                   a.want_pair_base ? ws.pair_base : nullptr, ws.world, ws.support,        \
+                                                   a.cand)
     if (a.use_world) GSF_PRE(true); else GSF_PRE(false);
 #undef GSF_PRE
     ++*L;
@@ -772,7 +841,14 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
 void run_world(Workspace& ws, DevState* ds, const float* params, int64_t P, const RasterParams& rp, cudaStream_t st,
                int64_t* L) {
   if (P <= 0) return;
-  k_world<<<div_up(P, 256), 256, 0, st>>>(params, P, rp, ws.world, ws.support, &ds->bad_index);
+  k_world<<<div_up(P, 256), 256, 0, st>>>(params, P, rp, ws.world, ws.support, &ds->bad_index, &ds->ncand);
+  ++*L;
+}
+
+void run_candidates(Workspace& ws, DevState* ds, const float* params, int64_t P, const RasterParams& rp,
+                    double theta_max, double dist_max, cudaStream_t st, int64_t* L) {
+  if (P <= 0) return;
+  k_candidates<<<div_up(P, 256), 256, 0, st>>>(P, ds, rp, params, ws.support, theta_max, dist_max, ws.cand);
   ++*L;
 }
 

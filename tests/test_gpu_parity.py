@@ -396,6 +396,27 @@ def test_tracking_stationary_recovers_repeatable(gpu_ctx, orc):
     assert rotation_error(res.pose, ores.pose) < 5e-4 and translation_error(res.pose, ores.pose) < 5e-4
 
 
+def test_tracking_leaves_trust_region(gpu_ctx, orc):
+    """The tracking loop preprocesses only the frame's trust-region candidates (k_candidates) until a
+    step leaves the region (0.03 rad / 0.05 m), then every primitive.  A narrow camera on a scene
+    that extends past the image and a start 9 cm off: the pose travels beyond the region, and the
+    trajectory still follows the fp64 oracle's (which always projects everything)."""
+    K = make_intrinsics(64, 48, 90.0)
+    m = f32_round(orc.random_scene(901, 400))
+    _upload(gpu_ctx, m)
+    fr = _frames(gpu_ctx, orc, m, [pose()], K)
+    start = perturbed(pose(), [0.01, -0.008, 0.006, 0.07, -0.05, 0.03])
+    tc = defaults_tracker()
+    tc.iterations = 60
+    res = gpu_ctx.track_frame(0, start, K, tc, defaults_weights(True))
+    assert translation_error(res.pose, start) > 0.05          # the region was left mid-loop
+    assert translation_error(res.pose, pose()) < 0.5 * translation_error(start, pose())
+    again = gpu_ctx.track_frame(0, start, K, tc, defaults_weights(True))
+    assert list(again.pose.translation) == list(res.pose.translation)
+    ores = orc.track_frame(m, fr[0][0], fr[0][1], start, K, tc, defaults_weights(True), defaults_raster())
+    assert rotation_error(res.pose, ores.pose) < 2e-3 and translation_error(res.pose, ores.pose) < 2e-3
+
+
 def test_tracking_empty_view_degraded(gpu_ctx, orc):
     """test_tracker.cpp:246-263"""
     _upload(gpu_ctx, f32_round(orc.random_scene(3, 30)))
