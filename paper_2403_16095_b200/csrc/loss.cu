@@ -60,61 +60,82 @@ __device__ __forceinline__ float axis_norm(int p, int n) {
   return z;
 }
 
-// horizontal pass over the 15 product maps (x, y, xx, yy, xy per channel), planar output
-__global__ void k_ssim_h(const float* __restrict__ x, const float* __restrict__ y, int W, int H, float* __restrict__ tmp) {
-  const int64_t npix = static_cast<int64_t>(W) * H;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= npix) return;
-  const int px = static_cast<int>(i % W);
-  const float zx = axis_norm(px, W);
-  float acc[15];
-#pragma unroll
-  for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
-#pragma unroll
-  for (int o = -kR; o <= kR; ++o) {
-    if (px + o < 0 || px + o >= W) continue;
-    const float w = c_win[o + kR];
-    const int64_t j = i + o;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float a = x[3 * j + c], b = y[3 * j + c];
-      acc[c] += w * a;
-      acc[3 + c] += w * b;
-      acc[6 + c] += w * (a * a);
-      acc[9 + c] += w * (b * b);
-      acc[12 + c] += w * (a * b);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 15; ++q) tmp[q * npix + i] = acc[q] / zx;
-}
+// SSIM (ssim.cpp:27-187), tiled: a CTA owns a 32x16 block of pixels, stages its inputs with a
+// 5-pixel halo in shared memory and runs both separable blur passes there (horizontal over the 15
+// product maps x, y, xx, yy, xy per channel, then vertical + the per-pixel fp64 SSIM and its three
+// adjoint seed maps; the adjoint blurs vertical first, then horizontal, each tap divided by its
+// own border normaliser, ssim.cpp:60-80).  Out-of-image taps read 0, which adds w*0 exactly like
+// the reference's skipped taps.
+constexpr int kSX = 32, kSY = 16, kSW = kSX + 2 * kR, kSHh = kSY + 2 * kR;
 
-// vertical pass + per-pixel SSIM (fp64) + the three adjoint seed maps (ssim.cpp:139-176)
-__global__ void __launch_bounds__(256) k_ssim_v(const float* __restrict__ tmp, int W, int H, double weight,
-                                                float* __restrict__ u, double* __restrict__ part) {
+constexpr size_t ssim_fwd_smem() { return sizeof(float) * (6 * kSHh * kSW + 15 * kSHh * kSX); }
+constexpr size_t ssim_bwd_smem() { return sizeof(float) * (9 * kSHh * kSW + 9 * kSY * kSW); }
+
+__global__ void __launch_bounds__(256) k_ssim_fwd(const float* __restrict__ x, const float* __restrict__ y, int W, int H,
+                                                  double weight, float* __restrict__ u, double* __restrict__ part) {
+  extern __shared__ float s_buf[];
+  float (*s_in)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                  // x0..2, y0..2
+  float (*s_h)[kSHh][kSX] = reinterpret_cast<float (*)[kSHh][kSX]>(s_buf + 6 * kSHh * kSW);   // 15 planes
   __shared__ double s_red[8];
   const int64_t npix = static_cast<int64_t>(W) * H;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  double ssum = 0.0;
-  if (i < npix) {
-    const int py = static_cast<int>(i / W);
-    const float zy = axis_norm(py, H);
+  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < kSHh * kSW; idx += 256) {
+    const int r = idx / kSW, c = idx - r * kSW;
+    const int gx = bx - kR + c, gy = by - kR + r;
+    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+    const int64_t j = static_cast<int64_t>(gy) * W + gx;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      s_in[ch][r][c] = in ? x[3 * j + ch] : 0.0f;
+      s_in[3 + ch][r][c] = in ? y[3 * j + ch] : 0.0f;
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < kSHh * kSX; idx += 256) {   // horizontal pass (k_ssim_h)
+    const int r = idx / kSX, c = idx - r * kSX;
+    const float zx = axis_norm(min(bx + c, W - 1), W);
     float acc[15];
 #pragma unroll
     for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
 #pragma unroll
     for (int o = -kR; o <= kR; ++o) {
-      if (py + o < 0 || py + o >= H) continue;
       const float w = c_win[o + kR];
-      const int64_t j = i + static_cast<int64_t>(o) * W;
 #pragma unroll
-      for (int q = 0; q < 15; ++q) acc[q] += w * tmp[q * npix + j];
+      for (int ch = 0; ch < 3; ++ch) {
+        const float a = s_in[ch][r][c + kR + o], b = s_in[3 + ch][r][c + kR + o];
+        acc[ch] += w * a;
+        acc[3 + ch] += w * b;
+        acc[6 + ch] += w * (a * a);
+        acc[9 + ch] += w * (b * b);
+        acc[12 + ch] += w * (a * b);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 15; ++q) s_h[q][r][c] = acc[q] / zx;
+  }
+  __syncthreads();
+  double ssum = 0.0;
+  for (int idx = tid; idx < kSY * kSX; idx += 256) {   // vertical pass + per-pixel SSIM (k_ssim_v)
+    const int r = idx / kSX, c = idx - r * kSX;
+    const int gx = bx + c, gy = by + r;
+    if (gx >= W || gy >= H) continue;
+    const int64_t i = static_cast<int64_t>(gy) * W + gx;
+    const float zy = axis_norm(gy, H);
+    float acc[15];
+#pragma unroll
+    for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
+#pragma unroll
+    for (int o = -kR; o <= kR; ++o) {
+      const float w = c_win[o + kR];
+#pragma unroll
+      for (int q = 0; q < 15; ++q) acc[q] += w * s_h[q][r + kR + o][c];
     }
     const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double mx = acc[c] / zy, my = acc[3 + c] / zy, ex2 = acc[6 + c] / zy, ey2 = acc[9 + c] / zy,
-                   exy = acc[12 + c] / zy;
+    for (int ch = 0; ch < 3; ++ch) {
+      const double mx = acc[ch] / zy, my = acc[3 + ch] / zy, ex2 = acc[6 + ch] / zy, ey2 = acc[9 + ch] / zy,
+                   exy = acc[12 + ch] / zy;
       const double a1 = 2.0 * mx * my + C1;
       const double a2 = 2.0 * (exy - mx * my) + C2;
       const double b1 = mx * mx + my * my + C1;
@@ -124,56 +145,68 @@ __global__ void __launch_bounds__(256) k_ssim_v(const float* __restrict__ tmp, i
       ssum += sv;
       if (u) {
         const double d_a1 = a2 / denom, d_a2 = a1 / denom, d_b1 = -sv / b1, d_b2 = -sv / b2;
-        u[c * npix + i] = static_cast<float>((2.0 * my * d_a1 - 2.0 * my * d_a2 + 2.0 * mx * d_b1 - 2.0 * mx * d_b2) * weight);
-        u[(3 + c) * npix + i] = static_cast<float>(d_b2 * weight);
-        u[(6 + c) * npix + i] = static_cast<float>(2.0 * d_a2 * weight);
+        u[ch * npix + i] = static_cast<float>((2.0 * my * d_a1 - 2.0 * my * d_a2 + 2.0 * mx * d_b1 - 2.0 * mx * d_b2) * weight);
+        u[(3 + ch) * npix + i] = static_cast<float>(d_b2 * weight);
+        u[(6 + ch) * npix + i] = static_cast<float>(2.0 * d_a2 * weight);
       }
     }
   }
   const double t = block_sum_d(ssum, s_red);
-  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  if (tid == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = t;
 }
 
-// adjoint, vertical first: tmp(x,y) = sum_o w u(x,y+o) / zy(y+o)   (ssim.cpp:60-70)
-__global__ void k_ssim_adj_v(const float* __restrict__ u, int W, int H, float* __restrict__ t2) {
+__global__ void __launch_bounds__(256) k_ssim_bwd(const float* __restrict__ u, const float* __restrict__ x,
+                                                  const float* __restrict__ y, int W, int H, float* __restrict__ dx) {
+  extern __shared__ float s_buf[];
+  float (*s_u)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                    // 9 planes + halo
+  float (*s_t)[kSY][kSW] = reinterpret_cast<float (*)[kSY][kSW]>(s_buf + 9 * kSHh * kSW);     // after the vertical pass
   const int64_t npix = static_cast<int64_t>(W) * H;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= npix) return;
-  const int py = static_cast<int>(i / W);
-  float acc[9];
+  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < kSHh * kSW; idx += 256) {
+    const int r = idx / kSW, c = idx - r * kSW;
+    const int gx = bx - kR + c, gy = by - kR + r;
+    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+    const int64_t j = static_cast<int64_t>(gy) * W + gx;
 #pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
-#pragma unroll
-  for (int o = -kR; o <= kR; ++o) {
-    if (py + o < 0 || py + o >= H) continue;
-    const float w = c_win[o + kR] / axis_norm(py + o, H);
-    const int64_t j = i + static_cast<int64_t>(o) * W;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] += w * u[q * npix + j];
+    for (int q = 0; q < 9; ++q) s_u[q][r][c] = in ? u[q * npix + j] : 0.0f;
   }
+  __syncthreads();
+  for (int idx = tid; idx < kSY * kSW; idx += 256) {   // vertical adjoint (k_ssim_adj_v)
+    const int r = idx / kSW, c = idx - r * kSW;
+    const int gy = by + r;
+    float acc[9];
 #pragma unroll
-  for (int q = 0; q < 9; ++q) t2[q * npix + i] = acc[q];
-}
-
-// then horizontal, and d_x = a_mu + 2 a_ex2 x + a_exy y   (ssim.cpp:72-80, 178-183)
-__global__ void k_ssim_adj_h(const float* __restrict__ t2, const float* __restrict__ x, const float* __restrict__ y, int W,
-                             int H, float* __restrict__ dx) {
-  const int64_t npix = static_cast<int64_t>(W) * H;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= npix) return;
-  const int px = static_cast<int>(i % W);
-  float acc[9];
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
 #pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
+    for (int o = -kR; o <= kR; ++o) {
+      const int yy = gy + o;
+      const float w = (yy >= 0 && yy < H) ? c_win[o + kR] / axis_norm(yy, H) : 0.0f;
 #pragma unroll
-  for (int o = -kR; o <= kR; ++o) {
-    if (px + o < 0 || px + o >= W) continue;
-    const float w = c_win[o + kR] / axis_norm(px + o, W);
+      for (int q = 0; q < 9; ++q) acc[q] += w * s_u[q][r + kR + o][c];
+    }
 #pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] += w * t2[q * npix + i + o];
+    for (int q = 0; q < 9; ++q) s_t[q][r][c] = acc[q];
   }
+  __syncthreads();
+  for (int idx = tid; idx < kSY * kSX; idx += 256) {   // horizontal adjoint + d_x (k_ssim_adj_h)
+    const int r = idx / kSX, c = idx - r * kSX;
+    const int gx = bx + c, gy = by + r;
+    if (gx >= W || gy >= H) continue;
+    const int64_t i = static_cast<int64_t>(gy) * W + gx;
+    float acc[9];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) dx[3 * i + c] = acc[c] + 2.0f * acc[3 + c] * x[3 * i + c] + acc[6 + c] * y[3 * i + c];
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
+#pragma unroll
+    for (int o = -kR; o <= kR; ++o) {
+      const int xx = gx + o;
+      const float w = (xx >= 0 && xx < W) ? c_win[o + kR] / axis_norm(xx, W) : 0.0f;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] += w * s_t[q][r][c + kR + o];
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) dx[3 * i + ch] = acc[ch] + 2.0f * acc[3 + ch] * x[3 * i + ch] + acc[6 + ch] * y[3 * i + ch];
+  }
 }
 
 // small-image fallback: global statistics (ssim.cpp:117-144), one block
@@ -284,18 +317,23 @@ void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W
     ws.ssim_blocks = 1;
     return;
   }
-  const int blocks = div_up(npix, 256);
-  float* tmp = ws.ssim_tmp;               // 15 planes
+  static bool attr = false;
+  if (!attr) {
+    GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ssim_fwd_smem())));
+    GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ssim_bwd_smem())));
+    attr = true;
+  }
+  const dim3 grid(div_up(W, kSX), div_up(H, kSY));
   float* u = ws.ssim_tmp + 15 * npix;     // 9 planes
-  float* t2 = ws.ssim_tmp;                // reuse the first 9 planes after the forward
-  k_ssim_h<<<blocks, 256, 0, st>>>(x, y, W, H, tmp);
-  k_ssim_v<<<blocks, 256, 0, st>>>(tmp, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr, ws.red_part);
-  *L += 2;
-  ws.ssim_blocks = blocks;
+  k_ssim_fwd<<<grid, 256, ssim_fwd_smem(), st>>>(x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr,
+                                                 ws.red_part);
+  ++*L;
+  ws.ssim_blocks = static_cast<int>(grid.x * grid.y);
   if (d_out) {
-    k_ssim_adj_v<<<blocks, 256, 0, st>>>(u, W, H, t2);
-    k_ssim_adj_h<<<blocks, 256, 0, st>>>(t2, x, y, W, H, d_out);
-    *L += 2;
+    k_ssim_bwd<<<grid, 256, ssim_bwd_smem(), st>>>(u, x, y, W, H, d_out);
+    ++*L;
   }
 }
 
