@@ -317,7 +317,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     dalloc(ws.color, 3 * npix); dalloc(ws.alpha_depth, npix); dalloc(ws.median_depth, npix); dalloc(ws.median_valid, npix);
     dalloc(ws.opacity, npix); dalloc(ws.uncertainty, npix); dalloc(ws.final_T, npix); dalloc(ws.count, npix);
     dalloc(ws.dominant, npix); dalloc(ws.median_prim, npix); dalloc(ws.dominant_w, npix); dalloc(ws.last, npix);
-    dalloc(ws.obs, npix); dalloc(ws.upstream, 7 * npix); dalloc(ws.dssim, 3 * npix); dalloc(ws.ssim_tmp, 24 * npix);
+    dalloc(ws.obs, npix); dalloc(ws.upstream, 7 * npix); dalloc(ws.dssim, 3 * npix); dalloc(ws.ssim_tmp, 9 * npix);
     ws.npix_cap = npix;
   }
   if (tiles > ws.tiles_cap) {

@@ -326,7 +326,7 @@ void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W
     attr = true;
   }
   const dim3 grid(div_up(W, kSX), div_up(H, kSY));
-  float* u = ws.ssim_tmp + 15 * npix;     // 9 planes
+  float* u = ws.ssim_tmp;                 // 9 adjoint seed planes
   k_ssim_fwd<<<grid, 256, ssim_fwd_smem(), st>>>(x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr,
                                                  ws.red_part);
   ++*L;
