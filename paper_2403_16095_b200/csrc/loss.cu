@@ -34,17 +34,17 @@ __device__ __forceinline__ double block_sum_d(double v, double* s_red) {
   return t;
 }
 
-__global__ void __launch_bounds__(256) k_loss_finalize(const double* __restrict__ loss_part, int tiles, int64_t npix,
-                                                       LossParams lp, int iteration, const double* __restrict__ ssim_part,
-                                                       int ssim_blocks, const double* __restrict__ iso_part,
-                                                       int iso_blocks, DevState* ds) {
-  __shared__ double s_red[8][LS_NUM];
-  __shared__ double s_red1[8][1];
+__global__ void __launch_bounds__(1024) k_loss_finalize(const double* __restrict__ loss_part, int tiles, int64_t npix,
+                                                        LossParams lp, int iteration, const double* __restrict__ ssim_part,
+                                                        int ssim_blocks, const double* __restrict__ iso_part,
+                                                        int iso_blocks, DevState* ds) {
+  __shared__ double s_red[32][LS_NUM];
+  __shared__ double s_red1[32][1];
   __shared__ double s_tot[LS_NUM];
   __shared__ double s_ssim[1], s_iso[1];
-  block_reduce_rows<LS_NUM>(loss_part, tiles, s_tot, s_red);
-  block_reduce_rows<1>(ssim_part, ssim_blocks, s_ssim, s_red1);
-  block_reduce_rows<1>(iso_part, iso_blocks, s_iso, s_red1);
+  block_reduce_rows<LS_NUM, 1024>(loss_part, tiles, s_tot, s_red);
+  block_reduce_rows<1, 1024>(ssim_part, ssim_blocks, s_ssim, s_red1);
+  block_reduce_rows<1, 1024>(iso_part, iso_blocks, s_iso, s_red1);
   if (threadIdx.x == 0) loss_scalars(ds, lp, s_tot, s_ssim[0], s_iso[0], npix, iteration);
 }
 
@@ -301,7 +301,7 @@ void run_loss_finalize(Workspace& ws, DevState* ds, const LossParams& lp, int ti
   const int ssim_blocks = lp.mode == 2 && lp.w_ssim > 0.0 ? ws.ssim_blocks : 0;
   const int iso_blocks = lp.mode == 2 ? ws.iso_blocks : 0;
   if (ws.loss_rows > 0) tiles = ws.loss_rows;   // the producer's row count (4 per tile for k_blend_track_w)
-  k_loss_finalize<<<1, 256, 0, st>>>(ws.loss_part, tiles, npix, lp, iteration, ws.red_part, ssim_blocks,
+  k_loss_finalize<<<1, 1024, 0, st>>>(ws.loss_part, tiles, npix, lp, iteration, ws.red_part, ssim_blocks,
                                      ws.red_part + ws.red_iso_offset, iso_blocks, ds);
   ++*L;
 }

@@ -1072,12 +1072,12 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   }
 }
 
-__global__ void k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds) {
-  __shared__ double s_red[8][6];
+__global__ void __launch_bounds__(1024) k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds) {
+  __shared__ double s_red[32][6];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double acc[6] = {0, 0, 0, 0, 0, 0};
   for (int b = tid; b < blocks; b += blockDim.x)
-    for (int a = 0; a < 6; ++a) acc[a] += pose_part[static_cast<size_t>(b) * 6 + a];
+    for (int a = 0; a < 6; ++a) acc[a] += __ldcg(pose_part + static_cast<size_t>(b) * 6 + a);
   for (int a = 0; a < 6; ++a) {
     const double t = warp_sum_d(acc[a]);
     if (lane == 0) s_red[warp][a] = t;
@@ -1085,7 +1085,7 @@ __global__ void k_pose_sum(const double* __restrict__ pose_part, int blocks, Dev
   __syncthreads();
   if (tid < 6) {
     double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += s_red[w][tid];
+    for (int w = 0; w < 32; ++w) t += s_red[w][tid];
     ds->d_pose[tid] = ds->halt ? 0.0 : t;
   }
 }
@@ -1238,7 +1238,7 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     GSF_CHAIN(10, true);
 #undef GSF_CHAIN
   ++*L;
-  k_pose_sum<<<1, 256, 0, st>>>(ws.pose_part, blocks, ds);
+  k_pose_sum<<<1, 1024, 0, st>>>(ws.pose_part, blocks, ds);
   ++*L;
   if (ws.prof) ws.prof->end(st);
 }
