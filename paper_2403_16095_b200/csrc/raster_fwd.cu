@@ -404,27 +404,6 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// Tracking forward pixel state: the fields pixel_accumulate_min keeps, with the colour and
-// alpha-depth sums as two float2 pairs so each contributor costs two packed FFMA2s; __ffma2_rn
-// rounds each lane exactly like __fmaf_rn, so the values equal the scalar (mirror) ones.
-struct TrackPix {
-  float2 rg, bd;   // (colour r, g), (colour b, alpha depth)
-  float op, T;
-  int last, done;
-};
-
-__device__ __forceinline__ void track_accumulate(TrackPix& s, const BlendG& g, float alpha, int list_index,
-                                                 const BlendConsts& k) {
-  const float w = fmul(alpha, s.T);
-  const float2 ww = make_float2(w, w);
-  s.rg = __ffma2_rn(ww, make_float2(g.r, g.g), s.rg);
-  s.bd = __ffma2_rn(ww, make_float2(g.b, g.depth_b), s.bd);
-  s.op = fadd(s.op, w);
-  s.last = list_index + 1;
-  s.T = fmul(s.T, fsub(1.0f, alpha));
-  if (s.T < k.term) s.done = 1;
-}
-
 // pixel_accumulate (gsf_shared.cuh) with the colour / alpha-depth sums as two packed FFMA2s;
 // every lane rounds like __fmaf_rn, so the state equals the mirror's bit for bit.
 __device__ __forceinline__ void full_accumulate(PixelState& s, float2& rg, float2& bd, const BlendG& g, const PairEval& e,
@@ -454,11 +433,10 @@ __device__ __forceinline__ void full_accumulate(PixelState& s, float2& rg, float
   if (s.T < k.term) s.done = 1;
 }
 
+// Plain render (LMODE 0) and the mapping forward with its fused loss partials (LMODE 2); the
+// tracking forward is k_blend_track below.
 template <int LMODE>
-#ifndef GSF_BLEND_MINB
-#define GSF_BLEND_MINB 5
-#endif
-__global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sid,
+__global__ void __launch_bounds__(256, 4) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sid,
                                                const BlendG* __restrict__ bg, const GuardG* __restrict__ gg,
                                                const float* __restrict__ obs, const float* __restrict__ loss_rgb,
                                                const float* __restrict__ loss_depth, int W, int H, int tiles_x,
@@ -486,13 +464,7 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
   PixelState s;
   pixel_init(s);
   if (!inside) s.done = 1;
-  float2 frg = make_float2(0.0f, 0.0f), fbd = make_float2(0.0f, 0.0f);   // LMODE 0/2 colour, alpha depth
-  TrackPix t;   // LMODE 1 state (the PixelState is then unused)
-  t.rg = t.bd = make_float2(0.0f, 0.0f);
-  t.op = 0.0f;
-  t.T = 1.0f;
-  t.last = 0;
-  t.done = inside ? 0 : 1;
+  float2 frg = make_float2(0.0f, 0.0f), fbd = make_float2(0.0f, 0.0f);   // colour (r, g), (b, alpha depth)
   bool obs_valid = false;
   float ov = 0.0f;
   if (obs && inside) {
@@ -503,7 +475,7 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
   const int lane = tid & 31, warp = tid >> 5;
   const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
   for (int start = rg.x; start < rg.y; start += 256) {
-    if (__syncthreads_and(LMODE == 1 ? t.done : s.done)) break;
+    if (__syncthreads_and(s.done)) break;
     const int j = start + tid;
     if (j < rg.y) {
       const int id = static_cast<int>(sid[j]);
@@ -521,34 +493,17 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
       while (bits) {
         const int k = c0 + __ffs(bits) - 1;
         bits &= bits - 1u;
-        if constexpr (LMODE == 1) {   // finished lanes ride along predicated instead of branching
-          const BlendG g = s_g[k];
-          const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
-          if (e.code && !t.done) track_accumulate(t, g, e.alpha, start + k - rg.x, kc);
-        } else {
-          if (s.done) continue;
-          const BlendG g = s_g[k];
-          const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
-          if (e.code) full_accumulate(s, frg, fbd, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
-        }
+        if (s.done) continue;
+        const BlendG g = s_g[k];
+        const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
+        if (e.code) full_accumulate(s, frg, fbd, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
       }
     }
   }
-  if (LMODE != 1) {
-    s.cr = frg.x;
-    s.cg = frg.y;
-    s.cb = fbd.x;
-    s.ad = fbd.y;
-  }
-  if (LMODE == 1) {
-    s.cr = t.rg.x;
-    s.cg = t.rg.y;
-    s.cb = t.bd.x;
-    s.ad = t.bd.y;
-    s.op = t.op;
-    s.T = t.T;
-    s.last = t.last;
-  }
+  s.cr = frg.x;
+  s.cg = frg.y;
+  s.cb = fbd.x;
+  s.ad = fbd.y;
   if (inside) {
     o_color[3 * pi + 0] = s.cr;
     o_color[3 * pi + 1] = s.cg;
@@ -557,15 +512,13 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
     o_op[pi] = s.op;
     o_T[pi] = s.T;
     o_last[pi] = s.last;
-    if (LMODE != 1) {   // tracking reads none of these
-      o_md[pi] = s.med_depth;
-      o_mv[pi] = s.median >= 0 ? 1 : 0;
-      o_unc[pi] = s.unc;
-      o_count[pi] = s.count;
-      o_dom[pi] = s.dominant;
-      o_med[pi] = s.median;
-      o_domw[pi] = s.best;
-    }
+    o_md[pi] = s.med_depth;
+    o_mv[pi] = s.median >= 0 ? 1 : 0;
+    o_unc[pi] = s.unc;
+    o_count[pi] = s.count;
+    o_dom[pi] = s.dominant;
+    o_med[pi] = s.median;
+    o_domw[pi] = s.best;
   }
   if (LMODE == 0) return;
   // fused loss epilogue: per-tile residual sums and mask counts (deterministic tree)
@@ -587,24 +540,18 @@ __global__ void __launch_bounds__(256, LMODE == 1 ? GSF_BLEND_MINB : 4) k_blend(
     for (int w = 0; w < 8; ++w) t += s_red[w][tid];
     loss_part[static_cast<int64_t>(tile) * LS_NUM + tid] = t;
   }
-  if (LMODE == 1 && fuse_final) {
-    // the last tile CTA finalises the loss (k_loss_finalize without its own launch)
-    __shared__ int s_last;
-    __shared__ double s_tot[LS_NUM];
-    if (last_cta(ticket, &s_last, tid < LS_NUM)) {
-      block_reduce_rows<LS_NUM>(loss_part, gridDim.x, s_tot, s_red);
-      if (tid == 0) loss_scalars(ds, lp, s_tot, 0.0, 0.0, static_cast<int64_t>(W) * H, iteration);
-    }
-  }
+  (void)fuse_final;
+  (void)iteration;
+  (void)ticket;
 }
 
-// Tracking forward (k_blend<1>'s maps and fused loss) with two pixels per lane: warp w of the
+// Tracking forward (the tracking loss's maps and its fused loss) with two pixels per lane: warp w of the
 // 128-thread CTA owns the 8x8 block (8 (w & 1), 8 (w >> 1)) of the tile and lane l the pixels
 // (l & 7, l >> 3) and (l & 7, (l >> 3) + 4).  Both pixels share dx, so rho and exp run on packed
 // FP32x2 and every per-entry cost (ballot walk, staging reads) is paid once for two pixels; an
 // 8x8 block meets ~0.6x as many (block, entry) pairs as two 8x4 blocks.  Each packed lane rounds
 // like the scalar op in the scalar order, and a pixel that does not take an entry sees alpha 0
-// (w = 0, T * 1): the maps equal k_blend<1>'s, and the mirror's, bit for bit.
+// (w = 0, T * 1): the maps equal the plain render's, and the mirror's, bit for bit.
 constexpr int kTrkThreads = 128;
 constexpr int kTrkBatch = 256;
 
@@ -817,7 +764,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
       a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket
   if (pf) pf->begin(PROF_BLEND, st);
   ws.loss_rows = ntiles;
-  if (a.lp.mode == 1 && loss_rgb) {   // k_blend<1>'s outputs, two pixels per lane
+  if (a.lp.mode == 1 && loss_rgb) {   // tracking loss: colour, alpha depth, opacity, T, last; two pixels per lane
     // with pose Jacobians (a pose backward follows) the lists and records are read by visible slot
     // and the entries' block masks are kept for the backward
     const bool sl = a.want_posejac;
