@@ -178,9 +178,11 @@ def run_ours(args):
     from paper_2403_16095_b200 import abi, api
 
     rank, world, local = dist_env()
+    device = local if world > 1 else 0
+    if torch.cuda.is_available():
+        torch.cuda.set_device(device)   # torch's NCCL collectives (barrier, max-over-ranks, id broadcast)
     if world > 1:
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo", init_method="env://")
-    device = local if world > 1 else 0
     ctx = api.Context(device)
     K = intrinsics()
     P = args.primitives
