@@ -169,9 +169,15 @@ struct gsf_ctx_s {
 
 namespace {
 
+// Device buffers come from the device's stream-ordered memory pool (cudaMallocAsync on the calling
+// context's stream, release threshold unlimited): a map that grows by spawning or densification
+// re-uses freed blocks instead of paying cudaMalloc/cudaFree (and cudaFree's device-wide sync) for
+// every buffer.  dalloc waits for its stream so the new block is usable from any stream at once.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
 template <class T>
 void dfree(T*& p) {
-  if (p) cudaFree(p);
+  if (p) cudaFreeAsync(p, g_alloc_stream);
   p = nullptr;
 }
 
@@ -182,8 +188,16 @@ template <class T>
 void dalloc(T*& p, size_t count) {
   dfree(p);
   if (count == 0) count = 1;
-  GSF_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * count));
+  GSF_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, g_alloc_stream));
+  GSF_CUDA_CHECK(cudaStreamSynchronize(g_alloc_stream));
   ++g_alloc_gen;
+}
+
+void keep_pool_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+  uint64_t threshold = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
 }
 
 void check_intrinsics(const gsf_intrinsics& k) {   // camera.hpp:20-26
@@ -300,15 +314,16 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   const int64_t npix = static_cast<int64_t>(W) * H;
   const int64_t tiles = static_cast<int64_t>((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile);
   if (P > ws.P_cap) {
-    dalloc(ws.bg_id, P); dalloc(ws.gg_id, P); dalloc(ws.bg_slot, P); dalloc(ws.gg_slot, P); dalloc(ws.cand, P); dalloc(ws.depth_id, P); dalloc(ws.rect_id, P); dalloc(ws.visible, P);
-    dalloc(ws.pj_id, static_cast<size_t>(P) * kPjFloats);
-    dalloc(ws.big_ids, P);
-    dalloc(ws.vis_list, P);
-    dalloc(ws.pair_base, P);
-    dalloc(ws.pj_slot, P);
-    dalloc(ws.world, P);
-    dalloc(ws.support, P);
-    ws.P_cap = P;
+    const int64_t Pc = P + P / 4 + 4096;   // headroom: a growing map (spawn, densify) rarely reallocates
+    dalloc(ws.bg_id, Pc); dalloc(ws.gg_id, Pc); dalloc(ws.bg_slot, Pc); dalloc(ws.gg_slot, Pc); dalloc(ws.cand, Pc); dalloc(ws.depth_id, Pc); dalloc(ws.rect_id, Pc); dalloc(ws.visible, Pc);
+    dalloc(ws.pj_id, static_cast<size_t>(Pc) * kPjFloats);
+    dalloc(ws.big_ids, Pc);
+    dalloc(ws.vis_list, Pc);
+    dalloc(ws.pair_base, Pc);
+    dalloc(ws.pj_slot, Pc);
+    dalloc(ws.world, Pc);
+    dalloc(ws.support, Pc);
+    ws.P_cap = Pc;
     dfree(ws.pose_part);
   }
   if (ws.pair_cap == 0) ws.pair_cap = std::max<int64_t>(1 << 20, 4 * P);
@@ -337,7 +352,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     dalloc(ws.pose_part, static_cast<size_t>(std::max<int64_t>(div_up(ws.P_cap, 256), 5 * ws.tiles_cap + 64)) * 6);
     ws.wtickets_half = ws.tiles_cap / 8 + 8;   // groups of 32 rows over 4 rows per tile, + the top ticket
     dalloc(ws.wtickets, 2 * ws.wtickets_half);
-    GSF_CUDA_CHECK(cudaMemset(ws.wtickets, 0, sizeof(uint32_t) * 2 * ws.wtickets_half));
+    GSF_CUDA_CHECK(cudaMemsetAsync(ws.wtickets, 0, sizeof(uint32_t) * 2 * ws.wtickets_half, c->stream));
   }
   const int64_t red = 2 * std::max<int64_t>(div_up(npix, 256), div_up(P, 256)) + 64;
   if (!ws.red_part || ws.red_iso_offset * 2 < red) {
@@ -439,6 +454,7 @@ int guard(gsf_ctx c, F&& f) {
   c->err_index = -1;
   try {
     cudaSetDevice(c->device);
+    g_alloc_stream = c->stream;
     f();
     return GSF_OK;
   } catch (const ENonFinite& e) {
@@ -636,6 +652,8 @@ int gsf_ctx_create(int device, gsf_ctx* out) {
   const int rc = guard(c, [&] {
     GSF_CUDA_CHECK(cudaSetDevice(device));
     GSF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    g_alloc_stream = c->stream;
+    keep_pool_memory(device);
     dalloc(c->ds, 1);
     GSF_CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&c->ds_host), sizeof(DevState)));
     reset_state(c, nullptr);
@@ -665,13 +683,14 @@ int gsf_ctx_destroy(gsf_ctx c) {
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
                   c->red_f};
   for (void* p : bufs)
-    if (p) cudaFree(p);
-  if (c->track_in.rgb) cudaFree(c->track_in.rgb);
-  if (c->track_in.depth) cudaFree(c->track_in.depth);
+    if (p) cudaFreeAsync(p, c->stream);
+  if (c->track_in.rgb) cudaFreeAsync(c->track_in.rgb, c->stream);
+  if (c->track_in.depth) cudaFreeAsync(c->track_in.depth, c->stream);
   for (Frame& f : c->frames) {
-    if (f.rgb) cudaFree(f.rgb);
-    if (f.depth) cudaFree(f.depth);
+    if (f.rgb) cudaFreeAsync(f.rgb, c->stream);
+    if (f.depth) cudaFreeAsync(f.depth, c->stream);
   }
+  cudaStreamSynchronize(c->stream);
   if (c->ds_host) cudaFreeHost(c->ds_host);
   if (c->kf_host) cudaFreeHost(c->kf_host);
   if (c->stage) cudaFreeHost(c->stage);

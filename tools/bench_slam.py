@@ -1,0 +1,79 @@
+"""System throughput of SlamSystem (slam/system.cpp:31-154) on one B200 — the paper's "system FPS"
+(8.5 FPS on an RTX 4090 for the full configuration): Replica-shaped 1200x680 frames,
+RunConfig defaults (tracking 15 iterations per frame, a keyframe every 30 frames with 60 mapping
+iterations, sliding_ba, uncertainty pruning and spawning).  Not a bench line.
+
+Frames: the reference room generator (~500k Gaussians) rendered on the device along a slow orbit
+(0.25 deg/frame) plus NoiseSpec noise, pre-rendered and held on the host; every process() call
+uploads its frame from host memory, as a live system would.
+
+Run on the GPU box:  python tools/bench_slam.py [frames] > gpurun_out/slam_fps.json
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    from paper_2403_16095_b200 import abi, api
+    nframes = int(sys.argv[1]) if len(sys.argv) > 1 else 91
+    K = bench.intrinsics()
+    truth, _ = bench.build_scene(500000)
+    poses = api.synth_orbit(1440, 1.0, 0.0)
+    gen = api.Context(0)
+    gen.upload(truth)
+    frames = []
+    for f in range(nframes):
+        r = gen.render(poses[f], K)
+        c, d = bench.noisy(r.color, r.alpha_depth, f)
+        frames.append((np.ascontiguousarray(c), np.ascontiguousarray(d)))
+    gen.close()
+
+    ctx = api.Context(0)
+    cfg = abi.defaults_slam(K)        # RunConfig defaults: 15 tracking its, keyframe every 30, 60 map its
+    slam = api.SlamSystem(ctx, cfg)
+    logs = []
+    t0 = time.perf_counter()
+    t_first = None
+    for f, (c, d) in enumerate(frames):
+        logs.append(slam.process(f, f / 30.0, c, d))
+        if f == 0:
+            t_first = time.perf_counter()
+    ctx.lib.gsf_synchronize(ctx.h)
+    t1 = time.perf_counter()
+    kf = [l for l in logs if l.keyframe]
+    tracked = [l for l in logs[1:]]
+    steady = nframes - 1
+    out = {
+        "metric": "SlamSystem frames/s (process() incl. frame upload, tracking, keyframe cycles)",
+        "frames": nframes, "width": K.width, "height": K.height,
+        "config": {"tracking_iterations": cfg.tracker.iterations, "keyframe_interval": cfg.tracker.keyframe_interval,
+                   "map_iterations": cfg.map_iterations, "init_iterations": cfg.init_iterations,
+                   "ba_iterations": cfg.tracker.ba_iterations, "ba_window": cfg.tracker.ba_window},
+        "fps_after_bootstrap": steady / (t1 - t_first),
+        "fps_including_bootstrap": nframes / (t1 - t0),
+        "bootstrap_s": t_first - t0,
+        "track_ms_mean": float(np.mean([l.track_ms for l in tracked])),
+        "keyframes": len(kf),
+        "keyframe_cycle_ms_mean": {k: float(np.mean([getattr(l, k) for l in kf[1:]])) if len(kf) > 1 else None
+                                   for k in ("map_ms", "ba_ms", "uncertainty_ms", "spawn_ms")},
+        "primitives_final": int(logs[-1].primitives),
+        "kf_psnr_db": [float(l.kf_psnr_db) for l in kf],
+        "paper_reference": "8.5 FPS full / 15.4 FPS light on RTX 4090 (PAPER.md:440-441)",
+        "data": "synthetic (reference room generator, seeded; frames rendered on device + NoiseSpec noise)",
+    }
+    print(json.dumps(out), flush=True)
+    slam.close()
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
