@@ -396,6 +396,28 @@ def test_tracking_stationary_recovers_repeatable(gpu_ctx, orc):
     assert rotation_error(res.pose, ores.pose) < 5e-4 and translation_error(res.pose, ores.pose) < 5e-4
 
 
+def test_tracking_100_iterations_cfg1_sized(gpu_ctx, orc):
+    """track_frame(100) on a cfg1-sized frame (640x480, f=525) against the fp64 oracle's
+    trajectory from the same start (tracker.cpp:30-84, 100 Adam steps on fp32 vs fp64 gradients)."""
+    K = make_intrinsics(640, 480, 525.0)
+    m = f32_round(orc.random_scene(4242, 3000, 1, 0.95, 0.01, 0.08))
+    _upload(gpu_ctx, m)
+    fr = _frames(gpu_ctx, orc, m, [pose()], K)
+    start = perturbed(pose(), [0.004, -0.003, 0.002, 0.008, -0.006, 0.004])   # test_tracker.cpp:222
+    tc = defaults_tracker()
+    tc.iterations = 100
+    w = defaults_weights()
+    res = gpu_ctx.track_frame(0, start, K, tc, w)
+    ores = orc.track_frame(m, fr[0][0], fr[0][1], start, K, tc, w, defaults_raster())
+    assert res.iterations_run == 100 and not res.degraded
+    assert rotation_error(res.pose, pose()) < 0.35 * rotation_error(start, pose())
+    assert translation_error(res.pose, pose()) < 0.35 * translation_error(start, pose())
+    # near the optimum Adam steps of ~lr (1.5e-3 rad, 2.2e-3 m) flip with the gradient signs, so fp32-vs-fp64
+    # gradient noise moves the end point by a fraction of a step: 1/3 of lr (SURVEY 8(c) fallback criterion)
+    assert rotation_error(res.pose, ores.pose) < 5e-4 and translation_error(res.pose, ores.pose) < 7e-4
+    assert res.final_loss == pytest.approx(ores.final_loss, rel=5e-2, abs=1e-6)
+
+
 def test_tracking_leaves_trust_region(gpu_ctx, orc):
     """The tracking loop preprocesses only the frame's trust-region candidates (k_candidates) until a
     step leaves the region (0.03 rad / 0.05 m), then every primitive.  A narrow camera on a scene
