@@ -473,187 +473,12 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
 }
 
 // Tracking backward (k_backward_pose<SEED_TRACK, false>) with two pixels per lane, the layout of
-// k_blend_track: warp w owns the tile's 8x8 block (8 (w & 1), 8 (w >> 1)), lane l the pixels
-// (l & 7, l >> 3) and (l & 7, (l >> 3) + 4).  The pair arithmetic of both pixels runs on packed
-// FP32x2 (shared dx); their screen-space gradients are added before the contraction with the
-// entry's pose matrix, so the 18 FFMA2 of M s and the staging reads are paid once per two
-// pixels.  Decisions (contributes / clamped) are the forward's: same rho, same tests.
-constexpr int kTbThreads = 128;
-#ifndef GSF_TB_BATCH
-#define GSF_TB_BATCH 128
-#endif
-constexpr int kTbBatch = GSF_TB_BATCH;
-constexpr size_t kTbSmem = static_cast<size_t>(kTbBatch) * (sizeof(BlendG) + 9 * sizeof(float4) + sizeof(int32_t) + 1);
-
-#ifndef GSF_TB_MINB
-#define GSF_TB_MINB 8
-#endif
-__global__ void __launch_bounds__(kTbThreads, GSF_TB_MINB) k_backward_track(BwdPtrs bp, int W, int H, int tiles_x,
-                                                                           BlendConsts kc, double near_plane,
-                                                                           double far_plane, LossParams lp, DevState* ds,
-                                                                           uint32_t* ticket) {
-  extern __shared__ float4 s_dyn[];   // kTbSmem
-  float4 (*s_pj)[9] = reinterpret_cast<float4 (*)[9]>(s_dyn);
-  BlendG* s_g = reinterpret_cast<BlendG*>(s_dyn + kTbBatch * 9);
-  int32_t* s_id = reinterpret_cast<int32_t*>(s_g + kTbBatch);
-  uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_id + kTbBatch);
-  __shared__ int s_wmax[kTbThreads / 32];
-  __shared__ double s_pred[8][6];
-  const int tile = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (ds->halt) {
-    __shared__ int s_last0;
-    if (last_cta(ticket, &s_last0, false) && tid < 6) ds->d_pose[tid] = 0.0;
-    return;
-  }
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int x = tx * kTile + 8 * (warp & 1) + (lane & 7);
-  const int ya = ty * kTile + 8 * (warp >> 1) + (lane >> 3), yb = ya + 4;
-  const bool in_a = x < W && ya < H, in_b = x < W && yb < H;
-  const int2 rg = bp.ranges[tile];
-  const PixBwd qa = load_pixel_bwd<SEED_TRACK>(bp, static_cast<int64_t>(ya) * W + x, in_a, lp, ds, near_plane, far_plane);
-  const PixBwd qb = load_pixel_bwd<SEED_TRACK>(bp, static_cast<int64_t>(yb) * W + x, in_b, lp, ds, near_plane, far_plane);
-  const int last_a = qa.last, last_b = qb.last;
-  const int ml = __reduce_max_sync(0xffffffffu, max(last_a, last_b));
-  if (lane == 0) s_wmax[warp] = ml;
-  if (lane < 6) s_pred[warp][lane] = 0.0;
-  __syncthreads();
-  int maxlast = 0;
-#pragma unroll
-  for (int w = 0; w < kTbThreads / 32; ++w) maxlast = max(maxlast, s_wmax[w]);
-  const float2 gc0 = make_float2(qa.gc0, qb.gc0), gc1 = make_float2(qa.gc1, qb.gc1), gc2 = make_float2(qa.gc2, qb.gc2),
-               gad = make_float2(qa.gad, qb.gad);
-  const float px = static_cast<float>(x) + 0.5f;
-  const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
-  const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
-  float2 T = make_float2(qa.T, qb.T), S = make_float2(0.f, 0.f);
-  const int end = rg.x + maxlast;
-  for (int bend = end; bend > rg.x; bend -= kTbBatch) {
-    const int bstart = max(rg.x, bend - kTbBatch);
-    const int cnt = bend - bstart;
-    for (int e = tid; e < cnt; e += kTbThreads) {
-      const int id = static_cast<int>(bp.sid[bstart + e]);
-      const BlendG gj = bp.bg[id];
-      s_g[e] = gj;
-      s_id[e] = id;
-      s_mask[e] = static_cast<uint8_t>(warp_block_mask8(gj, tile_x0, tile_y0, kc));
-    }
-    __syncthreads();
-    // one entry per thread: its slot, then all nine rows in flight at once
-    for (int e = tid; e < cnt; e += kTbThreads) {
-      if (!s_mask[e]) continue;   // entries no warp block can see are never read
-      const float4* src = reinterpret_cast<const float4*>(bp.pj) + (kPjFloats / 4) * static_cast<size_t>(bp.pj_slot[s_id[e]]);
-      float4 r[9];
-#pragma unroll
-      for (int j = 0; j < 9; ++j) r[j] = __ldg(src + j);
-#pragma unroll
-      for (int j = 0; j < 9; ++j) s_pj[e][j] = r[j];
-    }
-    __syncthreads();
-    float2 pa = make_float2(0.f, 0.f), pb2 = make_float2(0.f, 0.f), pc2 = make_float2(0.f, 0.f);
-    for (int c0 = ((cnt - 1) >> 5) << 5; c0 >= 0; c0 -= 32) {
-      const int kk = c0 + lane;
-      uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
-      while (bits) {
-        const int j = 31 - __clz(bits);
-        bits &= ~(1u << j);
-        const int k = c0 + j;
-        const int li = bstart + k - rg.x;
-        const BlendG g = s_g[k];
-        const float dx = __fadd_rn(px, -g.mx);
-        const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
-        const float2 rho = pair_rho2(dx, dy, g);
-        const bool skip_a = li >= last_a || rho.x > kc.rho_hi, skip_b = li >= last_b || rho.y > kc.rho_hi;
-        if (skip_a && skip_b) continue;
-        const bool fast_a = rho.x < g.rho_fast, fast_b = rho.y < g.rho_fast;
-        float2 gv = make_float2(exp_neg_half_fast(rho.x), exp_neg_half_fast(rho.y));
-        float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), gv);
-        bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
-        int cl_a = 0, cl_b = 0;
-        if (!skip_a && !fast_a) {
-          const GuardOut o = guard_decide(px, py.x, g, bp.gg + s_id[k], &kc);
-          al.x = o.alpha;
-          gv.x = o.gval;
-          cl_a = o.clamped;
-          ca = al.x >= 0.0f;
-        }
-        if (!skip_b && !fast_b) {
-          const GuardOut o = guard_decide(px, py.y, g, bp.gg + s_id[k], &kc);
-          al.y = o.alpha;
-          gv.y = o.gval;
-          cl_b = o.clamped;
-          cb = al.y >= 0.0f;
-        }
-        if (!ca && !cb) continue;
-        // non-contributing pixel: alpha 0 -> Tpre = T, w = 0, and its gradient terms are zeroed
-        const float2 am = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
-        const float2 inv = make_float2(rcp_approx(1.0f - am.x), rcp_approx(1.0f - am.y));
-        const float2 Tpre = __fmul2_rn(T, inv);
-        float2 q = __fmul2_rn(gc0, make_float2(g.r, g.r));
-        q = __ffma2_rn(gc1, make_float2(g.g, g.g), q);
-        q = __ffma2_rn(gc2, make_float2(g.b, g.b), q);
-        q = __ffma2_rn(gad, make_float2(g.depth, g.depth), q);
-        const float2 dal = __ffma2_rn(Tpre, q, __fmul2_rn(make_float2(-S.x, -S.y), inv));
-        const float2 w = __fmul2_rn(am, Tpre);
-        S = __ffma2_rn(w, q, S);
-        T = make_float2(ca ? Tpre.x : T.x, cb ? Tpre.y : T.y);
-        // d rho terms: gdg = gval * dal * sigma for contributing, unclamped pixels
-        float2 gdg = __fmul2_rn(__fmul2_rn(gv, dal), make_float2(g.sigma, g.sigma));
-        gdg = make_float2(ca && !cl_a ? gdg.x : 0.0f, cb && !cl_b ? gdg.y : 0.0f);
-        const float c01 = 0.5f * g.c01x2;
-        const float2 ux = __ffma2_rn(make_float2(c01, c01), dy, make_float2(g.c00 * dx, g.c00 * dx));
-        const float2 uy = __ffma2_rn(make_float2(g.c11, g.c11), dy, make_float2(c01 * dx, c01 * dx));
-        const float2 s0 = __fmul2_rn(gdg, ux), s1 = __fmul2_rn(gdg, uy);
-        const float2 s2 = __fmul2_rn(s0, ux), s3 = __fmul2_rn(s0, uy), s4 = __fmul2_rn(s1, uy);
-        const float2 s5 = __fmul2_rn(w, gad);
-        const float f0 = s0.x + s0.y, f1 = s1.x + s1.y, f2 = s2.x + s2.y, f3 = s3.x + s3.y, f4 = s4.x + s4.y,
-                    f5 = s5.x + s5.y;
-        const float4* M = s_pj[k];
-#define GSF_COL(F4A, F4B, F4C, SV)                   \
-        {                                            \
-          const float2 sv = make_float2(SV, SV);     \
-          pa = __ffma2_rn(sv, F4A, pa);              \
-          pb2 = __ffma2_rn(sv, F4B, pb2);            \
-          pc2 = __ffma2_rn(sv, F4C, pc2);            \
-        }
-        const float4 m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3], m4 = M[4], m5 = M[5], m6 = M[6], m7 = M[7], m8 = M[8];
-        GSF_COL(make_float2(m0.x, m0.y), make_float2(m0.z, m0.w), make_float2(m1.x, m1.y), f0)
-        GSF_COL(make_float2(m1.z, m1.w), make_float2(m2.x, m2.y), make_float2(m2.z, m2.w), f1)
-        GSF_COL(make_float2(m3.x, m3.y), make_float2(m3.z, m3.w), make_float2(m4.x, m4.y), f2)
-        GSF_COL(make_float2(m4.z, m4.w), make_float2(m5.x, m5.y), make_float2(m5.z, m5.w), f3)
-        GSF_COL(make_float2(m6.x, m6.y), make_float2(m6.z, m6.w), make_float2(m7.x, m7.y), f4)
-        GSF_COL(make_float2(m7.z, m7.w), make_float2(m8.x, m8.y), make_float2(m8.z, m8.w), f5)
-#undef GSF_COL
-      }
-    }
-    {
-      const float lv[6] = {pa.x, pa.y, pb2.x, pb2.y, pc2.x, pc2.y};
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        double v = lv[a];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (lane == 0) s_pred[warp][a] += v;
-      }
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-  if (tid < 6) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < kTbThreads / 32; ++w) t += s_pred[w][tid];
-    bp.tile_pose[static_cast<size_t>(tile) * 6 + tid] = t;
-  }
-  __shared__ int s_last;
-  __shared__ double s_pose[6];
-  if (last_cta(ticket, &s_last, tid < 6)) {
-    block_reduce_rows<6, kTbThreads>(bp.tile_pose, gridDim.x, s_pose, s_pred);
-    if (tid < 6) ds->d_pose[tid] = s_pose[tid];
-  }
-}
-
-// The same tracking backward as independent single-warp CTAs: CTA 4 t + q owns quadrant q (8x8
+// k_blend_track: the pair arithmetic of both pixels runs on packed FP32x2 (shared dx); their
+// screen-space gradients are added before the contraction with the entry's pose matrix, so the
+// 18 FFMA2 of M s and the staging reads are paid once per two pixels.  Decisions (contributes /
+// clamped) are the forward's: same rho, same tests.
+//
+// Independent single-warp CTAs: CTA 4 t + q owns quadrant q (8x8
 // pixels, two per lane) of tile t and walks the tile list back to front in chunks of 32 entries,
 // one per lane: the lane stages its entry, tests it against the warp's block and, if it can
 // reach it, stages the entry's pose matrix.  No CTA barriers: a warp that has passed its
@@ -1177,22 +1002,8 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
                                                                        a.near_plane, a.far_plane, a.lp, ds, ticket); \
   } while (0)
     if (a.seed_mode == SEED_TRACK && nf == 6) {
-      static bool tb_attr = false;
-      if (!tb_attr) {
-        GSF_CUDA_CHECK(cudaFuncSetAttribute(k_backward_track, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(kTbSmem)));
-        tb_attr = true;
-      }
-#ifndef GSF_TB_VARIANT
-#define GSF_TB_VARIANT 1
-#endif
-#if GSF_TB_VARIANT == 0
-      k_backward_track<<<ntiles, kTbThreads, kTbSmem, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane,
-                                                            a.lp, ds, ticket);
-#else
       k_backward_track_w<<<4 * ntiles, 32, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
                                                      ws.wtickets + ws.wtickets_half, 4 * ntiles);
-#endif
     } else if (a.seed_mode == SEED_TRACK) {
       GSF_BWDP(SEED_TRACK, true);
     } else {
