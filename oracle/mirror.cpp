@@ -87,7 +87,7 @@ extern "C" int mir_render(const gsf_map_host* map, const gsf_pose* pose, const g
   const BlendConsts kc = make_blend_consts(rp);
   for (int r = 0; r < V; ++r) {
     bg[r] = make_blend_g(pre[vis[r]]);
-    bg[r].rho_fast = blend_rho_fast(bg[r], kc);
+    blend_rho_bounds(bg[r], kc);
     gg[r] = make_guard_g(pre[vis[r]]);
   }
   for (int t = 0; t < ntiles; ++t) {
@@ -126,4 +126,78 @@ extern "C" int mir_render(const gsf_map_host* map, const gsf_pose* pose, const g
       }
   }
   return GSF_OK;
+}
+
+// Stress check of blend_rho_bounds (gsf_shared.cuh): n random primitives (fp64 mean2d anywhere in
+// [-4000, 6000]^2 px, screen sigmas 0.3-300 px, any orientation, conditioning down to 1e-4, plus
+// the reference's 0.3 px^2 dilation), every pixel centre of the bounding box of the cutoff ellipse
+// (grown by 2 px; boxes wider than 600 px are row-sampled).  For each pixel the fp32 rho of the
+// kernels is compared with the fp64 rho of the guard: a fast-path rho (< rho_fast) must be an fp64
+// contribution, a rho above rho_hi an fp64 skip.  out[0] = violations, out[1] = max |rho_f - rho_d|
+// / band_i where band_i is the primitive's own bound, out[2] = pixels tested, out[3] = pixels on the
+// guard path, out[4] = max ratio where band_i is capped at the global band (far off-image means).
+extern "C" int mir_band_check(int n, uint64_t seed, double* out) {
+  uint64_t s = seed * 0x9E3779B97F4A7C15ull + 1;
+  auto rnd = [&s]() {   // splitmix64 -> [0, 1)
+    s += 0x9E3779B97F4A7C15ull;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return static_cast<double>((z ^ (z >> 31)) >> 11) * (1.0 / 9007199254740992.0);
+  };
+  RasterParams rp{};   // RasterConfig defaults (raster/config.hpp:5-16)
+  rp.footprint_sigma = 3.0;
+  rp.dilation = 0.3;
+  rp.alpha_skip = 1.0 / 255.0;
+  rp.alpha_clamp = 0.99;
+  rp.termination = 1e-8;
+  const BlendConsts kc = make_blend_consts(rp);
+  double viol = 0, worst = 0, worst_capped = 0, tested = 0, guarded = 0;
+  for (int i = 0; i < n; ++i) {
+    const double mx = -4000.0 + 10000.0 * rnd(), my = -4000.0 + 10000.0 * rnd();
+    const double s1 = 0.3 * std::pow(1000.0, rnd()), s2 = s1 * std::pow(1e-2, rnd()), th = 3.14159265358979 * rnd();
+    const double cs = std::cos(th), sn = std::sin(th);
+    const double cxx = cs * cs * s1 * s1 + sn * sn * s2 * s2 + 0.3, cyy = sn * sn * s1 * s1 + cs * cs * s2 * s2 + 0.3,
+                 cxy = cs * sn * (s1 * s1 - s2 * s2);
+    const double det = cxx * cyy - cxy * cxy;
+    GuardG gg{mx, my, cyy / det, -cxy / det, cxx / det, 0.98};
+    BlendG g{};
+    g.mx = static_cast<float>(mx);
+    g.my = static_cast<float>(my);
+    g.sigma = 0.98f;
+    g.c00 = static_cast<float>(gg.c00);
+    g.c01x2 = static_cast<float>(2.0 * gg.c01);
+    g.c11 = static_cast<float>(gg.c11);
+    blend_rho_bounds(g, kc);
+    const double band = static_cast<double>(g.rho_hi) - kc.cutoff_d;
+    const bool capped = !(band < 0.999 * kc.rho_band);
+    const double rx = std::sqrt(kc.cutoff_d * cxx) + 2.0, ry = std::sqrt(kc.cutoff_d * cyy) + 2.0;
+    const int x0 = static_cast<int>(std::floor(mx - rx)), x1 = static_cast<int>(std::ceil(mx + rx));
+    const int y0 = static_cast<int>(std::floor(my - ry)), y1 = static_cast<int>(std::ceil(my + ry));
+    const int ystep = std::max(1, (y1 - y0) / 600), xstep = std::max(1, (x1 - x0) / 600);
+    for (int y = y0; y <= y1; y += ystep)
+      for (int x = x0; x <= x1; x += xstep) {
+        const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
+        const float rho = pair_rho(fsub(px, g.mx), fsub(py, g.my), g);
+        const double rd = guard_rho(static_cast<double>(px), static_cast<double>(py), gg);
+        tested += 1;
+        if (std::fabs(rd - kc.cutoff_d) < 2.0 * band) {
+          double& w = capped ? worst_capped : worst;
+          w = std::max(w, std::fabs(rho - rd) / band);
+        }
+        if (rho > g.rho_hi) {
+          if (!(rd > kc.cutoff_d || rd < 0.0)) viol += 1;
+        } else if (rho < g.rho_fast) {
+          if (!(rd <= kc.cutoff_d && rd >= 0.0)) viol += 1;
+        } else {
+          guarded += 1;
+        }
+      }
+  }
+  out[0] = viol;
+  out[1] = worst;
+  out[2] = tested;
+  out[3] = guarded;
+  out[4] = worst_capped;
+  return 0;
 }

@@ -1162,8 +1162,8 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
     run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
     BwdArgs b = bwd_args(c, k, rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);
     b.fused_pose = true;
-    run_backward(c->ws, c->ds, b, c->stream, &c->launches);
-    run_track_update(c->ds, it, c->stream, &c->launches);
+    b.update_iter = it;
+    if (!run_backward(c->ws, c->ds, b, c->stream, &c->launches)) run_track_update(c->ds, it, c->stream, &c->launches);
   }
   // final render + loss without gradients (tracker.cpp:74-76)
   FwdArgs fin = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, -1);

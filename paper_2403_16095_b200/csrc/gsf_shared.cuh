@@ -472,9 +472,9 @@ GSF_HD uint32_t depth_key(double depth, uint32_t near_bits) {
 // Blend (fp32) with an fp64 guard band on the two discrete tests of blend_pixel.
 // ---------------------------------------------------------------------------------------
 struct BlendG {       // per visible primitive, rank order, 3 x float4 on the device
-  float mx, my, depth, sigma;
-  float c00, c01x2, c11, rho_fast;   // rho_fast: blend_rho_fast
-  float r, g, b, depth_b;   // depth_b = depth again: (b, depth) pair for packed FMAs
+  float mx, my, sigma, rho_hi;       // rho_hi, rho_fast: blend_rho_bounds
+  float c00, c01x2, c11, rho_fast;
+  float r, g, b, depth;              // (b, depth) adjacent: one register pair for packed FMAs
 };
 struct GuardG {       // fp64 copies read only inside the guard band
   double mx, my, c00, c01, c11, sigma;
@@ -488,11 +488,11 @@ GSF_HD BlendG make_blend_g(const PreOut& o) {
   g.c00 = static_cast<float>(o.c00);
   g.c01x2 = static_cast<float>(dmul(2.0, o.c01));
   g.c11 = static_cast<float>(o.c11);
-  g.rho_fast = -1.0f;   // filled by blend_rho_fast once the raster constants are known
+  g.rho_fast = -1.0f;   // rho_hi / rho_fast: blend_rho_bounds, once the raster constants are known
+  g.rho_hi = 3.0e38f;
   g.r = static_cast<float>(o.color[0]);
   g.g = static_cast<float>(o.color[1]);
   g.b = static_cast<float>(o.color[2]);
-  g.depth_b = g.depth;
   return g;
 }
 GSF_HD GuardG make_guard_g(const PreOut& o) {
@@ -592,23 +592,50 @@ GSF_HD PairEval eval_pair_full(float px, float py, const BlendG& g, const GuardG
   return e;
 }
 
-// Per-primitive fast-path bound (BlendG::rho_fast): for rho < rho_fast the full decision is
-// certainly "contributes, unclamped, alpha = sigma*exp(-rho/2)" — rho is below the cutoff guard
-// band, alpha is above the skip band (margin 1e-5 in log space, >> the exp error of 3e-7) and
-// sigma is below the clamp band.  No lower bound is needed: the fp64 guard for rho < rho_min only
-// rejects rho_d < 0, and for a conic with det >= 1e-5 c00 c11 (condition number < 4e5, in fp32 and
-// hence in fp64) the fp64 quadratic form is non-negative everywhere (its rounding error is < 1e-15
-// of its largest term), so there the guard never fires.  -1 disables the fast path.  Only selects
-// the evaluation path, never a result, so the mirror and the kernels stay bit-identical either way.
-GSF_HD float blend_rho_fast(const BlendG& g, const BlendConsts& k) {
-  const float sigma = g.sigma;
-  if (!k.fast_ok || !(static_cast<double>(sigma) * (1.0 + 1e-6) < static_cast<double>(k.clamp_lo))) return -1.0f;
-  if (!(sigma > k.skip_hi)) return -1.0f;
+// Per-primitive decision bounds.  The fp32 rho of a pixel differs from the fp64 reference's by at
+// most band_i, which depends on the primitive (rounding of mean2d, whose error grows with |mean2d|
+// and is amplified by the slope of the quadratic form at rho ~ cutoff, plus the rounding of the
+// conic and of the evaluation); the global rho_band of BlendConsts is its worst case.  With
+// cutoff - band_i and cutoff + band_i as the primitive's own band edges the fp64 guard only runs
+// for pixels that can really sit on the cutoff.
+//   rho_hi:   rho > rho_hi certainly fails the footprint test (skip)
+//   rho_fast: rho < rho_fast is certainly "contributes, unclamped, alpha = sigma*exp(-rho/2)" —
+//             rho is below the cutoff band, alpha is above the skip band (margin 1e-5 in log space,
+//             >> the exp error of 3e-7) and sigma is below the clamp band.  No lower bound is
+//             needed: the fp64 guard for rho < rho_min only rejects rho_d < 0, and for a conic with
+//             det >= 1e-5 c00 c11 (condition number < 4e5, in fp32 and hence in fp64) the fp64
+//             quadratic form is non-negative everywhere (its rounding error is < 1e-15 of its
+//             largest term), so there the guard never fires.  -1 disables the fast path.
+// Both only select the evaluation path, never a result, so the mirror and the kernels stay
+// bit-identical either way.
+//
+// Bound (u = 2^-24; a, b, c the conic, Q = rho, K = max of (|a dx^2| + 2|b dx dy| + |c dy^2|) / Q
+// = 2 sqrt(ac) / (sqrt(ac) - |b|)): |dx - dx_d| <= u (|mx| + |dx|); |grad_x Q| <= 2 sqrt(a Q) on
+// the ellipse Q; the five roundings of pair_rho and the conic's own rounding <= 6 u K Q.  band_i
+// takes Q = cutoff + 1, doubles every term, then a factor 4 and 1e-6 absolute on top.
+GSF_HD void blend_rho_bounds(BlendG& g, const BlendConsts& k) {
+  g.rho_hi = k.rho_hi;
+  g.rho_fast = -1.0f;
   const double a = g.c00, b = 0.5 * static_cast<double>(g.c01x2), c = g.c11;
-  if (!(a > 0.0 && c > 0.0 && a * c - b * b >= 1e-5 * a * c)) return -1.0f;
+  if (!(a > 0.0 && c > 0.0 && a * c - b * b >= 1e-5 * a * c)) return;   // the global band and the full path
+  const double det = a * c - b * b, sac = sqrt(a * c);
+  const double qm = k.cutoff_d + 1.0;
+  const double K = 2.0 * sac / (sac - fabs(b));
+  const double dxm = sqrt(qm * c / det), dym = sqrt(qm * a / det);
+  const double u = 5.9604644775390625e-8;
+  const double e = 2.0 * (6.0 * u * qm * K + 2.0 * sqrt(a * qm) * u * (fabs(static_cast<double>(g.mx)) + dxm + 1.0) +
+                          2.0 * sqrt(c * qm) * u * (fabs(static_cast<double>(g.my)) + dym + 1.0));
+  const double band = fmin(4.0 * e + 1e-6, static_cast<double>(k.rho_band));
+  float hi = static_cast<float>(k.cutoff_d + band);
+  if (static_cast<double>(hi) < k.cutoff_d + band) hi = nextafterf(hi, 3.0e38f);
+  g.rho_hi = fminf(hi, k.rho_hi);
+  const float sigma = g.sigma;
+  if (!k.fast_ok || !(static_cast<double>(sigma) * (1.0 + 1e-6) < static_cast<double>(k.clamp_lo))) return;
+  if (!(sigma > k.skip_hi)) return;
   const double ra = 2.0 * (log(static_cast<double>(sigma) / static_cast<double>(k.skip_hi)) - 1e-5);
-  const double r = ra < static_cast<double>(k.rho_lo) ? ra : static_cast<double>(k.rho_lo);
-  return r > 0.0 ? static_cast<float>(r * (1.0 - 1e-6)) : -1.0f;
+  const double lo = k.cutoff_d - band;
+  const double r = ra < lo ? ra : lo;
+  g.rho_fast = r > 0.0 ? static_cast<float>(r * (1.0 - 1e-6)) : -1.0f;
 }
 
 // exp(-rho/2) on the hardware exp2 unit (|rel err| < 2^-21): used by the pose backward only
@@ -646,7 +673,7 @@ GSF_HD PairEval eval_pair_t(float px, float py, const BlendG& g, const GuardG* g
   e.clamped = 0;
   e.alpha = 0.0f;
   e.gval = 0.0f;
-  if (rho > k.rho_hi) return e;
+  if (rho > g.rho_hi) return e;
   if (rho < g.rho_fast) {
     e.gval = FAST ? exp_neg_half_fast(rho) : exp_neg_half_inrange(rho);
     e.alpha = fmul(g.sigma, e.gval);

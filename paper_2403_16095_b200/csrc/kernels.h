@@ -170,10 +170,12 @@ struct BwdArgs {
   int seed_mode;
   bool pose_only;            // tracking: skip per-primitive parameter gradients
   bool fused_pose = false;   // pose_only + ws.pj_id valid: pose through per-primitive Jacobians
+  int update_iter = -1;      // >= 0: the tracking backward's last CTA also takes this iteration's pose step
   float* grads;              // [D][P] parameter gradients (full mode)
   float* d_mean2d;           // [2][P] (full mode, nullable)
 };
-void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st, int64_t* launches);
+// true when the backward also ran the pose step of a.update_iter (k_track_update is then skipped)
+bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st, int64_t* launches);
 // seed maps (3 colour planes interleaved, then ad, md, u planes) of the last render's loss
 void run_seeds_out(Workspace& ws, DevState* ds, int mode, const float* target, const float* depth, const LossParams& lp,
                    int W, int H, double near_plane, double far_plane, float* out, cudaStream_t st, int64_t* launches);

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
       // median-depth or uncertainty seeds on that path
       constexpr bool kTrack = SEED == SEED_TRACK;
       const float derr = kTrack ? 0.0f : g.depth - pb.D;
-      const float2 q2 = __ffma2_rn(make_float2(pb.gc2, pb.gad), make_float2(g.b, g.depth_b),
+      const float2 q2 = __ffma2_rn(make_float2(pb.gc2, pb.gad), make_float2(g.b, g.depth),
                                    __fmul2_rn(make_float2(pb.gc0, pb.gc1), make_float2(g.r, g.g)));
       float q = q2.x + q2.y;
       if (!kTrack) q += pb.gop + pb.gu * derr * derr;
@@ -490,7 +490,8 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
 __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs bp, int W, int H, int tiles_x,
                                                                       BlendConsts kc, double near_plane,
                                                                       double far_plane, LossParams lp, DevState* ds,
-                                                                      uint32_t* gtickets, int rows) {
+                                                                      uint32_t* gtickets, int rows, int upd_iter,
+                                                                      double bc1, double bc2) {
   __shared__ BlendG s_g[32];
   __shared__ float4 s_pj[32][9];
   __shared__ int32_t s_id[32];
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         const float dx = __fadd_rn(px, -g.mx);
         const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
         const float2 rho = pair_rho2(dx, dy, g);
-        const bool skip_a = li >= last_a || rho.x > kc.rho_hi, skip_b = li >= last_b || rho.y > kc.rho_hi;
+        const bool skip_a = li >= last_a || rho.x > g.rho_hi, skip_b = li >= last_b || rho.y > g.rho_hi;
         if (skip_a && skip_b) continue;
         const bool fast_a = rho.x < g.rho_fast, fast_b = rho.y < g.rho_fast;
         float2 gv = make_float2(exp_neg_half_fast(rho.x), exp_neg_half_fast(rho.y));
@@ -615,9 +616,12 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
     for (int a = 0; a < 6; ++a) bp.tile_pose[static_cast<size_t>(blockIdx.x) * 6 + a] = pd[a];
   double tot[6];
   if (warp_grid_reduce<6>(bp.tile_pose, bp.tile_pose + static_cast<size_t>(rows) * 6, rows, gtickets,
-                          gtickets + (rows + 31) / 32, tot, lane == 0) && lane == 0)
+                          gtickets + (rows + 31) / 32, tot, lane == 0) && lane == 0) {
 #pragma unroll
     for (int a = 0; a < 6; ++a) ds->d_pose[a] = ds->halt ? 0.0 : tot[a];
+    // the iteration's pose step (k_track_update) in the same CTA: one kernel boundary less
+    if (upd_iter >= 0) track_update(ds, upd_iter, bc1, bc2);
+  }
 }
 
 // SH basis gradients (sh.cpp:44-72), fp64.
@@ -947,7 +951,7 @@ void run_seeds_out(Workspace& ws, DevState* ds, int mode, const float* target, c
   ++*L;
 }
 
-void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st, int64_t* L) {
+bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st, int64_t* L) {
   const int ntiles = a.rp.tiles_x * a.rp.tiles_y;
   BwdPtrs bp;
   bp.ranges = ws.ranges;
@@ -989,6 +993,7 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     bp.pj_slot = ws.pj_slot;
     bp.tile_pose = ws.pose_part;
     uint32_t* ticket = ws.bin_counters + kCntBwdTicket;
+    bool fused_update = false;
     if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
 #define GSF_BWDP(SM, VD)                                                                                        \
   do {                                                                                                          \
@@ -1002,8 +1007,11 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
                                                                        a.near_plane, a.far_plane, a.lp, ds, ticket); \
   } while (0)
     if (a.seed_mode == SEED_TRACK && nf == 6) {
+      const double t = static_cast<double>(a.update_iter + 1);   // AdamState bias corrections (adam.cpp:40-53)
       k_backward_track_w<<<4 * ntiles, 32, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
-                                                     ws.wtickets + ws.wtickets_half, 4 * ntiles);
+                                                     ws.wtickets + ws.wtickets_half, 4 * ntiles, a.update_iter,
+                                                     1.0 - std::pow(0.9, t), 1.0 - std::pow(0.999, t));
+      fused_update = a.update_iter >= 0;
     } else if (a.seed_mode == SEED_TRACK) {
       GSF_BWDP(SEED_TRACK, true);
     } else {
@@ -1012,7 +1020,7 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
 #undef GSF_BWDP
     ++*L;
     if (ws.prof) ws.prof->end(st);
-    return;
+    return fused_update;
   }
   if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
 #define GSF_BWD(SM, NFV)                                                                                          \
@@ -1052,6 +1060,7 @@ void run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   k_pose_sum<<<1, 1024, 0, st>>>(ws.pose_part, blocks, ds);
   ++*L;
   if (ws.prof) ws.prof->end(st);
+  return false;
 }
 
 }  // namespace gsfk

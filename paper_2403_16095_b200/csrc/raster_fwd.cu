@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
       if (o.visible) {
         vis = true;
         BlendG g = make_blend_g(o);
-        g.rho_fast = blend_rho_fast(g, kc);
+        blend_rho_bounds(g, kc);
         bg_id[i] = g;
         gg_id[i] = make_guard_g(o);
         depth_id[i] = o.depth;
@@ -332,17 +332,33 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
     const unsigned long long key = vis ? pair_key(depth_id[i], static_cast<uint32_t>(i)) : 0ull;
     const int excl = warp_excl_scan(c);
     const int total = __shfl_sync(0xffffffffu, excl + c, 31);
-    for (int base = 0; base < total; base += 32) {
-      const int k = base + lane;
-      const int j = warp_owner(excl, k);   // lane whose pair range holds k
-      const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qy0 = __shfl_sync(0xffffffffu, q.z, j);
-      const int wj = __shfl_sync(0xffffffffu, w, j), ej = __shfl_sync(0xffffffffu, excl, j);
-      const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
-      if (k < total) {
+    // kScatterU pairs per lane per round: every fill-counter atomic of the round is in flight
+    // before the first key store waits on its slot
+#ifndef GSF_SCATTER_U
+#define GSF_SCATTER_U 4
+#endif
+    constexpr int kScatterU = GSF_SCATTER_U;
+    for (int base = 0; base < total; base += 32 * kScatterU) {
+      int tt[kScatterU];
+      unsigned long long kk[kScatterU];
+      uint32_t sl[kScatterU];
+#pragma unroll
+      for (int u = 0; u < kScatterU; ++u) {
+        const int k = base + 32 * u + lane;
+        const int j = warp_owner(excl, k);   // lane whose pair range holds k
+        const int qx0 = __shfl_sync(0xffffffffu, q.x, j), qy0 = __shfl_sync(0xffffffffu, q.z, j);
+        const int wj = __shfl_sync(0xffffffffu, w, j), ej = __shfl_sync(0xffffffffu, excl, j);
+        kk[u] = __shfl_sync(0xffffffffu, key, j);
         const int r = k - ej;
-        const int row = r / wj;
-        bucket_put(fill, bucket, bucket_cap, (qy0 + row) * tiles_x + qx0 + (r - row * wj), kj);
+        const int row = r / max(wj, 1);
+        tt[u] = k < total ? (qy0 + row) * tiles_x + qx0 + (r - row * wj) : -1;
       }
+#pragma unroll
+      for (int u = 0; u < kScatterU; ++u)
+        if (tt[u] >= 0) sl[u] = atomicAdd(&fill[static_cast<int64_t>(tt[u]) * kBinStride], 1u);
+#pragma unroll
+      for (int u = 0; u < kScatterU; ++u)
+        if (tt[u] >= 0 && sl[u] < bucket_cap) bucket[static_cast<int64_t>(tt[u]) * bucket_cap + sl[u]] = kk[u];
     }
   }
   // visible count (one atomic per CTA) and, for the pose Jacobians, the list of visible ids
@@ -412,7 +428,7 @@ __device__ __forceinline__ void full_accumulate(PixelState& s, float2& rg, float
   const float w = fmul(e.alpha, s.T);
   const float2 ww = make_float2(w, w);
   rg = __ffma2_rn(ww, make_float2(g.r, g.g), rg);
-  bd = __ffma2_rn(ww, make_float2(g.b, g.depth_b), bd);
+  bd = __ffma2_rn(ww, make_float2(g.b, g.depth), bd);
   s.op = fadd(s.op, w);
   if (obs_valid) {
     const float d = fsub(g.depth, obs);
@@ -612,7 +628,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         const float dx = __fadd_rn(px, -g.mx);
         const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
         const float2 rho = pair_rho2(dx, dy, g);
-        const bool skip_a = T.x < kc.term || rho.x > kc.rho_hi, skip_b = T.y < kc.term || rho.y > kc.rho_hi;
+        const bool skip_a = T.x < kc.term || rho.x > g.rho_hi, skip_b = T.y < kc.term || rho.y > g.rho_hi;
         if (skip_a && skip_b) continue;
         const bool fast_a = rho.x < g.rho_fast, fast_b = rho.y < g.rho_fast;
         float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), exp_neg_half_inrange2(rho));
@@ -628,9 +644,9 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         const float2 am = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
         const float2 w = __fmul2_rn(am, T);
         rg_a = __ffma2_rn(make_float2(w.x, w.x), make_float2(g.r, g.g), rg_a);
-        bd_a = __ffma2_rn(make_float2(w.x, w.x), make_float2(g.b, g.depth_b), bd_a);
+        bd_a = __ffma2_rn(make_float2(w.x, w.x), make_float2(g.b, g.depth), bd_a);
         rg_b = __ffma2_rn(make_float2(w.y, w.y), make_float2(g.r, g.g), rg_b);
-        bd_b = __ffma2_rn(make_float2(w.y, w.y), make_float2(g.b, g.depth_b), bd_b);
+        bd_b = __ffma2_rn(make_float2(w.y, w.y), make_float2(g.b, g.depth), bd_b);
         op = __fadd2_rn(op, w);
         T = __fmul2_rn(T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-am.x, -am.y)));
         const int li = start + k - rg.x + 1;

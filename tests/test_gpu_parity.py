@@ -415,7 +415,12 @@ def test_tracking_100_iterations_cfg1_sized(gpu_ctx, orc):
     # near the optimum Adam steps of ~lr (1.5e-3 rad, 2.2e-3 m) flip with the gradient signs, so fp32-vs-fp64
     # gradient noise moves the end point by a fraction of a step: 1/3 of lr (SURVEY 8(c) fallback criterion)
     assert rotation_error(res.pose, ores.pose) < 5e-4 and translation_error(res.pose, ores.pose) < 7e-4
-    assert res.final_loss == pytest.approx(ores.final_loss, rel=5e-2, abs=1e-6)
+    # the final loss is the tracking loss of one more render at the end point (tracker.cpp:74-76); near the
+    # optimum it changes by tens of percent inside that 5e-4 ball, so it is checked against the oracle's
+    # loss at the GPU's own end point (render without observed depth, tracker.cpp:43)
+    ofin, _, _ = orc.tracking_loss(orc.render(m, res.pose, K), fr[0][0], fr[0][1], K, w)
+    print("final loss", res.final_loss, "oracle at the same pose", ofin.total, "oracle trajectory", ores.final_loss)
+    assert res.final_loss == pytest.approx(ofin.total, rel=1e-4, abs=1e-9)
 
 
 def test_tracking_leaves_trust_region(gpu_ctx, orc):
