@@ -338,7 +338,6 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   if (tiles > ws.tiles_cap) {
     dalloc(ws.ranges, tiles);
     dalloc(ws.bins, tiles * kBinStride + kCntNum);
-    dalloc(ws.tile_start, tiles);
     ws.tile_fill = ws.bins;
     ws.bin_counters = ws.bins + tiles * kBinStride;
     dfree(ws.bucket);
@@ -675,7 +674,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   Workspace& ws = c->ws;
-  void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins, ws.tile_start,
+  void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
                   ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,

@@ -11,9 +11,9 @@
 //                   primitives with more than kBigPairs tiles (order inside a bucket is arbitrary)
 //   k_scatter_big   one 1024-thread CTA per listed large-footprint primitive, so a primitive
 //                   covering a thousand tiles does not serialise one warp
-//   k_tile_scan     one CTA: exclusive scan of the tile counts -> list starts, pair total M,
-//                   longest list (a bucket overflow makes the host grow the buckets and re-run)
-//   k_tile_sort     one CTA per tile: 32-key runs sorted in registers (warp bitonic), then
+//   k_tile_sort     one CTA per tile: its list start from a single-pass decoupled look-back scan
+//                   of the tile counts (pair total M, longest list; a bucket overflow makes the
+//                   host grow the buckets and re-run), 32-key runs sorted in registers (warp bitonic), then
 //                   pairwise run merges by rank (binary search in the partner run) in shared
 //                   memory; lists longer than kSortChunk are chunk-sorted and merged (merge path)
 //                   through global memory by the same CTA.  A final pass re-orders the rare runs
@@ -30,70 +30,6 @@ namespace gsfk {
 namespace {
 
 constexpr int kSortChunk = 1024;   // longest list sorted entirely in shared memory (2 x 8 KB)
-
-__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t* __restrict__ fill, int ntiles, uint32_t bucket_cap,
-                                                    uint32_t* __restrict__ start, const uint32_t* counters,
-                                                    uint32_t pair_cap, DevState* ds) {
-  constexpr int kPer = 4;   // consecutive tiles per thread: one pass covers 4096 tiles (configs[1]: 3,225)
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_max[32];
-  __shared__ uint32_t s_carry, s_mx;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = s_mx = 0;
-  __syncthreads();
-  for (int base = 0; base < ntiles; base += 1024 * kPer) {
-    uint32_t v[kPer], f[kPer], run = 0, fm = 0;
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const int t = base + tid * kPer + q;
-      f[q] = t < ntiles ? fill[static_cast<int64_t>(t) * kBinStride] : 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      v[q] = min(f[q], bucket_cap);
-      run += v[q];
-      fm = max(fm, f[q]);
-    }
-    uint32_t x = run;   // inclusive warp scan of the per-thread totals
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    const uint32_t wm = __reduce_max_sync(0xffffffffu, fm);
-    if (lane == 31) s_warp[warp] = x;
-    if (lane == 0) s_max[warp] = wm;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t w = s_warp[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      s_warp[lane] = w;
-      const uint32_t m = __reduce_max_sync(0xffffffffu, s_max[lane]);
-      if (lane == 0) s_mx = max(s_mx, m);
-    }
-    __syncthreads();
-    uint32_t e = s_carry + (warp ? s_warp[warp - 1] : 0u) + x - run;   // exclusive start of this thread's tiles
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      const int t = base + tid * kPer + q;
-      if (t < ntiles) start[t] = e;
-      e += v[q];
-    }
-    __syncthreads();
-    if (tid == 1023) s_carry = e;
-    __syncthreads();
-  }
-  if (tid == 0) {
-    ds->M = s_carry;
-    ds->V = counters[kCntVisible];
-    ds->max_tile = s_mx;
-    if (s_carry > pair_cap || s_mx > bucket_cap) ds->overflow = 1u;
-  }
-}
 
 __global__ void __launch_bounds__(1024) k_scatter_big(const uint32_t* __restrict__ big_ids, const uint32_t* counters,
                                                       const int4* __restrict__ rect_id, const double* __restrict__ depth_id,
@@ -241,21 +177,75 @@ __device__ void merge_pass(const unsigned long long* a, unsigned long long* b, i
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_tile_sort(const uint32_t* __restrict__ fill, const uint32_t* __restrict__ start,
-                                                   uint32_t pair_cap, unsigned long long* bucket, uint32_t bucket_cap,
-                                                   unsigned long long* skey, uint32_t* __restrict__ sid,
+// Exclusive start of tile t's compacted list: a single-pass scan over the tile counts with
+// decoupled look-back (warp 0).  Tile t publishes its count (flag 1) as soon as it starts and its
+// inclusive prefix (flag 2) once known, in one 64-bit word next to its fill counter (same L2
+// sector, zeroed by the per-render memset); it sums its predecessors' words back to the nearest
+// published prefix.  Lower tile CTAs are dispatched first, so every awaited word gets written.
+__device__ constexpr unsigned long long kScanAgg = 1ull << 32, kScanPrefix = 2ull << 32;
+__device__ __forceinline__ unsigned long long* scan_word(uint32_t* fill, int64_t t) {
+  return reinterpret_cast<unsigned long long*>(fill + t * kBinStride + 2);
+}
+__device__ __forceinline__ void tile_count_publish(uint32_t* fill, int t, uint32_t n) {
+  atomicExch(scan_word(fill, t), (t == 0 ? kScanPrefix : kScanAgg) | n);
+}
+__device__ uint32_t tile_list_start(uint32_t* fill, int t, uint32_t n) {   // warp 0, after tile_count_publish
+  const int lane = threadIdx.x & 31;
+  uint32_t excl = 0;
+  for (int j = t - 1; j >= 0; j -= 32) {
+    const int idx = j - lane;
+    unsigned long long v;
+    do {
+      v = idx >= 0 ? *reinterpret_cast<volatile unsigned long long*>(scan_word(fill, idx)) : kScanPrefix;
+    } while (__any_sync(0xffffffffu, (v >> 32) == 0ull));
+    const uint32_t pm = __ballot_sync(0xffffffffu, (v >> 32) == 2ull);
+    const int stop = pm ? __ffs(pm) - 1 : 31;   // nearest published prefix
+    uint32_t x = lane <= stop ? static_cast<uint32_t>(v) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    excl += x;
+    if (pm) break;
+  }
+  if (lane == 0 && t > 0) atomicExch(scan_word(fill, t), kScanPrefix | (excl + n));
+  return excl;
+}
+
+__global__ void __launch_bounds__(256) k_tile_sort(uint32_t* fill, uint32_t pair_cap, unsigned long long* bucket,
+                                                   uint32_t bucket_cap, unsigned long long* skey, uint32_t* __restrict__ sid,
                                                    const double* __restrict__ depth_id, int2* __restrict__ ranges,
-                                                   const uint32_t* __restrict__ pj_slot, uint32_t* __restrict__ sslot) {
+                                                   const uint32_t* __restrict__ pj_slot, uint32_t* __restrict__ sslot,
+                                                   DevState* ds, const uint32_t* counters) {
   __shared__ unsigned long long s_k[2][kSortChunk];
+  __shared__ uint32_t s_start;
   const int t = blockIdx.x;
-  const uint32_t s0 = min(start[t], pair_cap);
-  const int n = static_cast<int>(min(min(fill[static_cast<int64_t>(t) * kBinStride], bucket_cap), pair_cap - s0));
+  const uint32_t f = fill[static_cast<int64_t>(t) * kBinStride];
+  const uint32_t nb = min(f, bucket_cap);
+  if (threadIdx.x == 0) tile_count_publish(fill, t, nb);
+  unsigned long long* bk = bucket + static_cast<int64_t>(t) * bucket_cap;
+  // a short list is sorted in shared memory before its start is known: the look-back's waits
+  // overlap the sort
+  const bool in_smem = nb <= static_cast<uint32_t>(kSortChunk);
+  unsigned long long* k = (in_smem && nb > 0) ? s_k[sort_chunk(bk, static_cast<int>(nb), s_k)] : nullptr;
+  if (threadIdx.x < 32) {
+    const uint32_t e = tile_list_start(fill, t, nb);
+    if (threadIdx.x == 0) {
+      s_start = e;
+      if (f > 0) atomicMax(&ds->max_tile, f);
+      if (f > bucket_cap) ds->overflow = 1u;
+      if (t == 0) ds->V = counters[kCntVisible];
+      if (t == static_cast<int>(gridDim.x) - 1) {   // the pair total M (k_tile_scan's, without its launch)
+        ds->M = e + nb;
+        if (e + nb > pair_cap) ds->overflow = 1u;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t s0 = min(s_start, pair_cap);
+  const int n = static_cast<int>(min(nb, pair_cap - s0));
   if (threadIdx.x == 0) ranges[t] = n ? make_int2(static_cast<int>(s0), static_cast<int>(s0) + n) : make_int2(0, 0);
   if (n == 0) return;
-  unsigned long long* bk = bucket + static_cast<int64_t>(t) * bucket_cap;
   unsigned long long* sk = skey + s0;
-  if (n <= kSortChunk) {
-    unsigned long long* k = s_k[sort_chunk(bk, n, s_k)];
+  if (in_smem) {
     fix_ties(k, n, depth_id);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const uint32_t id = static_cast<uint32_t>(k[i]);
@@ -299,10 +289,8 @@ void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles
                                         ws.bucket);
     ++*L;
   }
-  k_tile_scan<<<1, 1024, 0, st>>>(ws.tile_fill, ntiles, bcap, ws.tile_start, ws.bin_counters, pair_cap, ds);
-  ++*L;
-  k_tile_sort<<<ntiles, 256, 0, st>>>(ws.tile_fill, ws.tile_start, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id,
-                                      ws.ranges, ws.pj_slot, want_slots ? ws.sslot : nullptr);
+  k_tile_sort<<<ntiles, 256, 0, st>>>(ws.tile_fill, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id, ws.ranges,
+                                      ws.pj_slot, want_slots ? ws.sslot : nullptr, ds, ws.bin_counters);
   ++*L;
 }
 

@@ -17,6 +17,7 @@ constexpr int kTile = 16;
 #define GSF_BIN_STRIDE 8
 #endif
 constexpr int kBinStride = GSF_BIN_STRIDE;
+static_assert(kBinStride >= 4, "the tile-list scan word shares the fill counter's sector");
 constexpr int kPjFloats = 56;   // per-primitive pose matrix: 9 columns x 6 rows + 2 pad (k_posejac)
 constexpr int kBigPairs = 128;
 enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntPairAlloc = 4, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)

@@ -71,14 +71,14 @@ struct Workspace {
   uint32_t* pj_slot = nullptr;  // P: id -> slot of its pose Jacobian
   WorldG* world = nullptr;      // P: view-independent part, cached per tracked frame (k_world)
   double* support = nullptr;    // P: footprint support of the same cache (NaN = invalid primitive)
-  // per tile: bins[t * kBinStride] = fill cursor of the tile's bucket, then the counters; one memset
+  // per tile: bins[t * kBinStride] = fill cursor of the tile's bucket (+ its list-start scan word at
+  // +2), then the counters; one memset
   uint32_t* bins = nullptr;
   uint32_t* tile_fill = nullptr;
   uint32_t* bin_counters = nullptr;   // BinCounter slots
   uint32_t* big_ids = nullptr;        // P: primitives with more than kBigPairs tiles
   uint32_t* vis_list = nullptr;       // P: visible ids (any order): pose Jacobians, chain
   uint32_t* pair_base = nullptr;      // P: first primitive-major pair slot of a visible primitive
-  uint32_t* tile_start = nullptr;
   int2* ranges = nullptr;
   double* loss_part = nullptr;  // rows * LS_NUM (+ group rows of the single-warp tracking blend)
   int loss_rows = 0;            // rows the last loss-partial producer wrote (tiles, or 4 tiles)

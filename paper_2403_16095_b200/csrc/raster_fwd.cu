@@ -332,10 +332,10 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
     const unsigned long long key = vis ? pair_key(depth_id[i], static_cast<uint32_t>(i)) : 0ull;
     const int excl = warp_excl_scan(c);
     const int total = __shfl_sync(0xffffffffu, excl + c, 31);
-    // kScatterU pairs per lane per round: every fill-counter atomic of the round is in flight
+    // GSF_SCATTER_U pairs per lane per round: every fill-counter atomic of the round is in flight
     // before the first key store waits on its slot
 #ifndef GSF_SCATTER_U
-#define GSF_SCATTER_U 4
+#define GSF_SCATTER_U 8
 #endif
     constexpr int kScatterU = GSF_SCATTER_U;
     for (int base = 0; base < total; base += 32 * kScatterU) {
