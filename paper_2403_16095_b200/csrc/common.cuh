@@ -103,6 +103,31 @@ __device__ __forceinline__ bool block_hit8(const BlendG& g, float bx0, float by0
   return quad_min_rect(a, b, c, x0, x0 + 7.0f, y0, y0 + 7.0f) <= thr;
 }
 
+// Shared-memory loads from an explicit 32-bit address.  opaque_smem_base() returns the address of a
+// __shared__ object through a warp shuffle, which ptxas cannot re-derive: the hot loops then keep
+// one base register instead of re-forming (SR_CgaCtaId << 24) + offset with an S2R per access.
+__device__ __forceinline__ uint32_t opaque_smem_base(const void* p) {
+  return __shfl_sync(0xffffffffu, static_cast<uint32_t>(__cvta_generic_to_shared(p)), 0);
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ BlendG lds_blend(uint32_t a) {
+  const float4 a0 = lds_f4(a), a1 = lds_f4(a + 16), a2 = lds_f4(a + 32);
+  BlendG g;
+  g.mx = a0.x; g.my = a0.y; g.sigma = a0.z; g.rho_hi = a0.w;
+  g.c00 = a1.x; g.c01x2 = a1.y; g.c11 = a1.z; g.rho_fast = a1.w;
+  g.r = a2.x; g.g = a2.y; g.b = a2.z; g.depth = a2.w;
+  return g;
+}
+
 // Ampere-style asynchronous global -> shared copies (cp.async, 16 bytes, L1-allocating).
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));

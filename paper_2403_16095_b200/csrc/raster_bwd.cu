@@ -492,10 +492,13 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
                                                                       double far_plane, LossParams lp, DevState* ds,
                                                                       uint32_t* gtickets, int rows, int upd_iter,
                                                                       double bc1, double bc2) {
-  __shared__ BlendG s_g[32];
-  __shared__ float4 s_pj[32][9];
-  __shared__ int32_t s_id[32];
+  // one staging buffer: 32 records (3 float4), 32 pose matrices (9 float4), 32 slots
+  __shared__ float4 s_buf[32 * 3 + 32 * 9 + 8];
+  BlendG* s_g = reinterpret_cast<BlendG*>(s_buf);
+  float4 (*s_pj)[9] = reinterpret_cast<float4 (*)[9]>(s_buf + 32 * 3);
+  int32_t* s_id = reinterpret_cast<int32_t*>(s_buf + 32 * 12);
   const int lane = threadIdx.x;
+  const uint32_t sb = opaque_smem_base(s_buf);
   const int tile = blockIdx.x >> 2, qd = blockIdx.x & 3;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x = tx * kTile + 8 * (qd & 1) + (lane & 7);
@@ -541,7 +544,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         const int k = 31 - __clz(bits);
         bits &= ~(1u << k);
         const int li = bstart + k - rg.x;
-        const BlendG g = s_g[k];
+        const BlendG g = lds_blend(sb + 48u * k);
         const float dx = __fadd_rn(px, -g.mx);
         const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
         const float2 rho = pair_rho2(dx, dy, g);
@@ -553,14 +556,14 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
         int cl_a = 0, cl_b = 0;
         if (!skip_a && !fast_a) {
-          const GuardOut o = guard_decide(px, py.x, g, bp.gg_slot + s_id[k], &kc);
+          const GuardOut o = guard_decide(px, py.x, g, bp.gg_slot + lds_s32(sb + 6144u + 4u * k), &kc);
           al.x = o.alpha;
           gv.x = o.gval;
           cl_a = o.clamped;
           ca = al.x >= 0.0f;
         }
         if (!skip_b && !fast_b) {
-          const GuardOut o = guard_decide(px, py.y, g, bp.gg_slot + s_id[k], &kc);
+          const GuardOut o = guard_decide(px, py.y, g, bp.gg_slot + lds_s32(sb + 6144u + 4u * k), &kc);
           al.y = o.alpha;
           gv.y = o.gval;
           cl_b = o.clamped;
@@ -588,7 +591,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         const float2 s5 = __fmul2_rn(w, gad);
         const float f0 = s0.x + s0.y, f1 = s1.x + s1.y, f2 = s2.x + s2.y, f3 = s3.x + s3.y, f4 = s4.x + s4.y,
                     f5 = s5.x + s5.y;
-        const float4* M = s_pj[k];
+        const uint32_t M = sb + 1536u + 144u * k;
 #define GSF_COL(F4A, F4B, F4C, SV)                   \
         {                                            \
           const float2 sv = make_float2(SV, SV);     \
@@ -596,7 +599,8 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
           pb2 = __ffma2_rn(sv, F4B, pb2);            \
           pc2 = __ffma2_rn(sv, F4C, pc2);            \
         }
-        const float4 m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3], m4 = M[4], m5 = M[5], m6 = M[6], m7 = M[7], m8 = M[8];
+        const float4 m0 = lds_f4(M), m1 = lds_f4(M + 16), m2 = lds_f4(M + 32), m3 = lds_f4(M + 48), m4 = lds_f4(M + 64),
+                     m5 = lds_f4(M + 80), m6 = lds_f4(M + 96), m7 = lds_f4(M + 112), m8 = lds_f4(M + 128);
         GSF_COL(make_float2(m0.x, m0.y), make_float2(m0.z, m0.w), make_float2(m1.x, m1.y), f0)
         GSF_COL(make_float2(m1.z, m1.w), make_float2(m2.x, m2.y), make_float2(m2.z, m2.w), f1)
         GSF_COL(make_float2(m3.x, m3.y), make_float2(m3.z, m3.w), make_float2(m4.x, m4.y), f2)

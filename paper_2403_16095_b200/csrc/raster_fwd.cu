@@ -383,7 +383,10 @@ __global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float*
 // list owns pj[kPjFloats r, kPjFloats (r + 1)), staged through shared memory so the CTA writes one contiguous,
 // coalesced block.
 constexpr int kPjThreads = 128;
-__global__ void __launch_bounds__(kPjThreads) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
+#ifndef GSF_PJ_MINB
+#define GSF_PJ_MINB 1
+#endif
+__global__ void __launch_bounds__(kPjThreads, GSF_PJ_MINB) k_posejac(const float* __restrict__ params, int64_t P, const DevState* ds, int K,
                                                  const uint32_t* __restrict__ vis_list, const uint32_t* counters,
                                                  const WorldG* __restrict__ world, float* __restrict__ pj,
                                                  const BlendG* __restrict__ bg_id, const GuardG* __restrict__ gg_id,
@@ -588,6 +591,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   if (ds->halt) return;
   const int tile = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t sgb = opaque_smem_base(s_g);
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x = tx * kTile + 8 * (warp & 1) + (lane & 7);
   const int ya = ty * kTile + 8 * (warp >> 1) + (lane >> 3), yb = ya + 4;
@@ -624,7 +628,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       while (bits) {
         const int k = c0 + __ffs(bits) - 1;
         bits &= bits - 1u;
-        const BlendG g = s_g[k];
+        const BlendG g = lds_blend(sgb + 48u * k);
         const float dx = __fadd_rn(px, -g.mx);
         const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
         const float2 rho = pair_rho2(dx, dy, g);
