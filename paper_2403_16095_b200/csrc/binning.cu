@@ -8,10 +8,10 @@
 //   k_preprocess    (raster_fwd.cu) scatters every (tile, primitive) pair into its tile's bucket
 //                   with one atomic on the tile's fill counter (one counter per L2 sector); a warp
 //                   flattens the pairs of its 32 primitives over its lanes, and lists the few
-//                   primitives with more than kBigPairs tiles (order inside a bucket is arbitrary)
-//   k_scatter_big   one 1024-thread CTA per listed large-footprint primitive, so a primitive
-//                   covering a thousand tiles does not serialise one warp
-//   k_tile_sort     one CTA per tile: its list start from a single-pass decoupled look-back scan
+//                   primitives with more than kBigPairs tiles instead, so a primitive covering a
+//                   thousand tiles does not serialise one warp (order inside a bucket is arbitrary)
+//   k_tile_sort     one CTA per tile: appends the listed large primitives covering the tile to its
+//                   bucket, takes its list start from a single-pass decoupled look-back scan
 //                   of the tile counts (pair total M, longest list; a bucket overflow makes the
 //                   host grow the buckets and re-run), 32-key runs sorted in registers (warp bitonic), then
 //                   pairwise run merges by rank (binary search in the partner run) in shared
@@ -30,24 +30,6 @@ namespace gsfk {
 namespace {
 
 constexpr int kSortChunk = 1024;   // longest list sorted entirely in shared memory (2 x 8 KB)
-
-__global__ void __launch_bounds__(1024) k_scatter_big(const uint32_t* __restrict__ big_ids, const uint32_t* counters,
-                                                      const int4* __restrict__ rect_id, const double* __restrict__ depth_id,
-                                                      int tiles_x, uint32_t* __restrict__ fill, uint32_t bucket_cap,
-                                                      unsigned long long* __restrict__ bucket) {
-  const uint32_t nbig = counters[kCntBig];
-  for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
-    const uint32_t id = big_ids[b];
-    const int4 q = rect_id[id];
-    const unsigned long long key = pair_key(depth_id[id], id);
-    const int w = q.y - q.x + 1;
-    const int c = w * (q.w - q.z + 1);
-    for (int r = threadIdx.x; r < c; r += blockDim.x) {
-      const int row = r / w;
-      bucket_put(fill, bucket, bucket_cap, (q.z + row) * tiles_x + q.x + (r - row * w), key);
-    }
-  }
-}
 
 // Ascending bitonic sort of 32 keys, one per lane, in registers.
 __device__ __forceinline__ unsigned long long warp_sort32(unsigned long long k) {
@@ -214,14 +196,32 @@ __global__ void __launch_bounds__(256) k_tile_sort(uint32_t* fill, uint32_t pair
                                                    uint32_t bucket_cap, unsigned long long* skey, uint32_t* __restrict__ sid,
                                                    const double* __restrict__ depth_id, int2* __restrict__ ranges,
                                                    const uint32_t* __restrict__ pj_slot, uint32_t* __restrict__ sslot,
-                                                   DevState* ds, const uint32_t* counters) {
+                                                   DevState* ds, const uint32_t* counters,
+                                                   const uint32_t* __restrict__ big_ids, const int4* __restrict__ rect_id,
+                                                   int tiles_x) {
   __shared__ unsigned long long s_k[2][kSortChunk];
-  __shared__ uint32_t s_start;
+  __shared__ uint32_t s_start, s_nbig;
   const int t = blockIdx.x;
-  const uint32_t f = fill[static_cast<int64_t>(t) * kBinStride];
+  const int tx = t % tiles_x, ty = t / tiles_x;
+  unsigned long long* bk = bucket + static_cast<int64_t>(t) * bucket_cap;
+  // the listed large-footprint primitives (k_preprocess: more than kBigPairs tiles) that cover this
+  // tile join its bucket behind the scattered pairs (keys are unique, the sort fixes the order)
+  const uint32_t fs = fill[static_cast<int64_t>(t) * kBinStride];
+  const uint32_t nbig = counters[kCntBig];
+  if (threadIdx.x == 0) s_nbig = 0u;
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nbig; b += blockDim.x) {
+    const uint32_t id = big_ids[b];
+    const int4 q = rect_id[id];
+    if (tx >= q.x && tx <= q.y && ty >= q.z && ty <= q.w) {
+      const uint32_t slot = fs + atomicAdd(&s_nbig, 1u);
+      if (slot < bucket_cap) bk[slot] = pair_key(depth_id[id], id);
+    }
+  }
+  __syncthreads();
+  const uint32_t f = fs + s_nbig;
   const uint32_t nb = min(f, bucket_cap);
   if (threadIdx.x == 0) tile_count_publish(fill, t, nb);
-  unsigned long long* bk = bucket + static_cast<int64_t>(t) * bucket_cap;
   // a short list is sorted in shared memory before its start is known: the look-back's waits
   // overlap the sort
   const bool in_smem = nb <= static_cast<uint32_t>(kSortChunk);
@@ -284,13 +284,9 @@ void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles
                  bool want_slots) {
   const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
   const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
-  if (P > 0) {   // the regular pairs were scattered by k_preprocess
-    k_scatter_big<<<32, 1024, 0, st>>>(ws.big_ids, ws.bin_counters, ws.rect_id, ws.depth_id, tiles_x, ws.tile_fill, bcap,
-                                        ws.bucket);
-    ++*L;
-  }
   k_tile_sort<<<ntiles, 256, 0, st>>>(ws.tile_fill, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id, ws.ranges,
-                                      ws.pj_slot, want_slots ? ws.sslot : nullptr, ds, ws.bin_counters);
+                                      ws.pj_slot, want_slots ? ws.sslot : nullptr, ds, ws.bin_counters, ws.big_ids,
+                                      ws.rect_id, tiles_x);
   ++*L;
 }
 
