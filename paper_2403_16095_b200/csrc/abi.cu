@@ -651,6 +651,9 @@ int gsf_ctx_create(int device, gsf_ctx* out) {
   const int rc = guard(c, [&] {
     GSF_CUDA_CHECK(cudaSetDevice(device));
     GSF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    GSF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->ws.side, cudaStreamNonBlocking));
+    GSF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ws.ev_fork, cudaEventDisableTiming));
+    GSF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ws.ev_join, cudaEventDisableTiming));
     g_alloc_stream = c->stream;
     keep_pool_memory(device);
     dalloc(c->ds, 1);
@@ -693,6 +696,9 @@ int gsf_ctx_destroy(gsf_ctx c) {
   if (c->ds_host) cudaFreeHost(c->ds_host);
   if (c->kf_host) cudaFreeHost(c->kf_host);
   if (c->stage) cudaFreeHost(c->stage);
+  if (ws.ev_fork) cudaEventDestroy(ws.ev_fork);
+  if (ws.ev_join) cudaEventDestroy(ws.ev_join);
+  if (ws.side) cudaStreamDestroy(ws.side);
   cudaStreamDestroy(c->stream);
   delete c;
   return GSF_OK;

@@ -56,6 +56,10 @@ enum ProfName { PROF_PREPROCESS = 0, PROF_SORT = 1, PROF_BLEND = 2, PROF_BACKWAR
 // Device workspace of one context.  Capacities grow on demand (never shrink).
 struct Workspace {
   int64_t P_cap = 0, pair_cap = 0, npix_cap = 0, tiles_cap = 0;
+  // tracking: k_posejac runs on a side branch beside the binning (fork after k_preprocess, join
+  // before the blend); created with the context
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // per primitive, id-indexed (written by k_preprocess for the visible ones)
   BlendG* bg_id = nullptr;
   GuardG* gg_id = nullptr;
