@@ -128,6 +128,15 @@ __device__ __forceinline__ BlendG lds_blend(uint32_t a) {
   return g;
 }
 
+__device__ __forceinline__ void sts_s32(uint32_t a, int32_t v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// 16-byte asynchronous global -> shared copy to an explicit shared address (L2 only: read once)
+__device__ __forceinline__ void cp_async16_to(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 // Ampere-style asynchronous global -> shared copies (cp.async, 16 bytes, L1-allocating).
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));

@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(256, 4) k_backward_pose(BwdPtrs bp, int W, int
 // pixels' last contributors retires and frees its slot.  Per-warp pose rows are reduced by
 // warp_grid_reduce (fixed order).
 #ifndef GSF_TBW_MINB
-#define GSF_TBW_MINB 24
+#define GSF_TBW_MINB 22
 #endif
 __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs bp, int W, int H, int tiles_x,
                                                                       BlendConsts kc, double near_plane,
@@ -493,10 +493,9 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
                                                                       uint32_t* gtickets, int rows, int upd_iter,
                                                                       double bc1, double bc2) {
   // one staging buffer: 32 records (3 float4), 32 pose matrices (9 float4), 32 slots
-  __shared__ float4 s_buf[32 * 3 + 32 * 9 + 8];
-  BlendG* s_g = reinterpret_cast<BlendG*>(s_buf);
-  float4 (*s_pj)[9] = reinterpret_cast<float4 (*)[9]>(s_buf + 32 * 3);
-  int32_t* s_id = reinterpret_cast<int32_t*>(s_buf + 32 * 12);
+  // two staging buffers of 16 entries: records (3 float4) at +0, pose matrices (9 float4) at +768 B;
+  // their slots at 6144 + 64 b
+  __shared__ float4 s_buf[2 * 16 * 12 + 8];
   const int lane = threadIdx.x;
   const uint32_t sb = opaque_smem_base(s_buf);
   const int tile = blockIdx.x >> 2, qd = blockIdx.x & 3;
@@ -516,35 +515,62 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
     const float px = static_cast<float>(x) + 0.5f;
     const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
     float2 T = make_float2(qa.T, qb.T), S = make_float2(0.f, 0.f);
-    for (int bend = rg.x + maxlast; bend > rg.x; bend -= 32) {
-      const int bstart = max(rg.x, bend - 32);
-      const int cnt = bend - bstart;
-      // the entry's slot and the forward's block mask arrive together; only entries that can reach
-      // this block fetch their record and pose matrix (both indexed by slot)
-      bool hit = false;
-      if (lane < cnt) {
-        hit = (__ldg(bp.emask + bstart + lane) >> qd) & 1u;
-        if (hit) {
-          const uint32_t sl = __ldg(bp.sslot + bstart + lane);
-          const float4* src = reinterpret_cast<const float4*>(bp.pj) + (kPjFloats / 4) * static_cast<size_t>(sl);
-          const BlendG gj = bp.bg_slot[sl];
-          float4 r[9];
-#pragma unroll
-          for (int j = 0; j < 9; ++j) r[j] = __ldg(src + j);
-          s_g[lane] = gj;
-          s_id[lane] = static_cast<int32_t>(sl);
-#pragma unroll
-          for (int j = 0; j < 9; ++j) s_pj[lane][j] = r[j];
+    // The list is walked back to front in chunks of kC = 16 entries, double-buffered: while chunk c
+    // is processed, the records and pose matrices of chunk c + 1 (only the entries whose forward
+    // block mask has this quadrant) stream into the other buffer with cp.async, and the masks and
+    // slots of chunk c + 2 load into registers (lanes 0..15).
+    constexpr int kC = 16;
+    const int E = rg.x + maxlast;
+    const int nch = (maxlast + kC - 1) / kC;
+    auto fetch = [&](int c, uint32_t& m, uint32_t& sl) {
+      m = 0u;
+      sl = 0u;
+      if (c < nch) {
+        const int lo = max(rg.x, E - kC * (c + 1)), hi = E - kC * c;
+        if (lane < hi - lo) {
+          m = (__ldg(bp.emask + lo + lane) >> qd) & 1u;
+          sl = __ldg(bp.sslot + lo + lane);
         }
       }
-      uint32_t bits = __ballot_sync(0xffffffffu, hit);
+    };
+    auto issue = [&](int c, uint32_t m, uint32_t sl) {
+      if (c < nch) {
+        const int e = lane & 15;
+        const uint32_t me = __shfl_sync(0xffffffffu, m, e), se = __shfl_sync(0xffffffffu, sl, e);
+        if (me) {
+          const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 3072u;
+          const float4* rec = reinterpret_cast<const float4*>(bp.bg_slot + se);
+          const float4* pjm = reinterpret_cast<const float4*>(bp.pj) + (kPjFloats / 4) * static_cast<size_t>(se);
+#pragma unroll
+          for (int t = 0; t < 6; ++t) {
+            const int j = (lane >> 4) + 2 * t;   // float4 j of the entry: 0..2 record, 3..11 pose matrix
+            if (j < 3) cp_async16_to(buf + 48u * e + 16u * j, rec + j);
+            else cp_async16_to(buf + 768u + 144u * e + 16u * (j - 3), pjm + (j - 3));
+          }
+          if (lane < 16) sts_s32(sb + 6144u + static_cast<uint32_t>(c & 1) * 64u + 4u * e, static_cast<int32_t>(se));
+        }
+      }
+      cp_async_commit();
+    };
+    uint32_t m0, s0, m1, s1;
+    fetch(0, m0, s0);
+    fetch(1, m1, s1);
+    issue(0, m0, s0);
+    for (int c = 0; c < nch; ++c) {
+      issue(c + 1, m1, s1);
+      uint32_t m2, s2;
+      fetch(c + 2, m2, s2);
+      cp_async_wait_1();   // chunk c has landed (chunk c + 1 may still be in flight)
       __syncwarp();
+      const int lo = max(rg.x, E - kC * (c + 1));
+      const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 3072u, idb = sb + 6144u + static_cast<uint32_t>(c & 1) * 64u;
+      uint32_t bits = __ballot_sync(0xffffffffu, m0 != 0u);
       float2 pa = make_float2(0.f, 0.f), pb2 = make_float2(0.f, 0.f), pc2 = make_float2(0.f, 0.f);
       while (bits) {
         const int k = 31 - __clz(bits);
         bits &= ~(1u << k);
-        const int li = bstart + k - rg.x;
-        const BlendG g = lds_blend(sb + 48u * k);
+        const int li = lo + k - rg.x;
+        const BlendG g = lds_blend(buf + 48u * k);
         const float dx = __fadd_rn(px, -g.mx);
         const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
         const float2 rho = pair_rho2(dx, dy, g);
@@ -556,14 +582,14 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
         int cl_a = 0, cl_b = 0;
         if (!skip_a && !fast_a) {
-          const GuardOut o = guard_decide(px, py.x, g, bp.gg_slot + lds_s32(sb + 6144u + 4u * k), &kc);
+          const GuardOut o = guard_decide(px, py.x, g, bp.gg_slot + lds_s32(idb + 4u * k), &kc);
           al.x = o.alpha;
           gv.x = o.gval;
           cl_a = o.clamped;
           ca = al.x >= 0.0f;
         }
         if (!skip_b && !fast_b) {
-          const GuardOut o = guard_decide(px, py.y, g, bp.gg_slot + lds_s32(sb + 6144u + 4u * k), &kc);
+          const GuardOut o = guard_decide(px, py.y, g, bp.gg_slot + lds_s32(idb + 4u * k), &kc);
           al.y = o.alpha;
           gv.y = o.gval;
           cl_b = o.clamped;
@@ -591,7 +617,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         const float2 s5 = __fmul2_rn(w, gad);
         const float f0 = s0.x + s0.y, f1 = s1.x + s1.y, f2 = s2.x + s2.y, f3 = s3.x + s3.y, f4 = s4.x + s4.y,
                     f5 = s5.x + s5.y;
-        const uint32_t M = sb + 1536u + 144u * k;
+        const uint32_t M = buf + 768u + 144u * k;
 #define GSF_COL(F4A, F4B, F4C, SV)                   \
         {                                            \
           const float2 sv = make_float2(SV, SV);     \
@@ -610,8 +636,10 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
 #undef GSF_COL
       }
       pd[0] += pa.x; pd[1] += pa.y; pd[2] += pb2.x; pd[3] += pb2.y; pd[4] += pc2.x; pd[5] += pc2.y;
-      __syncwarp();
+      __syncwarp();   // buffer c & 1 is refilled by issue(c + 2)
+      m0 = m1; s0 = s1; m1 = m2; s1 = s2;
     }
+    cp_async_wait_all();
   }
 #pragma unroll
   for (int a = 0; a < 6; ++a) pd[a] = warp_sum_f64(pd[a]);
