@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(const float* __restrict__ x, c
   __syncthreads();
   for (int idx = tid; idx < kSHh * kSX; idx += 256) {   // horizontal pass (k_ssim_h)
     const int r = idx / kSX, c = idx - r * kSX;
-    const float zx = axis_norm(min(bx + c, W - 1), W);
+    const float izx = 1.0f / axis_norm(min(bx + c, W - 1), W);
     float acc[15];
 #pragma unroll
     for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(const float* __restrict__ x, c
       }
     }
 #pragma unroll
-    for (int q = 0; q < 15; ++q) s_h[q][r][c] = acc[q] / zx;
+    for (int q = 0; q < 15; ++q) s_h[q][r][c] = acc[q] * izx;
   }
   __syncthreads();
   double ssum = 0.0;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(const float* __restrict__ x, c
     const int gx = bx + c, gy = by + r;
     if (gx >= W || gy >= H) continue;
     const int64_t i = static_cast<int64_t>(gy) * W + gx;
-    const float zy = axis_norm(gy, H);
+    const double izy = 1.0 / static_cast<double>(axis_norm(gy, H));
     float acc[15];
 #pragma unroll
     for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
@@ -134,17 +134,18 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(const float* __restrict__ x, c
     const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      const double mx = acc[ch] / zy, my = acc[3 + ch] / zy, ex2 = acc[6 + ch] / zy, ey2 = acc[9 + ch] / zy,
-                   exy = acc[12 + ch] / zy;
+      const double mx = acc[ch] * izy, my = acc[3 + ch] * izy, ex2 = acc[6 + ch] * izy, ey2 = acc[9 + ch] * izy,
+                   exy = acc[12 + ch] * izy;
       const double a1 = 2.0 * mx * my + C1;
       const double a2 = 2.0 * (exy - mx * my) + C2;
       const double b1 = mx * mx + my * my + C1;
       const double b2 = (ex2 - mx * mx) + (ey2 - my * my) + C2;
-      const double denom = b1 * b2;
-      const double sv = a1 * a2 / denom;
+      const double idn = 1.0 / (b1 * b2);   // one fp64 reciprocal per channel instead of six divisions
+      const double sv = a1 * a2 * idn;
       ssum += sv;
       if (u) {
-        const double d_a1 = a2 / denom, d_a2 = a1 / denom, d_b1 = -sv / b1, d_b2 = -sv / b2;
+        // d sv / d b1 = -sv / b1 = -sv b2 / (b1 b2), likewise for b2
+        const double d_a1 = a2 * idn, d_a2 = a1 * idn, d_b1 = -sv * b2 * idn, d_b2 = -sv * b1 * idn;
         u[ch * npix + i] = static_cast<float>((2.0 * my * d_a1 - 2.0 * my * d_a2 + 2.0 * mx * d_b1 - 2.0 * mx * d_b2) * weight);
         u[(3 + ch) * npix + i] = static_cast<float>(d_b2 * weight);
         u[(6 + ch) * npix + i] = static_cast<float>(2.0 * d_a2 * weight);
@@ -160,9 +161,22 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(const float* __restrict__ u, c
   extern __shared__ float s_buf[];
   float (*s_u)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                    // 9 planes + halo
   float (*s_t)[kSY][kSW] = reinterpret_cast<float (*)[kSY][kSW]>(s_buf + 9 * kSHh * kSW);     // after the vertical pass
+  // per-tap adjoint weights c_win[o] / axis_norm(neighbour) (ssim.cpp:60-80), 0 outside the image:
+  // rows of this CTA's block (vertical) and its columns (horizontal), one table each
+  __shared__ float s_wy[kSY][2 * kR + 1], s_wx[kSX][2 * kR + 1];
   const int64_t npix = static_cast<int64_t>(W) * H;
   const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
   const int tid = threadIdx.x;
+  for (int idx = tid; idx < (kSY + kSX) * (2 * kR + 1); idx += 256) {
+    const int row = idx / (2 * kR + 1), o = idx - row * (2 * kR + 1) - kR;
+    if (row < kSY) {
+      const int yy = by + row + o;
+      s_wy[row][o + kR] = (yy >= 0 && yy < H) ? c_win[o + kR] / axis_norm(yy, H) : 0.0f;
+    } else {
+      const int xx = bx + (row - kSY) + o;
+      s_wx[row - kSY][o + kR] = (xx >= 0 && xx < W) ? c_win[o + kR] / axis_norm(xx, W) : 0.0f;
+    }
+  }
   for (int idx = tid; idx < kSHh * kSW; idx += 256) {
     const int r = idx / kSW, c = idx - r * kSW;
     const int gx = bx - kR + c, gy = by - kR + r;
@@ -174,14 +188,12 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(const float* __restrict__ u, c
   __syncthreads();
   for (int idx = tid; idx < kSY * kSW; idx += 256) {   // vertical adjoint (k_ssim_adj_v)
     const int r = idx / kSW, c = idx - r * kSW;
-    const int gy = by + r;
     float acc[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
 #pragma unroll
     for (int o = -kR; o <= kR; ++o) {
-      const int yy = gy + o;
-      const float w = (yy >= 0 && yy < H) ? c_win[o + kR] / axis_norm(yy, H) : 0.0f;
+      const float w = s_wy[r][o + kR];
 #pragma unroll
       for (int q = 0; q < 9; ++q) acc[q] += w * s_u[q][r + kR + o][c];
     }
@@ -199,8 +211,7 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(const float* __restrict__ u, c
     for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
 #pragma unroll
     for (int o = -kR; o <= kR; ++o) {
-      const int xx = gx + o;
-      const float w = (xx >= 0 && xx < W) ? c_win[o + kR] / axis_norm(xx, W) : 0.0f;
+      const float w = s_wx[c][o + kR];
 #pragma unroll
       for (int q = 0; q < 9; ++q) acc[q] += w * s_t[q][r][c + kR + o];
     }
