@@ -332,6 +332,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     dalloc(ws.color, 3 * npix); dalloc(ws.alpha_depth, npix); dalloc(ws.median_depth, npix); dalloc(ws.median_valid, npix);
     dalloc(ws.opacity, npix); dalloc(ws.uncertainty, npix); dalloc(ws.final_T, npix); dalloc(ws.count, npix);
     dalloc(ws.dominant, npix); dalloc(ws.median_prim, npix); dalloc(ws.dominant_w, npix); dalloc(ws.last, npix);
+    dalloc(ws.pxcode, npix);
     dalloc(ws.obs, npix); dalloc(ws.upstream, 7 * npix); dalloc(ws.dssim, 3 * npix); dalloc(ws.ssim_tmp, 9 * npix);
     ws.npix_cap = npix;
   }
@@ -680,7 +681,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
   void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
-                  ws.last, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
+                  ws.last, ws.pxcode, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
                   ws.red_part, c->bp_scratch, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
                   c->red_f};
@@ -1161,6 +1162,7 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
     FwdArgs fa = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it);
     fa.cand = c->ws.cand;
     fa.want_posejac = true;
+    fa.keep_maps = false;   // the loop reads T, last and the seed signs only
     fa.fuse_loss_final = true;
     fa.use_world = true;
     fa.want_pair_base = false;

@@ -105,6 +105,7 @@ struct Workspace {
   int32_t* median_prim = nullptr;
   float* dominant_w = nullptr;
   int32_t* last = nullptr;
+  uint8_t* pxcode = nullptr;     // tracking: per pixel, the signs of the loss seeds (pixel_seed_code)
   float* obs = nullptr;         // observed depth of the API render (npix)
   float* upstream = nullptr;    // explicit upstream maps for gsf_render_backward (7*npix)
   float* dssim = nullptr;       // 3*npix: d(w_ssim * ssim loss)/d colour (mapping)
@@ -138,6 +139,7 @@ struct FwdArgs {
   LossParams lp;
   int iteration;             // loop iteration (for device-side checks), -1 outside loops
   bool want_posejac = false; // tracking: emit the per-primitive pose Jacobians (ws.pj_id)
+  bool keep_maps = true;     // tracking loop: colour / alpha depth / opacity maps are not read back
   bool fuse_loss_final = false;  // tracking: the blend's last CTA runs the loss finalize
   bool use_world = false;        // preprocess from ws.world / ws.support (run_world ran for this map)
   const uint32_t* cand = nullptr;  // tracking: candidate ids (run_candidates), used while ds->cand_ok

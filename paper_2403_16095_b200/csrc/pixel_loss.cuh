@@ -38,6 +38,23 @@ __device__ __forceinline__ void loss_pixel(double* v, float cr, float cg, float 
   if (geo) { v[LS_GEO_SUM] = fabsf(ad - D); v[LS_GEO_CNT] = 1.0; }
 }
 
+// Tracking seeds (losses.cpp:330-337) are a global scale times a per-pixel sign: the fused tracking
+// forward stores the signs (2 bits each: colour 0..2, alpha depth; 1 = +, 2 = -, masks folded in)
+// so the pose backward reads one byte instead of the maps, the target and the sensor depth.
+__device__ __forceinline__ uint32_t sgn_code(float v) { return v > 0.0f ? 1u : (v < 0.0f ? 2u : 0u); }
+__device__ __forceinline__ float code_sgn(uint32_t c) { return c == 1u ? 1.0f : (c == 2u ? -1.0f : 0.0f); }
+__device__ __forceinline__ uint8_t pixel_seed_code(float cr, float cg, float cb, float ad, float op, const float* I,
+                                                   const float* depth, int64_t pi, double near_plane, double far_plane,
+                                                   float floor) {
+  const bool opm = op >= floor;
+  const float D = depth ? depth[pi] : 0.0f;
+  const bool geo = opm && depth && px_depth_valid(D, near_plane, far_plane);
+  uint32_t code = 0u;
+  if (opm) code = sgn_code(cr - I[0]) | (sgn_code(cg - I[1]) << 2) | (sgn_code(cb - I[2]) << 4);
+  if (geo) code |= sgn_code(ad - D) << 6;
+  return static_cast<uint8_t>(code);
+}
+
 struct PixSeeds {
   float gc0, gc1, gc2, gad, gmd, gu;
 };

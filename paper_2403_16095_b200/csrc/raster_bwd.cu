@@ -103,6 +103,7 @@ struct BwdPtrs {
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
   const uint32_t* sslot;    // tracking: tile lists as visible slots
   const uint8_t* emask;     // tracking: per entry, the 8x8 blocks it can reach (k_blend_track)
+  const uint8_t* pxcode;    // tracking: per pixel, the seed signs (pixel_seed_code, k_blend_track)
   const BlendG* bg_slot;    // tracking: records by visible slot
   const GuardG* gg_slot;
 };
@@ -307,6 +308,29 @@ __device__ __forceinline__ PixBwd load_pixel_bwd(const BwdPtrs& bp, int64_t pi, 
   return p;
 }
 
+// Tracking pixel inputs from the fused forward's seed signs: seeds_pixel<1>'s values (the same
+// global scale times the same sign), three loads instead of the maps, target and sensor depth.
+__device__ __forceinline__ PixBwd track_pixel_bwd(const BwdPtrs& bp, int64_t pi, bool inside, const DevState* ds) {
+  PixBwd p;
+  p.gop = p.gmd = p.gu = p.D = 0.0f;
+  p.med = -1;
+  p.gc0 = p.gc1 = p.gc2 = p.gad = 0.0f;
+  p.T = 1.0f;
+  p.last = 0;
+  if (!inside) return p;
+  const uint32_t code = bp.pxcode[pi];
+  const int last = bp.last[pi];
+  p.T = bp.final_T[pi];
+  const float sc = static_cast<float>(ds->seed_color), sg = static_cast<float>(ds->seed_geo);
+  p.gc0 = sc * code_sgn(code & 3u);
+  p.gc1 = sc * code_sgn((code >> 2) & 3u);
+  p.gc2 = sc * code_sgn((code >> 4) & 3u);
+  p.gad = sg * code_sgn(code >> 6);
+  // all seeds zero: nothing to propagate (rasterizer.cpp:411-413)
+  p.last = (p.gc0 != 0.f || p.gc1 != 0.f || p.gc2 != 0.f || p.gad != 0.f) ? last : 0;
+  return p;
+}
+
 // Tracking backward (pose only).  The pose gradient is linear in every pair's screen-space
 // gradient, so each lane pushes its own pixel's screen gradient through the primitive's SE(3)
 // Jacobian (compute_posejac) and accumulates the 6-vector in registers: no per-(tile, primitive)
@@ -506,8 +530,8 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   double pd[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (!ds->halt) {
     const int2 rg = bp.ranges[tile];
-    const PixBwd qa = load_pixel_bwd<SEED_TRACK>(bp, static_cast<int64_t>(ya) * W + x, in_a, lp, ds, near_plane, far_plane);
-    const PixBwd qb = load_pixel_bwd<SEED_TRACK>(bp, static_cast<int64_t>(yb) * W + x, in_b, lp, ds, near_plane, far_plane);
+    const PixBwd qa = track_pixel_bwd(bp, static_cast<int64_t>(ya) * W + x, in_a, ds);
+    const PixBwd qb = track_pixel_bwd(bp, static_cast<int64_t>(yb) * W + x, in_b, ds);
     const int last_a = qa.last, last_b = qb.last;
     const int maxlast = __reduce_max_sync(0xffffffffu, max(last_a, last_b));
     const float2 gc0 = make_float2(qa.gc0, qb.gc0), gc1 = make_float2(qa.gc1, qb.gc1), gc2 = make_float2(qa.gc2, qb.gc2),
@@ -1014,6 +1038,7 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.tile_pose = nullptr;
   bp.sslot = ws.sslot;
   bp.emask = ws.emask;
+  bp.pxcode = ws.pxcode;
   bp.bg_slot = ws.bg_slot;
   bp.gg_slot = ws.gg_slot;
   const bool view_dep = a.K > 1;

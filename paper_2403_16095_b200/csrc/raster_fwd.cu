@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     int tiles_x, BlendConsts kc, double near_plane, double far_plane, LossParams lp, DevState* ds,
     float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_op, float* __restrict__ o_T,
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
-    uint8_t* __restrict__ emask) {
+    uint8_t* __restrict__ emask, uint8_t* __restrict__ o_code) {
   __shared__ BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
@@ -664,29 +664,39 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   for (int q = 0; q < LS_NUM; ++q) v[q] = vb[q] = 0.0;
   if (in_a) {
     const int64_t pi = static_cast<int64_t>(ya) * W + x;
-    o_color[3 * pi + 0] = rg_a.x;
-    o_color[3 * pi + 1] = rg_a.y;
-    o_color[3 * pi + 2] = bd_a.x;
-    o_ad[pi] = bd_a.y;
-    o_op[pi] = op.x;
+    if (o_color) {
+      o_color[3 * pi + 0] = rg_a.x;
+      o_color[3 * pi + 1] = rg_a.y;
+      o_color[3 * pi + 2] = bd_a.x;
+      o_ad[pi] = bd_a.y;
+      o_op[pi] = op.x;
+    }
     o_T[pi] = T.x;
     o_last[pi] = last_a;
     if (loss_rgb)
       loss_pixel<1>(v, rg_a.x, rg_a.y, bd_a.x, bd_a.y, 0.0f, false, op.x, 0.0f, loss_rgb + 3 * pi, loss_depth, pi, false,
                     near_plane, far_plane, lp.opacity_floor);
+    if (o_code)
+      o_code[pi] = pixel_seed_code(rg_a.x, rg_a.y, bd_a.x, bd_a.y, op.x, loss_rgb + 3 * pi, loss_depth, pi, near_plane,
+                                   far_plane, lp.opacity_floor);
   }
   if (in_b) {
     const int64_t pi = static_cast<int64_t>(yb) * W + x;
-    o_color[3 * pi + 0] = rg_b.x;
-    o_color[3 * pi + 1] = rg_b.y;
-    o_color[3 * pi + 2] = bd_b.x;
-    o_ad[pi] = bd_b.y;
-    o_op[pi] = op.y;
+    if (o_color) {
+      o_color[3 * pi + 0] = rg_b.x;
+      o_color[3 * pi + 1] = rg_b.y;
+      o_color[3 * pi + 2] = bd_b.x;
+      o_ad[pi] = bd_b.y;
+      o_op[pi] = op.y;
+    }
     o_T[pi] = T.y;
     o_last[pi] = last_b;
     if (loss_rgb)
       loss_pixel<1>(vb, rg_b.x, rg_b.y, bd_b.x, bd_b.y, 0.0f, false, op.y, 0.0f, loss_rgb + 3 * pi, loss_depth, pi, false,
                     near_plane, far_plane, lp.opacity_floor);
+    if (o_code)
+      o_code[pi] = pixel_seed_code(rg_b.x, rg_b.y, bd_b.x, bd_b.y, op.y, loss_rgb + 3 * pi, loss_depth, pi, near_plane,
+                                   far_plane, lp.opacity_floor);
   }
   if (!loss_rgb) return;
 #pragma unroll
@@ -797,10 +807,11 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     const bool sl = a.want_posejac;
     k_blend_track<<<ntiles, kTrkThreads, 0, st>>>(ws.ranges, sl ? ws.sslot : ws.sid, sl ? ws.bg_slot : ws.bg_id,
                                                   sl ? ws.gg_slot : ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,
-                                                  tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color,
-                                                  ws.alpha_depth, ws.opacity, ws.final_T, ws.last, ws.loss_part,
+                                                  tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
+                                                  a.keep_maps ? ws.color : nullptr, ws.alpha_depth, ws.opacity, ws.final_T,
+                                                  ws.last, ws.loss_part,
                                                   a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket,
-                                                  sl ? ws.emask : nullptr);
+                                                  sl ? ws.emask : nullptr, sl ? ws.pxcode : nullptr);
   }
   else if (a.lp.mode == 2 && loss_rgb)
     k_blend<2><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
