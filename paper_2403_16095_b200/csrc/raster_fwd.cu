@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(256) k_candidates(int64_t P, DevState* ds, Ras
 // CACHED: the world part comes from k_world (tracking loop); otherwise every primitive is
 // validated and projected from its parameters (validate_primitives + project_all).
 template <bool CACHED>
-__global__ void __launch_bounds__(256, CACHED ? 3 : 2) k_preprocess(const float* __restrict__ params, int64_t P, const DevState* ds,
+#ifndef GSF_PRE_MINB
+#define GSF_PRE_MINB 4
+#endif
+__global__ void __launch_bounds__(256, CACHED ? GSF_PRE_MINB : 2) k_preprocess(const float* __restrict__ params, int64_t P, const DevState* ds,
                                                     RasterParams rp, BlendG* __restrict__ bg_id, GuardG* __restrict__ gg_id,
                                                     double* __restrict__ depth_id, int4* __restrict__ rect_id,
                                                     uint8_t* __restrict__ visible, int32_t* bad_index, BlendConsts kc,
