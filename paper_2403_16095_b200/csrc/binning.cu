@@ -201,6 +201,8 @@ __global__ void __launch_bounds__(256) k_tile_sort(uint32_t* fill, uint32_t pair
                                                    int tiles_x) {
   __shared__ unsigned long long s_k[2][kSortChunk];
   __shared__ uint32_t s_start, s_nbig;
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const int tx = t % tiles_x, ty = t / tiles_x;
   unsigned long long* bk = bucket + static_cast<int64_t>(t) * bucket_cap;
@@ -284,7 +286,7 @@ void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles
                  bool want_slots) {
   const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
   const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
-  k_tile_sort<<<ntiles, 256, 0, st>>>(ws.tile_fill, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id, ws.ranges,
+  launch_pdl(k_tile_sort, dim3(ntiles), dim3(256), 0, st, ws.tile_fill, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id, ws.ranges,
                                       ws.pj_slot, want_slots ? ws.sslot : nullptr, ds, ws.bin_counters, ws.big_ids,
                                       ws.rect_id, tiles_x);
   ++*L;

@@ -281,6 +281,13 @@ __device__ __forceinline__ void bucket_put(uint32_t* fill, unsigned long long* b
   if (slot < bucket_cap) bucket[t * bucket_cap + slot] = key;
 }
 
+// Programmatic dependent launch inside the tracking loop: each kernel lets its successor launch as
+// soon as all of its own CTAs are running (launch_dependents) and waits for its predecessor's
+// completion and memory (wait) before touching anything the predecessor writes.  Both are no-ops
+// without a programmatic edge.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 #define GSF_CUDA_CHECK(expr)                                                        \
   do {                                                                              \
     cudaError_t _e = (expr);                                                        \
@@ -294,6 +301,31 @@ struct CudaError {
   int line;
   CudaError(cudaError_t c, const char* e, const char* f, int l) : code(c), expr(e), file(f), line(l) {}
 };
+
+#ifndef GSF_NO_PDL
+// Launch with a programmatic (PDL) edge to the previous kernel on the stream.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GSF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+#else
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  kern<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+  GSF_CUDA_CHECK(cudaGetLastError());
+}
+#endif
+
 
 inline int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 

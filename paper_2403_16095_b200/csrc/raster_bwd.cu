@@ -520,6 +520,8 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   // two staging buffers of 16 entries: records (3 float4) at +0, pose matrices (9 float4) at +768 B;
   // their slots at 6144 + 64 b
   __shared__ float4 s_buf[2 * 16 * 12 + 8];
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x;
   const uint32_t sb = opaque_smem_base(s_buf);
   const int tile = blockIdx.x >> 2, qd = blockIdx.x & 3;
@@ -1065,7 +1067,7 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   } while (0)
     if (a.seed_mode == SEED_TRACK && nf == 6) {
       const double t = static_cast<double>(a.update_iter + 1);   // AdamState bias corrections (adam.cpp:40-53)
-      k_backward_track_w<<<4 * ntiles, 32, 0, st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
+      launch_pdl(k_backward_track_w, dim3(4 * ntiles), dim3(32), 0, st, bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
                                                      ws.wtickets + ws.wtickets_half, 4 * ntiles, a.update_iter,
                                                      1.0 - std::pow(0.9, t), 1.0 - std::pow(0.999, t));
       fused_update = a.update_iter >= 0;

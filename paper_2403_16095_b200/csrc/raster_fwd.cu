@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(256, CACHED ? GSF_PRE_MINB : 2) k_preprocess(c
   __shared__ uint32_t s_vis[8];
   __shared__ uint32_t s_base;
   __shared__ Cam s_cam;   // read through shared memory: 20 doubles need not live in registers
+  pdl_trigger();
   if (threadIdx.x < sizeof(Cam) / 4)
     reinterpret_cast<uint32_t*>(&s_cam)[threadIdx.x] = reinterpret_cast<const uint32_t*>(&ds->cam)[threadIdx.x];
   __syncthreads();
@@ -591,6 +592,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
   __shared__ double s_red[kTrkThreads / 32][LS_NUM];
+  pdl_wait();
+  pdl_trigger();
   if (ds->halt) return;
   const int tile = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -808,7 +811,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     // with pose Jacobians (a pose backward follows) the lists and records are read by visible slot
     // and the entries' block masks are kept for the backward
     const bool sl = a.want_posejac;
-    k_blend_track<<<ntiles, kTrkThreads, 0, st>>>(ws.ranges, sl ? ws.sslot : ws.sid, sl ? ws.bg_slot : ws.bg_id,
+    launch_pdl(k_blend_track, dim3(ntiles), dim3(kTrkThreads), 0, st, ws.ranges, sl ? ws.sslot : ws.sid, sl ? ws.bg_slot : ws.bg_id,
                                                   sl ? ws.gg_slot : ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,
                                                   tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
                                                   a.keep_maps ? ws.color : nullptr, ws.alpha_depth, ws.opacity, ws.final_T,
