@@ -1163,6 +1163,8 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
     fa.cand = c->ws.cand;
     fa.want_posejac = true;
     fa.keep_maps = false;   // the loop reads T, last and the seed signs only
+    fa.clean_bins = true;   // ... and each blend leaves the bins zeroed for the next iteration
+    fa.bins_clean = it > 0;
     fa.fuse_loss_final = true;
     fa.use_world = true;
     fa.want_pair_base = false;

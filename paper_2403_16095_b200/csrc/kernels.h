@@ -140,6 +140,8 @@ struct FwdArgs {
   int iteration;             // loop iteration (for device-side checks), -1 outside loops
   bool want_posejac = false; // tracking: emit the per-primitive pose Jacobians (ws.pj_id)
   bool keep_maps = true;     // tracking loop: colour / alpha depth / opacity maps are not read back
+  bool bins_clean = false;   // tracking loop: the previous iteration's blend re-zeroed the bins (no memset)
+  bool clean_bins = false;   // tracking loop: the blend re-zeroes the bins once the binning is consumed
   bool fuse_loss_final = false;  // tracking: the blend's last CTA runs the loss finalize
   bool use_world = false;        // preprocess from ws.world / ws.support (run_world ran for this map)
   const uint32_t* cand = nullptr;  // tracking: candidate ids (run_candidates), used while ds->cand_ok

@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(256, CACHED ? GSF_PRE_MINB : 2) k_preprocess(c
   __shared__ uint32_t s_vis[8];
   __shared__ uint32_t s_base;
   __shared__ Cam s_cam;   // read through shared memory: 20 doubles need not live in registers
+  pdl_wait();   // the camera comes from the previous iteration's pose step
   pdl_trigger();
   if (threadIdx.x < sizeof(Cam) / 4)
     reinterpret_cast<uint32_t*>(&s_cam)[threadIdx.x] = reinterpret_cast<const uint32_t*>(&ds->cam)[threadIdx.x];
@@ -587,13 +588,20 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     int tiles_x, BlendConsts kc, double near_plane, double far_plane, LossParams lp, DevState* ds,
     float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_op, float* __restrict__ o_T,
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
-    uint8_t* __restrict__ emask, uint8_t* __restrict__ o_code) {
+    uint8_t* __restrict__ emask, uint8_t* __restrict__ o_code, uint32_t* clean_bins, int64_t clean_cnt_off) {
   __shared__ BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
   __shared__ double s_red[kTrkThreads / 32][LS_NUM];
   pdl_wait();
   pdl_trigger();
+  if (clean_bins) {   // the binning is consumed: leave the bins zeroed for the next iteration (no memset)
+    if (threadIdx.x < 4) clean_bins[static_cast<int64_t>(blockIdx.x) * kBinStride + threadIdx.x] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      clean_bins[static_cast<int64_t>(clean_cnt_off) + kCntVisible] = 0u;
+      clean_bins[static_cast<int64_t>(clean_cnt_off) + kCntBig] = 0u;
+    }
+  }
   if (ds->halt) return;
   const int tile = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -768,11 +776,13 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   const int tiles_x = a.rp.tiles_x, tiles_y = a.rp.tiles_y;
   const int ntiles = tiles_x * tiles_y;
   Profiler* pf = ws.prof;
-  GSF_CUDA_CHECK(cudaMemsetAsync(ws.bins, 0, sizeof(uint32_t) * (ws.tiles_cap * kBinStride + kCntNum), st));
+  if (!a.bins_clean)
+    GSF_CUDA_CHECK(cudaMemsetAsync(ws.bins, 0, sizeof(uint32_t) * (ws.tiles_cap * kBinStride + kCntNum), st));
   if (pf) pf->begin(PROF_PREPROCESS, st);
   if (P > 0) {
 #define GSF_PRE(CV)                                                                                                    \
-  k_preprocess<CV><<<div_up(P, 256), 256, 0, st>>>(a.params, P, ds, a.rp, ws.bg_id, ws.gg_id, ws.depth_id, ws.rect_id,   \
+  launch_pdl(k_preprocess<CV>, dim3(div_up(P, 256)), dim3(256), 0, st, a.params, P, ds, a.rp, ws.bg_id, ws.gg_id,       \
+             ws.depth_id, ws.rect_id,                                                                                  \
                                                    ws.visible, &ds->bad_index, a.kc, ws.bin_counters,                    \
                                                    ws.vis_list, ws.pj_slot, ws.tile_fill,                                 \
                                                    static_cast<uint32_t>(ws.bucket_cap), ws.bucket, ws.big_ids,           \
@@ -817,7 +827,8 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
                                                   a.keep_maps ? ws.color : nullptr, ws.alpha_depth, ws.opacity, ws.final_T,
                                                   ws.last, ws.loss_part,
                                                   a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket,
-                                                  sl ? ws.emask : nullptr, sl ? ws.pxcode : nullptr);
+                                                  sl ? ws.emask : nullptr, sl ? ws.pxcode : nullptr,
+                                                  a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride);
   }
   else if (a.lp.mode == 2 && loss_rgb)
     k_blend<2><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
