@@ -517,6 +517,8 @@ void ensure_trace(gsf_ctx_s* c, int n) {
 namespace {
 
 __global__ void k_set_cam_from_kf(DevState* ds, const KfPose* kf, int k, int has_obs) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   const Cam old = ds->cam;
   ds->cam = make_cam(kf[k].rot, kf[k].trans, old.fx, old.fy, old.cx, old.cy, old.width, old.height, old.near_plane,
                      old.far_plane);
@@ -524,6 +526,8 @@ __global__ void k_set_cam_from_kf(DevState* ds, const KfPose* kf, int k, int has
 }
 
 __global__ void k_kf_grab(DevState* ds, KfPose* kf, int k, double* loss_acc, double* trace, int it, int store_trace) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   for (int a = 0; a < 6; ++a) kf[k].grad[a] = ds->d_pose[a];
   if (loss_acc) *loss_acc += ds->loss_total;
   if (store_trace && trace) trace[it] = ds->loss_total;
@@ -1367,7 +1371,7 @@ static void enqueue_map_view(gsf_ctx_s* c, const Frame& f, int k, const gsf_intr
   const LossParams lp = make_lp(2, &m.weights, m.raster);
   const int tiles = ((K.width + kTile - 1) / kTile) * ((K.height + kTile - 1) / kTile);
   const int64_t npix = static_cast<int64_t>(K.width) * K.height;
-  k_set_cam_from_kf<<<1, 1, 0, c->stream>>>(c->ds, c->kf, k, 1);
+  launch_pdl(k_set_cam_from_kf, dim3(1), dim3(1), 0, c->stream, c->ds, c->kf, k, 1);
   ++c->launches;
   FwdArgs fa = fwd_args(c, K, m.raster, f.depth, f.rgb, f.depth, lp, it);
   fa.use_world = use_world;
@@ -1379,7 +1383,7 @@ static void enqueue_map_view(gsf_ctx_s* c, const Frame& f, int k, const gsf_intr
   run_backward(c->ws, c->ds, b, c->stream, &c->launches);
   if (m.weights.w_iso > 0.0)
     run_iso(c->ws, c->ds, c->params, c->P, m.weights.w_iso, m.weights.iso_epsilon, c->grads, c->stream, &c->launches);
-  k_kf_grab<<<1, 1, 0, c->stream>>>(c->ds, c->kf, k, loss_acc, c->trace_dev, trace_index, trace_index >= 0 ? 1 : 0);
+  launch_pdl(k_kf_grab, dim3(1), dim3(1), 0, c->stream, c->ds, c->kf, k, loss_acc, c->trace_dev, trace_index, trace_index >= 0 ? 1 : 0);
   ++c->launches;
 }
 

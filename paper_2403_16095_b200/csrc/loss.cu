@@ -38,6 +38,8 @@ __global__ void __launch_bounds__(1024) k_loss_finalize(const double* __restrict
                                                         LossParams lp, int iteration, const double* __restrict__ ssim_part,
                                                         int ssim_blocks, const double* __restrict__ iso_part,
                                                         int iso_blocks, DevState* ds) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   __shared__ double s_red[32][LS_NUM];
   __shared__ double s_red1[32][1];
   __shared__ double s_tot[LS_NUM];
@@ -73,6 +75,8 @@ constexpr size_t ssim_bwd_smem() { return sizeof(float) * (9 * kSHh * kSW + 9 * 
 
 __global__ void __launch_bounds__(256) k_ssim_fwd(const float* __restrict__ x, const float* __restrict__ y, int W, int H,
                                                   double weight, float* __restrict__ u, double* __restrict__ part) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   extern __shared__ float s_buf[];
   float (*s_in)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                  // x0..2, y0..2
   float (*s_h)[kSHh][kSX] = reinterpret_cast<float (*)[kSHh][kSX]>(s_buf + 6 * kSHh * kSW);   // 15 planes
@@ -158,6 +162,8 @@ __global__ void __launch_bounds__(256) k_ssim_fwd(const float* __restrict__ x, c
 
 __global__ void __launch_bounds__(256) k_ssim_bwd(const float* __restrict__ u, const float* __restrict__ x,
                                                   const float* __restrict__ y, int W, int H, float* __restrict__ dx) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   extern __shared__ float s_buf[];
   float (*s_u)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                    // 9 planes + halo
   float (*s_t)[kSY][kSW] = reinterpret_cast<float (*)[kSY][kSW]>(s_buf + 9 * kSHh * kSW);     // after the vertical pass
@@ -267,6 +273,8 @@ __global__ void __launch_bounds__(256) k_ssim_global(const float* __restrict__ x
 __global__ void __launch_bounds__(256) k_iso(const float* __restrict__ params, int64_t P, const uint8_t* __restrict__ visible,
                                              const DevState* ds, double w_iso, double eps, int add_grad,
                                              float* __restrict__ grads, double* __restrict__ part) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   __shared__ double s_red[8];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   double term = 0.0;
@@ -312,7 +320,7 @@ void run_loss_finalize(Workspace& ws, DevState* ds, const LossParams& lp, int ti
   const int ssim_blocks = lp.mode == 2 && lp.w_ssim > 0.0 ? ws.ssim_blocks : 0;
   const int iso_blocks = lp.mode == 2 ? ws.iso_blocks : 0;
   if (ws.loss_rows > 0) tiles = ws.loss_rows;   // the producer's row count (4 per tile for k_blend_track_w)
-  k_loss_finalize<<<1, 1024, 0, st>>>(ws.loss_part, tiles, npix, lp, iteration, ws.red_part, ssim_blocks,
+  launch_pdl(k_loss_finalize, dim3(1), dim3(1024), 0, st, ws.loss_part, tiles, npix, lp, iteration, ws.red_part, ssim_blocks,
                                      ws.red_part + ws.red_iso_offset, iso_blocks, ds);
   ++*L;
 }
@@ -338,12 +346,12 @@ void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W
   }
   const dim3 grid(div_up(W, kSX), div_up(H, kSY));
   float* u = ws.ssim_tmp;                 // 9 adjoint seed planes
-  k_ssim_fwd<<<grid, 256, ssim_fwd_smem(), st>>>(x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr,
+  launch_pdl(k_ssim_fwd, grid, dim3(256), ssim_fwd_smem(), st, x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr,
                                                  ws.red_part);
   ++*L;
   ws.ssim_blocks = static_cast<int>(grid.x * grid.y);
   if (d_out) {
-    k_ssim_bwd<<<grid, 256, ssim_bwd_smem(), st>>>(u, x, y, W, H, d_out);
+    launch_pdl(k_ssim_bwd, grid, dim3(256), ssim_bwd_smem(), st, u, x, y, W, H, d_out);
     ++*L;
   }
 }
@@ -352,7 +360,7 @@ void run_iso(Workspace& ws, DevState* ds, const float* params, int64_t P, double
              cudaStream_t st, int64_t* L) {
   if (P <= 0) { ws.iso_blocks = 0; return; }
   const int blocks = div_up(P, 256);
-  k_iso<<<blocks, 256, 0, st>>>(params, P, ws.visible, ds, w_iso, eps, grads ? 1 : 0, grads, ws.red_part + ws.red_iso_offset);
+  launch_pdl(k_iso, dim3(blocks), dim3(256), 0, st, params, P, ws.visible, ds, w_iso, eps, grads ? 1 : 0, grads, ws.red_part + ws.red_iso_offset);
   ++*L;
   if (!grads) ws.iso_blocks = blocks;
 }

@@ -121,6 +121,8 @@ constexpr size_t bwd_smem_bytes() {
 template <int SEED, int NF>
 __global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc, double near_plane,
                                                   double far_plane, LossParams lp, const DevState* ds) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   extern __shared__ float4 s_dyn[];   // bwd_smem_bytes<NF>()
   float (*s_part)[kBwdBatch][NF] = reinterpret_cast<float (*)[kBwdBatch][NF]>(s_dyn);
   BlendG* s_g = reinterpret_cast<BlendG*>(&s_part[8][0][0]);
@@ -765,6 +767,8 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
                                                const float* __restrict__ params, int64_t P, int K,
                                                float* __restrict__ grads, float* __restrict__ d_mean2d,
                                                double* __restrict__ pose_part) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   __shared__ double s_red[8][6];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t r = blockIdx.x * blockDim.x + tid;
@@ -960,6 +964,8 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
 }
 
 __global__ void __launch_bounds__(1024) k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   __shared__ double s_red[32][6];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -1090,7 +1096,7 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
                                           static_cast<int>(bwd_smem_bytes<NFV>())));                             \
       attr_set = true;                                                                                            \
     }                                                                                                             \
-    k_backward<SM, NFV><<<ntiles, 256, bwd_smem_bytes<NFV>(), st>>>(bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, \
+    launch_pdl(k_backward<SM, NFV>, dim3(ntiles), dim3(256), bwd_smem_bytes<NFV>(), st, bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, \
                                                                      a.far_plane, a.lp, ds);                    \
   } while (0)
   if (a.seed_mode == SEED_TRACK) {
@@ -1106,7 +1112,7 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   if (ws.prof) ws.prof->begin(PROF_CHAIN, st);
   const int blocks = std::max(1, div_up(a.P, 256));
 #define GSF_CHAIN(NFV, FULLV)                                                                                            \
-  k_chain<NFV, FULLV><<<blocks, 256, 0, st>>>(ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base, ws.partials, ds, \
+  launch_pdl(k_chain<NFV, FULLV>, dim3(blocks), dim3(256), 0, st, ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base, ws.partials, ds, \
                                               a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part)
   if (nf == 6)
     GSF_CHAIN(6, false);
@@ -1116,7 +1122,7 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     GSF_CHAIN(10, true);
 #undef GSF_CHAIN
   ++*L;
-  k_pose_sum<<<1, 1024, 0, st>>>(ws.pose_part, blocks, ds);
+  launch_pdl(k_pose_sum, dim3(1), dim3(1024), 0, st, ws.pose_part, blocks, ds);
   ++*L;
   if (ws.prof) ws.prof->end(st);
   return false;

@@ -473,6 +473,8 @@ __global__ void __launch_bounds__(256, 4) k_blend(const int2* __restrict__ range
                                                float* __restrict__ o_domw, int32_t* __restrict__ o_last,
                                                double* __restrict__ loss_part, int fuse_final, int iteration,
                                                uint32_t* ticket) {
+  pdl_wait();   // PDL: the predecessor's results are complete from here
+  pdl_trigger();
   __shared__ BlendG s_g[256];
   __shared__ int32_t s_id[256];
   __shared__ uint8_t s_mask[256];
@@ -831,9 +833,9 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
                                                   a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride);
   }
   else if (a.lp.mode == 2 && loss_rgb)
-    k_blend<2><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
+    launch_pdl(k_blend<2>, dim3(ntiles), dim3(256), 0, st, GSF_BLEND_ARGS);
   else
-    k_blend<0><<<ntiles, 256, 0, st>>>(GSF_BLEND_ARGS);
+    launch_pdl(k_blend<0>, dim3(ntiles), dim3(256), 0, st, GSF_BLEND_ARGS);
 #undef GSF_BLEND_ARGS
   ++*L;
   if (pf) pf->end(st);
