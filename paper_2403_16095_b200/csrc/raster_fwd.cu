@@ -715,9 +715,16 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
                                    far_plane, lp.opacity_floor);
   }
   if (!loss_rgb) return;
+  // the tracking loss has two residual sums and two mask counts (losses.cpp:284-339); the counts
+  // are ballots (exact in fp64), the align / var slots of the mapping loss stay zero
 #pragma unroll
   for (int q = 0; q < LS_NUM; ++q) {
-    const double t = warp_sum_d(v[q] + vb[q]);
+    double t = 0.0;
+    if (q == LS_COLOR_SUM || q == LS_GEO_SUM)
+      t = warp_sum_d(v[q] + vb[q]);
+    else if (q == LS_COLOR_CNT || q == LS_GEO_CNT)
+      t = static_cast<double>(__popc(__ballot_sync(0xffffffffu, v[q] != 0.0)) +
+                              __popc(__ballot_sync(0xffffffffu, vb[q] != 0.0)));
     if (lane == 0) s_red[warp][q] = t;
   }
   __syncthreads();
