@@ -460,7 +460,10 @@ __device__ __forceinline__ void full_accumulate(PixelState& s, float2& rg, float
 // Plain render (LMODE 0) and the mapping forward with its fused loss partials (LMODE 2); the
 // tracking forward is k_blend_track below.
 template <int LMODE>
-__global__ void __launch_bounds__(256, 4) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sid,
+#ifndef GSF_BLEND_MINB
+#define GSF_BLEND_MINB 4
+#endif
+__global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __restrict__ ranges, const uint32_t* __restrict__ sid,
                                                const BlendG* __restrict__ bg, const GuardG* __restrict__ gg,
                                                const float* __restrict__ obs, const float* __restrict__ loss_rgb,
                                                const float* __restrict__ loss_depth, int W, int H, int tiles_x,
