@@ -1,13 +1,23 @@
 """TEST INFRASTRUCTURE ONLY — the CPU checker.
 
-ctypes bindings of oracle/liboracle.so: the fp64 restatement of the reference hot path
-(oracle/gsf_oracle.cpp, every function citing the /root/reference file:line it follows) and the
-fp32 mirror of the device decision path (oracle/mirror.cpp).  Only tests/, __graft_entry__.smoke()
-and bench.py's cpu_baseline / --impl reference legs may import this package, and only as the
-checker or the timed CPU baseline — never as the product.
+Two interchangeable backends behind the same orc_* entry points (oracle/gsf_oracle.h):
+
+* "port" — oracle/liboracle.so: the fp64 restatement of the reference hot path
+  (oracle/gsf_oracle.cpp, every function citing the /root/reference file:line it follows) plus the
+  fp32 mirror of the device decision path (oracle/mirror.cpp);
+* "reference" — oracle/_ref/libgsfref.so: the UNMODIFIED reference sources compiled here against
+  oracle/eigen_lite (oracle/Makefile.ref) behind a thin C shim (oracle/ref_capi.cpp).  Present
+  wherever it was built (this container; the .so travels to the GPU box with the snapshot).
+
+``with oracle.backend("reference"): ...`` routes every entry point the reference library exports
+to it (the mirror, the fixtures and the restatement-only helpers stay on the port).  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may import this
+package, and only as the checker or the timed CPU baseline — never as the product.  It does not
+import the product package.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import subprocess
@@ -15,16 +25,23 @@ from types import SimpleNamespace
 
 import numpy as np
 
-from paper_2403_16095_b200.abi import (Intrinsics, LossTerms, LossWeights, MapHost, MapperCfg, Pose, RasterCfg,
-                                       TrackerCfg, TrackResult)
+from .gsf_types import Intrinsics, LossTerms, LossWeights, MapHost, MapperCfg, Pose, RasterCfg, TrackerCfg, TrackResult
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libgsfref.so")
+REF_SOURCES = "/root/reference/proj"
 
 dp = C.POINTER(C.c_double)
 fp = C.POINTER(C.c_float)
 u8p = C.POINTER(C.c_uint8)
 i32p = C.POINTER(C.c_int32)
+vp = C.c_void_p   # struct pointers: any ctypes struct with the gsf_cuda.h layout, passed by reference
+
+
+def _as(T, x):
+    """x as a T (same C layout; e.g. the product's abi.Pose -> oracle's Pose)."""
+    return x if isinstance(x, T) else T.from_buffer_copy(x)
 
 
 class Maps(C.Structure):
@@ -56,20 +73,67 @@ class MirOut(C.Structure):
                 ("last_index", i32p), ("num_visible", C.c_int64), ("num_pairs", C.c_int64)]
 
 
-_lib = None
+_libs = {}
+_active = "port"
 
 
 def build():
     subprocess.run(["make", "-s", "-C", HERE], check=True)
+    if os.path.isdir(REF_SOURCES):
+        build_reference()
 
 
-def lib() -> C.CDLL:
-    global _lib
-    if _lib is not None:
-        return _lib
-    if not os.path.exists(LIB_PATH):
-        build()
-    L = C.CDLL(LIB_PATH)
+def build_reference():
+    """oracle/_ref/libgsfref.so from the unmodified reference sources (needs /root/reference)."""
+    subprocess.run(["make", "-s", "-j8", "-f", os.path.join(HERE, "Makefile.ref")], check=True)
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+@contextlib.contextmanager
+def backend(name: str):
+    """Route the entry points to "port" (restatement) or "reference" (the reference's own code)."""
+    global _active
+    assert name in ("port", "reference")
+    if name == "reference" and not reference_available():
+        raise FileNotFoundError(f"{REF_PATH} is missing (built by oracle.build_reference() where /root/reference exists)")
+    prev, _active = _active, name
+    try:
+        yield
+    finally:
+        _active = prev
+
+
+class _Dispatch:
+    def __getattr__(self, name):
+        if _active == "reference":
+            L = _load("reference")
+            try:
+                return getattr(L, name)
+            except AttributeError:
+                pass
+        return getattr(_load("port"), name)
+
+
+def lib():
+    _load("port")
+    return _Dispatch()
+
+
+def _current():
+    """The library the active backend's objects (results, map states) belong to."""
+    return _load("reference") if _active == "reference" else _load("port")
+
+
+def _load(which):
+    if which in _libs:
+        return _libs[which]
+    path = LIB_PATH if which == "port" else REF_PATH
+    if which == "port" and not os.path.exists(path):
+        subprocess.run(["make", "-s", "-C", HERE], check=True)
+    L = C.CDLL(path)
     sig = {
         "orc_last_error": (C.c_char_p, []),
         "orc_threads": (C.c_int, []),
@@ -116,14 +180,27 @@ def lib() -> C.CDLL:
         "orc_random_scene": (C.c_int, [C.c_uint32, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                        C.POINTER(MapHost)]),
         "orc_wavy_depth": (None, [C.c_int, C.c_int, C.c_double, C.c_int, dp]),
+        "orc_smooth_raster": (None, [C.POINTER(RasterCfg)]),
+        "orc_default_raster": (None, [C.POINTER(RasterCfg)]),
+        "orc_default_weights": (None, [C.POINTER(LossWeights), C.c_int]),
+        "orc_default_tracker": (None, [C.POINTER(TrackerCfg)]),
+        "orc_default_mapper": (None, [C.POINTER(MapperCfg)]),
+        "ref_synth_scene": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                      C.POINTER(Intrinsics), C.POINTER(MapHost), C.POINTER(C.c_int64), C.POINTER(Pose),
+                                      C.c_int]),
         "mir_render": (C.c_int, [C.POINTER(MapHost), C.POINTER(Pose), C.POINTER(Intrinsics), fp, C.POINTER(RasterCfg),
                                  C.POINTER(MirOut)]),
     }
     for name, (res, args) in sig.items():
-        f = getattr(L, name)
+        try:
+            f = getattr(L, name)
+        except AttributeError:   # the reference library exports the reference-backed subset
+            continue
         f.restype = res
-        f.argtypes = args
-    _lib = L
+        f.argtypes = [vp if (isinstance(a, type) and issubclass(a, C._Pointer) and issubclass(a._type_, C.Structure)
+                             and a._type_ is not Maps and a._type_ is not MirOut and a._type_ is not Grads
+                             and a._type_ is not Upstream and a._type_ is not GradcheckReport) else a for a in args]
+    _libs[which] = L
     return L
 
 
@@ -133,9 +210,9 @@ class OracleError(Exception):
         self.status = status
 
 
-def _check(rc):
+def _check(rc, L=None):
     if rc != 0:
-        raise OracleError(rc, lib().orc_last_error().decode())
+        raise OracleError(rc, (L or lib()).orc_last_error().decode())
 
 
 def _d(a):
@@ -181,8 +258,8 @@ def wavy_depth(w, h, base, hole_every=17):
 class Result:
     """Owning wrapper of an orc_result (RenderResult)."""
 
-    def __init__(self, handle, W, H, P):
-        self.h, self.W, self.H, self.P = handle, W, H, P
+    def __init__(self, handle, W, H, P, L):
+        self.h, self.W, self.H, self.P, self.L = handle, W, H, P, L
         n = W * H
         self.color = np.zeros((H, W, 3))
         self.alpha_depth = np.zeros((H, W))
@@ -202,41 +279,40 @@ class Result:
                  self.per_pixel_count.ctypes.data_as(i32p), self.dominant.ctypes.data_as(i32p),
                  self.median_prim.ctypes.data_as(i32p), self.dominant_weight.ctypes.data_as(dp),
                  self.visible.ctypes.data_as(u8p), 0)
-        _check(lib().orc_result_maps(handle, C.byref(m)))
+        _check(L.orc_result_maps(handle, C.byref(m)), L)
         self.visible = self.visible[:P]
         self.has_uncertainty = bool(m.has_uncertainty)
         _ = n
 
     def record(self):
-        t = lib().orc_result_record_total(self.h)
+        t = self.L.orc_result_record_total(self.h)
         rs = np.zeros(self.W * self.H + 1, np.uint32)
         prim = np.zeros(max(t, 1), np.int32)
         a = np.zeros(max(t, 1))
         tr = np.zeros(max(t, 1))
-        _check(lib().orc_result_record(self.h, rs.ctypes.data_as(C.POINTER(C.c_uint32)), prim.ctypes.data_as(i32p),
+        _check(self.L.orc_result_record(self.h, rs.ctypes.data_as(C.POINTER(C.c_uint32)), prim.ctypes.data_as(i32p),
                                        a.ctypes.data_as(dp), tr.ctypes.data_as(dp)))
         return rs, prim[:t], a[:t], tr[:t]
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_result_free(self.h)
+            self.L.orc_result_free(self.h)
             self.h = None
 
 
 def render(m, pose: Pose, K: Intrinsics, obs=None, cfg: RasterCfg = None, brute_force=False) -> Result:
-    from paper_2403_16095_b200.abi import defaults_raster
     cfg = cfg or defaults_raster()
     h = host_of(m)
     out = C.c_void_p()
     o = None if obs is None else np.ascontiguousarray(obs, dtype=np.float64)
-    _check(lib().orc_render(C.byref(h), C.byref(pose), C.byref(K), None if o is None else o.ctypes.data_as(dp),
-                            C.byref(cfg), 1 if brute_force else 0, C.byref(out)))
-    return Result(out, K.width, K.height, m.mean.shape[0])
+    L = _current()
+    _check(L.orc_render(C.byref(h), C.byref(pose), C.byref(K), None if o is None else o.ctypes.data_as(dp),
+                        C.byref(cfg), 1 if brute_force else 0, C.byref(out)), L)
+    return Result(out, K.width, K.height, m.mean.shape[0], L)
 
 
 def render_backward(m, pose, K, res: Result, d_color=None, d_alpha_depth=None, d_median_depth=None, d_opacity=None,
                     d_uncertainty=None, obs=None, cfg=None):
-    from paper_2403_16095_b200.abi import defaults_raster
     cfg = cfg or defaults_raster()
     keep = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in
             (d_color, d_alpha_depth, d_median_depth, d_opacity, d_uncertainty)]
@@ -249,8 +325,8 @@ def render_backward(m, pose, K, res: Result, d_color=None, d_alpha_depth=None, d
                g.d_opacity_logit.ctypes.data_as(dp), g.d_sh.ctypes.data_as(dp), g.d_mean2d.ctypes.data_as(dp))
     o = None if obs is None else np.ascontiguousarray(obs, dtype=np.float64)
     h = host_of(m)
-    _check(lib().orc_render_backward(C.byref(h), C.byref(pose), C.byref(K), res.h, C.byref(up),
-                                     None if o is None else o.ctypes.data_as(dp), C.byref(cfg), C.byref(go)))
+    _check(res.L.orc_render_backward(C.byref(h), C.byref(pose), C.byref(K), res.h, C.byref(up),
+                                     None if o is None else o.ctypes.data_as(dp), C.byref(cfg), C.byref(go)), res.L)
     g.d_pose = np.array(list(go.d_pose))
     return g
 
@@ -261,8 +337,8 @@ def tracking_loss(res: Result, target, obs, K, w):
     out = LossTerms()
     n = K.width * K.height
     dc, dd = np.zeros(3 * n), np.zeros(n)
-    _check(lib().orc_tracking_loss(res.h, t.ctypes.data_as(dp), o.ctypes.data_as(dp), C.byref(K), C.byref(w),
-                                   C.byref(out), dc.ctypes.data_as(dp), dd.ctypes.data_as(dp)))
+    _check(res.L.orc_tracking_loss(res.h, t.ctypes.data_as(dp), o.ctypes.data_as(dp), C.byref(K), C.byref(w),
+                                   C.byref(out), dc.ctypes.data_as(dp), dd.ctypes.data_as(dp)), res.L)
     return out, dc, dd
 
 
@@ -274,8 +350,8 @@ def mapping_loss(m, res: Result, target, obs, K, w):
     P = m.mean.shape[0]
     bufs = [np.zeros(3 * n), np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(3 * max(P, 1))]
     h = host_of(m)
-    _check(lib().orc_mapping_loss(C.byref(h), res.h, t.ctypes.data_as(dp), o.ctypes.data_as(dp), C.byref(K),
-                                  C.byref(w), C.byref(out), *[b.ctypes.data_as(dp) for b in bufs]))
+    _check(res.L.orc_mapping_loss(C.byref(h), res.h, t.ctypes.data_as(dp), o.ctypes.data_as(dp), C.byref(K),
+                                  C.byref(w), C.byref(out), *[b.ctypes.data_as(dp) for b in bufs]), res.L)
     return out, bufs
 
 
@@ -304,14 +380,15 @@ class MapState:
         self.K = m.sh.shape[1]
         h = host_of(m)
         s = C.c_void_p()
-        _check(lib().orc_mapstate_create(C.byref(h), C.byref(mcfg), C.byref(s)))
+        self.L = _current()
+        _check(self.L.orc_mapstate_create(C.byref(h), C.byref(mcfg), C.byref(s)), self.L)
         self.h = s
 
     def get(self):
-        P = lib().orc_mapstate_count(self.h)
+        P = self.L.orc_mapstate_count(self.h)
         m = empty_map(P, self.K)
         h = host_of(m)
-        _check(lib().orc_mapstate_get(self.h, C.byref(h)))
+        _check(self.L.orc_mapstate_get(self.h, C.byref(h)), self.L)
         return m
 
     def map_step(self, frames, poses, K, mcfg, iterations):
@@ -319,9 +396,9 @@ class MapState:
         keep = [(np.ascontiguousarray(r, dtype=np.float64), np.ascontiguousarray(d, dtype=np.float64)) for r, d in frames]
         rg = (dp * n)(*[k[0].ctypes.data_as(dp) for k in keep])
         dg = (dp * n)(*[k[1].ctypes.data_as(dp) for k in keep])
-        ps = (Pose * n)(*poses)
+        ps = (Pose * n)(*[_as(Pose, p) for p in poses])
         trace = np.zeros(max(iterations, 1))
-        _check(lib().orc_map_step(self.h, n, rg, dg, ps, C.byref(K), C.byref(mcfg), iterations, trace.ctypes.data_as(dp)))
+        _check(self.L.orc_map_step(self.h, n, rg, dg, ps, C.byref(K), C.byref(mcfg), iterations, trace.ctypes.data_as(dp)), self.L)
         return trace[:iterations]
 
     def sliding_ba(self, frames, poses, frame_ids, K, tcfg, mcfg, iterations):
@@ -329,35 +406,35 @@ class MapState:
         keep = [(np.ascontiguousarray(r, dtype=np.float64), np.ascontiguousarray(d, dtype=np.float64)) for r, d in frames]
         rg = (dp * n)(*[k[0].ctypes.data_as(dp) for k in keep])
         dg = (dp * n)(*[k[1].ctypes.data_as(dp) for k in keep])
-        ps = (Pose * n)(*poses)
+        ps = (Pose * n)(*[_as(Pose, p) for p in poses])
         fid = (C.c_int32 * n)(*frame_ids)
         trace = np.zeros(max(iterations, 1))
-        _check(lib().orc_sliding_ba(self.h, n, rg, dg, ps, fid, C.byref(K), C.byref(tcfg), C.byref(mcfg), iterations,
-                                    trace.ctypes.data_as(dp)))
+        _check(self.L.orc_sliding_ba(self.h, n, rg, dg, ps, fid, C.byref(K), C.byref(tcfg), C.byref(mcfg), iterations,
+                                    trace.ctypes.data_as(dp)), self.L)
         return trace[:iterations], [ps[i] for i in range(n)]
 
     def put(self, m):
         h = host_of(m)
-        _check(lib().orc_mapstate_put(self.h, C.byref(h)))
+        _check(self.L.orc_mapstate_put(self.h, C.byref(h)), self.L)
 
     def append(self, m):
         h = host_of(m)
-        _check(lib().orc_mapstate_append(self.h, C.byref(h)))
+        _check(self.L.orc_mapstate_append(self.h, C.byref(h)), self.L)
 
     def set_stats(self, accum, count):
         a = np.ascontiguousarray(accum, dtype=np.float64)
         c = np.ascontiguousarray(count, dtype=np.int32)
-        _check(lib().orc_mapstate_set_stats(self.h, a.ctypes.data_as(dp), c.ctypes.data_as(i32p)))
+        _check(self.L.orc_mapstate_set_stats(self.h, a.ctypes.data_as(dp), c.ctypes.data_as(i32p)), self.L)
 
     def densify(self, mcfg):
         """densify_and_cull (mapper.cpp:172-230): (split, cloned, removed)."""
         ch = np.zeros(3, np.int32)
-        _check(lib().orc_mapstate_densify(self.h, C.byref(mcfg), ch.ctypes.data_as(i32p)))
+        _check(self.L.orc_mapstate_densify(self.h, C.byref(mcfg), ch.ctypes.data_as(i32p)), self.L)
         return tuple(int(x) for x in ch)
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_mapstate_free(self.h)
+            self.L.orc_mapstate_free(self.h)
             self.h = None
 
 
@@ -366,10 +443,11 @@ def accumulate_uncertainty(m, results, depths, poses, K):
     keep = [np.ascontiguousarray(d, dtype=np.float64) for d in depths]
     rh = (C.c_void_p * max(n, 1))(*[r.h for r in results])
     dg = (dp * max(n, 1))(*[k.ctypes.data_as(dp) for k in keep])
-    ps = (Pose * max(n, 1))(*poses)
+    ps = (Pose * max(n, 1))(*[_as(Pose, p) for p in poses])
     cnt = C.c_int32()
     h = host_of(m)
-    _check(lib().orc_accumulate_uncertainty(C.byref(h), n, rh, dg, ps, C.byref(K), C.byref(cnt)))
+    L = results[0].L if results else lib()
+    _check(L.orc_accumulate_uncertainty(C.byref(h), n, rh, dg, ps, C.byref(K), C.byref(cnt)), L)
     return cnt.value
 
 
@@ -394,7 +472,7 @@ def uncertainty_partials(m, results, depths, poses, K):
     keep = [np.ascontiguousarray(d, dtype=np.float64) for d in depths]
     rh = (C.c_void_p * max(n, 1))(*[r.h for r in results])
     dg = (dp * max(n, 1))(*[k.ctypes.data_as(dp) for k in keep])
-    ps = (Pose * max(n, 1))(*poses)
+    ps = (Pose * max(n, 1))(*[_as(Pose, p) for p in poses])
     P = m.mean.shape[0]
     s = np.zeros(max(P, 1))
     c = np.zeros(max(P, 1), np.int32)
@@ -422,7 +500,6 @@ def gradcheck_linear(m, pose, K, cfg, obs, a_color, a_depth, a_opacity, a_uncert
 
 
 def mirror_render(m, pose, K, obs=None, cfg=None, pair_capacity=1 << 22):
-    from paper_2403_16095_b200.abi import defaults_raster
     cfg = cfg or defaults_raster()
     P = m.mean.shape[0]
     W, H = K.width, K.height
@@ -451,3 +528,58 @@ def mirror_render(m, pose, K, obs=None, cfg=None, pair_capacity=1 << 22):
     o.rank_to_id = o.rank_to_id[: o.num_visible]
     o.pair_rank = o.pair_rank[: o.num_pairs]
     return o
+
+
+# ---- configuration defaults of the reference structs (from the active backend) ------------------
+def defaults_raster() -> RasterCfg:
+    c = RasterCfg()
+    lib().orc_default_raster(C.byref(c))
+    return c
+
+
+def smooth_raster() -> RasterCfg:
+    """smooth_raster_config() (gradcheck.cpp:21-27): no skip, no termination, footprint sigma 8."""
+    c = RasterCfg()
+    if reference_available():
+        _load("reference").orc_smooth_raster(C.byref(c))
+    else:
+        c = defaults_raster()
+        c.alpha_skip, c.termination_threshold, c.footprint_sigma = 0.0, 0.0, 8.0
+    return c
+
+
+def defaults_weights(handheld_real=False) -> LossWeights:
+    w = LossWeights()
+    lib().orc_default_weights(C.byref(w), 1 if handheld_real else 0)
+    return w
+
+
+def defaults_tracker() -> TrackerCfg:
+    t = TrackerCfg()
+    lib().orc_default_tracker(C.byref(t))
+    return t
+
+
+def defaults_mapper() -> MapperCfg:
+    m = MapperCfg()
+    lib().orc_default_mapper(C.byref(m))
+    return m
+
+
+def synth_scene(count, extent=4.0, wall_layers=3, seed=0, frames=50, radius=1.0, K: Intrinsics = None, kind=0):
+    """The reference's own synthetic generator (io/synthetic.cpp:199-211: SyntheticSource's ground
+    truth and trajectory; frames are not rendered).  Needs the reference backend library."""
+    L = _load("reference")
+    K = K or Intrinsics(600.0, 600.0, 599.5, 339.5, 1200, 680, 1.0, 0.1, 10.0)
+    n = C.c_int64()
+    poses = (Pose * frames)()
+    rc = L.ref_synth_scene(kind, count, extent, wall_layers, frames, radius, seed, C.byref(K), None, C.byref(n), poses, 0)
+    if rc:
+        raise OracleError(rc, L.orc_last_error().decode())
+    m = empty_map(n.value, 1)
+    h = host_of(m)
+    rc = L.ref_synth_scene(kind, count, extent, wall_layers, frames, radius, seed, C.byref(K), C.byref(h), C.byref(n),
+                           poses, frames)
+    if rc:
+        raise OracleError(rc, L.orc_last_error().decode())
+    return m, [poses[i] for i in range(frames)]

@@ -362,7 +362,8 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   if (!c->counters) dalloc(c->counters, 16);
 }
 
-// After an overflow: grow the pair lists and/or the per-tile buckets to fit the last render.
+// After an overflow: grow the pair lists and/or the per-tile buckets to fit the largest render
+// since the last reset (DevState::M_max / max_tile are maxima over a whole loop's renders).
 void grow_pairs(gsf_ctx_s* c, uint32_t needed) {
   Workspace& ws = c->ws;
   if (needed > ws.pair_cap) {
@@ -374,6 +375,14 @@ void grow_pairs(gsf_ctx_s* c, uint32_t needed) {
     while (ws.bucket_cap < longest + longest / 4) ws.bucket_cap *= 2;
     dalloc(ws.bucket, static_cast<size_t>(ws.tiles_cap) * ws.bucket_cap);
   }
+}
+
+// Still overflowed after the growth retries: the tile lists were truncated, so no result is returned.
+void check_overflow(gsf_ctx_s* c, const char* what) {
+  if (c->ds_host->overflow)
+    throw EUnsupported(std::string(what) + ": pair capacity still exceeded after growing (" +
+                       std::to_string(c->ds_host->M_max) + " pairs, longest tile list " +
+                       std::to_string(c->ds_host->max_tile) + ")");
 }
 
 FwdArgs fwd_args(gsf_ctx_s* c, const gsf_intrinsics& k, const gsf_raster_cfg& cfg, const float* obs, const float* loss_rgb,
@@ -434,8 +443,9 @@ void render_sync(gsf_ctx_s* c, const gsf_pose& pose, const gsf_intrinsics& k, co
     read_state(c);
     if (c->ds_host->bad_index != std::numeric_limits<int32_t>::max()) throw_nonfinite(c->ds_host->bad_index);
     if (!c->ds_host->overflow) break;
-    grow_pairs(c, c->ds_host->M);
+    grow_pairs(c, c->ds_host->M_max);
   }
+  check_overflow(c, "render");
   c->have_render = true;
   c->render_gen = c->map_gen;
   c->rK = k;
@@ -1166,7 +1176,9 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
     FwdArgs fa = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it);
     fa.cand = c->ws.cand;
     fa.want_posejac = true;
-    fa.keep_maps = false;   // the loop reads T, last and the seed signs only
+    // the two-pixel pose backward (K == 1) reads T, last and the seed signs only; the view-dependent
+    // pose backward (k_backward_pose<SEED_TRACK, true>) derives its seeds from the maps
+    fa.keep_maps = c->K > 1;
     fa.clean_bins = true;   // ... and each blend leaves the bins zeroed for the next iteration
     fa.bins_clean = it > 0;
     fa.fuse_loss_final = true;
@@ -1275,8 +1287,9 @@ int gsf_track_frame(gsf_ctx c, int32_t slot, const gsf_pose* initial, const gsf_
       run_track(c, f, *K, *tcfg, *w, *rcfg);
       read_state(c);
       if (!h.overflow) break;
-      grow_pairs(c, h.M);
+      grow_pairs(c, h.M_max);
     }
+    check_overflow(c, "track_frame");
     const DevState& h = *c->ds_host;
     if (h.bad_index != std::numeric_limits<int32_t>::max()) throw_nonfinite(h.bad_index);
     *out = gsf_track_result{};
@@ -1331,8 +1344,9 @@ int gsf_tracking_gradient(gsf_ctx c, int32_t slot, const gsf_pose* pose, const g
       run_backward(c->ws, c->ds, b, c->stream, &c->launches);
       read_state(c);
       if (!c->ds_host->overflow) break;
-      grow_pairs(c, c->ds_host->M);
+      grow_pairs(c, c->ds_host->M_max);
     }
+    check_overflow(c, "tracking_gradient");
     if (c->ds_host->bad_index != std::numeric_limits<int32_t>::max()) throw_nonfinite(c->ds_host->bad_index);
     fill_terms(c, terms);
     for (int a = 0; a < 6; ++a) d_pose[a] = c->ds_host->d_pose[a];

@@ -163,7 +163,8 @@ __device__ void merge_pass(const unsigned long long* a, unsigned long long* b, i
 // decoupled look-back (warp 0).  Tile t publishes its count (flag 1) as soon as it starts and its
 // inclusive prefix (flag 2) once known, in one 64-bit word next to its fill counter (same L2
 // sector, zeroed by the per-render memset); it sums its predecessors' words back to the nearest
-// published prefix.  Lower tile CTAs are dispatched first, so every awaited word gets written.
+// published prefix.  Tiles are claimed in order from an atomic ticket (not blockIdx), so every
+// tile a CTA waits on already belongs to a running CTA, whatever order the CTAs are dispatched in.
 __device__ constexpr unsigned long long kScanAgg = 1ull << 32, kScanPrefix = 2ull << 32;
 __device__ __forceinline__ unsigned long long* scan_word(uint32_t* fill, int64_t t) {
   return reinterpret_cast<unsigned long long*>(fill + t * kBinStride + 2);
@@ -198,12 +199,14 @@ __global__ void __launch_bounds__(256) k_tile_sort(uint32_t* fill, uint32_t pair
                                                    const uint32_t* __restrict__ pj_slot, uint32_t* __restrict__ sslot,
                                                    DevState* ds, const uint32_t* counters,
                                                    const uint32_t* __restrict__ big_ids, const int4* __restrict__ rect_id,
-                                                   int tiles_x) {
+                                                   int tiles_x, uint32_t* ticket) {
   __shared__ unsigned long long s_k[2][kSortChunk];
-  __shared__ uint32_t s_start, s_nbig;
+  __shared__ uint32_t s_start, s_nbig, s_tile;
   pdl_wait();
   pdl_trigger();
-  const int t = blockIdx.x;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int t = static_cast<int>(s_tile);
   const int tx = t % tiles_x, ty = t / tiles_x;
   unsigned long long* bk = bucket + static_cast<int64_t>(t) * bucket_cap;
   // the listed large-footprint primitives (k_preprocess: more than kBigPairs tiles) that cover this
@@ -237,6 +240,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(uint32_t* fill, uint32_t pair
       if (t == 0) ds->V = counters[kCntVisible];
       if (t == static_cast<int>(gridDim.x) - 1) {   // the pair total M (k_tile_scan's, without its launch)
         ds->M = e + nb;
+        atomicMax(&ds->M_max, e + nb);
         if (e + nb > pair_cap) ds->overflow = 1u;
       }
     }
@@ -288,7 +292,7 @@ void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles
   const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
   launch_pdl(k_tile_sort, dim3(ntiles), dim3(256), 0, st, ws.tile_fill, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id, ws.ranges,
                                       ws.pj_slot, want_slots ? ws.sslot : nullptr, ds, ws.bin_counters, ws.big_ids,
-                                      ws.rect_id, tiles_x);
+                                      ws.rect_id, tiles_x, ws.bin_counters + kCntSortTicket);
   ++*L;
 }
 

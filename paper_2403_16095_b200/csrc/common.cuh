@@ -20,7 +20,7 @@ constexpr int kBinStride = GSF_BIN_STRIDE;
 static_assert(kBinStride >= 4, "the tile-list scan word shares the fill counter's sector");
 constexpr int kPjFloats = 56;   // per-primitive pose matrix: 9 columns x 6 rows + 2 pad (k_posejac)
 constexpr int kBigPairs = 128;
-enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntPairAlloc = 4, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
+enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntPairAlloc = 4, kCntSortTicket = 5, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
 constexpr int kTilePixels = kTile * kTile;
 constexpr int kFieldsBase = 11;       // mean 3, log_scale 3, quat 4, opacity 1; then 3*K SH
 
@@ -207,7 +207,8 @@ struct DevState {
   uint32_t V;              // visible primitives of the current render
   uint32_t M;              // (tile, primitive) pairs of the current render
   uint32_t overflow;       // pair / tile-bucket capacity exceeded (host grows and re-runs)
-  uint32_t max_tile;       // longest tile list of the current render
+  uint32_t max_tile;       // longest tile list over the renders since the last reset (atomicMax)
+  uint32_t M_max;          // largest pair total over the renders since the last reset (sizes the growth)
   int32_t bad_index;       // smallest non-finite primitive index, INT32_MAX if none
   int32_t halt;            // 0 run, 1 nothing to track at it 0, 2 diverged, 3 non-finite map
   int32_t halt_iter;

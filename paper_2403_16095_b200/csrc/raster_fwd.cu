@@ -605,6 +605,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       clean_bins[static_cast<int64_t>(clean_cnt_off) + kCntVisible] = 0u;
       clean_bins[static_cast<int64_t>(clean_cnt_off) + kCntBig] = 0u;
+      clean_bins[static_cast<int64_t>(clean_cnt_off) + kCntSortTicket] = 0u;
     }
   }
   if (ds->halt) return;

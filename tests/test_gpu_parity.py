@@ -423,6 +423,29 @@ def test_tracking_100_iterations_cfg1_sized(gpu_ctx, orc):
     assert res.final_loss == pytest.approx(ofin.total, rel=1e-4, abs=1e-9)
 
 
+@pytest.mark.parametrize("K_sh", [4, 9, 16])
+def test_tracking_view_dependent_sh(gpu_ctx, orc, K_sh):
+    """track_frame on a view-dependent map (SH 4/9/16): the loop takes the k_backward_pose<SEED_TRACK,
+    true> path, whose seeds come from the forward's maps; the trajectory follows the fp64 oracle's."""
+    K = make_intrinsics(64, 48, 55.0)
+    m = f32_round(orc.random_scene(77 + K_sh, 120, K_sh))
+    _upload(gpu_ctx, m)
+    fr = _frames(gpu_ctx, orc, m, [pose()], K)
+    start = perturbed(pose(), [0.004, -0.003, 0.002, 0.008, -0.006, 0.004])
+    tc = defaults_tracker()
+    tc.iterations = 30
+    w = defaults_weights(True)
+    res = gpu_ctx.track_frame(0, start, K, tc, w)
+    ores = orc.track_frame(m, fr[0][0], fr[0][1], start, K, tc, w, defaults_raster())
+    assert res.iterations_run == 30
+    assert rotation_error(res.pose, ores.pose) < 5e-4 and translation_error(res.pose, ores.pose) < 5e-4
+    # the first step alone: the gradient the loop used equals the standalone tracking gradient
+    tc.iterations = 1
+    one = gpu_ctx.track_frame(0, start, K, tc, w)
+    o1 = orc.track_frame(m, fr[0][0], fr[0][1], start, K, tc, w, defaults_raster())
+    assert rotation_error(one.pose, o1.pose) < 1e-6 and translation_error(one.pose, o1.pose) < 1e-6
+
+
 def test_tracking_leaves_trust_region(gpu_ctx, orc):
     """The tracking loop preprocesses only the frame's trust-region candidates (k_candidates) until a
     step leaves the region (0.03 rad / 0.05 m), then every primitive.  A narrow camera on a scene
