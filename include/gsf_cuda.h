@@ -176,9 +176,11 @@ int64_t gsf_kernel_launches(gsf_ctx ctx);
 int gsf_synchronize(gsf_ctx ctx);
 
 /* ---- timing hooks (benchmark evidence; no effect on results) -------------------------------
- * CUDA events on the context's stream.  Kernel classes for gsf_profile_read: 0 preprocess,
- * 1 scan+sort+binning, 2 blend (forward), 3 backward (per-pixel reverse sweep), 4 chain
- * (per-primitive fp64 chain + pose reduction). */
+ * CUDA events on the context's stream (profiling runs the loops eagerly, not as graphs).  Kernel
+ * classes for gsf_profile_read: 0 preprocess, 1 tile sort + list build (binning), 2 blend (forward),
+ * 3 backward (per-pixel reverse sweep), 4 chain (per-primitive fp64 chain + pose reduction),
+ * 5 SSIM, 6 Adam, 7 (unused), 8 pose Jacobians (k_posejac, timed on the side stream it overlaps
+ * the binning on). */
 int gsf_profile_enable(gsf_ctx ctx, int32_t on);
 int gsf_profile_read(gsf_ctx ctx, int32_t kernel_class, double* total_ms, int64_t* launches);
 int gsf_event_record(gsf_ctx ctx, int32_t slot);                       /* slot 0..7 */
@@ -358,14 +360,6 @@ int32_t gsf_slam_degraded_frames(gsf_slam slam);
 int gsf_ba_partition(int32_t n, int32_t nranks, int32_t rank, uint8_t* owned);
 int gsf_comm_unique_id(uint8_t id[128]);
 int gsf_comm_init(gsf_ctx ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
-
-/* ---- synthetic inputs (io/synthetic.cpp:56-186; support, not the hot path) ----------- */
-/* Room scene of SceneSpec{room, primitive_count, extent, wall_layers}, mt19937_64(seed).
- * Call with map->mean == NULL to get map->count; then with arrays of that size (K = 1). */
-int gsf_synth_room(int32_t primitive_count, double extent, int32_t wall_layers, uint64_t seed,
-                   gsf_map_host* map);
-/* Orbit trajectory (synthetic.cpp:158-186) with TrajectorySpec defaults except frames/radius/height. */
-int gsf_synth_orbit(int32_t frames, double radius, double height, gsf_pose* poses);
 
 #ifdef __cplusplus
 }

@@ -184,8 +184,6 @@ SIGNATURES = {
     "gsf_ba_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, u8p]),
     "gsf_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8 * 128)]),
     "gsf_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_uint8 * 128)]),
-    "gsf_synth_room": (C.c_int, [C.c_int32, C.c_double, C.c_int32, C.c_uint64, C.POINTER(MapHost)]),
-    "gsf_synth_orbit": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.POINTER(Pose)]),
 }
 
 _lib = None

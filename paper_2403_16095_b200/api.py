@@ -467,30 +467,6 @@ def ba_partition(n: int, nranks: int, rank: int) -> np.ndarray:
     return out[:n].astype(bool)
 
 
-def synth_room(primitive_count: int, extent: float = 4.0, wall_layers: int = 3, seed: int = 0) -> GaussianMap:
-    """SceneSpec{room, ...} scene of io/synthetic.cpp:56-116 (mt19937_64(seed))."""
-    lib = abi.load()
-    hm = abi.MapHost()
-    rc = lib.gsf_synth_room(primitive_count, extent, wall_layers, seed, C.byref(hm))
-    if rc != GSF_OK:
-        raise ValueError("synth_room failed")
-    m = GaussianMap.empty(int(hm.count), 1)
-    h2 = m.host()
-    rc = lib.gsf_synth_room(primitive_count, extent, wall_layers, seed, C.byref(h2))
-    if rc != GSF_OK:
-        raise ValueError("synth_room failed")
-    return m
-
-
-def synth_orbit(frames: int, radius: float = 1.0, height: float = 0.0):
-    lib = abi.load()
-    poses = (Pose * frames)()
-    rc = lib.gsf_synth_orbit(frames, radius, height, poses)
-    if rc != GSF_OK:
-        raise ValueError("synth_orbit failed")
-    return [poses[i] for i in range(frames)]
-
-
 class SlamSystem:
     """SlamSystem (slam/system.hpp) on a Context's device map: process() frames in stream order."""
 

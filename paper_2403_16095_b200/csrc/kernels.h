@@ -51,7 +51,7 @@ struct Profiler {
   }
 };
 enum ProfName { PROF_PREPROCESS = 0, PROF_SORT = 1, PROF_BLEND = 2, PROF_BACKWARD = 3, PROF_CHAIN = 4, PROF_SSIM = 5,
-                PROF_ADAM = 6, PROF_BINNING = 7, PROF_NUM = 8 };
+                PROF_ADAM = 6, PROF_BINNING = 7, PROF_POSEJAC = 8, PROF_NUM = 9 };
 
 // Device workspace of one context.  Capacities grow on demand (never shrink).
 struct Workspace {

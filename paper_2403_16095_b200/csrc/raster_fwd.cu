@@ -812,16 +812,18 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   if (side) {
     GSF_CUDA_CHECK(cudaEventRecord(ws.ev_fork, st));
     GSF_CUDA_CHECK(cudaStreamWaitEvent(ws.side, ws.ev_fork, 0));
+    if (pf) pf->begin(PROF_POSEJAC, ws.side);
     k_posejac<<<div_up(P, kPjThreads), kPjThreads, 0, ws.side>>>(a.params, P, ds, a.K, ws.vis_list, ws.bin_counters,
                                                      a.use_world ? ws.world : nullptr, ws.pj_id, ws.bg_id, ws.gg_id,
                                                      ws.bg_slot, ws.gg_slot);
     ++*L;
+    if (pf) pf->end(ws.side);
     GSF_CUDA_CHECK(cudaEventRecord(ws.ev_join, ws.side));
   }
   if (pf) pf->begin(PROF_SORT, st);
   run_binning(ws, ds, P, tiles_x, ntiles, st, L, a.want_posejac);
-  if (side) GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_join, 0));
   if (pf) pf->end(st);
+  if (side) GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_join, 0));
   const float* loss_rgb = a.loss_rgb;
 #define GSF_BLEND_ARGS                                                                                                 \
   ws.ranges, ws.sid, ws.bg_id, ws.gg_id, a.obs, loss_rgb, a.loss_depth, a.W, a.H,                                     \

@@ -49,18 +49,3 @@ def test_ba_partition_covers_window_once():
                 assert list(np.nonzero(owned[r])[0]) == [k for k in range(n) if k % world == r]
 
 
-def test_synthetic_room_and_orbit():
-    m = api.synth_room(5000, 4.0, 3, 0)
-    assert m.count > 4000 and np.isfinite(m.mean).all()
-    # all walls within the room, opacities 0.98 / 0.995
-    assert np.abs(m.mean).max() <= 2.0 + 1e-9
-    ops = 1 / (1 + np.exp(-m.opacity_logit))
-    assert set(np.round(ops, 3)) <= {0.98, 0.995}
-    poses = api.synth_orbit(50, 1.0)
-    assert len(poses) == 50
-    # camera centres on the radius-1 circle
-    from scipy.spatial.transform import Rotation as R
-    for p in poses[:5]:
-        Rm = R.from_rotvec(list(p.rotation_tangent)).as_matrix()
-        c = -Rm.T @ np.array(list(p.translation))
-        assert abs(np.hypot(c[0], c[2]) - 1.0) < 1e-9

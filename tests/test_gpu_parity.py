@@ -709,9 +709,10 @@ def test_checkpoint_roundtrip_and_format(gpu_ctx, orc, tmp_path):
 
 
 def _room_frames(ctx, n, K, orbit=1440):
-    truth = api.synth_room(30000, 4.0, 3, 0)
-    ctx.upload(truth)
-    poses = api.synth_orbit(orbit, 1.0, 0.0)
+    from tools import synth
+    t = synth.room(30000, 4.0, 3, 0)
+    ctx.upload(api.GaussianMap(t.mean, t.log_scale, t.quat, t.opacity_logit, t.sh))
+    poses = [api.pose_of(r, tr) for r, tr in synth.orbit(orbit, 1.0, 0.0)]
     frames = []
     for f in range(n):
         r = ctx.render(poses[f], K)

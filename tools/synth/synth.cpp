@@ -1,4 +1,5 @@
-// synth.cpp — synthetic scene / trajectory generators (support code, not the hot path).
+// synth.cpp — synthetic scene / trajectory generators for the benchmark and tests (tools/, not the
+// product: built into tools/synth/libgsf_synth.so, never into libgsf_cuda.so).
 //
 // Restates io/synthetic.cpp:39-186 (room scene, orbit trajectory) so the benchmark builds the
 // same Replica-shaped inputs the reference's own generator would, draw for draw from
@@ -9,7 +10,7 @@
 #include <random>
 #include <vector>
 
-#include "../../include/gsf_cuda.h"
+#include "../../include/gsf_cuda.h"   // gsf_map_host / gsf_pose layouts only
 
 namespace {
 
@@ -91,7 +92,7 @@ std::vector<Prim> build_room(int count, double extent, int wall_layers, std::mt1
         d = V3(1, 0, 0);
         len = 1.0;
       }
-      d = (1.0 / len) * d;
+      d = V3(d.x / len, d.y / len, d.z / len);   // Eigen's normalize(): *this /= norm()
       const double s = shade(rng);
       V3 rgb(tints[o].x + s, tints[o].y + s, tints[o].z + s);
       rgb.x = std::min(std::max(rgb.x, 0.02), 0.98);
@@ -107,11 +108,11 @@ std::vector<Prim> build_room(int count, double extent, int wall_layers, std::mt1
 void look_at(const V3& p, const V3& target, gsf_pose* out) {
   V3 f(target.x - p.x, target.y - p.y, target.z - p.z);
   double fl = std::sqrt(f.x * f.x + f.y * f.y + f.z * f.z);
-  f = (1.0 / fl) * f;
+  f = V3(f.x / fl, f.y / fl, f.z / fl);   // Eigen's normalized(): / norm()
   V3 r(f.y * 0.0 - f.z * 1.0, f.z * 0.0 - f.x * 0.0, f.x * 1.0 - f.y * 0.0);   // forward x UnitY
   double rl = std::sqrt(r.x * r.x + r.y * r.y + r.z * r.z);
   if (rl < 1e-9) { r = V3(1, 0, 0); rl = 1.0; }
-  r = (1.0 / rl) * r;
+  r = V3(r.x / rl, r.y / rl, r.z / rl);
   const V3 d(f.y * r.z - f.z * r.y, f.z * r.x - f.x * r.z, f.x * r.y - f.y * r.x);   // forward x right
   const double R[3][3] = {{r.x, r.y, r.z}, {d.x, d.y, d.z}, {f.x, f.y, f.z}};
   // log_map (lie.cpp:30-52)
