@@ -219,6 +219,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def fp32_peak_measured():
+    """The FP32 FMA-pipe peak measured on this pool's B200 by tools/fp32_peak.cu (packed FFMA2, the
+    instruction the blend / backward kernels use; scalar FFMA measured 71.7 TFLOP/s)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_fp32_peak.json")) as f:
+            d = json.load(f)
+        return float(d["ffma2_tflops"]), ("measured: tools/fp32_peak.cu, packed FFMA2 on 148 SMs at "
+                                          f"{d['clock_mhz_attr']:.0f} MHz (profiles/r02_fp32_peak.json)")
+    except Exception:
+        return None, None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -370,7 +382,10 @@ def run_ours(args):
     peaks, peak_src = measured_peaks()
     sm_count = torch.cuda.get_device_properties(device).multi_processor_count if torch.cuda.is_available() else 148
     clock_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    fp32_peak = sm_count * 128 * 2 * clock_mhz * 1e6 / 1e12   # TFLOP/s
+    fp32_peak, fp32_src = fp32_peak_measured()
+    if fp32_peak is None:
+        fp32_peak = sm_count * 128 * 2 * clock_mhz * 1e6 / 1e12   # TFLOP/s
+        fp32_src = f"derived: {sm_count} SMs x 128 FP32 lanes x 2 x {clock_mhz:.0f} MHz ({peak_src})"
     V = float(stat.num_visible)
     flops = {"blend": 11.0 * traversed + 24.0 * contributors,
              "backward": 13.0 * traversed + 70.0 * contributors}
@@ -389,7 +404,7 @@ def run_ours(args):
         pass
     roof = {"kernel": kname, "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
             "frac": achieved / fp32_peak, "traffic": traffic,
-            "peak_source": f"derived: {sm_count} SMs x 128 FP32 lanes x 2 x {clock_mhz:.0f} MHz ({peak_src})",
+            "peak_source": fp32_src,
             "algorithmic_flops_per_launch": flops[dom], "avg_launch_ms": per_launch[dom],
             "note": "issue / FP32-pipe bound: no dense contraction (no tensor-core work) and an L2-resident "
                     "working set (DRAM traffic per launch = 'traffic', from profiles/r01_traffic.json), so "

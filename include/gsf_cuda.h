@@ -260,8 +260,10 @@ int gsf_map_step(gsf_ctx ctx, const int32_t* slots, const gsf_pose* poses, int32
                  double* trace);
 /* sliding_ba (track/tracker.hpp:55-57).  poses is updated in place; frame_ids pick the anchor.
  * With a communicator set (gsf_comm_init), each rank passes the full window and renders
- * only the keyframes it owns (k mod nranks == rank); Gaussian gradients are summed with one
- * NCCL all-reduce per iteration; every rank returns the same map and all window poses. */
+ * only the keyframes it owns (k mod nranks == rank).  Per iteration one exchange: the loss, a
+ * divergence flag and the window pose gradients in one fp64 all-reduce, the Gaussian gradients in
+ * one fp32 all-reduce bucketed by parameter group (each group's Adam waits only for its bucket);
+ * every rank returns the same map and all window poses. */
 int gsf_sliding_ba(gsf_ctx ctx, const int32_t* slots, gsf_pose* poses, const int32_t* frame_ids,
                    int32_t n, const gsf_intrinsics* K, const gsf_tracker_cfg* tcfg,
                    const gsf_mapper_cfg* mcfg, int32_t iterations, double* trace);
@@ -359,7 +361,15 @@ int32_t gsf_slam_degraded_frames(gsf_slam slam);
  * logic, usable without a device (ctx may be NULL). */
 int gsf_ba_partition(int32_t n, int32_t nranks, int32_t rank, uint8_t* owned);
 int gsf_comm_unique_id(uint8_t id[128]);
+/* NCCL communicator of a keyframe-sharded job (one context per GPU/rank); id from rank 0's
+ * gsf_comm_unique_id, distributed by the caller. */
 int gsf_comm_init(gsf_ctx ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
+/* Host-staged communicator: the same sharded paths, with every sum-all-reduce staged through pinned
+ * host memory and handed to the caller's callback (e.g. an MPI / gloo process group).  The callback
+ * sums `count` elements of `dtype` in place across ranks and returns 0 on success. */
+enum { GSF_DT_U32 = 3, GSF_DT_F32 = 7, GSF_DT_F64 = 8 };   /* ncclUint32 / ncclFloat32 / ncclFloat64 */
+typedef int (*gsf_host_allreduce_fn)(void* buf, size_t count, int32_t dtype, void* user);
+int gsf_comm_init_host(gsf_ctx ctx, int32_t nranks, int32_t rank, gsf_host_allreduce_fn fn, void* user);
 
 #ifdef __cplusplus
 }

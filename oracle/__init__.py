@@ -70,7 +70,8 @@ class MirOut(C.Structure):
                 ("pair_capacity", C.c_int64), ("color", fp), ("alpha_depth", fp), ("median_depth", fp),
                 ("median_valid", u8p), ("opacity", fp), ("uncertainty", fp), ("final_transmittance", fp),
                 ("per_pixel_count", i32p), ("dominant", i32p), ("median_prim", i32p), ("dominant_weight", fp),
-                ("last_index", i32p), ("num_visible", C.c_int64), ("num_pairs", C.c_int64)]
+                ("last_index", i32p), ("num_visible", C.c_int64), ("num_pairs", C.c_int64),
+                ("num_flagged", C.c_int64)]
 
 
 _libs = {}
@@ -518,12 +519,12 @@ def mirror_render(m, pose, K, obs=None, cfg=None, pair_capacity=1 << 22):
                 o.uncertainty.ctypes.data_as(fp), o.final_transmittance.ctypes.data_as(fp),
                 o.per_pixel_count.ctypes.data_as(i32p), o.dominant.ctypes.data_as(i32p),
                 o.median_prim.ctypes.data_as(i32p), o.dominant_weight.ctypes.data_as(fp), o.last_index.ctypes.data_as(i32p),
-                0, 0)
+                0, 0, 0)
     ob = None if obs is None else np.ascontiguousarray(obs, dtype=np.float32)
     h = host_of(m)
     _check(lib().mir_render(C.byref(h), C.byref(pose), C.byref(K), None if ob is None else ob.ctypes.data_as(fp),
                             C.byref(cfg), C.byref(mo)))
-    o.num_visible, o.num_pairs = int(mo.num_visible), int(mo.num_pairs)
+    o.num_visible, o.num_pairs, o.num_flagged = int(mo.num_visible), int(mo.num_pairs), int(mo.num_flagged)
     o.visible = o.visible[:P]
     o.rank_to_id = o.rank_to_id[: o.num_visible]
     o.pair_rank = o.pair_rank[: o.num_pairs]

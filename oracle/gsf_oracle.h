@@ -139,6 +139,7 @@ typedef struct {
   float* uncertainty; float* final_transmittance; int32_t* per_pixel_count; int32_t* dominant;
   int32_t* median_prim; float* dominant_weight; int32_t* last_index;
   int64_t num_visible, num_pairs;
+  int64_t num_flagged;     /* pixels re-blended by the exact-decision fix-up */
 } mir_out;
 int mir_render(const gsf_map_host* map, const gsf_pose* pose, const gsf_intrinsics* K,
                const float* observed_depth, const gsf_raster_cfg* cfg, mir_out* out);

@@ -90,6 +90,7 @@ extern "C" int mir_render(const gsf_map_host* map, const gsf_pose* pose, const g
     blend_rho_bounds(bg[r], kc);
     gg[r] = make_guard_g(pre[vis[r]]);
   }
+  int64_t flagged = 0;
   for (int t = 0; t < ntiles; ++t) {
     const int tx = t % rp.tiles_x, ty = t / rp.tiles_x;
     for (int y = ty * ts; y < std::min(H, (ty + 1) * ts); ++y)
@@ -109,7 +110,23 @@ extern "C" int mir_render(const gsf_map_host* map, const gsf_pose* pose, const g
           const int r = lists[t][j];
           const PairEval e = eval_pair(px, py, bg[r], &gg[r], kc);
           if (!e.code) continue;
-          pixel_accumulate(s, bg[r], e, vis[r], static_cast<int32_t>(j), obs_valid, ov, kc);
+          pixel_accumulate(s, bg[r], e, vis[r], static_cast<int32_t>(j), obs_valid, ov, kc, true);
+        }
+        if (s.flag) {   // exact-decision fix-up: the pixel re-blended in fp64 (k_pixel_fixup)
+          ExactPixel q;
+          exact_init(q);
+          for (size_t j = 0; j < lists[t].size() && !q.done; ++j) {
+            const int r = lists[t][j];
+            double a = 0.0;
+            if (exact_alpha(static_cast<double>(px), static_cast<double>(py), gg[r], kc, &a))
+              exact_accumulate(q, a, bg[r], vis[r], static_cast<int32_t>(j), obs_valid, static_cast<double>(ov), kc);
+          }
+          s.cr = static_cast<float>(q.cr); s.cg = static_cast<float>(q.cg); s.cb = static_cast<float>(q.cb);
+          s.ad = static_cast<float>(q.ad); s.op = static_cast<float>(q.op); s.unc = static_cast<float>(q.unc);
+          s.T = static_cast<float>(q.T); s.best = static_cast<float>(q.best);
+          s.med_depth = static_cast<float>(q.med_depth);
+          s.count = q.count; s.dominant = q.dominant; s.median = q.median; s.last = q.last;
+          ++flagged;
         }
         if (out->color) { out->color[3 * pi] = s.cr; out->color[3 * pi + 1] = s.cg; out->color[3 * pi + 2] = s.cb; }
         if (out->alpha_depth) out->alpha_depth[pi] = s.ad;
@@ -125,6 +142,7 @@ extern "C" int mir_render(const gsf_map_host* map, const gsf_pose* pose, const g
         if (out->last_index) out->last_index[pi] = s.last;
       }
   }
+  out->num_flagged = flagged;
   return GSF_OK;
 }
 

@@ -184,7 +184,12 @@ SIGNATURES = {
     "gsf_ba_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, u8p]),
     "gsf_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8 * 128)]),
     "gsf_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_uint8 * 128)]),
+    "gsf_comm_init_host": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
 }
+
+# gsf_host_allreduce_fn: int (*)(void* buf, size_t count, int32_t dtype, void* user)
+HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+GSF_DT_U32, GSF_DT_F32, GSF_DT_F64 = 3, 7, 8
 
 _lib = None
 

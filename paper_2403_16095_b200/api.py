@@ -427,6 +427,30 @@ class Context:
         arr = (C.c_uint8 * 128)(*uid)
         self._check(self.lib.gsf_comm_init(self.h, nranks, rank, C.byref(arr)))
 
+    def comm_setup_host(self, group=None):
+        """Join the torch.distributed job through a host-staged communicator: every sum-all-reduce of
+        the sharded paths is staged through pinned host memory and summed by torch.distributed over
+        `group` (any backend, e.g. gloo).  Same decomposition as the NCCL path."""
+        import torch
+        import torch.distributed as dist
+        dt = {abi.GSF_DT_U32: (np.uint32, torch.int64), abi.GSF_DT_F32: (np.float32, torch.float32),
+              abi.GSF_DT_F64: (np.float64, torch.float64)}
+
+        def _allreduce(buf, count, dtype, user):
+            try:
+                npt, tt = dt[dtype]
+                a = np.ctypeslib.as_array(C.cast(buf, C.POINTER(np.ctypeslib.as_ctypes_type(npt))), (count,))
+                t = torch.from_numpy(a.astype(np.int64) if dtype == abi.GSF_DT_U32 else a.copy()).to(tt)
+                dist.all_reduce(t, group=group)
+                a[...] = t.numpy().astype(npt)
+                return 0
+            except Exception:   # noqa: BLE001 (reported to the library as a failed exchange)
+                return 1
+
+        self._host_ar = abi.HOST_ALLREDUCE_FN(_allreduce)   # kept alive with the context
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self._check(self.lib.gsf_comm_init_host(self.h, world, rank, C.cast(self._host_ar, C.c_void_p), None))
+
     def comm_setup(self, group=None):
         """Join this context to the torch.distributed job: rank 0 draws the NCCL unique id, it is
         broadcast over `group` (any backend), then every rank calls gsf_comm_init."""

@@ -50,6 +50,8 @@ struct NcclApi {
   int (*comm_init_rank)(void**, int, const void*, int) = nullptr;  // ncclUniqueId passed by value (128 B)
   int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*comm_destroy)(void*) = nullptr;
+  int (*group_start)() = nullptr;
+  int (*group_end)() = nullptr;
   const char* (*get_error)(int) = nullptr;
   bool load() {
     if (h) return true;
@@ -60,6 +62,8 @@ struct NcclApi {
     all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclAllReduce"));
     comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
     get_error = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+    group_start = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupStart"));
+    group_end = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupEnd"));
     return get_unique_id && all_reduce && comm_destroy;
   }
 };
@@ -120,7 +124,7 @@ struct gsf_ctx_s {
   float* adam_m = nullptr;
   float* adam_v = nullptr;
   double adam_step = 0.0;
-  float* nu = nullptr;
+  double* nu = nullptr;   // per-primitive uncertainty (fp64: prune compares it with tau exactly as the reference)
   uint8_t* observed = nullptr;
   float* d_mean2d = nullptr;
   double* grad_accum = nullptr;   // MapState::grad_accum (fp64 like the reference)
@@ -159,8 +163,17 @@ struct gsf_ctx_s {
   // staging for host inputs
   float* stage = nullptr;
   size_t stage_bytes = 0;
-  // comm
+  // comm: an NCCL communicator (gsf_comm_init) or a host-staged one (gsf_comm_init_host: the
+  // caller's all-reduce over host memory, e.g. a gloo/MPI process group)
   void* comm = nullptr;
+  gsf_host_allreduce_fn host_ar = nullptr;
+  void* host_ar_user = nullptr;
+  void* host_stage = nullptr;   // pinned staging of the host-staged all-reduce
+  size_t host_stage_bytes = 0;
+  cudaStream_t comm_stream = nullptr;   // NCCL buckets run here, overlapping the per-group Adam
+  cudaEvent_t ev_grads = nullptr, ev_bucket[8] = {nullptr};
+  double* ba_pack = nullptr;    // [loss sum, halt flag, 6 pose-gradient doubles per window keyframe]
+  int ba_pack_cap = 0;
   int nranks = 1, rank = 0;
   float* red_f = nullptr;   // allreduce scratch for the loss sum
   Profiler prof;
@@ -333,6 +346,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     dalloc(ws.opacity, npix); dalloc(ws.uncertainty, npix); dalloc(ws.final_T, npix); dalloc(ws.count, npix);
     dalloc(ws.dominant, npix); dalloc(ws.median_prim, npix); dalloc(ws.dominant_w, npix); dalloc(ws.last, npix);
     dalloc(ws.pxcode, npix);
+    dalloc(ws.fix_list, npix);
     dalloc(ws.obs, npix); dalloc(ws.upstream, 7 * npix); dalloc(ws.dssim, 3 * npix); dalloc(ws.ssim_tmp, 9 * npix);
     ws.npix_cap = npix;
   }
@@ -545,6 +559,29 @@ __global__ void k_kf_grab(DevState* ds, KfPose* kf, int k, double* loss_acc, dou
 
 __global__ void k_store(const double* src, double* dst) { *dst = *src; }
 
+// Sharded sliding_ba: everything a rank contributes besides the Gaussian gradients, packed into one
+// fp64 buffer for a single all-reduce — the window loss sum, a divergence flag (so every rank halts
+// at the same iteration) and the six pose-gradient components of each window keyframe (zero for
+// keyframes another rank owns).
+__global__ void k_ba_pack(const DevState* ds, const KfPose* kf, int n, const double* loss_acc, double* pack) {
+  for (int i = threadIdx.x; i < 6 * n; i += blockDim.x) pack[2 + i] = kf[i / 6].grad[i % 6];
+  if (threadIdx.x == 0) {
+    pack[0] = *loss_acc;
+    pack[1] = ds->halt == 2 ? 1.0 : 0.0;
+  }
+}
+__global__ void k_ba_unpack(DevState* ds, KfPose* kf, int n, double* loss_acc, const double* pack, int it) {
+  for (int i = threadIdx.x; i < 6 * n; i += blockDim.x) kf[i / 6].grad[i % 6] = pack[2 + i];
+  if (threadIdx.x == 0) {
+    *loss_acc = pack[0];
+    if (pack[1] > 0.0 && ds->halt != 2) {
+      ds->halt = 2;
+      ds->halt_iter = it;
+      ds->loss_total = pack[0];
+    }
+  }
+}
+
 // Pose Adam + perturbed for every non-anchor keyframe (tracker.cpp:168-179).
 __global__ void k_kf_update(DevState* ds, KfPose* kf, int n, int anchor, double lr_rot, double lr_trans) {
   const int k = threadIdx.x;
@@ -695,10 +732,10 @@ int gsf_ctx_destroy(gsf_ctx c) {
   void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
-                  ws.last, ws.pxcode, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
+                  ws.last, ws.pxcode, ws.fix_list, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
                   ws.red_part, c->bp_scratch, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
-                  c->red_f};
+                  c->red_f, c->ba_pack};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, c->stream);
   if (c->track_in.rgb) cudaFreeAsync(c->track_in.rgb, c->stream);
@@ -711,6 +748,11 @@ int gsf_ctx_destroy(gsf_ctx c) {
   if (c->ds_host) cudaFreeHost(c->ds_host);
   if (c->kf_host) cudaFreeHost(c->kf_host);
   if (c->stage) cudaFreeHost(c->stage);
+  if (c->host_stage) cudaFreeHost(c->host_stage);
+  if (c->ev_grads) cudaEventDestroy(c->ev_grads);
+  for (cudaEvent_t e : c->ev_bucket)
+    if (e) cudaEventDestroy(e);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (ws.ev_fork) cudaEventDestroy(ws.ev_fork);
   if (ws.ev_join) cudaEventDestroy(ws.ev_join);
   if (ws.side) cudaStreamDestroy(ws.side);
@@ -751,13 +793,13 @@ int gsf_map_upload(gsf_ctx c, const gsf_map_host* m) {
       ++c->launches;
       sync(c);
       cudaFree(tmp);
-      std::vector<float> nu(P, 0.0f);
+      std::vector<double> nu(P, 0.0);
       std::vector<uint8_t> ob(P, 0);
       for (int64_t i = 0; i < P; ++i) {
-        if (m->uncertainty) nu[i] = static_cast<float>(m->uncertainty[i]);
+        if (m->uncertainty) nu[i] = m->uncertainty[i];
         if (m->observed) ob[i] = m->observed[i];
       }
-      GSF_CUDA_CHECK(cudaMemcpy(c->nu, nu.data(), sizeof(float) * P, cudaMemcpyHostToDevice));
+      GSF_CUDA_CHECK(cudaMemcpy(c->nu, nu.data(), sizeof(double) * P, cudaMemcpyHostToDevice));
       GSF_CUDA_CHECK(cudaMemcpy(c->observed, ob.data(), P, cudaMemcpyHostToDevice));
       GSF_CUDA_CHECK(cudaMemset(c->adam_m, 0, sizeof(float) * P * D));
       GSF_CUDA_CHECK(cudaMemset(c->adam_v, 0, sizeof(float) * P * D));
@@ -784,9 +826,9 @@ int gsf_map_download(gsf_ctx c, gsf_map_host* m) {
     ++c->launches;
     double* h = static_cast<double*>(stage(c, sizeof(double) * P * D));
     GSF_CUDA_CHECK(cudaMemcpyAsync(h, tmp, sizeof(double) * P * D, cudaMemcpyDeviceToHost, c->stream));
-    std::vector<float> nu(P);
+    std::vector<double> nu(P);
     std::vector<uint8_t> ob(P);
-    GSF_CUDA_CHECK(cudaMemcpyAsync(nu.data(), c->nu, sizeof(float) * P, cudaMemcpyDeviceToHost, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(nu.data(), c->nu, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
     GSF_CUDA_CHECK(cudaMemcpyAsync(ob.data(), c->observed, P, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     cudaFree(tmp);
@@ -1488,6 +1530,7 @@ int gsf_comm_init(gsf_ctx c, int32_t nranks, int32_t rank, const uint8_t id[128]
     if (nranks < 1 || rank < 0 || rank >= nranks) throw EInval("comm_init: bad rank/size");
     c->nranks = nranks;
     c->rank = rank;
+    c->host_ar = nullptr;
     if (nranks == 1) return;
     if (!g_nccl.load()) throw EUnsupported("NCCL (libnccl.so.2) could not be loaded");
     auto init = reinterpret_cast<nccl_init_fn>(dlsym(g_nccl.h, "ncclCommInitRank"));
@@ -1496,6 +1539,23 @@ int gsf_comm_init(gsf_ctx c, int32_t nranks, int32_t rank, const uint8_t id[128]
     std::memcpy(uid.b, id, 128);
     const int r = init(&c->comm, nranks, uid, rank);
     if (r != 0) throw EUnsupported(std::string("ncclCommInitRank failed: ") + (g_nccl.get_error ? g_nccl.get_error(r) : "?"));
+    if (!c->comm_stream) GSF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    if (!c->ev_grads) GSF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_grads, cudaEventDisableTiming));
+    for (cudaEvent_t& e : c->ev_bucket)
+      if (!e) GSF_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  });
+}
+
+int gsf_comm_init_host(gsf_ctx c, int32_t nranks, int32_t rank, gsf_host_allreduce_fn fn, void* user) {
+  return guard(c, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw EInval("comm_init: bad rank/size");
+    if (nranks > 1 && !fn) throw EInval("comm_init_host: null all-reduce callback");
+    if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
+    c->comm = nullptr;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->host_ar = fn;
+    c->host_ar_user = user;
   });
 }
 
@@ -1503,10 +1563,66 @@ static double* kf_grad(gsf_ctx_s* c, int k) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(c->kf + k) + offsetof(KfPose, grad));
 }
 
-static void allreduce(gsf_ctx_s* c, void* buf, size_t count, int dtype /*7 f32, 8 f64*/) {
-  if (c->nranks <= 1) return;
-  const int r = g_nccl.all_reduce(buf, buf, count, dtype, 0 /*sum*/, c->comm, c->stream);
+static size_t dtype_bytes(int dtype) { return dtype == GSF_DT_F64 ? 8 : 4; }
+
+// Sum-all-reduce of a device buffer over the context's communicator, ordered on `st` (NCCL), or
+// staged through pinned host memory to the caller's callback (host communicator; synchronous).
+static void allreduce(gsf_ctx_s* c, void* buf, size_t count, int dtype, cudaStream_t st) {
+  if (c->nranks <= 1 || count == 0) return;
+  if (c->host_ar) {
+    const size_t bytes = count * dtype_bytes(dtype);
+    if (c->host_stage_bytes < bytes) {
+      if (c->host_stage) cudaFreeHost(c->host_stage);
+      c->host_stage = nullptr;
+      GSF_CUDA_CHECK(cudaMallocHost(&c->host_stage, bytes));
+      c->host_stage_bytes = bytes;
+    }
+    GSF_CUDA_CHECK(cudaMemcpyAsync(c->host_stage, buf, bytes, cudaMemcpyDeviceToHost, st));
+    GSF_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (c->host_ar(c->host_stage, count, dtype, c->host_ar_user) != 0) throw ERuntime("host all-reduce callback failed");
+    GSF_CUDA_CHECK(cudaMemcpyAsync(buf, c->host_stage, bytes, cudaMemcpyHostToDevice, st));
+    GSF_CUDA_CHECK(cudaStreamSynchronize(st));
+    return;
+  }
+  const int r = g_nccl.all_reduce(buf, buf, count, dtype, 0 /*sum*/, c->comm, st);
   if (r != 0) throw EUnsupported(std::string("ncclAllReduce failed: ") + (g_nccl.get_error ? g_nccl.get_error(r) : "?"));
+}
+
+// One exchange per sharded sliding_ba iteration: the packed fp64 scalars (loss,
+// divergence flag, window pose gradients) and the fp32 Gaussian gradients, bucketed by parameter
+// group (mean, log_scale, quat, opacity, SH: contiguous [field][P] slices).  Over NCCL the buckets
+// run on the communicator stream and each group's Adam waits only for its own bucket, so the
+// optimizer step of one group overlaps the reduction of the next; over a host communicator the
+// same sequence runs synchronously.
+static void exchange_and_step(gsf_ctx_s* c, int n, double* loss_acc, const AdamGroups& g, int it) {
+  if (c->ba_pack_cap < 2 + 6 * n) {
+    dalloc(c->ba_pack, 2 + 6 * n);
+    c->ba_pack_cap = 2 + 6 * n;
+  }
+  k_ba_pack<<<1, 128, 0, c->stream>>>(c->ds, c->kf, n, loss_acc, c->ba_pack);
+  ++c->launches;
+  static const int kGroupFields[6] = {0, 3, 6, 10, 11, -1};
+  const bool nccl = c->host_ar == nullptr;
+  cudaStream_t cs = nccl ? c->comm_stream : c->stream;
+  if (nccl) {
+    GSF_CUDA_CHECK(cudaEventRecord(c->ev_grads, c->stream));
+    GSF_CUDA_CHECK(cudaStreamWaitEvent(cs, c->ev_grads, 0));
+  }
+  allreduce(c, c->ba_pack, static_cast<size_t>(2 + 6 * n), GSF_DT_F64, cs);
+  for (int b = 0; b < 5; ++b) {
+    const int f0 = kGroupFields[b], f1 = b == 4 ? c->D : kGroupFields[b + 1];
+    allreduce(c, c->grads + static_cast<int64_t>(f0) * c->P, static_cast<size_t>(f1 - f0) * c->P, GSF_DT_F32, cs);
+    if (nccl) GSF_CUDA_CHECK(cudaEventRecord(c->ev_bucket[b], cs));
+  }
+  for (int b = 0; b < 5; ++b) {
+    if (nccl) GSF_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_bucket[b], 0));
+    if (b == 0) {
+      k_ba_unpack<<<1, 128, 0, c->stream>>>(c->ds, c->kf, n, loss_acc, c->ba_pack, it);
+      ++c->launches;
+    }
+    const int f0 = kGroupFields[b], f1 = b == 4 ? c->D : kGroupFields[b + 1];
+    run_adam_fields(c->params, c->grads, c->adam_m, c->adam_v, c->P, f0, f1, g, c->adam_step, c->stream, &c->launches);
+  }
 }
 
 int gsf_sliding_ba(gsf_ctx c, const int32_t* slots, gsf_pose* poses, const int32_t* frame_ids, int32_t n,
@@ -1554,15 +1670,14 @@ int gsf_sliding_ba(gsf_ctx c, const int32_t* slots, gsf_pose* poses, const int32
         }
         enqueue_map_view(c, *fr[k], k, *K, *m, it, loss_acc, -1, true);
       }
+      c->adam_step += 1.0;
       if (c->nranks > 1) {
-        allreduce(c, c->grads, static_cast<size_t>(c->P) * c->D, 7);
-        allreduce(c, loss_acc, 1, 8);
-        for (int k = 0; k < n; ++k) allreduce(c, kf_grad(c, k), 6, 8);
+        exchange_and_step(c, n, loss_acc, g, it);
+      } else {
+        run_adam(c->params, c->grads, c->adam_m, c->adam_v, c->P, c->D, g, c->adam_step, c->stream, &c->launches);
       }
       k_store<<<1, 1, 0, c->stream>>>(loss_acc, c->trace_dev + it);
       ++c->launches;
-      c->adam_step += 1.0;
-      run_adam(c->params, c->grads, c->adam_m, c->adam_v, c->P, c->D, g, c->adam_step, c->stream, &c->launches);
       k_kf_update<<<1, 32 * div_up(n, 32), 0, c->stream>>>(c->ds, c->kf, n, anchor, tcfg->lr_rotation, tcfg->lr_translation);
       ++c->launches;
     }
@@ -1639,8 +1754,8 @@ static uint32_t backproject_count(gsf_ctx_s* c, BackprojectArgs& a, const Frame&
 static void grow_map_soa(gsf_ctx_s* c, int64_t P_new) {
   const int64_t P_old = c->P;
   const int D = c->D;
-  float *params = nullptr, *m = nullptr, *v = nullptr, *nu = nullptr;
-  double* acc = nullptr;
+  float *params = nullptr, *m = nullptr, *v = nullptr;
+  double *nu = nullptr, *acc = nullptr;
   uint8_t* obs = nullptr;
   int32_t* cnt = nullptr;
   dalloc(params, static_cast<size_t>(P_new) * D);
@@ -1659,7 +1774,7 @@ static void grow_map_soa(gsf_ctx_s* c, int64_t P_new) {
     GSF_CUDA_CHECK(cudaMemcpy2DAsync(params, wb, c->params, ob, ob, D, cudaMemcpyDeviceToDevice, c->stream));
     GSF_CUDA_CHECK(cudaMemcpy2DAsync(m, wb, c->adam_m, ob, ob, D, cudaMemcpyDeviceToDevice, c->stream));
     GSF_CUDA_CHECK(cudaMemcpy2DAsync(v, wb, c->adam_v, ob, ob, D, cudaMemcpyDeviceToDevice, c->stream));
-    GSF_CUDA_CHECK(cudaMemcpyAsync(nu, c->nu, ob, cudaMemcpyDeviceToDevice, c->stream));
+    GSF_CUDA_CHECK(cudaMemcpyAsync(nu, c->nu, sizeof(double) * P_old, cudaMemcpyDeviceToDevice, c->stream));
     GSF_CUDA_CHECK(cudaMemcpyAsync(obs, c->observed, P_old, cudaMemcpyDeviceToDevice, c->stream));
     GSF_CUDA_CHECK(cudaMemcpyAsync(acc, c->grad_accum, sizeof(double) * P_old, cudaMemcpyDeviceToDevice, c->stream));
     GSF_CUDA_CHECK(cudaMemcpyAsync(cnt, c->grad_count, sizeof(int32_t) * P_old, cudaMemcpyDeviceToDevice, c->stream));
@@ -1826,7 +1941,8 @@ static gsf_structural_change densify_and_cull(gsf_ctx_s* c, const gsf_mapper_cfg
   }
   if (!z.empty())
     GSF_CUDA_CHECK(cudaMemcpyAsync(d_z, z.data(), sizeof(double) * z.size(), cudaMemcpyHostToDevice, c->stream));
-  float *params = nullptr, *mm = nullptr, *vv = nullptr, *nu = nullptr;
+  float *params = nullptr, *mm = nullptr, *vv = nullptr;
+  double* nu = nullptr;
   uint8_t* obs = nullptr;
   const int64_t cap = std::max<int64_t>(P_new, 1);
   dalloc(params, static_cast<size_t>(cap) * D);
@@ -2012,8 +2128,8 @@ int gsf_accumulate_uncertainty(gsf_ctx c, const int32_t* slots, const gsf_pose* 
                            c->unc_sum, c->unc_cnt, c->stream, &c->launches);
     }
     if (c->nranks > 1) {
-      allreduce(c, c->unc_sum, static_cast<size_t>(P), 8 /*f64*/);
-      allreduce(c, c->unc_cnt, static_cast<size_t>(P), 3 /*u32*/);
+      allreduce(c, c->unc_sum, static_cast<size_t>(P), GSF_DT_F64, c->stream);
+      allreduce(c, c->unc_cnt, static_cast<size_t>(P), GSF_DT_U32, c->stream);
     }
     GSF_CUDA_CHECK(cudaMemsetAsync(c->counters, 0, sizeof(uint32_t) * 16, c->stream));
     run_uncertainty_finalize(c->unc_sum, c->unc_cnt, c->nu, c->observed, P, c->counters, c->stream, &c->launches);
@@ -2033,7 +2149,7 @@ int gsf_prune_unreliable(gsf_ctx c, double tau, double reduced_opacity, int32_t*
     if (!c->counters) dalloc(c->counters, 16);
     const float target = static_cast<float>(std::log(reduced_opacity / (1.0 - reduced_opacity)));
     GSF_CUDA_CHECK(cudaMemsetAsync(c->counters, 0, sizeof(uint32_t) * 16, c->stream));
-    run_prune(c->nu, c->params + 10 * c->P, c->P, static_cast<float>(tau), target, c->counters, c->stream, &c->launches);
+    run_prune(c->nu, c->params + 10 * c->P, c->P, tau, target, c->counters, c->stream, &c->launches);
     uint32_t cnt = 0;
     GSF_CUDA_CHECK(cudaMemcpyAsync(&cnt, c->counters, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     sync(c);

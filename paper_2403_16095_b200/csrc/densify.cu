@@ -46,11 +46,11 @@ __global__ void k_densify_codes(const float* __restrict__ params, int64_t P, con
 
 // kind: 0 kept (moments carried), 1 clone (moments zero), 2 child (offset mean, shrunken scale)
 __global__ void k_densify_build(const float* __restrict__ params, const float* __restrict__ m, const float* __restrict__ v,
-                                const float* __restrict__ nu, const uint8_t* __restrict__ observed, int64_t P_old, int D,
+                                const double* __restrict__ nu, const uint8_t* __restrict__ observed, int64_t P_old, int D,
                                 const int32_t* __restrict__ src, const uint8_t* __restrict__ kind,
                                 const int32_t* __restrict__ zidx, const double* __restrict__ z, double log_split,
                                 int64_t P_new, float* __restrict__ params_n, float* __restrict__ m_n,
-                                float* __restrict__ v_n, float* __restrict__ nu_n, uint8_t* __restrict__ observed_n) {
+                                float* __restrict__ v_n, double* __restrict__ nu_n, uint8_t* __restrict__ observed_n) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= P_new) return;
   const int64_t s = src[j];
@@ -100,9 +100,9 @@ void run_densify_codes(const float* params, int64_t P, const double* accum, cons
   ++*L;
 }
 
-void run_densify_build(const float* params, const float* m, const float* v, const float* nu, const uint8_t* observed,
+void run_densify_build(const float* params, const float* m, const float* v, const double* nu, const uint8_t* observed,
                        int64_t P_old, int D, const int32_t* src, const uint8_t* kind, const int32_t* zidx, const double* z,
-                       double log_split, int64_t P_new, float* params_n, float* m_n, float* v_n, float* nu_n,
+                       double log_split, int64_t P_new, float* params_n, float* m_n, float* v_n, double* nu_n,
                        uint8_t* observed_n, cudaStream_t st, int64_t* L) {
   if (P_new <= 0) return;
   k_densify_build<<<div_up(P_new, 256), 256, 0, st>>>(params, m, v, nu, observed, P_old, D, src, kind, zidx, z, log_split,

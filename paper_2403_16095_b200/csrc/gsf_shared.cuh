@@ -36,6 +36,7 @@ GSF_HD float fmul(float a, float b) { return __fmul_rn(a, b); }
 GSF_HD float fadd(float a, float b) { return __fadd_rn(a, b); }
 GSF_HD float fsub(float a, float b) { return __fsub_rn(a, b); }
 GSF_HD float ffma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+GSF_HD float fdiv(float a, float b) { return __fdiv_rn(a, b); }
 GSF_HD double dmul(double a, double b) { return __dmul_rn(a, b); }
 GSF_HD double dadd(double a, double b) { return __dadd_rn(a, b); }
 GSF_HD double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -53,6 +54,7 @@ GSF_HD float fmul(float a, float b) { return a * b; }
 GSF_HD float fadd(float a, float b) { return a + b; }
 GSF_HD float fsub(float a, float b) { return a - b; }
 GSF_HD float ffma(float a, float b, float c) { return fmaf(a, b, c); }
+GSF_HD float fdiv(float a, float b) { return a / b; }
 GSF_HD double dmul(double a, double b) { return a * b; }
 GSF_HD double dadd(double a, double b) { return a + b; }
 GSF_HD double dsub(double a, double b) { return a - b; }
@@ -510,6 +512,11 @@ struct BlendConsts {
   float rho_hi, rho_lo, rho_min;      // cutoff + band, cutoff - band, band
   float skip_lo, skip_hi, clamp_lo, clamp_hi;
   int32_t fast_ok;                    // exp_neg_half needs no range check on the fast path
+  // exact-decision fix-up (pixel_flag_step / exact_*): fp64 termination threshold, the relative
+  // error bound of an unclamped fp32 alpha, the error of the fp32 clamp value and of the fp32
+  // termination threshold against their fp64 configuration values
+  double term_d;
+  float alpha_rel, clamp_err, term_err;
 };
 
 GSF_HD BlendConsts make_blend_consts(const RasterParams& rp) {
@@ -532,6 +539,15 @@ GSF_HD BlendConsts make_blend_consts(const RasterParams& rp) {
   k.clamp_lo = fsub(k.clamp, cb);
   k.clamp_hi = fadd(k.clamp, cb);
   k.fast_ok = k.cutoff_d < 170.0 ? 1 : 0;
+  k.term_d = rp.termination;
+  // fp32 alpha = sigma_f * exp_poly(rho_f): sigma rounding (u/2), the polynomial (< 3e-7), fmul (u/2)
+  // and the rho error inside the guard band (band_i / 2 <= 1e-6 relative for the bands the fast
+  // path admits; larger bands resolve on the fp64 guard path, whose alpha is the same fp32 product)
+  k.alpha_rel = 2e-6f;
+  k.clamp_err = static_cast<float>(dmax(rp.alpha_clamp - static_cast<double>(k.clamp),
+                                        static_cast<double>(k.clamp) - rp.alpha_clamp)) + 1e-9f;
+  k.term_err = static_cast<float>(dmax(rp.termination - static_cast<double>(k.term),
+                                       static_cast<double>(k.term) - rp.termination) * 2.0) + 1e-30f;
   return k;
 }
 
@@ -692,6 +708,8 @@ struct PixelState {
   float cr, cg, cb, ad, op, unc, best, med_depth;
   int32_t count, dominant, median, last;   // last = list index + 1 of the last contributor
   int32_t done;
+  float eT;        // bound on |T_fp32 - T_fp64| / T (exact-decision fix-up, render API only)
+  int32_t flag;    // a discrete decision lies within the fp32 error of its threshold
 };
 
 GSF_HD void pixel_init(PixelState& s) {
@@ -702,12 +720,17 @@ GSF_HD void pixel_init(PixelState& s) {
   s.median = -1;
   s.last = 0;
   s.done = 0;
+  s.eT = 0.0f;
+  s.flag = 0;
 }
 
 // Accumulate one contributing pair (rasterizer.cpp:116-137).  `id` is the primitive id.
+GSF_HD void pixel_flag_step(PixelState& s, float alpha, int clamped, float w, float t_next, const BlendConsts& k);
+
 GSF_HD void pixel_accumulate(PixelState& s, const BlendG& g, const PairEval& e, int32_t id, int32_t list_index,
-                             bool obs_valid, float obs, const BlendConsts& k) {
+                             bool obs_valid, float obs, const BlendConsts& k, bool flag_exact = false) {
   const float w = fmul(e.alpha, s.T);
+  if (flag_exact) pixel_flag_step(s, e.alpha, e.clamped, w, fmul(s.T, fsub(1.0f, e.alpha)), k);
   s.cr = ffma(w, g.r, s.cr);
   s.cg = ffma(w, g.g, s.cg);
   s.cb = ffma(w, g.b, s.cb);
@@ -746,6 +769,93 @@ GSF_HD void pixel_accumulate_min(PixelState& s, const BlendG& g, const PairEval&
   s.last = list_index + 1;
   s.T = fmul(s.T, fsub(1.0f, e.alpha));
   if (s.T < k.term) s.done = 1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Exact discrete decisions of the render API (rasterizer.cpp:116-137 in fp64).
+//
+// The fp32 blend agrees with the fp64 reference on every per-pair decision (the fp64 guard
+// bands above), but T, w = alpha T and the running maximum are fp32 accumulations: where the
+// termination test (T < 1e-8), the median crossing (T >= 0.5 > T') or the dominant's strict
+// maximum sits within their rounding error of its threshold, the fp64 reference can decide the
+// other way (~1e-5 of pixels on a saturated 500k-primitive frame).  pixel_flag_step carries a
+// bound on T's relative error along the walk and flags such pixels; exact_alpha /
+// exact_accumulate re-blend a flagged pixel in fp64 with the reference's formulas, and that
+// result replaces the fp32 one.  Device and mirror run the same functions, so they stay
+// bit-identical, and the flagged pixels' integer outputs are the fp64 reference's.
+// ---------------------------------------------------------------------------------------------
+GSF_HD void pixel_flag_step(PixelState& s, float alpha, int clamped, float w, float t_next, const BlendConsts& k) {
+  const float u = 5.9604645e-8f;
+  const float ea = clamped ? k.clamp_err : fmul(k.alpha_rel, alpha);   // |alpha_f - alpha_d|
+  const float om = fsub(1.0f, alpha);
+  const float e_pre = s.eT;
+  s.eT = fadd(fadd(e_pre, fdiv(ffma(u, om, ea), om)), u);               // + rel. error of (1 - alpha), fmul
+  const float m = fmul(4.0f, s.eT);
+  // termination: T' < term
+  if (fabsf(fsub(t_next, k.term)) <= fadd(fmul(m, k.term), k.term_err)) s.flag = 1;
+  // median crossing at 0.5 while no median is chosen (the first step's T = 1 is exact)
+  if (s.median < 0 && fabsf(fsub(t_next, 0.5f)) <= fmul(m, 0.5f)) s.flag = 1;
+  // dominant: first strict maximum of w (error of w: T's before the step, alpha's, the fmul)
+  if (s.best > 0.0f) {
+    const float ew = fadd(fadd(e_pre, fdiv(ea, alpha)), u);
+    const float big = w > s.best ? w : s.best;
+    if (fabsf(fsub(w, s.best)) <= fmul(fmul(8.0f, fadd(ew, fadd(e_pre, u))), big)) s.flag = 1;
+  }
+}
+
+// The reference's per-pair decision in fp64 (rasterizer.cpp:106-114) from the fp64 guard copies:
+// returns 0 (skip) or 1 with alpha = min(sigma g, clamp).
+GSF_HD int exact_alpha(double px, double py, const GuardG& g, const BlendConsts& k, double* alpha) {
+  const double rho = guard_rho(px, py, g);
+  if (rho > k.cutoff_d || rho < 0.0) return 0;
+  const double raw = dmul(g.sigma, exp_d(dmul(-0.5, rho)));
+  if (raw < k.skip_d) return 0;
+  *alpha = raw > k.clamp_d ? k.clamp_d : raw;
+  return 1;
+}
+
+struct ExactPixel {
+  double T, cr, cg, cb, ad, op, unc, best, med_depth;
+  int32_t count, dominant, median, last, done;
+};
+
+GSF_HD void exact_init(ExactPixel& s) {
+  s.T = 1.0;
+  s.cr = s.cg = s.cb = s.ad = s.op = s.unc = s.best = s.med_depth = 0.0;
+  s.count = 0;
+  s.dominant = -1;
+  s.median = -1;
+  s.last = 0;
+  s.done = 0;
+}
+
+// blend_pixel's accumulation (rasterizer.cpp:116-137) in fp64; colour and depth are the fp32
+// per-primitive values the fp32 path blends.
+GSF_HD void exact_accumulate(ExactPixel& s, double alpha, const BlendG& g, int32_t id, int32_t list_index, bool obs_valid,
+                             double obs, const BlendConsts& k) {
+  const double w = dmul(alpha, s.T);
+  s.cr = dadd(s.cr, dmul(w, static_cast<double>(g.r)));
+  s.cg = dadd(s.cg, dmul(w, static_cast<double>(g.g)));
+  s.cb = dadd(s.cb, dmul(w, static_cast<double>(g.b)));
+  s.ad = dadd(s.ad, dmul(w, static_cast<double>(g.depth)));
+  s.op = dadd(s.op, w);
+  if (obs_valid) {
+    const double d = dsub(static_cast<double>(g.depth), obs);
+    s.unc = dadd(s.unc, dmul(dmul(w, d), d));
+  }
+  if (w > s.best) {
+    s.best = w;
+    s.dominant = id;
+  }
+  s.count += 1;
+  s.last = list_index + 1;
+  const double t_next = dmul(s.T, dsub(1.0, alpha));
+  if (s.median < 0 && s.T >= 0.5 && t_next < 0.5) {
+    s.median = id;
+    s.med_depth = static_cast<double>(g.depth);
+  }
+  s.T = t_next;
+  if (s.T < k.term_d) s.done = 1;
 }
 
 }  // namespace gsfk

@@ -106,6 +106,7 @@ struct Workspace {
   float* dominant_w = nullptr;
   int32_t* last = nullptr;
   uint8_t* pxcode = nullptr;     // tracking: per pixel, the signs of the loss seeds (pixel_seed_code)
+  uint32_t* fix_list = nullptr;  // render API: pixels flagged for the exact-decision fix-up (k_pixel_fixup)
   float* obs = nullptr;         // observed depth of the API render (npix)
   float* upstream = nullptr;    // explicit upstream maps for gsf_render_backward (7*npix)
   float* dssim = nullptr;       // 3*npix: d(w_ssim * ssim loss)/d colour (mapping)
@@ -202,6 +203,9 @@ struct AdamGroups {
 };
 void run_adam(float* params, const float* grads, float* m, float* v, int64_t P, int D, const AdamGroups& g, double step,
               cudaStream_t st, int64_t* launches);
+// Adam over the fields [f0, f1) of the SoA map only (the per-group buckets of a sharded sliding_ba)
+void run_adam_fields(float* params, const float* grads, float* m, float* v, int64_t P, int f0, int f1,
+                     const AdamGroups& g, double step, cudaStream_t st, int64_t* launches);
 void run_track_update(DevState* ds, int iteration, cudaStream_t st, int64_t* launches);
 
 // densify.cu (mapper.cpp:172-230, 261-269)
@@ -209,9 +213,9 @@ void run_densify_stats(const uint8_t* visible, const float* d_mean2d, double* ac
                        cudaStream_t st, int64_t* launches);
 void run_densify_codes(const float* params, int64_t P, const double* accum, const int32_t* cnt, double cull_opacity,
                        double grad_threshold, double size_boundary, uint8_t* code, cudaStream_t st, int64_t* launches);
-void run_densify_build(const float* params, const float* m, const float* v, const float* nu, const uint8_t* observed,
+void run_densify_build(const float* params, const float* m, const float* v, const double* nu, const uint8_t* observed,
                        int64_t P_old, int D, const int32_t* src, const uint8_t* kind, const int32_t* zidx, const double* z,
-                       double log_split, int64_t P_new, float* params_n, float* m_n, float* v_n, float* nu_n,
+                       double log_split, int64_t P_new, float* params_n, float* m_n, float* v_n, double* nu_n,
                        uint8_t* observed_n, cudaStream_t st, int64_t* launches);
 
 // spawn.cu: initialize_map / spawn_gaussians candidates (one per stride-sampled pixel)
@@ -230,15 +234,15 @@ struct BackprojectArgs {
 int64_t run_backproject_count(const BackprojectArgs& a, uint32_t* blk_cnt, uint32_t* blk_off, uint32_t* total,
                               cudaStream_t st, int64_t* launches);
 void run_backproject_write(const BackprojectArgs& a, const uint32_t* blk_off, int64_t P_old, int64_t P_new, float* params,
-                           float* nu, uint8_t* observed, cudaStream_t st, int64_t* launches);
+                           double* nu, uint8_t* observed, cudaStream_t st, int64_t* launches);
 
 // uncert.cu
 void run_uncertainty_view(const Workspace& ws, const float* params, int64_t P, const float* obs, int W, int H,
                           double near_plane, double far_plane, const DevState* ds, double* sum, uint32_t* cnt,
                           cudaStream_t st, int64_t* launches);
-void run_uncertainty_finalize(const double* sum, const uint32_t* cnt, float* nu, uint8_t* observed, int64_t P,
+void run_uncertainty_finalize(const double* sum, const uint32_t* cnt, double* nu, uint8_t* observed, int64_t P,
                               uint32_t* observed_count, cudaStream_t st, int64_t* launches);
-void run_prune(const float* nu, float* opacity_logit, int64_t P, float tau, float target, uint32_t* reduced,
+void run_prune(const double* nu, float* opacity_logit, int64_t P, double tau, float target, uint32_t* reduced,
                cudaStream_t st, int64_t* launches);
 
 }  // namespace gsfk

@@ -18,8 +18,8 @@ namespace {
 constexpr int kAdamPer = 4;
 __global__ void __launch_bounds__(256) k_adam(float* __restrict__ params, const float* __restrict__ grads,
                                               float* __restrict__ m, float* __restrict__ v, int64_t P, AdamGroups g,
-                                              double bc1, double bc2) {
-  const int f = blockIdx.y;
+                                              double bc1, double bc2, int f0) {
+  const int f = f0 + static_cast<int>(blockIdx.y);
   const int grp = f < 3 ? 0 : (f < 6 ? 1 : (f < 10 ? 2 : (f < 11 ? 3 : 4)));
   const double lr = g.lr[grp];
   const int64_t base = static_cast<int64_t>(f) * P;
@@ -45,15 +45,19 @@ __global__ void k_track_update(DevState* ds, int iteration, double bc1, double b
 
 }  // namespace
 
-void run_adam(float* params, const float* grads, float* m, float* v, int64_t P, int D, const AdamGroups& g, double step,
-              cudaStream_t st, int64_t* L) {
-  const int64_t n = static_cast<int64_t>(D) * P;
-  if (n == 0) return;
+void run_adam_fields(float* params, const float* grads, float* m, float* v, int64_t P, int f0, int f1,
+                     const AdamGroups& g, double step, cudaStream_t st, int64_t* L) {
+  if (P == 0 || f1 <= f0) return;
   const double bc1 = 1.0 - std::pow(0.9, step);
   const double bc2 = 1.0 - std::pow(0.999, step);
-  const dim3 grid(static_cast<unsigned>(div_up(P, 256 * kAdamPer)), static_cast<unsigned>(D));
-  k_adam<<<grid, 256, 0, st>>>(params, grads, m, v, P, g, bc1, bc2);
+  const dim3 grid(static_cast<unsigned>(div_up(P, 256 * kAdamPer)), static_cast<unsigned>(f1 - f0));
+  k_adam<<<grid, 256, 0, st>>>(params, grads, m, v, P, g, bc1, bc2, f0);
   ++*L;
+}
+
+void run_adam(float* params, const float* grads, float* m, float* v, int64_t P, int D, const AdamGroups& g, double step,
+              cudaStream_t st, int64_t* L) {
+  run_adam_fields(params, grads, m, v, P, 0, D, g, step, st, L);
 }
 
 void run_track_update(DevState* ds, int iteration, cudaStream_t st, int64_t* L) {

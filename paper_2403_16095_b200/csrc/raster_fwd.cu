@@ -430,10 +430,12 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // pixel_accumulate (gsf_shared.cuh) with the colour / alpha-depth sums as two packed FFMA2s;
 // every lane rounds like __fmaf_rn, so the state equals the mirror's bit for bit.
+template <bool FLAG>
 __device__ __forceinline__ void full_accumulate(PixelState& s, float2& rg, float2& bd, const BlendG& g, const PairEval& e,
                                                 int32_t id, int32_t list_index, bool obs_valid, float obs,
                                                 const BlendConsts& k) {
   const float w = fmul(e.alpha, s.T);
+  if (FLAG) pixel_flag_step(s, e.alpha, e.clamped, w, fmul(s.T, fsub(1.0f, e.alpha)), k);
   const float2 ww = make_float2(w, w);
   rg = __ffma2_rn(ww, make_float2(g.r, g.g), rg);
   bd = __ffma2_rn(ww, make_float2(g.b, g.depth), bd);
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
                                                int32_t* __restrict__ o_dom, int32_t* __restrict__ o_med,
                                                float* __restrict__ o_domw, int32_t* __restrict__ o_last,
                                                double* __restrict__ loss_part, int fuse_final, int iteration,
-                                               uint32_t* ticket) {
+                                               uint32_t* ticket, uint32_t* __restrict__ fix_list, uint32_t* fix_cnt) {
   pdl_wait();   // PDL: the predecessor's results are complete from here
   pdl_trigger();
   __shared__ BlendG s_g[256];
@@ -525,7 +527,7 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
         if (s.done) continue;
         const BlendG g = s_g[k];
         const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
-        if (e.code) full_accumulate(s, frg, fbd, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+        if (e.code) full_accumulate<LMODE == 0>(s, frg, fbd, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
       }
     }
   }
@@ -548,6 +550,7 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
     o_dom[pi] = s.dominant;
     o_med[pi] = s.median;
     o_domw[pi] = s.best;
+    if (LMODE == 0 && s.flag) fix_list[atomicAdd(fix_cnt, 1u)] = static_cast<uint32_t>(pi);
   }
   if (LMODE == 0) return;
   // fused loss epilogue: per-tile residual sums and mask counts (deterministic tree)
@@ -572,6 +575,83 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
   (void)fuse_final;
   (void)iteration;
   (void)ticket;
+}
+
+// Exact-decision fix-up of the render API (gsf_shared.cuh: pixel_flag_step / exact_*): one warp
+// per flagged pixel re-blends its tile list in fp64 with the reference's formulas.  The lanes
+// evaluate 32 entries' decisions and alphas at once (exact_alpha from the fp64 guard copies); lane
+// 0 then accumulates them in list order (the reference's sequential rounding), and its results
+// replace the pixel's fp32 ones.  ~1e-5..1e-3 of the pixels of a frame are flagged.
+constexpr int kFixCtas = 296;
+__global__ void __launch_bounds__(256) k_pixel_fixup(
+    const uint32_t* __restrict__ fix_list, const uint32_t* fix_cnt, const int2* __restrict__ ranges,
+    const uint32_t* __restrict__ sid, const BlendG* __restrict__ bg, const GuardG* __restrict__ gg,
+    const float* __restrict__ obs, int W, int tiles_x, BlendConsts kc, double near_plane, double far_plane,
+    float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_md, uint8_t* __restrict__ o_mv,
+    float* __restrict__ o_op, float* __restrict__ o_unc, float* __restrict__ o_T, int32_t* __restrict__ o_count,
+    int32_t* __restrict__ o_dom, int32_t* __restrict__ o_med, float* __restrict__ o_domw, int32_t* __restrict__ o_last,
+    const DevState* ds) {
+  __shared__ double s_a[8][32];
+  __shared__ int32_t s_i[8][32];
+  pdl_wait();
+  pdl_trigger();
+  if (ds->halt) return;
+  const uint32_t n = *fix_cnt;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (uint32_t f = blockIdx.x * 8u + static_cast<uint32_t>(wib); f < n; f += gridDim.x * 8u) {
+    const uint32_t pi = fix_list[f];
+    const int x = static_cast<int>(pi % static_cast<uint32_t>(W)), y = static_cast<int>(pi / static_cast<uint32_t>(W));
+    const int2 rg = ranges[(y / kTile) * tiles_x + x / kTile];
+    const double px = static_cast<double>(static_cast<float>(x) + 0.5f), py = static_cast<double>(static_cast<float>(y) + 0.5f);
+    bool obs_valid = false;
+    double ov = 0.0;
+    if (obs) {
+      const float o = obs[pi];
+      const double d = o;
+      obs_valid = isfinite(d) && d > near_plane && d < far_plane;
+      ov = d;
+    }
+    ExactPixel q;
+    exact_init(q);
+    for (int c = rg.x; c < rg.y; c += 32) {
+      const int j = c + lane;
+      double a = 0.0;
+      int id = -1;
+      if (j < rg.y) {
+        id = static_cast<int>(sid[j]);
+        if (!exact_alpha(px, py, gg[id], kc, &a)) id = -1;
+      }
+      s_a[wib][lane] = a;
+      s_i[wib][lane] = id;
+      __syncwarp();
+      int done = 0;
+      if (lane == 0) {
+        const int cnt = min(32, rg.y - c);
+        for (int k = 0; k < cnt && !q.done; ++k)
+          if (s_i[wib][k] >= 0)
+            exact_accumulate(q, s_a[wib][k], bg[s_i[wib][k]], s_i[wib][k], c + k - rg.x, obs_valid, ov, kc);
+        done = q.done;
+      }
+      __syncwarp();
+      if (__shfl_sync(0xffffffffu, done, 0)) break;
+    }
+    if (lane == 0) {
+      o_color[3 * pi + 0] = static_cast<float>(q.cr);
+      o_color[3 * pi + 1] = static_cast<float>(q.cg);
+      o_color[3 * pi + 2] = static_cast<float>(q.cb);
+      o_ad[pi] = static_cast<float>(q.ad);
+      o_op[pi] = static_cast<float>(q.op);
+      o_T[pi] = static_cast<float>(q.T);
+      o_last[pi] = q.last;
+      o_md[pi] = static_cast<float>(q.med_depth);
+      o_mv[pi] = q.median >= 0 ? 1 : 0;
+      o_unc[pi] = static_cast<float>(q.unc);
+      o_count[pi] = q.count;
+      o_dom[pi] = q.dominant;
+      o_med[pi] = q.median;
+      o_domw[pi] = static_cast<float>(q.best);
+    }
+  }
 }
 
 // Tracking forward (the tracking loss's maps and its fused loss) with two pixels per lane: warp w of the
@@ -829,7 +909,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   ws.ranges, ws.sid, ws.bg_id, ws.gg_id, a.obs, loss_rgb, a.loss_depth, a.W, a.H,                                     \
       tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid, \
       ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w, ws.last, ws.loss_part, \
-      a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket
+      a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket, ws.fix_list, ws.bin_counters + kCntFixup
   if (pf) pf->begin(PROF_BLEND, st);
   ws.loss_rows = ntiles;
   if (a.lp.mode == 1 && loss_rgb) {   // tracking loss: colour, alpha depth, opacity, T, last; two pixels per lane
@@ -847,8 +927,15 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   }
   else if (a.lp.mode == 2 && loss_rgb)
     launch_pdl(k_blend<2>, dim3(ntiles), dim3(256), 0, st, GSF_BLEND_ARGS);
-  else
+  else {
     launch_pdl(k_blend<0>, dim3(ntiles), dim3(256), 0, st, GSF_BLEND_ARGS);
+    ++*L;
+    // the render API's exact discrete decisions: flagged pixels re-blended in fp64
+    launch_pdl(k_pixel_fixup, dim3(kFixCtas), dim3(256), 0, st, ws.fix_list, ws.bin_counters + kCntFixup, ws.ranges, ws.sid,
+               ws.bg_id, ws.gg_id, a.obs, a.W, tiles_x, a.kc, a.near_plane, a.far_plane, ws.color, ws.alpha_depth,
+               ws.median_depth, ws.median_valid, ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant,
+               ws.median_prim, ws.dominant_w, ws.last, ds);
+  }
 #undef GSF_BLEND_ARGS
   ++*L;
   if (pf) pf->end(st);

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(1024) k_bp_scan(const uint32_t* __restrict__ c
 }
 
 __global__ void __launch_bounds__(256) k_bp_write(BackprojectArgs a, const uint32_t* __restrict__ blk_off, int64_t P_old,
-                                                  int64_t P_new, float* __restrict__ params, float* __restrict__ nu,
+                                                  int64_t P_new, float* __restrict__ params, double* __restrict__ nu,
                                                   uint8_t* __restrict__ observed) {
   __shared__ uint32_t s_w[8];
   const int64_t cell = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) k_bp_write(BackprojectArgs a, const uint3
   for (int c = 0; c < 3; ++c)
     params[(11 + c) * P_new + i] = static_cast<float>((static_cast<double>(rgb[c]) - 0.5) / 0.28209479177387814);
   for (int k = 3; k < 3 * a.K; ++k) params[(11 + k) * P_new + i] = 0.0f;
-  nu[i] = 0.0f;
+  nu[i] = 0.0;
   observed[i] = 1;
 }
 
@@ -126,7 +126,7 @@ int64_t run_backproject_count(const BackprojectArgs& a, uint32_t* blk_cnt, uint3
 }
 
 void run_backproject_write(const BackprojectArgs& a, const uint32_t* blk_off, int64_t P_old, int64_t P_new, float* params,
-                           float* nu, uint8_t* observed, cudaStream_t st, int64_t* L) {
+                           double* nu, uint8_t* observed, cudaStream_t st, int64_t* L) {
   const int blocks = std::max(1, div_up(a.cells, 256));
   k_bp_write<<<blocks, 256, 0, st>>>(a, blk_off, P_old, P_new, params, nu, observed);
   ++*L;

@@ -28,12 +28,12 @@ __global__ void k_uncert_view(const int32_t* __restrict__ dominant, const float*
   atomicAdd(&cnt[owner], 1u);
 }
 
-__global__ void k_uncert_finalize(const double* __restrict__ sum, const uint32_t* __restrict__ cnt, float* __restrict__ nu,
+__global__ void k_uncert_finalize(const double* __restrict__ sum, const uint32_t* __restrict__ cnt, double* __restrict__ nu,
                                   uint8_t* __restrict__ observed, int64_t P, uint32_t* observed_count) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= P) return;
   if (cnt[i] > 0) {
-    nu[i] = static_cast<float>(sum[i] / cnt[i]);
+    nu[i] = sum[i] / cnt[i];
     observed[i] = 1;
     atomicAdd(observed_count, 1u);
   } else {
@@ -41,7 +41,7 @@ __global__ void k_uncert_finalize(const double* __restrict__ sum, const uint32_t
   }
 }
 
-__global__ void k_prune(const float* __restrict__ nu, float* __restrict__ opacity_logit, int64_t P, float tau, float target,
+__global__ void k_prune(const double* __restrict__ nu, float* __restrict__ opacity_logit, int64_t P, double tau, float target,
                         uint32_t* reduced) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= P) return;
@@ -62,14 +62,14 @@ void run_uncertainty_view(const Workspace& ws, const float* params, int64_t P, c
   ++*L;
 }
 
-void run_uncertainty_finalize(const double* sum, const uint32_t* cnt, float* nu, uint8_t* observed, int64_t P,
+void run_uncertainty_finalize(const double* sum, const uint32_t* cnt, double* nu, uint8_t* observed, int64_t P,
                               uint32_t* observed_count, cudaStream_t st, int64_t* L) {
   if (P <= 0) return;
   k_uncert_finalize<<<div_up(P, 256), 256, 0, st>>>(sum, cnt, nu, observed, P, observed_count);
   ++*L;
 }
 
-void run_prune(const float* nu, float* opacity_logit, int64_t P, float tau, float target, uint32_t* reduced, cudaStream_t st,
+void run_prune(const double* nu, float* opacity_logit, int64_t P, double tau, float target, uint32_t* reduced, cudaStream_t st,
                int64_t* L) {
   if (P <= 0) return;
   k_prune<<<div_up(P, 256), 256, 0, st>>>(nu, opacity_logit, P, tau, target, reduced);

@@ -66,7 +66,8 @@ def axis_primitive(z, opacity, color):
 def f32_round(m):
     """Round every parameter to the nearest fp32 so the fp64 oracle and the fp32 device map
     start from identical values (the device stores the map as fp32 SoA)."""
-    out = SimpleNamespace(**{k: (np.asarray(v, np.float32).astype(np.float64) if np.asarray(v).dtype == np.float64 else v.copy())
+    out = SimpleNamespace(**{k: (np.asarray(v, np.float32).astype(np.float64) if np.asarray(v).dtype == np.float64
+                                 else (v.copy() if isinstance(v, np.ndarray) else v))
                              for k, v in vars(m).items()})
     return out
 
@@ -103,3 +104,33 @@ def perturbed(p: Pose, d):
 
 
 RASTER = defaults_raster
+
+
+def mt19937_uniform(seed, lo, hi, n):
+    """n draws of std::uniform_real_distribution<double>(lo, hi) from std::mt19937(seed) as
+    libstdc++ computes them (generate_canonical<double, 53>: two 32-bit outputs, low first)."""
+    bg = np.random.MT19937()
+    bg._legacy_seeding(seed)
+    x = bg.random_raw(2 * n).astype(np.float64)
+    r = (x[0::2] + x[1::2] * 4294967296.0) / 18446744073709551616.0
+    r = np.where(r >= 1.0, np.nextafter(1.0, 0.0), r)
+    return r * (hi - lo) + lo
+
+
+def textured_wall(nx, ny, seed):
+    """test_tracker.cpp:62-84 (textured_wall with std::mt19937(seed)) draw for draw; the three colour
+    draws of a primitive land in Vec3(uc, uc, uc) right to left, as GCC evaluates the arguments."""
+    P = nx * ny
+    m = scene([])
+    jj, ii = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    x = -1.4 + 2.8 * (ii.ravel() + 0.5) / nx
+    y = -1.0 + 2.0 * (jj.ravel() + 0.5) / ny
+    m.mean = np.stack([x, y, 2.5 + 0.15 * np.sin(2.0 * x) * np.cos(3.0 * y)], 1)
+    m.log_scale = np.full((P, 3), math.log(0.09))
+    m.quat = np.tile([1.0, 0, 0, 0], (P, 1))
+    m.opacity_logit = np.full(P, logit(0.95))
+    u = mt19937_uniform(seed, -0.8, 0.8, 3 * P).reshape(P, 3)
+    m.sh = u[:, ::-1].reshape(P, 1, 3).copy()
+    m.uncertainty = np.zeros(P)
+    m.observed = np.zeros(P, np.uint8)
+    return m

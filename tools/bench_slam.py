@@ -27,7 +27,8 @@ def main():
     nframes = int(sys.argv[1]) if len(sys.argv) > 1 else 91
     K = bench.intrinsics()
     truth, _ = bench.build_scene(500000)
-    poses = api.synth_orbit(1440, 1.0, 0.0)
+    from tools import synth
+    poses = [api.pose_of(r, t) for r, t in synth.orbit(1440, 1.0, 0.0)]
     gen = api.Context(0)
     gen.upload(truth)
     frames = []

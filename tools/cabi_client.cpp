@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "gsf_cuda.h"
+#include "../tools/synth/gsf_synth.h"   // scene generator (tools, not the product)
 
 #define CHECK(call)                                                                          \
   do {                                                                                       \

@@ -10,7 +10,7 @@
 #include <random>
 #include <vector>
 
-#include "../../include/gsf_cuda.h"   // gsf_map_host / gsf_pose layouts only
+#include "gsf_synth.h"
 
 namespace {
 
