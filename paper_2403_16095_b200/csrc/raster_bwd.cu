@@ -684,6 +684,14 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   }
 }
 
+// The chain ADDS each primitive's bundle into the gradient buffer (GradientBundle::add,
+// output.cpp:36-48): callers zero it once, and a sliding_ba window sums its keyframes' bundles in
+// window order (tracker.cpp:164) before the single optimizer step.  One thread owns a primitive's
+// entries, so the read-modify-write is race-free and the order is fixed.
+__device__ __forceinline__ void acc_grad(float* __restrict__ g, int64_t i, double v) {
+  g[i] = static_cast<float>(static_cast<double>(g[i]) + v);
+}
+
 // SH basis gradients (sh.cpp:44-72), fp64.
 __device__ void sh_basis_grad(int degree, double x, double y, double z, double* g /*16*3*/) {
   const double C1 = 0.4886025119029199;
@@ -739,7 +747,7 @@ static __device__ __noinline__ void sh_backward(const float* __restrict__ params
   }
   if (grads)
     for (int k = 0; k < K; ++k)
-      for (int c = 0; c < 3; ++c) grads[(11 + 3 * k + c) * P + id] = static_cast<float>(b[k] * masked[c]);
+      for (int c = 0; c < 3; ++c) acc_grad(grads, (11 + 3 * k + c) * P + id, b[k] * masked[c]);
   through[0] = through[1] = through[2] = 0.0;
   if (deg >= 1 && len > 1e-12) {
     double gb[48];
@@ -900,18 +908,18 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
         // degree 0: colour_c = max(0.5 + C0 sh_c, 0), no view-direction gradient (sh.cpp:88-108)
         for (int c = 0; c < 3; ++c) {
           const double raw = 0.5 + 0.28209479177387814 * params[(11 + c) * P + id];
-          grads[(11 + c) * P + id] = static_cast<float>(raw < 0.0 ? 0.0 : 0.28209479177387814 * dcol[c]);
+          acc_grad(grads, (11 + c) * P + id, raw < 0.0 ? 0.0 : 0.28209479177387814 * dcol[c]);
         }
       } else if (K > 1) {
         sh_backward(params, P, id, K, cam, m0, m1, m2, dcol, FULL ? grads : nullptr, through);
         for (int a = 0; a < 3; ++a) pose[3 + a] += Wr[3 * a + 0] * through[0] + Wr[3 * a + 1] * through[1] + Wr[3 * a + 2] * through[2];
       }
       if (FULL) {
-        if (d_mean2d) { d_mean2d[id] = static_cast<float>(sg[0]); d_mean2d[P + id] = static_cast<float>(sg[1]); }
+        if (d_mean2d) { acc_grad(d_mean2d, id, sg[0]); acc_grad(d_mean2d, P + id, sg[1]); }
         // world parameters (rasterizer.cpp:528-546)
         for (int a = 0; a < 3; ++a) {
           const double dm = Wr[0 * 3 + a] * dp[0] + Wr[1 * 3 + a] * dp[1] + Wr[2 * 3 + a] * dp[2] + through[a];
-          grads[a * P + id] = static_cast<float>(dm);
+          acc_grad(grads, a * P + id, dm);
         }
         double dCw[3][3], T2[3][3];
         for (int a = 0; a < 3; ++a)
@@ -924,7 +932,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
             dM[a][b] = 2.0 * (dCw[a][0] * R[0][b] * s[b] + dCw[a][1] * R[1][b] * s[b] + dCw[a][2] * R[2][b] * s[b]);
         for (int a = 0; a < 3; ++a) {
           const double ds_ = R[0][a] * dM[0][a] + R[1][a] * dM[1][a] + R[2][a] * dM[2][a];
-          grads[(3 + a) * P + id] = static_cast<float>(ds_ * s[a]);
+          acc_grad(grads, (3 + a) * P + id, ds_ * s[a]);
         }
         double dR[3][3];
         for (int a = 0; a < 3; ++a)
@@ -942,9 +950,9 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
           dqn[kq] = acc;
         }
         const double qd = qn[0] * dqn[0] + qn[1] * dqn[1] + qn[2] * dqn[2] + qn[3] * dqn[3];
-        for (int a = 0; a < 4; ++a) grads[(6 + a) * P + id] = static_cast<float>((dqn[a] - qn[a] * qd) / qlen);
+        for (int a = 0; a < 4; ++a) acc_grad(grads, (6 + a) * P + id, (dqn[a] - qn[a] * qd) / qlen);
         const double sig = 1.0 / (1.0 + exp(-static_cast<double>(params[10 * P + id])));
-        grads[10 * P + id] = static_cast<float>((NF >= 10 ? sg[9] : 0.0) * sig * (1.0 - sig));
+        acc_grad(grads, 10 * P + id, (NF >= 10 ? sg[9] : 0.0) * sig * (1.0 - sig));
       }
     }
   }
