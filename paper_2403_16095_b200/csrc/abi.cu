@@ -317,7 +317,7 @@ void ensure_map(gsf_ctx_s* c, int64_t P, int K) {
 void alloc_pairs(Workspace& ws) {
 
   dalloc(ws.skey, ws.pair_cap); dalloc(ws.sid, ws.pair_cap);
-  dalloc(ws.sslot, ws.pair_cap); dalloc(ws.emask, ws.pair_cap);
+  dalloc(ws.sslot, ws.pair_cap); dalloc(ws.emask, 4 * ws.pair_cap);
   dalloc(ws.partials, ws.pair_cap * 10);
 }
 
@@ -357,6 +357,9 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
     ws.bin_counters = ws.bins + tiles * kBinStride;
     dfree(ws.bucket);
     dalloc(ws.loss_part, (5 * tiles + 64) * LS_NUM);
+    dalloc(ws.order, 2 * (1 + 5 * tiles));
+    dalloc(ws.qstat, 4 * tiles);
+    GSF_CUDA_CHECK(cudaMemsetAsync(ws.order, 0, sizeof(uint32_t) * 2 * (1 + 5 * tiles), c->stream));
     ws.tiles_cap = tiles;
     dfree(ws.pose_part);
   }
@@ -706,6 +709,9 @@ int gsf_ctx_create(int device, gsf_ctx* out) {
     GSF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->ws.side, cudaStreamNonBlocking));
     GSF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ws.ev_fork, cudaEventDisableTiming));
     GSF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ws.ev_join, cudaEventDisableTiming));
+    GSF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->ws.side2, cudaStreamNonBlocking));
+    GSF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ws.ev_lfork, cudaEventDisableTiming));
+    GSF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ws.ev_ljoin, cudaEventDisableTiming));
     g_alloc_stream = c->stream;
     keep_pool_memory(device);
     dalloc(c->ds, 1);
@@ -732,7 +738,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
   void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
-                  ws.last, ws.pxcode, ws.fix_list, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
+                  ws.last, ws.pxcode, ws.fix_list, ws.order, ws.qstat, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
                   ws.red_part, c->bp_scratch, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
                   c->red_f, c->ba_pack};
@@ -756,6 +762,9 @@ int gsf_ctx_destroy(gsf_ctx c) {
   if (ws.ev_fork) cudaEventDestroy(ws.ev_fork);
   if (ws.ev_join) cudaEventDestroy(ws.ev_join);
   if (ws.side) cudaStreamDestroy(ws.side);
+  if (ws.ev_lfork) cudaEventDestroy(ws.ev_lfork);
+  if (ws.ev_ljoin) cudaEventDestroy(ws.ev_ljoin);
+  if (ws.side2) cudaStreamDestroy(ws.side2);
   cudaStreamDestroy(c->stream);
   delete c;
   return GSF_OK;
@@ -1214,9 +1223,14 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
   // primitives that can be visible while the camera stays within kTrustTheta / kTrustDist of the
   // starting pose; the iterations preprocess only those until a step leaves the region
   run_candidates(c->ws, c->ds, c->params, c->P, make_rp(c, k, rcfg), kTrustTheta, kTrustDist, c->stream, &c->launches);
+  Workspace& ws = c->ws;
+  const int64_t obuf = 1 + 5 * ws.tiles_cap;   // one Workspace::order half
   for (int it = 0; it < tcfg.iterations; ++it) {
     FwdArgs fa = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, it);
     fa.cand = c->ws.cand;
+    // longest-first CTA order from the previous iteration's counts (any order gives the same bits)
+    fa.order = ws.order + (it & 1) * obuf;
+    fa.join_order = it > 0;
     fa.want_posejac = true;
     // the two-pixel pose backward (K == 1) reads T, last and the seed signs only; the view-dependent
     // pose backward (k_backward_pose<SEED_TRACK, true>) derives its seeds from the maps
@@ -1230,13 +1244,21 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
     BwdArgs b = bwd_args(c, k, rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);
     b.fused_pose = true;
     b.update_iter = it;
+    b.order = fa.order;
     if (!run_backward(c->ws, c->ds, b, c->stream, &c->launches)) run_track_update(c->ds, it, c->stream, &c->launches);
+    // the next iteration's orders on the second side branch, beside the next preprocess and binning
+    GSF_CUDA_CHECK(cudaEventRecord(ws.ev_lfork, c->stream));
+    GSF_CUDA_CHECK(cudaStreamWaitEvent(ws.side2, ws.ev_lfork, 0));
+    run_lpt(ws, tiles, ws.order + ((it + 1) & 1) * obuf, ws.side2, &c->launches);
+    GSF_CUDA_CHECK(cudaEventRecord(ws.ev_ljoin, ws.side2));
   }
   // final render + loss without gradients (tracker.cpp:74-76)
   FwdArgs fin = fwd_args(c, k, rcfg, nullptr, f.rgb, f.depth, lp, -1);
   fin.fuse_loss_final = true;
   fin.use_world = true;
   fin.want_pair_base = false;
+  fin.order = ws.order + (tcfg.iterations & 1) * obuf;
+  fin.join_order = tcfg.iterations > 0;   // also rejoins the k_lpt branch before the capture ends
   run_forward(c->ws, c->ds, fin, c->stream, &c->launches);
   (void)tiles;
   (void)npix;

@@ -178,6 +178,10 @@ __device__ __forceinline__ float2 exp_neg_half_inrange2(float2 rho) {
   const float2 y = __fmul2_rn(rho, make_float2(-0.72134752044448170368f, -0.72134752044448170368f));
   const float nx = rintf(y.x), ny = rintf(y.y);
   const float2 f = __fadd2_rn(y, make_float2(-nx, -ny));   // y - n, exactly fsub's result
+  // 2^n without F2I (XU pipe): n + 1.5 * 2^23 is exact for the integer n, and the low 9 bits of its
+  // pattern are n's, so (bits(t) << 23) + (127 << 23) is 2^n's pattern.  (y itself must not meet
+  // the magic constant: ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into one FFMA2.)
+  const float2 t = __fadd2_rn(make_float2(nx, ny), make_float2(12582912.0f, 12582912.0f));
   float2 p = make_float2(1.5403530393381606e-4f, 1.5403530393381606e-4f);
   p = __ffma2_rn(p, f, make_float2(1.3333558146428443e-3f, 1.3333558146428443e-3f));
   p = __ffma2_rn(p, f, make_float2(9.6181291076284772e-3f, 9.6181291076284772e-3f));
@@ -185,8 +189,8 @@ __device__ __forceinline__ float2 exp_neg_half_inrange2(float2 rho) {
   p = __ffma2_rn(p, f, make_float2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
   p = __ffma2_rn(p, f, make_float2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
   p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
-  return __fmul2_rn(p, make_float2(__int_as_float((127 + static_cast<int>(nx)) << 23),
-                                   __int_as_float((127 + static_cast<int>(ny)) << 23)));
+  return __fmul2_rn(p, make_float2(__uint_as_float((__float_as_uint(t.x) << 23) + 0x3f800000u),
+                                   __uint_as_float((__float_as_uint(t.y) << 23) + 0x3f800000u)));
 }
 
 // Loss partial slots written per tile by the fused blend epilogue (fixed order reduction).

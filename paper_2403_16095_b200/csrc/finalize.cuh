@@ -65,15 +65,15 @@ __device__ __forceinline__ bool last_cta(uint32_t* counter, int* s_flag, bool wr
 }
 
 // Two-level fixed-order reduction for grids of single-warp CTAs (blockDim.x == 32): CTA r wrote
-// row part[r][NV].  The last CTA of each group of 32 consecutive rows sums the group (lane l takes
+// row part[r][NV] (r = row, default blockIdx.x).  The last CTA of each group of 32 consecutive rows sums the group (lane l takes
 // row l, then a fixed shuffle tree) into gpart[g]; the last group sums gpart the same way.  Returns
 // true in exactly one CTA, whose lane 0 then holds the totals in out[NV].  gt[] (one ticket per
 // group) and *top must be zero before the launch; they are re-zeroed here.
 template <int NV>
 __device__ __forceinline__ bool warp_grid_reduce(const double* part, double* gpart, int rows, uint32_t* gt, uint32_t* top,
-                                                 double* out, bool wrote) {
+                                                 double* out, bool wrote, int row = -1) {
   const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x, g = r >> 5, g0 = g << 5, gn = min(32, rows - g0);
+  const int r = row >= 0 ? row : static_cast<int>(blockIdx.x), g = r >> 5, g0 = g << 5, gn = min(32, rows - g0);
   const int ngroups = (rows + 31) >> 5;
   if (wrote) __threadfence();
   __syncwarp();

@@ -60,13 +60,21 @@ struct Workspace {
   // before the blend); created with the context
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // tracking: longest-first CTA order of the tile kernels (k_lpt, from the previous iteration's
+  // per-quadrant step counts) on a second side branch: fork after the backward, join before the
+  // next blend.  Two buffers of [1 + 5 tiles_cap]: [0] = the tile count the orders were built for
+  // (0 = none: identity order), then the blend's tile order, then the backward's quadrant order.
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_lfork = nullptr, ev_ljoin = nullptr;
+  uint32_t* order = nullptr;    // 2 * (1 + 5 tiles_cap)
+  int2* qstat = nullptr;        // 4 tiles_cap: per (tile, quadrant) forward steps, entries taken
   // per primitive, id-indexed (written by k_preprocess for the visible ones)
   BlendG* bg_id = nullptr;
   GuardG* gg_id = nullptr;
   BlendG* bg_slot = nullptr;   // tracking: the same records indexed by visible slot (compact)
   GuardG* gg_slot = nullptr;
   uint32_t* sslot = nullptr;   // tracking: tile lists as visible slots (beside sid)
-  uint8_t* emask = nullptr;    // tracking: per list entry, the 8x8 blocks of its tile it can reach (k_blend_track)
+  uint8_t* emask = nullptr;    // tracking: 4 planes of pair_cap bytes, plane q = the entries some pixel of 8x8 block q took (k_blend_track)
   uint32_t* cand = nullptr;    // tracking: trust-region candidate ids (k_candidates)
   double* depth_id = nullptr;
   int4* rect_id = nullptr;
@@ -147,6 +155,8 @@ struct FwdArgs {
   bool use_world = false;        // preprocess from ws.world / ws.support (run_world ran for this map)
   const uint32_t* cand = nullptr;  // tracking: candidate ids (run_candidates), used while ds->cand_ok
   bool want_pair_base = true;    // primitive-major pair slots for a parameter-gradient backward
+  const uint32_t* order = nullptr;  // tracking: CTA order buffer (Workspace::order half) of the blend
+  bool join_order = false;          // wait for the k_lpt branch (ws.ev_ljoin) before the blend
 };
 void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st, int64_t* launches);
 // per-primitive validation + view-independent cache (ws.world, ws.support)
@@ -155,6 +165,8 @@ void run_world(Workspace& ws, DevState* ds, const float* params, int64_t P, cons
 // trust-region candidate list of the tracking loop (once per frame, after run_world, at its first camera)
 void run_candidates(Workspace& ws, DevState* ds, const float* params, int64_t P, const RasterParams& rp,
                     double theta_max, double dist_max, cudaStream_t st, int64_t* launches);
+// tracking: longest-first CTA orders for the next iteration (ws.qstat -> out, a Workspace::order half)
+void run_lpt(Workspace& ws, int ntiles, uint32_t* out, cudaStream_t st, int64_t* launches);
 void run_loss_tiles(Workspace& ws, int mode, const float* rgb, const float* depth, bool has_unc, int W, int H,
                     double near_plane, double far_plane, float floor, cudaStream_t st, int64_t* launches);
 
@@ -180,6 +192,7 @@ struct BwdArgs {
   bool pose_only;            // tracking: skip per-primitive parameter gradients
   bool fused_pose = false;   // pose_only + ws.pj_id valid: pose through per-primitive Jacobians
   int update_iter = -1;      // >= 0: the tracking backward's last CTA also takes this iteration's pose step
+  const uint32_t* order = nullptr;  // tracking: CTA order buffer (Workspace::order half) of the pose backward
   float* grads;              // [D][P] parameter gradients (full mode)
   float* d_mean2d;           // [2][P] (full mode, nullable)
 };

@@ -102,7 +102,9 @@ struct BwdPtrs {
   const uint32_t* pj_slot;  // id -> slot in pj (position in the visible list)
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
   const uint32_t* sslot;    // tracking: tile lists as visible slots
-  const uint8_t* emask;     // tracking: per entry, the 8x8 blocks it can reach (k_blend_track)
+  const uint8_t* emask;     // tracking: 4 planes (8x8 block q of the tile) x emask_plane entries: 1 if some
+                            // pixel of the block took the entry in the forward (k_blend_track)
+  int64_t emask_plane;
   const uint8_t* pxcode;    // tracking: per pixel, the seed signs (pixel_seed_code, k_blend_track)
   const BlendG* bg_slot;    // tracking: records by visible slot
   const GuardG* gg_slot;
@@ -517,7 +519,8 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
                                                                       BlendConsts kc, double near_plane,
                                                                       double far_plane, LossParams lp, DevState* ds,
                                                                       uint32_t* gtickets, int rows, int upd_iter,
-                                                                      double bc1, double bc2) {
+                                                                      double bc1, double bc2, const uint32_t* __restrict__ order,
+                                                                      int64_t tiles_cap) {
   // one staging buffer: 32 records (3 float4), 32 pose matrices (9 float4), 32 slots
   // two staging buffers of 16 entries: records (3 float4) at +0, pose matrices (9 float4) at +768 B;
   // their slots at 6144 + 64 b
@@ -526,7 +529,10 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   pdl_trigger();
   const int lane = threadIdx.x;
   const uint32_t sb = opaque_smem_base(s_buf);
-  const int tile = blockIdx.x >> 2, qd = blockIdx.x & 3;
+  // (tile, quadrant) item in longest-first order (k_lpt; identity when the order is for another grid)
+  const int item = (order && 4u * order[0] == gridDim.x) ? static_cast<int>(order[1 + tiles_cap + blockIdx.x])
+                                                         : static_cast<int>(blockIdx.x);
+  const int tile = item >> 2, qd = item & 3;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x = tx * kTile + 8 * (qd & 1) + (lane & 7);
   const int ya = ty * kTile + 8 * (qd >> 1) + (lane >> 3), yb = ya + 4;
@@ -556,7 +562,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       if (c < nch) {
         const int lo = max(rg.x, E - kC * (c + 1)), hi = E - kC * c;
         if (lane < hi - lo) {
-          m = (__ldg(bp.emask + lo + lane) >> qd) & 1u;
+          m = __ldg(bp.emask + qd * bp.emask_plane + lo + lane);
           sl = __ldg(bp.sslot + lo + lane);
         }
       }
@@ -673,10 +679,10 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   for (int a = 0; a < 6; ++a) pd[a] = warp_sum_f64(pd[a]);
   if (lane == 0)
 #pragma unroll
-    for (int a = 0; a < 6; ++a) bp.tile_pose[static_cast<size_t>(blockIdx.x) * 6 + a] = pd[a];
+    for (int a = 0; a < 6; ++a) bp.tile_pose[static_cast<size_t>(item) * 6 + a] = pd[a];
   double tot[6];
   if (warp_grid_reduce<6>(bp.tile_pose, bp.tile_pose + static_cast<size_t>(rows) * 6, rows, gtickets,
-                          gtickets + (rows + 31) / 32, tot, lane == 0) && lane == 0) {
+                          gtickets + (rows + 31) / 32, tot, lane == 0, item) && lane == 0) {
 #pragma unroll
     for (int a = 0; a < 6; ++a) ds->d_pose[a] = ds->halt ? 0.0 : tot[a];
     // the iteration's pose step (k_track_update) in the same CTA: one kernel boundary less
@@ -1054,6 +1060,7 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.tile_pose = nullptr;
   bp.sslot = ws.sslot;
   bp.emask = ws.emask;
+  bp.emask_plane = ws.pair_cap;
   bp.pxcode = ws.pxcode;
   bp.bg_slot = ws.bg_slot;
   bp.gg_slot = ws.gg_slot;
@@ -1083,7 +1090,8 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
       const double t = static_cast<double>(a.update_iter + 1);   // AdamState bias corrections (adam.cpp:40-53)
       launch_pdl(k_backward_track_w, dim3(4 * ntiles), dim3(32), 0, st, bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
                                                      ws.wtickets + ws.wtickets_half, 4 * ntiles, a.update_iter,
-                                                     1.0 - std::pow(0.9, t), 1.0 - std::pow(0.999, t));
+                                                     1.0 - std::pow(0.9, t), 1.0 - std::pow(0.999, t), a.order,
+                                                     static_cast<int64_t>(ws.tiles_cap));
       fused_update = a.update_iter >= 0;
     } else if (a.seed_mode == SEED_TRACK) {
       GSF_BWDP(SEED_TRACK, true);

@@ -673,7 +673,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     int tiles_x, BlendConsts kc, double near_plane, double far_plane, LossParams lp, DevState* ds,
     float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_op, float* __restrict__ o_T,
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
-    uint8_t* __restrict__ emask, uint8_t* __restrict__ o_code, uint32_t* clean_bins, int64_t clean_cnt_off) {
+    uint8_t* __restrict__ emask, int64_t emask_plane, uint8_t* __restrict__ o_code, uint32_t* clean_bins,
+    int64_t clean_cnt_off, const uint32_t* __restrict__ order, int2* __restrict__ qstat) {
   __shared__ BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
@@ -689,9 +690,11 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     }
   }
   if (ds->halt) return;
-  const int tile = blockIdx.x;
+  // longest-first CTA order (k_lpt; order[0] = the tile count it was built for, else identity)
+  const int tile = (order && order[0] == gridDim.x) ? static_cast<int>(order[1 + blockIdx.x]) : blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t sgb = opaque_smem_base(s_g);
+  uint32_t wsteps = 0u, wtaken = 0u;   // this warp's walked steps and taken entries (k_lpt's costs)
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x = tx * kTile + 8 * (warp & 1) + (lane & 7);
   const int ya = ty * kTile + 8 * (warp >> 1) + (lane >> 3), yb = ya + 4;
@@ -701,8 +704,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   // a pixel is done once T < term (T never grows); pixels outside the image start done (T = 0)
   float2 op = make_float2(0.f, 0.f), T = make_float2(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);
   int last_a = 0, last_b = 0;
-  const float px = static_cast<float>(x) + 0.5f;
-  const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
+  float px = static_cast<float>(x) + 0.5f;
+  float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
   const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
   for (int start = rg.x; start < rg.y; start += kTrkBatch) {
     if (__syncthreads_and(T.x < kc.term && T.y < kc.term)) break;
@@ -716,7 +719,6 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         s_id[e] = id;
         const uint8_t mk = static_cast<uint8_t>(warp_block_mask8(gj, tile_x0, tile_y0, kc));
         s_mask[e] = mk;
-        if (emask) emask[j] = mk;   // the pose backward's block test
       }
     }
     __syncthreads();
@@ -725,9 +727,17 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       if (__all_sync(0xffffffffu, T.x < kc.term && T.y < kc.term)) break;
       const int kk = c0 + lane;
       uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
+      uint32_t took = 0u;   // this lane's pixels took entry c0 + b (bit b)
+      wsteps += __popc(bits);
       while (bits) {
         const int k = c0 + __ffs(bits) - 1;
+        const uint32_t kbit = bits & (0u - bits);
         bits &= bits - 1u;
+#ifndef GSF_NO_PIN_PX
+        // keep the pixel centres in registers: at the 64-register cap ptxas otherwise re-forms
+        // them with I2F + FADD (XU pipe) on every step
+        asm volatile("" : "+f"(px), "+f"(py.x), "+f"(py.y));
+#endif
         const BlendG g = lds_blend(sgb + 48u * k);
         const float dx = __fadd_rn(px, -g.mx);
         const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
@@ -756,9 +766,18 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         const int li = start + k - rg.x + 1;
         if (ca) last_a = li;
         if (cb) last_b = li;
+        if (ca || cb) took |= kbit;
+      }
+      // the pose backward walks only the entries some pixel of its block took: every entry up to
+      // the block's last contributor has been walked here, so no stale byte is ever read
+      if (emask) {
+        took = __reduce_or_sync(0xffffffffu, took);
+        wtaken += __popc(took);
+        if (kk < cnt) emask[warp * emask_plane + start + kk] = static_cast<uint8_t>((took >> lane) & 1u);
       }
     }
   }
+  if (qstat && lane == 0) qstat[tile * 4 + warp] = make_int2(static_cast<int>(wsteps), static_cast<int>(wtaken));
   double v[LS_NUM], vb[LS_NUM];
 #pragma unroll
   for (int q = 0; q < LS_NUM; ++q) v[q] = vb[q] = 0.0;
@@ -916,14 +935,16 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     // with pose Jacobians (a pose backward follows) the lists and records are read by visible slot
     // and the entries' block masks are kept for the backward
     const bool sl = a.want_posejac;
+    if (a.join_order) GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_ljoin, 0));
     launch_pdl(k_blend_track, dim3(ntiles), dim3(kTrkThreads), 0, st, ws.ranges, sl ? ws.sslot : ws.sid, sl ? ws.bg_slot : ws.bg_id,
                                                   sl ? ws.gg_slot : ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,
                                                   tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
                                                   a.keep_maps ? ws.color : nullptr, ws.alpha_depth, ws.opacity, ws.final_T,
                                                   ws.last, ws.loss_part,
                                                   a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket,
-                                                  sl ? ws.emask : nullptr, sl ? ws.pxcode : nullptr,
-                                                  a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride);
+                                                  sl ? ws.emask : nullptr, ws.pair_cap, sl ? ws.pxcode : nullptr,
+                                                  a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride,
+                                                  a.order, sl ? ws.qstat : nullptr);
   }
   else if (a.lp.mode == 2 && loss_rgb)
     launch_pdl(k_blend<2>, dim3(ntiles), dim3(256), 0, st, GSF_BLEND_ARGS);
@@ -940,6 +961,80 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   ++*L;
   if (pf) pf->end(st);
   (void)tiles_y;
+}
+
+// Longest-first CTA orders for the tracking loop's tile kernels.  The hardware hands CTAs to SMs
+// roughly in blockIdx order, so a grid whose long tiles come last ends with a few SMs finishing
+// them while the rest idle (ncu: the average SM active 83-86 % of the kernel).  From the previous
+// iteration's per-(tile, quadrant) counts (the lists change little between iterations) one CTA
+// counting-sorts the tiles by forward steps and the (tile, quadrant) items by entries taken (the
+// pose backward's steps), longest first.  Only the dispatch order changes: every CTA still writes
+// its tile's rows, and the reductions over them run in tile order.
+constexpr int kLptThreads = 1024, kLptBuckets = 2048;
+__global__ void __launch_bounds__(kLptThreads) k_lpt(const int2* __restrict__ qstat, int ntiles, uint32_t* __restrict__ out,
+                                                    int64_t tiles_cap) {
+  __shared__ uint32_t hist[kLptBuckets];
+  __shared__ uint32_t s_wsum[kLptThreads / 32];
+  __shared__ uint32_t s_max;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int n = pass == 0 ? ntiles : 4 * ntiles;
+    uint32_t* ord = out + 1 + (pass == 0 ? 0 : tiles_cap);
+    auto key = [&](int i) -> uint32_t {
+      if (pass == 0) {
+        const int2 a = qstat[4 * i], b = qstat[4 * i + 1], c = qstat[4 * i + 2], d = qstat[4 * i + 3];
+        return static_cast<uint32_t>(max(a.x, 0) + max(b.x, 0) + max(c.x, 0) + max(d.x, 0));
+      }
+      return static_cast<uint32_t>(max(qstat[i].y, 0));
+    };
+    for (int b = tid; b < kLptBuckets; b += kLptThreads) hist[b] = 0u;
+    if (tid == 0) s_max = 1u;
+    __syncthreads();
+    uint32_t m = 0u;
+    for (int i = tid; i < n; i += kLptThreads) m = max(m, key(i));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) atomicMax(&s_max, m);
+    __syncthreads();
+    const uint64_t mx = s_max;
+    // bucket kLptBuckets-1-q for quantised cost q: ascending bucket index = descending cost
+    auto bucket = [&](uint32_t k) {
+      return kLptBuckets - 1 - static_cast<int>((static_cast<uint64_t>(k) * (kLptBuckets - 1)) / mx);
+    };
+    for (int i = tid; i < n; i += kLptThreads) atomicAdd(&hist[bucket(key(i))], 1u);
+    __syncthreads();
+    // exclusive scan of the 2048 buckets, two per thread
+    const uint32_t h0 = hist[2 * tid], h1 = hist[2 * tid + 1];
+    uint32_t incl = h0 + h1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = s_wsum[lane], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += v;
+      }
+      s_wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    const uint32_t base = s_wsum[warp] + incl - (h0 + h1);
+    hist[2 * tid] = base;
+    hist[2 * tid + 1] = base + h0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kLptThreads) ord[atomicAdd(&hist[bucket(key(i))], 1u)] = static_cast<uint32_t>(i);
+    __syncthreads();
+  }
+  if (tid == 0) out[0] = static_cast<uint32_t>(ntiles);
+}
+
+void run_lpt(Workspace& ws, int ntiles, uint32_t* out, cudaStream_t st, int64_t* L) {
+  k_lpt<<<1, kLptThreads, 0, st>>>(ws.qstat, ntiles, out, ws.tiles_cap);
+  ++*L;
 }
 
 void run_world(Workspace& ws, DevState* ds, const float* params, int64_t P, const RasterParams& rp, cudaStream_t st,

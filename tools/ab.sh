@@ -9,7 +9,7 @@ import json,sys
 v=sys.argv[1]
 try:
   d=json.loads(open(f"gpurun_out/ab_{v}.json").read().strip().splitlines()[-1])
-  k=d['kernels']; print(v, round(d['value'],3), 'it_ms', round(d['ms_per_iter']*1e3,1), ' '.join(f"{n}={k[n]['avg_ms']*1e3:.1f}" for n in k))
+  k=d['kernels']; print(v, round(d['value'],3), 'it_ms', round(d['ms_per_iter']*1e3,1), ' '.join(f"{n}={k[n]['avg_ms']*1e3:.1f}" for n in k if isinstance(k[n], dict)))
 except Exception as e: print(v,'FAILED',e)
 PY
 done
