@@ -67,7 +67,7 @@ struct Workspace {
   cudaStream_t side2 = nullptr;
   cudaEvent_t ev_lfork = nullptr, ev_ljoin = nullptr;
   uint32_t* order = nullptr;    // 2 * (1 + 5 tiles_cap)
-  int2* qstat = nullptr;        // 4 tiles_cap: per (tile, quadrant) forward steps, entries taken
+  int4* qstat = nullptr;        // 4 tiles_cap: per (tile, quadrant) forward steps, entries taken, list length
   // per primitive, id-indexed (written by k_preprocess for the visible ones)
   BlendG* bg_id = nullptr;
   GuardG* gg_id = nullptr;

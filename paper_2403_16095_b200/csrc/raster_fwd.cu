@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_op, float* __restrict__ o_T,
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
     uint8_t* __restrict__ emask, int64_t emask_plane, uint8_t* __restrict__ o_code, uint32_t* clean_bins,
-    int64_t clean_cnt_off, const uint32_t* __restrict__ order, int2* __restrict__ qstat) {
+    int64_t clean_cnt_off, const uint32_t* __restrict__ order, int4* __restrict__ qstat) {
   __shared__ BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
@@ -777,7 +777,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       }
     }
   }
-  if (qstat && lane == 0) qstat[tile * 4 + warp] = make_int2(static_cast<int>(wsteps), static_cast<int>(wtaken));
+  if (qstat && lane == 0)
+    qstat[tile * 4 + warp] = make_int4(static_cast<int>(wsteps), static_cast<int>(wtaken), rg.y - rg.x, 0);
   double v[LS_NUM], vb[LS_NUM];
 #pragma unroll
   for (int q = 0; q < LS_NUM; ++q) v[q] = vb[q] = 0.0;
@@ -971,8 +972,16 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
 // pose backward's steps), longest first.  Only the dispatch order changes: every CTA still writes
 // its tile's rows, and the reductions over them run in tile order.
 constexpr int kLptThreads = 1024, kLptBuckets = 2048;
-__global__ void __launch_bounds__(kLptThreads) k_lpt(const int2* __restrict__ qstat, int ntiles, uint32_t* __restrict__ out,
-                                                    int64_t tiles_cap) {
+#ifndef GSF_LPT_KEY
+#define GSF_LPT_KEY 1
+#endif
+#ifndef GSF_LPT_LDIV
+#define GSF_LPT_LDIV 4
+#endif
+#ifndef GSF_LPT_BADD
+#define GSF_LPT_BADD 0
+#endif
+__global__ void __launch_bounds__(kLptThreads) k_lpt(const int4* __restrict__ qstat, int ntiles, uint32_t* __restrict__ out, int64_t tiles_cap) {
   __shared__ uint32_t hist[kLptBuckets];
   __shared__ uint32_t s_wsum[kLptThreads / 32];
   __shared__ uint32_t s_max;
@@ -981,11 +990,17 @@ __global__ void __launch_bounds__(kLptThreads) k_lpt(const int2* __restrict__ qs
     const int n = pass == 0 ? ntiles : 4 * ntiles;
     uint32_t* ord = out + 1 + (pass == 0 ? 0 : tiles_cap);
     auto key = [&](int i) -> uint32_t {
-      if (pass == 0) {
-        const int2 a = qstat[4 * i], b = qstat[4 * i + 1], c = qstat[4 * i + 2], d = qstat[4 * i + 3];
+      if (pass == 0) {   // a tile CTA: its 4 warps walk concurrently after staging the list
+        const int4 a = qstat[4 * i], b = qstat[4 * i + 1], c = qstat[4 * i + 2], d = qstat[4 * i + 3];
+#if GSF_LPT_KEY == 0
         return static_cast<uint32_t>(max(a.x, 0) + max(b.x, 0) + max(c.x, 0) + max(d.x, 0));
+#elif GSF_LPT_KEY == 1
+        return static_cast<uint32_t>(max(max(a.x, b.x), max(max(c.x, d.x), 0)) + max(a.z, 0) / GSF_LPT_LDIV);
+#else
+        return static_cast<uint32_t>(max(max(a.x, b.x), max(max(c.x, d.x), 0)));
+#endif
       }
-      return static_cast<uint32_t>(max(qstat[i].y, 0));
+      return static_cast<uint32_t>(max(qstat[i].y, 0) + GSF_LPT_BADD);
     };
     for (int b = tid; b < kLptBuckets; b += kLptThreads) hist[b] = 0u;
     if (tid == 0) s_max = 1u;
