@@ -317,7 +317,7 @@ void ensure_map(gsf_ctx_s* c, int64_t P, int K) {
 void alloc_pairs(Workspace& ws) {
 
   dalloc(ws.skey, ws.pair_cap); dalloc(ws.sid, ws.pair_cap);
-  dalloc(ws.sslot, ws.pair_cap); dalloc(ws.emask, 4 * ws.pair_cap);
+  dalloc(ws.sslot, ws.pair_cap); dalloc(ws.emask, ws.pair_cap);
   dalloc(ws.partials, ws.pair_cap * 10);
 }
 

@@ -67,14 +67,14 @@ struct Workspace {
   cudaStream_t side2 = nullptr;
   cudaEvent_t ev_lfork = nullptr, ev_ljoin = nullptr;
   uint32_t* order = nullptr;    // 2 * (1 + 5 tiles_cap)
-  int4* qstat = nullptr;        // 4 tiles_cap: per (tile, quadrant) forward steps, entries taken, list length
+  int2* qstat = nullptr;        // 4 tiles_cap: per (tile, quadrant) forward (warp, entry) steps, list length
   // per primitive, id-indexed (written by k_preprocess for the visible ones)
   BlendG* bg_id = nullptr;
   GuardG* gg_id = nullptr;
   BlendG* bg_slot = nullptr;   // tracking: the same records indexed by visible slot (compact)
   GuardG* gg_slot = nullptr;
   uint32_t* sslot = nullptr;   // tracking: tile lists as visible slots (beside sid)
-  uint8_t* emask = nullptr;    // tracking: 4 planes of pair_cap bytes, plane q = the entries some pixel of 8x8 block q took (k_blend_track)
+  uint8_t* emask = nullptr;    // tracking: per list entry, the 8x8 blocks of its tile it can reach (k_blend_track)
   uint32_t* cand = nullptr;    // tracking: trust-region candidate ids (k_candidates)
   double* depth_id = nullptr;
   int4* rect_id = nullptr;

@@ -102,9 +102,7 @@ struct BwdPtrs {
   const uint32_t* pj_slot;  // id -> slot in pj (position in the visible list)
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
   const uint32_t* sslot;    // tracking: tile lists as visible slots
-  const uint8_t* emask;     // tracking: 4 planes (8x8 block q of the tile) x emask_plane entries: 1 if some
-                            // pixel of the block took the entry in the forward (k_blend_track)
-  int64_t emask_plane;
+  const uint8_t* emask;     // tracking: per entry, the 8x8 blocks it can reach (k_blend_track)
   const uint8_t* pxcode;    // tracking: per pixel, the seed signs (pixel_seed_code, k_blend_track)
   const BlendG* bg_slot;    // tracking: records by visible slot
   const GuardG* gg_slot;
@@ -562,7 +560,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       if (c < nch) {
         const int lo = max(rg.x, E - kC * (c + 1)), hi = E - kC * c;
         if (lane < hi - lo) {
-          m = __ldg(bp.emask + qd * bp.emask_plane + lo + lane);
+          m = (__ldg(bp.emask + lo + lane) >> qd) & 1u;
           sl = __ldg(bp.sslot + lo + lane);
         }
       }
@@ -1060,7 +1058,6 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.tile_pose = nullptr;
   bp.sslot = ws.sslot;
   bp.emask = ws.emask;
-  bp.emask_plane = ws.pair_cap;
   bp.pxcode = ws.pxcode;
   bp.bg_slot = ws.bg_slot;
   bp.gg_slot = ws.gg_slot;

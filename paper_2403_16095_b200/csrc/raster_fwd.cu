@@ -673,8 +673,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     int tiles_x, BlendConsts kc, double near_plane, double far_plane, LossParams lp, DevState* ds,
     float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_op, float* __restrict__ o_T,
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
-    uint8_t* __restrict__ emask, int64_t emask_plane, uint8_t* __restrict__ o_code, uint32_t* clean_bins,
-    int64_t clean_cnt_off, const uint32_t* __restrict__ order, int4* __restrict__ qstat) {
+    uint8_t* __restrict__ emask, uint8_t* __restrict__ o_code, uint32_t* clean_bins, int64_t clean_cnt_off,
+    const uint32_t* __restrict__ order, int2* __restrict__ qstat) {
   __shared__ BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
@@ -694,7 +694,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   const int tile = (order && order[0] == gridDim.x) ? static_cast<int>(order[1 + blockIdx.x]) : blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t sgb = opaque_smem_base(s_g);
-  uint32_t wsteps = 0u, wtaken = 0u;   // this warp's walked steps and taken entries (k_lpt's costs)
+  uint32_t wsteps = 0u;   // this warp's (warp, entry) steps: k_lpt's cost of the tile and of the
+                          // quadrant's pose backward (which walks the same block mask)
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x = tx * kTile + 8 * (warp & 1) + (lane & 7);
   const int ya = ty * kTile + 8 * (warp >> 1) + (lane >> 3), yb = ya + 4;
@@ -719,6 +720,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         s_id[e] = id;
         const uint8_t mk = static_cast<uint8_t>(warp_block_mask8(gj, tile_x0, tile_y0, kc));
         s_mask[e] = mk;
+        if (emask) emask[j] = mk;   // the pose backward's block test
       }
     }
     __syncthreads();
@@ -727,11 +729,9 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       if (__all_sync(0xffffffffu, T.x < kc.term && T.y < kc.term)) break;
       const int kk = c0 + lane;
       uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
-      uint32_t took = 0u;   // this lane's pixels took entry c0 + b (bit b)
       wsteps += __popc(bits);
       while (bits) {
         const int k = c0 + __ffs(bits) - 1;
-        const uint32_t kbit = bits & (0u - bits);
         bits &= bits - 1u;
 #ifndef GSF_NO_PIN_PX
         // keep the pixel centres in registers: at the 64-register cap ptxas otherwise re-forms
@@ -766,19 +766,11 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         const int li = start + k - rg.x + 1;
         if (ca) last_a = li;
         if (cb) last_b = li;
-        if (ca || cb) took |= kbit;
-      }
-      // the pose backward walks only the entries some pixel of its block took: every entry up to
-      // the block's last contributor has been walked here, so no stale byte is ever read
-      if (emask) {
-        took = __reduce_or_sync(0xffffffffu, took);
-        wtaken += __popc(took);
-        if (kk < cnt) emask[warp * emask_plane + start + kk] = static_cast<uint8_t>((took >> lane) & 1u);
       }
     }
   }
   if (qstat && lane == 0)
-    qstat[tile * 4 + warp] = make_int4(static_cast<int>(wsteps), static_cast<int>(wtaken), rg.y - rg.x, 0);
+    qstat[tile * 4 + warp] = make_int2(static_cast<int>(wsteps), rg.y - rg.x);
   double v[LS_NUM], vb[LS_NUM];
 #pragma unroll
   for (int q = 0; q < LS_NUM; ++q) v[q] = vb[q] = 0.0;
@@ -943,7 +935,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
                                                   a.keep_maps ? ws.color : nullptr, ws.alpha_depth, ws.opacity, ws.final_T,
                                                   ws.last, ws.loss_part,
                                                   a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket,
-                                                  sl ? ws.emask : nullptr, ws.pair_cap, sl ? ws.pxcode : nullptr,
+                                                  sl ? ws.emask : nullptr, sl ? ws.pxcode : nullptr,
                                                   a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride,
                                                   a.order, sl ? ws.qstat : nullptr);
   }
@@ -968,20 +960,14 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
 // roughly in blockIdx order, so a grid whose long tiles come last ends with a few SMs finishing
 // them while the rest idle (ncu: the average SM active 83-86 % of the kernel).  From the previous
 // iteration's per-(tile, quadrant) counts (the lists change little between iterations) one CTA
-// counting-sorts the tiles by forward steps and the (tile, quadrant) items by entries taken (the
-// pose backward's steps), longest first.  Only the dispatch order changes: every CTA still writes
-// its tile's rows, and the reductions over them run in tile order.
+// counting-sorts the tiles by their longest warp walk plus a quarter of the list length (the
+// staging) and the (tile, quadrant) items by their walk (the pose backward walks the same block
+// masks), longest first.  Measured per-CTA cycles as the cost (clock64) and a refined mask of
+// only the entries a block took were both slower: the bookkeeping costs more than it balances.
+// Only the dispatch order changes: every CTA still writes its tile's rows, and the reductions over them run in tile order.
 constexpr int kLptThreads = 1024, kLptBuckets = 2048;
-#ifndef GSF_LPT_KEY
-#define GSF_LPT_KEY 1
-#endif
-#ifndef GSF_LPT_LDIV
-#define GSF_LPT_LDIV 4
-#endif
-#ifndef GSF_LPT_BADD
-#define GSF_LPT_BADD 0
-#endif
-__global__ void __launch_bounds__(kLptThreads) k_lpt(const int4* __restrict__ qstat, int ntiles, uint32_t* __restrict__ out, int64_t tiles_cap) {
+__global__ void __launch_bounds__(kLptThreads) k_lpt(const int2* __restrict__ qstat, int ntiles, uint32_t* __restrict__ out,
+                                                    int64_t tiles_cap) {
   __shared__ uint32_t hist[kLptBuckets];
   __shared__ uint32_t s_wsum[kLptThreads / 32];
   __shared__ uint32_t s_max;
@@ -991,16 +977,10 @@ __global__ void __launch_bounds__(kLptThreads) k_lpt(const int4* __restrict__ qs
     uint32_t* ord = out + 1 + (pass == 0 ? 0 : tiles_cap);
     auto key = [&](int i) -> uint32_t {
       if (pass == 0) {   // a tile CTA: its 4 warps walk concurrently after staging the list
-        const int4 a = qstat[4 * i], b = qstat[4 * i + 1], c = qstat[4 * i + 2], d = qstat[4 * i + 3];
-#if GSF_LPT_KEY == 0
-        return static_cast<uint32_t>(max(a.x, 0) + max(b.x, 0) + max(c.x, 0) + max(d.x, 0));
-#elif GSF_LPT_KEY == 1
-        return static_cast<uint32_t>(max(max(a.x, b.x), max(max(c.x, d.x), 0)) + max(a.z, 0) / GSF_LPT_LDIV);
-#else
-        return static_cast<uint32_t>(max(max(a.x, b.x), max(max(c.x, d.x), 0)));
-#endif
+        const int2 a = qstat[4 * i], b = qstat[4 * i + 1], c = qstat[4 * i + 2], d = qstat[4 * i + 3];
+        return static_cast<uint32_t>(max(max(a.x, b.x), max(max(c.x, d.x), 0)) + max(a.y, 0) / 4);
       }
-      return static_cast<uint32_t>(max(qstat[i].y, 0) + GSF_LPT_BADD);
+      return static_cast<uint32_t>(max(qstat[i].x, 0));
     };
     for (int b = tid; b < kLptBuckets; b += kLptThreads) hist[b] = 0u;
     if (tid == 0) s_max = 1u;
