@@ -393,7 +393,11 @@ def run_ours(args):
     dom = max(("blend", "backward"), key=lambda k: prof[k][0])
     achieved = flops[dom] / (per_launch[dom] * 1e-3) / 1e12
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    pre_bytes = int(m.count) * (56 + 52)   # upper bound: every primitive (the trust region reads fewer)
+    # 56 B in + 52 B out per projected primitive; inside the trust region a launch
+    # projects the frame's candidates only (gsf_track_candidates), not all P
+    ncand = int(ctx.lib.gsf_track_candidates(ctx.h))
+    pre_units = ncand if ncand > 0 else int(m.count)
+    pre_bytes = pre_units * (56 + 52)
     kname = {"blend": "k_blend_track", "backward": "k_backward_track_w"}[dom]
     traffic = None
     try:
@@ -421,6 +425,8 @@ def run_ours(args):
                        "graph (ms_per_step); profiles/ holds the ncu launch list of the graph-replayed loop")
     kernels["preprocess"]["hbm_gbs"] = pre_bytes / (per_launch["preprocess"] * 1e-3) / 1e9
     kernels["preprocess"]["hbm_frac"] = kernels["preprocess"]["hbm_gbs"] / hbm
+    kernels["preprocess"]["projected_per_launch"] = pre_units
+    kernels["preprocess"]["algorithmic_bytes"] = pre_bytes
 
     mapping = None
     if not args.no_mapping:
@@ -504,6 +510,7 @@ def run_mapping(args, ctx, rank, world, device):
            "n_gpus": world, "scaling": "strong (window fixed, keyframes sharded)", "ms_per_iter": el / args.map_iters,
            "loss_trace": [float(x) for x in trace]}
     if world == 1:
+        out["per_view"], out["kernels"], out["roofline"] = mapping_evidence(mctx, slots, kposes, kf, K, tc, mc)
         mctx.lib.gsf_event_record(mctx.h, 2)
         mctx.map_step(slots[:4], kposes[:4], K, mc, 12)
         mctx.lib.gsf_event_record(mctx.h, 3)
@@ -511,6 +518,80 @@ def run_mapping(args, ctx, rank, world, device):
         out["map_step_it_per_s"] = 12 / (ms.value / 1e3)
     mctx.close()
     return out
+
+
+def view_stats(ctx, pose, K):
+    """V (visible), M (tile pairs), T (traversed (pixel, entry) pairs: every pixel of a tile times
+    the tile's list length) and C (contributors) of one render."""
+    r = ctx.render(pose, K)
+    tiles_x, tiles_y = (K.width + 15) // 16, (K.height + 15) // 16
+    tr, _ = ctx.render_tiles(tiles_x * tiles_y, r.num_pairs)
+    tl = (tr[:, 1] - tr[:, 0]).astype(np.float64)
+    tpix = np.array([min(16, K.width - (t % tiles_x) * 16) * min(16, K.height - (t // tiles_x) * 16)
+                     for t in range(tiles_x * tiles_y)], np.float64)
+    return {"V": float(r.num_visible), "M": float(r.num_pairs), "T": float((tl * tpix).sum()),
+            "C": float(r.per_pixel_count.sum())}
+
+
+def mapping_evidence(mctx, slots, kposes, kf, K, tc, mc, iters=2):
+    """Per-view workload (V, M, T, C averaged over the window's keyframes), per-kernel-class
+    device times of `iters` profiled sliding_ba iterations (CUDA-event brackets, eager launches),
+    and an algorithmic roofline entry per mapping kernel (SURVEY.md §8(d) formulas)."""
+    import ctypes as _C
+    stats = [view_stats(mctx, p, K) for p in kposes]
+    pv = {k: float(np.mean([s[k] for s in stats])) for k in ("V", "M", "T", "C")}
+    pv["views"] = len(stats)
+    mctx.lib.gsf_profile_enable(mctx.h, 1)
+    mctx.lib.gsf_event_record(mctx.h, 4)
+    mctx.sliding_ba(slots, [p for p in kposes], kf, K, tc, mc, iters)
+    mctx.lib.gsf_event_record(mctx.h, 5)
+    tot = _C.c_double()
+    mctx.lib.gsf_event_elapsed(mctx.h, 4, 5, _C.byref(tot))
+    prof = {}
+    for name, k in (("preprocess", 0), ("sort_binning", 1), ("blend", 2), ("backward", 3), ("chain", 4), ("ssim", 5),
+                    ("adam", 6)):
+        t, n = _C.c_double(), _C.c_int64()
+        mctx.lib.gsf_profile_read(mctx.h, k, _C.byref(t), _C.byref(n))
+        prof[name] = {"total_ms": t.value, "launches": n.value, "avg_ms": t.value / max(n.value, 1)}
+    mctx.lib.gsf_profile_enable(mctx.h, 0)
+    per_iter = tot.value / iters
+    for v in prof.values():
+        v["share_of_iteration"] = v["total_ms"] / max(tot.value, 1e-9)
+    prof["profiled_ms_per_iteration"] = per_iter
+    peaks, _ = measured_peaks()
+    fp32_peak, _ = fp32_peak_measured()
+    fp32_peak = fp32_peak or 73.9
+    hbm = float(peaks.get("hbm_gbs", 6451.8))
+    fp64_peak = 148 * 64 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    npix = K.width * K.height
+    V, M, T, Cn, P = pv["V"], pv["M"], pv["T"], pv["C"], float(mctx.P)
+    D = 14.0   # fields per primitive at SH K=1 (mean 3, log_scale 3, quat 4, opacity 1, SH 3)
+
+    def fp(kind, flops, unit_peak, note):
+        ms = prof[kind]["avg_ms"]
+        a = flops / (ms * 1e-3) / 1e12 if ms > 0 else None
+        return {"bound": note, "algorithmic": flops, "avg_launch_ms": ms, "achieved": a, "peak": unit_peak,
+                "unit": "TFLOP/s", "frac": (a / unit_peak) if a else None}
+
+    def bw(kind, nbytes, note):
+        ms = prof[kind]["avg_ms"]
+        a = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else None
+        return {"bound": note, "algorithmic_bytes": nbytes, "avg_launch_ms": ms, "achieved": a, "peak": hbm,
+                "unit": "GB/s", "frac": (a / hbm) if a else None}
+
+    roof = {
+        "blend k_blend<2>": fp("blend", 11 * T + 24 * Cn, fp32_peak, "fp32: 11 T + 24 C"),
+        "backward k_backward<SEED_MAP,10>": fp("backward", 13 * T + 70 * Cn, fp32_peak, "fp32: 13 T + 70 C"),
+        "chain k_chain<10> (+k_pose_sum)": fp("chain", 300 * V, fp64_peak,
+                                             "fp64: 300 V (peak = 148 SMs x 64 FP64 lanes x 2 x clock)"),
+        "chain_bytes": bw("chain", 40 * M + 4 * D * 3 * V, "hbm: 40 B per (primitive, tile) partial + params read, "
+                                                          "gradients read+written (3 x 4 D B per visible primitive)"),
+        "ssim k_ssim_fwd+k_ssim_bwd": bw("ssim", 108.0 * npix, "hbm: 2 images read (24 B/px), 9 adjoint planes "
+                                                                "written and read (72 B/px), d_colour written (12 B/px)"),
+        "adam k_adam": bw("adam", 28 * D * P, "hbm: 28 B per scalar (r p,g,m,v; w p,m,v)"),
+        "peaks": {"fp32_tflops": fp32_peak, "fp64_tflops_derived": fp64_peak, "hbm_gbs": hbm},
+    }
+    return pv, prof, roof
 
 
 def cpu_model():

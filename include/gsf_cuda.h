@@ -173,6 +173,15 @@ const char* gsf_last_error(gsf_ctx ctx);
 int64_t gsf_last_error_index(gsf_ctx ctx);
 /* Device-side kernel launches issued by this context since creation (evidence counter). */
 int64_t gsf_kernel_launches(gsf_ctx ctx);
+/* Binning capacities: (tile, primitive) pairs and per-tile bucket entries.  Renders grow both on
+ * overflow (retry with the loop's maxima; GSF_EUNSUPPORTED if still exceeded), so reserve only
+ * pre-sizes them to skip that retry (a value <= 0 leaves a capacity unchanged; smaller values are
+ * honoured too, which the overflow tests use). */
+int gsf_reserve(gsf_ctx ctx, int64_t pair_cap, int64_t bucket_cap);
+int gsf_capacity(gsf_ctx ctx, int64_t* pair_cap, int64_t* bucket_cap);
+/* Trust-region candidates of the last tracked frame (the primitives its iterations project;
+ * measurement evidence for the preprocess's algorithmic bytes), -1 on error. */
+int64_t gsf_track_candidates(gsf_ctx ctx);
 int gsf_synchronize(gsf_ctx ctx);
 
 /* ---- timing hooks (benchmark evidence; no effect on results) -------------------------------

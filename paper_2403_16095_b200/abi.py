@@ -127,6 +127,9 @@ SIGNATURES = {
     "gsf_last_error": (C.c_char_p, [C.c_void_p]),
     "gsf_last_error_index": (C.c_int64, [C.c_void_p]),
     "gsf_kernel_launches": (C.c_int64, [C.c_void_p]),
+    "gsf_track_candidates": (C.c_int64, [C.c_void_p]),
+    "gsf_reserve": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
+    "gsf_capacity": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "gsf_synchronize": (C.c_int, [C.c_void_p]),
     "gsf_profile_enable": (C.c_int, [C.c_void_p, C.c_int32]),
     "gsf_profile_read": (C.c_int, [C.c_void_p, C.c_int32, dp, i64p]),

@@ -183,6 +183,15 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self.lib.gsf_kernel_launches(self.h))
 
+    def reserve(self, pair_cap: int = 0, bucket_cap: int = 0):
+        """Pre-size the binning capacities ((tile, primitive) pairs, per-tile bucket entries)."""
+        self._check(self.lib.gsf_reserve(self.h, int(pair_cap), int(bucket_cap)))
+
+    def capacity(self):
+        a, b = C.c_int64(), C.c_int64()
+        self._check(self.lib.gsf_capacity(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     # ---- map -----------------------------------------------------------------------------
     def upload(self, m: GaussianMap):
         hm = m.host()

@@ -773,6 +773,40 @@ int gsf_ctx_destroy(gsf_ctx c) {
 const char* gsf_last_error(gsf_ctx c) { return c ? c->err.c_str() : "null context"; }
 int64_t gsf_last_error_index(gsf_ctx c) { return c ? c->err_index : -1; }
 int64_t gsf_kernel_launches(gsf_ctx c) { return c ? c->launches : 0; }
+
+int gsf_reserve(gsf_ctx c, int64_t pair_cap, int64_t bucket_cap) {
+  return guard(c, [&] {
+    if (pair_cap < 0 || bucket_cap < 0 || pair_cap > (int64_t{1} << 31) || bucket_cap > (int64_t{1} << 24))
+      throw EInval("reserve: capacity out of range");
+    sync(c);
+    Workspace& ws = c->ws;
+    if (pair_cap > 0 && pair_cap != ws.pair_cap) {
+      ws.pair_cap = std::max<int64_t>(pair_cap, 64);
+      if (ws.skey) alloc_pairs(ws);
+    }
+    if (bucket_cap > 0 && bucket_cap != ws.bucket_cap) {
+      ws.bucket_cap = std::max<int64_t>(bucket_cap, 32);
+      if (ws.bucket) dalloc(ws.bucket, static_cast<size_t>(ws.tiles_cap) * ws.bucket_cap);
+    }
+  });
+}
+
+int gsf_capacity(gsf_ctx c, int64_t* pair_cap, int64_t* bucket_cap) {
+  return guard(c, [&] {
+    if (pair_cap) *pair_cap = c->ws.pair_cap;
+    if (bucket_cap) *bucket_cap = c->ws.bucket_cap;
+  });
+}
+
+int64_t gsf_track_candidates(gsf_ctx c) {
+  if (!c) return -1;
+  int64_t n = -1;
+  const int rc = guard(c, [&] {
+    read_state(c);
+    n = static_cast<int64_t>(c->ds_host->ncand);
+  });
+  return rc == GSF_OK ? n : -1;
+}
 int gsf_synchronize(gsf_ctx c) {
   return guard(c, [&] { sync(c); });
 }
@@ -1696,7 +1730,9 @@ int gsf_sliding_ba(gsf_ctx c, const int32_t* slots, gsf_pose* poses, const int32
       if (c->nranks > 1) {
         exchange_and_step(c, n, loss_acc, g, it);
       } else {
+        if (c->ws.prof) c->ws.prof->begin(PROF_ADAM, c->stream);
         run_adam(c->params, c->grads, c->adam_m, c->adam_v, c->P, c->D, g, c->adam_step, c->stream, &c->launches);
+        if (c->ws.prof) c->ws.prof->end(c->stream);
       }
       k_store<<<1, 1, 0, c->stream>>>(loss_acc, c->trace_dev + it);
       ++c->launches;

@@ -75,6 +75,18 @@ __device__ __forceinline__ bool warp_grid_reduce(const double* part, double* gpa
   const int lane = threadIdx.x & 31;
   const int r = row >= 0 ? row : static_cast<int>(blockIdx.x), g = r >> 5, g0 = g << 5, gn = min(32, rows - g0);
   const int ngroups = (rows + 31) >> 5;
+#ifdef GSF_RELEASE_TICKET
+  // the row's writer publishes it with a release RMW on the group ticket (no full SC fence)
+  __syncwarp();
+  unsigned last = 0;
+  if (lane == 0) {
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&gt[g]) : "memory");
+    last = prev == static_cast<unsigned>(gn - 1);
+    if (last) gt[g] = 0u;
+  }
+  (void)wrote;
+#else
   if (wrote) __threadfence();
   __syncwarp();
   unsigned last = 0;
@@ -82,6 +94,7 @@ __device__ __forceinline__ bool warp_grid_reduce(const double* part, double* gpa
     last = atomicAdd(&gt[g], 1u) == static_cast<unsigned>(gn - 1);
     if (last) gt[g] = 0u;
   }
+#endif
   if (!__shfl_sync(0xffffffffu, last, 0)) return false;
   __threadfence();
   double v[NV];

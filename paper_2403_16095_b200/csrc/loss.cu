@@ -346,6 +346,7 @@ void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W
   }
   const dim3 grid(div_up(W, kSX), div_up(H, kSY));
   float* u = ws.ssim_tmp;                 // 9 adjoint seed planes
+  if (ws.prof) ws.prof->begin(PROF_SSIM, st);
   launch_pdl(k_ssim_fwd, grid, dim3(256), ssim_fwd_smem(), st, x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr,
                                                  ws.red_part);
   ++*L;
@@ -354,6 +355,7 @@ void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W
     launch_pdl(k_ssim_bwd, grid, dim3(256), ssim_bwd_smem(), st, u, x, y, W, H, d_out);
     ++*L;
   }
+  if (ws.prof) ws.prof->end(st);
 }
 
 void run_iso(Workspace& ws, DevState* ds, const float* params, int64_t P, double w_iso, double eps, float* grads,

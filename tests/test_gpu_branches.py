@@ -365,3 +365,69 @@ def test_ba_first_step_matches_fp64(gpu_ctx, orc):
         assert np.abs(np.r_[list(a.rotation_tangent), list(a.translation)] -
                       np.r_[list(b.rotation_tangent), list(b.translation)]).max() < 1e-9
     assert trace[0] == pytest.approx(otrace[0], rel=1e-5)
+
+
+def _list_extent(ctx, p, K):
+    r = ctx.render(p, K)
+    ntiles = ((K.width + 15) // 16) * ((K.height + 15) // 16)
+    tr, _ = ctx.render_tiles(ntiles, r.num_pairs)
+    return int((tr[:, 1] - tr[:, 0]).max()), int(r.num_pairs)
+
+
+def _cluster_scene(orc):
+    """random_scene(901, 400) plus 200 small primitives at (-0.52, 0.1, 1.5): outside the 64x48
+    f=90 view from a camera 8 cm to the -x side, inside it from the identity pose.  Tracking from
+    that start toward the identity brings the cluster into view mid-loop (fp64 oracle: lists
+    (89 longest, 938 pairs) at the start, (274, 1245) after 40 iterations, (272, 1235) after 60)."""
+    from types import SimpleNamespace
+    base = orc.random_scene(901, 400)
+    rng = np.random.default_rng(5)
+    cl = scene([dict(mean=[-0.52 + 0.004 * rng.standard_normal(), 0.1 + 0.004 * rng.standard_normal(), 1.5],
+                     scale=0.006, opacity=0.3, color=[0.9, 0.2, 0.1]) for _ in range(200)])
+    return f32_round(SimpleNamespace(**{k: np.concatenate([getattr(base, k), getattr(cl, k)])
+                                        for k in ("mean", "log_scale", "quat", "opacity_logit", "sh", "uncertainty",
+                                                  "observed")}))
+
+
+def test_overflow_mid_loop_grows_and_matches(gpu_ctx, orc):
+    """A tracking loop whose lists peak mid-loop (a cluster enters the view as the camera moves),
+    with the binning capacities reserved to fit the START render exactly: the captured loop
+    overflows only after it began.  track_frame must retry with the loop's maxima (DevState M_max /
+    max_tile), grow, and return the same pose bit for bit as a run that never overflowed — never a
+    pose from truncated lists.  The API render and tracking_gradient paths grow the same way."""
+    from paper_2403_16095_b200.abi import defaults_raster, defaults_tracker, defaults_weights
+    K = make_intrinsics(64, 48, 90.0)
+    m = _cluster_scene(orc)
+    gpu_ctx.upload(to_api_map(m))
+    gt = gpu_ctx.render(pose(), K)
+    gpu_ctx.frame_upload(0, gt.color, gt.alpha_depth, 64, 48)
+    tc = defaults_tracker()
+    tc.iterations = 60
+    w = defaults_weights(True)
+    start = perturbed(pose(), [0, 0, 0, -0.08, 0, 0])
+    ref = gpu_ctx.track_frame(0, start, K, tc, w)                 # default capacities: no overflow
+    L0, M0 = _list_extent(gpu_ctx, start, K)
+    L1, M1 = _list_extent(gpu_ctx, ref.pose, K)
+    assert L1 > L0 + 100 and M1 > M0 + 100, (L0, M0, L1, M1)     # the cluster entered mid-loop
+    ores = orc.track_frame(m, gt.color.astype(np.float64), gt.alpha_depth.astype(np.float64), start, K, tc, w,
+                           defaults_raster())
+    assert translation_error(ref.pose, ores.pose) < 2e-3 and rotation_error(ref.pose, ores.pose) < 2e-3
+    gpu_ctx.reserve(M0, L0)
+    assert gpu_ctx.capacity() == (max(M0, 64), max(L0, 32))
+    assert _list_extent(gpu_ctx, start, K) == (L0, M0)          # the start render fits: no growth
+    assert gpu_ctx.capacity() == (max(M0, 64), max(L0, 32))
+    res = gpu_ctx.track_frame(0, start, K, tc, w)
+    pc, bc = gpu_ctx.capacity()
+    assert pc > M1 and bc > L1, (pc, bc, M1, L1)                 # grown from the loop's maxima
+    assert list(res.pose.translation) == list(ref.pose.translation)
+    assert list(res.pose.rotation_tangent) == list(ref.pose.rotation_tangent)
+    assert res.final_loss == ref.final_loss and res.iterations_run == ref.iterations_run
+    # API render and tracking_gradient: the same growth protocol, same results as with room to spare
+    big = gpu_ctx.render(ref.pose, K)
+    tg_ref = gpu_ctx.tracking_gradient(0, ref.pose, K, w)
+    gpu_ctx.reserve(M0, L0)
+    small = gpu_ctx.render(ref.pose, K)
+    assert (small.per_pixel_count == big.per_pixel_count).all() and (small.color == big.color).all()
+    gpu_ctx.reserve(M0, L0)
+    tg = gpu_ctx.tracking_gradient(0, ref.pose, K, w)
+    assert np.array_equal(tg[1], tg_ref[1])
