@@ -317,7 +317,7 @@ void ensure_map(gsf_ctx_s* c, int64_t P, int K) {
 void alloc_pairs(Workspace& ws) {
 
   dalloc(ws.skey, ws.pair_cap); dalloc(ws.sid, ws.pair_cap);
-  dalloc(ws.sslot, ws.pair_cap); dalloc(ws.emask, ws.pair_cap);
+  dalloc(ws.sslot, ws.pair_cap); dalloc(ws.qlist, 4 * ws.pair_cap);
   dalloc(ws.partials, ws.pair_cap * 10);
 }
 
@@ -344,7 +344,7 @@ void ensure_ws(gsf_ctx_s* c, int W, int H) {
   if (npix > ws.npix_cap) {
     dalloc(ws.color, 3 * npix); dalloc(ws.alpha_depth, npix); dalloc(ws.median_depth, npix); dalloc(ws.median_valid, npix);
     dalloc(ws.opacity, npix); dalloc(ws.uncertainty, npix); dalloc(ws.final_T, npix); dalloc(ws.count, npix);
-    dalloc(ws.dominant, npix); dalloc(ws.median_prim, npix); dalloc(ws.dominant_w, npix); dalloc(ws.last, npix);
+    dalloc(ws.dominant, npix); dalloc(ws.median_prim, npix); dalloc(ws.dominant_w, npix); dalloc(ws.last, npix); dalloc(ws.lastc, npix);
     dalloc(ws.pxcode, npix);
     dalloc(ws.fix_list, npix);
     dalloc(ws.obs, npix); dalloc(ws.upstream, 7 * npix); dalloc(ws.dssim, 3 * npix); dalloc(ws.ssim_tmp, 9 * npix);
@@ -735,7 +735,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->comm);
   Workspace& ws = c->ws;
-  void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.emask, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins,
+  void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.qlist, ws.lastc, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
                   ws.last, ws.pxcode, ws.fix_list, ws.order, ws.qstat, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
@@ -1269,6 +1269,7 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
     // the two-pixel pose backward (K == 1) reads T, last and the seed signs only; the view-dependent
     // pose backward (k_backward_pose<SEED_TRACK, true>) derives its seeds from the maps
     fa.keep_maps = c->K > 1;
+    fa.qmode = c->K == 1 ? 1 : 0;
     fa.clean_bins = true;   // ... and each blend leaves the bins zeroed for the next iteration
     fa.bins_clean = it > 0;
     fa.fuse_loss_final = true;
@@ -1435,6 +1436,7 @@ int gsf_tracking_gradient(gsf_ctx c, int32_t slot, const gsf_pose* pose, const g
       reset_state(c, &cam);
       FwdArgs fa = fwd_args(c, *K, *rcfg, nullptr, f.rgb, f.depth, lp, -1);
       fa.want_posejac = true;
+      fa.qmode = c->K == 1 ? 2 : 0;
       run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
       run_loss_finalize(c->ws, c->ds, lp, tiles, npix, -1, c->stream, &c->launches);
       BwdArgs b = bwd_args(c, *K, *rcfg, f.depth, f.rgb, lp, SEED_TRACK, true);

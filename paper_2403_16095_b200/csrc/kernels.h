@@ -74,7 +74,12 @@ struct Workspace {
   BlendG* bg_slot = nullptr;   // tracking: the same records indexed by visible slot (compact)
   GuardG* gg_slot = nullptr;
   uint32_t* sslot = nullptr;   // tracking: tile lists as visible slots (beside sid)
-  uint8_t* emask = nullptr;    // tracking: per list entry, the 8x8 blocks of its tile it can reach (k_blend_track)
+  // tracking: per (tile, quadrant) work list of the pose backward, written by k_blend_track's walk:
+  // the visible slots of the entries whose footprint can reach the quadrant's 8x8 block, in list
+  // order, at 4 start + q (end - start) (4 pair_cap); lastc = each pixel's last contributor as an
+  // index into its quadrant's list (+1)
+  uint32_t* qlist = nullptr;
+  int32_t* lastc = nullptr;
   uint32_t* cand = nullptr;    // tracking: trust-region candidate ids (k_candidates)
   double* depth_id = nullptr;
   int4* rect_id = nullptr;
@@ -149,6 +154,10 @@ struct FwdArgs {
   int iteration;             // loop iteration (for device-side checks), -1 outside loops
   bool want_posejac = false; // tracking: emit the per-primitive pose Jacobians (ws.pj_id)
   bool keep_maps = true;     // tracking loop: colour / alpha depth / opacity maps are not read back
+  // k_blend_track's outputs for the two-pixel pose backward: 0 = last contributor as a list index
+  // (ws.last) only, 1 = the per-quadrant work lists (ws.qlist) + ws.lastc only (inside the tracking
+  // loop), 2 = both (gsf_tracking_gradient, whose render stays the context's latest)
+  int qmode = 0;
   bool bins_clean = false;   // tracking loop: the previous iteration's blend re-zeroed the bins (no memset)
   bool clean_bins = false;   // tracking loop: the blend re-zeroes the bins once the binning is consumed
   bool fuse_loss_final = false;  // tracking: the blend's last CTA runs the loss finalize

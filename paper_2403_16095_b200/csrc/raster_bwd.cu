@@ -101,8 +101,8 @@ struct BwdPtrs {
   const float* pj;          // pose Jacobians (fused tracking mode), 36 floats at the primitive's slot
   const uint32_t* pj_slot;  // id -> slot in pj (position in the visible list)
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
-  const uint32_t* sslot;    // tracking: tile lists as visible slots
-  const uint8_t* emask;     // tracking: per entry, the 8x8 blocks it can reach (k_blend_track)
+  const uint32_t* qlist;    // tracking: per (tile, quadrant) work lists (k_blend_track)
+  const int32_t* lastc;     // tracking: each pixel's last contributor as a work-list position + 1
   const uint8_t* pxcode;    // tracking: per pixel, the seed signs (pixel_seed_code, k_blend_track)
   const BlendG* bg_slot;    // tracking: records by visible slot
   const GuardG* gg_slot;
@@ -321,7 +321,7 @@ __device__ __forceinline__ PixBwd track_pixel_bwd(const BwdPtrs& bp, int64_t pi,
   p.last = 0;
   if (!inside) return p;
   const uint32_t code = bp.pxcode[pi];
-  const int last = bp.last[pi];
+  const int last = bp.lastc[pi];
   p.T = bp.final_T[pi];
   const float sc = static_cast<float>(ds->seed_color), sg = static_cast<float>(ds->seed_geo);
   p.gc0 = sc * code_sgn(code & 3u);
@@ -522,13 +522,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   // one staging buffer: 32 records (3 float4), 32 pose matrices (9 float4), 32 slots
   // two staging buffers of 16 entries: records (3 float4) at +0, pose matrices (9 float4) at +768 B;
   // their slots at 6144 + 64 b
-#ifdef GSF_TBW_SMEMFETCH
-  // + per buffer b: the chunk's list slots at 6272 + 64 b and the aligned word window of its
-  // forward block masks at 6400 + 32 b
-  __shared__ float4 s_buf[2 * 16 * 12 + 8 + 12];
-#else
   __shared__ float4 s_buf[2 * 16 * 12 + 8];
-#endif
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x;
@@ -553,21 +547,23 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
     const float px = static_cast<float>(x) + 0.5f;
     const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
     float2 T = make_float2(qa.T, qb.T), S = make_float2(0.f, 0.f);
-    // The list is walked back to front in chunks of kC = 16 entries, double-buffered: while chunk c
-    // is processed, the records and pose matrices of chunk c + 1 (only the entries whose forward
-    // block mask has this quadrant) stream into the other buffer with cp.async, and the masks and
+    // The quadrant's work list (the entries of the tile list whose footprint can reach this 8x8
+    // block, recorded by the forward's walk) is walked back to front from the pixels' last
+    // contributor in chunks of kC = 16 entries, double-buffered: while chunk c is processed, the
+    // records and pose matrices of chunk c + 1 stream into the other buffer with cp.async, and the
     // slots of chunk c + 2 load into registers (lanes 0..15).
     constexpr int kC = 16;
-    const int E = rg.x + maxlast;
+    const int E = maxlast;
     const int nch = (maxlast + kC - 1) / kC;
+    const uint32_t* ql = bp.qlist + 4 * static_cast<int64_t>(rg.x) + static_cast<int64_t>(qd) * (rg.y - rg.x);
     auto fetch = [&](int c, uint32_t& m, uint32_t& sl) {
       m = 0u;
       sl = 0u;
       if (c < nch) {
-        const int lo = max(rg.x, E - kC * (c + 1)), hi = E - kC * c;
+        const int lo = max(0, E - kC * (c + 1)), hi = E - kC * c;
         if (lane < hi - lo) {
-          m = (__ldg(bp.emask + lo + lane) >> qd) & 1u;
-          sl = __ldg(bp.sslot + lo + lane);
+          m = 1u;
+          sl = __ldg(ql + lo + lane);
         }
       }
     };
@@ -590,76 +586,6 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       }
       cp_async_commit();
     };
-#ifdef GSF_TBW_SMEMFETCH
-    // masks and slots of chunk c + 2 stream into shared memory (cp.async, in the group of chunk
-    // c + 1's records): no registers held across the chunk, no load consumed right after issue
-    auto fetch_async = [&](int c) {
-      if (c < nch) {
-        const int lo = max(rg.x, E - kC * (c + 1)), hi = E - kC * c;
-        const uint32_t b = static_cast<uint32_t>(c & 1);
-        if (lane < hi - lo) cp_async4_to(sb + 6272u + 64u * b + 4u * lane, bp.sslot + lo + lane);
-        const int w0 = lo >> 2, nw = ((hi - 1) >> 2) - w0 + 1;
-        if (lane >= 16 && lane - 16 < nw)
-          cp_async4_to(sb + 6400u + 32u * b + 4u * (lane - 16), reinterpret_cast<const uint32_t*>(bp.emask) + w0 + (lane - 16));
-      }
-    };
-    // lane e < 16 (and e + 16): this quadrant's bit of chunk c's entry e, and its slot
-    auto chunk_entry = [&](int c, uint32_t& m, uint32_t& sl) {
-      m = 0u;
-      sl = 0u;
-      if (c < nch) {
-        const int lo = max(rg.x, E - kC * (c + 1)), hi = E - kC * c;
-        const int e = lane & 15;
-        const uint32_t b = static_cast<uint32_t>(c & 1);
-        if (e < hi - lo) {
-          m = (lds_u8(sb + 6400u + 32u * b + static_cast<uint32_t>((lo & 3) + e)) >> qd) & 1u;
-          sl = static_cast<uint32_t>(lds_s32(sb + 6272u + 64u * b + 4u * e));
-        }
-      }
-    };
-    auto issue_direct = [&](int c, uint32_t me, uint32_t se) {
-      if (c < nch && me) {
-        const int e = lane & 15;
-        const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 3072u;
-        const float4* rec = reinterpret_cast<const float4*>(bp.bg_slot + se);
-        const float4* pjm = reinterpret_cast<const float4*>(bp.pj) + (kPjFloats / 4) * static_cast<size_t>(se);
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          const int j = (lane >> 4) + 2 * t;
-          if (j < 3) cp_async16_to(buf + 48u * e + 16u * j, rec + j);
-          else cp_async16_to(buf + 768u + 144u * e + 16u * (j - 3), pjm + (j - 3));
-        }
-        if (lane < 16) sts_s32(sb + 6144u + static_cast<uint32_t>(c & 1) * 64u + 4u * e, static_cast<int32_t>(se));
-      }
-    };
-    {   // chunk 0's masks / slots, then its records with chunk 1's masks / slots behind them
-      fetch_async(0);
-      cp_async_commit();
-      cp_async_wait_all();
-      __syncwarp();
-      uint32_t m, sl;
-      chunk_entry(0, m, sl);
-      issue_direct(0, m, sl);
-      fetch_async(1);
-      cp_async_commit();
-    }
-    for (int c = 0; c < nch; ++c) {
-      cp_async_wait_all();   // chunk c's records and chunk c + 1's masks / slots have landed
-      __syncwarp();
-      uint32_t m0, s0;
-      chunk_entry(c, m0, s0);   // read before fetch_async(c + 2) refills this buffer
-      {
-        uint32_t m1, s1;
-        chunk_entry(c + 1, m1, s1);
-        __syncwarp();
-        issue_direct(c + 1, m1, s1);
-        fetch_async(c + 2);
-        cp_async_commit();
-      }
-      (void)s0;
-      m0 = lane < 16 ? m0 : 0u;
-      const int lo = max(rg.x, E - kC * (c + 1));
-#else
     uint32_t m0, s0, m1, s1;
     fetch(0, m0, s0);
     fetch(1, m1, s1);
@@ -670,15 +596,14 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       fetch(c + 2, m2, s2);
       cp_async_wait_1();   // chunk c has landed (chunk c + 1 may still be in flight)
       __syncwarp();
-      const int lo = max(rg.x, E - kC * (c + 1));
-#endif
+      const int lo = max(0, E - kC * (c + 1));
       const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 3072u, idb = sb + 6144u + static_cast<uint32_t>(c & 1) * 64u;
-      uint32_t bits = __ballot_sync(0xffffffffu, m0 != 0u);
+      uint32_t bits = (E - kC * c - lo) >= 32 ? 0xffffffffu : ((1u << (E - kC * c - lo)) - 1u);
       float2 pa = make_float2(0.f, 0.f), pb2 = make_float2(0.f, 0.f), pc2 = make_float2(0.f, 0.f);
       while (bits) {
         const int k = 31 - __clz(bits);
         bits &= ~(1u << k);
-        const int li = lo + k - rg.x;
+        const int li = lo + k;
         const BlendG g = lds_blend(buf + 48u * k);
         const float dx = __fadd_rn(px, -g.mx);
         const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
@@ -746,9 +671,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       }
       pd[0] += pa.x; pd[1] += pa.y; pd[2] += pb2.x; pd[3] += pb2.y; pd[4] += pc2.x; pd[5] += pc2.y;
       __syncwarp();   // buffer c & 1 is refilled by issue(c + 2)
-#ifndef GSF_TBW_SMEMFETCH
       m0 = m1; s0 = s1; m1 = m2; s1 = s2;
-#endif
     }
     cp_async_wait_all();
   }
@@ -1135,8 +1058,8 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.rect = ws.rect_id;
   bp.pair_base = ws.pair_base;
   bp.tile_pose = nullptr;
-  bp.sslot = ws.sslot;
-  bp.emask = ws.emask;
+  bp.qlist = ws.qlist;
+  bp.lastc = ws.lastc;
   bp.pxcode = ws.pxcode;
   bp.bg_slot = ws.bg_slot;
   bp.gg_slot = ws.gg_slot;

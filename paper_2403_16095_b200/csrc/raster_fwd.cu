@@ -667,18 +667,28 @@ constexpr int kTrkBatch = 256;
 #ifndef GSF_TRK_MINB
 #define GSF_TRK_MINB 8
 #endif
+// QM: 0 = each pixel's last contributor as a list index (o_last); 1 = the pose backward's
+// per-quadrant work lists (qlist) and the last contributor as a work-list position (o_lastc);
+// 2 = both.
+template <int QM>
 __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     const int2* __restrict__ ranges, const uint32_t* __restrict__ sid, const BlendG* __restrict__ bg,
     const GuardG* __restrict__ gg, const float* __restrict__ loss_rgb, const float* __restrict__ loss_depth, int W, int H,
     int tiles_x, BlendConsts kc, double near_plane, double far_plane, LossParams lp, DevState* ds,
     float* __restrict__ o_color, float* __restrict__ o_ad, float* __restrict__ o_op, float* __restrict__ o_T,
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
-    uint8_t* __restrict__ emask, uint8_t* __restrict__ o_code, uint32_t* clean_bins, int64_t clean_cnt_off,
+    uint32_t* __restrict__ qlist, int32_t* __restrict__ o_lastc, uint8_t* __restrict__ o_code, uint32_t* clean_bins,
+    int64_t clean_cnt_off,
     const uint32_t* __restrict__ order, int2* __restrict__ qstat) {
   __shared__ BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
   __shared__ double s_red[kTrkThreads / 32][LS_NUM];
+#ifdef GSF_TRK_PREFETCH
+  // the loss epilogue's inputs (target colour, sensor depth of the lane's two pixels) stream into
+  // shared memory while the tile is walked
+  __shared__ float s_obs[kTrkThreads][8];
+#endif
   pdl_wait();
   pdl_trigger();
   if (clean_bins) {   // the binning is consumed: leave the bins zeroed for the next iteration (no memset)
@@ -700,11 +710,29 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   const int x = tx * kTile + 8 * (warp & 1) + (lane & 7);
   const int ya = ty * kTile + 8 * (warp >> 1) + (lane >> 3), yb = ya + 4;
   const bool in_a = x < W && ya < H, in_b = x < W && yb < H;
+#ifdef GSF_TRK_PREFETCH
+  if (loss_rgb) {
+    const uint32_t so = static_cast<uint32_t>(__cvta_generic_to_shared(&s_obs[tid][0]));
+    if (in_a) {
+      const int64_t pa = static_cast<int64_t>(ya) * W + x;
+      for (int ch = 0; ch < 3; ++ch) cp_async4_to(so + 4u * ch, loss_rgb + 3 * pa + ch);
+      if (loss_depth) cp_async4_to(so + 24u, loss_depth + pa);
+    }
+    if (in_b) {
+      const int64_t pb = static_cast<int64_t>(yb) * W + x;
+      for (int ch = 0; ch < 3; ++ch) cp_async4_to(so + 12u + 4u * ch, loss_rgb + 3 * pb + ch);
+      if (loss_depth) cp_async4_to(so + 28u, loss_depth + pb);
+    }
+    cp_async_commit();
+  }
+#endif
   const int2 rg = ranges[tile];
   float2 rg_a = make_float2(0.f, 0.f), bd_a = rg_a, rg_b = rg_a, bd_b = rg_a;
   // a pixel is done once T < term (T never grows); pixels outside the image start done (T = 0)
   float2 op = make_float2(0.f, 0.f), T = make_float2(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);
   int last_a = 0, last_b = 0;
+  int lc_a = 0, lc_b = 0;   // the same, as positions in this warp's work list (qlist)
+  const int64_t qbase = 4 * static_cast<int64_t>(rg.x) + static_cast<int64_t>(warp) * (rg.y - rg.x);
   float px = static_cast<float>(x) + 0.5f;
   float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
   const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
@@ -720,7 +748,6 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         s_id[e] = id;
         const uint8_t mk = static_cast<uint8_t>(warp_block_mask8(gj, tile_x0, tile_y0, kc));
         s_mask[e] = mk;
-        if (emask) emask[j] = mk;   // the pose backward's block test
       }
     }
     __syncthreads();
@@ -729,10 +756,15 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       if (__all_sync(0xffffffffu, T.x < kc.term && T.y < kc.term)) break;
       const int kk = c0 + lane;
       uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
+      // the pose backward's work list: this block's entries in list order (its only staging input)
+      if (QM != 0 && ((bits >> lane) & 1u))
+        qlist[qbase + wsteps + static_cast<uint32_t>(__popc(bits & ((1u << lane) - 1u)))] = static_cast<uint32_t>(s_id[kk]);
+      uint32_t ci = wsteps;
       wsteps += __popc(bits);
       while (bits) {
         const int k = c0 + __ffs(bits) - 1;
         bits &= bits - 1u;
+        ++ci;
 #ifndef GSF_NO_PIN_PX
         // keep the pixel centres in registers: at the 64-register cap ptxas otherwise re-forms
         // them with I2F + FADD (XU pipe) on every step
@@ -767,9 +799,15 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         bd_b = __ffma2_rn(make_float2(w.y, w.y), make_float2(g.b, g.depth), bd_b);
         op = __fadd2_rn(op, w);
         T = __fmul2_rn(T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-am.x, -am.y)));
-        const int li = start + k - rg.x + 1;
-        if (ca) last_a = li;
-        if (cb) last_b = li;
+        if (QM != 1) {
+          const int li = start + k - rg.x + 1;
+          if (ca) last_a = li;
+          if (cb) last_b = li;
+        }
+        if (QM != 0) {
+          if (ca) lc_a = static_cast<int>(ci);
+          if (cb) lc_b = static_cast<int>(ci);
+        }
       }
     }
   }
@@ -778,6 +816,13 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   double v[LS_NUM], vb[LS_NUM];
 #pragma unroll
   for (int q = 0; q < LS_NUM; ++q) v[q] = vb[q] = 0.0;
+#ifdef GSF_TRK_PREFETCH
+  if (loss_rgb) cp_async_wait_all();
+  const float* Ia = &s_obs[tid][0];
+  const float* Ib = &s_obs[tid][3];
+  const float* Dl = loss_depth ? &s_obs[tid][6] : nullptr;
+  const int64_t da = 0, db = 1;
+#endif
   if (in_a) {
     const int64_t pi = static_cast<int64_t>(ya) * W + x;
     if (o_color) {
@@ -788,12 +833,18 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       o_op[pi] = op.x;
     }
     o_T[pi] = T.x;
-    o_last[pi] = last_a;
+    if (QM != 1) o_last[pi] = last_a;
+    if (QM != 0) o_lastc[pi] = lc_a;
+#ifndef GSF_TRK_PREFETCH
+    const float* Ia = loss_rgb + 3 * pi;
+    const float* Dl = loss_depth;
+    const int64_t da = pi;
+#endif
     if (loss_rgb)
-      loss_pixel<1>(v, rg_a.x, rg_a.y, bd_a.x, bd_a.y, 0.0f, false, op.x, 0.0f, loss_rgb + 3 * pi, loss_depth, pi, false,
+      loss_pixel<1>(v, rg_a.x, rg_a.y, bd_a.x, bd_a.y, 0.0f, false, op.x, 0.0f, Ia, Dl, da, false,
                     near_plane, far_plane, lp.opacity_floor);
     if (o_code)
-      o_code[pi] = pixel_seed_code(rg_a.x, rg_a.y, bd_a.x, bd_a.y, op.x, loss_rgb + 3 * pi, loss_depth, pi, near_plane,
+      o_code[pi] = pixel_seed_code(rg_a.x, rg_a.y, bd_a.x, bd_a.y, op.x, Ia, Dl, da, near_plane,
                                    far_plane, lp.opacity_floor);
   }
   if (in_b) {
@@ -806,12 +857,18 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       o_op[pi] = op.y;
     }
     o_T[pi] = T.y;
-    o_last[pi] = last_b;
+    if (QM != 1) o_last[pi] = last_b;
+    if (QM != 0) o_lastc[pi] = lc_b;
+#ifndef GSF_TRK_PREFETCH
+    const float* Ib = loss_rgb + 3 * pi;
+    const float* Dl = loss_depth;
+    const int64_t db = pi;
+#endif
     if (loss_rgb)
-      loss_pixel<1>(vb, rg_b.x, rg_b.y, bd_b.x, bd_b.y, 0.0f, false, op.y, 0.0f, loss_rgb + 3 * pi, loss_depth, pi, false,
+      loss_pixel<1>(vb, rg_b.x, rg_b.y, bd_b.x, bd_b.y, 0.0f, false, op.y, 0.0f, Ib, Dl, db, false,
                     near_plane, far_plane, lp.opacity_floor);
     if (o_code)
-      o_code[pi] = pixel_seed_code(rg_b.x, rg_b.y, bd_b.x, bd_b.y, op.y, loss_rgb + 3 * pi, loss_depth, pi, near_plane,
+      o_code[pi] = pixel_seed_code(rg_b.x, rg_b.y, bd_b.x, bd_b.y, op.y, Ib, Dl, db, near_plane,
                                    far_plane, lp.opacity_floor);
   }
   if (!loss_rgb) return;
@@ -933,15 +990,19 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     // and the entries' block masks are kept for the backward
     const bool sl = a.want_posejac;
     if (a.join_order) GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_ljoin, 0));
-    launch_pdl(k_blend_track, dim3(ntiles), dim3(kTrkThreads), 0, st, ws.ranges, sl ? ws.sslot : ws.sid, sl ? ws.bg_slot : ws.bg_id,
-                                                  sl ? ws.gg_slot : ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,
-                                                  tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds,
-                                                  a.keep_maps ? ws.color : nullptr, ws.alpha_depth, ws.opacity, ws.final_T,
-                                                  ws.last, ws.loss_part,
-                                                  a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket,
-                                                  sl ? ws.emask : nullptr, sl ? ws.pxcode : nullptr,
-                                                  a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride,
-                                                  a.order, sl ? ws.qstat : nullptr);
+    const int qm = sl ? a.qmode : 0;
+#define GSF_BLEND_TRACK(QMV)                                                                                           \
+    launch_pdl(k_blend_track<QMV>, dim3(ntiles), dim3(kTrkThreads), 0, st, ws.ranges, sl ? ws.sslot : ws.sid,          \
+               sl ? ws.bg_slot : ws.bg_id, sl ? ws.gg_slot : ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H, tiles_x, a.kc, \
+               a.near_plane, a.far_plane, a.lp, ds, a.keep_maps ? ws.color : nullptr, ws.alpha_depth, ws.opacity,       \
+               ws.final_T, ws.last, ws.loss_part, a.fuse_loss_final ? 1 : 0, a.iteration,                              \
+               ws.bin_counters + kCntBlendTicket, ws.qlist, ws.lastc, sl ? ws.pxcode : nullptr,                        \
+               a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride, a.order,               \
+               sl ? ws.qstat : nullptr)
+    if (qm == 1) GSF_BLEND_TRACK(1);
+    else if (qm == 2) GSF_BLEND_TRACK(2);
+    else GSF_BLEND_TRACK(0);
+#undef GSF_BLEND_TRACK
   }
   else if (a.lp.mode == 2 && loss_rgb)
     launch_pdl(k_blend<2>, dim3(ntiles), dim3(256), 0, st, GSF_BLEND_ARGS);
