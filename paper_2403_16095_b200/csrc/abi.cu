@@ -1174,7 +1174,9 @@ int gsf_mapping_loss(gsf_ctx c, const float* target, const float* depth, const g
     if (w->w_ssim > 0.0) run_ssim(ws, c->ds, ws.color, tgt, k.width, k.height, 1.0f, ws.dssim, c->stream, &c->launches);
     run_iso(ws, c->ds, c->params, c->P, w->w_iso, w->iso_epsilon, nullptr, c->stream, &c->launches);
     run_loss_finalize(ws, c->ds, lp, tiles, npix, -1, c->stream, &c->launches);
-    float* sout = ws.ssim_tmp + 15 * npix;   // 6 planes after the SSIM scratch's first 15 planes
+    // 6 seed planes in the SSIM scratch (9 planes): its adjoint seeds u were consumed by k_ssim_bwd,
+    // which precedes this on the stream; the seeds read the SSIM gradient from ws.dssim
+    float* sout = ws.ssim_tmp;
     run_seeds_out(ws, c->ds, 2, tgt, dep, lp, k.width, k.height, k.near_plane, k.far_plane, sout, c->stream, &c->launches);
     if (d_ls_direct && c->P > 0) {
       GSF_CUDA_CHECK(cudaMemsetAsync(c->grads, 0, sizeof(float) * c->P * c->D, c->stream));

@@ -226,6 +226,231 @@ __global__ void __launch_bounds__(256) k_ssim_bwd(const float* __restrict__ u, c
   }
 }
 
+// Register-blocked, channel-at-a-time SSIM (same maths as k_ssim_fwd / k_ssim_bwd).  The forward
+// stages the six input planes of the 32x16 block (+5 px halo) once; then per channel the horizontal
+// pass gives each thread 4 consecutive outputs of one row (14 input columns read once, the 5 product
+// maps a, b, a^2, b^2, ab formed once per input, 11 taps per output from the constant window) and
+// the vertical pass 2 consecutive rows of one column (12 staged rows read once), followed by the
+// per-pixel fp64 SSIM of those two pixels.  The adjoint runs the same blocking per channel over its
+// three seed planes (vertical: 4 rows x 1 column, horizontal: 2 columns x 1 row).
+constexpr int kHG = 4;                   // horizontal outputs per thread
+constexpr int kHItems = kSHh * (kSX / kHG);   // 26 rows x 8 groups = 208
+constexpr size_t ssim_fwd2_smem() { return sizeof(float) * (6 * kSHh * kSW + 5 * kSHh * kSX); }
+constexpr size_t ssim_bwd2_smem() { return sizeof(float) * (3 * kSHh * kSW + 3 * kSY * kSW); }
+
+__global__ void __launch_bounds__(256) k_ssim_fwd2(const float* __restrict__ x, const float* __restrict__ y, int W, int H,
+                                                   double weight, float* __restrict__ u, double* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float s_buf[];
+  float (*s_in)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                  // x0..2, y0..2
+  float (*s_h)[kSHh][kSX] = reinterpret_cast<float (*)[kSHh][kSX]>(s_buf + 6 * kSHh * kSW);   // 5 planes, one channel
+  __shared__ double s_red[8];
+  __shared__ float s_izx[kSX];
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < kSHh * kSW; idx += 256) {
+    const int r = idx / kSW, c = idx - r * kSW;
+    const int gx = bx - kR + c, gy = by - kR + r;
+    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+    const int64_t j = static_cast<int64_t>(gy) * W + gx;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      s_in[ch][r][c] = in ? x[3 * j + ch] : 0.0f;
+      s_in[3 + ch][r][c] = in ? y[3 * j + ch] : 0.0f;
+    }
+  }
+  if (tid < kSX) s_izx[tid] = 1.0f / axis_norm(min(bx + tid, W - 1), W);
+  // vertical-pass pixels of this thread: column vc, rows 2 vr and 2 vr + 1
+  const int vc = tid & (kSX - 1), vr = tid >> 5;
+  const int gx = bx + vc;
+  double izy[2];
+  bool vin[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int gy = by + 2 * vr + j;
+    vin[j] = gx < W && gy < H;
+    izy[j] = vin[j] ? 1.0 / static_cast<double>(axis_norm(gy, H)) : 0.0;
+  }
+  double ssum = 0.0;
+  __syncthreads();
+  for (int ch = 0; ch < 3; ++ch) {
+    if (tid < kHItems) {   // horizontal pass: row hr, outputs hx .. hx + 3
+      const int hr = tid / (kSX / kHG), hx = (tid - hr * (kSX / kHG)) * kHG;
+      float acc[5][kHG];
+#pragma unroll
+      for (int q = 0; q < 5; ++q)
+#pragma unroll
+        for (int j = 0; j < kHG; ++j) acc[q][j] = 0.0f;
+#pragma unroll
+      for (int p = 0; p < kHG + 2 * kR; ++p) {
+        const float a = s_in[ch][hr][hx + p], b = s_in[3 + ch][hr][hx + p];
+        const float v[5] = {a, b, a * a, b * b, a * b};
+#pragma unroll
+        for (int j = 0; j < kHG; ++j) {
+          const int o = p - j;
+          if (o >= 0 && o <= 2 * kR) {
+            const float w = c_win[o];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) acc[q][j] += w * v[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        float4 o4;
+        o4.x = acc[q][0] * s_izx[hx];
+        o4.y = acc[q][1] * s_izx[hx + 1];
+        o4.z = acc[q][2] * s_izx[hx + 2];
+        o4.w = acc[q][3] * s_izx[hx + 3];
+        *reinterpret_cast<float4*>(&s_h[q][hr][hx]) = o4;
+      }
+    }
+    __syncthreads();
+    {   // vertical pass + per-pixel SSIM of (vc, 2 vr) and (vc, 2 vr + 1)
+      float acc[5][2];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) acc[q][0] = acc[q][1] = 0.0f;
+#pragma unroll
+      for (int p = 0; p < 2 + 2 * kR; ++p) {
+        float v[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) v[q] = s_h[q][2 * vr + p][vc];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int o = p - j;
+          if (o >= 0 && o <= 2 * kR) {
+            const float w = c_win[o];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) acc[q][j] += w * v[q];
+          }
+        }
+      }
+      const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (!vin[j]) continue;
+        const int64_t i = static_cast<int64_t>(by + 2 * vr + j) * W + gx;
+        const double mx = acc[0][j] * izy[j], my = acc[1][j] * izy[j], ex2 = acc[2][j] * izy[j],
+                     ey2 = acc[3][j] * izy[j], exy = acc[4][j] * izy[j];
+        const double a1 = 2.0 * mx * my + C1;
+        const double a2 = 2.0 * (exy - mx * my) + C2;
+        const double b1 = mx * mx + my * my + C1;
+        const double b2 = (ex2 - mx * mx) + (ey2 - my * my) + C2;
+        const double idn = 1.0 / (b1 * b2);
+        const double sv = a1 * a2 * idn;
+        ssum += sv;
+        if (u) {
+          const double d_a1 = a2 * idn, d_a2 = a1 * idn, d_b1 = -sv * b2 * idn, d_b2 = -sv * b1 * idn;
+          u[ch * npix + i] = static_cast<float>((2.0 * my * d_a1 - 2.0 * my * d_a2 + 2.0 * mx * d_b1 - 2.0 * mx * d_b2) * weight);
+          u[(3 + ch) * npix + i] = static_cast<float>(d_b2 * weight);
+          u[(6 + ch) * npix + i] = static_cast<float>(2.0 * d_a2 * weight);
+        }
+      }
+    }
+    __syncthreads();   // s_h is rewritten by the next channel's horizontal pass
+  }
+  const double t = block_sum_d(ssum, s_red);
+  if (tid == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = t;
+}
+
+constexpr int kVG = 4;   // adjoint vertical outputs per thread (rows)
+
+__global__ void __launch_bounds__(256) k_ssim_bwd2(const float* __restrict__ u, const float* __restrict__ x,
+                                                   const float* __restrict__ y, int W, int H, float* __restrict__ dx) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float s_buf[];
+  float (*s_u)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                    // 3 planes + halo
+  float (*s_t)[kSY][kSW] = reinterpret_cast<float (*)[kSY][kSW]>(s_buf + 3 * kSHh * kSW);     // after the vertical pass
+  __shared__ float s_wy[kSY][2 * kR + 1], s_wx[kSX][2 * kR + 1];
+  const int64_t npix = static_cast<int64_t>(W) * H;
+  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < (kSY + kSX) * (2 * kR + 1); idx += 256) {
+    const int row = idx / (2 * kR + 1), o = idx - row * (2 * kR + 1) - kR;
+    if (row < kSY) {
+      const int yy = by + row + o;
+      s_wy[row][o + kR] = (yy >= 0 && yy < H) ? c_win[o + kR] / axis_norm(yy, H) : 0.0f;
+    } else {
+      const int xx = bx + (row - kSY) + o;
+      s_wx[row - kSY][o + kR] = (xx >= 0 && xx < W) ? c_win[o + kR] / axis_norm(xx, W) : 0.0f;
+    }
+  }
+  // horizontal-pass pixels of this thread: row hr, columns 2 hc and 2 hc + 1
+  const int hr = tid >> 4, hc = (tid & 15) * 2;
+  for (int ch = 0; ch < 3; ++ch) {
+    __syncthreads();   // s_u / s_t of the previous channel are consumed
+    for (int idx = tid; idx < kSHh * kSW; idx += 256) {
+      const int r = idx / kSW, c = idx - r * kSW;
+      const int gx = bx - kR + c, gy = by - kR + r;
+      const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+      const int64_t j = static_cast<int64_t>(gy) * W + gx;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) s_u[q][r][c] = in ? u[(3 * q + ch) * npix + j] : 0.0f;
+    }
+    __syncthreads();
+    for (int item = tid; item < (kSY / kVG) * kSW; item += 256) {   // vertical adjoint: column c, rows r0 .. r0 + 3
+      const int c = item % kSW, r0 = (item / kSW) * kVG;
+      float acc[3][kVG];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int j = 0; j < kVG; ++j) acc[q][j] = 0.0f;
+#pragma unroll
+      for (int p = 0; p < kVG + 2 * kR; ++p) {
+        float v[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[q] = s_u[q][r0 + p][c];
+#pragma unroll
+        for (int j = 0; j < kVG; ++j) {
+          const int o = p - j;
+          if (o >= 0 && o <= 2 * kR) {
+            const float w = s_wy[r0 + j][o];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) acc[q][j] += w * v[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int j = 0; j < kVG; ++j) s_t[q][r0 + j][c] = acc[q][j];
+    }
+    __syncthreads();
+    {   // horizontal adjoint of (hc, hr), (hc + 1, hr)
+      float acc[3][2];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc[q][0] = acc[q][1] = 0.0f;
+#pragma unroll
+      for (int p = 0; p < 2 + 2 * kR; ++p) {
+        float v[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[q] = s_t[q][hr][hc + p];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int o = p - j;
+          if (o >= 0 && o <= 2 * kR) {
+            const float w = s_wx[hc + j][o];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) acc[q][j] += w * v[q];
+          }
+        }
+      }
+      const int gy = by + hr;   // d_x = a0 + 2 a1 x + a2 y for this channel
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int gxx = bx + hc + j;
+        if (gxx < W && gy < H) {
+          const int64_t i = static_cast<int64_t>(gy) * W + gxx;
+          dx[3 * i + ch] = acc[0][j] + 2.0f * acc[1][j] * x[3 * i + ch] + acc[2][j] * y[3 * i + ch];
+        }
+      }
+    }
+  }
+}
+
 // small-image fallback: global statistics (ssim.cpp:117-144), one block
 __global__ void __launch_bounds__(256) k_ssim_global(const float* __restrict__ x, const float* __restrict__ y, int64_t n,
                                                      float* __restrict__ dx, double* part) {
@@ -342,17 +567,30 @@ void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W
                                         static_cast<int>(ssim_fwd_smem())));
     GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(ssim_bwd_smem())));
+    GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ssim_fwd2_smem())));
+    GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_bwd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(ssim_bwd2_smem())));
     attr = true;
   }
   const dim3 grid(div_up(W, kSX), div_up(H, kSY));
   float* u = ws.ssim_tmp;                 // 9 adjoint seed planes
   if (ws.prof) ws.prof->begin(PROF_SSIM, st);
+#ifndef GSF_SSIM2
   launch_pdl(k_ssim_fwd, grid, dim3(256), ssim_fwd_smem(), st, x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr,
                                                  ws.red_part);
+#else
+  launch_pdl(k_ssim_fwd2, grid, dim3(256), ssim_fwd2_smem(), st, x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)),
+             d_out ? u : nullptr, ws.red_part);
+#endif
   ++*L;
   ws.ssim_blocks = static_cast<int>(grid.x * grid.y);
   if (d_out) {
+#ifndef GSF_SSIM2
     launch_pdl(k_ssim_bwd, grid, dim3(256), ssim_bwd_smem(), st, u, x, y, W, H, d_out);
+#else
+    launch_pdl(k_ssim_bwd2, grid, dim3(256), ssim_bwd2_smem(), st, u, x, y, W, H, d_out);
+#endif
     ++*L;
   }
   if (ws.prof) ws.prof->end(st);

@@ -9,7 +9,9 @@ import json,sys
 v=sys.argv[1]
 try:
   d=json.loads(open(f"gpurun_out/abm_{v}.json").read().strip().splitlines()[-1]); m=d['mapping']
-  print(v, 'track', round(d['value'],3), 'sliding_ba', round(m['value'],2), 'it/s', round(m['ms_per_iter'],3), 'ms  map_step', round(m['map_step_it_per_s'],1))
+  k=m.get('kernels',{})
+  print(v, 'track', round(d['value'],3), 'sliding_ba', round(m['value'],2), 'it/s', round(m['ms_per_iter'],3), 'ms  map_step', round(m['map_step_it_per_s'],1),
+        ' '.join(f"{n}={k[n]['avg_ms']*1e3:.1f}" for n in k if isinstance(k[n], dict)))
 except Exception as e: print(v,'FAILED',e)
 PY
 done
