@@ -60,7 +60,6 @@ struct Workspace {
   // before the blend); created with the context
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  bool join_pending = false;   // GSF_LATE_JOIN: the k_posejac branch is joined before the pose backward
   // tracking: longest-first CTA order of the tile kernels (k_lpt, from the previous iteration's
   // per-quadrant step counts) on a second side branch: fork after the backward, join before the
   // next blend.  Two buffers of [1 + 5 tiles_cap]: [0] = the tile count the orders were built for

@@ -62,171 +62,14 @@ __device__ __forceinline__ float axis_norm(int p, int n) {
   return z;
 }
 
-// SSIM (ssim.cpp:27-187), tiled: a CTA owns a 32x16 block of pixels, stages its inputs with a
-// 5-pixel halo in shared memory and runs both separable blur passes there (horizontal over the 15
-// product maps x, y, xx, yy, xy per channel, then vertical + the per-pixel fp64 SSIM and its three
-// adjoint seed maps; the adjoint blurs vertical first, then horizontal, each tap divided by its
-// own border normaliser, ssim.cpp:60-80).  Out-of-image taps read 0, which adds w*0 exactly like
-// the reference's skipped taps.
+// SSIM (ssim.cpp:27-187), tiled: a CTA owns a 32x16 block of pixels and stages its inputs with a
+// 5-pixel halo in shared memory; both separable blur passes run there (out-of-image taps read 0,
+// which adds w*0 exactly like the reference's skipped taps), the per-pixel SSIM and its three
+// adjoint seed maps in fp64; the adjoint blurs vertical first, then horizontal, each tap divided by
+// its own border normaliser (ssim.cpp:60-80).
 constexpr int kSX = 32, kSY = 16, kSW = kSX + 2 * kR, kSHh = kSY + 2 * kR;
 
-constexpr size_t ssim_fwd_smem() { return sizeof(float) * (6 * kSHh * kSW + 15 * kSHh * kSX); }
-constexpr size_t ssim_bwd_smem() { return sizeof(float) * (9 * kSHh * kSW + 9 * kSY * kSW); }
-
-__global__ void __launch_bounds__(256) k_ssim_fwd(const float* __restrict__ x, const float* __restrict__ y, int W, int H,
-                                                  double weight, float* __restrict__ u, double* __restrict__ part) {
-  pdl_wait();   // PDL: the predecessor's results are complete from here
-  pdl_trigger();
-  extern __shared__ float s_buf[];
-  float (*s_in)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                  // x0..2, y0..2
-  float (*s_h)[kSHh][kSX] = reinterpret_cast<float (*)[kSHh][kSX]>(s_buf + 6 * kSHh * kSW);   // 15 planes
-  __shared__ double s_red[8];
-  const int64_t npix = static_cast<int64_t>(W) * H;
-  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < kSHh * kSW; idx += 256) {
-    const int r = idx / kSW, c = idx - r * kSW;
-    const int gx = bx - kR + c, gy = by - kR + r;
-    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
-    const int64_t j = static_cast<int64_t>(gy) * W + gx;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      s_in[ch][r][c] = in ? x[3 * j + ch] : 0.0f;
-      s_in[3 + ch][r][c] = in ? y[3 * j + ch] : 0.0f;
-    }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < kSHh * kSX; idx += 256) {   // horizontal pass (k_ssim_h)
-    const int r = idx / kSX, c = idx - r * kSX;
-    const float izx = 1.0f / axis_norm(min(bx + c, W - 1), W);
-    float acc[15];
-#pragma unroll
-    for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
-#pragma unroll
-    for (int o = -kR; o <= kR; ++o) {
-      const float w = c_win[o + kR];
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        const float a = s_in[ch][r][c + kR + o], b = s_in[3 + ch][r][c + kR + o];
-        acc[ch] += w * a;
-        acc[3 + ch] += w * b;
-        acc[6 + ch] += w * (a * a);
-        acc[9 + ch] += w * (b * b);
-        acc[12 + ch] += w * (a * b);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 15; ++q) s_h[q][r][c] = acc[q] * izx;
-  }
-  __syncthreads();
-  double ssum = 0.0;
-  for (int idx = tid; idx < kSY * kSX; idx += 256) {   // vertical pass + per-pixel SSIM (k_ssim_v)
-    const int r = idx / kSX, c = idx - r * kSX;
-    const int gx = bx + c, gy = by + r;
-    if (gx >= W || gy >= H) continue;
-    const int64_t i = static_cast<int64_t>(gy) * W + gx;
-    const double izy = 1.0 / static_cast<double>(axis_norm(gy, H));
-    float acc[15];
-#pragma unroll
-    for (int q = 0; q < 15; ++q) acc[q] = 0.0f;
-#pragma unroll
-    for (int o = -kR; o <= kR; ++o) {
-      const float w = c_win[o + kR];
-#pragma unroll
-      for (int q = 0; q < 15; ++q) acc[q] += w * s_h[q][r + kR + o][c];
-    }
-    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      const double mx = acc[ch] * izy, my = acc[3 + ch] * izy, ex2 = acc[6 + ch] * izy, ey2 = acc[9 + ch] * izy,
-                   exy = acc[12 + ch] * izy;
-      const double a1 = 2.0 * mx * my + C1;
-      const double a2 = 2.0 * (exy - mx * my) + C2;
-      const double b1 = mx * mx + my * my + C1;
-      const double b2 = (ex2 - mx * mx) + (ey2 - my * my) + C2;
-      const double idn = 1.0 / (b1 * b2);   // one fp64 reciprocal per channel instead of six divisions
-      const double sv = a1 * a2 * idn;
-      ssum += sv;
-      if (u) {
-        // d sv / d b1 = -sv / b1 = -sv b2 / (b1 b2), likewise for b2
-        const double d_a1 = a2 * idn, d_a2 = a1 * idn, d_b1 = -sv * b2 * idn, d_b2 = -sv * b1 * idn;
-        u[ch * npix + i] = static_cast<float>((2.0 * my * d_a1 - 2.0 * my * d_a2 + 2.0 * mx * d_b1 - 2.0 * mx * d_b2) * weight);
-        u[(3 + ch) * npix + i] = static_cast<float>(d_b2 * weight);
-        u[(6 + ch) * npix + i] = static_cast<float>(2.0 * d_a2 * weight);
-      }
-    }
-  }
-  const double t = block_sum_d(ssum, s_red);
-  if (tid == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = t;
-}
-
-__global__ void __launch_bounds__(256) k_ssim_bwd(const float* __restrict__ u, const float* __restrict__ x,
-                                                  const float* __restrict__ y, int W, int H, float* __restrict__ dx) {
-  pdl_wait();   // PDL: the predecessor's results are complete from here
-  pdl_trigger();
-  extern __shared__ float s_buf[];
-  float (*s_u)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                    // 9 planes + halo
-  float (*s_t)[kSY][kSW] = reinterpret_cast<float (*)[kSY][kSW]>(s_buf + 9 * kSHh * kSW);     // after the vertical pass
-  // per-tap adjoint weights c_win[o] / axis_norm(neighbour) (ssim.cpp:60-80), 0 outside the image:
-  // rows of this CTA's block (vertical) and its columns (horizontal), one table each
-  __shared__ float s_wy[kSY][2 * kR + 1], s_wx[kSX][2 * kR + 1];
-  const int64_t npix = static_cast<int64_t>(W) * H;
-  const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < (kSY + kSX) * (2 * kR + 1); idx += 256) {
-    const int row = idx / (2 * kR + 1), o = idx - row * (2 * kR + 1) - kR;
-    if (row < kSY) {
-      const int yy = by + row + o;
-      s_wy[row][o + kR] = (yy >= 0 && yy < H) ? c_win[o + kR] / axis_norm(yy, H) : 0.0f;
-    } else {
-      const int xx = bx + (row - kSY) + o;
-      s_wx[row - kSY][o + kR] = (xx >= 0 && xx < W) ? c_win[o + kR] / axis_norm(xx, W) : 0.0f;
-    }
-  }
-  for (int idx = tid; idx < kSHh * kSW; idx += 256) {
-    const int r = idx / kSW, c = idx - r * kSW;
-    const int gx = bx - kR + c, gy = by - kR + r;
-    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
-    const int64_t j = static_cast<int64_t>(gy) * W + gx;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) s_u[q][r][c] = in ? u[q * npix + j] : 0.0f;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < kSY * kSW; idx += 256) {   // vertical adjoint (k_ssim_adj_v)
-    const int r = idx / kSW, c = idx - r * kSW;
-    float acc[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
-#pragma unroll
-    for (int o = -kR; o <= kR; ++o) {
-      const float w = s_wy[r][o + kR];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] += w * s_u[q][r + kR + o][c];
-    }
-#pragma unroll
-    for (int q = 0; q < 9; ++q) s_t[q][r][c] = acc[q];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < kSY * kSX; idx += 256) {   // horizontal adjoint + d_x (k_ssim_adj_h)
-    const int r = idx / kSX, c = idx - r * kSX;
-    const int gx = bx + c, gy = by + r;
-    if (gx >= W || gy >= H) continue;
-    const int64_t i = static_cast<int64_t>(gy) * W + gx;
-    float acc[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] = 0.0f;
-#pragma unroll
-    for (int o = -kR; o <= kR; ++o) {
-      const float w = s_wx[c][o + kR];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] += w * s_t[q][r][c + kR + o];
-    }
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch) dx[3 * i + ch] = acc[ch] + 2.0f * acc[3 + ch] * x[3 * i + ch] + acc[6 + ch] * y[3 * i + ch];
-  }
-}
-
-// Register-blocked, channel-at-a-time SSIM (same maths as k_ssim_fwd / k_ssim_bwd).  The forward
+// Register-blocked and channel-at-a-time (85 us per 1200x680 view, 94 us for the all-planes version).  The forward
 // stages the six input planes of the 32x16 block (+5 px halo) once; then per channel the horizontal
 // pass gives each thread 4 consecutive outputs of one row (14 input columns read once, the 5 product
 // maps a, b, a^2, b^2, ab formed once per input, 11 taps per output from the constant window) and
@@ -563,10 +406,6 @@ void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W
   }
   static bool attr = false;
   if (!attr) {
-    GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ssim_fwd_smem())));
-    GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(ssim_bwd_smem())));
     GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(ssim_fwd2_smem())));
     GSF_CUDA_CHECK(cudaFuncSetAttribute(k_ssim_bwd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -576,21 +415,12 @@ void run_ssim(Workspace& ws, DevState* ds, const float* x, const float* y, int W
   const dim3 grid(div_up(W, kSX), div_up(H, kSY));
   float* u = ws.ssim_tmp;                 // 9 adjoint seed planes
   if (ws.prof) ws.prof->begin(PROF_SSIM, st);
-#ifndef GSF_SSIM2
-  launch_pdl(k_ssim_fwd, grid, dim3(256), ssim_fwd_smem(), st, x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)), d_out ? u : nullptr,
-                                                 ws.red_part);
-#else
   launch_pdl(k_ssim_fwd2, grid, dim3(256), ssim_fwd2_smem(), st, x, y, W, H, 1.0 / (3.0 * static_cast<double>(npix)),
              d_out ? u : nullptr, ws.red_part);
-#endif
   ++*L;
   ws.ssim_blocks = static_cast<int>(grid.x * grid.y);
   if (d_out) {
-#ifndef GSF_SSIM2
-    launch_pdl(k_ssim_bwd, grid, dim3(256), ssim_bwd_smem(), st, u, x, y, W, H, d_out);
-#else
     launch_pdl(k_ssim_bwd2, grid, dim3(256), ssim_bwd2_smem(), st, u, x, y, W, H, d_out);
-#endif
     ++*L;
   }
   if (ws.prof) ws.prof->end(st);

@@ -1073,10 +1073,6 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     bp.tile_pose = ws.pose_part;
     uint32_t* ticket = ws.bin_counters + kCntBwdTicket;
     bool fused_update = false;
-    if (ws.join_pending) {   // k_posejac's branch (pose Jacobians, slot-indexed records) joins here
-      GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_join, 0));
-      ws.join_pending = false;
-    }
     if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
 #define GSF_BWDP(SM, VD)                                                                                        \
   do {                                                                                                          \

@@ -679,10 +679,9 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
     uint32_t* __restrict__ qlist, int32_t* __restrict__ o_lastc, uint8_t* __restrict__ o_code, uint32_t* clean_bins,
     int64_t clean_cnt_off,
-    const uint32_t* __restrict__ order, int2* __restrict__ qstat, const uint32_t* __restrict__ qslot) {
+    const uint32_t* __restrict__ order, int2* __restrict__ qstat) {
   __shared__ BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
-  __shared__ uint32_t s_qs[QM != 0 ? kTrkBatch : 1];   // work-list values when the list holds ids (qslot)
   __shared__ uint8_t s_mask[kTrkBatch];
   __shared__ double s_red[kTrkThreads / 32][LS_NUM];
   pdl_wait();
@@ -726,7 +725,6 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         const BlendG gj = bg[id];
         s_g[e] = gj;
         s_id[e] = id;
-        if (QM != 0 && qslot) s_qs[e] = qslot[j];
         const uint8_t mk = static_cast<uint8_t>(warp_block_mask8(gj, tile_x0, tile_y0, kc));
         s_mask[e] = mk;
       }
@@ -739,8 +737,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
       // the pose backward's work list: this block's entries in list order (its only staging input)
       if (QM != 0 && ((bits >> lane) & 1u))
-        qlist[qbase + wsteps + static_cast<uint32_t>(__popc(bits & ((1u << lane) - 1u)))] =
-            qslot ? s_qs[kk] : static_cast<uint32_t>(s_id[kk]);
+        qlist[qbase + wsteps + static_cast<uint32_t>(__popc(bits & ((1u << lane) - 1u)))] = static_cast<uint32_t>(s_id[kk]);
       uint32_t ci = wsteps;
       wsteps += __popc(bits);
       while (bits) {
@@ -913,10 +910,6 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   const int tiles_x = a.rp.tiles_x, tiles_y = a.rp.tiles_y;
   const int ntiles = tiles_x * tiles_y;
   Profiler* pf = ws.prof;
-  if (ws.join_pending) {   // a previous tracking forward's k_posejac branch had no pose backward
-    GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_join, 0));
-    ws.join_pending = false;
-  }
   if (!a.bins_clean)
     GSF_CUDA_CHECK(cudaMemsetAsync(ws.bins, 0, sizeof(uint32_t) * (ws.tiles_cap * kBinStride + kCntNum), st));
   if (pf) pf->begin(PROF_PREPROCESS, st);
@@ -951,16 +944,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   if (pf) pf->begin(PROF_SORT, st);
   run_binning(ws, ds, P, tiles_x, ntiles, st, L, a.want_posejac);
   if (pf) pf->end(st);
-#ifdef GSF_LATE_JOIN
-  // the tracking blend reads id-indexed records (its work lists take the slots from ws.sslot), so only
-  // the pose backward needs k_posejac's outputs: the branch is joined there (run_backward)
-  const bool late = side && a.lp.mode == 1 && a.loss_rgb;
-  if (side && !late) GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_join, 0));
-  ws.join_pending = late;
-#else
   if (side) GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_join, 0));
-  const bool late = false;
-#endif
   const float* loss_rgb = a.loss_rgb;
 #define GSF_BLEND_ARGS                                                                                                 \
   ws.ranges, ws.sid, ws.bg_id, ws.gg_id, a.obs, loss_rgb, a.loss_depth, a.W, a.H,                                     \
@@ -976,14 +960,13 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     if (a.join_order) GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_ljoin, 0));
     const int qm = sl ? a.qmode : 0;
 #define GSF_BLEND_TRACK(QMV)                                                                                           \
-    launch_pdl(k_blend_track<QMV>, dim3(ntiles), dim3(kTrkThreads), 0, st, ws.ranges, sl && !late ? ws.sslot : ws.sid,  \
-               sl && !late ? ws.bg_slot : ws.bg_id, sl && !late ? ws.gg_slot : ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H,   \
-               tiles_x, a.kc,                                                                                           \
+    launch_pdl(k_blend_track<QMV>, dim3(ntiles), dim3(kTrkThreads), 0, st, ws.ranges, sl ? ws.sslot : ws.sid,          \
+               sl ? ws.bg_slot : ws.bg_id, sl ? ws.gg_slot : ws.gg_id, loss_rgb, a.loss_depth, a.W, a.H, tiles_x, a.kc, \
                a.near_plane, a.far_plane, a.lp, ds, a.keep_maps ? ws.color : nullptr, ws.alpha_depth, ws.opacity,       \
                ws.final_T, ws.last, ws.loss_part, a.fuse_loss_final ? 1 : 0, a.iteration,                              \
                ws.bin_counters + kCntBlendTicket, ws.qlist, ws.lastc, sl ? ws.pxcode : nullptr,                        \
                a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride, a.order,               \
-               sl ? ws.qstat : nullptr, late ? ws.sslot : nullptr)
+               sl ? ws.qstat : nullptr)
     if (qm == 1) GSF_BLEND_TRACK(1);
     else if (qm == 2) GSF_BLEND_TRACK(2);
     else GSF_BLEND_TRACK(0);
