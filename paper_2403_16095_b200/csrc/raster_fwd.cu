@@ -27,7 +27,7 @@ namespace {
 // Rows: rot0 rot1 rot2 trans0 trans1 trans2, so the kernel accumulates three float2 pairs with
 // packed FFMA2s.  In fp64: d = A s (A from J, Bc), rot = p_cam x d + Cr s_cov, trans = d.
 __device__ void compute_posejac(const float* __restrict__ p, int64_t stride, const Cam& cam, int K, float* out,
-                                const double* Sw) {
+                                const double* Sw, const BlendG* conic = nullptr) {
   const double m0 = p[0], m1 = p[stride], m2 = p[2 * stride];
   const double* W = cam.W;
   const double pc[3] = {W[0] * m0 + W[1] * m1 + W[2] * m2 + cam.t[0], W[3] * m0 + W[4] * m1 + W[5] * m2 + cam.t[1],
@@ -122,14 +122,39 @@ __device__ void compute_posejac(const float* __restrict__ p, int64_t stride, con
   const double A[3][6] = {{J00, 0.0, Bc[0][0], Bc[0][1], Bc[0][2], 0.0},
                           {0.0, J11, Bc[1][0], Bc[1][1], Bc[1][2], 0.0},
                           {J02, J12, Bc[2][0], Bc[2][1], Bc[2][2], 1.0}};
+  double Mc[6][6];
   for (int j = 0; j < 6; ++j) {
     const double d0 = A[0][j], d1 = A[1][j], d2 = A[2][j];
     double col[6] = {pc[1] * d2 - pc[2] * d1, pc[2] * d0 - pc[0] * d2, pc[0] * d1 - pc[1] * d0, d0, d1, d2};
     if (j >= 2 && j <= 4)
       for (int a = 0; a < 3; ++a) col[a] += Cr[a][j - 2];
     const double scale = (j >= 2 && j <= 4) ? 0.5 : 1.0;   // the kernel's s_cov carries no 1/2
-    for (int a = 0; a < 6; ++a) out[6 * j + a] = static_cast<float>(scale * col[a]);
+    for (int a = 0; a < 6; ++a) Mc[j][a] = scale * col[a];
   }
+  if (conic) {
+    // Columns re-expressed in the pixel-offset basis t = g (dx, dy, dx^2, dx dy, dy^2) the two-pixel
+    // pose backward forms directly: with the record's conic (c00, c01, c11) the screen partials are
+    // s0 = c00 t0 + c01 t1, s1 = c01 t0 + c11 t1, s2 = g ux^2, s3 = g ux uy, s4 = g uy^2 (ux, uy linear in dx, dy)
+    const double c00 = conic->c00, c01 = 0.5 * static_cast<double>(conic->c01x2), c11 = conic->c11;
+    double N[5][6];
+    for (int a = 0; a < 6; ++a) {
+      N[0][a] = c00 * Mc[0][a] + c01 * Mc[1][a];
+      N[1][a] = c01 * Mc[0][a] + c11 * Mc[1][a];
+      N[2][a] = c00 * c00 * Mc[2][a] + c00 * c01 * Mc[3][a] + c01 * c01 * Mc[4][a];
+      N[3][a] = 2.0 * c00 * c01 * Mc[2][a] + (c00 * c11 + c01 * c01) * Mc[3][a] + 2.0 * c01 * c11 * Mc[4][a];
+      N[4][a] = c01 * c01 * Mc[2][a] + c01 * c11 * Mc[3][a] + c11 * c11 * Mc[4][a];
+    }
+#ifdef GSF_SIGFOLD
+    // ... and scaled by the primitive's opacity sigma, which multiplies every (dx, dy)-basis partial
+    const double sg = conic->sigma;
+#else
+    const double sg = 1.0;
+#endif
+    for (int j = 0; j < 5; ++j)
+      for (int a = 0; a < 6; ++a) Mc[j][a] = sg * N[j][a];
+  }
+  for (int j = 0; j < 6; ++j)
+    for (int a = 0; a < 6; ++a) out[6 * j + a] = static_cast<float>(Mc[j][a]);
   for (int c = 0; c < 3; ++c)
     for (int a = 0; a < 6; ++a) out[36 + 6 * c + a] = a < 3 ? 0.0f : static_cast<float>(Tc[a - 3][c]);
   out[54] = out[55] = 0.0f;
@@ -406,7 +431,10 @@ __global__ void __launch_bounds__(kPjThreads, GSF_PJ_MINB) k_posejac(const float
     bg_slot[r] = bg_id[id];   // the tracking kernels read records by visible slot (compact, no id hop)
     gg_slot[r] = gg_id[id];
     float v[kPjFloats];
-    compute_posejac(params + id, P, ds->cam, K, v, world ? world[id].S : nullptr);
+    // K == 1: columns in the two-pixel backward's offset basis (k_backward_track_w); the view-dependent
+    // pose backward (k_backward_pose) takes the screen-partial basis
+    const BlendG rec = bg_id[id];
+    compute_posejac(params + id, P, ds->cam, K, v, world ? world[id].S : nullptr, K == 1 ? &rec : nullptr);
 #pragma unroll
     for (int q = 0; q < kPjFloats; ++q) s_out[threadIdx.x * (kPjFloats + 1) + q] = v[q];
   }
