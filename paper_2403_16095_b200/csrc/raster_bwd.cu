@@ -522,11 +522,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   // one staging buffer: 32 records (3 float4), 32 pose matrices (9 float4), 32 slots
   // two staging buffers of 16 entries: records (3 float4) at +0, pose matrices (9 float4) at +768 B;
   // their slots at 6144 + 64 b
-#ifdef GSF_TBW_BULK
-  __shared__ float4 s_buf[2 * 16 * 12 + 8 + 1];   // + two mbarriers (one per buffer) at 6272
-#else
   __shared__ float4 s_buf[2 * 16 * 12 + 8];
-#endif
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x;
@@ -571,36 +567,6 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         }
       }
     };
-#ifdef GSF_TBW_BULK
-    // TMA bulk copies: one 48 B record (lanes 0..15) or one 144 B pose matrix (lanes 16..31) per
-    // entry, completing on the buffer's mbarrier; chunk c waits on phase (c >> 1) & 1
-    const uint32_t bar0 = sb + 6272u;
-    if (lane == 0) {
-      mbar_init(bar0, 1u);
-      mbar_init(bar0 + 8u, 1u);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");   // visible to the async proxy
-    }
-    __syncwarp();
-    auto issue = [&](int c, uint32_t m, uint32_t sl) {
-      if (c < nch) {
-        const int e = lane & 15;
-        const uint32_t me = __shfl_sync(0xffffffffu, m, e), se = __shfl_sync(0xffffffffu, sl, e);
-        const uint32_t bar = bar0 + 8u * static_cast<uint32_t>(c & 1);
-        const uint32_t cnt = static_cast<uint32_t>(min(kC, E - kC * c));
-        if (lane == 0) mbar_arrive_expect_tx(bar, cnt * 192u);
-        __syncwarp();
-        if (me) {
-          const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 3072u;
-          if (lane < 16) {
-            bulk_copy_to(buf + 48u * e, bp.bg_slot + se, 48u, bar);
-            sts_s32(sb + 6144u + static_cast<uint32_t>(c & 1) * 64u + 4u * e, static_cast<int32_t>(se));
-          } else {
-            bulk_copy_to(buf + 768u + 144u * e, bp.pj + static_cast<size_t>(kPjFloats) * se, 144u, bar);
-          }
-        }
-      }
-    };
-#else
     auto issue = [&](int c, uint32_t m, uint32_t sl) {
       if (c < nch) {
         const int e = lane & 15;
@@ -620,7 +586,6 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       }
       cp_async_commit();
     };
-#endif
     uint32_t m0, s0, m1, s1;
     fetch(0, m0, s0);
     fetch(1, m1, s1);
@@ -629,11 +594,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       issue(c + 1, m1, s1);
       uint32_t m2, s2;
       fetch(c + 2, m2, s2);
-#ifdef GSF_TBW_BULK
-      mbar_wait(bar0 + 8u * static_cast<uint32_t>(c & 1), static_cast<uint32_t>((c >> 1) & 1));
-#else
       cp_async_wait_1();   // chunk c has landed (chunk c + 1 may still be in flight)
-#endif
       __syncwarp();
       const int lo = max(0, E - kC * (c + 1));
       const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 3072u, idb = sb + 6144u + static_cast<uint32_t>(c & 1) * 64u;
@@ -680,11 +641,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         const float2 w = __fmul2_rn(am, Tpre);
         S = __ffma2_rn(w, q, S);
         T = Tpre;   // a pixel that does not take the entry has am = 0: rcp(1) = 1 exactly, T unchanged
-#ifdef GSF_SIGFOLD
-        float2 gdg = __fmul2_rn(gv, dal);   // sigma is folded into the pose matrix columns 0..4
-#else
         float2 gdg = __fmul2_rn(__fmul2_rn(gv, dal), make_float2(g.sigma, g.sigma));
-#endif
         gdg = make_float2(ca && !cl_a ? gdg.x : 0.0f, cb && !cl_b ? gdg.y : 0.0f);
         // the pose matrix takes t = g (dx, dy, dx^2, dx dy, dy^2) (compute_posejac's offset basis);
         // both pixels share dx, so the pair sums need no per-pixel ux, uy
@@ -715,9 +672,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
       __syncwarp();   // buffer c & 1 is refilled by issue(c + 2)
       m0 = m1; s0 = s1; m1 = m2; s1 = s2;
     }
-#ifndef GSF_TBW_BULK
     cp_async_wait_all();
-#endif
   }
 #pragma unroll
   for (int a = 0; a < 6; ++a) pd[a] = warp_sum_f64(pd[a]);

@@ -144,14 +144,8 @@ __device__ void compute_posejac(const float* __restrict__ p, int64_t stride, con
       N[3][a] = 2.0 * c00 * c01 * Mc[2][a] + (c00 * c11 + c01 * c01) * Mc[3][a] + 2.0 * c01 * c11 * Mc[4][a];
       N[4][a] = c01 * c01 * Mc[2][a] + c01 * c11 * Mc[3][a] + c11 * c11 * Mc[4][a];
     }
-#ifdef GSF_SIGFOLD
-    // ... and scaled by the primitive's opacity sigma, which multiplies every (dx, dy)-basis partial
-    const double sg = conic->sigma;
-#else
-    const double sg = 1.0;
-#endif
     for (int j = 0; j < 5; ++j)
-      for (int a = 0; a < 6; ++a) Mc[j][a] = sg * N[j][a];
+      for (int a = 0; a < 6; ++a) Mc[j][a] = N[j][a];
   }
   for (int j = 0; j < 6; ++j)
     for (int a = 0; a < 6; ++a) out[6 * j + a] = static_cast<float>(Mc[j][a]);
@@ -739,6 +733,9 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   float2 op = make_float2(0.f, 0.f), T = make_float2(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);
   int last_a = 0, last_b = 0;
   int lc_a = 0, lc_b = 0;   // the same, as positions in this warp's work list (qlist)
+#ifdef GSF_TAKEN_LIST
+  uint32_t qn = 0u;         // entries in this warp's work list
+#endif
   const int64_t qbase = 4 * static_cast<int64_t>(rg.x) + static_cast<int64_t>(warp) * (rg.y - rg.x);
   float px = static_cast<float>(x) + 0.5f;
   float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
@@ -764,8 +761,10 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       const int kk = c0 + lane;
       uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
       // the pose backward's work list: this block's entries in list order (its only staging input)
+#ifndef GSF_TAKEN_LIST
       if (QM != 0 && ((bits >> lane) & 1u))
         qlist[qbase + wsteps + static_cast<uint32_t>(__popc(bits & ((1u << lane) - 1u)))] = static_cast<uint32_t>(s_id[kk]);
+#endif
       uint32_t ci = wsteps;
       wsteps += __popc(bits);
       while (bits) {
@@ -811,10 +810,21 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
           if (ca) last_a = li;
           if (cb) last_b = li;
         }
+#ifdef GSF_TAKEN_LIST
+        // only entries some pixel of the block took enter the backward's work list
+        if (QM != 0 && __any_sync(0xffffffffu, ca || cb)) {
+          if (lane == 0) qlist[qbase + qn] = static_cast<uint32_t>(s_id[k]);
+          ++qn;
+          if (ca) lc_a = static_cast<int>(qn);
+          if (cb) lc_b = static_cast<int>(qn);
+        }
+        (void)ci;
+#else
         if (QM != 0) {
           if (ca) lc_a = static_cast<int>(ci);
           if (cb) lc_b = static_cast<int>(ci);
         }
+#endif
       }
     }
   }
