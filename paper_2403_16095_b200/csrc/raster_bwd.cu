@@ -614,6 +614,26 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         float2 gv = make_float2(exp_neg_half_fast(rho.x), exp_neg_half_fast(rho.y));
         float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), gv);
         bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
+#ifdef GSF_TBW_GA
+        // al = the pixel's alpha (0 where it does not take the entry: T, S unchanged), ga = the alpha the
+        // gradient flows through (0 also where the alpha is clamped, rasterizer.cpp:451): no selects after
+        al = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
+        float2 ga = al;
+        if (!skip_a && !fast_a) {
+          const GuardOut o = guard_decide(px, py.x, g, bp.gg_slot + lds_s32(idb + 4u * k), &kc);
+          ca = o.alpha >= 0.0f;
+          al.x = ca ? o.alpha : 0.0f;
+          ga.x = ca && !o.clamped ? o.alpha : 0.0f;
+        }
+        if (!skip_b && !fast_b) {
+          const GuardOut o = guard_decide(px, py.y, g, bp.gg_slot + lds_s32(idb + 4u * k), &kc);
+          cb = o.alpha >= 0.0f;
+          al.y = cb ? o.alpha : 0.0f;
+          ga.y = cb && !o.clamped ? o.alpha : 0.0f;
+        }
+        if (!ca && !cb) continue;
+        const float2 am = al;
+#else
         int cl_a = 0, cl_b = 0;
         if (!skip_a && !fast_a) {
           const GuardOut o = guard_decide(px, py.x, g, bp.gg_slot + lds_s32(idb + 4u * k), &kc);
@@ -631,6 +651,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         }
         if (!ca && !cb) continue;
         const float2 am = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
+#endif
         const float2 inv = make_float2(rcp_approx(1.0f - am.x), rcp_approx(1.0f - am.y));
         const float2 Tpre = __fmul2_rn(T, inv);
         float2 q = __fmul2_rn(gc0, make_float2(g.r, g.r));
@@ -641,8 +662,12 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         const float2 w = __fmul2_rn(am, Tpre);
         S = __ffma2_rn(w, q, S);
         T = Tpre;   // a pixel that does not take the entry has am = 0: rcp(1) = 1 exactly, T unchanged
+#ifdef GSF_TBW_GA
+        const float2 gdg = __fmul2_rn(ga, dal);
+#else
         float2 gdg = __fmul2_rn(__fmul2_rn(gv, dal), make_float2(g.sigma, g.sigma));
         gdg = make_float2(ca && !cl_a ? gdg.x : 0.0f, cb && !cl_b ? gdg.y : 0.0f);
+#endif
         // the pose matrix takes t = g (dx, dy, dx^2, dx dy, dy^2) (compute_posejac's offset basis);
         // both pixels share dx, so the pair sums need no per-pixel ux, uy
         const float G = gdg.x + gdg.y;
@@ -786,7 +811,11 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t r = blockIdx.x * blockDim.x + tid;
   double pose[6] = {0, 0, 0, 0, 0, 0};
-  const bool active = r < counters[kCntVisible] && !ds->halt;
+  const uint32_t V = counters[kCntVisible];
+  // the grid is sized for all P; CTAs past the visible list have no primitive and no pose row
+  // (k_pose_sum reads the rows of the first ceil(V / 256) CTAs only)
+  if (blockIdx.x * blockDim.x >= V) return;
+  const bool active = r < V && !ds->halt;
   int64_t id = 0;
   int c = 0;
   const float* pp = partials;
@@ -976,9 +1005,11 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   }
 }
 
-__global__ void __launch_bounds__(1024) k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds) {
+__global__ void __launch_bounds__(1024) k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds,
+                                                   const uint32_t* counters) {
   pdl_wait();   // PDL: the predecessor's results are complete from here
   pdl_trigger();
+  blocks = min(blocks, static_cast<int>((counters[kCntVisible] + 255u) / 256u));   // k_chain's CTAs with a row
   __shared__ double s_red[32][6];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double acc[6] = {0, 0, 0, 0, 0, 0};
@@ -1136,7 +1167,7 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     GSF_CHAIN(10, true);
 #undef GSF_CHAIN
   ++*L;
-  launch_pdl(k_pose_sum, dim3(1), dim3(1024), 0, st, ws.pose_part, blocks, ds);
+  launch_pdl(k_pose_sum, dim3(1), dim3(1024), 0, st, ws.pose_part, blocks, ds, static_cast<const uint32_t*>(ws.bin_counters));
   ++*L;
   if (ws.prof) ws.prof->end(st);
   return false;

@@ -265,16 +265,16 @@ __global__ void __launch_bounds__(256, CACHED ? GSF_PRE_MINB : 2) k_preprocess(c
   __shared__ Cam s_cam;   // read through shared memory: 20 doubles need not live in registers
   pdl_wait();   // the camera comes from the previous iteration's pose step
   pdl_trigger();
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (cand && ds->cand_ok) {   // inside the trust region: only the frame's candidates (k_candidates)
+    const uint32_t n = ds->ncand;
+    if (static_cast<uint32_t>(blockIdx.x) * blockDim.x >= n) return;   // whole CTA, before any barrier
+    i = i < n ? static_cast<int64_t>(cand[i]) : P;
+  }
   if (threadIdx.x < sizeof(Cam) / 4)
     reinterpret_cast<uint32_t*>(&s_cam)[threadIdx.x] = reinterpret_cast<const uint32_t*>(&ds->cam)[threadIdx.x];
   __syncthreads();
   const Cam& cam = s_cam;
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (cand && ds->cand_ok) {   // inside the trust region: only the frame's candidates (k_candidates)
-    const uint32_t n = ds->ncand;
-    if (static_cast<uint32_t>(blockIdx.x) * blockDim.x >= n) return;   // whole CTA: no barrier follows
-    i = i < n ? static_cast<int64_t>(cand[i]) : P;
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   bool vis = false;
   int4 q = make_int4(0, -1, 0, -1);
@@ -733,9 +733,6 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   float2 op = make_float2(0.f, 0.f), T = make_float2(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);
   int last_a = 0, last_b = 0;
   int lc_a = 0, lc_b = 0;   // the same, as positions in this warp's work list (qlist)
-#ifdef GSF_TAKEN_LIST
-  uint32_t qn = 0u;         // entries in this warp's work list
-#endif
   const int64_t qbase = 4 * static_cast<int64_t>(rg.x) + static_cast<int64_t>(warp) * (rg.y - rg.x);
   float px = static_cast<float>(x) + 0.5f;
   float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
@@ -761,10 +758,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       const int kk = c0 + lane;
       uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
       // the pose backward's work list: this block's entries in list order (its only staging input)
-#ifndef GSF_TAKEN_LIST
       if (QM != 0 && ((bits >> lane) & 1u))
         qlist[qbase + wsteps + static_cast<uint32_t>(__popc(bits & ((1u << lane) - 1u)))] = static_cast<uint32_t>(s_id[kk]);
-#endif
       uint32_t ci = wsteps;
       wsteps += __popc(bits);
       while (bits) {
@@ -810,21 +805,10 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
           if (ca) last_a = li;
           if (cb) last_b = li;
         }
-#ifdef GSF_TAKEN_LIST
-        // only entries some pixel of the block took enter the backward's work list
-        if (QM != 0 && __any_sync(0xffffffffu, ca || cb)) {
-          if (lane == 0) qlist[qbase + qn] = static_cast<uint32_t>(s_id[k]);
-          ++qn;
-          if (ca) lc_a = static_cast<int>(qn);
-          if (cb) lc_b = static_cast<int>(qn);
-        }
-        (void)ci;
-#else
         if (QM != 0) {
           if (ca) lc_a = static_cast<int>(ci);
           if (cb) lc_b = static_cast<int>(ci);
         }
-#endif
       }
     }
   }
