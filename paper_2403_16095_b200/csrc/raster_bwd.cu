@@ -614,7 +614,6 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         float2 gv = make_float2(exp_neg_half_fast(rho.x), exp_neg_half_fast(rho.y));
         float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), gv);
         bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
-#ifdef GSF_TBW_GA
         // al = the pixel's alpha (0 where it does not take the entry: T, S unchanged), ga = the alpha the
         // gradient flows through (0 also where the alpha is clamped, rasterizer.cpp:451): no selects after
         al = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
@@ -633,25 +632,6 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         }
         if (!ca && !cb) continue;
         const float2 am = al;
-#else
-        int cl_a = 0, cl_b = 0;
-        if (!skip_a && !fast_a) {
-          const GuardOut o = guard_decide(px, py.x, g, bp.gg_slot + lds_s32(idb + 4u * k), &kc);
-          al.x = o.alpha;
-          gv.x = o.gval;
-          cl_a = o.clamped;
-          ca = al.x >= 0.0f;
-        }
-        if (!skip_b && !fast_b) {
-          const GuardOut o = guard_decide(px, py.y, g, bp.gg_slot + lds_s32(idb + 4u * k), &kc);
-          al.y = o.alpha;
-          gv.y = o.gval;
-          cl_b = o.clamped;
-          cb = al.y >= 0.0f;
-        }
-        if (!ca && !cb) continue;
-        const float2 am = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
-#endif
         const float2 inv = make_float2(rcp_approx(1.0f - am.x), rcp_approx(1.0f - am.y));
         const float2 Tpre = __fmul2_rn(T, inv);
         float2 q = __fmul2_rn(gc0, make_float2(g.r, g.r));
@@ -662,12 +642,7 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
         const float2 w = __fmul2_rn(am, Tpre);
         S = __ffma2_rn(w, q, S);
         T = Tpre;   // a pixel that does not take the entry has am = 0: rcp(1) = 1 exactly, T unchanged
-#ifdef GSF_TBW_GA
         const float2 gdg = __fmul2_rn(ga, dal);
-#else
-        float2 gdg = __fmul2_rn(__fmul2_rn(gv, dal), make_float2(g.sigma, g.sigma));
-        gdg = make_float2(ca && !cl_a ? gdg.x : 0.0f, cb && !cl_b ? gdg.y : 0.0f);
-#endif
         // the pose matrix takes t = g (dx, dy, dx^2, dx dy, dy^2) (compute_posejac's offset basis);
         // both pixels share dx, so the pair sums need no per-pixel ux, uy
         const float G = gdg.x + gdg.y;
