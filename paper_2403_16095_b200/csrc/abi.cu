@@ -319,6 +319,11 @@ void alloc_pairs(Workspace& ws) {
   dalloc(ws.skey, ws.pair_cap); dalloc(ws.sid, ws.pair_cap);
   dalloc(ws.sslot, ws.pair_cap); dalloc(ws.qlist, 4 * ws.pair_cap);
   dalloc(ws.partials, ws.pair_cap * 10);
+  // [pair][4 quadrants][10] (k_backward_q) + a written-flag byte per (pair, quadrant): k_pair_combine
+  // reads the flagged slots and clears the flags, so they start cleared
+  dalloc(ws.qpart, ws.pair_cap * 40);
+  dalloc(ws.qflag, ws.pair_cap);
+  GSF_CUDA_CHECK(cudaMemset(ws.qflag, 0, sizeof(uint32_t) * ws.pair_cap));
 }
 
 void ensure_ws(gsf_ctx_s* c, int W, int H) {
@@ -738,7 +743,7 @@ int gsf_ctx_destroy(gsf_ctx c) {
   void* bufs[] = {ws.bg_id, ws.gg_id, ws.bg_slot, ws.gg_slot, ws.sslot, ws.qlist, ws.lastc, ws.cand, ws.depth_id, ws.rect_id, ws.visible, ws.bins,
                   ws.bucket, ws.skey, ws.sid, ws.big_ids, ws.vis_list, ws.pair_base, ws.pj_slot, ws.world, ws.support, ws.partials, ws.ranges, ws.loss_part, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid,
                   ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w,
-                  ws.last, ws.pxcode, ws.fix_list, ws.order, ws.qstat, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id,
+                  ws.last, ws.pxcode, ws.fix_list, ws.order, ws.qstat, ws.obs, ws.upstream, ws.dssim, ws.ssim_tmp, ws.pose_part, ws.wtickets, ws.pj_id, ws.qflag, ws.qpart,
                   ws.red_part, c->bp_scratch, c->params, c->grads, c->adam_m, c->adam_v, c->nu, c->observed, c->d_mean2d,
                   c->grad_accum, c->grad_count, c->ds, c->kf, c->trace_dev, c->unc_sum, c->unc_cnt, c->counters,
                   c->red_f, c->ba_pack};

@@ -125,6 +125,8 @@ struct Workspace {
   float* dssim = nullptr;       // 3*npix: d(w_ssim * ssim loss)/d colour (mapping)
   float* ssim_tmp = nullptr;    // SSIM scratch maps (see loss.cu)
   // temporaries
+  float* qpart = nullptr;       // [pair][4 quadrants][10] partials of k_backward_q (k_pair_combine folds them)
+  uint32_t* qflag = nullptr;    // per pair: 4 bytes, quadrant q's slot written (k_backward_q -> k_pair_combine)
   double* pose_part = nullptr;  // chain blocks * 6 (or 4 tiles * 6 + group rows for the tracking backward)
   uint32_t* wtickets = nullptr; // zeroed group tickets of the single-warp grid reductions (self-resetting)
   int64_t wtickets_half = 0;    // entries per region: [0, half) blend, [half, 2 half) backward

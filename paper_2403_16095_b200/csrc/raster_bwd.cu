@@ -103,6 +103,8 @@ struct BwdPtrs {
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
   const uint32_t* qlist;    // tracking: per (tile, quadrant) work lists (k_blend_track)
   const int32_t* lastc;     // tracking: each pixel's last contributor as a work-list position + 1
+  uint8_t* qflag;           // full bundle: per (pair, quadrant) written flag (k_backward_q)
+  float* qpart;             // full bundle: [pair][quadrant][10] partials (k_backward_q)
   const uint8_t* pxcode;    // tracking: per pixel, the seed signs (pixel_seed_code, k_blend_track)
   const BlendG* bg_slot;    // tracking: records by visible slot
   const GuardG* gg_slot;
@@ -308,6 +310,167 @@ __device__ __forceinline__ PixBwd load_pixel_bwd(const BwdPtrs& bp, int64_t pi, 
   if (p.gc0 == 0.f && p.gc1 == 0.f && p.gc2 == 0.f && p.gad == 0.f && p.gop == 0.f && p.gmd == 0.f && p.gu == 0.f)
     p.last = 0;
   return p;
+}
+
+// Mapping / full-bundle backward (render_backward phase 1, rasterizer.cpp:374-464) as independent
+// single-warp CTAs: CTA 4 t + q owns quadrant q (8x8 pixels, two per lane: (l & 7, l >> 3) and
+// (l & 7, (l >> 3) + 4)) of tile t and walks the tile list back to front from its pixels' last
+// contributor in chunks of 32 entries.  Lane e stages entry e of the chunk (record, rectangle and
+// pair base by cp.async, the id two chunks ahead), tests it against the quadrant's block
+// (block_hit8), and the warp walks the set bits.  Per entry the two pixels' ten partials are summed
+// per lane, reduced across the warp (reduce-scatter) and written ONCE to the (pair, quadrant) slot
+// (partials [pair][4][10]); no CTA barriers, no float atomics.  Fields 0..4 are kept in the
+// pixel-offset basis t = g (dx, dy, dx^2, dx dy, dy^2) (k_chain re-expresses them with the conic),
+// so a step forms them from the shared dx.  k_chain reads every (pair, quadrant) slot in a fixed
+// order and zeroes it, so slots no quadrant walked read 0 on the next backward.
+constexpr int kBqChunk = 32;
+#ifndef GSF_BQ_MINB
+#define GSF_BQ_MINB 20
+#endif
+template <int SEED>
+__global__ void __launch_bounds__(32, GSF_BQ_MINB) k_backward_q(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc,
+                                                               double near_plane, double far_plane, LossParams lp,
+                                                               const DevState* ds) {
+  // per buffer (2): 32 records (48 B) at +0, 32 rectangles (16 B) at +1536, 32 pair bases at +2048,
+  // 32 ids at +2176; 2304 B per buffer
+  __shared__ float4 s_buf[2 * 144];
+  pdl_wait();
+  pdl_trigger();
+  if (ds->halt) return;
+  const int lane = threadIdx.x;
+  const uint32_t sb = opaque_smem_base(s_buf);
+  const int item = static_cast<int>(blockIdx.x);
+  const int tile = item >> 2, qd = item & 3;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int bx0 = tx * kTile + 8 * (qd & 1), by0 = ty * kTile + 8 * (qd >> 1);
+  const int x = bx0 + (lane & 7);
+  const int ya = by0 + (lane >> 3), yb = ya + 4;
+  const bool in_a = x < W && ya < H, in_b = x < W && yb < H;
+  const PixBwd qa = load_pixel_bwd<SEED>(bp, static_cast<int64_t>(ya) * W + x, in_a, lp, ds, near_plane, far_plane);
+  const PixBwd qb = load_pixel_bwd<SEED>(bp, static_cast<int64_t>(yb) * W + x, in_b, lp, ds, near_plane, far_plane);
+  const int last_a = qa.last, last_b = qb.last;
+  const int maxlast = __reduce_max_sync(0xffffffffu, max(last_a, last_b));
+  if (maxlast == 0) return;
+  const int2 rg = bp.ranges[tile];
+  const float2 gc0 = make_float2(qa.gc0, qb.gc0), gc1 = make_float2(qa.gc1, qb.gc1), gc2 = make_float2(qa.gc2, qb.gc2),
+               gad = make_float2(qa.gad, qb.gad), gop = make_float2(qa.gop, qb.gop), gu = make_float2(qa.gu, qb.gu),
+               Dd = make_float2(qa.D, qb.D);
+  const float gmd_a = qa.gmd, gmd_b = qb.gmd;
+  const int med_a = qa.med, med_b = qb.med;
+  const float px = static_cast<float>(x) + 0.5f;
+  const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
+  float2 T = make_float2(qa.T, qb.T), S = make_float2(0.f, 0.f);
+  bool fvalid;
+  const int fidx = rs_field(10, lane, fvalid);
+  const int E = rg.x + maxlast;
+  const int nch = (maxlast + kBqChunk - 1) / kBqChunk;
+  // chunk c: list entries [lo, hi) with hi = E - 32 c; lane e holds entry hi - 1 - e (back to front)
+  auto fetch = [&](int c) -> int32_t {
+    if (c >= nch) return -1;
+    const int j = E - kBqChunk * c - 1 - lane;
+    return j >= rg.x ? static_cast<int32_t>(__ldg(bp.sid + j)) : -1;
+  };
+  auto issue = [&](int c, int32_t id) {
+    if (c < nch && id >= 0) {
+      const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 2304u;
+      const float4* rec = reinterpret_cast<const float4*>(bp.bg + id);
+      cp_async16_to(buf + 48u * lane, rec);
+      cp_async16_to(buf + 48u * lane + 16u, rec + 1);
+      cp_async16_to(buf + 48u * lane + 32u, rec + 2);
+      cp_async16_to(buf + 1536u + 16u * lane, bp.rect + id);
+      sts_s32(buf + 2176u + 4u * lane, id);
+      sts_s32(buf + 2048u + 4u * lane, static_cast<int32_t>(__ldg(bp.pair_base + id)));
+    }
+    cp_async_commit();
+  };
+  int32_t id0 = fetch(0), id1 = fetch(1);
+  issue(0, id0);
+  const float qx0 = static_cast<float>(bx0), qy0 = static_cast<float>(by0);
+  for (int c = 0; c < nch; ++c) {
+    issue(c + 1, id1);
+    const int32_t id2 = fetch(c + 2);
+    cp_async_wait_1();
+    __syncwarp();
+    const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 2304u;
+    const int hi = E - kBqChunk * c;
+    bool hit = false;
+    if (id0 >= 0) hit = block_hit8(lds_blend(buf + 48u * lane), qx0, qy0, kc);
+    uint32_t bits = __ballot_sync(0xffffffffu, hit);
+    while (bits) {
+      const int e = __ffs(bits) - 1;   // lowest lane = latest entry: back to front
+      bits &= bits - 1u;
+      const int li = hi - 1 - e - rg.x;
+      const BlendG g = lds_blend(buf + 48u * e);
+      const float dx = __fadd_rn(px, -g.mx);
+      const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
+      const float2 rho = pair_rho2(dx, dy, g);
+      const bool skip_a = li >= last_a || rho.x > g.rho_hi, skip_b = li >= last_b || rho.y > g.rho_hi;
+      if (__all_sync(0xffffffffu, skip_a && skip_b)) continue;
+      const bool fast_a = rho.x < g.rho_fast, fast_b = rho.y < g.rho_fast;
+      float2 gv = make_float2(exp_neg_half_fast(rho.x), exp_neg_half_fast(rho.y));
+      bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
+      gv = make_float2(ca ? gv.x : 0.0f, cb ? gv.y : 0.0f);
+      float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), gv);   // 0 where the pixel does not take the entry
+      float2 gz = gv;                                              // gval where the gradient flows (0 if clamped)
+      const int32_t eid = lds_s32(buf + 2176u + 4u * e);
+      if (!skip_a && !fast_a) {
+        const GuardOut o = guard_decide(px, py.x, g, bp.gg + eid, &kc);
+        ca = o.alpha >= 0.0f;
+        al.x = ca ? o.alpha : 0.0f;
+        gz.x = ca && !o.clamped ? o.gval : 0.0f;
+      }
+      if (!skip_b && !fast_b) {
+        const GuardOut o = guard_decide(px, py.y, g, bp.gg + eid, &kc);
+        cb = o.alpha >= 0.0f;
+        al.y = cb ? o.alpha : 0.0f;
+        gz.y = cb && !o.clamped ? o.gval : 0.0f;
+      }
+      const bool contrib = ca || cb;
+      if (!__any_sync(0xffffffffu, contrib)) continue;
+      const float2 inv = make_float2(rcp_approx(1.0f - al.x), rcp_approx(1.0f - al.y));
+      const float2 Tpre = __fmul2_rn(T, inv);
+      const float2 derr = __fadd2_rn(make_float2(g.depth, g.depth), make_float2(-Dd.x, -Dd.y));
+      float2 q = __ffma2_rn(gu, __fmul2_rn(derr, derr), gop);
+      q = __ffma2_rn(gc0, make_float2(g.r, g.r), q);
+      q = __ffma2_rn(gc1, make_float2(g.g, g.g), q);
+      q = __ffma2_rn(gc2, make_float2(g.b, g.b), q);
+      q = __ffma2_rn(gad, make_float2(g.depth, g.depth), q);
+      const float2 dal = __ffma2_rn(Tpre, q, __fmul2_rn(make_float2(-S.x, -S.y), inv));
+      const float2 w = __fmul2_rn(al, Tpre);
+      S = __ffma2_rn(w, q, S);
+      T = Tpre;
+      const float2 dgz = __fmul2_rn(gz, dal);                                   // d opacity-logit partial
+      const float2 gdg = __fmul2_rn(dgz, make_float2(g.sigma, g.sigma));        // d rho partial (x -1/2 folded)
+      float f[10];
+      {
+        const float G = gdg.x + gdg.y;
+        const float2 gy = __fmul2_rn(gdg, dy), gy2 = __fmul2_rn(gy, dy);
+        f[1] = gy.x + gy.y;
+        f[0] = dx * G;
+        f[2] = (dx * dx) * G;
+        f[3] = dx * f[1];
+        f[4] = gy2.x + gy2.y;
+        const float2 dd = __ffma2_rn(make_float2(2.0f, 2.0f), __fmul2_rn(gu, derr), gad);
+        const float2 f5 = __fmul2_rn(w, dd);
+        f[5] = (f5.x + (ca && eid == med_a ? gmd_a : 0.0f)) + (f5.y + (cb && eid == med_b ? gmd_b : 0.0f));
+        const float2 c0 = __fmul2_rn(w, gc0), c1 = __fmul2_rn(w, gc1), c2 = __fmul2_rn(w, gc2);
+        f[6] = c0.x + c0.y;
+        f[7] = c1.x + c1.y;
+        f[8] = c2.x + c2.y;
+        f[9] = dgz.x + dgz.y;
+      }
+      const float val = warp_reduce_scatter<10>(f, lane);
+      const int4 rq = lds_i4(buf + 1536u + 16u * e);
+      const uint32_t slot = static_cast<uint32_t>(lds_s32(buf + 2048u + 4u * e)) +
+                            static_cast<uint32_t>((ty - rq.z) * (rq.y - rq.x + 1) + (tx - rq.x));
+      if (fvalid) bp.qpart[(static_cast<size_t>(slot) * 4 + qd) * 10 + fidx] = val;
+      if (lane == 0) bp.qflag[static_cast<size_t>(slot) * 4 + qd] = 1;
+    }
+    __syncwarp();   // buffer c & 1 is refilled by issue(c + 2)
+    id0 = id1;
+    id1 = id2;
+  }
+  cp_async_wait_all();
 }
 
 // Tracking pixel inputs from the fused forward's seed signs: seeds_pixel<1>'s values (the same
@@ -689,6 +852,37 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   }
 }
 
+// k_backward_q's four quadrant slots of every (tile, primitive) pair folded in quadrant order into the
+// pair's [10] partial (the layout k_chain gathers): one thread per pair slot, the slots of consecutive
+// threads contiguous, flags of the slots no quadrant wrote mask stale values and are cleared.
+__global__ void __launch_bounds__(256) k_pair_combine(const float* __restrict__ qpart, uint32_t* __restrict__ qflag,
+                                                      float* __restrict__ partials, const uint32_t* counters) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t M = counters[kCntPairAlloc];
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < M; p += gridDim.x * blockDim.x) {
+    const uint32_t fl = qflag[p];
+    const float4* src = reinterpret_cast<const float4*>(qpart + static_cast<size_t>(p) * 40);
+    float4 v[10];
+#pragma unroll
+    for (int h = 0; h < 10; ++h) v[h] = __ldcs(src + h);   // read once: streaming
+    if (fl) qflag[p] = 0u;
+    float t[10];
+#pragma unroll
+    for (int f = 0; f < 10; ++f) t[f] = 0.0f;
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd) {
+      if (!((fl >> (8 * qd)) & 1u)) continue;
+      const float* q = reinterpret_cast<const float*>(v) + qd * 10;
+#pragma unroll
+      for (int f = 0; f < 10; ++f) t[f] += q[f];
+    }
+    float2* dst = reinterpret_cast<float2*>(partials + static_cast<size_t>(p) * 10);
+#pragma unroll
+    for (int h = 0; h < 5; ++h) dst[h] = make_float2(t[2 * h], t[2 * h + 1]);
+  }
+}
+
 // The chain ADDS each primitive's bundle into the gradient buffer (GradientBundle::add,
 // output.cpp:36-48): callers zero it once, and a sliding_ba window sums its keyframes' bundles in
 // window order (tracker.cpp:164) before the single optimizer step.  One thread owns a primitive's
@@ -779,7 +973,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
                                                const float* __restrict__ partials, const DevState* ds,
                                                const float* __restrict__ params, int64_t P, int K,
                                                float* __restrict__ grads, float* __restrict__ d_mean2d,
-                                               double* __restrict__ pose_part) {
+                                               double* __restrict__ pose_part, const BlendG* __restrict__ bg) {
   pdl_wait();   // PDL: the predecessor's results are complete from here
   pdl_trigger();
   __shared__ double s_red[8][6];
@@ -790,7 +984,8 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   // the grid is sized for all P; CTAs past the visible list have no primitive and no pose row
   // (k_pose_sum reads the rows of the first ceil(V / 256) CTAs only)
   if (blockIdx.x * blockDim.x >= V) return;
-  const bool active = r < V && !ds->halt;
+  const bool halted = ds->halt != 0;
+  bool active = r < V;   // halted: the slots are still read and zeroed, no gradient is written
   int64_t id = 0;
   int c = 0;
   const float* pp = partials;
@@ -834,6 +1029,19 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == j) sg[f] = v;
     }
+  }
+  if (halted) active = false;
+  if (active && NF == 10) {
+    // fields 0..4 arrive in the pixel-offset basis t = g (dx, dy, dx^2, dx dy, dy^2): back to
+    // (d_mean2d x, y, d_cov2d 00, 01, 11) with the record's conic (ux, uy = conic rows . (dx, dy))
+    const BlendG gr = bg[id];
+    const double c00 = gr.c00, c01 = 0.5 * static_cast<double>(gr.c01x2), c11 = gr.c11;
+    const double t0 = sg[0], t1 = sg[1], t2 = sg[2], t3 = sg[3], t4 = sg[4];
+    sg[0] = c00 * t0 + c01 * t1;
+    sg[1] = c01 * t0 + c11 * t1;
+    sg[2] = 0.5 * (c00 * c00 * t2 + 2.0 * c00 * c01 * t3 + c01 * c01 * t4);
+    sg[3] = 0.5 * (c00 * c01 * t2 + (c00 * c11 + c01 * c01) * t3 + c01 * c11 * t4);
+    sg[4] = 0.5 * (c01 * c01 * t2 + 2.0 * c01 * c11 * t3 + c11 * c11 * t4);
   }
   if (active) {
     bool zero = true;
@@ -1058,6 +1266,8 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.up_uncert = a.up_uncert;
   bp.dssim = (a.seed_mode == SEED_MAP && a.lp.w_ssim > 0.0) ? ws.dssim : nullptr;
   bp.partials = ws.partials;
+  bp.qflag = reinterpret_cast<uint8_t*>(ws.qflag);
+  bp.qpart = ws.qpart;
   bp.pj = nullptr;
   bp.pj_slot = nullptr;
   bp.rect = ws.rect_id;
@@ -1119,12 +1329,22 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     launch_pdl(k_backward<SM, NFV>, dim3(ntiles), dim3(256), bwd_smem_bytes<NFV>(), st, bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, \
                                                                      a.far_plane, a.lp, ds);                    \
   } while (0)
-  if (a.seed_mode == SEED_TRACK) {
-    if (nf == 6) GSF_BWD(SEED_TRACK, 6); else if (nf == 9) GSF_BWD(SEED_TRACK, 9); else GSF_BWD(SEED_TRACK, 10);
+  if (nf == 10) {   // the full bundle: per-quadrant single-warp CTAs (k_backward_q)
+#define GSF_BQ(SM) launch_pdl(k_backward_q<SM>, dim3(4 * ntiles), dim3(32), 0, st, bp, a.W, a.H, a.rp.tiles_x, a.kc, \
+                              a.near_plane, a.far_plane, a.lp, static_cast<const DevState*>(ds))
+    if (a.seed_mode == SEED_TRACK) GSF_BQ(SEED_TRACK);
+    else if (a.seed_mode == SEED_MAP) GSF_BQ(SEED_MAP);
+    else GSF_BQ(SEED_EXPLICIT);
+#undef GSF_BQ
+    ++*L;
+    launch_pdl(k_pair_combine, dim3(4 * 148), dim3(256), 0, st, static_cast<const float*>(ws.qpart), ws.qflag, ws.partials,
+               static_cast<const uint32_t*>(ws.bin_counters));
+  } else if (a.seed_mode == SEED_TRACK) {
+    if (nf == 6) GSF_BWD(SEED_TRACK, 6); else GSF_BWD(SEED_TRACK, 9);
   } else if (a.seed_mode == SEED_MAP) {
-    if (nf == 6) GSF_BWD(SEED_MAP, 6); else if (nf == 9) GSF_BWD(SEED_MAP, 9); else GSF_BWD(SEED_MAP, 10);
+    if (nf == 6) GSF_BWD(SEED_MAP, 6); else GSF_BWD(SEED_MAP, 9);
   } else {
-    if (nf == 6) GSF_BWD(SEED_EXPLICIT, 6); else if (nf == 9) GSF_BWD(SEED_EXPLICIT, 9); else GSF_BWD(SEED_EXPLICIT, 10);
+    if (nf == 6) GSF_BWD(SEED_EXPLICIT, 6); else GSF_BWD(SEED_EXPLICIT, 9);
   }
 #undef GSF_BWD
   ++*L;
@@ -1133,7 +1353,7 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   const int blocks = std::max(1, div_up(a.P, 256));
 #define GSF_CHAIN(NFV, FULLV)                                                                                            \
   launch_pdl(k_chain<NFV, FULLV>, dim3(blocks), dim3(256), 0, st, ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base, ws.partials, ds, \
-                                              a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part)
+                                              a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part, ws.bg_id)
   if (nf == 6)
     GSF_CHAIN(6, false);
   else if (nf == 9)
