@@ -399,20 +399,24 @@ def run_ours(args):
     pre_units = ncand if ncand > 0 else int(m.count)
     pre_bytes = pre_units * (56 + 52)
     kname = {"blend": "k_blend_track", "backward": "k_backward_track_w"}[dom]
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            t = json.load(f)[kname]
-        traffic = float(t["dram_read_bytes"] + t["dram_write_bytes"])
-    except Exception:
-        pass
+    traffic, traffic_src = None, None
+    for tf in ("r02_traffic.json", "r01_traffic.json"):   # the newest ncu capture of the kernel
+        try:
+            with open(os.path.join(ROOT, "profiles", tf)) as f:
+                t = json.load(f)[kname]
+            traffic = float(t["dram_read_bytes"] + t["dram_write_bytes"])
+            traffic_src = "profiles/" + tf
+            break
+        except Exception:
+            pass
     roof = {"kernel": kname, "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
             "frac": achieved / fp32_peak, "traffic": traffic,
             "peak_source": fp32_src,
             "algorithmic_flops_per_launch": flops[dom], "avg_launch_ms": per_launch[dom],
             "note": "issue / FP32-pipe bound: no dense contraction (no tensor-core work) and an L2-resident "
-                    "working set (DRAM traffic per launch = 'traffic', from profiles/r01_traffic.json), so "
-                    "neither the HBM nor the tensor roofline binds; 'hbm' below gives the HBM position",
+                    "working set (DRAM traffic per launch = 'traffic', from one ncu --set full capture: "
+                    "'traffic_source'), so neither the HBM nor the tensor roofline binds; 'hbm' below gives the HBM "
+                    "position", "traffic_source": traffic_src,
             "hbm": {"achieved_gbs": (traffic / (per_launch[dom] * 1e-3) / 1e9) if traffic else None,
                     "peak_gbs": hbm, "frac": (traffic / (per_launch[dom] * 1e-3) / 1e9 / hbm) if traffic else None}}
     # shares of the profiled (eager, event-bracketed) pass's own elapsed time: the brackets and the
@@ -581,7 +585,7 @@ def mapping_evidence(mctx, slots, kposes, kf, K, tc, mc, iters=2):
 
     roof = {
         "blend k_blend<2>": fp("blend", 11 * T + 24 * Cn, fp32_peak, "fp32: 11 T + 24 C"),
-        "backward k_backward<SEED_MAP,10>": fp("backward", 13 * T + 70 * Cn, fp32_peak, "fp32: 13 T + 70 C"),
+        "backward k_backward_q<SEED_MAP> + k_pair_combine": fp("backward", 13 * T + 70 * Cn, fp32_peak, "fp32: 13 T + 70 C"),
         "chain k_chain<10> (+k_pose_sum)": fp("chain", 300 * V, fp64_peak,
                                              "fp64: 300 V (peak = 148 SMs x 64 FP64 lanes x 2 x clock)"),
         "chain_bytes": bw("chain", 40 * M + 4 * D * 3 * V, "hbm: 40 B per (primitive, tile) partial + params read, "

@@ -1497,10 +1497,23 @@ static void enqueue_map_view(gsf_ctx_s* c, const Frame& f, int k, const gsf_intr
   FwdArgs fa = fwd_args(c, K, m.raster, f.depth, f.rgb, f.depth, lp, it);
   fa.use_world = use_world;
   run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
+#ifndef GSF_NO_MAP_LPT
+  // longest-first order of the backward's (tile, quadrant) CTAs from the forward's per-quadrant steps,
+  // on a side branch beside the SSIM / iso / loss tail, joined before the backward
+  Workspace& wsl = c->ws;
+  GSF_CUDA_CHECK(cudaEventRecord(wsl.ev_lfork, c->stream));
+  GSF_CUDA_CHECK(cudaStreamWaitEvent(wsl.side2, wsl.ev_lfork, 0));
+  run_lpt(wsl, tiles, wsl.order, wsl.side2, &c->launches);
+  GSF_CUDA_CHECK(cudaEventRecord(wsl.ev_ljoin, wsl.side2));
+#endif
   if (m.weights.w_ssim > 0.0) run_ssim(c->ws, c->ds, c->ws.color, f.rgb, K.width, K.height, 1.0f, c->ws.dssim, c->stream, &c->launches);
   run_iso(c->ws, c->ds, c->params, c->P, m.weights.w_iso, m.weights.iso_epsilon, nullptr, c->stream, &c->launches);
   run_loss_finalize(c->ws, c->ds, lp, tiles, npix, it, c->stream, &c->launches);
   BwdArgs b = bwd_args(c, K, m.raster, f.depth, f.rgb, lp, SEED_MAP, false);
+#ifndef GSF_NO_MAP_LPT
+  GSF_CUDA_CHECK(cudaStreamWaitEvent(c->stream, wsl.ev_ljoin, 0));
+  b.order = wsl.order;
+#endif
   run_backward(c->ws, c->ds, b, c->stream, &c->launches);
   if (m.weights.w_iso > 0.0)
     run_iso(c->ws, c->ds, c->params, c->P, m.weights.w_iso, m.weights.iso_epsilon, c->grads, c->stream, &c->launches);

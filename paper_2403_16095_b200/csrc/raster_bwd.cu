@@ -330,7 +330,8 @@ constexpr int kBqChunk = 32;
 template <int SEED>
 __global__ void __launch_bounds__(32, GSF_BQ_MINB) k_backward_q(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc,
                                                                double near_plane, double far_plane, LossParams lp,
-                                                               const DevState* ds) {
+                                                               const DevState* ds, const uint32_t* __restrict__ order,
+                                                               int64_t tiles_cap) {
   // per buffer (2): 32 records (48 B) at +0, 32 rectangles (16 B) at +1536, 32 pair bases at +2048,
   // 32 ids at +2176; 2304 B per buffer
   __shared__ float4 s_buf[2 * 144];
@@ -339,7 +340,9 @@ __global__ void __launch_bounds__(32, GSF_BQ_MINB) k_backward_q(BwdPtrs bp, int 
   if (ds->halt) return;
   const int lane = threadIdx.x;
   const uint32_t sb = opaque_smem_base(s_buf);
-  const int item = static_cast<int>(blockIdx.x);
+  // (tile, quadrant) item in longest-first order (k_lpt over the forward's per-quadrant steps)
+  const int item = (order && 4u * order[0] == gridDim.x) ? static_cast<int>(order[1 + tiles_cap + blockIdx.x])
+                                                         : static_cast<int>(blockIdx.x);
   const int tile = item >> 2, qd = item & 3;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int bx0 = tx * kTile + 8 * (qd & 1), by0 = ty * kTile + 8 * (qd >> 1);
@@ -1331,7 +1334,8 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   } while (0)
   if (nf == 10) {   // the full bundle: per-quadrant single-warp CTAs (k_backward_q)
 #define GSF_BQ(SM) launch_pdl(k_backward_q<SM>, dim3(4 * ntiles), dim3(32), 0, st, bp, a.W, a.H, a.rp.tiles_x, a.kc, \
-                              a.near_plane, a.far_plane, a.lp, static_cast<const DevState*>(ds))
+                              a.near_plane, a.far_plane, a.lp, static_cast<const DevState*>(ds), a.order,           \
+                              static_cast<int64_t>(ws.tiles_cap))
     if (a.seed_mode == SEED_TRACK) GSF_BQ(SEED_TRACK);
     else if (a.seed_mode == SEED_MAP) GSF_BQ(SEED_MAP);
     else GSF_BQ(SEED_EXPLICIT);

@@ -499,10 +499,12 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
                                                int32_t* __restrict__ o_dom, int32_t* __restrict__ o_med,
                                                float* __restrict__ o_domw, int32_t* __restrict__ o_last,
                                                double* __restrict__ loss_part, int fuse_final, int iteration,
-                                               uint32_t* ticket, uint32_t* __restrict__ fix_list, uint32_t* fix_cnt) {
+                                               uint32_t* ticket, uint32_t* __restrict__ fix_list, uint32_t* fix_cnt,
+                                               int2* __restrict__ qstat) {
   pdl_wait();   // PDL: the predecessor's results are complete from here
   pdl_trigger();
   __shared__ BlendG s_g[256];
+  __shared__ uint32_t s_ws[8];
   __shared__ int32_t s_id[256];
   __shared__ uint8_t s_mask[256];
   __shared__ double s_red[8][LS_NUM];
@@ -527,6 +529,7 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
   const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
   const int lane = tid & 31, warp = tid >> 5;
   const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
+  uint32_t wsteps = 0u;   // this warp's (warp, entry) steps: the LPT cost of the mapping backward's quadrants
   for (int start = rg.x; start < rg.y; start += 256) {
     if (__syncthreads_and(s.done)) break;
     const int j = start + tid;
@@ -543,6 +546,7 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       const int kk = c0 + lane;
       uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
+      wsteps += __popc(bits);
       while (bits) {
         const int k = c0 + __ffs(bits) - 1;
         bits &= bits - 1u;
@@ -587,12 +591,18 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
     const double t = warp_sum_d(v[q]);
     if (lane == 0) s_red[warp][q] = t;
   }
+  if (qstat && lane == 0) s_ws[warp] = wsteps;
   __syncthreads();
   if (tid < LS_NUM) {
     double t = 0.0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) t += s_red[w][tid];
     loss_part[static_cast<int64_t>(tile) * LS_NUM + tid] = t;
+  }
+  // quadrant q (8x8) = the 8x4 warp blocks q & 1 + 4 (q >> 1) and + 2
+  if (qstat && tid >= 32 && tid < 36) {
+    const int q = tid - 32, wa = (q & 1) + 4 * (q >> 1);
+    qstat[tile * 4 + q] = make_int2(static_cast<int>(s_ws[wa] + s_ws[wa + 2]), rg.y - rg.x);
   }
   (void)fuse_final;
   (void)iteration;
@@ -972,7 +982,8 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
   ws.ranges, ws.sid, ws.bg_id, ws.gg_id, a.obs, loss_rgb, a.loss_depth, a.W, a.H,                                     \
       tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color, ws.alpha_depth, ws.median_depth, ws.median_valid, \
       ws.opacity, ws.uncertainty, ws.final_T, ws.count, ws.dominant, ws.median_prim, ws.dominant_w, ws.last, ws.loss_part, \
-      a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket, ws.fix_list, ws.bin_counters + kCntFixup
+      a.fuse_loss_final ? 1 : 0, a.iteration, ws.bin_counters + kCntBlendTicket, ws.fix_list, ws.bin_counters + kCntFixup, \
+      a.lp.mode == 2 ? ws.qstat : nullptr
   if (pf) pf->begin(PROF_BLEND, st);
   ws.loss_rows = ntiles;
   if (a.lp.mode == 1 && loss_rgb) {   // tracking loss: colour, alpha depth, opacity, T, last; two pixels per lane
