@@ -987,6 +987,12 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   // the grid is sized for all P; CTAs past the visible list have no primitive and no pose row
   // (k_pose_sum reads the rows of the first ceil(V / 256) CTAs only)
   if (blockIdx.x * blockDim.x >= V) return;
+#ifdef GSF_CHAIN_PF
+  float pf_par[14];
+#define GSF_PAR(F) pf_par[F]
+#else
+#define GSF_PAR(F) params[(F) * P + id]
+#endif
   const bool halted = ds->halt != 0;
   bool active = r < V;   // halted: the slots are still read and zeroed, no gradient is written
   int64_t id = 0;
@@ -994,6 +1000,11 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   const float* pp = partials;
   if (active) {
     id = vis_list[r];
+#ifdef GSF_CHAIN_PF
+    // the primitive's parameters, loaded before the pair gather so their latency overlaps it
+#pragma unroll
+    for (int f = 0; f < 14; ++f) pf_par[f] = (f < 11 || K == 1) ? params[f * P + id] : 0.0f;
+#endif
     const int4 q = rect_id[id];
     c = (q.y - q.x + 1) * (q.w - q.z + 1);
     pp = partials + static_cast<size_t>(pair_base[id]) * NF;
@@ -1053,20 +1064,20 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
     if (!zero) {
       const Cam& cam = ds->cam;
       const double* Wr = cam.W;
-      const double m0 = params[0 * P + id], m1 = params[1 * P + id], m2 = params[2 * P + id];
+      const double m0 = GSF_PAR(0), m1 = GSF_PAR(1), m2 = GSF_PAR(2);
       const double pc[3] = {Wr[0] * m0 + Wr[1] * m1 + Wr[2] * m2 + cam.t[0], Wr[3] * m0 + Wr[4] * m1 + Wr[5] * m2 + cam.t[1],
                             Wr[6] * m0 + Wr[7] * m1 + Wr[8] * m2 + cam.t[2]};
       const double iz = 1.0 / pc[2], iz2 = iz * iz, z = pc[2];
       const double J[2][3] = {{cam.fx * iz, 0.0, -cam.fx * pc[0] * iz2}, {0.0, cam.fy * iz, -cam.fy * pc[1] * iz2}};
-      const double qw0 = params[6 * P + id], qx0 = params[7 * P + id], qy0 = params[8 * P + id], qz0 = params[9 * P + id];
+      const double qw0 = GSF_PAR(6), qx0 = GSF_PAR(7), qy0 = GSF_PAR(8), qz0 = GSF_PAR(9);
       const double qlen = sqrt(qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0);
       const double qn[4] = {qw0 / qlen, qx0 / qlen, qy0 / qlen, qz0 / qlen};
       const double w = qn[0], x = qn[1], y = qn[2], zq = qn[3];
       const double R[3][3] = {{1 - 2 * (y * y + zq * zq), 2 * (x * y - w * zq), 2 * (x * zq + w * y)},
                               {2 * (x * y + w * zq), 1 - 2 * (x * x + zq * zq), 2 * (y * zq - w * x)},
                               {2 * (x * zq - w * y), 2 * (y * zq + w * x), 1 - 2 * (x * x + y * y)}};
-      const double s[3] = {exp(static_cast<double>(params[3 * P + id])), exp(static_cast<double>(params[4 * P + id])),
-                           exp(static_cast<double>(params[5 * P + id]))};
+      const double s[3] = {exp(static_cast<double>(GSF_PAR(3))), exp(static_cast<double>(GSF_PAR(4))),
+                           exp(static_cast<double>(GSF_PAR(5)))};
       double Cw[3][3], Cc[3][3], T1[3][3];
       for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b)
@@ -1127,7 +1138,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
       if (K == 1 && FULL) {
         // degree 0: colour_c = max(0.5 + C0 sh_c, 0), no view-direction gradient (sh.cpp:88-108)
         for (int c = 0; c < 3; ++c) {
-          const double raw = 0.5 + 0.28209479177387814 * params[(11 + c) * P + id];
+          const double raw = 0.5 + 0.28209479177387814 * GSF_PAR(11 + c);
           acc_grad(grads, (11 + c) * P + id, raw < 0.0 ? 0.0 : 0.28209479177387814 * dcol[c]);
         }
       } else if (K > 1) {
@@ -1171,7 +1182,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
         }
         const double qd = qn[0] * dqn[0] + qn[1] * dqn[1] + qn[2] * dqn[2] + qn[3] * dqn[3];
         for (int a = 0; a < 4; ++a) acc_grad(grads, (6 + a) * P + id, (dqn[a] - qn[a] * qd) / qlen);
-        const double sig = 1.0 / (1.0 + exp(-static_cast<double>(params[10 * P + id])));
+        const double sig = 1.0 / (1.0 + exp(-static_cast<double>(GSF_PAR(10))));
         acc_grad(grads, 10 * P + id, (NF >= 10 ? sg[9] : 0.0) * sig * (1.0 - sig));
       }
     }
@@ -1190,6 +1201,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
     pose_part[static_cast<size_t>(blockIdx.x) * 6 + tid] = t;
   }
 }
+#undef GSF_PAR
 
 __global__ void __launch_bounds__(1024) k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds,
                                                    const uint32_t* counters) {
