@@ -987,12 +987,8 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   // the grid is sized for all P; CTAs past the visible list have no primitive and no pose row
   // (k_pose_sum reads the rows of the first ceil(V / 256) CTAs only)
   if (blockIdx.x * blockDim.x >= V) return;
-#ifdef GSF_CHAIN_PF
   float pf_par[14];
 #define GSF_PAR(F) pf_par[F]
-#else
-#define GSF_PAR(F) params[(F) * P + id]
-#endif
   const bool halted = ds->halt != 0;
   bool active = r < V;   // halted: the slots are still read and zeroed, no gradient is written
   int64_t id = 0;
@@ -1000,11 +996,9 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   const float* pp = partials;
   if (active) {
     id = vis_list[r];
-#ifdef GSF_CHAIN_PF
     // the primitive's parameters, loaded before the pair gather so their latency overlaps it
 #pragma unroll
     for (int f = 0; f < 14; ++f) pf_par[f] = (f < 11 || K == 1) ? params[f * P + id] : 0.0f;
-#endif
     const int4 q = rect_id[id];
     c = (q.y - q.x + 1) * (q.w - q.z + 1);
     pp = partials + static_cast<size_t>(pair_base[id]) * NF;

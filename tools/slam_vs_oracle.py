@@ -10,7 +10,9 @@ exercised by tests/test_gpu_parity.py); everything else is RunConfig defaults (1
 iterations per frame, a keyframe every 30 frames with 60 mapping iterations, sliding_ba 10,
 uncertainty pruning, spawning).
 
-Run on the GPU box:  python tools/slam_vs_oracle.py [frames] > gpurun_out/slam_vs_oracle.json
+Run on the GPU box:  python tools/slam_vs_oracle.py [frames] [port|reference] > gpurun_out/slam_vs_oracle.json
+("reference": the oracle entry points route to the reference compiled from its unmodified sources,
+oracle/_ref/libgsfref.so; the orchestration is oracle/slam.py's restatement of system.cpp either way)
 """
 import json
 import os
@@ -37,6 +39,7 @@ def main():
     from oracle.slam import OracleSlam
     from tools import synth
     nframes = int(sys.argv[1]) if len(sys.argv) > 1 else 91
+    which = sys.argv[2] if len(sys.argv) > 2 else "port"
     s = 2.0 / 15.0
     K = api.intrinsics(600.0 * s, 600.0 * s, 599.5 * s, 339.5 * s, 160, 90, near_plane=0.1, far_plane=10.0)
     truth, _ = bench.build_scene(500000)
@@ -60,20 +63,23 @@ def main():
     t0 = time.perf_counter()
     dev = [slam.process(f, f / 30.0, c, d) for f, (c, d) in enumerate(frames)]
     t_dev = time.perf_counter() - t0
-    ref = OracleSlam(cfg())
     t0 = time.perf_counter()
-    ora = [ref.process(f, c, d) for f, (c, d) in enumerate(frames)]
+    with orc.backend(which):
+        ref = OracleSlam(cfg())
+        ora = [ref.process(f, c, d) for f, (c, d) in enumerate(frames)]
     t_ora = time.perf_counter() - t0
 
     dev_poses = [l.pose for l in dev]
     kf_idx = [f for f, l in enumerate(dev) if l.keyframe]
     # keyframe PSNR of each arm's final map rendered at its own keyframe pose
     dev_psnr = [float(l.kf_psnr_db) for l in dev if l.keyframe]
-    m = ref.st.get()
+    dev_final = [psnr(ctx.render(dev_poses[k], K).color, frames[k][0]) for k in kf_idx]
     ora_psnr = []
-    for kf in ref.keyframes:
-        rr = orc.render(m, kf["pose"], K)
-        ora_psnr.append(psnr(rr.color, kf["rgb"]))
+    with orc.backend(which):
+        m = ref.st.get()
+        for kf in ref.keyframes:
+            rr = orc.render(m, kf["pose"], K)
+            ora_psnr.append(psnr(rr.color, kf["rgb"]))
     per_frame = []
     for f in range(nframes):
         per_frame.append({
@@ -85,10 +91,10 @@ def main():
         })
     out = {
         "what": "SlamSystem device vs the fp64 oracle orchestration on the same frames (160x90, RunConfig defaults, "
-                "densify off)",
+                "densify off)", "oracle_backend": which,
         "frames": nframes, "keyframes": kf_idx,
         "ate_rmse_cm": {"device": ate_cm(dev_poses, poses[:nframes]), "oracle": ate_cm(ora, poses[:nframes])},
-        "kf_psnr_db": {"device_at_keyframe_time": dev_psnr, "oracle_final_map": ora_psnr},
+        "kf_psnr_db": {"device_at_keyframe_time": dev_psnr, "device_final_map": dev_final, "oracle_final_map": ora_psnr},
         "max_dev_vs_oracle_cm": max(p["dev_vs_oracle_cm"] for p in per_frame),
         "wall_s": {"device": t_dev, "oracle": t_ora},
         "per_frame": per_frame[::5],
