@@ -290,7 +290,10 @@ void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles
                  bool want_slots) {
   const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
   const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
-  launch_pdl(k_tile_sort, dim3(ntiles), dim3(256), 0, st, ws.tile_fill, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id, ws.ranges,
+#ifndef GSF_SORT_THREADS
+#define GSF_SORT_THREADS 256
+#endif
+  launch_pdl(k_tile_sort, dim3(ntiles), dim3(GSF_SORT_THREADS), 0, st, ws.tile_fill, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id, ws.ranges,
                                       ws.pj_slot, want_slots ? ws.sslot : nullptr, ds, ws.bin_counters, ws.big_ids,
                                       ws.rect_id, tiles_x, ws.bin_counters + kCntSortTicket);
   ++*L;

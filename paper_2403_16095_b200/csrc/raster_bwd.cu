@@ -1,18 +1,25 @@
 // raster_bwd.cu — reverse-order backward of the tile rasterizer on sm_100a.
 //
-// k_backward  render_backward phase 1 (rasterizer.cpp:374-464).  One 256-thread CTA per 16x16
-//             tile walks the tile list back to front in batches staged through shared memory.
-//             Every thread re-evaluates its pixel's pair with the forward's exact decision
-//             arithmetic (gsf_shared.cuh), recovers T by division from the final transmittance
-//             and accumulates the screen-space adjoints.  The per-(tile, primitive) sum over
-//             the 256 pixels is a warp reduce-scatter (12 shuffles for 10 fields instead of 50)
-//             followed by a fixed-order cross-warp sum; the CTA writes it ONCE into the pair's
-//             unique slot.  No float atomics anywhere: results are bit-repeatable.
-// k_chain     phase 2 (rasterizer.cpp:480-570) in fp64, one thread per visible primitive: a
-//             fixed-order gather of its pair slots (= the reference's tile-order reduction,
-//             :466-478), the projection/covariance chain, the SE(3) pose pieces and the
-//             world-parameter gradients; the pose 6-vector is reduced block-wise in fp64.
-// k_pose_sum  fixed-order sum of the per-block pose partials (rasterizer.cpp:570).
+// k_backward_q        render_backward phase 1 (rasterizer.cpp:374-464) for the full gradient bundle
+//                     (mapping, the render_backward API): one single-warp CTA per (16x16 tile, 8x8
+//                     quadrant), two pixels per lane, walking the tile list back to front from its
+//                     pixels' last contributor.  Every pair is re-evaluated with the forward's exact
+//                     decision arithmetic (gsf_shared.cuh), T is recovered by division from the final
+//                     transmittance, and an entry's ten screen-space partials are reduced across the
+//                     warp (reduce-scatter) and written ONCE into the (pair, quadrant) slot.
+// k_pair_combine      folds the four quadrant slots of every (tile, primitive) pair in quadrant order.
+// k_backward_track_w  the tracking (pose-only) backward: the same walk over the forward's per-quadrant
+//                     work lists, each lane contracting its pixels' partials with the entry's SE(3)
+//                     Jacobian (k_posejac) so no per-pair partial is stored; the last CTA sums the
+//                     rows and runs the pose step.  k_backward_pose: the view-dependent-SH variant.
+// k_chain             phase 2 (rasterizer.cpp:480-570) in fp64, one thread per visible primitive: a
+//                     fixed-order gather of its pair slots (= the reference's tile-order reduction,
+//                     :466-478), the projection/covariance chain, the SE(3) pose pieces and the
+//                     world-parameter gradients; the pose 6-vector is reduced block-wise in fp64.
+// k_pose_sum          fixed-order sum of the per-block pose partials (rasterizer.cpp:570).
+// No float atomics on any path: results are bit-repeatable.
+#include <stdexcept>
+
 #include "kernels.h"
 #include "pixel_loss.cuh"
 #include "finalize.cuh"
@@ -109,164 +116,6 @@ struct BwdPtrs {
   const BlendG* bg_slot;    // tracking: records by visible slot
   const GuardG* gg_slot;
 };
-
-#ifndef GSF_BWD_BATCH
-#define GSF_BWD_BATCH 192
-#endif
-constexpr int kBwdBatch = GSF_BWD_BATCH;
-
-template <int NF>
-constexpr size_t bwd_smem_bytes() {
-  return static_cast<size_t>(kBwdBatch) * (8 * NF * sizeof(float) + sizeof(BlendG) + 2 * sizeof(int32_t) + 1);
-}
-
-template <int SEED, int NF>
-__global__ void __launch_bounds__(256) k_backward(BwdPtrs bp, int W, int H, int tiles_x, BlendConsts kc, double near_plane,
-                                                  double far_plane, LossParams lp, const DevState* ds) {
-  pdl_wait();   // PDL: the predecessor's results are complete from here
-  pdl_trigger();
-  extern __shared__ float4 s_dyn[];   // bwd_smem_bytes<NF>()
-  float (*s_part)[kBwdBatch][NF] = reinterpret_cast<float (*)[kBwdBatch][NF]>(s_dyn);
-  BlendG* s_g = reinterpret_cast<BlendG*>(&s_part[8][0][0]);
-  int32_t* s_id = reinterpret_cast<int32_t*>(s_g + kBwdBatch);
-  uint32_t* s_slot = reinterpret_cast<uint32_t*>(s_id + kBwdBatch);
-  uint8_t* s_mask = reinterpret_cast<uint8_t*>(s_slot + kBwdBatch);
-  __shared__ int s_wmax[8];
-  const int tile = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (ds->halt) return;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int x = tx * kTile + tile_lx(tid), y = ty * kTile + tile_ly(tid);
-  const bool inside = x < W && y < H;
-  const int64_t pi = static_cast<int64_t>(y) * W + x;
-  const int2 rg = bp.ranges[tile];
-
-  float gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, gad = 0.f, gop = 0.f, gmd = 0.f, gu = 0.f, D = 0.f, T = 1.f;
-  int med = -1, last = 0;
-  if (inside) {
-    last = bp.last[pi];
-    T = bp.final_T[pi];
-    med = bp.median_prim[pi];
-    if (SEED == SEED_EXPLICIT) {
-      if (bp.up_color) { gc0 = bp.up_color[3 * pi]; gc1 = bp.up_color[3 * pi + 1]; gc2 = bp.up_color[3 * pi + 2]; }
-      if (bp.up_adepth) gad = bp.up_adepth[pi];
-      if (bp.up_opacity) gop = bp.up_opacity[pi];
-      if (bp.up_mdepth) gmd = bp.up_mdepth[pi];
-      if (bp.up_uncert && lp.uncertainty_full_gradient) gu = bp.up_uncert[pi];
-      if (bp.obs) {
-        D = bp.obs[pi];
-        if (!dvalid(D, near_plane, far_plane)) gu = 0.f;
-      } else {
-        gu = 0.f;
-      }
-    } else {
-      const PixSeeds sd = seeds_pixel<SEED == SEED_TRACK ? 1 : 2>(pi, bp.color, bp.alpha_depth[pi], bp.median_depth[pi],
-                                                                  bp.median_valid[pi] != 0, bp.opacity[pi], bp.target,
-                                                                  bp.obs, bp.dssim, ds, lp, near_plane, far_plane);
-      gc0 = sd.gc0; gc1 = sd.gc1; gc2 = sd.gc2; gad = sd.gad; gmd = sd.gmd;
-      gu = lp.uncertainty_full_gradient ? sd.gu : 0.0f;
-      if (SEED == SEED_MAP && bp.obs) D = bp.obs[pi];
-    }
-    if (med < 0) gmd = 0.f;
-    if (gc0 == 0.f && gc1 == 0.f && gc2 == 0.f && gad == 0.f && gop == 0.f && gmd == 0.f && gu == 0.f) last = 0;
-  }
-  int ml = __reduce_max_sync(0xffffffffu, last);
-  if (lane == 0) s_wmax[warp] = ml;
-  __syncthreads();
-  int maxlast = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) maxlast = max(maxlast, s_wmax[w]);
-  bool fvalid;
-  const int fidx = rs_field(NF, lane, fvalid);
-  const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
-  float S = 0.0f;
-  const int end = rg.x + maxlast;
-  for (int bend = end; bend > rg.x; bend -= kBwdBatch) {
-    const int bstart = max(rg.x, bend - kBwdBatch);
-    const int cnt = bend - bstart;
-    if (tid < cnt) {
-      const int id = static_cast<int>(bp.sid[bstart + tid]);
-      const BlendG gj = bp.bg[id];
-      s_g[tid] = gj;
-      s_id[tid] = id;
-      const int4 q = bp.rect[id];
-      s_slot[tid] = bp.pair_base[id] + static_cast<uint32_t>((ty - q.z) * (q.y - q.x + 1) + (tx - q.x));
-      s_mask[tid] = static_cast<uint8_t>(warp_block_mask(gj, static_cast<float>(tx * kTile), static_cast<float>(ty * kTile), kc));
-    }
-    __syncthreads();
-    // back to front over only the entries whose footprint can reach this warp's block; the
-    // cross-warp sum below skips the (warp, entry) slots this loop never writes
-    for (int c0 = ((cnt - 1) >> 5) << 5; c0 >= 0; c0 -= 32) {
-     const int kk = c0 + lane;
-     uint32_t bits = __ballot_sync(0xffffffffu, kk < cnt && ((s_mask[kk] >> warp) & 1u));
-     while (bits) {
-      const int jb = 31 - __clz(bits);
-      bits &= ~(1u << jb);
-      const int k = c0 + jb;
-      const int li = bstart + k - rg.x;
-      float f[NF];
-#pragma unroll
-      for (int q = 0; q < NF; ++q) f[q] = 0.0f;
-      bool contrib = false;
-      if (li < last) {
-        const BlendG g = s_g[k];
-        const PairEval e = eval_pair_t<true>(px, py, g, bp.gg + s_id[k], kc);
-        if (e.code) {
-          contrib = true;
-          const float alpha = e.alpha;
-          const float inv = rcp_approx(1.0f - alpha);
-          const float Tpre = T * inv;
-          const float derr = g.depth - D;
-          const float q = gc0 * g.r + gc1 * g.g + gc2 * g.b + gad * g.depth + gop + gu * derr * derr;
-          const float dal = Tpre * q - S * inv;
-          const float w = alpha * Tpre;
-          S += w * q;
-          if (NF >= 9) { f[6] = w * gc0; f[7] = w * gc1; f[8] = w * gc2; }
-          f[5] = w * (gad + 2.0f * gu * derr) + (s_id[k] == med ? gmd : 0.0f);
-          if (!e.clamped) {
-            if (NF >= 10) f[9] = dal * e.gval;
-            const float dg = dal * g.sigma;
-            const float c01 = 0.5f * g.c01x2;
-            const float ux = g.c00 * e.dx + c01 * e.dy, uy = c01 * e.dx + g.c11 * e.dy;
-            const float gdg = e.gval * dg;
-            f[0] = gdg * ux;
-            f[1] = gdg * uy;
-            const float h = 0.5f * gdg;
-            f[2] = h * ux * ux;
-            f[3] = h * ux * uy;
-            f[4] = h * uy * uy;
-          }
-          T = Tpre;
-        }
-      }
-      if (__any_sync(0xffffffffu, contrib)) {
-        const float val = warp_reduce_scatter<NF>(f, lane);
-        if (fvalid) s_part[warp][k][fidx] = val;
-      } else if (lane < NF) {
-        s_part[warp][k][lane] = 0.0f;
-      }
-     }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < cnt * NF; idx += 256) {
-      const int k = idx / NF, fi = idx - k * NF;
-      const uint32_t m = s_mask[k];
-      float sum = 0.0f;
-#pragma unroll
-      for (int w = 0; w < 8; ++w)
-        if ((m >> w) & 1u) sum += s_part[w][k][fi];
-      bp.partials[static_cast<size_t>(s_slot[k]) * NF + fi] = sum;
-    }
-    __syncthreads();
-  }
-  for (int j = end + tid; j < rg.y; j += 256) {   // entries behind every pixel's last contributor
-    const int id = static_cast<int>(bp.sid[j]);
-    const int4 q = bp.rect[id];
-    const size_t slot = bp.pair_base[id] + static_cast<uint32_t>((ty - q.z) * (q.y - q.x + 1) + (tx - q.x));
-#pragma unroll
-    for (int fi = 0; fi < NF; ++fi) bp.partials[slot * NF + fi] = 0.0f;
-  }
-}
 
 // Per-pixel backward inputs (rasterizer.cpp:395-413): seeds, final T and the contributor limit.
 struct PixBwd {
@@ -1327,18 +1176,10 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     return fused_update;
   }
   if (ws.prof) ws.prof->begin(PROF_BACKWARD, st);
-#define GSF_BWD(SM, NFV)                                                                                          \
-  do {                                                                                                            \
-    static bool attr_set = false;                                                                                 \
-    if (!attr_set) {                                                                                              \
-      GSF_CUDA_CHECK(cudaFuncSetAttribute(k_backward<SM, NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                          static_cast<int>(bwd_smem_bytes<NFV>())));                             \
-      attr_set = true;                                                                                            \
-    }                                                                                                             \
-    launch_pdl(k_backward<SM, NFV>, dim3(ntiles), dim3(256), bwd_smem_bytes<NFV>(), st, bp, a.W, a.H, a.rp.tiles_x, a.kc, a.near_plane, \
-                                                                     a.far_plane, a.lp, ds);                    \
-  } while (0)
-  if (nf == 10) {   // the full bundle: per-quadrant single-warp CTAs (k_backward_q)
+  // the full bundle (a pose-only backward always takes the fused path above): per-quadrant
+  // single-warp CTAs (k_backward_q), then the quadrant slots folded per pair
+  if (nf != 10) throw std::logic_error("render_backward: a pose-only backward needs the fused pose path");
+  {
 #define GSF_BQ(SM) launch_pdl(k_backward_q<SM>, dim3(4 * ntiles), dim3(32), 0, st, bp, a.W, a.H, a.rp.tiles_x, a.kc, \
                               a.near_plane, a.far_plane, a.lp, static_cast<const DevState*>(ds), a.order,           \
                               static_cast<int64_t>(ws.tiles_cap))
@@ -1349,28 +1190,13 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
     ++*L;
     launch_pdl(k_pair_combine, dim3(4 * 148), dim3(256), 0, st, static_cast<const float*>(ws.qpart), ws.qflag, ws.partials,
                static_cast<const uint32_t*>(ws.bin_counters));
-  } else if (a.seed_mode == SEED_TRACK) {
-    if (nf == 6) GSF_BWD(SEED_TRACK, 6); else GSF_BWD(SEED_TRACK, 9);
-  } else if (a.seed_mode == SEED_MAP) {
-    if (nf == 6) GSF_BWD(SEED_MAP, 6); else GSF_BWD(SEED_MAP, 9);
-  } else {
-    if (nf == 6) GSF_BWD(SEED_EXPLICIT, 6); else GSF_BWD(SEED_EXPLICIT, 9);
   }
-#undef GSF_BWD
   ++*L;
   if (ws.prof) ws.prof->end(st);
   if (ws.prof) ws.prof->begin(PROF_CHAIN, st);
   const int blocks = std::max(1, div_up(a.P, 256));
-#define GSF_CHAIN(NFV, FULLV)                                                                                            \
-  launch_pdl(k_chain<NFV, FULLV>, dim3(blocks), dim3(256), 0, st, ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base, ws.partials, ds, \
-                                              a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part, ws.bg_id)
-  if (nf == 6)
-    GSF_CHAIN(6, false);
-  else if (nf == 9)
-    GSF_CHAIN(9, false);
-  else
-    GSF_CHAIN(10, true);
-#undef GSF_CHAIN
+  launch_pdl(k_chain<10, true>, dim3(blocks), dim3(256), 0, st, ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base,
+             ws.partials, ds, a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part, ws.bg_id);
   ++*L;
   launch_pdl(k_pose_sum, dim3(1), dim3(1024), 0, st, ws.pose_part, blocks, ds, static_cast<const uint32_t*>(ws.bin_counters));
   ++*L;

@@ -321,6 +321,8 @@ __global__ void __launch_bounds__(256, CACHED ? GSF_PRE_MINB : 2) k_preprocess(c
       }
     }
   }
+  // a CTA with no visible primitive has no pair, slot or list entry to emit: skip the CTA scans
+  if (!__syncthreads_or(vis)) return;
   const uint32_t bits = __ballot_sync(0xffffffffu, vis);
   if (lane == 0) s_vis[warp] = static_cast<uint32_t>(__popc(bits));
   // tile binning (binning.cu): every (tile, primitive) pair into its tile's bucket
@@ -452,7 +454,7 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // pixel_accumulate (gsf_shared.cuh) with the colour / alpha-depth sums as two packed FFMA2s;
 // every lane rounds like __fmaf_rn, so the state equals the mirror's bit for bit.
-template <bool FLAG>
+template <bool FLAG, bool DOM = true>
 __device__ __forceinline__ void full_accumulate(PixelState& s, float2& rg, float2& bd, const BlendG& g, const PairEval& e,
                                                 int32_t id, int32_t list_index, bool obs_valid, float obs,
                                                 const BlendConsts& k) {
@@ -466,11 +468,13 @@ __device__ __forceinline__ void full_accumulate(PixelState& s, float2& rg, float
     const float d = fsub(g.depth, obs);
     s.unc = ffma(fmul(w, d), d, s.unc);
   }
-  if (w > s.best) {
-    s.best = w;
-    s.dominant = id;
+  if (DOM) {   // the dominant contributor and the count: the render API and the uncertainty pass
+    if (w > s.best) {
+      s.best = w;
+      s.dominant = id;
+    }
+    s.count += 1;
   }
-  s.count += 1;
   s.last = list_index + 1;
   const float t_next = fmul(s.T, fsub(1.0f, e.alpha));
   if (s.median < 0 && s.T >= 0.5f && t_next < 0.5f) {
@@ -553,7 +557,8 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
         if (s.done) continue;
         const BlendG g = s_g[k];
         const PairEval e = eval_pair(px, py, g, gg + s_id[k], kc);
-        if (e.code) full_accumulate<LMODE == 0>(s, frg, fbd, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
+        // the mapping objective reads neither the dominant contributor nor the count (LMODE 2)
+        if (e.code) full_accumulate<LMODE == 0, LMODE != 2>(s, frg, fbd, g, e, s_id[k], start + k - rg.x, obs_valid, ov, kc);
       }
     }
   }
@@ -572,10 +577,12 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
     o_md[pi] = s.med_depth;
     o_mv[pi] = s.median >= 0 ? 1 : 0;
     o_unc[pi] = s.unc;
-    o_count[pi] = s.count;
-    o_dom[pi] = s.dominant;
+    if (LMODE != 2) {
+      o_count[pi] = s.count;
+      o_dom[pi] = s.dominant;
+      o_domw[pi] = s.best;
+    }
     o_med[pi] = s.median;
-    o_domw[pi] = s.best;
     if (LMODE == 0 && s.flag) fix_list[atomicAdd(fix_cnt, 1u)] = static_cast<uint32_t>(pi);
   }
   if (LMODE == 0) return;
