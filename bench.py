@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--map-primitives", type=int, default=1000000)
     ap.add_argument("--window", type=int, default=16)
-    ap.add_argument("--map-iters", type=int, default=3)
+    ap.add_argument("--map-iters", type=int, default=10)
     ap.add_argument("--no-mapping", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="small workload for smoke timing")

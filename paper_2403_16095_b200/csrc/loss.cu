@@ -40,14 +40,35 @@ __global__ void __launch_bounds__(1024) k_loss_finalize(const double* __restrict
                                                         int iso_blocks, DevState* ds) {
   pdl_wait();   // PDL: the predecessor's results are complete from here
   pdl_trigger();
-  __shared__ double s_red[32][LS_NUM];
-  __shared__ double s_red1[32][1];
-  __shared__ double s_tot[LS_NUM];
-  __shared__ double s_ssim[1], s_iso[1];
-  block_reduce_rows<LS_NUM, 1024>(loss_part, tiles, s_tot, s_red);
-  block_reduce_rows<1, 1024>(ssim_part, ssim_blocks, s_ssim, s_red1);
-  block_reduce_rows<1, 1024>(iso_part, iso_blocks, s_iso, s_red1);
-  if (threadIdx.x == 0) loss_scalars(ds, lp, s_tot, s_ssim[0], s_iso[0], npix, iteration);
+  // one pass over the three partial arrays (thread t owns rows t, t + 1024, ... of each: a fixed
+  // order), one warp reduction and one barrier for all LS_NUM + 2 sums
+  constexpr int NV = LS_NUM + 2;
+  __shared__ double s_red[32][NV];
+  __shared__ double s_tot[NV];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  for (int r = tid; r < tiles; r += 1024) {
+    const double* row = loss_part + static_cast<int64_t>(r) * LS_NUM;
+#pragma unroll
+    for (int q = 0; q < LS_NUM; ++q) acc[q] += __ldcg(row + q);
+  }
+  for (int r = tid; r < ssim_blocks; r += 1024) acc[LS_NUM] += __ldcg(ssim_part + r);
+  for (int r = tid; r < iso_blocks; r += 1024) acc[LS_NUM + 1] += __ldcg(iso_part + r);
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double t = warp_sum_f64(acc[q]);
+    if (lane == 0) s_red[warp][q] = t;
+  }
+  __syncthreads();
+  if (tid < NV) {
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) t += s_red[w][tid];
+    s_tot[tid] = t;
+  }
+  __syncthreads();
+  if (tid == 0) loss_scalars(ds, lp, s_tot, s_tot[LS_NUM], s_tot[LS_NUM + 1], npix, iteration);
 }
 
 // ---- SSIM ------------------------------------------------------------------------------------

@@ -908,6 +908,160 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   }
 }
 
+// Mapping forward (blend_pixel, rasterizer.cpp:96-140, with the mapping loss's partials,
+// losses.cpp:156-282) as independent single-warp CTAs: CTA 4 t + q owns quadrant q (8x8 pixels,
+// two per lane, the layout of k_blend_track) of tile t and walks the tile list front to back in
+// chunks of 32 entries: lane e stages entry e of the chunk (record by cp.async, id two chunks
+// ahead), tests it against the quadrant's block (block_hit8) and the warp walks the set bits with
+// the forward's exact decision path.  No CTA barriers; the quadrant's loss partials are one row
+// of loss_part (4 rows per tile) and its (warp, entry) steps the backward's LPT cost (qstat).
+// Per pixel the state updates run in pixel_accumulate's operation order (packed FP32x2 rounds like
+// the scalar op), so the maps equal k_blend<2>'s.
+#ifndef GSF_FQ_MINB
+#define GSF_FQ_MINB 24
+#endif
+__global__ void __launch_bounds__(32, GSF_FQ_MINB) k_blend_mq(
+    const int2* __restrict__ ranges, const uint32_t* __restrict__ sid, const BlendG* __restrict__ bg,
+    const GuardG* __restrict__ gg, const float* __restrict__ obs, const float* __restrict__ loss_rgb,
+    const float* __restrict__ loss_depth, int W, int H, int tiles_x, BlendConsts kc, double near_plane,
+    double far_plane, LossParams lp, DevState* ds, float* __restrict__ o_color, float* __restrict__ o_ad,
+    float* __restrict__ o_md, uint8_t* __restrict__ o_mv, float* __restrict__ o_op, float* __restrict__ o_unc,
+    float* __restrict__ o_T, int32_t* __restrict__ o_med, int32_t* __restrict__ o_last, double* __restrict__ loss_part,
+    int2* __restrict__ qstat) {
+  __shared__ float4 s_buf[2 * 3 * 32 + 16];   // two buffers of 32 records (1536 B) + their ids (128 B) at 3072 + 128 b
+  pdl_wait();
+  pdl_trigger();
+  if (ds->halt) return;
+  const int lane = threadIdx.x;
+  const uint32_t sb = opaque_smem_base(s_buf);
+  const int item = static_cast<int>(blockIdx.x);
+  const int tile = item >> 2, qd = item & 3;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int bx0 = tx * kTile + 8 * (qd & 1), by0 = ty * kTile + 8 * (qd >> 1);
+  const int x = bx0 + (lane & 7);
+  const int ya = by0 + (lane >> 3), yb = ya + 4;
+  const bool in_a = x < W && ya < H, in_b = x < W && yb < H;
+  const int64_t pa = static_cast<int64_t>(ya) * W + x, pb = static_cast<int64_t>(yb) * W + x;
+  const int2 rg = ranges[tile];
+  float2 rg_a = make_float2(0.f, 0.f), bd_a = rg_a, rg_b = rg_a, bd_b = rg_a;
+  float2 op = make_float2(0.f, 0.f), unc = make_float2(0.f, 0.f);
+  float2 T = make_float2(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);   // outside the image: done from the start
+  int last_a = 0, last_b = 0, med_a = -1, med_b = -1;
+  float md_a = 0.0f, md_b = 0.0f;
+  bool ov_a = false, ov_b = false;
+  float obs_a = 0.0f, obs_b = 0.0f;
+  if (obs) {
+    if (in_a) { obs_a = obs[pa]; ov_a = depth_valid(obs_a, near_plane, far_plane); }
+    if (in_b) { obs_b = obs[pb]; ov_b = depth_valid(obs_b, near_plane, far_plane); }
+  }
+  const float px = static_cast<float>(x) + 0.5f;
+  const float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
+  const float qx0 = static_cast<float>(bx0), qy0 = static_cast<float>(by0);
+  const int len = rg.y - rg.x;
+  const int nch = (len + 31) / 32;
+  auto fetch = [&](int c) -> int32_t {
+    const int j = rg.x + 32 * c + lane;
+    return (c < nch && j < rg.y) ? static_cast<int32_t>(__ldg(sid + j)) : -1;
+  };
+  auto issue = [&](int c, int32_t id) {
+    if (c < nch && id >= 0) {
+      const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 1536u;
+      const float4* rec = reinterpret_cast<const float4*>(bg + id);
+      cp_async16_to(buf + 48u * lane, rec);
+      cp_async16_to(buf + 48u * lane + 16u, rec + 1);
+      cp_async16_to(buf + 48u * lane + 32u, rec + 2);
+      sts_s32(sb + 3072u + static_cast<uint32_t>(c & 1) * 128u + 4u * lane, id);
+    }
+    cp_async_commit();
+  };
+  uint32_t steps = 0u;
+  int32_t id0 = fetch(0), id1 = fetch(1);
+  issue(0, id0);
+  for (int c = 0; c < nch; ++c) {
+    if (__all_sync(0xffffffffu, T.x < kc.term && T.y < kc.term)) break;
+    issue(c + 1, id1);
+    const int32_t id2 = fetch(c + 2);
+    cp_async_wait_1();
+    __syncwarp();
+    const uint32_t buf = sb + static_cast<uint32_t>(c & 1) * 1536u, idb = sb + 3072u + static_cast<uint32_t>(c & 1) * 128u;
+    bool hit = false;
+    if (id0 >= 0) hit = block_hit8(lds_blend(buf + 48u * lane), qx0, qy0, kc);
+    uint32_t bits = __ballot_sync(0xffffffffu, hit);
+    steps += __popc(bits);
+    while (bits) {
+      const int e = __ffs(bits) - 1;   // lowest lane = earliest entry: front to back
+      bits &= bits - 1u;
+      const BlendG g = lds_blend(buf + 48u * e);
+      const float dx = __fadd_rn(px, -g.mx);
+      const float2 dy = __fadd2_rn(py, make_float2(-g.my, -g.my));
+      const float2 rho = pair_rho2(dx, dy, g);
+      const bool skip_a = T.x < kc.term || rho.x > g.rho_hi, skip_b = T.y < kc.term || rho.y > g.rho_hi;
+      if (__all_sync(0xffffffffu, skip_a && skip_b)) continue;
+      const bool fast_a = rho.x < g.rho_fast, fast_b = rho.y < g.rho_fast;
+      float2 al = __fmul2_rn(make_float2(g.sigma, g.sigma), exp_neg_half_inrange2(rho));
+      bool ca = !skip_a && fast_a, cb = !skip_b && fast_b;
+      const int32_t eid = lds_s32(idb + 4u * e);
+      if (__any_sync(0xffffffffu, (!skip_a && !fast_a) || (!skip_b && !fast_b))) {
+        if (!skip_a && !fast_a) {
+          al.x = guard_decide(px, py.x, g, gg + eid, &kc).alpha;
+          ca = al.x >= 0.0f;
+        }
+        if (!skip_b && !fast_b) {
+          al.y = guard_decide(px, py.y, g, gg + eid, &kc).alpha;
+          cb = al.y >= 0.0f;
+        }
+      }
+      const float2 am = make_float2(ca ? al.x : 0.0f, cb ? al.y : 0.0f);
+      const float2 w = __fmul2_rn(am, T);
+      rg_a = __ffma2_rn(make_float2(w.x, w.x), make_float2(g.r, g.g), rg_a);
+      bd_a = __ffma2_rn(make_float2(w.x, w.x), make_float2(g.b, g.depth), bd_a);
+      rg_b = __ffma2_rn(make_float2(w.y, w.y), make_float2(g.r, g.g), rg_b);
+      bd_b = __ffma2_rn(make_float2(w.y, w.y), make_float2(g.b, g.depth), bd_b);
+      op = __fadd2_rn(op, w);
+      if (ca && ov_a) { const float d = __fadd_rn(g.depth, -obs_a); unc.x = __fmaf_rn(__fmul_rn(w.x, d), d, unc.x); }
+      if (cb && ov_b) { const float d = __fadd_rn(g.depth, -obs_b); unc.y = __fmaf_rn(__fmul_rn(w.y, d), d, unc.y); }
+      const float2 tn = __fmul2_rn(T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-am.x, -am.y)));
+      if (ca && med_a < 0 && T.x >= 0.5f && tn.x < 0.5f) { med_a = eid; md_a = g.depth; }
+      if (cb && med_b < 0 && T.y >= 0.5f && tn.y < 0.5f) { med_b = eid; md_b = g.depth; }
+      T = tn;
+      const int li = 32 * c + e + 1;
+      if (ca) last_a = li;
+      if (cb) last_b = li;
+    }
+    __syncwarp();   // buffer c & 1 is refilled by issue(c + 2)
+    id0 = id1;
+    id1 = id2;
+  }
+  cp_async_wait_all();
+  if (qstat && lane == 0) qstat[item] = make_int2(static_cast<int>(steps), len);
+  double v[LS_NUM], vb[LS_NUM];
+#pragma unroll
+  for (int q = 0; q < LS_NUM; ++q) v[q] = vb[q] = 0.0;
+  const bool has_unc = obs != nullptr;
+  if (in_a) {
+    o_color[3 * pa + 0] = rg_a.x; o_color[3 * pa + 1] = rg_a.y; o_color[3 * pa + 2] = bd_a.x;
+    o_ad[pa] = bd_a.y; o_op[pa] = op.x; o_T[pa] = T.x; o_last[pa] = last_a;
+    o_md[pa] = md_a; o_mv[pa] = med_a >= 0 ? 1 : 0; o_unc[pa] = unc.x; o_med[pa] = med_a;
+    if (loss_rgb)
+      loss_pixel<2>(v, rg_a.x, rg_a.y, bd_a.x, bd_a.y, md_a, med_a >= 0, op.x, unc.x, loss_rgb + 3 * pa, loss_depth, pa,
+                    has_unc, near_plane, far_plane, lp.opacity_floor);
+  }
+  if (in_b) {
+    o_color[3 * pb + 0] = rg_b.x; o_color[3 * pb + 1] = rg_b.y; o_color[3 * pb + 2] = bd_b.x;
+    o_ad[pb] = bd_b.y; o_op[pb] = op.y; o_T[pb] = T.y; o_last[pb] = last_b;
+    o_md[pb] = md_b; o_mv[pb] = med_b >= 0 ? 1 : 0; o_unc[pb] = unc.y; o_med[pb] = med_b;
+    if (loss_rgb)
+      loss_pixel<2>(vb, rg_b.x, rg_b.y, bd_b.x, bd_b.y, md_b, med_b >= 0, op.y, unc.y, loss_rgb + 3 * pb, loss_depth, pb,
+                    has_unc, near_plane, far_plane, lp.opacity_floor);
+  }
+  if (!loss_rgb) return;
+#pragma unroll
+  for (int q = 0; q < LS_NUM; ++q) {
+    const double t = warp_sum_d(v[q] + vb[q]);
+    if (lane == 0) loss_part[static_cast<int64_t>(item) * LS_NUM + q] = t;
+  }
+}
+
 // Stand-alone loss partials over stored maps (evaluate_*_loss called on a RenderResult).
 template <int LMODE>
 __global__ void __launch_bounds__(256) k_loss_tiles(const float* __restrict__ color, const float* __restrict__ ad,
@@ -1012,8 +1166,18 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     else GSF_BLEND_TRACK(0);
 #undef GSF_BLEND_TRACK
   }
-  else if (a.lp.mode == 2 && loss_rgb)
+  else if (a.lp.mode == 2 && loss_rgb) {
+#ifdef GSF_MAP_FWD8
     launch_pdl(k_blend<2>, dim3(ntiles), dim3(256), 0, st, GSF_BLEND_ARGS);
+#else
+    // the mapping forward as per-quadrant single-warp CTAs, one loss row per quadrant
+    ws.loss_rows = 4 * ntiles;
+    launch_pdl(k_blend_mq, dim3(4 * ntiles), dim3(32), 0, st, ws.ranges, ws.sid, ws.bg_id, ws.gg_id, a.obs, loss_rgb,
+               a.loss_depth, a.W, a.H, tiles_x, a.kc, a.near_plane, a.far_plane, a.lp, ds, ws.color, ws.alpha_depth,
+               ws.median_depth, ws.median_valid, ws.opacity, ws.uncertainty, ws.final_T, ws.median_prim, ws.last,
+               ws.loss_part, ws.qstat);
+#endif
+  }
   else {
     launch_pdl(k_blend<0>, dim3(ntiles), dim3(256), 0, st, GSF_BLEND_ARGS);
     ++*L;
