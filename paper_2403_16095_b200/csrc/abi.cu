@@ -78,12 +78,6 @@ struct Frame {
 };
 
 // Per-keyframe pose + Adam state for sliding_ba / map_step, device resident.
-struct KfPose {
-  double rot[3], trans[3];
-  double m[6], v[6];
-  double t;
-  double grad[6];
-};
 
 }  // namespace
 
@@ -557,13 +551,6 @@ __global__ void k_set_cam_from_kf(DevState* ds, const KfPose* kf, int k, int has
   ds->has_obs = has_obs;
 }
 
-__global__ void k_kf_grab(DevState* ds, KfPose* kf, int k, double* loss_acc, double* trace, int it, int store_trace) {
-  pdl_wait();   // PDL: the predecessor's results are complete from here
-  pdl_trigger();
-  for (int a = 0; a < 6; ++a) kf[k].grad[a] = ds->d_pose[a];
-  if (loss_acc) *loss_acc += ds->loss_total;
-  if (store_trace && trace) trace[it] = ds->loss_total;
-}
 
 __global__ void k_store(const double* src, double* dst) { *dst = *src; }
 
@@ -1487,13 +1474,18 @@ static AdamGroups groups_of(const gsf_mapper_cfg& m) {
 }
 
 // One mapping-objective forward/backward of keyframe k into c->grads (accumulating).
+// cam_staged: the previous view's k_pose_sum already made keyframe k's camera current; next_k >= 0:
+// this view's k_pose_sum stages keyframe next_k's camera for the following view.
 static void enqueue_map_view(gsf_ctx_s* c, const Frame& f, int k, const gsf_intrinsics& K, const gsf_mapper_cfg& m, int it,
-                             double* loss_acc, int trace_index, bool use_world = false) {
+                             double* loss_acc, int trace_index, bool use_world = false, bool cam_staged = false,
+                             int next_k = -1) {
   const LossParams lp = make_lp(2, &m.weights, m.raster);
   const int tiles = ((K.width + kTile - 1) / kTile) * ((K.height + kTile - 1) / kTile);
   const int64_t npix = static_cast<int64_t>(K.width) * K.height;
-  launch_pdl(k_set_cam_from_kf, dim3(1), dim3(1), 0, c->stream, c->ds, c->kf, k, 1);
-  ++c->launches;
+  if (!cam_staged) {
+    launch_pdl(k_set_cam_from_kf, dim3(1), dim3(1), 0, c->stream, c->ds, c->kf, k, 1);
+    ++c->launches;
+  }
   FwdArgs fa = fwd_args(c, K, m.raster, f.depth, f.rgb, f.depth, lp, it);
   fa.use_world = use_world;
   run_forward(c->ws, c->ds, fa, c->stream, &c->launches);
@@ -1514,11 +1506,16 @@ static void enqueue_map_view(gsf_ctx_s* c, const Frame& f, int k, const gsf_intr
   GSF_CUDA_CHECK(cudaStreamWaitEvent(c->stream, wsl.ev_ljoin, 0));
   b.order = wsl.order;
 #endif
+  b.iso_w = m.weights.w_iso;   // the iso gradient is added by k_chain (no second iso pass)
+  b.iso_eps = m.weights.iso_epsilon;
+  // k_kf_grab and the next view's k_set_cam_from_kf run in the chain's k_pose_sum
+  b.post.kf = c->kf;
+  b.post.grab = k;
+  b.post.loss_acc = loss_acc;
+  b.post.trace = c->trace_dev;
+  b.post.trace_index = trace_index;
+  b.post.next = next_k;
   run_backward(c->ws, c->ds, b, c->stream, &c->launches);
-  if (m.weights.w_iso > 0.0)
-    run_iso(c->ws, c->ds, c->params, c->P, m.weights.w_iso, m.weights.iso_epsilon, c->grads, c->stream, &c->launches);
-  launch_pdl(k_kf_grab, dim3(1), dim3(1), 0, c->stream, c->ds, c->kf, k, loss_acc, c->trace_dev, trace_index, trace_index >= 0 ? 1 : 0);
-  ++c->launches;
 }
 
 static void upload_kf(gsf_ctx_s* c, const gsf_pose* poses, int n) {
@@ -1741,12 +1738,17 @@ int gsf_sliding_ba(gsf_ctx c, const int32_t* slots, gsf_pose* poses, const int32
       GSF_CUDA_CHECK(cudaMemsetAsync(loss_acc, 0, sizeof(double), c->stream));
       // the map is constant across this iteration's keyframes: validate + cache it once
       run_world(c->ws, c->ds, c->params, c->P, make_rp(c, *K, m->raster), c->stream, &c->launches);
+      bool staged = false;
       for (int k = 0; k < n; ++k) {
         if (!owned[k]) {
           GSF_CUDA_CHECK(cudaMemsetAsync(kf_grad(c, k), 0, sizeof(double) * 6, c->stream));
           continue;
         }
-        enqueue_map_view(c, *fr[k], k, *K, *m, it, loss_acc, -1, true);
+        int next = -1;   // the next owned view of this iteration (the poses change after its last view)
+        for (int j = k + 1; j < n && next < 0; ++j)
+          if (owned[j]) next = j;
+        enqueue_map_view(c, *fr[k], k, *K, *m, it, loss_acc, -1, true, staged, next);
+        staged = next >= 0;
       }
       c->adam_step += 1.0;
       if (c->nranks > 1) {

@@ -9,6 +9,25 @@
 
 namespace gsfk {
 
+// A window keyframe's pose, its Adam moments and its summed pose gradient (sliding_ba / map_step).
+struct KfPose {
+  double rot[3], trans[3];
+  double m[6], v[6];
+  double t;
+  double grad[6];
+};
+
+// Keyframe bookkeeping folded into the chain's pose sum (mapping views): copy the view's pose
+// gradient and loss out, and stage the next view's camera, without launches of their own.
+struct PoseSumPost {
+  KfPose* kf = nullptr;
+  int grab = -1;              // keyframe whose grad receives d_pose (-1: none)
+  double* loss_acc = nullptr; // += the view's total loss
+  double* trace = nullptr;    // [trace_index] = the view's total loss (if trace_index >= 0)
+  int trace_index = -1;
+  int next = -1;              // keyframe whose camera becomes ds->cam (-1: none)
+};
+
 // Optional CUDA-event brackets around named kernels (bench / roofline evidence only).
 struct Profiler {
   struct Mark { int name; cudaEvent_t a, b; };
@@ -205,6 +224,9 @@ struct BwdArgs {
   int update_iter = -1;      // >= 0: the tracking backward's last CTA also takes this iteration's pose step
   const uint32_t* order = nullptr;  // tracking: CTA order buffer (Workspace::order half) of the pose backward
   float* grads;              // [D][P] parameter gradients (full mode)
+  double iso_w = 0.0;        // > 0: k_chain also adds the iso term's direct log-scale gradient (losses.cpp:272-280)
+  PoseSumPost post;          // mapping views: k_pose_sum's keyframe bookkeeping
+  double iso_eps = 0.0;
   float* d_mean2d;           // [2][P] (full mode, nullable)
 };
 // true when the backward also ran the pose step of a.update_iter (k_track_update is then skipped)

@@ -714,14 +714,15 @@ __global__ void __launch_bounds__(256) k_pair_combine(const float* __restrict__ 
   const uint32_t M = counters[kCntPairAlloc];
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < M; p += gridDim.x * blockDim.x) {
     const uint32_t fl = qflag[p];
-    const float4* src = reinterpret_cast<const float4*>(qpart + static_cast<size_t>(p) * 40);
-    float4 v[10];
-#pragma unroll
-    for (int h = 0; h < 10; ++h) v[h] = __ldcs(src + h);   // read once: streaming
     if (fl) qflag[p] = 0u;
     float t[10];
 #pragma unroll
     for (int f = 0; f < 10; ++f) t[f] = 0.0f;
+    // all four slots are read (a read conditioned on the flag waits on it: measured slower)
+    const float4* src = reinterpret_cast<const float4*>(qpart + static_cast<size_t>(p) * 40);
+    float4 v[10];
+#pragma unroll
+    for (int h = 0; h < 10; ++h) v[h] = __ldcs(src + h);   // read once: streaming
 #pragma unroll
     for (int qd = 0; qd < 4; ++qd) {
       if (!((fl >> (8 * qd)) & 1u)) continue;
@@ -825,7 +826,8 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
                                                const float* __restrict__ partials, const DevState* ds,
                                                const float* __restrict__ params, int64_t P, int K,
                                                float* __restrict__ grads, float* __restrict__ d_mean2d,
-                                               double* __restrict__ pose_part, const BlendG* __restrict__ bg) {
+                                               double* __restrict__ pose_part, const BlendG* __restrict__ bg,
+                                               double iso_w, double iso_eps) {
   pdl_wait();   // PDL: the predecessor's results are complete from here
   pdl_trigger();
   __shared__ double s_red[8][6];
@@ -1030,6 +1032,23 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
       }
     }
   }
+  if (active && FULL && iso_w > 0.0) {
+    // the iso term's direct log-scale gradient of every visible primitive (losses.cpp:272-280, k_iso's
+    // arithmetic), added after the primitive's bundle like the stand-alone pass did
+    const double sx[3] = {exp(static_cast<double>(GSF_PAR(3))), exp(static_cast<double>(GSF_PAR(4))),
+                          exp(static_cast<double>(GSF_PAR(5)))};
+    int a = 0, b = 0;
+    for (int c = 1; c < 3; ++c) {
+      if (sx[c] > sx[a]) a = c;
+      if (sx[c] < sx[b]) b = c;
+    }
+    const double ratio = sx[a] / sx[b];
+    if (ratio > iso_eps) {
+      const double g = iso_w * ratio / static_cast<double>(V);
+      acc_grad(grads, (3 + a) * P + id, g);
+      acc_grad(grads, (3 + b) * P + id, -g);
+    }
+  }
   // deterministic block reduction of the pose pieces
 #pragma unroll
   for (int a = 0; a < 6; ++a) {
@@ -1047,7 +1066,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
 #undef GSF_PAR
 
 __global__ void __launch_bounds__(1024) k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds,
-                                                   const uint32_t* counters) {
+                                                   const uint32_t* counters, PoseSumPost post) {
   pdl_wait();   // PDL: the predecessor's results are complete from here
   pdl_trigger();
   blocks = min(blocks, static_cast<int>((counters[kCntVisible] + 255u) / 256u));   // k_chain's CTAs with a row
@@ -1064,7 +1083,20 @@ __global__ void __launch_bounds__(1024) k_pose_sum(const double* __restrict__ po
   if (tid < 6) {
     double t = 0.0;
     for (int w = 0; w < 32; ++w) t += s_red[w][tid];
-    ds->d_pose[tid] = ds->halt ? 0.0 : t;
+    t = ds->halt ? 0.0 : t;
+    ds->d_pose[tid] = t;
+    if (post.grab >= 0) post.kf[post.grab].grad[tid] = t;   // k_kf_grab's copy
+  }
+  if (tid == 0) {
+    if (post.loss_acc) *post.loss_acc += ds->loss_total;
+    if (post.trace && post.trace_index >= 0) post.trace[post.trace_index] = ds->loss_total;
+    if (post.next >= 0) {   // k_set_cam_from_kf for the next view (every reader of this view's camera ran)
+      const Cam old = ds->cam;
+      const KfPose& p = post.kf[post.next];
+      ds->cam = make_cam(p.rot, p.trans, old.fx, old.fy, old.cx, old.cy, old.width, old.height, old.near_plane,
+                         old.far_plane);
+      ds->has_obs = 1;
+    }
   }
 }
 
@@ -1196,9 +1228,10 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   if (ws.prof) ws.prof->begin(PROF_CHAIN, st);
   const int blocks = std::max(1, div_up(a.P, 256));
   launch_pdl(k_chain<10, true>, dim3(blocks), dim3(256), 0, st, ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base,
-             ws.partials, ds, a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part, ws.bg_id);
+             ws.partials, ds, a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part, ws.bg_id, a.iso_w, a.iso_eps);
   ++*L;
-  launch_pdl(k_pose_sum, dim3(1), dim3(1024), 0, st, ws.pose_part, blocks, ds, static_cast<const uint32_t*>(ws.bin_counters));
+  launch_pdl(k_pose_sum, dim3(1), dim3(1024), 0, st, ws.pose_part, blocks, ds, static_cast<const uint32_t*>(ws.bin_counters),
+             a.post);
   ++*L;
   if (ws.prof) ws.prof->end(st);
   return false;
