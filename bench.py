@@ -584,7 +584,7 @@ def mapping_evidence(mctx, slots, kposes, kf, K, tc, mc, iters=2):
                 "unit": "GB/s", "frac": (a / hbm) if a else None}
 
     roof = {
-        "blend k_blend<2>": fp("blend", 11 * T + 24 * Cn, fp32_peak, "fp32: 11 T + 24 C"),
+        "blend k_blend_mq": fp("blend", 11 * T + 24 * Cn, fp32_peak, "fp32: 11 T + 24 C"),
         "backward k_backward_q<SEED_MAP> + k_pair_combine": fp("backward", 13 * T + 70 * Cn, fp32_peak, "fp32: 13 T + 70 C"),
         "chain k_chain<10> (+k_pose_sum)": fp("chain", 300 * V, fp64_peak,
                                              "fp64: 300 V (peak = 148 SMs x 64 FP64 lanes x 2 x clock)"),

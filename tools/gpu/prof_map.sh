@@ -4,6 +4,6 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 TAG=${TAG:-pm}
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k "regex:^(k_chain|k_backward_q|k_pair_combine|k_blend|k_preprocess)$" --launch-skip 32 -c 5 \
+  -k "regex:^(k_chain|k_backward_q|k_pair_combine|k_blend_mq|k_preprocess)$" --launch-skip 16 -c 5 \
   -o gpurun_out/${TAG}_map python tools/profile_map.py 1 > gpurun_out/${TAG}_map.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/${TAG}_map.log
