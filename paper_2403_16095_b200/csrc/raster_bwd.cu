@@ -840,6 +840,17 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   if (blockIdx.x * blockDim.x >= V) return;
   float pf_par[14];
 #define GSF_PAR(F) pf_par[F]
+#ifdef GSF_CHAIN_GPF
+  float gpre[16];
+#define GSF_ACC(ARR, F, IDX, V)                                                      \
+  {                                                                                  \
+    const float nv_ = static_cast<float>(static_cast<double>(gpre[F]) + (V));        \
+    gpre[F] = nv_;                                                                   \
+    ARR[IDX] = nv_;                                                                  \
+  }
+#else
+#define GSF_ACC(ARR, F, IDX, V) acc_grad(ARR, IDX, V)
+#endif
   const bool halted = ds->halt != 0;
   bool active = r < V;   // halted: the slots are still read and zeroed, no gradient is written
   int64_t id = 0;
@@ -850,6 +861,15 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
     // the primitive's parameters, loaded before the pair gather so their latency overlaps it
 #pragma unroll
     for (int f = 0; f < 14; ++f) pf_par[f] = (f < 11 || K == 1) ? params[f * P + id] : 0.0f;
+#ifdef GSF_CHAIN_GPF
+    // ... and its accumulated gradients: the read-modify-writes below then need no load each (a load
+    // after a store into the same array cannot be hoisted by the compiler: 14 serial round trips)
+    if (FULL) {
+#pragma unroll
+      for (int f = 0; f < 14; ++f) gpre[f] = (f < 11 || K == 1) ? grads[f * P + id] : 0.0f;
+      if (d_mean2d) { gpre[14] = d_mean2d[id]; gpre[15] = d_mean2d[P + id]; }
+    }
+#endif
     const int4 q = rect_id[id];
     c = (q.y - q.x + 1) * (q.w - q.z + 1);
     pp = partials + static_cast<size_t>(pair_base[id]) * NF;
@@ -984,18 +1004,18 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
         // degree 0: colour_c = max(0.5 + C0 sh_c, 0), no view-direction gradient (sh.cpp:88-108)
         for (int c = 0; c < 3; ++c) {
           const double raw = 0.5 + 0.28209479177387814 * GSF_PAR(11 + c);
-          acc_grad(grads, (11 + c) * P + id, raw < 0.0 ? 0.0 : 0.28209479177387814 * dcol[c]);
+          GSF_ACC(grads, 11 + c, (11 + c) * P + id, raw < 0.0 ? 0.0 : 0.28209479177387814 * dcol[c]);
         }
       } else if (K > 1) {
         sh_backward(params, P, id, K, cam, m0, m1, m2, dcol, FULL ? grads : nullptr, through);
         for (int a = 0; a < 3; ++a) pose[3 + a] += Wr[3 * a + 0] * through[0] + Wr[3 * a + 1] * through[1] + Wr[3 * a + 2] * through[2];
       }
       if (FULL) {
-        if (d_mean2d) { acc_grad(d_mean2d, id, sg[0]); acc_grad(d_mean2d, P + id, sg[1]); }
+        if (d_mean2d) { GSF_ACC(d_mean2d, 14, id, sg[0]); GSF_ACC(d_mean2d, 15, P + id, sg[1]); }
         // world parameters (rasterizer.cpp:528-546)
         for (int a = 0; a < 3; ++a) {
           const double dm = Wr[0 * 3 + a] * dp[0] + Wr[1 * 3 + a] * dp[1] + Wr[2 * 3 + a] * dp[2] + through[a];
-          acc_grad(grads, a * P + id, dm);
+          GSF_ACC(grads, a, a * P + id, dm);
         }
         double dCw[3][3], T2[3][3];
         for (int a = 0; a < 3; ++a)
@@ -1008,7 +1028,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
             dM[a][b] = 2.0 * (dCw[a][0] * R[0][b] * s[b] + dCw[a][1] * R[1][b] * s[b] + dCw[a][2] * R[2][b] * s[b]);
         for (int a = 0; a < 3; ++a) {
           const double ds_ = R[0][a] * dM[0][a] + R[1][a] * dM[1][a] + R[2][a] * dM[2][a];
-          acc_grad(grads, (3 + a) * P + id, ds_ * s[a]);
+          GSF_ACC(grads, 3 + a, (3 + a) * P + id, ds_ * s[a]);
         }
         double dR[3][3];
         for (int a = 0; a < 3; ++a)
@@ -1026,9 +1046,9 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
           dqn[kq] = acc;
         }
         const double qd = qn[0] * dqn[0] + qn[1] * dqn[1] + qn[2] * dqn[2] + qn[3] * dqn[3];
-        for (int a = 0; a < 4; ++a) acc_grad(grads, (6 + a) * P + id, (dqn[a] - qn[a] * qd) / qlen);
+        for (int a = 0; a < 4; ++a) GSF_ACC(grads, 6 + a, (6 + a) * P + id, (dqn[a] - qn[a] * qd) / qlen);
         const double sig = 1.0 / (1.0 + exp(-static_cast<double>(GSF_PAR(10))));
-        acc_grad(grads, 10 * P + id, (NF >= 10 ? sg[9] : 0.0) * sig * (1.0 - sig));
+        GSF_ACC(grads, 10, 10 * P + id, (NF >= 10 ? sg[9] : 0.0) * sig * (1.0 - sig));
       }
     }
   }
@@ -1045,8 +1065,11 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
     const double ratio = sx[a] / sx[b];
     if (ratio > iso_eps) {
       const double g = iso_w * ratio / static_cast<double>(V);
-      acc_grad(grads, (3 + a) * P + id, g);
-      acc_grad(grads, (3 + b) * P + id, -g);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {   // static register indices
+        if (c == a) GSF_ACC(grads, 3 + c, (3 + c) * P + id, g);
+        if (c == b) GSF_ACC(grads, 3 + c, (3 + c) * P + id, -g);
+      }
     }
   }
   // deterministic block reduction of the pose pieces
@@ -1064,6 +1087,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   }
 }
 #undef GSF_PAR
+#undef GSF_ACC
 
 __global__ void __launch_bounds__(1024) k_pose_sum(const double* __restrict__ pose_part, int blocks, DevState* ds,
                                                    const uint32_t* counters, PoseSumPost post) {

@@ -282,21 +282,12 @@ __global__ void __launch_bounds__(256, CACHED ? GSF_PRE_MINB : 2) k_preprocess(c
     PreOut o;
     bool ok = true;
     if (CACHED) {
-#ifdef GSF_PRE_SPEC
-      // the mean is loaded with the support (one round trip instead of two; an invalid primitive's
-      // mean is read and ignored)
-      const double sup = support[i];
-      const double m0 = params[i], m1 = params[P + i], m2 = params[2 * P + i];
-      ok = !isnan(sup);
-      if (ok) o = project_core(m0, m1, m2, sup, CachedSrc{world + i, ParamSrc{params + i, P, rp.sh_coeffs}}, cam, rp);
-#else
       const double sup = support[i];
       ok = !isnan(sup);
       if (ok) {
         const double m0 = params[i], m1 = params[P + i], m2 = params[2 * P + i];
         o = project_core(m0, m1, m2, sup, CachedSrc{world + i, ParamSrc{params + i, P, rp.sh_coeffs}}, cam, rp);
       }
-#endif
     } else {
       // validate_primitives (rasterizer.cpp:34-44): every field finite and |q| > 1e-12
       // (all loads issued before any test: no short-circuit chain of dependent memory latencies)
