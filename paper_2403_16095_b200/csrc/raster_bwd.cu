@@ -840,7 +840,6 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   if (blockIdx.x * blockDim.x >= V) return;
   float pf_par[14];
 #define GSF_PAR(F) pf_par[F]
-#ifdef GSF_CHAIN_GPF
   float gpre[16];
 #define GSF_ACC(ARR, F, IDX, V)                                                      \
   {                                                                                  \
@@ -848,9 +847,6 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
     gpre[F] = nv_;                                                                   \
     ARR[IDX] = nv_;                                                                  \
   }
-#else
-#define GSF_ACC(ARR, F, IDX, V) acc_grad(ARR, IDX, V)
-#endif
   const bool halted = ds->halt != 0;
   bool active = r < V;   // halted: the slots are still read and zeroed, no gradient is written
   int64_t id = 0;
@@ -861,7 +857,6 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
     // the primitive's parameters, loaded before the pair gather so their latency overlaps it
 #pragma unroll
     for (int f = 0; f < 14; ++f) pf_par[f] = (f < 11 || K == 1) ? params[f * P + id] : 0.0f;
-#ifdef GSF_CHAIN_GPF
     // ... and its accumulated gradients: the read-modify-writes below then need no load each (a load
     // after a store into the same array cannot be hoisted by the compiler: 14 serial round trips)
     if (FULL) {
@@ -869,7 +864,6 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
       for (int f = 0; f < 14; ++f) gpre[f] = (f < 11 || K == 1) ? grads[f * P + id] : 0.0f;
       if (d_mean2d) { gpre[14] = d_mean2d[id]; gpre[15] = d_mean2d[P + id]; }
     }
-#endif
     const int4 q = rect_id[id];
     c = (q.y - q.x + 1) * (q.w - q.z + 1);
     pp = partials + static_cast<size_t>(pair_base[id]) * NF;
