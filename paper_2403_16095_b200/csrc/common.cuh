@@ -20,7 +20,7 @@ constexpr int kBinStride = GSF_BIN_STRIDE;
 static_assert(kBinStride >= 4, "the tile-list scan word shares the fill counter's sector");
 constexpr int kPjFloats = 56;   // per-primitive pose matrix: 9 columns x 6 rows + 2 pad (k_posejac)
 constexpr int kBigPairs = 128;
-enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntPairAlloc = 4, kCntSortTicket = 5, kCntFixup = 6, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
+enum BinCounter { kCntVisible = 0, kCntBlendTicket = 1, kCntBwdTicket = 2, kCntBig = 3, kCntPairAlloc = 4, kCntSortTicket = 5, kCntFixup = 6, kCntTileAlloc = 7, kCntNum = 8 };             // tile edge (RasterConfig::tile_size, config.hpp:10)
 constexpr int kTilePixels = kTile * kTile;
 constexpr int kFieldsBase = 11;       // mean 3, log_scale 3, quat 4, opacity 1; then 3*K SH
 

@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(256, GSF_BLEND_MINB) k_blend(const int2* __res
                                                int2* __restrict__ qstat) {
   pdl_wait();   // PDL: the predecessor's results are complete from here
   pdl_trigger();
-  __shared__ BlendG s_g[256];
+  __shared__ __align__(16) BlendG s_g[256];
   __shared__ uint32_t s_ws[8];
   __shared__ int32_t s_id[256];
   __shared__ uint8_t s_mask[256];
@@ -718,8 +718,8 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
     uint32_t* __restrict__ qlist, int32_t* __restrict__ o_lastc, uint8_t* __restrict__ o_code, uint32_t* clean_bins,
     int64_t clean_cnt_off,
-    const uint32_t* __restrict__ order, int2* __restrict__ qstat) {
-  __shared__ BlendG s_g[kTrkBatch];
+    const uint32_t* __restrict__ order, int2* __restrict__ qstat, const uint32_t* pair_alloc, uint32_t pair_cap) {
+  __shared__ __align__(16) BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
   __shared__ double s_red[kTrkThreads / 32][LS_NUM];
@@ -737,6 +737,10 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   // longest-first CTA order (k_lpt; order[0] = the tile count it was built for, else identity)
   const int tile = (order && order[0] == gridDim.x) ? static_cast<int>(order[1 + blockIdx.x]) : blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the tile's list: positions [lo, hi) of sid; this warp's work list at qbase of qlist
+  const int2 rg = ranges[tile];
+  const int lo = rg.x, hi = rg.y;
+  const int64_t qbase = 4 * static_cast<int64_t>(lo) + static_cast<int64_t>(warp) * (hi - lo);
   const uint32_t sgb = opaque_smem_base(s_g);
   uint32_t wsteps = 0u;   // this warp's (warp, entry) steps: k_lpt's cost of the tile and of the
                           // quadrant's pose backward (which walks the same block mask)
@@ -744,22 +748,20 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
   const int x = tx * kTile + 8 * (warp & 1) + (lane & 7);
   const int ya = ty * kTile + 8 * (warp >> 1) + (lane >> 3), yb = ya + 4;
   const bool in_a = x < W && ya < H, in_b = x < W && yb < H;
-  const int2 rg = ranges[tile];
   float2 rg_a = make_float2(0.f, 0.f), bd_a = rg_a, rg_b = rg_a, bd_b = rg_a;
   // a pixel is done once T < term (T never grows); pixels outside the image start done (T = 0)
   float2 op = make_float2(0.f, 0.f), T = make_float2(in_a ? 1.f : 0.f, in_b ? 1.f : 0.f);
   int last_a = 0, last_b = 0;
   int lc_a = 0, lc_b = 0;   // the same, as positions in this warp's work list (qlist)
-  const int64_t qbase = 4 * static_cast<int64_t>(rg.x) + static_cast<int64_t>(warp) * (rg.y - rg.x);
   float px = static_cast<float>(x) + 0.5f;
   float2 py = make_float2(static_cast<float>(ya) + 0.5f, static_cast<float>(yb) + 0.5f);
   const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
-  for (int start = rg.x; start < rg.y; start += kTrkBatch) {
+  for (int start = lo; start < hi; start += kTrkBatch) {
     if (__syncthreads_and(T.x < kc.term && T.y < kc.term)) break;
 #pragma unroll
     for (int h = 0; h < kTrkBatch / kTrkThreads; ++h) {
       const int e = tid + h * kTrkThreads, j = start + e;
-      if (j < rg.y) {
+      if (j < hi) {
         const int id = static_cast<int>(sid[j]);
         const BlendG gj = bg[id];
         s_g[e] = gj;
@@ -769,7 +771,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
       }
     }
     __syncthreads();
-    const int cnt = min(kTrkBatch, rg.y - start);
+    const int cnt = min(kTrkBatch, hi - start);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       if (__all_sync(0xffffffffu, T.x < kc.term && T.y < kc.term)) break;
       const int kk = c0 + lane;
@@ -818,7 +820,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
         op = __fadd2_rn(op, w);
         T = __fmul2_rn(T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-am.x, -am.y)));
         if (QM != 1) {
-          const int li = start + k - rg.x + 1;
+          const int li = start + k - lo + 1;
           if (ca) last_a = li;
           if (cb) last_b = li;
         }
@@ -830,7 +832,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     }
   }
   if (qstat && lane == 0)
-    qstat[tile * 4 + warp] = make_int2(static_cast<int>(wsteps), rg.y - rg.x);
+    qstat[tile * 4 + warp] = make_int2(static_cast<int>(wsteps), hi - lo);
   double v[LS_NUM], vb[LS_NUM];
 #pragma unroll
   for (int q = 0; q < LS_NUM; ++q) v[q] = vb[q] = 0.0;
@@ -904,6 +906,12 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     if (last_cta(ticket, &s_last, tid < LS_NUM)) {
       block_reduce_rows<LS_NUM, kTrkThreads>(loss_part, gridDim.x, s_tot, s_red);
       if (tid == 0) loss_scalars(ds, lp, s_tot, 0.0, 0.0, static_cast<int64_t>(W) * H, iteration);
+      if (pair_alloc && tid == 0) {   // atomically placed lists (k_tile_sort any_order): the pair total M
+        const uint32_t m = *pair_alloc;
+        ds->M = m;
+        atomicMax(&ds->M_max, m);
+        if (m > pair_cap) ds->overflow = 1u;
+      }
     }
   }
 }
@@ -1134,8 +1142,13 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     if (pf) pf->end(ws.side);
     GSF_CUDA_CHECK(cudaEventRecord(ws.ev_join, ws.side));
   }
+  // tracking loop (two-pixel pose backward): the sort runs inside the blend (k_blend_track<1, true>)
+  // the tracking loop's lists are only read back through `ranges` (not exported): k_tile_sort places
+  // each with one atomic instead of the ordered look-back scan, and the blend's last CTA takes M
+  const bool any_order =
+      a.lp.mode == 1 && a.loss_rgb && a.want_posejac && a.qmode == 1 && a.fuse_loss_final && a.clean_bins;
   if (pf) pf->begin(PROF_SORT, st);
-  run_binning(ws, ds, P, tiles_x, ntiles, st, L, a.want_posejac);
+  run_binning(ws, ds, P, tiles_x, ntiles, st, L, a.want_posejac, any_order);
   if (pf) pf->end(st);
   if (side) GSF_CUDA_CHECK(cudaStreamWaitEvent(st, ws.ev_join, 0));
   const float* loss_rgb = a.loss_rgb;
@@ -1160,7 +1173,8 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
                ws.final_T, ws.last, ws.loss_part, a.fuse_loss_final ? 1 : 0, a.iteration,                              \
                ws.bin_counters + kCntBlendTicket, ws.qlist, ws.lastc, sl ? ws.pxcode : nullptr,                        \
                a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride, a.order,               \
-               sl ? ws.qstat : nullptr)
+               sl ? ws.qstat : nullptr, any_order ? ws.bin_counters + kCntTileAlloc : nullptr,           \
+               static_cast<uint32_t>(ws.pair_cap))
     if (qm == 1) GSF_BLEND_TRACK(1);
     else if (qm == 2) GSF_BLEND_TRACK(2);
     else GSF_BLEND_TRACK(0);
