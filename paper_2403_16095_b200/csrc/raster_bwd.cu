@@ -713,30 +713,58 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
 // threads contiguous, flags of the slots no quadrant wrote mask stale values and are cleared.
 __global__ void __launch_bounds__(256) k_pair_combine(const float* __restrict__ qpart, uint32_t* __restrict__ qflag,
                                                       float* __restrict__ partials, const uint32_t* counters) {
+  // a warp folds 32 consecutive pairs: their 32 x 160 B of slots are read coalesced (lane-contiguous
+  // 16 B pieces) into shared memory, each lane folds its own pair from there, and the 32 x 40 B of
+  // results leave through the same buffer as contiguous 16 B stores (per-lane 160 B / 40 B strides
+  // left the LSU queue throttled: ncu lg_throttle)
+  __shared__ float4 s_q[8][32 * 10];
   pdl_wait();
   pdl_trigger();
   const uint32_t M = counters[kCntPairAlloc];
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < M; p += gridDim.x * blockDim.x) {
-    const uint32_t fl = qflag[p];
-    if (fl) qflag[p] = 0u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float4* sq = s_q[warp];
+  for (uint32_t base = (blockIdx.x * 8u + warp) * 32u; base < M; base += gridDim.x * 8u * 32u) {
+    const int np = static_cast<int>(min(32u, M - base));
+    const float4* src = reinterpret_cast<const float4*>(qpart) + static_cast<size_t>(base) * 10;
+#pragma unroll
+    for (int h = 0; h < 10; ++h) {
+      const int i = h * 32 + lane;
+      if (i < np * 10) sq[i] = __ldcs(src + i);   // read once: streaming
+    }
+    uint32_t fl = 0u;
+    if (lane < np) {
+      fl = qflag[base + lane];
+      if (fl) qflag[base + lane] = 0u;
+    }
+    __syncwarp();
     float t[10];
 #pragma unroll
     for (int f = 0; f < 10; ++f) t[f] = 0.0f;
-    // all four slots are read (a read conditioned on the flag waits on it: measured slower)
-    const float4* src = reinterpret_cast<const float4*>(qpart + static_cast<size_t>(p) * 40);
-    float4 v[10];
+    if (lane < np) {
+      float4 v[10];
 #pragma unroll
-    for (int h = 0; h < 10; ++h) v[h] = __ldcs(src + h);   // read once: streaming
+      for (int h = 0; h < 10; ++h) v[h] = sq[lane * 10 + h];
+      // all four slots are read; the unwritten ones are masked by their flag
 #pragma unroll
-    for (int qd = 0; qd < 4; ++qd) {
-      if (!((fl >> (8 * qd)) & 1u)) continue;
-      const float* q = reinterpret_cast<const float*>(v) + qd * 10;
+      for (int qd = 0; qd < 4; ++qd) {
+        if (!((fl >> (8 * qd)) & 1u)) continue;
+        const float* q = reinterpret_cast<const float*>(v) + qd * 10;
 #pragma unroll
-      for (int f = 0; f < 10; ++f) t[f] += q[f];
+        for (int f = 0; f < 10; ++f) t[f] += q[f];
+      }
     }
-    float2* dst = reinterpret_cast<float2*>(partials + static_cast<size_t>(p) * 10);
+    __syncwarp();
+    float* so = reinterpret_cast<float*>(sq);
+    if (lane < np)
 #pragma unroll
-    for (int h = 0; h < 5; ++h) dst[h] = make_float2(t[2 * h], t[2 * h + 1]);
+      for (int h = 0; h < 5; ++h) reinterpret_cast<float2*>(so + lane * 10)[h] = make_float2(t[2 * h], t[2 * h + 1]);
+    __syncwarp();
+    float4* dst = reinterpret_cast<float4*>(partials + static_cast<size_t>(base) * 10);
+    for (int i = lane; i < np * 10 / 4; i += 32) dst[i] = sq[i];
+    if (lane == 0 && (np * 10) % 4)   // a tail pair count leaves two floats
+      reinterpret_cast<float2*>(partials + static_cast<size_t>(base) * 10)[np * 5 - 1] =
+          reinterpret_cast<const float2*>(so)[np * 5 - 1];
+    __syncwarp();
   }
 }
 
@@ -881,11 +909,20 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
 #pragma unroll
   for (int f = 0; f < NF; ++f) sg[f] = 0.0;
   const bool coop = c > kChainCoop;
-  if (!coop)
+  if (!coop) {
+    // 8-byte vectors (a pair slot is 40 B): 5 loads per pair instead of 10 (chain -8 us per view;
+    // two or four pairs' loads in flight measured slower: more registers at the 128 cap)
+    static_assert(NF % 2 == 0, "pair slots are read as float2");
     for (int k = 0; k < c; ++k) {
+      const float2* v = reinterpret_cast<const float2*>(pp + k * NF);
 #pragma unroll
-      for (int f = 0; f < NF; ++f) sg[f] += static_cast<double>(pp[k * NF + f]);
+      for (int f = 0; f < NF / 2; ++f) {
+        const float2 x = __ldg(v + f);
+        sg[2 * f] += static_cast<double>(x.x);
+        sg[2 * f + 1] += static_cast<double>(x.y);
+      }
     }
+  }
   uint32_t big = __ballot_sync(0xffffffffu, coop);
   while (big) {
     const int j = __ffs(big) - 1;
