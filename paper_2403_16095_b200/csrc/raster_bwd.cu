@@ -847,7 +847,66 @@ static __device__ __noinline__ void sh_backward(const float* __restrict__ params
   }
 }
 
-constexpr int kChainCoop = 64;
+#ifndef GSF_CHAIN_COOP
+#define GSF_CHAIN_COOP 16
+#endif
+constexpr int kChainCoop = GSF_CHAIN_COOP;
+
+// The large-footprint primitives (k_preprocess's big list: more than kBigPairs tiles, up to a few
+// thousand pair slots each) summed before k_chain, one CTA per primitive: coalesced lane-strided
+// reads of the primitive's contiguous [pair][10] slots, per-thread fp64 sums, a fixed-order CTA
+// tree, and the ten fp64 totals written over the primitive's first two slots (80 B), which
+// k_chain reads instead of gathering.  In k_chain one warp walked such a list alone while the rest
+// of the grid had finished (the kernel's tail: SMs active ~40 % of its duration under ncu).
+constexpr int kBigSumThreads = 256;
+__global__ void __launch_bounds__(kBigSumThreads) k_big_sum(const uint32_t* __restrict__ big_ids, const uint32_t* counters,
+                                                            const int4* __restrict__ rect_id,
+                                                            const uint32_t* __restrict__ pair_base, float* partials) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double s_w[kBigSumThreads / 32][10];
+  const uint32_t nbig = counters[kCntBig];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+    const uint32_t id = big_ids[b];
+    const int4 q = rect_id[id];
+    const int c = (q.y - q.x + 1) * (q.w - q.z + 1);
+    float* pp = partials + static_cast<size_t>(pair_base[id]) * 10;
+    double acc[10];
+#pragma unroll
+    for (int f = 0; f < 10; ++f) acc[f] = 0.0;
+    for (int k0 = threadIdx.x; k0 < c; k0 += 2 * kBigSumThreads) {
+      float2 v[2][5];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + u * kBigSumThreads;
+#pragma unroll
+        for (int f = 0; f < 5; ++f)
+          v[u][f] = k < c ? __ldg(reinterpret_cast<const float2*>(pp + static_cast<size_t>(k) * 10) + f) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+          acc[2 * f] += static_cast<double>(v[u][f].x);
+          acc[2 * f + 1] += static_cast<double>(v[u][f].y);
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < 10; ++f) {
+      const double t = warp_sum_d(acc[f]);
+      if (lane == 0) s_w[warp][f] = t;
+    }
+    __syncthreads();   // every read of the slots is done before they are overwritten
+    if (threadIdx.x < 10) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < kBigSumThreads / 32; ++w) t += s_w[w][threadIdx.x];
+      reinterpret_cast<double*>(pp)[threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
+}
 
 template <int NF, bool FULL>
 #ifndef GSF_CHAIN_MINB
@@ -902,14 +961,20 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   }
   // fixed-order gather of the primitive's pair partials: its slots hold the tiles of its
   // rectangle in row-major order (the reference's tile-order reduction, rasterizer.cpp:466-478).
-  // Short lists are summed by their own lane; a list longer than kChainCoop is summed by the
+  // Short lists (<= kChainCoop = 16 pairs) are summed by their own lane; a longer list by the
   // whole warp (lane-strided, then a fixed shuffle tree) so one huge footprint cannot leave a
   // single thread walking thousands of L2 round trips.
   double sg[NF];
 #pragma unroll
   for (int f = 0; f < NF; ++f) sg[f] = 0.0;
-  const bool coop = c > kChainCoop;
-  if (!coop) {
+  // c > kBigPairs: summed by k_big_sum into the first two slots (fp64)
+  const bool presum = c > kBigPairs;
+  if (presum) {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) sg[f] = __ldg(reinterpret_cast<const double*>(pp) + f);
+  }
+  const bool coop = c > kChainCoop && !presum;
+  if (!coop && !presum) {
     // 8-byte vectors (a pair slot is 40 B): 5 loads per pair instead of 10 (chain -8 us per view;
     // two or four pairs' loads in flight measured slower: more registers at the 128 cap)
     static_assert(NF % 2 == 0, "pair slots are read as float2");
@@ -932,9 +997,30 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
     double acc[NF];
 #pragma unroll
     for (int f = 0; f < NF; ++f) acc[f] = 0.0;
-    for (int k = lane; k < cj; k += 32) {
+#ifndef GSF_COOP_U
+#define GSF_COOP_U 4
+#endif
+    // GSF_COOP_U lane-strided pairs' loads in flight per round, summed in k order: one primitive
+    // covering thousands of tiles otherwise leaves its warp walking L2 round trips one at a time
+    // (the kernel's tail: ncu saw the SMs active 36 % of its duration)
+    constexpr int kCU = GSF_COOP_U;
+    for (int k0 = lane; k0 < cj; k0 += 32 * kCU) {
+      float2 v[kCU][NF / 2];
 #pragma unroll
-      for (int f = 0; f < NF; ++f) acc[f] += static_cast<double>(pj[k * NF + f]);
+      for (int u = 0; u < kCU; ++u) {
+        const int k = k0 + 32 * u;
+#pragma unroll
+        for (int f = 0; f < NF / 2; ++f)
+          v[u][f] = k < cj ? __ldg(reinterpret_cast<const float2*>(pj + k * NF) + f) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kCU; ++u)
+        if (k0 + 32 * u < cj)
+#pragma unroll
+          for (int f = 0; f < NF / 2; ++f) {
+            acc[2 * f] += static_cast<double>(v[u][f].x);
+            acc[2 * f + 1] += static_cast<double>(v[u][f].y);
+          }
     }
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
@@ -1286,6 +1372,10 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   ++*L;
   if (ws.prof) ws.prof->end(st);
   if (ws.prof) ws.prof->begin(PROF_CHAIN, st);
+  launch_pdl(k_big_sum, dim3(2 * 148), dim3(kBigSumThreads), 0, st, static_cast<const uint32_t*>(ws.big_ids),
+             static_cast<const uint32_t*>(ws.bin_counters), static_cast<const int4*>(ws.rect_id),
+             static_cast<const uint32_t*>(ws.pair_base), ws.partials);
+  ++*L;
   const int blocks = std::max(1, div_up(a.P, 256));
   launch_pdl(k_chain<10, true>, dim3(blocks), dim3(256), 0, st, ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base,
              ws.partials, ds, a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part, ws.bg_id, a.iso_w, a.iso_eps);
