@@ -1274,7 +1274,6 @@ static void enqueue_track(gsf_ctx_s* c, const Frame& f, const gsf_intrinsics& k,
     b.fused_pose = true;
     b.update_iter = it;
     b.order = fa.order;
-    b.clear_counters = true;
     if (!run_backward(c->ws, c->ds, b, c->stream, &c->launches)) run_track_update(c->ds, it, c->stream, &c->launches);
     // the next iteration's orders on the second side branch, beside the next preprocess and binning
     GSF_CUDA_CHECK(cudaEventRecord(ws.ev_lfork, c->stream));

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(uint32_t* fill, uint32_t pair
   __shared__ uint32_t s_start, s_nbig, s_tile;
   pdl_wait();
   pdl_trigger();
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  if (threadIdx.x == 0) s_tile = alloc ? blockIdx.x : atomicAdd(ticket, 1u);
   __syncthreads();
   const int t = static_cast<int>(s_tile);
   const int tx = t % tiles_x, ty = t / tiles_x;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_tile_sort(uint32_t* fill, uint32_t pair
   __syncthreads();
   const uint32_t f = fs + s_nbig;
   const uint32_t nb = min(f, bucket_cap);
-  if (alloc) {   // any list placement will do: one atomic, no look-back (the pair total: the consumer's last CTA)
+  if (alloc) {   // any list placement will do: one atomic, no look-back
     if (threadIdx.x == 0) {
       const uint32_t e = nb ? atomicAdd(alloc, nb) : 0u;
       s_start = e;
@@ -112,6 +112,17 @@ __global__ void __launch_bounds__(256) k_tile_sort(uint32_t* fill, uint32_t pair
       if (f > bucket_cap) ds->overflow = 1u;
       if (e + nb > pair_cap) ds->overflow = 1u;
       if (t == 0) ds->V = counters[kCntVisible];
+      // the last CTA to place its list records the pair total M and re-zeroes both counters
+      __threadfence();
+      if (atomicAdd(ticket, 1u) == gridDim.x - 1) {   // (the ticket is free: tiles go by blockIdx here)
+        __threadfence();
+        const uint32_t m = atomicAdd(alloc, 0u);
+        ds->M = m;
+        atomicMax(&ds->M_max, m);
+        if (m > pair_cap) ds->overflow = 1u;
+        *alloc = 0u;
+        *ticket = 0u;
+      }
     }
   } else if (threadIdx.x == 0) {
     tile_count_publish(fill, t, nb);
@@ -165,7 +176,10 @@ void run_binning(Workspace& ws, DevState* ds, int64_t P, int tiles_x, int ntiles
   const uint32_t pair_cap = static_cast<uint32_t>(ws.pair_cap);
   const uint32_t bcap = static_cast<uint32_t>(ws.bucket_cap);
   // the tracking loop's short lists sort as fast with 128 threads, and more CTAs fit an SM
-  const int threads = any_order ? 128 : 256;
+#ifndef GSF_MAP_SORT_THREADS
+#define GSF_MAP_SORT_THREADS 256
+#endif
+  const int threads = any_order ? (want_slots ? 128 : GSF_MAP_SORT_THREADS) : 256;
   launch_pdl(k_tile_sort, dim3(ntiles), dim3(threads), 0, st, ws.tile_fill, pair_cap, ws.bucket, bcap, ws.skey, ws.sid, ws.depth_id, ws.ranges,
                                       ws.pj_slot, want_slots ? ws.sslot : nullptr, ds, ws.bin_counters, ws.big_ids,
                                       ws.rect_id, tiles_x, ws.bin_counters + kCntSortTicket,

@@ -221,7 +221,6 @@ struct BwdArgs {
   int seed_mode;
   bool pose_only;            // tracking: skip per-primitive parameter gradients
   bool fused_pose = false;   // pose_only + ws.pj_id valid: pose through per-primitive Jacobians
-  bool clear_counters = false;   // tracking loop: zero k_tile_sort's list-placement counter (k_backward_track_w)
   int update_iter = -1;      // >= 0: the tracking backward's last CTA also takes this iteration's pose step
   const uint32_t* order = nullptr;  // tracking: CTA order buffer (Workspace::order half) of the pose backward
   float* grads;              // [D][P] parameter gradients (full mode)

@@ -109,7 +109,6 @@ struct BwdPtrs {
   const uint32_t* pj_slot;  // id -> slot in pj (position in the visible list)
   double* tile_pose;     // per-tile pose partials (fused tracking mode)
   const uint32_t* qlist;    // tracking: per (tile, quadrant) work lists (k_blend_track)
-  uint32_t* clear_counters; // tracking loop: bin counters whose list-placement counter is zeroed here
   const int32_t* lastc;     // tracking: each pixel's last contributor as a work-list position + 1
   uint8_t* qflag;           // full bundle: per (pair, quadrant) written flag (k_backward_q)
   float* qpart;             // full bundle: [pair][quadrant][10] partials (k_backward_q)
@@ -542,9 +541,6 @@ __global__ void __launch_bounds__(32, GSF_TBW_MINB) k_backward_track_w(BwdPtrs b
   pdl_wait();
   pdl_trigger();
   const int lane = threadIdx.x;
-  // the list-placement counter of the loop's k_tile_sort (any_order), read by the blend's last CTA
-  // (zeroed here, not there: a halted blend returns before its last CTA)
-  if (bp.clear_counters && blockIdx.x == 0 && lane == 0) bp.clear_counters[kCntTileAlloc] = 0u;
   const uint32_t sb = opaque_smem_base(s_buf);
   // (tile, quadrant) item in longest-first order (k_lpt; identity when the order is for another grid)
   const int item = (order && 4u * order[0] == gridDim.x) ? static_cast<int>(order[1 + tiles_cap + blockIdx.x])
@@ -858,7 +854,10 @@ constexpr int kChainCoop = GSF_CHAIN_COOP;
 // tree, and the ten fp64 totals written over the primitive's first two slots (80 B), which
 // k_chain reads instead of gathering.  In k_chain one warp walked such a list alone while the rest
 // of the grid had finished (the kernel's tail: SMs active ~40 % of its duration under ncu).
-constexpr int kBigSumThreads = 256;
+#ifndef GSF_BIGSUM_THREADS
+#define GSF_BIGSUM_THREADS 256
+#endif
+constexpr int kBigSumThreads = GSF_BIGSUM_THREADS;
 __global__ void __launch_bounds__(kBigSumThreads) k_big_sum(const uint32_t* __restrict__ big_ids, const uint32_t* counters,
                                                             const int4* __restrict__ rect_id,
                                                             const uint32_t* __restrict__ pair_base, float* partials) {
@@ -1309,7 +1308,6 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
   bp.pair_base = ws.pair_base;
   bp.tile_pose = nullptr;
   bp.qlist = ws.qlist;
-  bp.clear_counters = a.clear_counters ? ws.bin_counters : nullptr;
   bp.lastc = ws.lastc;
   bp.pxcode = ws.pxcode;
   bp.bg_slot = ws.bg_slot;

@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     int32_t* __restrict__ o_last, double* __restrict__ loss_part, int fuse_final, int iteration, uint32_t* ticket,
     uint32_t* __restrict__ qlist, int32_t* __restrict__ o_lastc, uint8_t* __restrict__ o_code, uint32_t* clean_bins,
     int64_t clean_cnt_off,
-    const uint32_t* __restrict__ order, int2* __restrict__ qstat, const uint32_t* pair_alloc, uint32_t pair_cap) {
+    const uint32_t* __restrict__ order, int2* __restrict__ qstat) {
   __shared__ __align__(16) BlendG s_g[kTrkBatch];
   __shared__ int32_t s_id[kTrkBatch];
   __shared__ uint8_t s_mask[kTrkBatch];
@@ -906,12 +906,6 @@ __global__ void __launch_bounds__(kTrkThreads, GSF_TRK_MINB) k_blend_track(
     if (last_cta(ticket, &s_last, tid < LS_NUM)) {
       block_reduce_rows<LS_NUM, kTrkThreads>(loss_part, gridDim.x, s_tot, s_red);
       if (tid == 0) loss_scalars(ds, lp, s_tot, 0.0, 0.0, static_cast<int64_t>(W) * H, iteration);
-      if (pair_alloc && tid == 0) {   // atomically placed lists (k_tile_sort any_order): the pair total M
-        const uint32_t m = *pair_alloc;
-        ds->M = m;
-        atomicMax(&ds->M_max, m);
-        if (m > pair_cap) ds->overflow = 1u;
-      }
     }
   }
 }
@@ -1143,10 +1137,14 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
     GSF_CUDA_CHECK(cudaEventRecord(ws.ev_join, ws.side));
   }
   // tracking loop (two-pixel pose backward): the sort runs inside the blend (k_blend_track<1, true>)
-  // the tracking loop's lists are only read back through `ranges` (not exported): k_tile_sort places
-  // each with one atomic instead of the ordered look-back scan, and the blend's last CTA takes M
-  const bool any_order =
-      a.lp.mode == 1 && a.loss_rgb && a.want_posejac && a.qmode == 1 && a.fuse_loss_final && a.clean_bins;
+  // the tracking loop's and the mapping forward's lists are only read back through `ranges` (never
+  // exported): k_tile_sort places each with one atomic instead of the ordered look-back scan
+#ifdef GSF_NO_ANY_ORDER
+  const bool any_order = false;
+#else
+  const bool any_order = a.loss_rgb && ((a.lp.mode == 1 && a.want_posejac && a.qmode == 1 && a.fuse_loss_final &&
+                                         a.clean_bins) || a.lp.mode == 2);
+#endif
   if (pf) pf->begin(PROF_SORT, st);
   run_binning(ws, ds, P, tiles_x, ntiles, st, L, a.want_posejac, any_order);
   if (pf) pf->end(st);
@@ -1173,8 +1171,7 @@ void run_forward(Workspace& ws, DevState* ds, const FwdArgs& a, cudaStream_t st,
                ws.final_T, ws.last, ws.loss_part, a.fuse_loss_final ? 1 : 0, a.iteration,                              \
                ws.bin_counters + kCntBlendTicket, ws.qlist, ws.lastc, sl ? ws.pxcode : nullptr,                        \
                a.clean_bins ? ws.bins : nullptr, static_cast<int64_t>(ws.tiles_cap) * kBinStride, a.order,               \
-               sl ? ws.qstat : nullptr, any_order ? ws.bin_counters + kCntTileAlloc : nullptr,           \
-               static_cast<uint32_t>(ws.pair_cap))
+               sl ? ws.qstat : nullptr)
     if (qm == 1) GSF_BLEND_TRACK(1);
     else if (qm == 2) GSF_BLEND_TRACK(2);
     else GSF_BLEND_TRACK(0);
