@@ -922,11 +922,10 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
   pdl_trigger();
   __shared__ double s_red[8][6];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t r = blockIdx.x * blockDim.x + tid;
   double pose[6] = {0, 0, 0, 0, 0, 0};
   const uint32_t V = counters[kCntVisible];
-  // the grid is sized for all P; CTAs past the visible list have no primitive and no pose row
-  // (k_pose_sum reads the rows of the first ceil(V / 256) CTAs only)
+  // CTAs past the visible list have no primitive and no pose row (k_pose_sum reads the rows of
+  // the first min(grid, ceil(V / 256)) CTAs only)
   if (blockIdx.x * blockDim.x >= V) return;
   float pf_par[14];
 #define GSF_PAR(F) pf_par[F]
@@ -938,7 +937,11 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
     ARR[IDX] = nv_;                                                                  \
   }
   const bool halted = ds->halt != 0;
-  bool active = r < V;   // halted: the slots are still read and zeroed, no gradient is written
+  // CTA-strided over the visible list (a grid of the resident CTAs, not one CTA per 256 of P: the
+  // thousands of empty CTAs past V cost dispatch time); each CTA keeps one pose row
+  for (uint32_t rb = blockIdx.x * blockDim.x; rb < V; rb += gridDim.x * blockDim.x) {
+  const uint32_t r = rb + tid;
+  bool active = r < V;   // halted: the slots are still read, no gradient is written
   int64_t id = 0;
   int c = 0;
   const float* pp = partials;
@@ -1095,13 +1098,14 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
                dJ[1][2] * (2.0 * cam.fy * pc[1] * iz3);
       for (int a = 0; a < 3; ++a) dp[a] += J[0][a] * sg[0] + J[1][a] * sg[1];
       dp[2] += sg[5];
-      // pose (rasterizer.cpp:519-526)
-      pose[0] = pc[1] * dp[2] - pc[2] * dp[1];
-      pose[1] = pc[2] * dp[0] - pc[0] * dp[2];
-      pose[2] = pc[0] * dp[1] - pc[1] * dp[0];
-      pose[3] = dp[0];
-      pose[4] = dp[1];
-      pose[5] = dp[2];
+      // pose (rasterizer.cpp:519-526): this primitive's part, added to the thread's row below
+      double pz[6];
+      pz[0] = pc[1] * dp[2] - pc[2] * dp[1];
+      pz[1] = pc[2] * dp[0] - pc[0] * dp[2];
+      pz[2] = pc[0] * dp[1] - pc[1] * dp[0];
+      pz[3] = dp[0];
+      pz[4] = dp[1];
+      pz[5] = dp[2];
       for (int j = 0; j < 3; ++j) {
         // E = skew(unit_j); sum dCc .* (E Cc - Cc E)
         double E[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
@@ -1115,7 +1119,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
             for (int c = 0; c < 3; ++c) { ec += E[a][c] * Cc[c][b]; ce += Cc[a][c] * E[c][b]; }
             acc += dCc[a][b] * (ec - ce);
           }
-        pose[j] += acc;
+        pz[j] += acc;
       }
       double through[3] = {0.0, 0.0, 0.0};
       double dcol[3] = {0.0, 0.0, 0.0};
@@ -1128,8 +1132,10 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
         }
       } else if (K > 1) {
         sh_backward(params, P, id, K, cam, m0, m1, m2, dcol, FULL ? grads : nullptr, through);
-        for (int a = 0; a < 3; ++a) pose[3 + a] += Wr[3 * a + 0] * through[0] + Wr[3 * a + 1] * through[1] + Wr[3 * a + 2] * through[2];
+        for (int a = 0; a < 3; ++a) pz[3 + a] += Wr[3 * a + 0] * through[0] + Wr[3 * a + 1] * through[1] + Wr[3 * a + 2] * through[2];
       }
+#pragma unroll
+      for (int a = 0; a < 6; ++a) pose[a] += pz[a];
       if (FULL) {
         if (d_mean2d) { GSF_ACC(d_mean2d, 14, id, sg[0]); GSF_ACC(d_mean2d, 15, P + id, sg[1]); }
         // world parameters (rasterizer.cpp:528-546)
@@ -1191,6 +1197,7 @@ __global__ void __launch_bounds__(256, GSF_CHAIN_MINB) k_chain(const uint32_t* _
         if (c == b) GSF_ACC(grads, 3 + c, (3 + c) * P + id, -g);
       }
     }
+  }
   }
   // deterministic block reduction of the pose pieces
 #pragma unroll
@@ -1374,7 +1381,10 @@ bool run_backward(Workspace& ws, DevState* ds, const BwdArgs& a, cudaStream_t st
              static_cast<const uint32_t*>(ws.bin_counters), static_cast<const int4*>(ws.rect_id),
              static_cast<const uint32_t*>(ws.pair_base), ws.partials);
   ++*L;
-  const int blocks = std::max(1, div_up(a.P, 256));
+#ifndef GSF_CHAIN_CTAS
+#define GSF_CHAIN_CTAS (4 * 148)
+#endif
+  const int blocks = std::max(1, std::min(div_up(a.P, 256), GSF_CHAIN_CTAS));
   launch_pdl(k_chain<10, true>, dim3(blocks), dim3(256), 0, st, ws.vis_list, ws.bin_counters, ws.rect_id, ws.pair_base,
              ws.partials, ds, a.params, a.P, a.K, a.grads, a.d_mean2d, ws.pose_part, ws.bg_id, a.iso_w, a.iso_eps);
   ++*L;
