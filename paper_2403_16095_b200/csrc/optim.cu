@@ -18,7 +18,7 @@ namespace {
 constexpr int kAdamPer = 4;
 __global__ void __launch_bounds__(256) k_adam(float* __restrict__ params, const float* __restrict__ grads,
                                               float* __restrict__ m, float* __restrict__ v, int64_t P, AdamGroups g,
-                                              double bc1, double bc2, int f0) {
+                                              double ibc1, double ibc2, int f0) {
   const int f = f0 + static_cast<int>(blockIdx.y);
   const int grp = f < 3 ? 0 : (f < 6 ? 1 : (f < 10 ? 2 : (f < 11 ? 3 : 4)));
   const double lr = g.lr[grp];
@@ -34,7 +34,10 @@ __global__ void __launch_bounds__(256) k_adam(float* __restrict__ params, const 
     const double vv = 0.999 * static_cast<double>(v[e]) + (1.0 - 0.999) * gr * gr;
     m[e] = static_cast<float>(mm);
     v[e] = static_cast<float>(vv);
-    const double upd = lr * (mm / bc1) / (sqrt(vv / bc2) + 1e-8);
+    // the bias corrections as host reciprocals (ibc = 1 / bc): two fp64 divisions fewer per entry
+    // (the kernel is FP64-bound, not HBM-bound: 145 -> 107 us at 994k x 14); one fp64 ulp apart
+    // from m / bc before the fp32 store
+    const double upd = lr * (mm * ibc1) / (sqrt(vv * ibc2) + 1e-8);
     params[e] = static_cast<float>(static_cast<double>(params[e]) - upd);
   }
 }
@@ -51,7 +54,7 @@ void run_adam_fields(float* params, const float* grads, float* m, float* v, int6
   const double bc1 = 1.0 - std::pow(0.9, step);
   const double bc2 = 1.0 - std::pow(0.999, step);
   const dim3 grid(static_cast<unsigned>(div_up(P, 256 * kAdamPer)), static_cast<unsigned>(f1 - f0));
-  k_adam<<<grid, 256, 0, st>>>(params, grads, m, v, P, g, bc1, bc2, f0);
+  k_adam<<<grid, 256, 0, st>>>(params, grads, m, v, P, g, 1.0 / bc1, 1.0 / bc2, f0);
   ++*L;
 }
 
