@@ -8,13 +8,16 @@
 //                     transmittance, and an entry's ten screen-space partials are reduced across the
 //                     warp (reduce-scatter) and written ONCE into the (pair, quadrant) slot.
 // k_pair_combine      folds the four quadrant slots of every (tile, primitive) pair in quadrant order.
+// k_big_sum           pre-sums the pair slots of the large-footprint primitives (> kBigPairs tiles),
+//                     one CTA each, for k_chain.
 // k_backward_track_w  the tracking (pose-only) backward: the same walk over the forward's per-quadrant
 //                     work lists, each lane contracting its pixels' partials with the entry's SE(3)
 //                     Jacobian (k_posejac) so no per-pair partial is stored; the last CTA sums the
 //                     rows and runs the pose step.  k_backward_pose: the view-dependent-SH variant.
-// k_chain             phase 2 (rasterizer.cpp:480-570) in fp64, one thread per visible primitive: a
-//                     fixed-order gather of its pair slots (= the reference's tile-order reduction,
-//                     :466-478), the projection/covariance chain, the SE(3) pose pieces and the
+// k_chain             phase 2 (rasterizer.cpp:480-570) in fp64, one thread per visible primitive (4 x 148
+//                     CTAs strided over the visible list): a fixed-order gather of its pair slots (the
+//                     reference's tile-order reduction, :466-478; warp-cooperative above 16 slots,
+//                     k_big_sum's totals above kBigPairs), the projection/covariance chain, the SE(3) pose pieces and the
 //                     world-parameter gradients; the pose 6-vector is reduced block-wise in fp64.
 // k_pose_sum          fixed-order sum of the per-block pose partials (rasterizer.cpp:570).
 // No float atomics on any path: results are bit-repeatable.
