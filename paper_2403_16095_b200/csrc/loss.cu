@@ -100,7 +100,7 @@ constexpr int kSX = 32, kSY = 16, kSW = kSX + 2 * kR, kSHh = kSY + 2 * kR;
 constexpr int kHG = 4;                   // horizontal outputs per thread
 constexpr int kHItems = kSHh * (kSX / kHG);   // 26 rows x 8 groups = 208
 constexpr size_t ssim_fwd2_smem() { return sizeof(float) * (6 * kSHh * kSW + 5 * kSHh * kSX); }
-constexpr size_t ssim_bwd2_smem() { return sizeof(float) * (3 * kSHh * kSW + 3 * kSY * kSW); }
+constexpr size_t ssim_bwd2_smem() { return sizeof(float) * (2 * 3 * kSHh * kSW + 3 * kSY * kSW); }
 
 __global__ void __launch_bounds__(256) k_ssim_fwd2(const float* __restrict__ x, const float* __restrict__ y, int W, int H,
                                                    double weight, float* __restrict__ u, double* __restrict__ part) {
@@ -221,13 +221,18 @@ __global__ void __launch_bounds__(256) k_ssim_fwd2(const float* __restrict__ x, 
 
 constexpr int kVG = 4;   // adjoint vertical outputs per thread (rows)
 
-__global__ void __launch_bounds__(256) k_ssim_bwd2(const float* __restrict__ u, const float* __restrict__ x,
+#ifndef GSF_SSIMB_MINB
+#define GSF_SSIMB_MINB 5
+#endif
+__global__ void __launch_bounds__(256, GSF_SSIMB_MINB) k_ssim_bwd2(const float* __restrict__ u, const float* __restrict__ x,
                                                    const float* __restrict__ y, int W, int H, float* __restrict__ dx) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ float s_buf[];
-  float (*s_u)[kSHh][kSW] = reinterpret_cast<float (*)[kSHh][kSW]>(s_buf);                    // 3 planes + halo
-  float (*s_t)[kSY][kSW] = reinterpret_cast<float (*)[kSY][kSW]>(s_buf + 3 * kSHh * kSW);     // after the vertical pass
+  // two buffers of the channel's 3 adjoint planes + halo (channel ch + 1 streams in by cp.async
+  // while ch is filtered), then the vertical pass's output
+  float (*s_ub)[3][kSHh][kSW] = reinterpret_cast<float (*)[3][kSHh][kSW]>(s_buf);
+  float (*s_t)[kSY][kSW] = reinterpret_cast<float (*)[kSY][kSW]>(s_buf + 2 * 3 * kSHh * kSW);
   __shared__ float s_wy[kSY][2 * kR + 1], s_wx[kSX][2 * kR + 1];
   const int64_t npix = static_cast<int64_t>(W) * H;
   const int bx = blockIdx.x * kSX, by = blockIdx.y * kSY;
@@ -244,17 +249,28 @@ __global__ void __launch_bounds__(256) k_ssim_bwd2(const float* __restrict__ u, 
   }
   // horizontal-pass pixels of this thread: row hr, columns 2 hc and 2 hc + 1
   const int hr = tid >> 4, hc = (tid & 15) * 2;
-  for (int ch = 0; ch < 3; ++ch) {
-    __syncthreads();   // s_u / s_t of the previous channel are consumed
+  auto stage = [&](int ch) {
     for (int idx = tid; idx < kSHh * kSW; idx += 256) {
       const int r = idx / kSW, c = idx - r * kSW;
       const int gx = bx - kR + c, gy = by - kR + r;
       const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
-      const int64_t j = static_cast<int64_t>(gy) * W + gx;
+      const int64_t j = in ? static_cast<int64_t>(gy) * W + gx : 0;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) s_u[q][r][c] = in ? u[(3 * q + ch) * npix + j] : 0.0f;
+      for (int q = 0; q < 3; ++q) cp_async4_zfill(&s_ub[ch & 1][q][r][c], u + (3 * q + ch) * npix + j, in);
+    }
+    cp_async_commit();
+  };
+  stage(0);
+  for (int ch = 0; ch < 3; ++ch) {
+    __syncthreads();   // s_t and the buffer channel ch + 1 lands in (channel ch - 1's) are consumed
+    if (ch + 1 < 3) {
+      stage(ch + 1);
+      cp_async_wait_1();   // channel ch has landed (this thread's copies)
+    } else {
+      cp_async_wait_all();
     }
     __syncthreads();
+    float (*s_u)[kSHh][kSW] = s_ub[ch & 1];
     for (int item = tid; item < (kSY / kVG) * kSW; item += 256) {   // vertical adjoint: column c, rows r0 .. r0 + 3
       const int c = item % kSW, r0 = (item / kSW) * kVG;
       float acc[3][kVG];
