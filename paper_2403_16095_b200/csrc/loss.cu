@@ -142,54 +142,54 @@ __global__ void __launch_bounds__(256) k_ssim_fwd2(const float* __restrict__ x, 
   for (int ch = 0; ch < 3; ++ch) {
     if (tid < kHItems) {   // horizontal pass: row hr, outputs hx .. hx + 3
       const int hr = tid / (kSX / kHG), hx = (tid - hr * (kSX / kHG)) * kHG;
-      float acc[5][kHG];
+      // outputs in pairs (hx, hx + 1), (hx + 2, hx + 3) on packed FFMA2: each lane rounds like the
+      // scalar FMA, and a tap outside the window adds 0 * v (exact), so the sums equal the scalar ones
+      float2 acc[5][kHG / 2];
 #pragma unroll
       for (int q = 0; q < 5; ++q)
 #pragma unroll
-        for (int j = 0; j < kHG; ++j) acc[q][j] = 0.0f;
+        for (int k = 0; k < kHG / 2; ++k) acc[q][k] = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int p = 0; p < kHG + 2 * kR; ++p) {
         const float a = s_in[ch][hr][hx + p], b = s_in[3 + ch][hr][hx + p];
         const float v[5] = {a, b, a * a, b * b, a * b};
 #pragma unroll
-        for (int j = 0; j < kHG; ++j) {
-          const int o = p - j;
-          if (o >= 0 && o <= 2 * kR) {
-            const float w = c_win[o];
+        for (int k = 0; k < kHG / 2; ++k) {
+          const int o0 = p - 2 * k, o1 = o0 - 1;
+          const bool in0 = o0 >= 0 && o0 <= 2 * kR, in1 = o1 >= 0 && o1 <= 2 * kR;
+          if (in0 || in1) {
+            const float2 w = make_float2(in0 ? c_win[in0 ? o0 : 0] : 0.0f, in1 ? c_win[in1 ? o1 : 0] : 0.0f);
 #pragma unroll
-            for (int q = 0; q < 5; ++q) acc[q][j] += w * v[q];
+            for (int q = 0; q < 5; ++q) acc[q][k] = __ffma2_rn(w, make_float2(v[q], v[q]), acc[q][k]);
           }
         }
       }
+      const float2 iz01 = make_float2(s_izx[hx], s_izx[hx + 1]), iz23 = make_float2(s_izx[hx + 2], s_izx[hx + 3]);
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
-        float4 o4;
-        o4.x = acc[q][0] * s_izx[hx];
-        o4.y = acc[q][1] * s_izx[hx + 1];
-        o4.z = acc[q][2] * s_izx[hx + 2];
-        o4.w = acc[q][3] * s_izx[hx + 3];
-        *reinterpret_cast<float4*>(&s_h[q][hr][hx]) = o4;
+        const float2 lo = __fmul2_rn(acc[q][0], iz01), hi = __fmul2_rn(acc[q][1], iz23);
+        *reinterpret_cast<float4*>(&s_h[q][hr][hx]) = make_float4(lo.x, lo.y, hi.x, hi.y);
       }
     }
     __syncthreads();
     {   // vertical pass + per-pixel SSIM of (vc, 2 vr) and (vc, 2 vr + 1)
-      float acc[5][2];
+      float2 acc2[5];   // rows (2 vr, 2 vr + 1), packed like the horizontal pass
 #pragma unroll
-      for (int q = 0; q < 5; ++q) acc[q][0] = acc[q][1] = 0.0f;
+      for (int q = 0; q < 5; ++q) acc2[q] = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int p = 0; p < 2 + 2 * kR; ++p) {
         float v[5];
 #pragma unroll
         for (int q = 0; q < 5; ++q) v[q] = s_h[q][2 * vr + p][vc];
+        const float2 w = make_float2(p <= 2 * kR ? c_win[p <= 2 * kR ? p : 0] : 0.0f, p >= 1 ? c_win[p >= 1 ? p - 1 : 0] : 0.0f);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int o = p - j;
-          if (o >= 0 && o <= 2 * kR) {
-            const float w = c_win[o];
+        for (int q = 0; q < 5; ++q) acc2[q] = __ffma2_rn(w, make_float2(v[q], v[q]), acc2[q]);
+      }
+      float acc[5][2];
 #pragma unroll
-            for (int q = 0; q < 5; ++q) acc[q][j] += w * v[q];
-          }
-        }
+      for (int q = 0; q < 5; ++q) {
+        acc[q][0] = acc2[q].x;
+        acc[q][1] = acc2[q].y;
       }
       const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
 #pragma unroll
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256) k_ssim_fwd2(const float* __restrict__ x, 
 constexpr int kVG = 4;   // adjoint vertical outputs per thread (rows)
 
 #ifndef GSF_SSIMB_MINB
-#define GSF_SSIMB_MINB 5
+#define GSF_SSIMB_MINB 4
 #endif
 __global__ void __launch_bounds__(256, GSF_SSIMB_MINB) k_ssim_bwd2(const float* __restrict__ u, const float* __restrict__ x,
                                                    const float* __restrict__ y, int W, int H, float* __restrict__ dx) {
@@ -273,50 +273,56 @@ __global__ void __launch_bounds__(256, GSF_SSIMB_MINB) k_ssim_bwd2(const float* 
     float (*s_u)[kSHh][kSW] = s_ub[ch & 1];
     for (int item = tid; item < (kSY / kVG) * kSW; item += 256) {   // vertical adjoint: column c, rows r0 .. r0 + 3
       const int c = item % kSW, r0 = (item / kSW) * kVG;
-      float acc[3][kVG];
+      float2 acc[3][kVG / 2];   // rows (r0 + 2k, r0 + 2k + 1) on packed FFMA2 (0 * v outside the window: exact)
 #pragma unroll
       for (int q = 0; q < 3; ++q)
 #pragma unroll
-        for (int j = 0; j < kVG; ++j) acc[q][j] = 0.0f;
+        for (int k = 0; k < kVG / 2; ++k) acc[q][k] = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int p = 0; p < kVG + 2 * kR; ++p) {
         float v[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) v[q] = s_u[q][r0 + p][c];
 #pragma unroll
-        for (int j = 0; j < kVG; ++j) {
-          const int o = p - j;
-          if (o >= 0 && o <= 2 * kR) {
-            const float w = s_wy[r0 + j][o];
+        for (int k = 0; k < kVG / 2; ++k) {
+          const int o0 = p - 2 * k, o1 = o0 - 1;
+          const bool in0 = o0 >= 0 && o0 <= 2 * kR, in1 = o1 >= 0 && o1 <= 2 * kR;
+          if (in0 || in1) {
+            const float2 w = make_float2(in0 ? s_wy[r0 + 2 * k][in0 ? o0 : 0] : 0.0f,
+                                         in1 ? s_wy[r0 + 2 * k + 1][in1 ? o1 : 0] : 0.0f);
 #pragma unroll
-            for (int q = 0; q < 3; ++q) acc[q][j] += w * v[q];
+            for (int q = 0; q < 3; ++q) acc[q][k] = __ffma2_rn(w, make_float2(v[q], v[q]), acc[q][k]);
           }
         }
       }
 #pragma unroll
       for (int q = 0; q < 3; ++q)
 #pragma unroll
-        for (int j = 0; j < kVG; ++j) s_t[q][r0 + j][c] = acc[q][j];
+        for (int k = 0; k < kVG / 2; ++k) {
+          s_t[q][r0 + 2 * k][c] = acc[q][k].x;
+          s_t[q][r0 + 2 * k + 1][c] = acc[q][k].y;
+        }
     }
     __syncthreads();
     {   // horizontal adjoint of (hc, hr), (hc + 1, hr)
-      float acc[3][2];
+      float2 acc2[3];   // columns (hc, hc + 1), packed
 #pragma unroll
-      for (int q = 0; q < 3; ++q) acc[q][0] = acc[q][1] = 0.0f;
+      for (int q = 0; q < 3; ++q) acc2[q] = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int p = 0; p < 2 + 2 * kR; ++p) {
         float v[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) v[q] = s_t[q][hr][hc + p];
+        const float2 w = make_float2(p <= 2 * kR ? s_wx[hc][p <= 2 * kR ? p : 0] : 0.0f,
+                                     p >= 1 ? s_wx[hc + 1][p >= 1 ? p - 1 : 0] : 0.0f);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int o = p - j;
-          if (o >= 0 && o <= 2 * kR) {
-            const float w = s_wx[hc + j][o];
+        for (int q = 0; q < 3; ++q) acc2[q] = __ffma2_rn(w, make_float2(v[q], v[q]), acc2[q]);
+      }
+      float acc[3][2];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) acc[q][j] += w * v[q];
-          }
-        }
+      for (int q = 0; q < 3; ++q) {
+        acc[q][0] = acc2[q].x;
+        acc[q][1] = acc2[q].y;
       }
       const int gy = by + hr;   // d_x = a0 + 2 a1 x + a2 y for this channel
 #pragma unroll
