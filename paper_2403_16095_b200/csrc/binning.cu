@@ -18,9 +18,10 @@
 //                   memory; lists longer than kSortChunk are chunk-sorted and merged (merge path)
 //                   through global memory by the same CTA.  A final pass re-orders the rare runs
 //                   whose fp32 depths tie by the exact fp64 depth (then id).  In the tracking loop
-//                   the lists are read back only through `ranges`, so each tile takes its start
-//                   from one atomic (any_order: no look-back; 128-thread CTAs; the blend's last
-//                   CTA records M): -4 us per iteration.  Measured and dropped: the sort fused
+//                   and the mapping forward the lists are read back only through `ranges`, so each
+//                   tile takes its start from one atomic (any_order: no look-back; the last CTA to
+//                   place its list records M and re-zeroes the counters; 128-thread CTAs for the
+//                   tracking loop's short lists): -4 us per tracking iteration, -1 us per view.  Measured and dropped: the sort fused
 //                   into the tracking blend (+20 us: the CTA-serial sort phases stretch every
 //                   blend CTA), one warp per tile with register bitonic sorts (+25 us: 3 k
 //                   warps leave the SMs 21 % occupied and each warp's 36-stage shuffle chain is
