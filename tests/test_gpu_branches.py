@@ -431,3 +431,44 @@ def test_overflow_mid_loop_grows_and_matches(gpu_ctx, orc):
     gpu_ctx.reserve(M0, L0)
     tg = gpu_ctx.tracking_gradient(0, ref.pose, K, w)
     assert np.array_equal(tg[1], tg_ref[1])
+
+
+def test_mapping_overflow_reported_then_matches(gpu_ctx, orc):
+    """map_step with the binning capacities reserved below its views' lists: the mapping forward's
+    lists are placed by one atomic each (k_tile_sort any_order, the last CTA recording M), so a
+    list that does not fit must still raise the overflow — map_step reports it (EUnsupported: the
+    map was already stepping, mapper.cpp has no rerun) instead of returning a map from truncated
+    lists — and after a render at those poses has grown the capacities the same call reproduces
+    the run that never overflowed, bit for bit."""
+    from paper_2403_16095_b200.abi import defaults_mapper
+    K = make_intrinsics(64, 48, 90.0)
+    truth = _cluster_scene(orc)
+    poses = [pose(), perturbed(pose(), [0.01, -0.02, 0.01, 0.03, -0.02, 0.01])]
+    gpu_ctx.upload(to_api_map(truth))
+    for s, p in enumerate(poses):
+        r = gpu_ctx.render(p, K)
+        gpu_ctx.frame_upload(s, r.color, r.alpha_depth, 64, 48)
+    rng = np.random.default_rng(17)
+    pert = f32_round(truth)
+    pert.mean = (pert.mean + 0.01 * rng.standard_normal(pert.mean.shape)).astype(np.float32).astype(np.float64)
+    mc = defaults_mapper()
+    mc.densify_interval = 0
+    gpu_ctx.upload(to_api_map(pert))
+    exts = [_list_extent(gpu_ctx, p, K) for p in poses]
+    L, M = max(e[0] for e in exts), max(e[1] for e in exts)
+    t_ref = gpu_ctx.map_step([0, 1], poses, K, mc, 6)
+    a = gpu_ctx.download()
+    gpu_ctx.upload(to_api_map(pert))
+    gpu_ctx.reserve(M // 3, max(L // 3, 32))
+    with pytest.raises(NotImplementedError, match="pair capacity"):
+        gpu_ctx.map_step([0, 1], poses, K, mc, 6)
+    gpu_ctx.upload(to_api_map(pert))
+    for p in poses:
+        gpu_ctx.render(p, K)   # the render API grows the capacities to these views' lists
+    pc, bc = gpu_ctx.capacity()
+    assert pc >= M and bc >= L, (pc, bc, M, L)
+    t = gpu_ctx.map_step([0, 1], poses, K, mc, 6)
+    b = gpu_ctx.download()
+    assert np.array_equal(t, t_ref)
+    for k in ("mean", "log_scale", "quat", "opacity_logit", "sh"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
