@@ -586,7 +586,7 @@ def mapping_evidence(mctx, slots, kposes, kf, K, tc, mc, iters=2):
     roof = {
         "blend k_blend_mq": fp("blend", 11 * T + 24 * Cn, fp32_peak, "fp32: 11 T + 24 C"),
         "backward k_backward_q<SEED_MAP> + k_pair_combine": fp("backward", 13 * T + 70 * Cn, fp32_peak, "fp32: 13 T + 70 C"),
-        "chain k_chain<10> (+k_pose_sum)": fp("chain", 300 * V, fp64_peak,
+        "chain k_big_sum + k_chain<10> (+k_pose_sum)": fp("chain", 300 * V, fp64_peak,
                                              "fp64: 300 V (peak = 148 SMs x 64 FP64 lanes x 2 x clock)"),
         "chain_bytes": bw("chain", 40 * M + 4 * D * 3 * V, "hbm: 40 B per (primitive, tile) partial + params read, "
                                                           "gradients read+written (3 x 4 D B per visible primitive)"),
